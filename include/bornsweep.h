@@ -1,0 +1,161 @@
+/*
+ * bornsweep.h -- C ABI of the B200-native Born-series sweep (libbornsweep.so).
+ *
+ * Drop-in boundary for the reference's hot path (arxiv 2603.18527, "bornprec"):
+ * the operator API of bp::Problem (proj/include/bp/problem.hpp:16-49), the correction-map
+ * API of bp::CorrectionMap / apply_correction (proj/include/bp/correction.hpp:16-59) and the
+ * driver bp::run (proj/include/bp/iterate.hpp:14-67).  The reference is a C++ library with no
+ * FFI of its own; these are the plain-pointer entry points a ctypes / cffi / extern "C"
+ * binding of that API would call.  No torch types cross this boundary.
+ *
+ * Data conventions (identical to the reference):
+ *   field    nx*ny complex128, row-major with x slow: data[ix*ny + iy], re/im interleaved
+ *            (proj/include/bp/field.hpp:14-26; std::complex<double> is array-compatible
+ *            with double[2]).  Batched entry points take `batch` fields back to back.
+ *   grid     DirichletInterior, h = lx/(nx+1) (proj/include/bp/grid.hpp:12-24).
+ *   DST-I    forward = plain sine sum, inverse carries 4/((nx+1)(ny+1))
+ *            (proj/include/bp/transforms.hpp:15-24).
+ * Supported on the GPU: square grids with nx+1 = ny+1 = 2^k, 8 <= 2^k <= 512
+ * (other shapes return BP_ENOTSUP; the reference accepts any size through FFTW).
+ *
+ * Errors: every function returns a status; nothing throws across the boundary.
+ *   BP_EINVAL   <-> std::invalid_argument (e.g. proj/src/problem.cpp:16, iterate.cpp:90-94,
+ *                   helmholtz.cpp:18)
+ *   BP_ERUNTIME <-> std::runtime_error (near-zero symbol, proj/src/symbol.cpp:30-31,109-110)
+ *   BP_ECUDA / BP_ENCCL for device / collective failures.  bp_last_error() (thread-local)
+ *   holds the message.  Numerical failure is NOT an error: it is reported through
+ *   bp_trace.terminated exactly like bp::Termination (proj/include/bp/iterate.hpp:20).
+ *
+ * Threading: a problem handle is immutable after creation (like bp::Problem, problem.hpp:14-15);
+ * concurrent calls on distinct handles are safe, each handle owns its stream.
+ */
+#ifndef BORNSWEEP_H
+#define BORNSWEEP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BP_ABI_VERSION 1
+
+enum {
+    BP_OK = 0,
+    BP_EINVAL = 1,
+    BP_ERUNTIME = 2,
+    BP_ECUDA = 3,
+    BP_ENCCL = 4,
+    BP_ENOTSUP = 5
+};
+
+/* bp::Bc (proj/include/bp/grid.hpp:10) */
+enum { BP_BC_PERIODIC = 0, BP_BC_DIRICHLET = 1, BP_BC_NEUMANN = 2 };
+
+/* bp::GridSpec (proj/include/bp/grid.hpp:15-43) */
+typedef struct {
+    int32_t nx, ny;
+    double lx, ly;
+    int32_t bc;
+} bp_grid;
+
+/* CorrectionMap variants (proj/include/bp/correction.hpp:16-40) plus the diagonal
+ * relaxation gamma(x) = (i/eta) V(x) ("scalar/diagonal relaxation"). */
+enum {
+    BP_MAP_SCALAR = 0,         /* ScalarMap{gamma}                                      */
+    BP_MAP_OPTIMAL_SCALAR = 1, /* OptimalScalarMap{metric}             (BP_ENOTSUP yet) */
+    BP_MAP_FOURIER_DIAG = 2,   /* FourierDiagMap{m}                    (BP_ENOTSUP yet) */
+    BP_MAP_POINTWISE = 3       /* gamma(x) = (i/eta) V(x), Osnabrugge-style CBS          */
+};
+enum { BP_METRIC_EUCLIDEAN = 0, BP_METRIC_RETA = 1 }; /* bp::OptMetric */
+
+typedef struct {
+    int32_t kind;
+    double gamma_re, gamma_im; /* BP_MAP_SCALAR */
+    int32_t metric;            /* BP_MAP_OPTIMAL_SCALAR */
+    const double* m;           /* BP_MAP_FOURIER_DIAG: nx*ny complex (host) */
+} bp_map;
+
+/* bp::IterFormat / IterationConfig (proj/include/bp/iterate.hpp:12-18) */
+enum { BP_FMT_DIRECT = 0, BP_FMT_CBS = 1, BP_FMT_NPBS = 2 };
+typedef struct {
+    int32_t format;   /* default BP_FMT_NPBS */
+    double rtol;      /* default 1e-6 */
+    int32_t max_iters;/* default 1000 */
+} bp_iter_config;
+
+/* bp::Termination (proj/include/bp/iterate.hpp:20) */
+enum { BP_TERM_CONVERGED = 0, BP_TERM_MAX_ITERS = 1, BP_TERM_DIVERGED = 2, BP_TERM_STAGNATED = 3 };
+
+/* bp::IterationTrace scalars (proj/include/bp/iterate.hpp:25-32); the per-step vectors
+ * res_l2_rel / res_reta_rel are returned through caller arrays of max_iters+1 entries
+ * (entries past iters are set to NaN). */
+typedef struct {
+    int32_t iters;
+    int32_t terminated;
+    double fnorm_l2;
+    double fnorm_reta;
+} bp_trace;
+
+typedef struct bp_problem bp_problem;
+
+const char* bp_last_error(void);
+int bp_abi_version(void);
+
+/* Dirichlet five-point Helmholtz batch: A = L_D - k2, L_ref = L_D - (k0^2 + i eta),
+ * V = k2 - (k0^2 + i eta)   (HelmholtzProblem ctor, proj/src/helmholtz.cpp:11-25, with the
+ * DirichletInterior five-point pattern of proj/src/newton_problem.cpp:17-44).
+ * k2: batch*nx*ny complex (sponge damping already folded in, like make_helmholtz);
+ * k0, eta: batch each.  device: CUDA ordinal. */
+int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, const double* k0,
+                      const double* eta, int32_t device, bp_problem** out);
+int bp_problem_destroy(bp_problem* p);
+int bp_problem_batch(const bp_problem* p, int32_t* batch, bp_grid* grid);
+
+/* Operator applications on batch fields, host buffers in and out
+ * (Problem::apply_* / born_residual, proj/src/problem.cpp:19-49; residual f - A u,
+ * proj/src/iterate.cpp:45-50).  The *_device variants take device pointers. */
+int bp_apply_A(const bp_problem* p, const double* u, double* out);
+int bp_apply_V(const bp_problem* p, const double* u, double* out);
+int bp_apply_V_adjoint(const bp_problem* p, const double* u, double* out);
+int bp_apply_Lref(const bp_problem* p, const double* u, double* out);
+int bp_apply_G(const bp_problem* p, const double* q, double* out);
+int bp_born_residual(const bp_problem* p, const double* u, const double* f, double* out);
+int bp_residual(const bp_problem* p, const double* u, const double* f, double* out);
+/* forward_transform / inverse_transform for the problem's DST-I basis
+ * (proj/src/transforms.cpp:105-148) */
+int bp_forward_transform(const bp_problem* p, const double* field, double* modes);
+int bp_inverse_transform(const bp_problem* p, const double* modes, double* field);
+
+/* bp::run (proj/src/iterate.cpp:88-153) over the whole batch; every member iterates and
+ * terminates independently.  f, u0 (nullable), u_out: batch*nx*ny complex host buffers;
+ * res_l2, res_reta: batch*(max_iters+1) (nullable); info: batch entries. */
+int bp_run(const bp_problem* p, const bp_map* map, const double* f, const bp_iter_config* cfg,
+           const double* u0, double* u_out, double* res_l2, double* res_reta, bp_trace* info);
+
+/* Same with device-resident f / u0 / u_out (CUDA device pointers, same dense layout);
+ * traces and info are host buffers.  Used by bench.py's device-resident measurement. */
+int bp_run_device(const bp_problem* p, const bp_map* map, const double* f_dev,
+                  const bp_iter_config* cfg, const double* u0_dev, double* u_out_dev,
+                  double* res_l2, double* res_reta, bp_trace* info);
+
+/* Debug / parity hook: like bp_run, and additionally copies the iterates u^m,
+ * m = 0..n_snap-1, of every member into snapshots (n_snap x batch x nx x ny complex). */
+int bp_run_snapshots(const bp_problem* p, const bp_map* map, const double* f,
+                     const bp_iter_config* cfg, const double* u0, double* u_out,
+                     double* res_l2, double* res_reta, bp_trace* info, double* snapshots,
+                     int32_t n_snap);
+
+/* Instrumentation for bench.py: number of sweep kernels launched by the last run on this
+ * handle, total sweeps executed per member (active sweeps), and the summed device time of
+ * the fused sweep kernels measured with CUDA events on the handle's stream (ms; 0 unless
+ * enabled with bp_set_kernel_timing). */
+int bp_set_kernel_timing(bp_problem* p, int32_t enable);
+int bp_last_run_stats(const bp_problem* p, int64_t* kernel_launches, int64_t* active_sweeps,
+                      double* row_kernel_ms, double* col_kernel_ms, int64_t* timed_sweeps);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

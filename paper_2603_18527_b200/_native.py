@@ -1,0 +1,122 @@
+"""ctypes bindings of the two native libraries (built in-tree by ``__graft_entry__.build()``).
+
+* ``libbornsweep.so``      -- the sm_100a CUDA path behind ``include/bornsweep.h``
+* ``libbornsweep_host.so`` -- seeded instance synthesis behind ``include/bornsweep_instances.h``
+
+There is no fallback: if the CUDA library is missing, loading raises ``NativeLibraryMissing``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbornsweep.so")
+HOST_LIB_PATH = os.path.join(HERE, "libbornsweep_host.so")
+
+_dp = C.POINTER(C.c_double)
+
+
+class NativeLibraryMissing(ImportError):
+    pass
+
+
+class Grid(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("lx", C.c_double), ("ly", C.c_double),
+                ("bc", C.c_int32)]
+
+
+class Map(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("gamma_re", C.c_double), ("gamma_im", C.c_double),
+                ("metric", C.c_int32), ("m", _dp)]
+
+
+class IterConfig(C.Structure):
+    _fields_ = [("format", C.c_int32), ("rtol", C.c_double), ("max_iters", C.c_int32)]
+
+
+class Trace(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("terminated", C.c_int32), ("fnorm_l2", C.c_double),
+                ("fnorm_reta", C.c_double)]
+
+
+class InstanceSpec(C.Structure):
+    _fields_ = [("n", C.c_int32), ("ppw", C.c_double), ("contrast", C.c_double),
+                ("sigma_cells", C.c_double), ("src_sigma_cells", C.c_double),
+                ("n_sources", C.c_int32), ("seed", C.c_uint64), ("sponge_points", C.c_int32),
+                ("sponge_strength", C.c_double), ("eta_factor", C.c_double)]
+
+
+# Every symbol include/bornsweep.h declares (tests/test_abi.py checks the header agrees).
+ABI_FUNCTIONS = {
+    "bp_last_error": (C.c_char_p, []),
+    "bp_abi_version": (C.c_int, []),
+    "bp_problem_create": (C.c_int, [C.POINTER(Grid), C.c_int32, _dp, _dp, _dp, C.c_int32,
+                                    C.POINTER(C.c_void_p)]),
+    "bp_problem_destroy": (C.c_int, [C.c_void_p]),
+    "bp_problem_batch": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(Grid)]),
+    "bp_apply_A": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "bp_apply_V": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "bp_apply_V_adjoint": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "bp_apply_Lref": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "bp_apply_G": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "bp_born_residual": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "bp_residual": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "bp_forward_transform": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "bp_inverse_transform": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "bp_run": (C.c_int, [C.c_void_p, C.POINTER(Map), _dp, C.POINTER(IterConfig), _dp, _dp, _dp,
+                         _dp, C.POINTER(Trace)]),
+    "bp_run_device": (C.c_int, [C.c_void_p, C.POINTER(Map), C.c_void_p, C.POINTER(IterConfig),
+                                C.c_void_p, C.c_void_p, _dp, _dp, C.POINTER(Trace)]),
+    "bp_run_snapshots": (C.c_int, [C.c_void_p, C.POINTER(Map), _dp, C.POINTER(IterConfig), _dp,
+                                   _dp, _dp, _dp, C.POINTER(Trace), _dp, C.c_int32]),
+    "bp_set_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+    "bp_last_run_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                    _dp, _dp, C.POINTER(C.c_int64)]),
+}
+
+HOST_FUNCTIONS = {
+    "bp_make_instances": (C.c_int, [C.POINTER(InstanceSpec), C.c_int64, C.c_int32, _dp, _dp, _dp,
+                                    _dp, C.c_int32]),
+    "bp_rng_normals": (None, [C.c_uint64, C.c_int64, C.c_int32, _dp]),
+    "bp_rng_uniforms": (None, [C.c_uint64, C.c_int64, C.c_int32, _dp]),
+    "bp_sponge_profile": (None, [C.c_int32, C.c_int32, C.c_int32, C.c_double, _dp]),
+    "bp_gaussian_bump": (None, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                C.c_double, C.c_double, C.c_double, _dp]),
+    "bp_gaussian_smooth": (None, [C.c_int32, C.c_int32, C.c_double, _dp, _dp]),
+}
+
+_lib = None
+_host = None
+
+
+def _bind(lib, table):
+    for name, (res, args) in table.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def lib():
+    """The CUDA library.  Raises if it was not built -- there is no CPU fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryMissing(
+                f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        _lib = _bind(C.CDLL(LIB_PATH), ABI_FUNCTIONS)
+    return _lib
+
+
+def host_lib():
+    global _host
+    if _host is None:
+        if not os.path.exists(HOST_LIB_PATH):
+            raise NativeLibraryMissing(f"{HOST_LIB_PATH} is missing: build the package first")
+        _host = _bind(C.CDLL(HOST_LIB_PATH), HOST_FUNCTIONS)
+    return _host
+
+
+def last_error() -> str:
+    return lib().bp_last_error().decode()

@@ -1,0 +1,243 @@
+"""Python mirror of the reference's operator / preconditioner / driver API over the C ABI.
+
+Reference interface (all under /root/reference/proj):
+  bp::Problem          include/bp/problem.hpp:16-49   -> HelmholtzDirichlet
+  bp::CorrectionMap    include/bp/correction.hpp:16-40 -> ScalarMap, PointwiseMap, ...
+  bp::IterationConfig  include/bp/iterate.hpp:14-18   -> IterationConfig
+  bp::run / RunResult  include/bp/iterate.hpp:57-67   -> run() / RunResult
+Error behaviour follows the reference's exceptions: std::invalid_argument -> ValueError,
+std::runtime_error -> RuntimeError.  Fields are numpy complex128 arrays shaped
+(batch, nx, ny) (or (nx, ny) for a single member), row-major x slow like bp::ComplexField.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+
+BC_PERIODIC, BC_DIRICHLET, BC_NEUMANN = 0, 1, 2
+FORMATS = {"direct": 0, "cbs": 1, "npbs": 2}
+TERMINATION = {0: "converged", 1: "max_iters", 2: "diverged", 3: "stagnated"}
+
+
+class BornSweepError(RuntimeError):
+    pass
+
+
+class CudaError(BornSweepError):
+    pass
+
+
+def _raise(rc: int) -> None:
+    msg = N.last_error()
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise RuntimeError(msg)
+    if rc == 5:
+        raise NotImplementedError(msg)
+    if rc == 3:
+        raise CudaError(msg)
+    raise BornSweepError(f"status {rc}: {msg}")
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        _raise(rc)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+# ---------------------------------------------------------------------------- maps
+@dataclass
+class ScalarMap:
+    """bp::ScalarMap (classical CBS coefficient), correction.hpp:16-18."""
+    gamma: complex = 1.0 + 0.0j
+
+    def _c(self):
+        g = complex(self.gamma)
+        return N.Map(0, g.real, g.imag, 0, None)
+
+
+@dataclass
+class PointwiseMap:
+    """Diagonal relaxation gamma(x) = (i/eta) V(x) (Osnabrugge CBS)."""
+
+    def _c(self):
+        return N.Map(3, 0.0, 0.0, 0, None)
+
+
+@dataclass
+class OptimalScalarMap:
+    """bp::OptimalScalarMap (correction.hpp:20-23).  Not on the GPU yet: run() raises."""
+    metric: str = "euclidean"
+
+    def _c(self):
+        return N.Map(1, 0.0, 0.0, 0 if self.metric == "euclidean" else 1, None)
+
+
+@dataclass
+class IterationConfig:
+    """bp::IterationConfig (iterate.hpp:14-18)."""
+    format: str = "npbs"
+    rtol: float = 1e-6
+    max_iters: int = 1000
+
+    def _c(self):
+        return N.IterConfig(FORMATS[self.format], float(self.rtol), int(self.max_iters))
+
+
+@dataclass
+class IterationTrace:
+    """bp::IterationTrace (iterate.hpp:25-32); entry 0 is the initial residual."""
+    res_l2_rel: np.ndarray
+    res_reta_rel: np.ndarray
+    iters: int
+    terminated: str
+    fnorm_l2: float
+    fnorm_reta: float
+
+
+@dataclass
+class RunResult:
+    u: np.ndarray
+    traces: list = field(default_factory=list)
+    snapshots: np.ndarray | None = None
+
+    @property
+    def trace(self) -> IterationTrace:
+        return self.traces[0]
+
+
+# ---------------------------------------------------------------------------- problem
+class HelmholtzDirichlet:
+    """Batch of Dirichlet five-point Helmholtz problems on the GPU.
+
+    A = L_D - k2, L_ref = L_D - (k0^2 + i eta), V = k2 - (k0^2 + i eta): the reference's
+    HelmholtzProblem splitting (helmholtz.cpp:11-25) on the DirichletInterior / DST-I /
+    five-point pattern of NewtonJacobianProblem (newton_problem.cpp:17-44).
+    """
+
+    def __init__(self, k2, k0, eta, lx: float = 1.0, device: int = 0):
+        k2 = np.asarray(k2, dtype=np.complex128)
+        self.single = k2.ndim == 2
+        k2 = np.ascontiguousarray(k2.reshape((1,) + k2.shape) if self.single else k2)
+        self.batch, self.nx, self.ny = k2.shape
+        k0 = np.ascontiguousarray(np.broadcast_to(np.asarray(k0, np.float64), (self.batch,)))
+        eta = np.ascontiguousarray(np.broadcast_to(np.asarray(eta, np.float64), (self.batch,)))
+        self.k0, self.eta, self.lx, self.device = k0, eta, lx, device
+        g = N.Grid(self.nx, self.ny, lx, lx, BC_DIRICHLET)
+        h = C.c_void_p()
+        self._lib = N.lib()
+        _check(self._lib.bp_problem_create(C.byref(g), self.batch, _ptr(k2), _ptr(k0), _ptr(eta),
+                                           device, C.byref(h)))
+        self._h = h
+
+    # context management / lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.bp_problem_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def shape(self):
+        return (self.batch, self.nx, self.ny)
+
+    def _field(self, x):
+        x = np.asarray(x, dtype=np.complex128)
+        if x.shape == (self.nx, self.ny) and self.batch == 1:
+            x = x.reshape(self.shape)
+        if x.shape != self.shape:
+            raise ValueError(f"field shape {x.shape} does not match problem {self.shape}")
+        return np.ascontiguousarray(x)
+
+    def _out(self, out):
+        return out.reshape(self.nx, self.ny) if self.single else out
+
+    def _unary(self, fn, x):
+        x = self._field(x)
+        out = np.empty_like(x)
+        _check(getattr(self._lib, fn)(self._h, _ptr(x), _ptr(out)))
+        return self._out(out)
+
+    def apply_A(self, u): return self._unary("bp_apply_A", u)
+    def apply_V(self, u): return self._unary("bp_apply_V", u)
+    def apply_V_adjoint(self, u): return self._unary("bp_apply_V_adjoint", u)
+    def apply_Lref(self, u): return self._unary("bp_apply_Lref", u)
+    def apply_G(self, q): return self._unary("bp_apply_G", q)
+    def forward_transform(self, x): return self._unary("bp_forward_transform", x)
+    def inverse_transform(self, x): return self._unary("bp_inverse_transform", x)
+
+    def born_residual(self, u, f):
+        u, f = self._field(u), self._field(f)
+        out = np.empty_like(u)
+        _check(self._lib.bp_born_residual(self._h, _ptr(u), _ptr(f), _ptr(out)))
+        return self._out(out)
+
+    def residual(self, u, f):
+        u, f = self._field(u), self._field(f)
+        out = np.empty_like(u)
+        _check(self._lib.bp_residual(self._h, _ptr(u), _ptr(f), _ptr(out)))
+        return self._out(out)
+
+    def set_kernel_timing(self, enable: bool) -> None:
+        _check(self._lib.bp_set_kernel_timing(self._h, int(bool(enable))))
+
+    def last_run_stats(self) -> dict:
+        la, sw, tm = C.c_int64(), C.c_int64(), C.c_int64()
+        r, c = C.c_double(), C.c_double()
+        _check(self._lib.bp_last_run_stats(self._h, C.byref(la), C.byref(sw), C.byref(r),
+                                           C.byref(c), C.byref(tm)))
+        return {"kernel_launches": la.value, "active_sweeps": sw.value, "row_ms": r.value,
+                "col_ms": c.value, "timed_sweeps": tm.value}
+
+
+def run(problem: HelmholtzDirichlet, cmap, f, config: IterationConfig | None = None, u0=None,
+        n_snap: int = 0) -> RunResult:
+    """bp::run (iterate.cpp:88-153) over every member of the batch."""
+    config = config or IterationConfig()
+    f = problem._field(f)
+    u0 = None if u0 is None else problem._field(u0)
+    u = np.empty_like(f)
+    stride = config.max_iters + 1
+    l2 = np.empty((problem.batch, stride))
+    rt = np.empty((problem.batch, stride))
+    info = (N.Trace * problem.batch)()
+    mp, cfg = cmap._c(), config._c()
+    lib = problem._lib
+    snaps = None
+    if n_snap:
+        snaps = np.zeros((n_snap,) + problem.shape, np.complex128)
+        rc = lib.bp_run_snapshots(problem.handle, C.byref(mp), _ptr(f), C.byref(cfg), _ptr(u0),
+                                  _ptr(u), _ptr(l2), _ptr(rt), info, _ptr(snaps), n_snap)
+    else:
+        rc = lib.bp_run(problem.handle, C.byref(mp), _ptr(f), C.byref(cfg), _ptr(u0), _ptr(u),
+                        _ptr(l2), _ptr(rt), info)
+    _check(rc)
+    traces = []
+    for b in range(problem.batch):
+        k = info[b].iters + 1
+        traces.append(IterationTrace(l2[b, :k].copy(), rt[b, :k].copy(), info[b].iters,
+                                     TERMINATION[info[b].terminated], info[b].fnorm_l2,
+                                     info[b].fnorm_reta))
+    if snaps is not None and problem.single:
+        snaps = snaps[:, 0]
+    return RunResult(problem._out(u), traces, snaps)

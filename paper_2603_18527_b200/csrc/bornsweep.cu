@@ -1,0 +1,871 @@
+// bornsweep.cu -- C ABI (include/bornsweep.h) over the sm_100a sweep kernels.
+//
+// Host side of the drop-in boundary: problem handles (bp::Problem), operator applications,
+// and the iteration driver (bp::run, proj/src/iterate.cpp:88-153) executed as a device-side
+// loop: each sweep is two kernel launches, the termination test runs on the device, and the
+// host replays CUDA graphs of GRAPH_SWEEPS sweeps, polling one pinned counter per replay.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bornsweep.h"
+#include "sweep_kernels.cuh"
+
+using namespace bs;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CU(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (call);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            return set_err(BP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+constexpr int kGraphSweeps = 16;
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kSymbolDivGuard = 1e-14;  // proj/include/bp/symbol.hpp:24
+
+// ------------------------------------------------------------------ small kernels
+__global__ void pack_kernel(const double2* __restrict__ dense, double2* __restrict__ padded,
+                            int batch, int log2n) {
+    const int n = 1 << log2n, nd = n - 1;
+    const size_t total = (size_t)batch * n * n;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t b = idx >> (2 * log2n);
+        const int i = (int)((idx >> log2n) & (n - 1)), j = (int)(idx & (n - 1));
+        double2 v = make_double2(0.0, 0.0);
+        if (dense && i > 0 && j > 0) v = dense[(b * nd + (i - 1)) * nd + (j - 1)];
+        padded[idx] = v;
+    }
+}
+
+// select: per-member ping/pong source (result_buf) when non-null
+__global__ void unpack_kernel(const double2* __restrict__ p0, const double2* __restrict__ p1,
+                              const int* __restrict__ select, double2* __restrict__ dense,
+                              int batch, int log2n) {
+    const int n = 1 << log2n, nd = n - 1;
+    const size_t total = (size_t)batch * nd * nd;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t b = idx / ((size_t)nd * nd);
+        const size_t r = idx % ((size_t)nd * nd);
+        const int i = (int)(r / nd) + 1, j = (int)(r % nd) + 1;
+        const double2* src = (select && select[b]) ? p1 : p0;
+        dense[idx] = src[(b << (2 * log2n)) + ((size_t)i << log2n) + j];
+    }
+}
+
+// op: 0 A u, 1 V u, 2 V^H u, 3 f - A u (sub = f)
+__global__ void pointwise_kernel(int op, const double2* __restrict__ u, const double2* __restrict__ k2,
+                                 const double2* __restrict__ f, const double* __restrict__ k0sq,
+                                 const double* __restrict__ eta, double inv_h2,
+                                 double2* __restrict__ out, int batch, int log2n) {
+    const int n = 1 << log2n;
+    const size_t total = (size_t)batch * n * n;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t b = idx >> (2 * log2n);
+        const int i = (int)((idx >> log2n) & (n - 1)), j = (int)(idx & (n - 1));
+        double2 o = make_double2(0.0, 0.0);
+        if (i > 0 && j > 0) {
+            const double2 uu = u[idx], kk = k2[idx];
+            const double2 shift = make_double2(k0sq[b], eta[b]);
+            if (op == 1) {
+                o = cmul(uu, csub(kk, shift));
+            } else if (op == 2) {
+                o = cmul(cconj(csub(kk, shift)), uu);
+            } else {
+                double2 s = cscale(uu, 4.0);
+                s = csub(s, u[idx - n]);
+                s = csub(s, u[idx + n]);
+                s = csub(s, u[idx - 1]);
+                if (j + 1 < n) s = csub(s, u[idx + 1]);
+                o = csub(cscale(s, inv_h2), cmul(kk, uu));
+                if (op == 3) o = csub(f[idx], o);
+            }
+        }
+        out[idx] = o;
+    }
+}
+
+// per-member sum of |x|^2 over a padded field; partials[b*nchunk + c], deterministic
+__global__ void norm_partial_kernel(const double2* __restrict__ x, int log2n, int nchunk,
+                                    double* __restrict__ partials) {
+    const int b = blockIdx.y, c = blockIdx.x;
+    const size_t per = (size_t)1 << (2 * log2n);
+    const size_t chunk = (per + nchunk - 1) / nchunk;
+    const size_t lo = c * chunk, hi = min(per, lo + chunk);
+    double s = 0.0;
+    for (size_t k = lo + threadIdx.x; k < hi; k += blockDim.x) s += cnorm(x[b * per + k]);
+    __shared__ double red[256];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int d = blockDim.x / 2; d > 0; d >>= 1) {
+        if (threadIdx.x < d) red[threadIdx.x] += red[threadIdx.x + d];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partials[b * nchunk + c] = red[0];
+}
+
+__global__ void norm_final_kernel(const double* __restrict__ partials, int nchunk, int batch,
+                                  double* __restrict__ out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c) s += partials[b * nchunk + c];
+    out[b] = sqrt(s);
+}
+
+__global__ void init_control_kernel(Control c, int batch) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < batch) {
+        c.status[b] = ST_ACTIVE;
+        c.sweep[b] = 0;
+        c.counter[b] = 0u;
+        c.iters[b] = 0;
+        c.term[b] = 1;
+        c.result_buf[b] = 0;
+    }
+    if (b == 0) *c.n_active = batch;
+}
+
+__global__ void fill_nan_kernel(double* p, size_t n) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
+         k += (size_t)gridDim.x * blockDim.x)
+        p[k] = __longlong_as_double(0x7ff8000000000000LL);
+}
+
+// ------------------------------------------------------------------ launch tables
+constexpr int kMinLog2 = 3, kMaxLog2 = 9;
+
+template <int L>
+struct RowCfg {
+    static constexpr int T = Geom<L>::T;
+    static constexpr int NW = 8;
+    static constexpr int EPB = NW * (32 / T);
+    static constexpr size_t SMEM = sizeof(double2) * EPB * Geom<L>::PAD_N;
+};
+template <int L>
+struct ColCfg {
+    static constexpr int C = 8;
+    static constexpr int THREADS = C * Geom<L>::T;
+    static constexpr size_t SMEM = sizeof(double2) * (C * Geom<L>::PAD_N + C * Geom<L>::T);
+};
+
+template <int L, int MODE>
+cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare = false) {
+    using Cf = RowCfg<L>;
+    auto k = row_kernel<L, MODE, Cf::NW>;
+    if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    const long rows = (long)a.batch << L;
+    const int grid = (int)((rows + Cf::EPB - 1) / Cf::EPB);
+    k<<<grid, Cf::NW * 32, Cf::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int L, int MODE>
+cudaError_t launch_col_t(const ColArgs& a, cudaStream_t s, bool prepare = false) {
+    using Cf = ColCfg<L>;
+    auto k = col_kernel<L, MODE, Cf::C>;
+    if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    const int grid = a.batch * ((1 << L) / Cf::C);
+    k<<<grid, Cf::THREADS, Cf::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int L>
+cudaError_t launch_row_l(int mode, const RowArgs& a, cudaStream_t s) {
+    switch (mode) {
+        case R_FWD: return launch_row_t<L, R_FWD>(a, s);
+        case R_FWD_BORN: return launch_row_t<L, R_FWD_BORN>(a, s);
+        case R_INV: return launch_row_t<L, R_INV>(a, s);
+        default: return launch_row_t<L, R_SWEEP>(a, s);
+    }
+}
+template <int L>
+cudaError_t launch_col_l(int mode, const ColArgs& a, cudaStream_t s) {
+    switch (mode) {
+        case C_ONE: return launch_col_t<L, C_ONE>(a, s);
+        case C_GREEN: return launch_col_t<L, C_GREEN>(a, s);
+        default: return launch_col_t<L, C_LREF>(a, s);
+    }
+}
+
+cudaError_t launch_row(int log2n, int mode, const RowArgs& a, cudaStream_t s) {
+    switch (log2n) {
+        case 3: return launch_row_l<3>(mode, a, s);
+        case 4: return launch_row_l<4>(mode, a, s);
+        case 5: return launch_row_l<5>(mode, a, s);
+        case 6: return launch_row_l<6>(mode, a, s);
+        case 7: return launch_row_l<7>(mode, a, s);
+        case 8: return launch_row_l<8>(mode, a, s);
+        case 9: return launch_row_l<9>(mode, a, s);
+    }
+    return cudaErrorInvalidValue;
+}
+cudaError_t launch_col(int log2n, int mode, const ColArgs& a, cudaStream_t s) {
+    switch (log2n) {
+        case 3: return launch_col_l<3>(mode, a, s);
+        case 4: return launch_col_l<4>(mode, a, s);
+        case 5: return launch_col_l<5>(mode, a, s);
+        case 6: return launch_col_l<6>(mode, a, s);
+        case 7: return launch_col_l<7>(mode, a, s);
+        case 8: return launch_col_l<8>(mode, a, s);
+        case 9: return launch_col_l<9>(mode, a, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int L>
+cudaError_t prepare_l() {
+    RowArgs a{};
+    ColArgs c{};
+    cudaError_t e = cudaSuccess;
+    for (cudaError_t r : {launch_row_t<L, R_FWD>(a, nullptr, true), launch_row_t<L, R_FWD_BORN>(a, nullptr, true),
+                          launch_row_t<L, R_INV>(a, nullptr, true), launch_row_t<L, R_SWEEP>(a, nullptr, true),
+                          launch_col_t<L, C_ONE>(c, nullptr, true), launch_col_t<L, C_GREEN>(c, nullptr, true),
+                          launch_col_t<L, C_LREF>(c, nullptr, true)})
+        if (r != cudaSuccess) e = r;
+    return e;
+}
+
+cudaError_t prepare_kernels(int log2n) {
+    switch (log2n) {
+        case 3: return prepare_l<3>();
+        case 4: return prepare_l<4>();
+        case 5: return prepare_l<5>();
+        case 6: return prepare_l<6>();
+        case 7: return prepare_l<7>();
+        case 8: return prepare_l<8>();
+        case 9: return prepare_l<9>();
+    }
+    return cudaErrorInvalidValue;
+}
+
+int grid_for(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 16); }
+
+}  // namespace
+
+// ------------------------------------------------------------------ handle
+struct bp_problem {
+    bp_grid grid{};
+    int batch = 0, device = 0, log2n = 0, n = 0;
+    size_t field = 0;   // padded elements per member (n*n)
+    size_t alloc = 0;   // padded elements per buffer (batch*n*n + n)
+    double inv_h2 = 0, green_scale = 0;
+    cudaStream_t stream = nullptr;
+    // device constants
+    double2* k2 = nullptr;
+    double* k0sq = nullptr;
+    double* eta = nullptr;
+    double2* tw = nullptr;
+    double* sinp = nullptr;
+    double* lap = nullptr;
+    // workspace
+    double2 *f = nullptr, *u0 = nullptr, *u1 = nullptr, *T = nullptr, *x = nullptr, *y = nullptr;
+    double2* dense = nullptr;  // batch * nx*ny staging
+    double2* partial = nullptr;
+    double* norm_part = nullptr;
+    double *fnorm_l2 = nullptr, *fnorm_reta = nullptr;
+    int* ctl_int = nullptr;  // status, sweep, iters, term, result_buf, n_active
+    unsigned* counter = nullptr;
+    double *trace_l2 = nullptr, *trace_reta = nullptr;
+    int trace_cap = 0;
+    int* host_active = nullptr;  // pinned
+    // graph cache
+    cudaGraphExec_t graph = nullptr;
+    int graph_map_kind = -1;
+    double2 graph_gamma{};
+    int graph_max_iters = -1;
+    double graph_rtol = -1;
+    // instrumentation
+    bool timing = false;
+    int64_t stat_launches = 0, stat_sweeps = 0, stat_timed = 0;
+    double stat_row_ms = 0, stat_col_ms = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        cudaGetDevice(&prev);
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+Control make_control(const bp_problem* p) {
+    Control c{};
+    int* ci = p->ctl_int;
+    const int B = p->batch;
+    c.status = ci;
+    c.sweep = ci + B;
+    c.iters = ci + 2 * B;
+    c.term = ci + 3 * B;
+    c.result_buf = ci + 4 * B;
+    c.n_active = ci + 5 * B;
+    c.counter = p->counter;
+    c.partial = p->partial;
+    c.fnorm_l2 = p->fnorm_l2;
+    c.fnorm_reta = p->fnorm_reta;
+    c.trace_l2 = p->trace_l2;
+    c.trace_reta = p->trace_reta;
+    return c;
+}
+
+RowArgs row_args(const bp_problem* p) {
+    RowArgs a{};
+    a.batch = p->batch;
+    a.inv_h2 = p->inv_h2;
+    a.k0sq = p->k0sq;
+    a.eta = p->eta;
+    a.k2 = p->k2;
+    a.f = p->f;
+    a.T = p->T;
+    a.u0 = p->u0;
+    a.u1 = p->u1;
+    a.tw = p->tw;
+    a.sinp = p->sinp;
+    a.map_kind = MK_SCALAR;
+    a.gamma = make_double2(1.0, 0.0);
+    a.ctl = make_control(p);
+    return a;
+}
+
+ColArgs col_args(const bp_problem* p) {
+    ColArgs c{};
+    c.batch = p->batch;
+    c.k0sq = p->k0sq;
+    c.eta = p->eta;
+    c.lap = p->lap;
+    c.scale = p->green_scale;
+    c.T = p->T;
+    c.tw = p->tw;
+    c.sinp = p->sinp;
+    c.status = nullptr;
+    return c;
+}
+
+int check_problem(const bp_problem* p) {
+    if (!p) return set_err(BP_EINVAL, "null problem handle");
+    return BP_OK;
+}
+
+// dense host -> padded device
+int upload(bp_problem* p, const double* host, double2* dst, bool host_ptr = true) {
+    const size_t nd = (size_t)p->grid.nx * p->grid.ny;
+    const size_t bytes = sizeof(double2) * nd * p->batch;
+    const double2* src = reinterpret_cast<const double2*>(host);
+    if (host_ptr) {
+        CU(cudaMemcpyAsync(p->dense, host, bytes, cudaMemcpyHostToDevice, p->stream));
+        src = p->dense;
+    }
+    pack_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(src, dst, p->batch, p->log2n);
+    CU(cudaGetLastError());
+    return BP_OK;
+}
+
+int download(bp_problem* p, const double2* p0, const double2* p1, const int* select, double* host,
+             bool host_ptr = true) {
+    const size_t nd = (size_t)p->grid.nx * p->grid.ny;
+    double2* dst = host_ptr ? p->dense : reinterpret_cast<double2*>(host);
+    unpack_kernel<<<grid_for(nd * p->batch), 256, 0, p->stream>>>(p0, p1, select, dst, p->batch,
+                                                                   p->log2n);
+    CU(cudaGetLastError());
+    if (host_ptr)
+        CU(cudaMemcpyAsync(host, p->dense, sizeof(double2) * nd * p->batch, cudaMemcpyDeviceToHost,
+                           p->stream));
+    return BP_OK;
+}
+
+int norms(bp_problem* p, const double2* x, double* out) {
+    const int nchunk = 64;
+    dim3 g(nchunk, p->batch);
+    norm_partial_kernel<<<g, 256, 0, p->stream>>>(x, p->log2n, nchunk, p->norm_part);
+    norm_final_kernel<<<(p->batch + 127) / 128, 128, 0, p->stream>>>(p->norm_part, nchunk,
+                                                                      p->batch, out);
+    CU(cudaGetLastError());
+    return BP_OK;
+}
+
+// Green operator on padded `in` -> padded `out` (out - sub when sub != null)
+int green(bp_problem* p, const double2* in, double2* out, const double2* sub, bool born) {
+    RowArgs a = row_args(p);
+    a.in = in;
+    CU(launch_row(p->log2n, born ? R_FWD_BORN : R_FWD, a, p->stream));
+    ColArgs c = col_args(p);
+    CU(launch_col(p->log2n, C_GREEN, c, p->stream));
+    a.out = out;
+    a.sub = sub;
+    CU(launch_row(p->log2n, R_INV, a, p->stream));
+    return BP_OK;
+}
+
+int ensure_trace(bp_problem* p, int max_iters) {
+    if (p->trace_cap >= max_iters + 1) return BP_OK;
+    cudaFree(p->trace_l2);
+    cudaFree(p->trace_reta);
+    p->trace_l2 = p->trace_reta = nullptr;
+    const size_t n = (size_t)p->batch * (max_iters + 1);
+    CU(cudaMalloc(&p->trace_l2, sizeof(double) * n));
+    CU(cudaMalloc(&p->trace_reta, sizeof(double) * n));
+    p->trace_cap = max_iters + 1;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+    return BP_OK;
+}
+
+int sweep_once(bp_problem* p, const RowArgs& a, const ColArgs& c, cudaEvent_t* ev) {
+    if (ev) CU(cudaEventRecord(ev[0], p->stream));
+    CU(launch_row(p->log2n, R_SWEEP, a, p->stream));
+    if (ev) CU(cudaEventRecord(ev[1], p->stream));
+    CU(launch_col(p->log2n, C_GREEN, c, p->stream));
+    if (ev) CU(cudaEventRecord(ev[2], p->stream));
+    return BP_OK;
+}
+
+// The driver: bp::run over the batch.  f_dev/u0_dev padded device fields already staged.
+int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool have_u0,
+             double* snapshots, int n_snap) {
+    const int B = p->batch;
+    RowArgs a = row_args(p);
+    a.ctl.max_iters = cfg->max_iters;
+    a.ctl.rtol = cfg->rtol;
+    a.map_kind = map->kind;
+    a.gamma = make_double2(map->gamma_re, map->gamma_im);
+    ColArgs c = col_args(p);
+    c.status = a.ctl.status;
+
+    // fnorm_l2 = ||f||, fnorm_reta = ||G f||  (iterate.cpp:93,102)
+    int rc = norms(p, p->f, p->fnorm_l2);
+    if (rc) return rc;
+    rc = green(p, p->f, p->y, nullptr, false);
+    if (rc) return rc;
+    rc = norms(p, p->y, p->fnorm_reta);
+    if (rc) return rc;
+    std::vector<double> fn(B);
+    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    for (int b = 0; b < B; ++b)
+        if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
+
+    if (!have_u0) CU(cudaMemsetAsync(p->u0, 0, sizeof(double2) * p->alloc, p->stream));
+    CU(cudaMemsetAsync(p->u1, 0, sizeof(double2) * p->alloc, p->stream));
+    init_control_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(a.ctl, B);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_l2, (size_t)B * p->trace_cap);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_reta, (size_t)B * p->trace_cap);
+    CU(cudaGetLastError());
+
+    // q^0 = V u^0 + f -> forward y-DST -> T ; column pass
+    a.in = p->u0;
+    CU(launch_row(p->log2n, R_FWD_BORN, a, p->stream));
+    CU(launch_col(p->log2n, C_GREEN, c, p->stream));
+
+    p->stat_launches = 2;
+    p->stat_row_ms = p->stat_col_ms = 0;
+    p->stat_timed = 0;
+    const long max_launch = (long)cfg->max_iters + 1;  // launch k records entry k-1
+    const size_t nd = (size_t)p->grid.nx * p->grid.ny;
+
+    if (snapshots && n_snap > 0) {
+        // u^0
+        rc = download(p, p->u0, p->u0, nullptr, snapshots);
+        if (rc) return rc;
+    }
+
+    if ((snapshots && n_snap > 0) || p->timing) {
+        cudaEvent_t ev[3];
+        for (auto& e : ev) CU(cudaEventCreate(&e));
+        long k = 0;
+        for (k = 1; k <= max_launch; ++k) {
+            rc = sweep_once(p, a, c, p->timing ? ev : nullptr);
+            if (rc) break;
+            p->stat_launches += 2;
+            if (snapshots && k < n_snap) {
+                // u^k lives in buffer k&1 for every member still iterating
+                rc = download(p, (k & 1) ? p->u1 : p->u0, nullptr, nullptr,
+                              snapshots + 2 * nd * B * k);
+                if (rc) break;
+            }
+            CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
+                               p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            if (p->timing) {
+                float r = 0, cc = 0;
+                cudaEventElapsedTime(&r, ev[0], ev[1]);
+                cudaEventElapsedTime(&cc, ev[1], ev[2]);
+                p->stat_row_ms += r;
+                p->stat_col_ms += cc;
+                ++p->stat_timed;
+            }
+            if (*p->host_active == 0) break;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (rc) return rc;
+    } else {
+        // graph of kGraphSweeps sweeps, replayed until every member terminated
+        const bool reuse = p->graph && p->graph_map_kind == map->kind &&
+                           p->graph_gamma.x == map->gamma_re && p->graph_gamma.y == map->gamma_im &&
+                           p->graph_max_iters == cfg->max_iters && p->graph_rtol == cfg->rtol;
+        if (!reuse) {
+            if (p->graph) cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+            cudaGraph_t g;
+            CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+            for (int s = 0; s < kGraphSweeps; ++s) {
+                launch_row(p->log2n, R_SWEEP, a, p->stream);
+                launch_col(p->log2n, C_GREEN, c, p->stream);
+            }
+            CU(cudaStreamEndCapture(p->stream, &g));
+            CU(cudaGraphInstantiate(&p->graph, g, 0));
+            cudaGraphDestroy(g);
+            p->graph_map_kind = map->kind;
+            p->graph_gamma = a.gamma;
+            p->graph_max_iters = cfg->max_iters;
+            p->graph_rtol = cfg->rtol;
+        }
+        long launched = 0;
+        while (launched < max_launch) {
+            CU(cudaGraphLaunch(p->graph, p->stream));
+            launched += kGraphSweeps;
+            p->stat_launches += 2 * kGraphSweeps;
+            CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
+                               p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            if (*p->host_active == 0) break;
+        }
+    }
+    return BP_OK;
+}
+
+int finish_run(bp_problem* p, const bp_iter_config* cfg, double* u_out, bool host_ptr,
+               double* res_l2, double* res_reta, bp_trace* info) {
+    const int B = p->batch;
+    Control c = make_control(p);
+    int rc = download(p, p->u0, p->u1, c.result_buf, u_out, host_ptr);
+    if (rc) return rc;
+    std::vector<int> iters(B), term(B);
+    std::vector<double> f1(B), f2(B);
+    CU(cudaMemcpyAsync(iters.data(), c.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaMemcpyAsync(term.data(), c.term, sizeof(int) * B, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaMemcpyAsync(f1.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaMemcpyAsync(f2.data(), p->fnorm_reta, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
+    const int stride = cfg->max_iters + 1;
+    if (res_l2)
+        CU(cudaMemcpy2DAsync(res_l2, sizeof(double) * stride, p->trace_l2, sizeof(double) * p->trace_cap,
+                             sizeof(double) * stride, B, cudaMemcpyDeviceToHost, p->stream));
+    if (res_reta)
+        CU(cudaMemcpy2DAsync(res_reta, sizeof(double) * stride, p->trace_reta,
+                             sizeof(double) * p->trace_cap, sizeof(double) * stride, B,
+                             cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    p->stat_sweeps = 0;
+    for (int b = 0; b < B; ++b) {
+        if (info) {
+            info[b].iters = iters[b];
+            info[b].terminated = term[b];
+            info[b].fnorm_l2 = f1[b];
+            info[b].fnorm_reta = f2[b];
+        }
+        p->stat_sweeps += iters[b];
+    }
+    return BP_OK;
+}
+
+int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* cfg) {
+    if (int rc = check_problem(p)) return rc;
+    if (!map || !cfg) return set_err(BP_EINVAL, "run: null map or config");
+    if (!(cfg->rtol > 0.0 && cfg->rtol < 1.0)) return set_err(BP_EINVAL, "run: rtol must lie in (0,1)");
+    if (cfg->max_iters < 1) return set_err(BP_EINVAL, "run: max_iters must be >= 1");
+    if (cfg->format != BP_FMT_NPBS && cfg->format != BP_FMT_CBS)
+        return set_err(BP_ENOTSUP, "run: only the CBS / NPBS formats are implemented on the GPU");
+    if (map->kind != BP_MAP_SCALAR && map->kind != BP_MAP_POINTWISE)
+        return set_err(BP_ENOTSUP, "run: correction map not implemented on the GPU yet");
+    return BP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bp_last_error(void) { return g_err.c_str(); }
+int bp_abi_version(void) { return BP_ABI_VERSION; }
+
+int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, const double* k0,
+                      const double* eta, int32_t device, bp_problem** out) {
+    if (!out) return set_err(BP_EINVAL, "null output handle");
+    *out = nullptr;
+    if (!grid || !k2 || !k0 || !eta) return set_err(BP_EINVAL, "null argument");
+    if (grid->nx < 2 || grid->ny < 2) return set_err(BP_EINVAL, "GridSpec: nx,ny must be >= 2");
+    if (!(grid->lx > 0.0) || !(grid->ly > 0.0)) return set_err(BP_EINVAL, "GridSpec: lx,ly must be > 0");
+    if (batch < 1) return set_err(BP_EINVAL, "batch must be >= 1");
+    if (grid->bc != BP_BC_DIRICHLET)
+        return set_err(BP_ENOTSUP, "only DirichletInterior grids are implemented on the GPU");
+    const int n = grid->nx + 1;
+    int log2n = 0;
+    while ((1 << log2n) < n) ++log2n;
+    if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > kMaxLog2)
+        return set_err(BP_ENOTSUP, "GPU path needs square grids with nx+1 = 2^k, 8 <= 2^k <= 512");
+    if (grid->lx != grid->ly) return set_err(BP_ENOTSUP, "GPU path needs lx == ly (hx == hy)");
+    const size_t nd = (size_t)grid->nx * grid->ny;
+    for (int b = 0; b < batch; ++b) {
+        if (!(eta[b] > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
+        if (!std::isfinite(k0[b])) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
+    }
+    for (size_t k = 0; k < 2 * nd * batch; ++k)
+        if (!std::isfinite(k2[k])) return set_err(BP_EINVAL, "HelmholtzProblem: k2 not finite");
+
+    // symbol invertibility (Problem ctor -> check_invertible, proj/src/symbol.cpp:102-111)
+    const double h = grid->lx / n;
+    const double ax = 4.0 / (h * h);
+    std::vector<double> lap(n, 0.0);
+    for (int j = 1; j < n; ++j) {
+        const double sx = std::sin(j * kPi / (2.0 * n));
+        lap[j] = ax * sx * sx;
+    }
+    for (int b = 0; b < batch; ++b) {
+        double mn = INFINITY, mx = 0.0;
+        const double k0sq = k0[b] * k0[b];
+        for (int pp = 1; pp < n; ++pp)
+            for (int qq = 1; qq < n; ++qq) {
+                const double a = std::hypot((lap[pp] + lap[qq]) - k0sq, -eta[b]);
+                mn = std::min(mn, a);
+                mx = std::max(mx, a);
+            }
+        if (mn < kSymbolDivGuard * mx)
+            return set_err(BP_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
+    }
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return set_err(BP_ECUDA, "no such CUDA device");
+    DeviceGuard guard(device);
+    auto* p = new bp_problem();
+    p->grid = *grid;
+    p->batch = batch;
+    p->device = device;
+    p->log2n = log2n;
+    p->n = n;
+    p->field = (size_t)n * n;
+    p->alloc = p->field * batch + n;
+    p->inv_h2 = 1.0 / (h * h);
+    p->green_scale = 4.0 / ((double)n * n);
+    auto fail = [&](int code) {
+        bp_problem_destroy(p);
+        return code;
+    };
+#define CUF(call)                                                                                   \
+    do {                                                                                            \
+        cudaError_t _e = (call);                                                                    \
+        if (_e != cudaSuccess) return fail(set_err(BP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e))); \
+    } while (0)
+    CUF(prepare_kernels(log2n));
+    CUF(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    const size_t fb = sizeof(double2) * p->alloc;
+    CUF(cudaMalloc(&p->k2, fb));
+    CUF(cudaMalloc(&p->f, fb));
+    CUF(cudaMalloc(&p->u0, fb));
+    CUF(cudaMalloc(&p->u1, fb));
+    CUF(cudaMalloc(&p->T, fb));
+    CUF(cudaMalloc(&p->x, fb));
+    CUF(cudaMalloc(&p->y, fb));
+    for (double2* buf : {p->k2, p->f, p->u0, p->u1, p->T, p->x, p->y})
+        CUF(cudaMemsetAsync(buf, 0, fb, p->stream));
+    CUF(cudaMalloc(&p->dense, sizeof(double2) * nd * batch));
+    CUF(cudaMalloc(&p->partial, sizeof(double2) * (size_t)batch * n));
+    CUF(cudaMalloc(&p->norm_part, sizeof(double) * (size_t)batch * 64));
+    CUF(cudaMalloc(&p->fnorm_l2, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->fnorm_reta, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->ctl_int, sizeof(int) * (5 * (size_t)batch + 1)));
+    CUF(cudaMalloc(&p->counter, sizeof(unsigned) * batch));
+    CUF(cudaMallocHost(&p->host_active, sizeof(int)));
+    CUF(cudaMalloc(&p->k0sq, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->eta, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->tw, sizeof(double2) * n));
+    CUF(cudaMalloc(&p->sinp, sizeof(double) * n));
+    CUF(cudaMalloc(&p->lap, sizeof(double) * n));
+    std::vector<double> k0sq(batch), tw(2 * n), sinp(n);
+    for (int b = 0; b < batch; ++b) k0sq[b] = k0[b] * k0[b];
+    for (int k = 0; k < n; ++k) {
+        tw[2 * k] = std::cos(2.0 * kPi * k / n);
+        tw[2 * k + 1] = -std::sin(2.0 * kPi * k / n);
+        sinp[k] = std::sin(kPi * k / n);
+    }
+    CUF(cudaMemcpyAsync(p->k0sq, k0sq.data(), sizeof(double) * batch, cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->eta, eta, sizeof(double) * batch, cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->sinp, sinp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->lap, lap.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
+    if (int rc = upload(p, k2, p->k2)) return fail(rc);
+    CUF(cudaStreamSynchronize(p->stream));
+    if (int rc = ensure_trace(p, 1000)) return fail(rc);
+#undef CUF
+    *out = p;
+    return BP_OK;
+}
+
+int bp_problem_destroy(bp_problem* p) {
+    if (!p) return BP_OK;
+    DeviceGuard guard(p->device);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    if (p->graph) cudaGraphExecDestroy(p->graph);
+    for (void* q : {(void*)p->k2, (void*)p->f, (void*)p->u0, (void*)p->u1, (void*)p->T, (void*)p->x,
+                    (void*)p->y, (void*)p->dense, (void*)p->partial, (void*)p->norm_part,
+                    (void*)p->fnorm_l2, (void*)p->fnorm_reta, (void*)p->ctl_int, (void*)p->counter,
+                    (void*)p->trace_l2, (void*)p->trace_reta, (void*)p->k0sq, (void*)p->eta,
+                    (void*)p->tw, (void*)p->sinp, (void*)p->lap})
+        if (q) cudaFree(q);
+    if (p->host_active) cudaFreeHost(p->host_active);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+    return BP_OK;
+}
+
+int bp_problem_batch(const bp_problem* p, int32_t* batch, bp_grid* grid) {
+    if (int rc = check_problem(p)) return rc;
+    if (batch) *batch = p->batch;
+    if (grid) *grid = p->grid;
+    return BP_OK;
+}
+
+static int pointwise_op(const bp_problem* cp, int op, const double* u, const double* f, double* out) {
+    if (int rc = check_problem(cp)) return rc;
+    if (!u || !out || (op == 3 && !f)) return set_err(BP_EINVAL, "null field");
+    auto* p = const_cast<bp_problem*>(cp);
+    DeviceGuard guard(p->device);
+    if (int rc = upload(p, u, p->x)) return rc;
+    if (op == 3)
+        if (int rc = upload(p, f, p->f)) return rc;
+    pointwise_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(
+        op, p->x, p->k2, p->f, p->k0sq, p->eta, p->inv_h2, p->y, p->batch, p->log2n);
+    CU(cudaGetLastError());
+    if (int rc = download(p, p->y, p->y, nullptr, out)) return rc;
+    CU(cudaStreamSynchronize(p->stream));
+    return BP_OK;
+}
+
+int bp_apply_A(const bp_problem* p, const double* u, double* out) { return pointwise_op(p, 0, u, nullptr, out); }
+int bp_apply_V(const bp_problem* p, const double* u, double* out) { return pointwise_op(p, 1, u, nullptr, out); }
+int bp_apply_V_adjoint(const bp_problem* p, const double* u, double* out) { return pointwise_op(p, 2, u, nullptr, out); }
+int bp_residual(const bp_problem* p, const double* u, const double* f, double* out) { return pointwise_op(p, 3, u, f, out); }
+
+static int spectral_op(const bp_problem* cp, int which, const double* in, const double* f, double* out) {
+    if (int rc = check_problem(cp)) return rc;
+    if (!in || !out || (which == 1 && !f)) return set_err(BP_EINVAL, "null field");
+    auto* p = const_cast<bp_problem*>(cp);
+    DeviceGuard guard(p->device);
+    if (int rc = upload(p, in, p->x)) return rc;
+    RowArgs a = row_args(p);
+    ColArgs c = col_args(p);
+    a.in = p->x;
+    switch (which) {
+        case 0:  // G
+            if (int rc = green(p, p->x, p->y, nullptr, false)) return rc;
+            break;
+        case 1:  // born residual: G(V u + f) - u
+            if (int rc = upload(p, f, p->f)) return rc;
+            if (int rc = green(p, p->x, p->y, p->x, true)) return rc;
+            break;
+        case 2:  // L_ref
+            CU(launch_row(p->log2n, R_FWD, a, p->stream));
+            CU(launch_col(p->log2n, C_LREF, c, p->stream));
+            a.out = p->y;
+            CU(launch_row(p->log2n, R_INV, a, p->stream));
+            break;
+        case 3:  // forward transform (plain sine sums)
+        case 4:  // inverse transform (x 4/((nx+1)(ny+1)))
+            CU(launch_row(p->log2n, R_FWD, a, p->stream));
+            c.scale = which == 3 ? 1.0 : p->green_scale;
+            CU(launch_col(p->log2n, C_ONE, c, p->stream));
+            if (int rc = download(p, p->T, p->T, nullptr, out)) return rc;
+            CU(cudaStreamSynchronize(p->stream));
+            return BP_OK;
+    }
+    if (int rc = download(p, p->y, p->y, nullptr, out)) return rc;
+    CU(cudaStreamSynchronize(p->stream));
+    return BP_OK;
+}
+
+int bp_apply_G(const bp_problem* p, const double* q, double* out) { return spectral_op(p, 0, q, nullptr, out); }
+int bp_born_residual(const bp_problem* p, const double* u, const double* f, double* out) {
+    return spectral_op(p, 1, u, f, out);
+}
+int bp_apply_Lref(const bp_problem* p, const double* u, double* out) { return spectral_op(p, 2, u, nullptr, out); }
+int bp_forward_transform(const bp_problem* p, const double* field, double* modes) {
+    return spectral_op(p, 3, field, nullptr, modes);
+}
+int bp_inverse_transform(const bp_problem* p, const double* modes, double* field) {
+    return spectral_op(p, 4, modes, nullptr, field);
+}
+
+static int run_impl(const bp_problem* cp, const bp_map* map, const double* f, const bp_iter_config* cfg,
+                    const double* u0, double* u_out, double* res_l2, double* res_reta, bp_trace* info,
+                    bool host_ptr, double* snapshots, int n_snap) {
+    if (int rc = validate_run(cp, map, cfg)) return rc;
+    if (!f || !u_out) return set_err(BP_EINVAL, "run: null field");
+    auto* p = const_cast<bp_problem*>(cp);
+    DeviceGuard guard(p->device);
+    if (int rc = ensure_trace(p, cfg->max_iters)) return rc;
+    if (int rc = upload(p, f, p->f, host_ptr)) return rc;
+    if (u0)
+        if (int rc = upload(p, u0, p->u0, host_ptr)) return rc;
+    if (int rc = run_core(p, map, cfg, u0 != nullptr, snapshots, n_snap)) return rc;
+    return finish_run(p, cfg, u_out, host_ptr, res_l2, res_reta, info);
+}
+
+int bp_run(const bp_problem* p, const bp_map* map, const double* f, const bp_iter_config* cfg,
+           const double* u0, double* u_out, double* res_l2, double* res_reta, bp_trace* info) {
+    return run_impl(p, map, f, cfg, u0, u_out, res_l2, res_reta, info, true, nullptr, 0);
+}
+
+int bp_run_device(const bp_problem* p, const bp_map* map, const double* f_dev,
+                  const bp_iter_config* cfg, const double* u0_dev, double* u_out_dev,
+                  double* res_l2, double* res_reta, bp_trace* info) {
+    return run_impl(p, map, f_dev, cfg, u0_dev, u_out_dev, res_l2, res_reta, info, false, nullptr, 0);
+}
+
+int bp_run_snapshots(const bp_problem* p, const bp_map* map, const double* f,
+                     const bp_iter_config* cfg, const double* u0, double* u_out, double* res_l2,
+                     double* res_reta, bp_trace* info, double* snapshots, int32_t n_snap) {
+    return run_impl(p, map, f, cfg, u0, u_out, res_l2, res_reta, info, true, snapshots, n_snap);
+}
+
+int bp_set_kernel_timing(bp_problem* p, int32_t enable) {
+    if (int rc = check_problem(p)) return rc;
+    p->timing = enable != 0;
+    return BP_OK;
+}
+
+int bp_last_run_stats(const bp_problem* p, int64_t* kernel_launches, int64_t* active_sweeps,
+                      double* row_kernel_ms, double* col_kernel_ms, int64_t* timed_sweeps) {
+    if (int rc = check_problem(p)) return rc;
+    if (kernel_launches) *kernel_launches = p->stat_launches;
+    if (active_sweeps) *active_sweeps = p->stat_sweeps;
+    if (row_kernel_ms) *row_kernel_ms = p->stat_row_ms;
+    if (col_kernel_ms) *col_kernel_ms = p->stat_col_ms;
+    if (timed_sweeps) *timed_sweeps = p->stat_timed;
+    return BP_OK;
+}
+
+}  // extern "C"

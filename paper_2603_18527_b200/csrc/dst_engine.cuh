@@ -1,0 +1,297 @@
+// dst_engine.cuh -- register/shared-memory DST-I engine for sm_100a (fp64 complex).
+//
+// One "engine" transforms one line of n = 2^LOG2N complex samples x_0..x_{n-1}
+// (x_0 == 0 is the Dirichlet padding slot; the DST-I length is n-1) into
+//     Y_k = sum_{j=1}^{n-1} x_j sin(pi j k / n),     k = 0..n-1 (Y_0 = 0),
+// i.e. the reference's forward DST-I convention (plain sine sum; FFTW RODFT00 / 2,
+// proj/include/bp/transforms.hpp:15-24).  Applying it twice gives (n/2) x.
+//
+// Algorithm (one length-n complex FFT per complex line, not the 2(n+1) odd extension):
+//   y_j = sin(pi j/n)(x_j + x_{n-j}) + (x_j - x_{n-j})/2          (pre-processing)
+//   W   = DFT_n(y)                                                (Stockham passes)
+//   Y_2k   = (i/2)(W_k - W_{n-k})                                 (post-processing)
+//   Y_2k+1 = W_0/2 + sum_{m=1}^{k} (W_m + W_{n-m})/2              (prefix sum)
+// The real and imaginary parts of x are two real DST-I problems; packing them as one
+// complex y makes W_k and W_{n-k} separate them with no extra work.  The last radix-2
+// Stockham pass is fused into the post-processing.
+//
+// Thread layout: T = n/P threads per engine, P points per thread.
+//   input   thread t holds x_{t + T m} and the mirror x_{n - t - T m}, m < P
+//           (stride-T: consecutive threads read consecutive addresses -> coalesced)
+//   output  thread t holds Y_{t P + l}, l < P (contiguous block)
+// Passes exchange data through one padded shared-memory line per engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bs {
+
+// ------------------------------------------------------------------ complex helpers
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double cnorm(double2 a) { return a.x * a.x + a.y * a.y; }
+// multiply by -i / +i
+__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }
+__device__ __forceinline__ double2 mul_pi(double2 a) { return make_double2(-a.y, a.x); }
+
+// a * exp(-2 pi i K / R), R <= 16, compile-time K
+template <int K, int R>
+__device__ __forceinline__ double2 mul_w(double2 a) {
+    constexpr int k16 = (K * 16 / R) % 16;  // angle in units of 2pi/16
+    constexpr double C1 = 0.92387953251128673848;  // cos(pi/8)
+    constexpr double S1 = 0.38268343236508978178;  // sin(pi/8)
+    constexpr double R2 = 0.70710678118654752440;  // 1/sqrt(2)
+    if constexpr (k16 == 0) return a;
+    else if constexpr (k16 == 4) return mul_mi(a);
+    else if constexpr (k16 == 8) return make_double2(-a.x, -a.y);
+    else if constexpr (k16 == 12) return mul_pi(a);
+    else if constexpr (k16 == 2) return make_double2((a.x + a.y) * R2, (a.y - a.x) * R2);
+    else if constexpr (k16 == 6) return make_double2((a.y - a.x) * R2, -(a.x + a.y) * R2);
+    else {
+        // exp(-i pi k16/8) = c - i s
+        constexpr double c = k16 == 1 ? C1 : k16 == 3 ? S1 : k16 == 5 ? -S1 : k16 == 7 ? -C1
+                           : k16 == 9 ? -C1 : k16 == 11 ? -S1 : k16 == 13 ? S1 : C1;
+        constexpr double s = k16 == 1 ? S1 : k16 == 3 ? C1 : k16 == 5 ? C1 : k16 == 7 ? S1
+                           : k16 == 9 ? -S1 : k16 == 11 ? -C1 : k16 == 13 ? -C1 : -S1;
+        return make_double2(a.x * c + a.y * s, a.y * c - a.x * s);
+    }
+}
+
+// In-register forward DFT of size R (natural order in and out), radix-2 DIT recursion.
+template <int R>
+struct Dft {
+    template <int STRIDE = 1>
+    __device__ __forceinline__ static void run(double2* v) {
+        double2 e[R / 2], o[R / 2];
+#pragma unroll
+        for (int k = 0; k < R / 2; ++k) {
+            e[k] = v[(2 * k) * STRIDE];
+            o[k] = v[(2 * k + 1) * STRIDE];
+        }
+        Dft<R / 2>::template run<1>(e);
+        Dft<R / 2>::template run<1>(o);
+        combine<0, STRIDE>(e, o, v);
+    }
+    template <int K, int STRIDE = 1>
+    __device__ __forceinline__ static void combine(const double2* e, const double2* o, double2* v) {
+        if constexpr (K < R / 2) {
+            const double2 t = mul_w<K, R>(o[K]);
+            v[K * STRIDE] = cadd(e[K], t);
+            v[(K + R / 2) * STRIDE] = csub(e[K], t);
+            combine<K + 1, STRIDE>(e, o, v);
+        }
+    }
+};
+template <>
+struct Dft<1> {
+    template <int STRIDE = 1>
+    __device__ __forceinline__ static void run(double2*) {}
+};
+template <>
+struct Dft<2> {
+    template <int STRIDE = 1>
+    __device__ __forceinline__ static void run(double2* v) {
+        const double2 a = v[0], b = v[STRIDE];
+        v[0] = cadd(a, b);
+        v[STRIDE] = csub(a, b);
+    }
+};
+
+// ------------------------------------------------------------------ engine geometry
+template <int LOG2N>
+struct Geom {
+    static constexpr int N = 1 << LOG2N;
+    static constexpr int P = (N / 2) < 16 ? (N / 2) : 16;  // points per thread
+    static constexpr int T = N / P;                        // threads per engine
+    static constexpr int H = N / 2;
+    static constexpr int PAD_N = N + N / 16 + 1;           // padded smem line (double2)
+    __host__ __device__ static constexpr int pidx(int i) { return i + (i >> 4); }
+};
+
+// Stockham pass list: product of radices == N/2; first radix == P.
+template <int LOG2N>
+struct Passes {
+    using G = Geom<LOG2N>;
+    // remaining product after the first pass
+    static constexpr int REM = G::H / G::P;
+    static constexpr int R2 = REM >= 16 ? 16 : REM;          // second pass radix (1 = none)
+    static constexpr int REM2 = REM / (R2 > 0 ? R2 : 1);
+    static constexpr int R3 = REM2 >= 16 ? 16 : REM2;        // third pass radix
+    static constexpr int REM3 = REM2 / (R3 > 0 ? R3 : 1);
+    static constexpr int R4 = REM3;                          // fourth (<= 16 for N <= 4096*16)
+    static_assert(R4 <= 16, "engine supports n <= 65536");
+};
+
+// ------------------------------------------------------------------ sync/scan policies
+// Engine threads are T contiguous lanes of one warp (T <= 32).
+template <int T>
+struct WarpSeg {
+    __device__ __forceinline__ void sync() const { __syncwarp(); }
+    // exclusive prefix over the T lanes of this engine (lane segment aligned to T)
+    __device__ __forceinline__ double2 exclusive_scan(double2 v, int t) const {
+        double2 incl = v;
+#pragma unroll
+        for (int d = 1; d < T; d <<= 1) {
+            const double ux = __shfl_up_sync(0xffffffffu, incl.x, d, T);
+            const double uy = __shfl_up_sync(0xffffffffu, incl.y, d, T);
+            if (t >= d) {
+                incl.x += ux;
+                incl.y += uy;
+            }
+        }
+        return csub(incl, v);
+    }
+    // deterministic sum over the T lanes of the engine (result valid in every lane)
+    __device__ __forceinline__ double sum(double v) const {
+#pragma unroll
+        for (int d = T / 2; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d, T);
+        return v;
+    }
+};
+
+// Engines spread over the CTA (column kernel): E engines x T threads; scan scratch in smem.
+template <int T, int E>
+struct BlockSeg {
+    double2* scratch;  // E*T double2
+    int e;
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ double2 exclusive_scan(double2 v, int t) const {
+        scratch[e * T + t] = v;
+        __syncthreads();
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int nwarps = (blockDim.x + 31) >> 5;
+        constexpr int CH = (T + 31) / 32;  // 32-wide chunks per engine
+        for (int ee = warp; ee < E; ee += nwarps) {
+            double2 carry = make_double2(0.0, 0.0);
+            for (int c = 0; c < CH; ++c) {
+                const int tt = c * 32 + lane;
+                double2 x = tt < T ? scratch[ee * T + tt] : make_double2(0.0, 0.0);
+                double2 incl = x;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const double ux = __shfl_up_sync(0xffffffffu, incl.x, d);
+                    const double uy = __shfl_up_sync(0xffffffffu, incl.y, d);
+                    if (lane >= d) {
+                        incl.x += ux;
+                        incl.y += uy;
+                    }
+                }
+                if (tt < T) scratch[ee * T + tt] = cadd(carry, csub(incl, x));
+                const double tx = __shfl_sync(0xffffffffu, incl.x, 31);
+                const double ty = __shfl_sync(0xffffffffu, incl.y, 31);
+                carry = cadd(carry, make_double2(tx, ty));
+            }
+        }
+        __syncthreads();
+        return scratch[e * T + t];
+    }
+};
+
+// ------------------------------------------------------------------ the engine
+template <int LOG2N>
+struct DstEngine {
+    using G = Geom<LOG2N>;
+    using PS = Passes<LOG2N>;
+    static constexpr int N = G::N, P = G::P, T = G::T, H = G::H;
+
+    // One Stockham pass of radix R over the line in `buf` (read all, sync, write all, sync).
+    // Ns = product of previous radices.  Twiddles from tw[k] = exp(-2 pi i k / N).
+    template <int R, int NS, class Pol>
+    __device__ __forceinline__ static void pass(double2* buf, int t, const double2* __restrict__ tw,
+                                                const Pol& pol) {
+        if constexpr (R > 1) {
+            constexpr int V = P / R;  // butterflies per thread
+            constexpr int STRIDE_IN = N / R;
+            double2 v[P];
+#pragma unroll
+            for (int b = 0; b < V; ++b) {
+                const int jj = t + T * b;
+                const int jm = jj % NS;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    double2 x = buf[G::pidx(jj + r * STRIDE_IN)];
+                    if (NS > 1 && r > 0) x = cmul(x, __ldg(&tw[(jm * r) * (N / (NS * R))]));
+                    v[b * R + r] = x;
+                }
+                Dft<R>::template run<1>(&v[b * R]);
+            }
+            pol.sync();
+#pragma unroll
+            for (int b = 0; b < V; ++b) {
+                const int jj = t + T * b;
+                const int base = (jj / NS) * NS * R + (jj % NS);
+#pragma unroll
+                for (int r = 0; r < R; ++r) buf[G::pidx(base + r * NS)] = v[b * R + r];
+            }
+            pol.sync();
+        }
+    }
+
+    // x[m] = x_{t+Tm}, xm[m] = x_{N-t-Tm} (mirror; must be 0 where the index is N).
+    // On return y[l] = Y_{tP+l}.  buf: this engine's padded smem line (G::PAD_N double2).
+    template <class Pol>
+    __device__ __forceinline__ static void run(const double2 (&x)[P], const double2 (&xm)[P], double2 (&y)[P],
+                                               int t, double2* buf, const double2* __restrict__ tw,
+                                               const double* __restrict__ sinp, const Pol& pol) {
+        // --- pre-processing + first Stockham pass (radix P, Ns = 1, data already in registers)
+        double2 v[P];
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            const int j = t + T * m;
+            const double s = __ldg(&sinp[j]);
+            const double2 a = cadd(x[m], xm[m]);
+            const double2 d = csub(x[m], xm[m]);
+            v[m] = (j == 0) ? make_double2(0.0, 0.0)
+                            : make_double2(fma(s, a.x, 0.5 * d.x), fma(s, a.y, 0.5 * d.y));
+        }
+        Dft<P>::template run<1>(v);
+#pragma unroll
+        for (int r = 0; r < P; ++r) buf[G::pidx(t * P + r)] = v[r];
+        pol.sync();
+        // --- remaining passes up to length N/2 (radix-2 last pass fused below)
+        pass<PS::R2, P>(buf, t, tw, pol);
+        pass<PS::R3, P * PS::R2>(buf, t, tw, pol);
+        pass<PS::R4, P * PS::R2 * PS::R3>(buf, t, tw, pol);
+        // --- fused final radix-2 pass + DST-I post-processing + prefix sum
+        constexpr int K = P / 2;  // k values per thread: k = t*K + i
+        double2 ev[K], od[K];     // Y_2k and S_k
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const int k = t * K + i;
+            const double2 w = __ldg(&tw[k]);  // exp(-2 pi i k/N)
+            const double2 a = buf[G::pidx(k)];
+            const double2 b = cmul(buf[G::pidx(k + H)], w);
+            const double2 Wk = cadd(a, b);
+            if (k == 0) {
+                ev[i] = make_double2(0.0, 0.0);
+                od[i] = cscale(Wk, 0.5);
+            } else {
+                // W_{N-k} = a_{H-k} - w^{H-k} b_{H-k},  w^{H-k} = -conj(w^k)
+                const double2 a2 = buf[G::pidx(H - k)];
+                const double2 b2 = buf[G::pidx(N - k)];
+                const double2 Wnk = cadd(a2, cmul(b2, cconj(w)));
+                const double2 dif = csub(Wk, Wnk);
+                ev[i] = make_double2(-0.5 * dif.y, 0.5 * dif.x);  // (i/2)(Wk - Wnk)
+                od[i] = cscale(cadd(Wk, Wnk), 0.5);
+            }
+        }
+        // local inclusive prefix of S
+#pragma unroll
+        for (int i = 1; i < K; ++i) od[i] = cadd(od[i], od[i - 1]);
+        const double2 off = pol.exclusive_scan(od[K - 1], t);
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            y[2 * i] = ev[i];
+            y[2 * i + 1] = cadd(od[i], off);
+        }
+        pol.sync();  // buffer free for reuse
+    }
+};
+
+}  // namespace bs

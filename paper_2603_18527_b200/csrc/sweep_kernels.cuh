@@ -1,0 +1,351 @@
+// sweep_kernels.cuh -- fused Born-sweep kernels for sm_100a (fp64 complex).
+//
+// HBM layout (per member b of the batch, "padded" n x n with n = nx+1 = 2^LOG2N):
+//   element (ix, iy) of the reference's dense nx*ny field lives at [(ix+1)*n + (iy+1)];
+//   row 0 and column 0 are the Dirichlet zero nodes.  Every field buffer has one extra
+//   zero row at its end so the five-point stencil of the last member reads zeros.
+//   Rows are 16*n bytes (128-B aligned); the DST-I engine's x_0 slot is column 0.
+//
+// Per sweep (two launches, 128 algorithmic bytes per grid point):
+//   row kernel   (96 B/pt)  T -> inverse y-DST -> G q^m;  r_bs = G q^m - u^m;
+//                           ||r_bs||^2 (= ||G r^m||^2, the R_eta norm, by the key identity
+//                           PAPER.md:149-156); ||f - A u^m||^2 (five-point stencil);
+//                           u^{m+1} = u^m + gamma r_bs;  q^{m+1} = V u^{m+1} + f;
+//                           forward y-DST -> T;  last row of a member finalises the
+//                           trace entry m and the termination test of proj/src/iterate.cpp:134-150.
+//   column kernel (32 B/pt) T -> forward x-DST -> x 4/(n^2 lambda) -> inverse x-DST -> T.
+#pragma once
+
+#include "dst_engine.cuh"
+
+namespace bs {
+
+enum RowMode { R_FWD = 0, R_FWD_BORN = 1, R_INV = 2, R_SWEEP = 3 };
+enum ColMode { C_ONE = 0, C_GREEN = 1, C_LREF = 2 };
+enum Status { ST_ACTIVE = 0, ST_DONE = 1 };
+enum MapKind { MK_SCALAR = 0, MK_POINTWISE = 3 };
+
+struct Control {
+    int* status;          // [batch]
+    int* sweep;           // [batch] next trace entry to record
+    unsigned* counter;    // [batch] rows finished in the current launch
+    int* iters;           // [batch]
+    int* term;            // [batch]
+    int* result_buf;      // [batch] ping-pong index holding the result
+    int* n_active;        // [1]
+    double2* partial;     // [batch][n] per-row (||r||^2, ||r_bs||^2)
+    const double* fnorm_l2;
+    const double* fnorm_reta;
+    double* trace_l2;     // [batch][max_iters+1]
+    double* trace_reta;
+    int max_iters;
+    double rtol;
+};
+
+struct RowArgs {
+    int batch;
+    double inv_h2;             // 1/h^2
+    const double* k0sq;        // [batch]
+    const double* eta;         // [batch]
+    const double2* k2;         // padded
+    const double2* f;          // padded (R_FWD_BORN, R_SWEEP)
+    const double2* in;         // R_FWD: field to transform; R_FWD_BORN: u
+    double2* out;              // R_INV output (padded)
+    const double2* sub;        // R_INV: optional field subtracted from the output
+    double2* T;                // intermediate (padded)
+    double2* u0;               // R_SWEEP ping
+    double2* u1;               // R_SWEEP pong
+    const double2* tw;         // exp(-2 pi i k/n), k < n
+    const double* sinp;        // sin(pi j/n), j < n
+    int map_kind;
+    double2 gamma;
+    Control ctl;
+};
+
+struct ColArgs {
+    int batch;
+    const double* k0sq;
+    const double* eta;
+    const double* lap;         // (4/h^2) sin^2(j pi / (2n)), j < n
+    double scale;              // C_ONE scale / Green normalisation 4/n^2
+    double2* T;
+    const double2* tw;
+    const double* sinp;
+    const int* status;         // nullable: skip inactive members
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
+
+template <int T>
+__device__ __forceinline__ double seg_sum(double v) {
+#pragma unroll
+    for (int d = T / 2; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d, T);
+    return v;
+}
+
+// Trace entry m for member b + termination test, restating proj/src/iterate.cpp:105-150.
+__device__ void finalize_entry(const Control& c, int b, int m, double sum_l2, double sum_reta) {
+    const int stride = c.max_iters + 1;
+    const double rel = sqrt(sum_l2) / c.fnorm_l2[b];
+    const double rel_reta = sqrt(sum_reta) / c.fnorm_reta[b];
+    c.trace_l2[(size_t)b * stride + m] = rel;
+    c.trace_reta[(size_t)b * stride + m] = rel_reta;
+    int term = -1;
+    if (m == 0) {
+        if (rel <= c.rtol) term = 0;  // converged before any update (iterate.cpp:112-115)
+    } else {
+        if (!isfinite(rel) || rel > 1e8) term = 2;  // diverged
+        else if (rel <= c.rtol) term = 0;           // converged
+        else if (m + 1 > 20) {                      // stagnated over a 20-step window
+            const double past = c.trace_l2[(size_t)b * stride + (m - 20)];
+            if (fabs(past - rel) < 1e-14 * fmax(1.0, past)) term = 3;
+        }
+    }
+    if (term < 0 && m >= c.max_iters) term = 1;  // max_iters
+    if (term >= 0) {
+        c.iters[b] = m;
+        c.term[b] = term;
+        c.result_buf[b] = m & 1;
+        c.status[b] = ST_DONE;
+        atomicSub(c.n_active, 1);
+    }
+    c.sweep[b] = m + 1;
+    c.counter[b] = 0u;
+}
+
+// ------------------------------------------------------------------ row kernel (T <= 32)
+// NW warps per CTA; 32/T engines (rows) per warp; one global row per engine.
+template <int LOG2N, int MODE, int NW>
+__global__ void __launch_bounds__(NW * 32, (NW >= 8 ? 2 : 4))
+row_kernel(const RowArgs a) {
+    using G = Geom<LOG2N>;
+    constexpr int N = G::N, P = G::P, T = G::T;
+    static_assert(T <= 32, "row kernel handles n <= 512");
+    constexpr int EPW = 32 / T;
+    constexpr int EPB = NW * EPW;
+    extern __shared__ double2 smem[];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = lane % T;
+    const int e = warp * EPW + lane / T;
+    const long grow = (long)blockIdx.x * EPB + e;
+    const int b = (int)(grow >> LOG2N);
+    const int i = (int)(grow & (N - 1));
+    bool valid = (b < a.batch) && (i != 0);
+    int m = 0;
+    if (MODE == R_SWEEP && valid) {
+        valid = __ldcg(&a.ctl.status[b]) == ST_ACTIVE;
+        m = __ldcg(&a.ctl.sweep[b]);
+    }
+    if (!__syncthreads_or(valid)) return;
+
+    double2* buf = smem + e * G::PAD_N;
+    const WarpSeg<T> pol{};
+    const size_t mem = (size_t)(valid ? b : 0) * N * N;
+    const size_t row = mem + (size_t)(valid ? i : 0) * N;
+    const double2 zero = make_double2(0.0, 0.0);
+
+    double2 q[P];
+    double acc_l2 = 0.0, acc_reta = 0.0;
+
+    if constexpr (MODE == R_INV || MODE == R_SWEEP) {
+        // ---- inverse y-DST of the column-pass output
+        double2 x[P], xm[P], y[P];
+#pragma unroll
+        for (int mm = 0; mm < P; ++mm) {
+            const int j = t + T * mm;
+            x[mm] = valid ? a.T[row + j] : zero;
+            xm[mm] = (valid && j != 0) ? a.T[row + (N - j)] : zero;
+        }
+        DstEngine<LOG2N>::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+        // stage through smem: contiguous -> stride layout (coalesced global access)
+#pragma unroll
+        for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
+        pol.sync();
+        double2 z[P];
+#pragma unroll
+        for (int mm = 0; mm < P; ++mm) z[mm] = buf[G::pidx(t + T * mm)];
+        pol.sync();
+
+        if constexpr (MODE == R_INV) {
+#pragma unroll
+            for (int mm = 0; mm < P; ++mm) {
+                const int j = t + T * mm;
+                double2 o = z[mm];
+                if (a.sub) o = csub(o, valid ? a.sub[row + j] : zero);
+                if (valid) a.out[row + j] = (j == 0) ? zero : o;
+            }
+            return;
+        } else {
+            // ---- fused Born update, residual norms, next source term
+            const double2* ucur = (m & 1) ? a.u1 : a.u0;
+            double2* unext = (m & 1) ? a.u0 : a.u1;
+            const double k0sq = valid ? a.k0sq[b] : 0.0;
+            const double eta = valid ? a.eta[b] : 1.0;
+            const double2 shift = make_double2(k0sq, eta);
+            const double inv_h2 = a.inv_h2;
+#pragma unroll
+            for (int mm = 0; mm < P; ++mm) {
+                const int j = t + T * mm;
+                double2 u = zero, k2 = zero, f = zero, un = zero, us = zero, uw = zero, ue = zero;
+                if (valid) {
+                    u = ucur[row + j];
+                    k2 = a.k2[row + j];
+                    f = a.f[row + j];
+                    un = ucur[row - N + j];
+                    us = ucur[row + N + j];
+                    if (j > 0) uw = ucur[row + j - 1];
+                    if (j + 1 < N) ue = ucur[row + j + 1];
+                }
+                const double2 V = csub(k2, shift);
+                const double2 rb = csub(z[mm], u);
+                // five-point (proj/src/kernels.cpp:56-69 order) and A u = L_D u - k2 u
+                double2 s = cscale(u, 4.0);
+                s = csub(s, un);
+                s = csub(s, us);
+                s = csub(s, uw);
+                s = csub(s, ue);
+                const double2 au = csub(cscale(s, inv_h2), cmul(k2, u));
+                const double2 r = csub(f, au);
+                if (j != 0) {
+                    acc_reta += cnorm(rb);
+                    acc_l2 += cnorm(r);
+                }
+                double2 g = a.gamma;
+                if (a.map_kind == MK_POINTWISE) g = cscale(mul_pi(V), 1.0 / eta);  // (i/eta) V
+                double2 unew = cadd(u, cmul(g, rb));
+                if (j == 0) unew = zero;
+                if (valid) unext[row + j] = unew;
+                q[mm] = cadd(cmul(V, unew), f);
+            }
+        }
+    } else {
+        // ---- R_FWD / R_FWD_BORN: source of the forward transform
+        const double k0sq = valid ? a.k0sq[b] : 0.0;
+        const double eta = valid ? a.eta[b] : 1.0;
+        const double2 shift = make_double2(k0sq, eta);
+#pragma unroll
+        for (int mm = 0; mm < P; ++mm) {
+            const int j = t + T * mm;
+            double2 v = valid ? a.in[row + j] : zero;
+            if constexpr (MODE == R_FWD_BORN) {
+                const double2 V = csub(valid ? a.k2[row + j] : zero, shift);
+                v = cadd(cmul(v, V), valid ? a.f[row + j] : zero);  // kernels::mul(u, v) then add f
+            }
+            q[mm] = (j == 0) ? zero : v;
+        }
+    }
+
+    // ---- forward y-DST of q: mirror exchange through smem
+    double2 qm[P], y2[P];
+#pragma unroll
+    for (int mm = 0; mm < P; ++mm) buf[G::pidx(t + T * mm)] = q[mm];
+    pol.sync();
+#pragma unroll
+    for (int mm = 0; mm < P; ++mm) {
+        const int j = t + T * mm;
+        qm[mm] = (j == 0) ? zero : buf[G::pidx(N - j)];
+    }
+    pol.sync();
+    DstEngine<LOG2N>::run(q, qm, y2, t, buf, a.tw, a.sinp, pol);
+#pragma unroll
+    for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y2[l];
+    pol.sync();
+#pragma unroll
+    for (int mm = 0; mm < P; ++mm) {
+        const int j = t + T * mm;
+        if (valid) a.T[row + j] = buf[G::pidx(j)];
+    }
+
+    if constexpr (MODE == R_SWEEP) {
+        acc_l2 = seg_sum<T>(acc_l2);
+        acc_reta = seg_sum<T>(acc_reta);
+        int last = 0;
+        if (valid && t == 0) {
+            a.ctl.partial[(size_t)b * N + i] = make_double2(acc_l2, acc_reta);
+            __threadfence();
+            const unsigned old = atomicAdd(&a.ctl.counter[b], 1u);
+            last = (old == (unsigned)(N - 2));
+        }
+        last = __shfl_sync(0xffffffffu, last, (lane / T) * T);
+        if (last) {
+            __threadfence();
+            double s1 = 0.0, s2 = 0.0;
+            for (int r = 1 + t; r < N; r += T) {
+                const double2 pr = ldcg2(&a.ctl.partial[(size_t)b * N + r]);
+                s1 += pr.x;
+                s2 += pr.y;
+            }
+            s1 = seg_sum<T>(s1);
+            s2 = seg_sum<T>(s2);
+            if (t == 0) finalize_entry(a.ctl, b, m, s1, s2);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ column kernel
+// C columns per CTA, T threads per column (thread = c + C*t): row segments of C*16 bytes.
+template <int LOG2N, int MODE, int C>
+__global__ void __launch_bounds__(C * Geom<LOG2N>::T, (C * Geom<LOG2N>::T >= 256 ? 2 : 4))
+col_kernel(const ColArgs a) {
+    using G = Geom<LOG2N>;
+    constexpr int N = G::N, P = G::P, T = G::T;
+    extern __shared__ double2 smem[];
+    const int c = threadIdx.x % C, t = threadIdx.x / C;
+    constexpr int GROUPS = N / C;
+    const int b = blockIdx.x / GROUPS;
+    const int q = (blockIdx.x % GROUPS) * C + c;
+    if (a.status && __ldcg(&a.status[b]) != ST_ACTIVE) return;  // uniform per CTA
+
+    double2* buf = smem + c * G::PAD_N;
+    const BlockSeg<T, C> pol{smem + C * G::PAD_N, c};
+    const size_t mem = (size_t)b * N * N;
+    const double2 zero = make_double2(0.0, 0.0);
+
+    double2 x[P], xm[P], y[P];
+#pragma unroll
+    for (int mm = 0; mm < P; ++mm) {
+        const int j = t + T * mm;
+        x[mm] = a.T[mem + (size_t)j * N + q];
+        xm[mm] = (j == 0) ? zero : a.T[mem + (size_t)(N - j) * N + q];
+    }
+    DstEngine<LOG2N>::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+
+    if constexpr (MODE == C_ONE) {
+#pragma unroll
+        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * N + q] = cscale(y[l], a.scale);
+    } else {
+        const double k0sq = a.k0sq[b], eta = a.eta[b];
+        const double lq = a.lap[q];
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+            const int p = t * P + l;
+            // lambda = (a_p + a_q) - (k0^2 + i eta)   (symbol.cpp:69-80 + shift_symbol :97-100)
+            const double lr = (a.lap[p] + lq) - k0sq;
+            const double li = -eta;
+            double2 w;
+            if constexpr (MODE == C_GREEN) {
+                const double s = a.scale / (lr * lr + li * li);
+                w = make_double2(lr * s, -li * s);  // scale / lambda
+            } else {
+                w = make_double2(lr * a.scale, li * a.scale);  // scale * lambda
+            }
+            const double2 v = (p == 0 || q == 0) ? zero : cmul(y[l], w);
+            buf[G::pidx(p)] = v;
+        }
+        pol.sync();
+#pragma unroll
+        for (int mm = 0; mm < P; ++mm) {
+            const int j = t + T * mm;
+            x[mm] = buf[G::pidx(j)];
+            xm[mm] = (j == 0) ? zero : buf[G::pidx(N - j)];
+        }
+        pol.sync();
+        DstEngine<LOG2N>::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+#pragma unroll
+        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * N + q] = y[l];
+    }
+}
+
+}  // namespace bs

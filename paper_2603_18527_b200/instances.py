@@ -1,0 +1,72 @@
+"""Seeded synthetic instances of BASELINE.json's configs (host-side input synthesis).
+
+Wraps ``libbornsweep_host.so`` (include/bornsweep_instances.h).  Every arm -- the CUDA path,
+the plain-C oracle and the reference build -- consumes the arrays returned here.
+
+Decisions: an "n x n grid, h = 1/n" config is the reference's
+DirichletInterior grid with N = n-1 interior points per side (proj/include/bp/grid.hpp:12-24),
+so the DST-I length n-1 maps onto a power-of-two transform of length n.  The reference's
+default sponge (N/8 points, strength 1; proj/src/helmholtz.cpp:67-72) is folded into k2,
+because the lossless cavity the configs literally describe does not converge.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _native as N
+
+
+@dataclass(frozen=True)
+class InstanceSpec:
+    n: int
+    ppw: float
+    contrast: float
+    sigma_cells: float = 4.0
+    src_sigma_cells: float = 2.0
+    n_sources: int = 0
+    seed: int = 0
+    sponge_points: int = -1
+    sponge_strength: float = 1.0
+    eta_factor: float = 1.01
+
+    def _c(self):
+        return N.InstanceSpec(self.n, self.ppw, self.contrast, self.sigma_cells,
+                              self.src_sigma_cells, self.n_sources, self.seed, self.sponge_points,
+                              self.sponge_strength, self.eta_factor)
+
+
+# BASELINE.json configs (synthetic stand-ins)
+CONFIGS = {
+    # c0: 2D CBS, 128x128 (h = 1/128), contrast 0.3, 10 ppw, single RHS, gamma = 1
+    "c0": dict(spec=InstanceSpec(n=128, ppw=10.0, contrast=0.3), batch=1, map="scalar",
+               rtol=1e-6),
+    # c1: 64 independent media on 512x512, contrast 0.5, 8 ppw, pointwise gamma(x) = iV/eta
+    "c1": dict(spec=InstanceSpec(n=512, ppw=8.0, contrast=0.5), batch=64, map="pointwise",
+               rtol=1e-6),
+}
+
+
+def make_instances(spec: InstanceSpec, first: int = 0, count: int = 1, nthreads: int = 0):
+    """(k2, f, k0, eta) for members first..first+count-1: complex (count, N, N) arrays."""
+    nd = spec.n - 1
+    k2 = np.empty((count, nd, nd), np.complex128)
+    f = np.empty((count, nd, nd), np.complex128)
+    k0 = np.empty(count)
+    eta = np.empty(count)
+    dp = C.POINTER(C.c_double)
+    s = spec._c()
+    rc = N.host_lib().bp_make_instances(C.byref(s), first, count, k2.ctypes.data_as(dp),
+                                        f.ctypes.data_as(dp), k0.ctypes.data_as(dp),
+                                        eta.ctypes.data_as(dp), nthreads)
+    if rc:
+        raise ValueError(f"invalid instance spec {spec}")
+    return k2, f, k0, eta
+
+
+def config_instances(name: str, first: int = 0, count: int | None = None, **overrides):
+    cfg = CONFIGS[name]
+    spec = replace(cfg["spec"], **overrides) if overrides else cfg["spec"]
+    return make_instances(spec, first, cfg["batch"] if count is None else count)

@@ -1,0 +1,99 @@
+"""Generate the committed golden fixtures (run HERE, where /root/reference and scipy exist).
+
+    python tests/golden/make_golden.py
+
+* dst_scipy.npz      -- 2-D DST-I vectors from scipy.fft.dstn(type=1) (== FFTW RODFT00), scaled
+                        to the reference's forward convention (x0.25, proj/src/transforms.cpp:117)
+* ref_rng.npz        -- RngState normals / uniforms from the reference's own rng.hpp
+* ref_samplers.npz   -- sponge_profile / gaussian_bump from the reference's samplers.cpp
+* ref_ops_n{16,32}.npz, ref_run_*.npz
+                     -- operator outputs and run() trajectories produced by the reference's own
+                        L1-L3 code (oracle/_ref) on instances from libbornsweep_host.so
+The GPU box never reads /root/reference: tests consume only these files.
+"""
+import os
+import sys
+
+import numpy as np
+import scipy.fft as sf
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import MAP_OPTIMAL_SCALAR, MAP_POINTWISE, MAP_SCALAR, Reference, ReferenceProblem  # noqa: E402
+import paper_2603_18527_b200 as bs  # noqa: E402
+
+
+def dst_golden():
+    rng = np.random.default_rng(20261020)
+    out = {}
+    for nx, ny in [(16, 12), (15, 15), (7, 7), (31, 31), (3, 5)]:
+        x = rng.standard_normal((nx, ny)) + 1j * rng.standard_normal((nx, ny))
+        y = (sf.dstn(x.real, type=1) + 1j * sf.dstn(x.imag, type=1)) * 0.25
+        out[f"x_{nx}x{ny}"] = x
+        out[f"y_{nx}x{ny}"] = y
+    np.savez_compressed(os.path.join(HERE, "dst_scipy.npz"), **out)
+
+
+def rng_golden():
+    out = {}
+    for seed, idx in [(0, -1), (0, 0), (0, 7), (12345, 3), (2**63 + 5, 63)]:
+        out[f"normal_{seed}_{idx}"] = Reference.rng_normals(seed, idx, 257)
+        out[f"uniform_{seed}_{idx}"] = Reference.rng_uniforms(seed, idx, 64)
+    np.savez_compressed(os.path.join(HERE, "ref_rng.npz"), **out)
+
+
+def sampler_golden():
+    out = {}
+    for nx, layer in [(15, 1), (31, 3), (127, 15), (12, 0)]:
+        out[f"sponge_{nx}_{layer}"] = Reference.sponge_profile(nx, nx, layer, 1.0)
+    for nx, cx, cy, w in [(15, 0.5, 0.5, 2 / 16), (31, 0.3, 0.7, 0.05), (127, 0.5, 0.5, 2 / 128)]:
+        out[f"bump_{nx}_{cx}_{cy}_{w}"] = Reference.gaussian_bump(nx, nx, cx, cy, w)
+    np.savez_compressed(os.path.join(HERE, "ref_samplers.npz"), **out)
+
+
+def ops_golden():
+    rng = np.random.default_rng(7)
+    for n in (16, 32):
+        spec = bs.InstanceSpec(n=n, ppw=8.0, contrast=0.4, sigma_cells=2.0)
+        k2, f, k0, eta = bs.make_instances(spec, 0, 1)
+        p = ReferenceProblem(k2[0], k0[0], eta[0])
+        x = rng.standard_normal(k2[0].shape) + 1j * rng.standard_normal(k2[0].shape)
+        np.savez_compressed(
+            os.path.join(HERE, f"ref_ops_n{n}.npz"), k2=k2[0], f=f[0], k0=k0[0], eta=eta[0], x=x,
+            A=p.apply_A(x), V=p.apply_V(x), VH=p.apply_V_adjoint(x), Lref=p.apply_Lref(x),
+            G=p.apply_G(x), born=p.born_residual(x, f[0]), res=p.residual(x, f[0]),
+            fwd=p.forward_dst(x), inv=p.inverse_dst(x), symbol=p.symbol())
+
+
+def run_golden():
+    cases = {
+        # name: (n, ppw, contrast, map, gamma, metric, rtol, max_iters)
+        "c0like_n32_scalar": (32, 10.0, 0.3, MAP_SCALAR, 1.0, 0, 1e-6, 2000),
+        "n32_pointwise": (32, 8.0, 0.5, MAP_POINTWISE, 0.0, 0, 1e-6, 3000),
+        "n16_optl2": (16, 8.0, 0.4, MAP_OPTIMAL_SCALAR, 0.0, 0, 1e-8, 2000),
+        "n16_optreta": (16, 8.0, 0.4, MAP_OPTIMAL_SCALAR, 0.0, 1, 1e-8, 2000),
+        "n32_scalar_maxiters": (32, 10.0, 0.3, MAP_SCALAR, 0.8 + 0.1j, 0, 1e-6, 37),
+    }
+    for name, (n, ppw, contrast, mk, gamma, metric, rtol, mi) in cases.items():
+        spec = bs.InstanceSpec(n=n, ppw=ppw, contrast=contrast, sigma_cells=2.0, seed=11)
+        k2, f, k0, eta = bs.make_instances(spec, 0, 1)
+        p = ReferenceProblem(k2[0], k0[0], eta[0])
+        r = p.run(f[0], map_kind=mk, gamma=gamma, metric=metric, rtol=rtol, max_iters=mi)
+        np.savez_compressed(os.path.join(HERE, f"ref_run_{name}.npz"), k2=k2[0], f=f[0], k0=k0[0],
+                            eta=eta[0], map_kind=mk, gamma=gamma, metric=metric, rtol=rtol,
+                            max_iters=mi, u=r.u, res_l2=r.res_l2, res_reta=r.res_reta,
+                            iters=r.iters, terminated=r.terminated, fnorm_l2=r.fnorm_l2,
+                            fnorm_reta=r.fnorm_reta)
+        print(name, r.iters, r.terminated)
+
+
+if __name__ == "__main__":
+    Reference.set_mode("serial")
+    dst_golden()
+    rng_golden()
+    sampler_golden()
+    ops_golden()
+    run_golden()
+    print("golden fixtures written to", HERE)
