@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the Born-series sweep (BASELINE.json metric: Gpts/s, grid-point sweeps/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "c1"): 64 independent seeded media on the 511^2 interior
+grid of a 512-cell box (h = 1/512), contrast 0.5, 8 ppw, pointwise map gamma(x) = iV/eta,
+rtol 1e-6.  A STEP is one bp::run call over the whole batch limited to --sweeps sweeps
+(max_iters), i.e. --sweeps Born sweeps of every member plus the run's setup (||f||, ||G f||)
+and result gather.  Work counted = sweeps actually executed (sum of iters) x 511^2 points.
+
+* value   -- device-resident: f, u and the media live in HBM before the timed region;
+             K steps timed with CUDA events on the library stream, max over ranks.
+* e2e     -- the same steps through the public C ABI with PINNED HOST buffers: every step
+             uploads the media (bp_problem_set_medium) and the sources, runs, and reads u and
+             the traces back; H2D/D2H inside the timed region.
+* roofline -- the fused row kernel (96 algorithmic B/pt) timed per launch with
+             CUDA events on the launching stream inside the timed region, vs MEASURED_PEAKS.
+* cpu_baseline -- the reference's own code (oracle/_ref) on the host cores, bounded sample.
+
+N > 1 (torchrun): members are sharded across ranks (64/N each, no collective on the data
+path: "scaling": "strong", total work fixed); torch.distributed only for barrier + max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Born-series sweeps x grid points per sec (Gpts/s); achieved HBM GB/s vs peak"
+UNIT = "Gpts/s"
+ROW_BYTES_PER_PT = 96     # row kernel: T in, u in, k2 in, f in, u out, T out (16 B each)
+COL_BYTES_PER_PT = 32     # column kernel: T in, T out
+SWEEP_BYTES_PER_PT = 128
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(k2, f, k0, eta, sweeps, threads):
+    """The reference's own code (oracle/_ref: proj/src sources + FFTW shim + restated run) on
+    the host: OpenMP over members like proj/src/bench.cpp:143, each member iterated `sweeps`
+    times.  Returns (Gpts/s, seconds, kind, sample)."""
+    from oracle import MAP_POINTWISE, Reference, Oracle, OracleProblem
+    nd = k2.shape[1]
+    if Reference.available():
+        t0 = time.perf_counter()
+        _, _, _, info = Reference.run_batch(k2, k0, eta, f, map_kind=MAP_POINTWISE, rtol=1e-6,
+                                            max_iters=sweeps, nthreads=threads)
+        dt = time.perf_counter() - t0
+        done = sum(i for i, _ in info)
+        kind = "reference"
+    else:  # the plain-C port
+        Oracle.set_threads(threads)
+        t0 = time.perf_counter()
+        done = 0
+        for b in range(k2.shape[0]):
+            done += OracleProblem(k2[b], k0[b], eta[b]).run(f[b], map_kind=MAP_POINTWISE,
+                                                            max_iters=sweeps).iters
+        dt = time.perf_counter() - t0
+        kind = "port"
+    sample = (f"{k2.shape[0]} c1 members x {sweeps} sweeps of {nd}x{nd} (full bp::run incl. "
+              f"setup), OpenMP over members, {threads} threads; transforms through the project "
+              f"FFTW-API shim (FFTW absent)")
+    return done * nd * nd / dt / 1e9, dt, kind, sample
+
+
+def run_reference_arm(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    import paper_2603_18527_b200 as bs
+    cores = os.cpu_count() or 1
+    members = min(cores, 64)
+    k2, f, k0, eta = bs.config_instances("c1", 0, members)
+    sweeps = args.ref_sweeps
+    for _ in range(args.warmup):
+        cpu_baseline(k2, f, k0, eta, sweeps, cores)
+    vals, times = [], []
+    for _ in range(args.steps):
+        v, dt, kind, sample = cpu_baseline(k2, f, k0, eta, sweeps, cores)
+        vals.append(v)
+        times.append(dt)
+    value = float(np.sum([members * sweeps * 511 * 511 for _ in times]) / np.sum(times) / 1e9)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded RngState media, BASELINE.json c1 construction)",
+        "impl": "reference",
+        "config": {"workload": "c1", "grid": "511x511", "batch_sample": members,
+                   "sweeps_per_step": sweeps, "parallelism": "OpenMP over members"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def load_traffic():
+    """dram bytes per row-kernel launch from the committed ncu summary (profiles/), if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d["row_kernel"]["dram_bytes_per_launch"], os.path.relpath(path, ROOT)
+    except Exception:
+        return None, None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_18527_b200 as bs
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    total = args.batch
+    if total % world:
+        raise SystemExit(f"batch {total} not divisible by {world} ranks")
+    per = total // world
+    first = rank * per
+    k2, f, k0, eta = bs.config_instances("c1", first, per)
+    nd = k2.shape[1]
+    pts = nd * nd
+    cmap = bs.PointwiseMap()
+    cfg = bs.IterationConfig(rtol=1e-6, max_iters=args.sweeps)
+
+    prob = bs.HelmholtzDirichlet(k2, k0, eta, device=local_rank)
+    stream = torch.cuda.ExternalStream(prob.stream, device=local_rank)
+    f_dev = torch.from_numpy(f).to(f"cuda:{local_rank}")
+    u_dev = torch.empty_like(f_dev)
+    import ctypes as C
+    from paper_2603_18527_b200 import _native as N
+    lib = N.lib()
+    stride = cfg.max_iters + 1
+    l2 = np.empty((per, stride))
+    rt = np.empty((per, stride))
+    info = (N.Trace * per)()
+    mp, cc = cmap._c(), cfg._c()
+    dp = C.POINTER(C.c_double)
+
+    def step_device():
+        rc = lib.bp_run_device(prob.handle, C.byref(mp), C.c_void_p(f_dev.data_ptr()), C.byref(cc),
+                               None, C.c_void_p(u_dev.data_ptr()), l2.ctypes.data_as(dp),
+                               rt.ctypes.data_as(dp), info)
+        if rc:
+            raise RuntimeError(N.last_error())
+        return prob.last_run_stats()
+
+    prob.set_kernel_timing(True)
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    sweeps_done = 0
+    launches = 0
+    row_ms = col_ms = 0.0
+    timed = 0
+    with ClockSampler(local_rank) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            st = step_device()
+            sweeps_done += st["active_sweeps"]
+            launches += st["kernel_launches"]
+            row_ms += st["row_ms"]
+            col_ms += st["col_ms"]
+            timed += st["timed_sweeps"]
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    work = sum_over_ranks(float(sweeps_done * pts))
+    value = work / (elapsed_ms * 1e-3) / 1e9
+    # per-launch kernel durations (row / column kernels; each launch covers the rank's batch)
+    row_avg = row_ms / max(timed, 1)
+    col_avg = col_ms / max(timed, 1)
+    pts_per_launch = per * pts
+    peak, peak_src = measured_peak()
+    row_gbs = ROW_BYTES_PER_PT * pts_per_launch / (row_avg * 1e-3) / 1e9
+    col_gbs = COL_BYTES_PER_PT * pts_per_launch / (col_avg * 1e-3) / 1e9
+    sweep_gbs = SWEEP_BYTES_PER_PT * pts_per_launch / ((row_avg + col_avg) * 1e-3) / 1e9
+    traffic, traffic_src = load_traffic()
+
+    # ------------------------------------------------------------------ e2e through host buffers
+    pin_k2 = torch.empty(k2.shape, dtype=torch.complex128, pin_memory=True)
+    pin_f = torch.empty(f.shape, dtype=torch.complex128, pin_memory=True)
+    pin_u = torch.empty(f.shape, dtype=torch.complex128, pin_memory=True)
+    pin_k2.numpy()[...] = k2
+    pin_f.numpy()[...] = f
+    k2h, fh, uh = pin_k2.numpy(), pin_f.numpy(), pin_u.numpy()
+    prob.set_kernel_timing(False)
+
+    def step_e2e():
+        prob.set_medium(k2h, k0, eta)
+        rc = lib.bp_run(prob.handle, C.byref(mp), fh.ctypes.data_as(dp), C.byref(cc), None,
+                        uh.ctypes.data_as(dp), l2.ctypes.data_as(dp), rt.ctypes.data_as(dp), info)
+        if rc:
+            raise RuntimeError(N.last_error())
+        return prob.last_run_stats()
+
+    for _ in range(max(1, args.warmup)):
+        step_e2e()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_sweeps = 0
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_sweeps += step_e2e()["active_sweeps"]
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_value = sum_over_ranks(float(e2e_sweeps * pts)) / (e2e_ms * 1e-3) / 1e9
+    h2d = int(k2h.nbytes + fh.nbytes + k0.nbytes + eta.nbytes) * world
+    d2h = int(uh.nbytes + l2.nbytes + rt.nbytes + per * C.sizeof(N.Trace)) * world
+
+    # ------------------------------------------------------------------ CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        m = min(cores, per)
+        v, dt, kind, sample = cpu_baseline(k2[:m], f[:m], k0[:m], eta[:m], args.cpu_sweeps, cores)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+               "seconds": round(dt, 3)}
+
+    prob.close()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded RngState media + centre Gaussian-bump sources, BASELINE c1 construction)",
+            "config": {"workload": "c1: 64 x 511^2 Dirichlet Helmholtz CBS batch, contrast 0.5, "
+                                   "8 ppw, sponge N/8, pointwise gamma(x)=iV/eta, rtol 1e-6",
+                       "grid": f"{nd}x{nd} (n={nd + 1}, h=1/{nd + 1})", "global_batch": total,
+                       "members_per_gpu": per, "sweeps_per_step": args.sweeps,
+                       "parallelism": f"batch-shard x{world}",
+                       "l2": "no flush needed: ~1.7 GB working set per step >> 126 MB L2"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "path": "bp_problem_set_medium + bp_run with pinned host buffers"},
+            "roofline": {"bound": "hbm", "kernel": "row_kernel<9,R_SWEEP>",
+                         "achieved": row_gbs, "peak": peak, "unit": "GB/s", "frac": row_gbs / peak,
+                         "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": ROW_BYTES_PER_PT * pts_per_launch,
+                         "avg_launch_ms": row_avg,
+                         "column_kernel": {"achieved": col_gbs, "frac": col_gbs / peak,
+                                           "avg_launch_ms": col_avg,
+                                           "algorithmic_bytes_per_launch": COL_BYTES_PER_PT * pts_per_launch},
+                         "sweep": {"achieved": sweep_gbs, "frac": sweep_gbs / peak,
+                                   "bytes_per_pt": SWEEP_BYTES_PER_PT,
+                                   "gpts_per_s_kernels_only": pts_per_launch / ((row_avg + col_avg) * 1e-3) / 1e9}},
+            "cpu_baseline": cpu,
+            "gpu_launches": int(sum_over_ranks(float(launches))),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=15)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=64, help="members of config c1 (whole job)")
+    ap.add_argument("--sweeps", type=int, default=127, help="sweeps per step (max_iters)")
+    ap.add_argument("--cpu-sweeps", type=int, default=3)
+    ap.add_argument("--ref-sweeps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

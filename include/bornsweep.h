@@ -111,6 +111,11 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
                       const double* eta, int32_t device, bp_problem** out);
 int bp_problem_destroy(bp_problem* p);
 int bp_problem_batch(const bp_problem* p, int32_t* batch, bp_grid* grid);
+/* Replace the media of every member (same grid and batch): equivalent to constructing new
+ * problems, without re-allocating device workspace. */
+int bp_problem_set_medium(bp_problem* p, const double* k2, const double* k0, const double* eta);
+/* The cudaStream_t the handle launches on (for CUDA-event timing by the caller). */
+int bp_problem_stream(const bp_problem* p, void** stream);
 
 /* Operator applications on batch fields, host buffers in and out
  * (Problem::apply_* / born_residual, proj/src/problem.cpp:19-49; residual f - A u,

@@ -327,6 +327,11 @@ int bpref_run(void* h, int map_kind, double g_re, double g_im, int metric, const
 // Batch of independent members, OpenMP over members (the sample-parallel loop of
 // proj/src/bench.cpp:143-151).  k2/f/u_out: batch x nx x ny complex; k0/eta: batch.
 // res arrays: batch x (max_iters+1).
+// NOTE: the kernels' chunked reductions (proj/src/kernels.cpp:124-157) are not safe inside
+// the outer OpenMP loop: with nested parallelism off, the inner team has one thread, which
+// sums only chunk 0 of thread_count() chunks.  Under Mode::Auto the reference's own
+// bench path therefore computes wrong norms for members >= 16384 points; here the members
+// run with Mode::Serial (the reference's ground-truth kernels) and the mode is restored.
 int bpref_run_batch(int nx, int ny, double lx, double ly, int batch, const double* k2,
                     const double* k0, const double* eta, int map_kind, double g_re,
                     double g_im, int metric, const double* f, int format, double rtol,
@@ -334,6 +339,8 @@ int bpref_run_batch(int nx, int ny, double lx, double ly, int batch, const doubl
                     TraceOut* info, int nthreads) {
     const long npts = static_cast<long>(nx) * ny;
     int rc = 0;
+    const bp::parallel::Mode saved = bp::parallel::mode();
+    if (nthreads > 1) bp::parallel::set_mode(bp::parallel::Mode::Serial);
 #pragma omp parallel for schedule(dynamic) num_threads(nthreads)
     for (int b = 0; b < batch; ++b) {
         void* h = nullptr;
@@ -349,6 +356,7 @@ int bpref_run_batch(int nx, int ny, double lx, double ly, int batch, const doubl
             rc = r;
         }
     }
+    bp::parallel::set_mode(saved);
     return rc;
 }
 

@@ -55,6 +55,8 @@ ABI_FUNCTIONS = {
                                     C.POINTER(C.c_void_p)]),
     "bp_problem_destroy": (C.c_int, [C.c_void_p]),
     "bp_problem_batch": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(Grid)]),
+    "bp_problem_set_medium": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "bp_problem_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "bp_apply_A": (C.c_int, [C.c_void_p, _dp, _dp]),
     "bp_apply_V": (C.c_int, [C.c_void_p, _dp, _dp]),
     "bp_apply_V_adjoint": (C.c_int, [C.c_void_p, _dp, _dp]),

@@ -198,6 +198,20 @@ class HelmholtzDirichlet:
         _check(self._lib.bp_residual(self._h, _ptr(u), _ptr(f), _ptr(out)))
         return self._out(out)
 
+    def set_medium(self, k2, k0, eta) -> None:
+        """Swap in new media (same grid/batch) without re-allocating device workspace."""
+        k2 = self._field(k2)
+        k0 = np.ascontiguousarray(np.broadcast_to(np.asarray(k0, np.float64), (self.batch,)))
+        eta = np.ascontiguousarray(np.broadcast_to(np.asarray(eta, np.float64), (self.batch,)))
+        _check(self._lib.bp_problem_set_medium(self._h, _ptr(k2), _ptr(k0), _ptr(eta)))
+        self.k0, self.eta = k0, eta
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(self._lib.bp_problem_stream(self._h, C.byref(s)))
+        return s.value or 0
+
     def set_kernel_timing(self, enable: bool) -> None:
         _check(self._lib.bp_set_kernel_timing(self._h, int(bool(enable))))
 

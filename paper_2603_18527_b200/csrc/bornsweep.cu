@@ -256,6 +256,37 @@ cudaError_t prepare_kernels(int log2n) {
     return cudaErrorInvalidValue;
 }
 
+std::vector<double> lap_table(int n, double h) {
+    // (4/h^2) sin^2(j pi / (2n)), the DirichletInterior five-point symbol factor
+    // (proj/src/symbol.cpp:69-80, same operation order)
+    const double ax = 4.0 / (h * h);
+    std::vector<double> lap(n, 0.0);
+    for (int j = 1; j < n; ++j) {
+        const double sx = std::sin(j * kPi / (2.0 * n));
+        lap[j] = ax * sx * sx;
+    }
+    return lap;
+}
+
+// Problem ctor -> check_invertible (proj/src/symbol.cpp:102-111)
+int check_symbol(const bp_grid& g, int batch, const double* k0, const double* eta) {
+    const int n = g.nx + 1;
+    std::vector<double> lap = lap_table(n, g.lx / n);
+    for (int b = 0; b < batch; ++b) {
+        double mn = INFINITY, mx = 0.0;
+        const double k0sq = k0[b] * k0[b];
+        for (int pp = 1; pp < n; ++pp)
+            for (int qq = 1; qq < n; ++qq) {
+                const double a = std::hypot((lap[pp] + lap[qq]) - k0sq, -eta[b]);
+                mn = std::min(mn, a);
+                mx = std::max(mx, a);
+            }
+        if (mn < kSymbolDivGuard * mx)
+            return set_err(BP_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
+    }
+    return BP_OK;
+}
+
 int grid_for(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 16); }
 
 }  // namespace
@@ -329,6 +360,7 @@ Control make_control(const bp_problem* p) {
     c.fnorm_reta = p->fnorm_reta;
     c.trace_l2 = p->trace_l2;
     c.trace_reta = p->trace_reta;
+    c.trace_stride = p->trace_cap;
     return c;
 }
 
@@ -482,7 +514,9 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     CU(launch_row(p->log2n, R_FWD_BORN, a, p->stream));
     CU(launch_col(p->log2n, C_GREEN, c, p->stream));
 
-    p->stat_launches = 2;
+    // kernels launched so far in this run: pack f (+ pack u0), 2x norms (2 each), Green (3),
+    // init_control, 2x fill_nan, initial row + column pass
+    p->stat_launches = 13 + (have_u0 ? 1 : 0);
     p->stat_row_ms = p->stat_col_ms = 0;
     p->stat_timed = 0;
     const long max_launch = (long)cfg->max_iters + 1;  // launch k records entry k-1
@@ -494,27 +528,45 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         if (rc) return rc;
     }
 
-    if ((snapshots && n_snap > 0) || p->timing) {
-        cudaEvent_t ev[3];
-        for (auto& e : ev) CU(cudaEventCreate(&e));
+    if (snapshots && n_snap > 0) {
+        // debug path: one sweep at a time, copying u^k after launch k
         long k = 0;
         for (k = 1; k <= max_launch; ++k) {
-            rc = sweep_once(p, a, c, p->timing ? ev : nullptr);
-            if (rc) break;
+            rc = sweep_once(p, a, c, nullptr);
+            if (rc) return rc;
             p->stat_launches += 2;
-            if (snapshots && k < n_snap) {
+            if (k < n_snap) {
                 // u^k lives in buffer k&1 for every member still iterating
                 rc = download(p, (k & 1) ? p->u1 : p->u0, nullptr, nullptr,
                               snapshots + 2 * nd * B * k);
-                if (rc) break;
+                if (rc) return rc;
             }
             CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
                                p->stream));
             CU(cudaStreamSynchronize(p->stream));
-            if (p->timing) {
+            if (*p->host_active == 0) break;
+        }
+    } else if (p->timing) {
+        // instrumented path: CUDA events around every row / column launch on the handle's
+        // stream, polled once per kGraphSweeps sweeps (same cadence as the graph path)
+        std::vector<cudaEvent_t> ev(3 * kGraphSweeps);
+        for (auto& e : ev) CU(cudaEventCreate(&e));
+        long launched = 0;
+        while (launched < max_launch) {
+            for (int s = 0; s < kGraphSweeps; ++s) {
+                rc = sweep_once(p, a, c, &ev[3 * s]);
+                if (rc) break;
+            }
+            if (rc) break;
+            launched += kGraphSweeps;
+            p->stat_launches += 2 * kGraphSweeps;
+            CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
+                               p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            for (int s = 0; s < kGraphSweeps; ++s) {
                 float r = 0, cc = 0;
-                cudaEventElapsedTime(&r, ev[0], ev[1]);
-                cudaEventElapsedTime(&cc, ev[1], ev[2]);
+                cudaEventElapsedTime(&r, ev[3 * s], ev[3 * s + 1]);
+                cudaEventElapsedTime(&cc, ev[3 * s + 1], ev[3 * s + 2]);
                 p->stat_row_ms += r;
                 p->stat_col_ms += cc;
                 ++p->stat_timed;
@@ -565,6 +617,7 @@ int finish_run(bp_problem* p, const bp_iter_config* cfg, double* u_out, bool hos
     Control c = make_control(p);
     int rc = download(p, p->u0, p->u1, c.result_buf, u_out, host_ptr);
     if (rc) return rc;
+    p->stat_launches += 1;  // unpack
     std::vector<int> iters(B), term(B);
     std::vector<double> f1(B), f2(B);
     CU(cudaMemcpyAsync(iters.data(), c.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, p->stream));
@@ -636,26 +689,9 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
     for (size_t k = 0; k < 2 * nd * batch; ++k)
         if (!std::isfinite(k2[k])) return set_err(BP_EINVAL, "HelmholtzProblem: k2 not finite");
 
-    // symbol invertibility (Problem ctor -> check_invertible, proj/src/symbol.cpp:102-111)
+    if (int rc = check_symbol(*grid, batch, k0, eta)) return rc;
     const double h = grid->lx / n;
-    const double ax = 4.0 / (h * h);
-    std::vector<double> lap(n, 0.0);
-    for (int j = 1; j < n; ++j) {
-        const double sx = std::sin(j * kPi / (2.0 * n));
-        lap[j] = ax * sx * sx;
-    }
-    for (int b = 0; b < batch; ++b) {
-        double mn = INFINITY, mx = 0.0;
-        const double k0sq = k0[b] * k0[b];
-        for (int pp = 1; pp < n; ++pp)
-            for (int qq = 1; qq < n; ++qq) {
-                const double a = std::hypot((lap[pp] + lap[qq]) - k0sq, -eta[b]);
-                mn = std::min(mn, a);
-                mx = std::max(mx, a);
-            }
-        if (mn < kSymbolDivGuard * mx)
-            return set_err(BP_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
-    }
+    std::vector<double> lap = lap_table(n, h);
 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
@@ -849,6 +885,34 @@ int bp_run_snapshots(const bp_problem* p, const bp_map* map, const double* f,
                      const bp_iter_config* cfg, const double* u0, double* u_out, double* res_l2,
                      double* res_reta, bp_trace* info, double* snapshots, int32_t n_snap) {
     return run_impl(p, map, f, cfg, u0, u_out, res_l2, res_reta, info, true, snapshots, n_snap);
+}
+
+int bp_problem_stream(const bp_problem* p, void** stream) {
+    if (int rc = check_problem(p)) return rc;
+    if (!stream) return set_err(BP_EINVAL, "null output");
+    *stream = (void*)p->stream;
+    return BP_OK;
+}
+
+int bp_problem_set_medium(bp_problem* p, const double* k2, const double* k0, const double* eta) {
+    if (int rc = check_problem(p)) return rc;
+    if (!k2 || !k0 || !eta) return set_err(BP_EINVAL, "null argument");
+    const size_t nd = (size_t)p->grid.nx * p->grid.ny;
+    for (int b = 0; b < p->batch; ++b) {
+        if (!(eta[b] > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
+        if (!std::isfinite(k0[b])) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
+    }
+    for (size_t k = 0; k < 2 * nd * p->batch; ++k)
+        if (!std::isfinite(k2[k])) return set_err(BP_EINVAL, "HelmholtzProblem: k2 not finite");
+    if (int rc = check_symbol(p->grid, p->batch, k0, eta)) return rc;
+    DeviceGuard guard(p->device);
+    std::vector<double> k0sq(p->batch);
+    for (int b = 0; b < p->batch; ++b) k0sq[b] = k0[b] * k0[b];
+    CU(cudaMemcpyAsync(p->k0sq, k0sq.data(), sizeof(double) * p->batch, cudaMemcpyHostToDevice, p->stream));
+    CU(cudaMemcpyAsync(p->eta, eta, sizeof(double) * p->batch, cudaMemcpyHostToDevice, p->stream));
+    if (int rc = upload(p, k2, p->k2)) return rc;
+    CU(cudaStreamSynchronize(p->stream));
+    return BP_OK;
 }
 
 int bp_set_kernel_timing(bp_problem* p, int32_t enable) {

@@ -38,6 +38,7 @@ struct Control {
     const double* fnorm_reta;
     double* trace_l2;     // [batch][max_iters+1]
     double* trace_reta;
+    int trace_stride;     // allocated entries per member (>= max_iters+1)
     int max_iters;
     double rtol;
 };
@@ -86,7 +87,7 @@ __device__ __forceinline__ double seg_sum(double v) {
 
 // Trace entry m for member b + termination test, restating proj/src/iterate.cpp:105-150.
 __device__ void finalize_entry(const Control& c, int b, int m, double sum_l2, double sum_reta) {
-    const int stride = c.max_iters + 1;
+    const int stride = c.trace_stride;
     const double rel = sqrt(sum_l2) / c.fnorm_l2[b];
     const double rel_reta = sqrt(sum_reta) / c.fnorm_reta[b];
     c.trace_l2[(size_t)b * stride + m] = rel;
