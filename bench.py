@@ -364,7 +364,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=64, help="members of config c1 (whole job)")
     ap.add_argument("--sweeps", type=int, default=127, help="sweeps per step (max_iters)")
-    ap.add_argument("--cpu-sweeps", type=int, default=3)
+    ap.add_argument("--cpu-sweeps", type=int, default=100)
     ap.add_argument("--ref-sweeps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
