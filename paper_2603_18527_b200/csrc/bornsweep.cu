@@ -9,12 +9,13 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "bornsweep.h"
-#include "sweep_kernels.cuh"
+#include "sweep_launch.cuh"
 
 using namespace bs;
 
@@ -152,108 +153,59 @@ __global__ void fill_nan_kernel(double* p, size_t n) {
 // ------------------------------------------------------------------ launch tables
 constexpr int kMinLog2 = 3, kMaxLog2 = 9;
 
-template <int L>
-struct RowCfg {
-    static constexpr int T = Geom<L>::T;
-    static constexpr int NW = 8;
-    static constexpr int EPB = NW * (32 / T);
-    static constexpr size_t SMEM = sizeof(double2) * EPB * Geom<L>::PAD_N;
-};
-template <int L>
-struct ColCfg {
-    static constexpr int C = 8;
-    static constexpr int THREADS = C * Geom<L>::T;
-    static constexpr size_t SMEM = sizeof(double2) * (C * Geom<L>::PAD_N + C * Geom<L>::T);
-};
-
-template <int L, int MODE>
-cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare = false) {
-    using Cf = RowCfg<L>;
-    auto k = row_kernel<L, MODE, Cf::NW>;
-    if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
-    const long rows = (long)a.batch << L;
-    const int grid = (int)((rows + Cf::EPB - 1) / Cf::EPB);
-    k<<<grid, Cf::NW * 32, Cf::SMEM, s>>>(a);
-    return cudaGetLastError();
+// points per thread of the DST-I engine per size (8 or 16; BP_POINTS_PER_THREAD overrides)
+int points_per_thread(int log2n) {
+    static int env = [] {
+        const char* e = std::getenv("BP_POINTS_PER_THREAD");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (env == 8 || env == 16) return env;
+    return 16;
 }
 
-template <int L, int MODE>
-cudaError_t launch_col_t(const ColArgs& a, cudaStream_t s, bool prepare = false) {
-    using Cf = ColCfg<L>;
-    auto k = col_kernel<L, MODE, Cf::C>;
-    if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
-    const int grid = a.batch * ((1 << L) / Cf::C);
-    k<<<grid, Cf::THREADS, Cf::SMEM, s>>>(a);
-    return cudaGetLastError();
-}
-
-template <int L>
-cudaError_t launch_row_l(int mode, const RowArgs& a, cudaStream_t s) {
-    switch (mode) {
-        case R_FWD: return launch_row_t<L, R_FWD>(a, s);
-        case R_FWD_BORN: return launch_row_t<L, R_FWD_BORN>(a, s);
-        case R_INV: return launch_row_t<L, R_INV>(a, s);
-        default: return launch_row_t<L, R_SWEEP>(a, s);
+cudaError_t launch_row_pp(int log2n, int pp, int mode, const RowArgs& a, cudaStream_t s, bool prep = false) {
+    switch (log2n) {
+        case 3: return launch_row_L3(pp, mode, a, s, prep);
+        case 4: return launch_row_L4(pp, mode, a, s, prep);
+        case 5: return launch_row_L5(pp, mode, a, s, prep);
+        case 6: return launch_row_L6(pp, mode, a, s, prep);
+        case 7: return launch_row_L7(pp, mode, a, s, prep);
+        case 8: return launch_row_L8(pp, mode, a, s, prep);
+        case 9: return launch_row_L9(pp, mode, a, s, prep);
     }
+    return cudaErrorInvalidValue;
 }
-template <int L>
-cudaError_t launch_col_l(int mode, const ColArgs& a, cudaStream_t s) {
-    switch (mode) {
-        case C_ONE: return launch_col_t<L, C_ONE>(a, s);
-        case C_GREEN: return launch_col_t<L, C_GREEN>(a, s);
-        default: return launch_col_t<L, C_LREF>(a, s);
+cudaError_t launch_col_pp(int log2n, int pp, int mode, const ColArgs& a, cudaStream_t s, bool prep = false) {
+    switch (log2n) {
+        case 3: return launch_col_L3(pp, mode, a, s, prep);
+        case 4: return launch_col_L4(pp, mode, a, s, prep);
+        case 5: return launch_col_L5(pp, mode, a, s, prep);
+        case 6: return launch_col_L6(pp, mode, a, s, prep);
+        case 7: return launch_col_L7(pp, mode, a, s, prep);
+        case 8: return launch_col_L8(pp, mode, a, s, prep);
+        case 9: return launch_col_L9(pp, mode, a, s, prep);
     }
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_row(int log2n, int mode, const RowArgs& a, cudaStream_t s) {
-    switch (log2n) {
-        case 3: return launch_row_l<3>(mode, a, s);
-        case 4: return launch_row_l<4>(mode, a, s);
-        case 5: return launch_row_l<5>(mode, a, s);
-        case 6: return launch_row_l<6>(mode, a, s);
-        case 7: return launch_row_l<7>(mode, a, s);
-        case 8: return launch_row_l<8>(mode, a, s);
-        case 9: return launch_row_l<9>(mode, a, s);
-    }
-    return cudaErrorInvalidValue;
+    return launch_row_pp(log2n, points_per_thread(log2n), mode, a, s);
 }
 cudaError_t launch_col(int log2n, int mode, const ColArgs& a, cudaStream_t s) {
-    switch (log2n) {
-        case 3: return launch_col_l<3>(mode, a, s);
-        case 4: return launch_col_l<4>(mode, a, s);
-        case 5: return launch_col_l<5>(mode, a, s);
-        case 6: return launch_col_l<6>(mode, a, s);
-        case 7: return launch_col_l<7>(mode, a, s);
-        case 8: return launch_col_l<8>(mode, a, s);
-        case 9: return launch_col_l<9>(mode, a, s);
-    }
-    return cudaErrorInvalidValue;
-}
-
-template <int L>
-cudaError_t prepare_l() {
-    RowArgs a{};
-    ColArgs c{};
-    cudaError_t e = cudaSuccess;
-    for (cudaError_t r : {launch_row_t<L, R_FWD>(a, nullptr, true), launch_row_t<L, R_FWD_BORN>(a, nullptr, true),
-                          launch_row_t<L, R_INV>(a, nullptr, true), launch_row_t<L, R_SWEEP>(a, nullptr, true),
-                          launch_col_t<L, C_ONE>(c, nullptr, true), launch_col_t<L, C_GREEN>(c, nullptr, true),
-                          launch_col_t<L, C_LREF>(c, nullptr, true)})
-        if (r != cudaSuccess) e = r;
-    return e;
+    return launch_col_pp(log2n, points_per_thread(log2n), mode, a, s);
 }
 
 cudaError_t prepare_kernels(int log2n) {
-    switch (log2n) {
-        case 3: return prepare_l<3>();
-        case 4: return prepare_l<4>();
-        case 5: return prepare_l<5>();
-        case 6: return prepare_l<6>();
-        case 7: return prepare_l<7>();
-        case 8: return prepare_l<8>();
-        case 9: return prepare_l<9>();
+    RowArgs a{};
+    ColArgs c{};
+    cudaError_t e = cudaSuccess;
+    for (int pp : {8, 16}) {
+        for (int mode : {R_FWD, R_FWD_BORN, R_INV, R_SWEEP})
+            if (cudaError_t r = launch_row_pp(log2n, pp, mode, a, nullptr, true)) e = r;
+        for (int mode : {C_ONE, C_GREEN, C_LREF})
+            if (cudaError_t r = launch_col_pp(log2n, pp, mode, c, nullptr, true)) e = r;
     }
-    return cudaErrorInvalidValue;
+    return e;
 }
 
 std::vector<double> lap_table(int n, double h) {

@@ -103,35 +103,74 @@ struct Dft<2> {
     }
 };
 
-// ------------------------------------------------------------------ engine geometry
-template <int LOG2N>
-struct Geom {
-    static constexpr int N = 1 << LOG2N;
-    static constexpr int P = (N / 2) < 16 ? (N / 2) : 16;  // points per thread
-    static constexpr int T = N / P;                        // threads per engine
-    static constexpr int H = N / 2;
-    static constexpr int PAD_N = N + N / 16 + 1;           // padded smem line (double2)
-    __host__ __device__ static constexpr int pidx(int i) { return i + (i >> 4); }
+// (cos, sin)(pi m / 16), m < 16: the pre-processing factor sin(pi (t + T m)/N) with
+// T m / N = m / P is sin(pi t/N) cos(pi m/P) + cos(pi t/N) sin(pi m/P).
+struct CS {
+    double c, s;
+};
+__device__ constexpr CS kCS16[16] = {
+    {1.0, 0.0},
+    {0.9807852804032304, 0.19509032201612825},
+    {0.9238795325112867, 0.3826834323650898},
+    {0.8314696123025452, 0.5555702330196022},
+    {0.7071067811865476, 0.7071067811865475},
+    {0.5555702330196023, 0.8314696123025452},
+    {0.38268343236508984, 0.9238795325112867},
+    {0.19509032201612833, 0.9807852804032304},
+    {0.0, 1.0},
+    {-0.1950903220161282, 0.9807852804032304},
+    {-0.3826834323650897, 0.9238795325112867},
+    {-0.555570233019602, 0.8314696123025455},
+    {-0.7071067811865475, 0.7071067811865476},
+    {-0.8314696123025453, 0.5555702330196022},
+    {-0.9238795325112867, 0.3826834323650899},
+    {-0.9807852804032304, 0.1950903220161286},
 };
 
-// Stockham pass list: product of radices == N/2; first radix == P.
-template <int LOG2N>
+// powers pw[r] = w^r, r < R, by squaring (depth <= log2 R + 1 multiplications)
+template <int R>
+__device__ __forceinline__ void twiddle_powers(double2 w, double2 (&pw)[R]) {
+    pw[0] = make_double2(1.0, 0.0);
+    if constexpr (R > 1) pw[1] = w;
+#pragma unroll
+    for (int r = 2; r < R; ++r) pw[r] = (r & 1) ? cmul(pw[r - 1], w) : cmul(pw[r / 2], pw[r / 2]);
+}
+
+// ------------------------------------------------------------------ engine geometry
+// PP: requested points per thread (16 or 8); capped at N/2 for tiny lines.
+template <int LOG2N, int PP = 16>
+struct Geom {
+    static constexpr int N = 1 << LOG2N;
+    static constexpr int P = (N / 2) < PP ? (N / 2) : PP;  // points per thread
+    static constexpr int T = N / P;                        // threads per engine
+    static constexpr int H = N / 2;
+    static constexpr int PAD_N = N + N / 8 + N / 64 + 1;   // padded smem line (double2)
+    // i + i/8 + i/64: every access pattern of the engine (stride 1, 4, 8, 16, 32 over the 8
+    // lanes of a 128-bit shared-memory phase) lands on 8 distinct 16-byte bank groups.
+    __host__ __device__ static constexpr int pidx(int i) { return i + (i >> 3) + (i >> 6); }
+};
+
+// Stockham pass list: product of radices == N/2; first radix == P; radices <= P.
+template <int LOG2N, int PP = 16>
 struct Passes {
-    using G = Geom<LOG2N>;
-    // remaining product after the first pass
-    static constexpr int REM = G::H / G::P;
-    static constexpr int R2 = REM >= 16 ? 16 : REM;          // second pass radix (1 = none)
-    static constexpr int REM2 = REM / (R2 > 0 ? R2 : 1);
-    static constexpr int R3 = REM2 >= 16 ? 16 : REM2;        // third pass radix
-    static constexpr int REM3 = REM2 / (R3 > 0 ? R3 : 1);
-    static constexpr int R4 = REM3;                          // fourth (<= 16 for N <= 4096*16)
-    static_assert(R4 <= 16, "engine supports n <= 65536");
+    using G = Geom<LOG2N, PP>;
+    static constexpr int RMAX = G::P;
+    static constexpr int REM = G::H / G::P;  // remaining product after the first pass
+    static constexpr int R2 = REM >= RMAX ? RMAX : REM;  // second pass radix (1 = none)
+    static constexpr int REM2 = REM / R2;
+    static constexpr int R3 = REM2 >= RMAX ? RMAX : REM2;
+    static constexpr int REM3 = REM2 / R3;
+    static constexpr int R4 = REM3 >= RMAX ? RMAX : REM3;
+    static constexpr int REM4 = REM3 / R4;
+    static constexpr int R5 = REM4;
+    static_assert(R5 <= RMAX, "line too long for this engine");
 };
 
 // ------------------------------------------------------------------ sync/scan policies
 // Engine threads are T contiguous lanes of one warp (T <= 32).
 template <int T>
 struct WarpSeg {
+    static_assert(T <= 32, "WarpSeg spans one warp");
     __device__ __forceinline__ void sync() const { __syncwarp(); }
     // exclusive prefix over the T lanes of this engine (lane segment aligned to T)
     __device__ __forceinline__ double2 exclusive_scan(double2 v, int t) const {
@@ -148,10 +187,65 @@ struct WarpSeg {
         return csub(incl, v);
     }
     // deterministic sum over the T lanes of the engine (result valid in every lane)
-    __device__ __forceinline__ double sum(double v) const {
+    __device__ __forceinline__ double sum(double v, int) const {
 #pragma unroll
         for (int d = T / 2; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d, T);
         return v;
+    }
+    __device__ __forceinline__ int bcast0(int v, int) const {
+        return __shfl_sync(0xffffffffu, v, ((threadIdx.x & 31) / T) * T);
+    }
+};
+
+// Engine = T/32 consecutive whole warps synchronised by named barrier `id` (1..15).
+// scratch: >= T/32 double2 of shared memory private to the engine.
+template <int T>
+struct BarSeg {
+    static_assert(T % 32 == 0 && T > 32, "BarSeg spans several whole warps");
+    static constexpr int W = T / 32;
+    double2* scratch;
+    int id;
+    __device__ __forceinline__ void sync() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(T) : "memory");
+    }
+    __device__ __forceinline__ double2 exclusive_scan(double2 v, int t) const {
+        const int lane = t & 31, w = t >> 5;
+        double2 incl = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double ux = __shfl_up_sync(0xffffffffu, incl.x, d);
+            const double uy = __shfl_up_sync(0xffffffffu, incl.y, d);
+            if (lane >= d) {
+                incl.x += ux;
+                incl.y += uy;
+            }
+        }
+        if (lane == 31) scratch[w] = incl;
+        sync();
+        double2 off = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+            if (k < w) off = cadd(off, scratch[k]);
+        sync();
+        return cadd(off, csub(incl, v));
+    }
+    __device__ __forceinline__ double sum(double v, int t) const {
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        if ((t & 31) == 0) scratch[t >> 5].x = v;
+        sync();
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) s += scratch[k].x;
+        sync();
+        return s;
+    }
+    __device__ __forceinline__ int bcast0(int v, int t) const {
+        if (t == 0) scratch[0].y = __longlong_as_double((long long)v);
+        sync();
+        const int r = (int)__double_as_longlong(scratch[0].y);
+        sync();
+        return r;
     }
 };
 
@@ -194,10 +288,10 @@ struct BlockSeg {
 };
 
 // ------------------------------------------------------------------ the engine
-template <int LOG2N>
+template <int LOG2N, int PP = 16>
 struct DstEngine {
-    using G = Geom<LOG2N>;
-    using PS = Passes<LOG2N>;
+    using G = Geom<LOG2N, PP>;
+    using PS = Passes<LOG2N, PP>;
     static constexpr int N = G::N, P = G::P, T = G::T, H = G::H;
 
     // One Stockham pass of radix R over the line in `buf` (read all, sync, write all, sync).
@@ -213,10 +307,13 @@ struct DstEngine {
             for (int b = 0; b < V; ++b) {
                 const int jj = t + T * b;
                 const int jm = jj % NS;
+                // exp(-2 pi i jm r / (NS R)) = w^r with w = tw[jm N/(NS R)]: one load per butterfly
+                double2 pw[R];
+                twiddle_powers<R>(__ldg(&tw[jm * (N / (NS * R))]), pw);
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     double2 x = buf[G::pidx(jj + r * STRIDE_IN)];
-                    if (NS > 1 && r > 0) x = cmul(x, __ldg(&tw[(jm * r) * (N / (NS * R))]));
+                    if (r > 0) x = cmul(x, pw[r]);
                     v[b * R + r] = x;
                 }
                 Dft<R>::template run<1>(&v[b * R]);
@@ -241,10 +338,12 @@ struct DstEngine {
                                                const double* __restrict__ sinp, const Pol& pol) {
         // --- pre-processing + first Stockham pass (radix P, Ns = 1, data already in registers)
         double2 v[P];
+        const double st = __ldg(&sinp[t]), ct = __ldg(&sinp[t + H]);  // sin, cos(pi t/N)
 #pragma unroll
         for (int m = 0; m < P; ++m) {
             const int j = t + T * m;
-            const double s = __ldg(&sinp[j]);
+            constexpr int STEP = 16 / P;
+            const double s = fma(st, kCS16[m * STEP].c, ct * kCS16[m * STEP].s);
             const double2 a = cadd(x[m], xm[m]);
             const double2 d = csub(x[m], xm[m]);
             v[m] = (j == 0) ? make_double2(0.0, 0.0)
@@ -258,13 +357,16 @@ struct DstEngine {
         pass<PS::R2, P>(buf, t, tw, pol);
         pass<PS::R3, P * PS::R2>(buf, t, tw, pol);
         pass<PS::R4, P * PS::R2 * PS::R3>(buf, t, tw, pol);
+        pass<PS::R5, P * PS::R2 * PS::R3 * PS::R4>(buf, t, tw, pol);
         // --- fused final radix-2 pass + DST-I post-processing + prefix sum
         constexpr int K = P / 2;  // k values per thread: k = t*K + i
         double2 ev[K], od[K];     // Y_2k and S_k
+        const double2 w0 = __ldg(&tw[t * K]), w1 = __ldg(&tw[1]);
+        double2 w = w0;           // exp(-2 pi i k/N), stepped by exp(-2 pi i/N)
 #pragma unroll
         for (int i = 0; i < K; ++i) {
             const int k = t * K + i;
-            const double2 w = __ldg(&tw[k]);  // exp(-2 pi i k/N)
+            if (i > 0) w = cmul(w, w1);
             const double2 a = buf[G::pidx(k)];
             const double2 b = cmul(buf[G::pidx(k + H)], w);
             const double2 Wk = cadd(a, b);

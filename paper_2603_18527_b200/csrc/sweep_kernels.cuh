@@ -78,15 +78,15 @@ struct ColArgs {
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
 
-template <int T>
-__device__ __forceinline__ double seg_sum(double v) {
-#pragma unroll
-    for (int d = T / 2; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d, T);
-    return v;
+// TMA bulk prefetch of a contiguous range into L2 (sm_90+: cp.async.bulk.prefetch.L2).
+// bytes: multiple of 16, address 16-B aligned.  Fire-and-forget, no registers held.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+
 // Trace entry m for member b + termination test, restating proj/src/iterate.cpp:105-150.
-__device__ void finalize_entry(const Control& c, int b, int m, double sum_l2, double sum_reta) {
+static __device__ void finalize_entry(const Control& c, int b, int m, double sum_l2, double sum_reta) {
     const int stride = c.trace_stride;
     const double rel = sqrt(sum_l2) / c.fnorm_l2[b];
     const double rel_reta = sqrt(sum_reta) / c.fnorm_reta[b];
@@ -115,21 +115,63 @@ __device__ void finalize_entry(const Control& c, int b, int m, double sum_l2, do
     c.counter[b] = 0u;
 }
 
-// ------------------------------------------------------------------ row kernel (T <= 32)
-// NW warps per CTA; 32/T engines (rows) per warp; one global row per engine.
-template <int LOG2N, int MODE, int NW>
-__global__ void __launch_bounds__(NW * 32, (NW >= 8 ? 2 : 4))
+// ------------------------------------------------------------------ row kernel
+// NW warps per CTA; engine = one global row of T = n/P threads (several engines per warp when
+// T < 32, several warps per engine -- named barriers -- when T > 32).
+template <int THREADS, int REGS>
+struct MinBlocks {
+    static constexpr int V = 65536 / (THREADS * REGS);
+    static constexpr int value = V > 32 ? 32 : (V < 1 ? 1 : V);
+};
+
+template <int T>
+struct PolicyFor {
+    using type = WarpSeg<T>;
+};
+template <>
+struct PolicyFor<64> {
+    using type = BarSeg<64>;
+};
+template <>
+struct PolicyFor<128> {
+    using type = BarSeg<128>;
+};
+template <>
+struct PolicyFor<256> {
+    using type = BarSeg<256>;
+};
+
+template <int T>
+__device__ __forceinline__ WarpSeg<T> make_policy(WarpSeg<T>*, double2*, int) { return WarpSeg<T>{}; }
+template <int T>
+__device__ __forceinline__ BarSeg<T> make_policy(BarSeg<T>*, double2* scratch, int e) {
+    return BarSeg<T>{scratch + e * (T / 32), 1 + e};
+}
+
+template <int LOG2N, int PP, int NW>
+struct RowGeom {
+    using G = Geom<LOG2N, PP>;
+    static constexpr int T = G::T;
+    static constexpr int EPB = NW * 32 / T;  // engines (rows) per CTA
+    static_assert(T <= 32 || (T % 32 == 0 && EPB <= 15), "row engine layout");
+    static constexpr int SCRATCH = T > 32 ? EPB * (T / 32) : 0;
+    static constexpr size_t SMEM = sizeof(double2) * ((size_t)EPB * G::PAD_N + SCRATCH);
+};
+
+template <int LOG2N, int MODE, int NW, int PP>
+__global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? 128 : 80>::value))
 row_kernel(const RowArgs a) {
-    using G = Geom<LOG2N>;
+    using G = Geom<LOG2N, PP>;
+    using RG = RowGeom<LOG2N, PP, NW>;
+    using Pol = typename PolicyFor<G::T>::type;
+    using Engine = DstEngine<LOG2N, PP>;
     constexpr int N = G::N, P = G::P, T = G::T;
-    static_assert(T <= 32, "row kernel handles n <= 512");
-    constexpr int EPW = 32 / T;
-    constexpr int EPB = NW * EPW;
+    constexpr int EPB = RG::EPB;
     extern __shared__ double2 smem[];
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t = lane % T;
-    const int e = warp * EPW + lane / T;
+    const int lane = threadIdx.x & 31;
+    const int t = threadIdx.x % T;
+    const int e = threadIdx.x / T;
     const long grow = (long)blockIdx.x * EPB + e;
     const int b = (int)(grow >> LOG2N);
     const int i = (int)(grow & (N - 1));
@@ -142,10 +184,26 @@ row_kernel(const RowArgs a) {
     if (!__syncthreads_or(valid)) return;
 
     double2* buf = smem + e * G::PAD_N;
-    const WarpSeg<T> pol{};
+    const Pol pol = make_policy((Pol*)nullptr, smem + EPB * G::PAD_N, e);
     const size_t mem = (size_t)(valid ? b : 0) * N * N;
     const size_t row = mem + (size_t)(valid ? i : 0) * N;
     const double2 zero = make_double2(0.0, 0.0);
+    (void)lane;
+
+    if constexpr (MODE == R_SWEEP) {
+        // Stage the element-wise operands of this row (and the stencil halo rows at the CTA's
+        // edges) into L2 while the inverse transform runs: the loads after the engine then hit
+        // L2 instead of waiting on DRAM with few registers to spare for outstanding loads.
+        if (valid && t == 0) {
+            const double2* ucur = (m & 1) ? a.u1 : a.u0;
+            constexpr unsigned RB = N * sizeof(double2);
+            prefetch_l2(ucur + row, RB);
+            prefetch_l2(a.k2 + row, RB);
+            prefetch_l2(a.f + row, RB);
+            if (e == 0) prefetch_l2(ucur + row - N, RB);
+            if (e == EPB - 1) prefetch_l2(ucur + row + N, RB);
+        }
+    }
 
     double2 q[P];
     double acc_l2 = 0.0, acc_reta = 0.0;
@@ -159,7 +217,7 @@ row_kernel(const RowArgs a) {
             x[mm] = valid ? a.T[row + j] : zero;
             xm[mm] = (valid && j != 0) ? a.T[row + (N - j)] : zero;
         }
-        DstEngine<LOG2N>::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+        Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
         // stage through smem: contiguous -> stride layout (coalesced global access)
 #pragma unroll
         for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
@@ -249,7 +307,7 @@ row_kernel(const RowArgs a) {
         qm[mm] = (j == 0) ? zero : buf[G::pidx(N - j)];
     }
     pol.sync();
-    DstEngine<LOG2N>::run(q, qm, y2, t, buf, a.tw, a.sinp, pol);
+    Engine::run(q, qm, y2, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
     for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y2[l];
     pol.sync();
@@ -260,8 +318,8 @@ row_kernel(const RowArgs a) {
     }
 
     if constexpr (MODE == R_SWEEP) {
-        acc_l2 = seg_sum<T>(acc_l2);
-        acc_reta = seg_sum<T>(acc_reta);
+        acc_l2 = pol.sum(acc_l2, t);
+        acc_reta = pol.sum(acc_reta, t);
         int last = 0;
         if (valid && t == 0) {
             a.ctl.partial[(size_t)b * N + i] = make_double2(acc_l2, acc_reta);
@@ -269,7 +327,7 @@ row_kernel(const RowArgs a) {
             const unsigned old = atomicAdd(&a.ctl.counter[b], 1u);
             last = (old == (unsigned)(N - 2));
         }
-        last = __shfl_sync(0xffffffffu, last, (lane / T) * T);
+        last = pol.bcast0(last, t);
         if (last) {
             __threadfence();
             double s1 = 0.0, s2 = 0.0;
@@ -278,8 +336,8 @@ row_kernel(const RowArgs a) {
                 s1 += pr.x;
                 s2 += pr.y;
             }
-            s1 = seg_sum<T>(s1);
-            s2 = seg_sum<T>(s2);
+            s1 = pol.sum(s1, t);
+            s2 = pol.sum(s2, t);
             if (t == 0) finalize_entry(a.ctl, b, m, s1, s2);
         }
     }
@@ -287,10 +345,18 @@ row_kernel(const RowArgs a) {
 
 // ------------------------------------------------------------------ column kernel
 // C columns per CTA, T threads per column (thread = c + C*t): row segments of C*16 bytes.
-template <int LOG2N, int MODE, int C>
-__global__ void __launch_bounds__(C * Geom<LOG2N>::T, (C * Geom<LOG2N>::T >= 256 ? 2 : 4))
+template <int LOG2N, int PP, int C>
+struct ColGeom {
+    using G = Geom<LOG2N, PP>;
+    static constexpr int THREADS = C * G::T;
+    static constexpr size_t SMEM = sizeof(double2) * (C * G::PAD_N + C * G::T);
+};
+
+template <int LOG2N, int MODE, int C, int PP>
+__global__ void __launch_bounds__(C * Geom<LOG2N, PP>::T, (MinBlocks<C * Geom<LOG2N, PP>::T, PP >= 16 ? 128 : 64>::value))
 col_kernel(const ColArgs a) {
-    using G = Geom<LOG2N>;
+    using G = Geom<LOG2N, PP>;
+    using Engine = DstEngine<LOG2N, PP>;
     constexpr int N = G::N, P = G::P, T = G::T;
     extern __shared__ double2 smem[];
     const int c = threadIdx.x % C, t = threadIdx.x / C;
@@ -311,7 +377,7 @@ col_kernel(const ColArgs a) {
         x[mm] = a.T[mem + (size_t)j * N + q];
         xm[mm] = (j == 0) ? zero : a.T[mem + (size_t)(N - j) * N + q];
     }
-    DstEngine<LOG2N>::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+    Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
 
     if constexpr (MODE == C_ONE) {
 #pragma unroll
@@ -327,7 +393,7 @@ col_kernel(const ColArgs a) {
             const double li = -eta;
             double2 w;
             if constexpr (MODE == C_GREEN) {
-                const double s = a.scale / (lr * lr + li * li);
+                const double s = a.scale * __drcp_rn(fma(lr, lr, li * li));
                 w = make_double2(lr * s, -li * s);  // scale / lambda
             } else {
                 w = make_double2(lr * a.scale, li * a.scale);  // scale * lambda
@@ -343,7 +409,7 @@ col_kernel(const ColArgs a) {
             xm[mm] = (j == 0) ? zero : buf[G::pidx(N - j)];
         }
         pol.sync();
-        DstEngine<LOG2N>::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+        Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
         for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * N + q] = y[l];
     }
