@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbornsweep.so")
+# BP_LIB_PATH: load an alternative build of the same ABI (A/B kernel experiments only)
+LIB_PATH = os.environ.get("BP_LIB_PATH") or os.path.join(HERE, "libbornsweep.so")
 HOST_LIB_PATH = os.path.join(HERE, "libbornsweep_host.so")
 
 _dp = C.POINTER(C.c_double)

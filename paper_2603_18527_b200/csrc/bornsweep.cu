@@ -658,7 +658,9 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
     p->field = (size_t)n * n;
     p->alloc = p->field * batch + n;
     p->inv_h2 = 1.0 / (h * h);
-    p->green_scale = 4.0 / ((double)n * n);
+    // 4/((nx+1)(ny+1)) (proj/src/transforms.cpp:99) divided by the gain of the four engine
+    // passes of a Green application (kEngineGain^4 = 256, exact)
+    p->green_scale = 4.0 / ((double)n * n) / (kEngineGain * kEngineGain * kEngineGain * kEngineGain);
     auto fail = [&](int code) {
         bp_problem_destroy(p);
         return code;
@@ -784,7 +786,8 @@ static int spectral_op(const bp_problem* cp, int which, const double* in, const 
         case 3:  // forward transform (plain sine sums)
         case 4:  // inverse transform (x 4/((nx+1)(ny+1)))
             CU(launch_row(p->log2n, R_FWD, a, p->stream));
-            c.scale = which == 3 ? 1.0 : p->green_scale;
+            // two engine passes (gain 16) for a 2-D transform
+            c.scale = (which == 3 ? 1.0 : 4.0 / ((double)p->n * p->n)) / (kEngineGain * kEngineGain);
             CU(launch_col(p->log2n, C_ONE, c, p->stream));
             if (int rc = download(p, p->T, p->T, nullptr, out)) return rc;
             CU(cudaStreamSynchronize(p->stream));

@@ -4,7 +4,8 @@
 // (x_0 == 0 is the Dirichlet padding slot; the DST-I length is n-1) into
 //     Y_k = sum_{j=1}^{n-1} x_j sin(pi j k / n),     k = 0..n-1 (Y_0 = 0),
 // i.e. the reference's forward DST-I convention (plain sine sum; FFTW RODFT00 / 2,
-// proj/include/bp/transforms.hpp:15-24).  Applying it twice gives (n/2) x.
+// proj/include/bp/transforms.hpp:15-24), TIMES kEngineGain = 4: the factors 1/2 of the pre-
+// and post-processing below are dropped and callers fold 4^k into one scale (exact).
 //
 // Algorithm (one length-n complex FFT per complex line, not the 2(n+1) odd extension):
 //   y_j = sin(pi j/n)(x_j + x_{n-j}) + (x_j - x_{n-j})/2          (pre-processing)
@@ -26,6 +27,8 @@
 #include <stdint.h>
 
 namespace bs {
+
+constexpr double kEngineGain = 4.0;  // each engine pass returns 4 x the plain sine sum
 
 // ------------------------------------------------------------------ complex helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -148,6 +151,9 @@ struct Geom {
     // i + i/8 + i/64: every access pattern of the engine (stride 1, 4, 8, 16, 32 over the 8
     // lanes of a 128-bit shared-memory phase) lands on 8 distinct 16-byte bank groups.
     __host__ __device__ static constexpr int pidx(int i) { return i + (i >> 3) + (i >> 6); }
+    struct Pidx {
+        __device__ __forceinline__ int operator()(int i) const { return pidx(i); }
+    };
 };
 
 // Stockham pass list: product of radices == N/2; first radix == P; radices <= P.
@@ -194,6 +200,19 @@ struct WarpSeg {
     }
     __device__ __forceinline__ int bcast0(int v, int) const {
         return __shfl_sync(0xffffffffu, v, ((threadIdx.x & 31) / T) * T);
+    }
+    // xm[m] = x_{N - t - T m} for data in the stride layout x[m] = x_{t + T m} (N = T P):
+    // lane T - t holds it in register P-1-m; lane 0 holds its own mirror in register P-m.
+    template <int P, class Idx>
+    __device__ __forceinline__ void mirror(const double2 (&x)[P], double2 (&xm)[P], int t, double2*,
+                                           Idx) const {
+        const int src = ((threadIdx.x & 31) / T) * T + ((T - t) & (T - 1));
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            const double2 v = make_double2(__shfl_sync(0xffffffffu, x[P - 1 - m].x, src),
+                                           __shfl_sync(0xffffffffu, x[P - 1 - m].y, src));
+            xm[m] = (t != 0) ? v : (m == 0 ? make_double2(0.0, 0.0) : x[P - m]);
+        }
     }
 };
 
@@ -247,16 +266,35 @@ struct BarSeg {
         sync();
         return r;
     }
+    // mirror exchange through the engine's shared-memory line (idx = padding function)
+    template <int P, class Idx>
+    __device__ __forceinline__ void mirror(const double2 (&x)[P], double2 (&xm)[P], int t, double2* buf,
+                                           Idx idx) const {
+        constexpr int N = T * P;
+#pragma unroll
+        for (int m = 0; m < P; ++m) buf[idx(t + T * m)] = x[m];
+        sync();
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            const int j = t + T * m;
+            xm[m] = (j == 0) ? make_double2(0.0, 0.0) : buf[idx(N - j)];
+        }
+        sync();
+    }
 };
 
-// Engines spread over the CTA (column kernel): E engines x T threads; scan scratch in smem.
+// Engines spread over the CTA (column kernel): E engines x T threads; scan scratch in smem,
+// laid out [t][e] with row pitch E+1 so both the write (lanes = engines) and the per-engine
+// scan read (lanes = t) are bank-conflict free.
 template <int T, int E>
 struct BlockSeg {
-    double2* scratch;  // E*T double2
+    static constexpr int SCRATCH = T * (E + 1);  // double2
+    double2* scratch;
     int e;
+    __device__ __forceinline__ static int sidx(int ee, int tt) { return tt * (E + 1) + ee; }
     __device__ __forceinline__ void sync() const { __syncthreads(); }
     __device__ __forceinline__ double2 exclusive_scan(double2 v, int t) const {
-        scratch[e * T + t] = v;
+        scratch[sidx(e, t)] = v;
         __syncthreads();
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         const int nwarps = (blockDim.x + 31) >> 5;
@@ -265,7 +303,7 @@ struct BlockSeg {
             double2 carry = make_double2(0.0, 0.0);
             for (int c = 0; c < CH; ++c) {
                 const int tt = c * 32 + lane;
-                double2 x = tt < T ? scratch[ee * T + tt] : make_double2(0.0, 0.0);
+                double2 x = tt < T ? scratch[sidx(ee, tt)] : make_double2(0.0, 0.0);
                 double2 incl = x;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
@@ -276,14 +314,14 @@ struct BlockSeg {
                         incl.y += uy;
                     }
                 }
-                if (tt < T) scratch[ee * T + tt] = cadd(carry, csub(incl, x));
+                if (tt < T) scratch[sidx(ee, tt)] = cadd(carry, csub(incl, x));
                 const double tx = __shfl_sync(0xffffffffu, incl.x, 31);
                 const double ty = __shfl_sync(0xffffffffu, incl.y, 31);
                 carry = cadd(carry, make_double2(tx, ty));
             }
         }
         __syncthreads();
-        return scratch[e * T + t];
+        return scratch[sidx(e, t)];
     }
 };
 
@@ -338,7 +376,9 @@ struct DstEngine {
                                                const double* __restrict__ sinp, const Pol& pol) {
         // --- pre-processing + first Stockham pass (radix P, Ns = 1, data already in registers)
         double2 v[P];
-        const double st = __ldg(&sinp[t]), ct = __ldg(&sinp[t + H]);  // sin, cos(pi t/N)
+        // 2 sin(pi t/N), 2 cos(pi t/N): the engine computes 4x the sine sum (the 1/2 factors
+        // of pre- and post-processing are folded into the caller's scale, exact powers of 2)
+        const double st = 2.0 * __ldg(&sinp[t]), ct = 2.0 * __ldg(&sinp[t + H]);
 #pragma unroll
         for (int m = 0; m < P; ++m) {
             const int j = t + T * m;
@@ -347,7 +387,7 @@ struct DstEngine {
             const double2 a = cadd(x[m], xm[m]);
             const double2 d = csub(x[m], xm[m]);
             v[m] = (j == 0) ? make_double2(0.0, 0.0)
-                            : make_double2(fma(s, a.x, 0.5 * d.x), fma(s, a.y, 0.5 * d.y));
+                            : make_double2(fma(s, a.x, d.x), fma(s, a.y, d.y));
         }
         Dft<P>::template run<1>(v);
 #pragma unroll
@@ -372,15 +412,15 @@ struct DstEngine {
             const double2 Wk = cadd(a, b);
             if (k == 0) {
                 ev[i] = make_double2(0.0, 0.0);
-                od[i] = cscale(Wk, 0.5);
+                od[i] = Wk;
             } else {
                 // W_{N-k} = a_{H-k} - w^{H-k} b_{H-k},  w^{H-k} = -conj(w^k)
                 const double2 a2 = buf[G::pidx(H - k)];
                 const double2 b2 = buf[G::pidx(N - k)];
                 const double2 Wnk = cadd(a2, cmul(b2, cconj(w)));
                 const double2 dif = csub(Wk, Wnk);
-                ev[i] = make_double2(-0.5 * dif.y, 0.5 * dif.x);  // (i/2)(Wk - Wnk)
-                od[i] = cscale(cadd(Wk, Wnk), 0.5);
+                ev[i] = make_double2(-dif.y, dif.x);  // i (Wk - Wnk)
+                od[i] = cadd(Wk, Wnk);
             }
         }
         // local inclusive prefix of S

@@ -18,6 +18,10 @@
 
 #include "dst_engine.cuh"
 
+#ifndef BS_SHFL_MIRROR
+#define BS_SHFL_MIRROR 1
+#endif
+
 namespace bs {
 
 enum RowMode { R_FWD = 0, R_FWD_BORN = 1, R_INV = 2, R_SWEEP = 3 };
@@ -215,7 +219,7 @@ row_kernel(const RowArgs a) {
         for (int mm = 0; mm < P; ++mm) {
             const int j = t + T * mm;
             x[mm] = valid ? a.T[row + j] : zero;
-            xm[mm] = (valid && j != 0) ? a.T[row + (N - j)] : zero;
+            xm[mm] = (valid && j != 0) ? a.T[row + (N - j)] : zero;  // mirror: L1 hit
         }
         Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
         // stage through smem: contiguous -> stride layout (coalesced global access)
@@ -296,8 +300,11 @@ row_kernel(const RowArgs a) {
         }
     }
 
-    // ---- forward y-DST of q: mirror exchange through smem
+    // ---- forward y-DST of q (mirror by warp shuffles, or shared memory for multi-warp rows)
     double2 qm[P], y2[P];
+#if BS_SHFL_MIRROR
+    pol.mirror(q, qm, t, buf, typename G::Pidx{});
+#else
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) buf[G::pidx(t + T * mm)] = q[mm];
     pol.sync();
@@ -307,6 +314,7 @@ row_kernel(const RowArgs a) {
         qm[mm] = (j == 0) ? zero : buf[G::pidx(N - j)];
     }
     pol.sync();
+#endif
     Engine::run(q, qm, y2, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
     for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y2[l];
@@ -349,7 +357,7 @@ template <int LOG2N, int PP, int C>
 struct ColGeom {
     using G = Geom<LOG2N, PP>;
     static constexpr int THREADS = C * G::T;
-    static constexpr size_t SMEM = sizeof(double2) * (C * G::PAD_N + C * G::T);
+    static constexpr size_t SMEM = sizeof(double2) * (C * G::PAD_N + BlockSeg<G::T, C>::SCRATCH);
 };
 
 template <int LOG2N, int MODE, int C, int PP>

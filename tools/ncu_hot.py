@@ -7,6 +7,7 @@ import sys
 
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+col_name = sys.argv[4] if len(sys.argv) > 4 else "Warp Stall Sampling (All Samples)"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
                       "-k", f"regex:{kre}"], capture_output=True, text=True).stdout
 agg, sass, fn_tot = {}, [], {}
@@ -21,11 +22,12 @@ for r in csv.reader(io.StringIO(out)):
         cur_fn = r[1]
         continue
     if r[0] == "Line No":
+        col = r.index(col_name, 3)
         continue
     if r[0]:
         cur_line = f"{cur_file}:{r[0]} {r[1].strip()[:80]}"
     try:
-        v = int(r[4])
+        v = int(float(r[col]))
     except (ValueError, IndexError):
         continue
     key = (cur_fn, cur_line)
