@@ -204,11 +204,9 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
+    from paper_2603_18527_b200.sharding import shard_members
     total = args.batch
-    if total % world:
-        raise SystemExit(f"batch {total} not divisible by {world} ranks")
-    per = total // world
-    first = rank * per
+    first, per = shard_members(total, world, rank)
     k2, f, k0, eta = bs.config_instances("c1", first, per)
     nd = k2.shape[1]
     pts = nd * nd
