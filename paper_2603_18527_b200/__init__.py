@@ -5,6 +5,7 @@ metric), rebuilt as hand-written sm_100a CUDA behind a C ABI (include/bornsweep.
 Python mirror of the reference's operator / map / driver API (api.py).
 """
 from .api import (  # noqa: F401
+    FourierDiagMap,
     HelmholtzDirichlet,
     IterationConfig,
     IterationTrace,
@@ -18,7 +19,7 @@ from .instances import CONFIGS, InstanceSpec, config_instances, make_instances  
 from . import _native  # noqa: F401
 
 __all__ = [
-    "HelmholtzDirichlet", "IterationConfig", "IterationTrace", "OptimalScalarMap", "PointwiseMap",
+    "FourierDiagMap", "HelmholtzDirichlet", "IterationConfig", "IterationTrace", "OptimalScalarMap", "PointwiseMap",
     "RunResult", "ScalarMap", "run", "CONFIGS", "InstanceSpec", "config_instances",
     "make_instances",
 ]

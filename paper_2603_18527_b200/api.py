@@ -74,11 +74,28 @@ class PointwiseMap:
 
 @dataclass
 class OptimalScalarMap:
-    """bp::OptimalScalarMap (correction.hpp:20-23).  Not on the GPU yet: run() raises."""
+    """bp::OptimalScalarMap (correction.hpp:20-23): per-step least-squares gamma in the
+    Euclidean ("euclidean", the reference's default CBS map, bench.cpp:140-141) or the
+    R_eta ("reta") metric."""
     metric: str = "euclidean"
 
     def _c(self):
+        if self.metric not in ("euclidean", "reta"):
+            raise ValueError(f"unknown optimal-scalar metric {self.metric!r}")
         return N.Map(1, 0.0, 0.0, 0 if self.metric == "euclidean" else 1, None)
+
+
+class FourierDiagMap:
+    """bp::FourierDiagMap (correction.hpp:25-32): du = T^{-1}(m * T(x)) in the DST-I basis,
+    one multiplier m (nx x ny complex, mode layout) shared by the batch -- the learned M_theta
+    of the paper's NPBS in its desk-scale form.  The identity m == 1 is plain
+    preconditioned Richardson (make_identity_fourier_diag, correction.cpp:78-84)."""
+
+    def __init__(self, m):
+        self.m = np.ascontiguousarray(np.asarray(m, dtype=np.complex128))
+
+    def _c(self):
+        return N.Map(2, 0.0, 0.0, 0, _ptr(self.m))
 
 
 @dataclass

@@ -200,9 +200,10 @@ cudaError_t prepare_kernels(int log2n) {
     ColArgs c{};
     cudaError_t e = cudaSuccess;
     for (int pp : {8, 16}) {
-        for (int mode : {R_FWD, R_FWD_BORN, R_INV, R_SWEEP})
+        for (int mode : {R_FWD, R_FWD_BORN, R_INV, R_SWEEP, R_OPT_A, R_OPT_B, R_RETA_A, R_RETA_C,
+                         R_FD_A, R_FD_B})
             if (cudaError_t r = launch_row_pp(log2n, pp, mode, a, nullptr, true)) e = r;
-        for (int mode : {C_ONE, C_GREEN, C_LREF})
+        for (int mode : {C_ONE, C_GREEN, C_LREF, C_FD})
             if (cudaError_t r = launch_col_pp(log2n, pp, mode, c, nullptr, true)) e = r;
     }
     return e;
@@ -261,7 +262,9 @@ struct bp_problem {
     // workspace
     double2 *f = nullptr, *u0 = nullptr, *u1 = nullptr, *T = nullptr, *x = nullptr, *y = nullptr;
     double2* dense = nullptr;  // batch * nx*ny staging
-    double2* partial = nullptr;
+    double* partial = nullptr;
+    double2* gamma = nullptr;
+    double2* fd = nullptr;  // FourierDiag multiplier (padded n x n), uploaded per run
     double* norm_part = nullptr;
     double *fnorm_l2 = nullptr, *fnorm_reta = nullptr;
     int* ctl_int = nullptr;  // status, sweep, iters, term, result_buf, n_active
@@ -272,6 +275,7 @@ struct bp_problem {
     // graph cache
     cudaGraphExec_t graph = nullptr;
     int graph_map_kind = -1;
+    int graph_metric = -1;
     double2 graph_gamma{};
     int graph_max_iters = -1;
     double graph_rtol = -1;
@@ -308,6 +312,7 @@ Control make_control(const bp_problem* p) {
     c.n_active = ci + 5 * B;
     c.counter = p->counter;
     c.partial = p->partial;
+    c.gamma = p->gamma;
     c.fnorm_l2 = p->fnorm_l2;
     c.fnorm_reta = p->fnorm_reta;
     c.trace_l2 = p->trace_l2;
@@ -327,6 +332,7 @@ RowArgs row_args(const bp_problem* p) {
     a.T = p->T;
     a.u0 = p->u0;
     a.u1 = p->u1;
+    a.X = p->x;
     a.tw = p->tw;
     a.sinp = p->sinp;
     a.map_kind = MK_SCALAR;
@@ -342,6 +348,7 @@ ColArgs col_args(const bp_problem* p) {
     c.eta = p->eta;
     c.lap = p->lap;
     c.scale = p->green_scale;
+    c.fd = p->fd;
     c.T = p->T;
     c.tw = p->tw;
     c.sinp = p->sinp;
@@ -420,12 +427,53 @@ int ensure_trace(bp_problem* p, int max_iters) {
     return BP_OK;
 }
 
-int sweep_once(bp_problem* p, const RowArgs& a, const ColArgs& c, cudaEvent_t* ev) {
+// Launch sequence of one sweep per correction map (see RowMode in sweep_kernels.cuh).
+struct SweepPlan {
+    int n = 0;
+    bool row[5]{};
+    int mode[5]{};
+    void add(bool r, int md) {
+        row[n] = r;
+        mode[n++] = md;
+    }
+};
+
+SweepPlan plan_for(const bp_map* map) {
+    SweepPlan s;
+    switch (map->kind) {
+        case BP_MAP_OPTIMAL_SCALAR:
+            if (map->metric == BP_METRIC_RETA) {
+                s.add(true, R_RETA_A);
+                s.add(false, C_GREEN);
+                s.add(true, R_RETA_C);
+            } else {
+                s.add(true, R_OPT_A);
+            }
+            s.add(true, R_OPT_B);
+            s.add(false, C_GREEN);
+            break;
+        case BP_MAP_FOURIER_DIAG:
+            s.add(true, R_FD_A);
+            s.add(false, C_FD);
+            s.add(true, R_FD_B);
+            s.add(false, C_GREEN);
+            break;
+        default:  // scalar gamma or pointwise gamma(x): one fused row pass
+            s.add(true, R_SWEEP);
+            s.add(false, C_GREEN);
+    }
+    return s;
+}
+
+// ev (optional): plan.n + 1 events recorded around the launches
+int sweep_once(bp_problem* p, const SweepPlan& plan, const RowArgs& a, const ColArgs& c,
+               cudaEvent_t* ev) {
     if (ev) CU(cudaEventRecord(ev[0], p->stream));
-    CU(launch_row(p->log2n, R_SWEEP, a, p->stream));
-    if (ev) CU(cudaEventRecord(ev[1], p->stream));
-    CU(launch_col(p->log2n, C_GREEN, c, p->stream));
-    if (ev) CU(cudaEventRecord(ev[2], p->stream));
+    for (int k = 0; k < plan.n; ++k) {
+        if (plan.row[k]) CU(launch_row(p->log2n, plan.mode[k], a, p->stream));
+        else CU(launch_col(p->log2n, plan.mode[k], c, p->stream));
+        if (ev) CU(cudaEventRecord(ev[k + 1], p->stream));
+    }
     return BP_OK;
 }
 
@@ -440,6 +488,14 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     a.gamma = make_double2(map->gamma_re, map->gamma_im);
     ColArgs c = col_args(p);
     c.status = a.ctl.status;
+    const SweepPlan plan = plan_for(map);
+    if (map->kind == BP_MAP_FOURIER_DIAG) {
+        // one multiplier for the whole batch, reference mode layout -> padded
+        const size_t bytes = sizeof(double2) * (size_t)p->grid.nx * p->grid.ny;
+        CU(cudaMemcpyAsync(p->dense, map->m, bytes, cudaMemcpyHostToDevice, p->stream));
+        pack_kernel<<<grid_for(p->field), 256, 0, p->stream>>>(p->dense, p->fd, 1, p->log2n);
+        CU(cudaGetLastError());
+    }
 
     // fnorm_l2 = ||f||, fnorm_reta = ||G f||  (iterate.cpp:93,102)
     int rc = norms(p, p->f, p->fnorm_l2);
@@ -484,9 +540,9 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         // debug path: one sweep at a time, copying u^k after launch k
         long k = 0;
         for (k = 1; k <= max_launch; ++k) {
-            rc = sweep_once(p, a, c, nullptr);
+            rc = sweep_once(p, plan, a, c, nullptr);
             if (rc) return rc;
-            p->stat_launches += 2;
+            p->stat_launches += plan.n;
             if (k < n_snap) {
                 // u^k lives in buffer k&1 for every member still iterating
                 rc = download(p, (k & 1) ? p->u1 : p->u0, nullptr, nullptr,
@@ -501,26 +557,27 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     } else if (p->timing) {
         // instrumented path: CUDA events around every row / column launch on the handle's
         // stream, polled once per kGraphSweeps sweeps (same cadence as the graph path)
-        std::vector<cudaEvent_t> ev(3 * kGraphSweeps);
+        const int ne = plan.n + 1;
+        std::vector<cudaEvent_t> ev(ne * kGraphSweeps);
         for (auto& e : ev) CU(cudaEventCreate(&e));
         long launched = 0;
         while (launched < max_launch) {
             for (int s = 0; s < kGraphSweeps; ++s) {
-                rc = sweep_once(p, a, c, &ev[3 * s]);
+                rc = sweep_once(p, plan, a, c, &ev[ne * s]);
                 if (rc) break;
             }
             if (rc) break;
             launched += kGraphSweeps;
-            p->stat_launches += 2 * kGraphSweeps;
+            p->stat_launches += plan.n * kGraphSweeps;
             CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
                                p->stream));
             CU(cudaStreamSynchronize(p->stream));
             for (int s = 0; s < kGraphSweeps; ++s) {
-                float r = 0, cc = 0;
-                cudaEventElapsedTime(&r, ev[3 * s], ev[3 * s + 1]);
-                cudaEventElapsedTime(&cc, ev[3 * s + 1], ev[3 * s + 2]);
-                p->stat_row_ms += r;
-                p->stat_col_ms += cc;
+                for (int k = 0; k < plan.n; ++k) {
+                    float ms = 0;
+                    cudaEventElapsedTime(&ms, ev[ne * s + k], ev[ne * s + k + 1]);
+                    (plan.row[k] ? p->stat_row_ms : p->stat_col_ms) += ms;
+                }
                 ++p->stat_timed;
             }
             if (*p->host_active == 0) break;
@@ -530,6 +587,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     } else {
         // graph of kGraphSweeps sweeps, replayed until every member terminated
         const bool reuse = p->graph && p->graph_map_kind == map->kind &&
+                           p->graph_metric == map->metric &&
                            p->graph_gamma.x == map->gamma_re && p->graph_gamma.y == map->gamma_im &&
                            p->graph_max_iters == cfg->max_iters && p->graph_rtol == cfg->rtol;
         if (!reuse) {
@@ -537,14 +595,12 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             p->graph = nullptr;
             cudaGraph_t g;
             CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-            for (int s = 0; s < kGraphSweeps; ++s) {
-                launch_row(p->log2n, R_SWEEP, a, p->stream);
-                launch_col(p->log2n, C_GREEN, c, p->stream);
-            }
+            for (int s = 0; s < kGraphSweeps; ++s) sweep_once(p, plan, a, c, nullptr);
             CU(cudaStreamEndCapture(p->stream, &g));
             CU(cudaGraphInstantiate(&p->graph, g, 0));
             cudaGraphDestroy(g);
             p->graph_map_kind = map->kind;
+            p->graph_metric = map->metric;
             p->graph_gamma = a.gamma;
             p->graph_max_iters = cfg->max_iters;
             p->graph_rtol = cfg->rtol;
@@ -553,7 +609,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         while (launched < max_launch) {
             CU(cudaGraphLaunch(p->graph, p->stream));
             launched += kGraphSweeps;
-            p->stat_launches += 2 * kGraphSweeps;
+            p->stat_launches += plan.n * kGraphSweeps;
             CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
                                p->stream));
             CU(cudaStreamSynchronize(p->stream));
@@ -605,8 +661,13 @@ int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* c
     if (cfg->max_iters < 1) return set_err(BP_EINVAL, "run: max_iters must be >= 1");
     if (cfg->format != BP_FMT_NPBS && cfg->format != BP_FMT_CBS)
         return set_err(BP_ENOTSUP, "run: only the CBS / NPBS formats are implemented on the GPU");
-    if (map->kind != BP_MAP_SCALAR && map->kind != BP_MAP_POINTWISE)
-        return set_err(BP_ENOTSUP, "run: correction map not implemented on the GPU yet");
+    if (map->kind < BP_MAP_SCALAR || map->kind > BP_MAP_POINTWISE)
+        return set_err(BP_EINVAL, "unknown correction map");
+    if (map->kind == BP_MAP_FOURIER_DIAG && !map->m)
+        return set_err(BP_EINVAL, "FourierDiag correction: shape mismatch");
+    if (map->kind == BP_MAP_OPTIMAL_SCALAR && map->metric != BP_METRIC_EUCLIDEAN &&
+        map->metric != BP_METRIC_RETA)
+        return set_err(BP_EINVAL, "unknown optimal-scalar metric");
     return BP_OK;
 }
 
@@ -683,7 +744,9 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
     for (double2* buf : {p->k2, p->f, p->u0, p->u1, p->T, p->x, p->y})
         CUF(cudaMemsetAsync(buf, 0, fb, p->stream));
     CUF(cudaMalloc(&p->dense, sizeof(double2) * nd * batch));
-    CUF(cudaMalloc(&p->partial, sizeof(double2) * (size_t)batch * n));
+    CUF(cudaMalloc(&p->partial, sizeof(double) * (size_t)batch * n * kPartStride));
+    CUF(cudaMalloc(&p->gamma, sizeof(double2) * (size_t)batch));
+    CUF(cudaMalloc(&p->fd, sizeof(double2) * p->field));
     CUF(cudaMalloc(&p->norm_part, sizeof(double) * (size_t)batch * 64));
     CUF(cudaMalloc(&p->fnorm_l2, sizeof(double) * batch));
     CUF(cudaMalloc(&p->fnorm_reta, sizeof(double) * batch));
@@ -721,7 +784,7 @@ int bp_problem_destroy(bp_problem* p) {
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->graph) cudaGraphExecDestroy(p->graph);
     for (void* q : {(void*)p->k2, (void*)p->f, (void*)p->u0, (void*)p->u1, (void*)p->T, (void*)p->x,
-                    (void*)p->y, (void*)p->dense, (void*)p->partial, (void*)p->norm_part,
+                    (void*)p->y, (void*)p->dense, (void*)p->partial, (void*)p->gamma, (void*)p->fd, (void*)p->norm_part,
                     (void*)p->fnorm_l2, (void*)p->fnorm_reta, (void*)p->ctl_int, (void*)p->counter,
                     (void*)p->trace_l2, (void*)p->trace_reta, (void*)p->k0sq, (void*)p->eta,
                     (void*)p->tw, (void*)p->sinp, (void*)p->lap})

@@ -24,10 +24,44 @@
 
 namespace bs {
 
-enum RowMode { R_FWD = 0, R_FWD_BORN = 1, R_INV = 2, R_SWEEP = 3 };
-enum ColMode { C_ONE = 0, C_GREEN = 1, C_LREF = 2 };
+// Row-kernel modes.  Per sweep the driver launches (SC = scalar / pointwise map,
+// L2 / RE = OptimalScalar Euclidean / R_eta, FD = FourierDiag):
+//   SC: R_SWEEP, C_GREEN
+//   L2: R_OPT_A, R_OPT_B, C_GREEN
+//   RE: R_RETA_A, C_GREEN, R_RETA_C, R_OPT_B, C_GREEN
+//   FD: R_FD_A, C_FD, R_FD_B, C_GREEN
+enum RowMode {
+    R_FWD = 0,       // in -> forward y-DST -> T
+    R_FWD_BORN = 1,  // V in + f -> forward -> T
+    R_INV = 2,       // T -> inverse -> out (- sub)
+    R_SWEEP = 3,     // fused scalar/pointwise sweep (entry m, update, next source)
+    R_OPT_A = 4,     // entry m; x = r_bs -> X; <w,r>, |w|^2 with w = A x = r - V x -> gamma
+    R_OPT_B = 5,     // u' = u + gamma X; q = V u' + f -> forward -> T
+    R_RETA_A = 6,    // entry m; x = r_bs -> X; V x -> forward -> T (for G V x)
+    R_RETA_C = 7,    // T -> inverse = G V x; w = x - G V x; <w,x>, |w|^2 -> gamma
+    R_FD_A = 8,      // entry m; x = r_bs -> forward -> T (for the FourierDiag multiply)
+    R_FD_B = 9,      // T -> inverse = du; u' = u + du; q = V u' + f -> forward -> T
+};
+enum ColMode { C_ONE = 0, C_GREEN = 1, C_LREF = 2, C_FD = 3 };
 enum Status { ST_ACTIVE = 0, ST_DONE = 1 };
-enum MapKind { MK_SCALAR = 0, MK_POINTWISE = 3 };
+enum MapKind { MK_SCALAR = 0, MK_OPTIMAL = 1, MK_FOURIER_DIAG = 2, MK_POINTWISE = 3 };
+constexpr int kPartStride = 8;  // doubles of per-row partial sums
+
+template <int MODE>
+struct RowSpec {
+    static constexpr bool INV = MODE == R_INV || MODE == R_SWEEP || MODE == R_OPT_A ||
+                                MODE == R_RETA_A || MODE == R_RETA_C || MODE == R_FD_A || MODE == R_FD_B;
+    static constexpr bool FWD = MODE == R_FWD || MODE == R_FWD_BORN || MODE == R_SWEEP ||
+                                MODE == R_OPT_B || MODE == R_RETA_A || MODE == R_FD_A || MODE == R_FD_B;
+    // records trace entry m = sweep[b] (and the termination test)
+    static constexpr bool ENTRY = MODE == R_SWEEP || MODE == R_OPT_A || MODE == R_RETA_A || MODE == R_FD_A;
+    // runs after the entry of this sweep was recorded: m = sweep[b] - 1
+    static constexpr bool POST = MODE == R_OPT_B || MODE == R_RETA_C || MODE == R_FD_B;
+    static constexpr bool ITER = ENTRY || POST;
+    static constexpr bool GAMMA = MODE == R_OPT_A || MODE == R_RETA_C;  // reduces a gamma
+    static constexpr int NPART = MODE == R_OPT_A ? 5 : MODE == R_RETA_C ? 3 : ENTRY ? 2 : 0;
+    static constexpr bool UPDATE = MODE == R_SWEEP || MODE == R_OPT_B || MODE == R_FD_B;
+};
 
 struct Control {
     int* status;          // [batch]
@@ -37,7 +71,8 @@ struct Control {
     int* term;            // [batch]
     int* result_buf;      // [batch] ping-pong index holding the result
     int* n_active;        // [1]
-    double2* partial;     // [batch][n] per-row (||r||^2, ||r_bs||^2)
+    double* partial;      // [batch][n][kPartStride] per-row partial sums
+    double2* gamma;       // [batch] optimal-scalar gamma of the current sweep
     const double* fnorm_l2;
     const double* fnorm_reta;
     double* trace_l2;     // [batch][max_iters+1]
@@ -58,8 +93,9 @@ struct RowArgs {
     double2* out;              // R_INV output (padded)
     const double2* sub;        // R_INV: optional field subtracted from the output
     double2* T;                // intermediate (padded)
-    double2* u0;               // R_SWEEP ping
-    double2* u1;               // R_SWEEP pong
+    double2* u0;               // iterate ping
+    double2* u1;               // iterate pong
+    double2* X;                // direction x^m (optimal-scalar / FourierDiag modes)
     const double2* tw;         // exp(-2 pi i k/n), k < n
     const double* sinp;        // sin(pi j/n), j < n
     int map_kind;
@@ -72,7 +108,8 @@ struct ColArgs {
     const double* k0sq;
     const double* eta;
     const double* lap;         // (4/h^2) sin^2(j pi / (2n)), j < n
-    double scale;              // C_ONE scale / Green normalisation 4/n^2
+    double scale;              // C_ONE scale / Green normalisation 4/n^2 (/ engine gain)
+    const double2* fd;         // C_FD: FourierDiag multiplier, padded n x n (shared by the batch)
     double2* T;
     const double2* tw;
     const double* sinp;
@@ -116,7 +153,14 @@ static __device__ void finalize_entry(const Control& c, int b, int m, double sum
         atomicSub(c.n_active, 1);
     }
     c.sweep[b] = m + 1;
-    c.counter[b] = 0u;
+}
+
+// optimal_scalar (proj/src/correction.cpp:10-18): <w, r> / <w, w>, 0 on a zero / non-finite
+// denominator.  num = sum conj(w) r.
+static __device__ void finalize_gamma(const Control& c, int b, double num_re, double num_im, double den) {
+    double2 g = make_double2(0.0, 0.0);
+    if (den > 0.0 && isfinite(den)) g = make_double2(num_re / den, num_im / den);
+    c.gamma[b] = g;
 }
 
 // ------------------------------------------------------------------ row kernel
@@ -169,21 +213,21 @@ row_kernel(const RowArgs a) {
     using RG = RowGeom<LOG2N, PP, NW>;
     using Pol = typename PolicyFor<G::T>::type;
     using Engine = DstEngine<LOG2N, PP>;
+    using S = RowSpec<MODE>;
     constexpr int N = G::N, P = G::P, T = G::T;
     constexpr int EPB = RG::EPB;
     extern __shared__ double2 smem[];
 
-    const int lane = threadIdx.x & 31;
     const int t = threadIdx.x % T;
     const int e = threadIdx.x / T;
     const long grow = (long)blockIdx.x * EPB + e;
     const int b = (int)(grow >> LOG2N);
     const int i = (int)(grow & (N - 1));
     bool valid = (b < a.batch) && (i != 0);
-    int m = 0;
-    if (MODE == R_SWEEP && valid) {
+    int m = 0;  // trace entry this launch belongs to
+    if (S::ITER && valid) {
         valid = __ldcg(&a.ctl.status[b]) == ST_ACTIVE;
-        m = __ldcg(&a.ctl.sweep[b]);
+        m = __ldcg(&a.ctl.sweep[b]) - (S::POST ? 1 : 0);
     }
     if (!__syncthreads_or(valid)) return;
 
@@ -192,28 +236,34 @@ row_kernel(const RowArgs a) {
     const size_t mem = (size_t)(valid ? b : 0) * N * N;
     const size_t row = mem + (size_t)(valid ? i : 0) * N;
     const double2 zero = make_double2(0.0, 0.0);
-    (void)lane;
+    const double2* ucur = (m & 1) ? a.u1 : a.u0;  // u^m
+    double2* unext = (m & 1) ? a.u0 : a.u1;       // u^{m+1}
+    const double k0sq = valid ? a.k0sq[b] : 0.0;
+    const double eta = valid ? a.eta[b] : 1.0;
+    const double2 shift = make_double2(k0sq, eta);
 
-    if constexpr (MODE == R_SWEEP) {
+    if constexpr (S::ITER && MODE != R_RETA_C) {
         // Stage the element-wise operands of this row (and the stencil halo rows at the CTA's
-        // edges) into L2 while the inverse transform runs: the loads after the engine then hit
-        // L2 instead of waiting on DRAM with few registers to spare for outstanding loads.
+        // edges) into L2 while the transform runs: the loads after the engine then hit L2.
         if (valid && t == 0) {
-            const double2* ucur = (m & 1) ? a.u1 : a.u0;
             constexpr unsigned RB = N * sizeof(double2);
             prefetch_l2(ucur + row, RB);
             prefetch_l2(a.k2 + row, RB);
             prefetch_l2(a.f + row, RB);
-            if (e == 0) prefetch_l2(ucur + row - N, RB);
-            if (e == EPB - 1) prefetch_l2(ucur + row + N, RB);
+            if constexpr (S::ENTRY) {
+                if (e == 0) prefetch_l2(ucur + row - N, RB);
+                if (e == EPB - 1) prefetch_l2(ucur + row + N, RB);
+            }
+            if constexpr (MODE == R_OPT_B) prefetch_l2(a.X + row, RB);
         }
     }
 
-    double2 q[P];
-    double acc_l2 = 0.0, acc_reta = 0.0;
+    double2 q[P];                    // source of the forward transform
+    double acc[S::NPART > 0 ? S::NPART : 1] = {};
 
-    if constexpr (MODE == R_INV || MODE == R_SWEEP) {
-        // ---- inverse y-DST of the column-pass output
+    // ---- inverse y-DST of the column-pass output, staged to the stride layout
+    double2 z[P];
+    if constexpr (S::INV) {
         double2 x[P], xm[P], y[P];
 #pragma unroll
         for (int mm = 0; mm < P; ++mm) {
@@ -222,115 +272,146 @@ row_kernel(const RowArgs a) {
             xm[mm] = (valid && j != 0) ? a.T[row + (N - j)] : zero;  // mirror: L1 hit
         }
         Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
-        // stage through smem: contiguous -> stride layout (coalesced global access)
 #pragma unroll
         for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
         pol.sync();
-        double2 z[P];
 #pragma unroll
         for (int mm = 0; mm < P; ++mm) z[mm] = buf[G::pidx(t + T * mm)];
         pol.sync();
+    }
 
+    // ---- element-wise phase
+#pragma unroll
+    for (int mm = 0; mm < P; ++mm) {
+        const int j = t + T * mm;
         if constexpr (MODE == R_INV) {
-#pragma unroll
-            for (int mm = 0; mm < P; ++mm) {
-                const int j = t + T * mm;
-                double2 o = z[mm];
-                if (a.sub) o = csub(o, valid ? a.sub[row + j] : zero);
-                if (valid) a.out[row + j] = (j == 0) ? zero : o;
+            double2 o = z[mm];
+            if (a.sub) o = csub(o, valid ? a.sub[row + j] : zero);
+            if (valid) a.out[row + j] = (j == 0) ? zero : o;
+        } else if constexpr (MODE == R_FWD) {
+            const double2 v = valid ? a.in[row + j] : zero;
+            q[mm] = (j == 0) ? zero : v;
+        } else if constexpr (MODE == R_FWD_BORN) {
+            const double2 v = valid ? a.in[row + j] : zero;
+            const double2 V = csub(valid ? a.k2[row + j] : zero, shift);
+            const double2 o = cadd(cmul(v, V), valid ? a.f[row + j] : zero);  // mul(u, v) + f
+            q[mm] = (j == 0) ? zero : o;
+        } else if constexpr (MODE == R_RETA_C) {
+            // z = G V x: w = x - G V x (correction.cpp:38-44); gamma = <w, x> / <w, w>
+            const double2 x = valid ? a.X[row + j] : zero;
+            const double2 w = csub(x, z[mm]);
+            if (j != 0) {
+                acc[0] += w.x * x.x + w.y * x.y;  // Re conj(w) x
+                acc[1] += w.x * x.y - w.y * x.x;  // Im conj(w) x
+                acc[2] += cnorm(w);
             }
-            return;
         } else {
-            // ---- fused Born update, residual norms, next source term
-            const double2* ucur = (m & 1) ? a.u1 : a.u0;
-            double2* unext = (m & 1) ? a.u0 : a.u1;
-            const double k0sq = valid ? a.k0sq[b] : 0.0;
-            const double eta = valid ? a.eta[b] : 1.0;
-            const double2 shift = make_double2(k0sq, eta);
-            const double inv_h2 = a.inv_h2;
-#pragma unroll
-            for (int mm = 0; mm < P; ++mm) {
-                const int j = t + T * mm;
-                double2 u = zero, k2 = zero, f = zero, un = zero, us = zero, uw = zero, ue = zero;
+            double2 u = zero, k2 = zero, f = zero;
+            if (valid) {
+                u = ucur[row + j];
+                k2 = a.k2[row + j];
+                f = a.f[row + j];
+            }
+            const double2 V = csub(k2, shift);
+            if constexpr (S::ENTRY) {
+                // r^m = f - A u^m (five-point in proj/src/kernels.cpp:56-69 order);
+                // x^m = G q^m - u^m = born_residual (problem.cpp:41-49) = G r^m (key identity)
+                double2 un = zero, us = zero, uw = zero, ue = zero;
                 if (valid) {
-                    u = ucur[row + j];
-                    k2 = a.k2[row + j];
-                    f = a.f[row + j];
                     un = ucur[row - N + j];
                     us = ucur[row + N + j];
                     if (j > 0) uw = ucur[row + j - 1];
                     if (j + 1 < N) ue = ucur[row + j + 1];
                 }
-                const double2 V = csub(k2, shift);
-                const double2 rb = csub(z[mm], u);
-                // five-point (proj/src/kernels.cpp:56-69 order) and A u = L_D u - k2 u
+                const double2 x = csub(z[mm], u);
                 double2 s = cscale(u, 4.0);
                 s = csub(s, un);
                 s = csub(s, us);
                 s = csub(s, uw);
                 s = csub(s, ue);
-                const double2 au = csub(cscale(s, inv_h2), cmul(k2, u));
-                const double2 r = csub(f, au);
+                const double2 r = csub(f, csub(cscale(s, a.inv_h2), cmul(k2, u)));
                 if (j != 0) {
-                    acc_reta += cnorm(rb);
-                    acc_l2 += cnorm(r);
+                    acc[0] += cnorm(r);
+                    acc[1] += cnorm(x);
                 }
-                double2 g = a.gamma;
-                if (a.map_kind == MK_POINTWISE) g = cscale(mul_pi(V), 1.0 / eta);  // (i/eta) V
-                double2 unew = cadd(u, cmul(g, rb));
+                if constexpr (MODE == R_SWEEP) {
+                    double2 g = a.gamma;
+                    if (a.map_kind == MK_POINTWISE) g = cscale(mul_pi(V), 1.0 / eta);  // (i/eta) V
+                    double2 unew = cadd(u, cmul(g, x));
+                    if (j == 0) unew = zero;
+                    if (valid) unext[row + j] = unew;
+                    q[mm] = cadd(cmul(V, unew), f);
+                } else if constexpr (MODE == R_OPT_A) {
+                    // w = A x = (L_ref - V) G r = r - V x (key identity; the reference applies
+                    // A by stencil, correction.cpp:33-36 -- equal to roundoff)
+                    const double2 w = csub(r, cmul(V, x));
+                    if (j != 0) {
+                        acc[2] += w.x * r.x + w.y * r.y;
+                        acc[3] += w.x * r.y - w.y * r.x;
+                        acc[4] += cnorm(w);
+                    }
+                    if (valid) a.X[row + j] = (j == 0) ? zero : x;
+                } else if constexpr (MODE == R_RETA_A) {
+                    if (valid) a.X[row + j] = (j == 0) ? zero : x;
+                    q[mm] = (j == 0) ? zero : cmul(x, V);  // apply_V(x)
+                } else {  // R_FD_A: forward transform of the direction itself
+                    q[mm] = (j == 0) ? zero : x;
+                }
+            } else {
+                // R_OPT_B: u' = u + gamma x ; R_FD_B: u' = u + du (du = z)
+                double2 du;
+                if constexpr (MODE == R_OPT_B) {
+                    const double2 x = valid ? a.X[row + j] : zero;
+                    const double2 g = valid ? a.ctl.gamma[b] : zero;
+                    du = cmul(g, x);  // kernels::scale(x, gamma)
+                } else {
+                    du = z[mm];
+                }
+                double2 unew = cadd(u, du);
                 if (j == 0) unew = zero;
                 if (valid) unext[row + j] = unew;
                 q[mm] = cadd(cmul(V, unew), f);
             }
         }
-    } else {
-        // ---- R_FWD / R_FWD_BORN: source of the forward transform
-        const double k0sq = valid ? a.k0sq[b] : 0.0;
-        const double eta = valid ? a.eta[b] : 1.0;
-        const double2 shift = make_double2(k0sq, eta);
+    }
+    if constexpr (MODE == R_INV) return;
+
+    // ---- forward y-DST of q (mirror by warp shuffles, or shared memory for multi-warp rows)
+    if constexpr (S::FWD) {
+        double2 qm[P], y2[P];
+#if BS_SHFL_MIRROR
+        pol.mirror(q, qm, t, buf, typename G::Pidx{});
+#else
+#pragma unroll
+        for (int mm = 0; mm < P; ++mm) buf[G::pidx(t + T * mm)] = q[mm];
+        pol.sync();
 #pragma unroll
         for (int mm = 0; mm < P; ++mm) {
             const int j = t + T * mm;
-            double2 v = valid ? a.in[row + j] : zero;
-            if constexpr (MODE == R_FWD_BORN) {
-                const double2 V = csub(valid ? a.k2[row + j] : zero, shift);
-                v = cadd(cmul(v, V), valid ? a.f[row + j] : zero);  // kernels::mul(u, v) then add f
-            }
-            q[mm] = (j == 0) ? zero : v;
+            qm[mm] = (j == 0) ? zero : buf[G::pidx(N - j)];
+        }
+        pol.sync();
+#endif
+        Engine::run(q, qm, y2, t, buf, a.tw, a.sinp, pol);
+#pragma unroll
+        for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y2[l];
+        pol.sync();
+#pragma unroll
+        for (int mm = 0; mm < P; ++mm) {
+            const int j = t + T * mm;
+            if (valid) a.T[row + j] = buf[G::pidx(j)];
         }
     }
 
-    // ---- forward y-DST of q (mirror by warp shuffles, or shared memory for multi-warp rows)
-    double2 qm[P], y2[P];
-#if BS_SHFL_MIRROR
-    pol.mirror(q, qm, t, buf, typename G::Pidx{});
-#else
+    // ---- per-row partials; the last row of the member finalises (deterministic order)
+    if constexpr (S::NPART > 0) {
 #pragma unroll
-    for (int mm = 0; mm < P; ++mm) buf[G::pidx(t + T * mm)] = q[mm];
-    pol.sync();
-#pragma unroll
-    for (int mm = 0; mm < P; ++mm) {
-        const int j = t + T * mm;
-        qm[mm] = (j == 0) ? zero : buf[G::pidx(N - j)];
-    }
-    pol.sync();
-#endif
-    Engine::run(q, qm, y2, t, buf, a.tw, a.sinp, pol);
-#pragma unroll
-    for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y2[l];
-    pol.sync();
-#pragma unroll
-    for (int mm = 0; mm < P; ++mm) {
-        const int j = t + T * mm;
-        if (valid) a.T[row + j] = buf[G::pidx(j)];
-    }
-
-    if constexpr (MODE == R_SWEEP) {
-        acc_l2 = pol.sum(acc_l2, t);
-        acc_reta = pol.sum(acc_reta, t);
+        for (int k = 0; k < S::NPART; ++k) acc[k] = pol.sum(acc[k], t);
         int last = 0;
         if (valid && t == 0) {
-            a.ctl.partial[(size_t)b * N + i] = make_double2(acc_l2, acc_reta);
+            double* pr = a.ctl.partial + ((size_t)b * N + i) * kPartStride;
+#pragma unroll
+            for (int k = 0; k < S::NPART; ++k) pr[k] = acc[k];
             __threadfence();
             const unsigned old = atomicAdd(&a.ctl.counter[b], 1u);
             last = (old == (unsigned)(N - 2));
@@ -338,15 +419,22 @@ row_kernel(const RowArgs a) {
         last = pol.bcast0(last, t);
         if (last) {
             __threadfence();
-            double s1 = 0.0, s2 = 0.0;
+            double s[S::NPART];
+#pragma unroll
+            for (int k = 0; k < S::NPART; ++k) s[k] = 0.0;
             for (int r = 1 + t; r < N; r += T) {
-                const double2 pr = ldcg2(&a.ctl.partial[(size_t)b * N + r]);
-                s1 += pr.x;
-                s2 += pr.y;
+                const double* pr = a.ctl.partial + ((size_t)b * N + r) * kPartStride;
+#pragma unroll
+                for (int k = 0; k < S::NPART; ++k) s[k] += __ldcg(pr + k);
             }
-            s1 = pol.sum(s1, t);
-            s2 = pol.sum(s2, t);
-            if (t == 0) finalize_entry(a.ctl, b, m, s1, s2);
+#pragma unroll
+            for (int k = 0; k < S::NPART; ++k) s[k] = pol.sum(s[k], t);
+            if (t == 0) {
+                a.ctl.counter[b] = 0u;
+                if constexpr (MODE == R_OPT_A) finalize_gamma(a.ctl, b, s[2], s[3], s[4]);
+                if constexpr (MODE == R_RETA_C) finalize_gamma(a.ctl, b, s[0], s[1], s[2]);
+                if constexpr (S::ENTRY) finalize_entry(a.ctl, b, m, s[0], s[1]);
+            }
         }
     }
 }
@@ -400,7 +488,9 @@ col_kernel(const ColArgs a) {
             const double lr = (a.lap[p] + lq) - k0sq;
             const double li = -eta;
             double2 w;
-            if constexpr (MODE == C_GREEN) {
+            if constexpr (MODE == C_FD) {
+                w = cscale(a.fd[(size_t)p * N + q], a.scale);  // FourierDiag m_pq (correction.cpp:63-68)
+            } else if constexpr (MODE == C_GREEN) {
                 const double s = a.scale * __drcp_rn(fma(lr, lr, li * li));
                 w = make_double2(lr * s, -li * s);  // scale / lambda
             } else {

@@ -36,7 +36,13 @@ cudaError_t launch_row_p(int mode, const RowArgs& a, cudaStream_t s, bool prepar
         case R_FWD: return launch_row_t<L, R_FWD, PP>(a, s, prepare);
         case R_FWD_BORN: return launch_row_t<L, R_FWD_BORN, PP>(a, s, prepare);
         case R_INV: return launch_row_t<L, R_INV, PP>(a, s, prepare);
-        default: return launch_row_t<L, R_SWEEP, PP>(a, s, prepare);
+        case R_SWEEP: return launch_row_t<L, R_SWEEP, PP>(a, s, prepare);
+        case R_OPT_A: return launch_row_t<L, R_OPT_A, PP>(a, s, prepare);
+        case R_OPT_B: return launch_row_t<L, R_OPT_B, PP>(a, s, prepare);
+        case R_RETA_A: return launch_row_t<L, R_RETA_A, PP>(a, s, prepare);
+        case R_RETA_C: return launch_row_t<L, R_RETA_C, PP>(a, s, prepare);
+        case R_FD_A: return launch_row_t<L, R_FD_A, PP>(a, s, prepare);
+        default: return launch_row_t<L, R_FD_B, PP>(a, s, prepare);
     }
 }
 
@@ -45,6 +51,7 @@ cudaError_t launch_col_p(int mode, const ColArgs& a, cudaStream_t s, bool prepar
     switch (mode) {
         case C_ONE: return launch_col_t<L, C_ONE, PP>(a, s, prepare);
         case C_GREEN: return launch_col_t<L, C_GREEN, PP>(a, s, prepare);
+        case C_FD: return launch_col_t<L, C_FD, PP>(a, s, prepare);
         default: return launch_col_t<L, C_LREF, PP>(a, s, prepare);
     }
 }

@@ -11,7 +11,8 @@ import pytest
 
 from conftest import GOLDEN
 import paper_2603_18527_b200 as bs
-from oracle import MAP_POINTWISE, MAP_SCALAR, Oracle, OracleProblem
+from oracle import (MAP_FOURIER_DIAG, MAP_OPTIMAL_SCALAR, MAP_POINTWISE, MAP_SCALAR, Oracle,
+                    OracleProblem)
 
 pytestmark = pytest.mark.gpu
 
@@ -127,6 +128,12 @@ def _oracle_run(k2, f, k0, eta, cmap, rtol, max_iters, u0=None, n_snap=0):
     o = OracleProblem(k2, k0, eta)
     if isinstance(cmap, bs.PointwiseMap):
         return o.run(f, map_kind=MAP_POINTWISE, rtol=rtol, max_iters=max_iters, u0=u0, n_snap=n_snap)
+    if isinstance(cmap, bs.OptimalScalarMap):
+        return o.run(f, map_kind=MAP_OPTIMAL_SCALAR, metric=0 if cmap.metric == "euclidean" else 1,
+                     rtol=rtol, max_iters=max_iters, u0=u0, n_snap=n_snap)
+    if isinstance(cmap, bs.FourierDiagMap):
+        return o.run(f, map_kind=MAP_FOURIER_DIAG, m=cmap.m, rtol=rtol, max_iters=max_iters, u0=u0,
+                     n_snap=n_snap)
     return o.run(f, map_kind=MAP_SCALAR, gamma=cmap.gamma, rtol=rtol, max_iters=max_iters, u0=u0,
                  n_snap=n_snap)
 
@@ -147,6 +154,8 @@ RUN_FIXTURES = {
     "c0like_n32_scalar": lambda g: bs.ScalarMap(complex(g["gamma"])),
     "n32_pointwise": lambda g: bs.PointwiseMap(),
     "n32_scalar_maxiters": lambda g: bs.ScalarMap(complex(g["gamma"])),
+    "n16_optl2": lambda g: bs.OptimalScalarMap("euclidean"),
+    "n16_optreta": lambda g: bs.OptimalScalarMap("reta"),
 }
 
 
@@ -166,12 +175,24 @@ def test_run_matches_reference_fixture(gpu, name):
         assert rel(res.u, g["u"]) < FIELD_TOL
 
 
+def _fd_map(n, seed=5):
+    """random-init FourierDiag multiplier near the identity (the NPBS M_theta stand-in)"""
+    rng = np.random.default_rng(seed)
+    nd = n - 1
+    return bs.FourierDiagMap(1.0 + 0.3 * (rng.standard_normal((nd, nd)) + 1j * rng.standard_normal((nd, nd))))
+
+
 @pytest.mark.parametrize("n,cmap", [(32, bs.ScalarMap(1.0)), (64, bs.PointwiseMap()),
-                                    (128, bs.ScalarMap(1.0)), (256, bs.PointwiseMap())])
+                                    (128, bs.ScalarMap(1.0)), (256, bs.PointwiseMap()),
+                                    (64, bs.OptimalScalarMap("euclidean")),
+                                    (128, bs.OptimalScalarMap("reta")),
+                                    (64, "fd"), (512, bs.OptimalScalarMap("euclidean"))])
 def test_per_iterate_parity(gpu, n, cmap):
     """u^m for m = 0..K within 1e-10 relative L2 of the oracle's iterates."""
+    if cmap == "fd":
+        cmap = _fd_map(n)
     k2, f, k0, eta = instance(n, ppw=10.0, contrast=0.3, seed=2)
-    K = 40
+    K = 40 if n < 512 else 12
     cfg = bs.IterationConfig(rtol=1e-12, max_iters=K)
     with bs.HelmholtzDirichlet(k2, k0, eta) as p:
         res = bs.run(p, cmap, f, cfg, n_snap=K + 1)
@@ -269,8 +290,8 @@ def test_errors_follow_reference(gpu):
             bs.run(p, bs.ScalarMap(), f, bs.IterationConfig(rtol=0.0))
         with pytest.raises(ValueError, match="max_iters"):
             bs.run(p, bs.ScalarMap(), f, bs.IterationConfig(max_iters=0))
-        with pytest.raises(NotImplementedError):
-            bs.run(p, bs.OptimalScalarMap(), f)
+        with pytest.raises(ValueError, match="metric"):
+            bs.run(p, bs.OptimalScalarMap("bogus"), f)
         with pytest.raises(ValueError, match="shape"):
             p.apply_G(np.zeros((3, 3), np.complex128))
     with pytest.raises(ValueError, match="eta"):
@@ -287,3 +308,27 @@ def test_cbs_equals_npbs_on_gpu(gpu):
         a = bs.run(p, bs.ScalarMap(1.0), f, bs.IterationConfig(format="cbs", rtol=1e-12, max_iters=50))
         b = bs.run(p, bs.ScalarMap(1.0), f, bs.IterationConfig(format="npbs", rtol=1e-12, max_iters=50))
     assert rel(a.u, b.u) < 1e-12
+
+
+def test_config0_full_solve_optimal_scalar(gpu):
+    """Config 0 with the reference's default CBS map, OptimalScalar-L2 (bench.cpp:140-141)."""
+    cfg0 = bs.CONFIGS["c0"]
+    k2, f, k0, eta = bs.make_instances(cfg0["spec"], 0, 1)
+    cmap = bs.OptimalScalarMap("euclidean")
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        res = bs.run(p, cmap, f, bs.IterationConfig(rtol=cfg0["rtol"], max_iters=20000))
+    ref = _oracle_run(k2[0], f[0], k0[0], eta[0], cmap, cfg0["rtol"], 20000)
+    assert ref.terminated == "converged"
+    assert_run_parity(res.trace, res.u, ref)
+
+
+@pytest.mark.parametrize("kind", ["reta", "fd"])
+def test_other_maps_full_solve(gpu, kind):
+    k2, f, k0, eta = instance(64, ppw=10.0, contrast=0.3, seed=7)
+    cmap = bs.OptimalScalarMap("reta") if kind == "reta" else _fd_map(64, seed=1)
+    if kind == "fd":  # a contracting multiplier: identity scaled into the CBS-stable range
+        cmap = bs.FourierDiagMap(np.full((63, 63), 0.9 + 0.0j))
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        res = bs.run(p, cmap, f, bs.IterationConfig(rtol=1e-8, max_iters=5000))
+    ref = _oracle_run(k2[0], f[0], k0[0], eta[0], cmap, 1e-8, 5000)
+    assert_run_parity(res.trace, res.u, ref)
