@@ -15,7 +15,7 @@
  *   grid     DirichletInterior, h = lx/(nx+1) (proj/include/bp/grid.hpp:12-24).
  *   DST-I    forward = plain sine sum, inverse carries 4/((nx+1)(ny+1))
  *            (proj/include/bp/transforms.hpp:15-24).
- * Supported on the GPU: square grids with nx+1 = ny+1 = 2^k, 8 <= 2^k <= 512
+ * Supported on the GPU: square grids with nx+1 = ny+1 = 2^k, 8 <= 2^k <= 4096
  * (other shapes return BP_ENOTSUP; the reference accepts any size through FFTW).
  *
  * Errors: every function returns a status; nothing throws across the boundary.

@@ -151,7 +151,7 @@ __global__ void fill_nan_kernel(double* p, size_t n) {
 }
 
 // ------------------------------------------------------------------ launch tables
-constexpr int kMinLog2 = 3, kMaxLog2 = 9;
+constexpr int kMinLog2 = 3, kMaxLog2 = 12;
 
 // points per thread of the DST-I engine per size (8 or 16; BP_POINTS_PER_THREAD overrides)
 int points_per_thread(int log2n) {
@@ -172,6 +172,9 @@ cudaError_t launch_row_pp(int log2n, int pp, int mode, const RowArgs& a, cudaStr
         case 7: return launch_row_L7(pp, mode, a, s, prep);
         case 8: return launch_row_L8(pp, mode, a, s, prep);
         case 9: return launch_row_L9(pp, mode, a, s, prep);
+        case 10: return launch_row_L10(pp, mode, a, s, prep);
+        case 11: return launch_row_L11(pp, mode, a, s, prep);
+        case 12: return launch_row_L12(pp, mode, a, s, prep);
     }
     return cudaErrorInvalidValue;
 }
@@ -184,6 +187,9 @@ cudaError_t launch_col_pp(int log2n, int pp, int mode, const ColArgs& a, cudaStr
         case 7: return launch_col_L7(pp, mode, a, s, prep);
         case 8: return launch_col_L8(pp, mode, a, s, prep);
         case 9: return launch_col_L9(pp, mode, a, s, prep);
+        case 10: return launch_col_L10(pp, mode, a, s, prep);
+        case 11: return launch_col_L11(pp, mode, a, s, prep);
+        case 12: return launch_col_L12(pp, mode, a, s, prep);
     }
     return cudaErrorInvalidValue;
 }
@@ -692,7 +698,7 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
     int log2n = 0;
     while ((1 << log2n) < n) ++log2n;
     if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > kMaxLog2)
-        return set_err(BP_ENOTSUP, "GPU path needs square grids with nx+1 = 2^k, 8 <= 2^k <= 512");
+        return set_err(BP_ENOTSUP, "GPU path needs square grids with nx+1 = 2^k, 8 <= 2^k <= 4096");
     if (grid->lx != grid->ly) return set_err(BP_ENOTSUP, "GPU path needs lx == ly (hx == hy)");
     const size_t nd = (size_t)grid->nx * grid->ny;
     for (int b = 0; b < batch; ++b) {

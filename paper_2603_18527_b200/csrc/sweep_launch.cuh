@@ -7,7 +7,12 @@
 namespace bs {
 
 constexpr int kRowWarps = 8;   // warps per row-kernel CTA
-constexpr int kColCols = 8;    // columns per column-kernel CTA (128-B row segments)
+// columns per column-kernel CTA: 8 (128-B row segments) while a CTA of 8 lines fits; long
+// lines (n >= 1024) hold fewer columns per CTA so the shared-memory lines still fit
+template <int L>
+struct ColCols {
+    static constexpr int value = L <= 9 ? 8 : (L == 10 ? 4 : 2);
+};
 
 template <int L, int MODE, int PP>
 cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
@@ -22,10 +27,11 @@ cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
 
 template <int L, int MODE, int PP>
 cudaError_t launch_col_t(const ColArgs& a, cudaStream_t s, bool prepare) {
-    using CG = ColGeom<L, PP, kColCols>;
-    auto k = col_kernel<L, MODE, kColCols, PP>;
+    constexpr int C = ColCols<L>::value;
+    using CG = ColGeom<L, PP, C>;
+    auto k = col_kernel<L, MODE, C, PP>;
     if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
-    const int grid = a.batch * ((1 << L) / kColCols);
+    const int grid = a.batch * ((1 << L) / C);
     k<<<grid, CG::THREADS, CG::SMEM, s>>>(a);
     return cudaGetLastError();
 }
@@ -60,13 +66,19 @@ cudaError_t launch_col_p(int mode, const ColArgs& a, cudaStream_t s, bool prepar
 cudaError_t launch_row_size(int log2n, int pp, int mode, const RowArgs& a, cudaStream_t s, bool prepare);
 cudaError_t launch_col_size(int log2n, int pp, int mode, const ColArgs& a, cudaStream_t s, bool prepare);
 
+// P = 8 needs T = n/8 <= 256 threads per line; longer lines always use P = 16
+template <int L>
+struct Pp8 {
+    static constexpr int value = ((1 << L) / 8 <= 256) ? 8 : 16;
+};
+
 #define BS_DEFINE_SIZE(L)                                                                        \
     cudaError_t launch_row_L##L(int pp, int mode, const RowArgs& a, cudaStream_t s, bool prep) {  \
-        if (pp == 8) return launch_row_p<L, 8>(mode, a, s, prep);                                \
+        if (pp == 8) return launch_row_p<L, Pp8<L>::value>(mode, a, s, prep);                    \
         return launch_row_p<L, 16>(mode, a, s, prep);                                            \
     }                                                                                            \
     cudaError_t launch_col_L##L(int pp, int mode, const ColArgs& a, cudaStream_t s, bool prep) {  \
-        if (pp == 8) return launch_col_p<L, 8>(mode, a, s, prep);                                \
+        if (pp == 8) return launch_col_p<L, Pp8<L>::value>(mode, a, s, prep);                    \
         return launch_col_p<L, 16>(mode, a, s, prep);                                            \
     }
 
@@ -81,5 +93,8 @@ BS_DECLARE_SIZE(6)
 BS_DECLARE_SIZE(7)
 BS_DECLARE_SIZE(8)
 BS_DECLARE_SIZE(9)
+BS_DECLARE_SIZE(10)
+BS_DECLARE_SIZE(11)
+BS_DECLARE_SIZE(12)
 
 }  // namespace bs

@@ -46,6 +46,9 @@ CONFIGS = {
     # c1: 64 independent media on 512x512, contrast 0.5, 8 ppw, pointwise gamma(x) = iV/eta
     "c1": dict(spec=InstanceSpec(n=512, ppw=8.0, contrast=0.5), batch=64, map="pointwise",
                rtol=1e-6),
+    # c2: one high-frequency 4096x4096 grid, 6 ppw, contrast 0.5, 16 seeded point sources
+    "c2": dict(spec=InstanceSpec(n=4096, ppw=6.0, contrast=0.5, n_sources=16), batch=1,
+               map="pointwise", rtol=1e-6),
 }
 
 

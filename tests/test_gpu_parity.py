@@ -62,7 +62,7 @@ def test_transforms_match_scipy_goldens(gpu):
 
 
 def test_unsupported_shapes_raise(gpu):
-    for shape in [(16, 12), (3, 5), (14, 14), (1023, 1023)]:
+    for shape in [(16, 12), (3, 5), (14, 14), (1022, 1022), (8191, 8191)]:
         with pytest.raises(NotImplementedError):
             bs.HelmholtzDirichlet(np.ones(shape, np.complex128), 1.0, 1.0)
 
@@ -331,4 +331,46 @@ def test_other_maps_full_solve(gpu, kind):
     with bs.HelmholtzDirichlet(k2, k0, eta) as p:
         res = bs.run(p, cmap, f, bs.IterationConfig(rtol=1e-8, max_iters=5000))
     ref = _oracle_run(k2[0], f[0], k0[0], eta[0], cmap, 1e-8, 5000)
+    assert_run_parity(res.trace, res.u, ref)
+
+
+# ------------------------------------------------------------------ long lines (n = 1024 .. 4096)
+@pytest.mark.parametrize("n", [1024, 2048, 4096])
+def test_long_line_operators_match_oracle(gpu, n):
+    Oracle.set_threads(os.cpu_count() or 8)
+    k2, f, k0, eta = instance(n, batch=1, ppw=6.0, seed=n)
+    rng = np.random.default_rng(n + 1)
+    u = rand_field(rng, k2.shape)
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        G, born, fw = p.apply_G(u), p.born_residual(u, f), p.forward_transform(u)
+        back = p.inverse_transform(fw)
+    o = OracleProblem(k2[0], k0[0], eta[0])
+    assert rel(G[0], o.apply_G(u[0])) < OP_TOL
+    assert rel(born[0], o.born_residual(u[0], f[0])) < OP_TOL
+    assert rel(fw[0], Oracle.forward_dst(u[0])) < OP_TOL
+    assert rel(back[0], u[0]) < 1e-12
+
+
+@pytest.mark.parametrize("n,cmap,K", [(1024, bs.PointwiseMap(), 12), (2048, bs.ScalarMap(1.0), 6)])
+def test_long_line_per_iterate(gpu, n, cmap, K):
+    Oracle.set_threads(os.cpu_count() or 8)
+    k2, f, k0, eta = instance(n, ppw=8.0, contrast=0.3, seed=3)
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        res = bs.run(p, cmap, f, bs.IterationConfig(rtol=1e-12, max_iters=K), n_snap=K + 1)
+    ref = _oracle_run(k2[0], f[0], k0[0], eta[0], cmap, 1e-12, K, n_snap=K + 1)
+    for m in range(1, K + 1):
+        assert rel(res.snapshots[m], ref.snapshots[m]) < FIELD_TOL, m
+    assert_run_parity(res.trace, res.u, ref)
+
+
+def test_config2_grid_first_sweeps(gpu):
+    """BASELINE config 2 on one GPU: 4095^2, 6 ppw, contrast 0.5, 16 point sources, pointwise
+    map -- the first sweeps against the oracle (a full solve is O(1e4) sweeps)."""
+    Oracle.set_threads(os.cpu_count() or 8)
+    k2, f, k0, eta = bs.config_instances("c2")
+    K = 3
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        res = bs.run(p, bs.PointwiseMap(), f, bs.IterationConfig(rtol=1e-6, max_iters=K))
+    ref = _oracle_run(k2[0], f[0], k0[0], eta[0], bs.PointwiseMap(), 1e-6, K)
+    assert res.trace.iters == ref.iters == K
     assert_run_parity(res.trace, res.u, ref)
