@@ -37,6 +37,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Born-series sweeps x grid points per sec (Gpts/s); achieved HBM GB/s vs peak"
+WORKLOADS = {
+    "c0": "c0: 1 x 127^2 Dirichlet Helmholtz CBS, contrast 0.3, 10 ppw, sponge N/8, rtol 1e-6",
+    "c1": "c1: 64 x 511^2 Dirichlet Helmholtz CBS batch, contrast 0.5, 8 ppw, sponge N/8, rtol 1e-6",
+    "c2": "c2: 1 x 4095^2 Dirichlet Helmholtz CBS, contrast 0.5, 6 ppw, 16 point sources, rtol 1e-6",
+}
 UNIT = "Gpts/s"
 ROW_BYTES_PER_PT = 96     # row kernel: T in, u in, k2 in, f in, u out, T out (16 B each)
 COL_BYTES_PER_PT = 32     # column kernel: T in, T out
@@ -205,12 +210,14 @@ def run_ours(args):
         return float(t.item())
 
     from paper_2603_18527_b200.sharding import shard_members
-    total = args.batch
+    cfgd = bs.CONFIGS[args.config]
+    total = args.batch if args.config == "c1" else cfgd["batch"]
     first, per = shard_members(total, world, rank)
-    k2, f, k0, eta = bs.config_instances("c1", first, per)
+    k2, f, k0, eta = bs.config_instances(args.config, first, per)
     nd = k2.shape[1]
     pts = nd * nd
-    cmap = bs.PointwiseMap()
+    cmap = {"pointwise": bs.PointwiseMap(), "scalar": bs.ScalarMap(1.0),
+            "optimal_l2": bs.OptimalScalarMap("euclidean")}[args.map or cfgd["map"]]
     cfg = bs.IterationConfig(rtol=1e-6, max_iters=args.sweeps)
 
     prob = bs.HelmholtzDirichlet(k2, k0, eta, device=local_rank)
@@ -324,8 +331,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded RngState media + centre Gaussian-bump sources, BASELINE c1 construction)",
-            "config": {"workload": "c1: 64 x 511^2 Dirichlet Helmholtz CBS batch, contrast 0.5, "
-                                   "8 ppw, sponge N/8, pointwise gamma(x)=iV/eta, rtol 1e-6",
+            "config": {"workload": WORKLOADS[args.config] + f"; map {args.map or cfgd['map']}",
                        "grid": f"{nd}x{nd} (n={nd + 1}, h=1/{nd + 1})", "global_batch": total,
                        "members_per_gpu": per, "sweeps_per_step": args.sweeps,
                        "parallelism": f"batch-shard x{world}",
@@ -361,6 +367,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=64, help="members of config c1 (whole job)")
+    ap.add_argument("--config", choices=["c0", "c1", "c2"], default="c1",
+                    help="workload; the headline metric is quoted on c1 (BASELINE.json configs[1])")
+    ap.add_argument("--map", choices=["pointwise", "scalar", "optimal_l2"], default=None,
+                    help="correction map (default: the config's canonical map)")
     ap.add_argument("--sweeps", type=int, default=127, help="sweeps per step (max_iters)")
     ap.add_argument("--cpu-sweeps", type=int, default=100)
     ap.add_argument("--ref-sweeps", type=int, default=2)
