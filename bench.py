@@ -339,7 +339,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "bp_problem_set_medium + bp_run with pinned host buffers"},
-            "roofline": {"bound": "hbm", "kernel": "row_kernel<9,R_SWEEP>",
+            "roofline": {"bound": "hbm", "kernel": f"row_kernel<{int(np.log2(nd + 1))},R_SWEEP>",
                          "achieved": row_gbs, "peak": peak, "unit": "GB/s", "frac": row_gbs / peak,
                          "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": ROW_BYTES_PER_PT * pts_per_launch,
