@@ -97,6 +97,14 @@ typedef struct {
     double fnorm_reta;
 } bp_trace;
 
+/* 3-D grid (config c3): the reference has no 3-D; the extension keeps the
+ * DirichletInterior convention per axis, layout data[(ix*ny + iy)*nz + iz]. */
+typedef struct {
+    int32_t nx, ny, nz;
+    double lx, ly, lz;
+    int32_t bc;
+} bp_grid3;
+
 typedef struct bp_problem bp_problem;
 
 const char* bp_last_error(void);
@@ -109,6 +117,10 @@ int bp_abi_version(void);
  * k0, eta: batch each.  device: CUDA ordinal. */
 int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, const double* k0,
                       const double* eta, int32_t device, bp_problem** out);
+/* 3-D batch: A = L_D - k2 with the seven-point L_D, symbol sum of three DST-I factors.
+ * Cubic grids, n+1 = 2^k, 8 <= 2^k <= 512.  All other entry points take the handle. */
+int bp_problem_create3d(const bp_grid3* grid, int32_t batch, const double* k2, const double* k0,
+                        const double* eta, int32_t device, bp_problem** out);
 int bp_problem_destroy(bp_problem* p);
 int bp_problem_batch(const bp_problem* p, int32_t* batch, bp_grid* grid);
 /* Replace the media of every member (same grid and batch): equivalent to constructing new

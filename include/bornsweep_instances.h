@@ -34,9 +34,10 @@ typedef struct {
     int32_t sponge_points;  /* -1: reference default N/8 (proj/src/helmholtz.cpp:67)        */
     double sponge_strength; /* reference default 1.0                                        */
     double eta_factor;      /* eta = eta_factor * max|k2_damped - k0^2|                     */
+    int32_t dim;            /* 2 (default when 0) or 3: N^3 cube, 3-D smoothing / sponge / bump */
 } bp_instance_spec;
 
-/* Members first..first+count-1 into k2/f (count x N x N complex) and k0/eta (count). */
+/* Members first..first+count-1 into k2/f (count x N^dim complex) and k0/eta (count). */
 int bp_make_instances(const bp_instance_spec* spec, int64_t first, int32_t count, double* k2,
                       double* f, double* k0, double* eta, int32_t nthreads);
 

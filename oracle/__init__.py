@@ -93,6 +93,10 @@ class Oracle:
             lib.bpo_last_error.restype = C.c_char_p
             lib.bpo_problem_create.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp,
                                                C.c_double, C.c_double, C.POINTER(C.c_void_p)]
+            lib.bpo_problem_create3.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, _dp,
+                                                C.c_double, C.c_double, C.POINTER(C.c_void_p)]
+            lib.bpo_forward_dst3.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
+            lib.bpo_inverse_dst3.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
             for name in ("bpo_apply_A", "bpo_apply_V", "bpo_apply_V_adjoint", "bpo_apply_Lref"):
                 getattr(lib, name).argtypes = [C.c_void_p, _dp, _dp]
                 getattr(lib, name).restype = None
@@ -127,14 +131,20 @@ class Oracle:
     def forward_dst(cls, x):
         x = _c(x)
         out = np.empty_like(x)
-        cls.lib().bpo_forward_dst(x.shape[0], x.shape[1], _ptr(x), _ptr(out))
+        if x.ndim == 3:
+            cls.lib().bpo_forward_dst3(*x.shape, _ptr(x), _ptr(out))
+        else:
+            cls.lib().bpo_forward_dst(x.shape[0], x.shape[1], _ptr(x), _ptr(out))
         return out
 
     @classmethod
     def inverse_dst(cls, x):
         x = _c(x)
         out = np.empty_like(x)
-        cls.lib().bpo_inverse_dst(x.shape[0], x.shape[1], _ptr(x), _ptr(out))
+        if x.ndim == 3:
+            cls.lib().bpo_inverse_dst3(*x.shape, _ptr(x), _ptr(out))
+        else:
+            cls.lib().bpo_inverse_dst(x.shape[0], x.shape[1], _ptr(x), _ptr(out))
         return out
 
     @classmethod
@@ -151,12 +161,17 @@ class OracleProblem:
     backend = "oracle"
 
     def __init__(self, k2, k0: float, eta: float, lx: float = 1.0, ly: float = 1.0):
+        """k2 of shape (nx, ny) -> the reference's 2-D problem; (nx, ny, nz) -> 3-D extension."""
         k2 = _c(k2)
-        self.nx, self.ny = k2.shape
+        self.shape = k2.shape
+        self.nx, self.ny = k2.shape[:2]
         self.k2, self.k0, self.eta, self.lx, self.ly = k2, float(k0), float(eta), lx, ly
         self._lib = Oracle.lib()
         h = C.c_void_p()
-        rc = self._lib.bpo_problem_create(self.nx, self.ny, lx, ly, _ptr(k2), k0, eta, C.byref(h))
+        if k2.ndim == 3:
+            rc = self._lib.bpo_problem_create3(*k2.shape, lx, _ptr(k2), k0, eta, C.byref(h))
+        else:
+            rc = self._lib.bpo_problem_create(self.nx, self.ny, lx, ly, _ptr(k2), k0, eta, C.byref(h))
         if rc:
             raise (ValueError if rc == 1 else OracleError)(self._lib.bpo_last_error().decode())
         self._h = h
@@ -167,7 +182,7 @@ class OracleProblem:
             self._h = None
 
     def _un(self, name, u):
-        u = _c(u, (self.nx, self.ny))
+        u = _c(u, self.shape)
         out = np.empty_like(u)
         rc = getattr(self._lib, name)(self._h, _ptr(u), _ptr(out))
         if rc:
@@ -175,7 +190,7 @@ class OracleProblem:
         return out
 
     def symbol(self):
-        out = np.empty((self.nx, self.ny), np.complex128)
+        out = np.empty(self.shape, np.complex128)
         self._lib.bpo_problem_symbol(self._h, _ptr(out))
         return out
 
@@ -186,28 +201,28 @@ class OracleProblem:
     def apply_G(self, q): return self._un("bpo_apply_G", q)
 
     def born_residual(self, u, f):
-        u, f = _c(u, (self.nx, self.ny)), _c(f, (self.nx, self.ny))
+        u, f = _c(u, self.shape), _c(f, self.shape)
         out = np.empty_like(u)
         if self._lib.bpo_born_residual(self._h, _ptr(u), _ptr(f), _ptr(out)):
             raise OracleError(self._lib.bpo_last_error().decode())
         return out
 
     def residual(self, u, f):
-        u, f = _c(u, (self.nx, self.ny)), _c(f, (self.nx, self.ny))
+        u, f = _c(u, self.shape), _c(f, self.shape)
         out = np.empty_like(u)
         self._lib.bpo_residual(self._h, _ptr(u), _ptr(f), _ptr(out))
         return out
 
     def run(self, f, *, map_kind=MAP_SCALAR, gamma=1.0 + 0j, metric=METRIC_EUCLIDEAN, m=None,
             fmt=FMT_NPBS, rtol=1e-6, max_iters=1000, u0=None, n_snap=0) -> RunResult:
-        f = _c(f, (self.nx, self.ny))
-        u0 = None if u0 is None else _c(u0, (self.nx, self.ny))
-        mm = None if m is None else _c(m, (self.nx, self.ny))
+        f = _c(f, self.shape)
+        u0 = None if u0 is None else _c(u0, self.shape)
+        mm = None if m is None else _c(m, self.shape)
         u = np.empty_like(f)
         l2 = np.full(max_iters + 1, np.nan)
         rt = np.full(max_iters + 1, np.nan)
         tr = _Trace()
-        snaps = np.zeros((n_snap, self.nx, self.ny), np.complex128) if n_snap else None
+        snaps = np.zeros((n_snap,) + self.shape, np.complex128) if n_snap else None
         mp = Oracle.Map(map_kind, complex(gamma).real, complex(gamma).imag, metric, _ptr(mm))
         rc = self._lib.bpo_run(self._h, C.byref(mp), _ptr(f), fmt, rtol, max_iters, _ptr(u0),
                                _ptr(u), _ptr(l2), _ptr(rt), C.byref(tr), _ptr(snaps), n_snap)
@@ -335,6 +350,7 @@ class ReferenceProblem(OracleProblem):
 
     def __init__(self, k2, k0: float, eta: float, lx: float = 1.0, ly: float = 1.0):
         k2 = _c(k2)
+        self.shape = k2.shape
         self.nx, self.ny = k2.shape
         self.k2, self.k0, self.eta, self.lx, self.ly = k2, float(k0), float(eta), lx, ly
         self._rl = Reference.lib()
@@ -350,7 +366,7 @@ class ReferenceProblem(OracleProblem):
             self._h = None
 
     def _op(self, op, u):
-        u = _c(u, (self.nx, self.ny))
+        u = _c(u, self.shape)
         out = np.empty_like(u)
         rc = self._rl.bpref_apply(self._h, op, _ptr(u), _ptr(out))
         if rc:
@@ -371,14 +387,14 @@ class ReferenceProblem(OracleProblem):
     def inverse_dst(self, x): return self._op(6, x)
 
     def born_residual(self, u, f):
-        u, f = _c(u, (self.nx, self.ny)), _c(f, (self.nx, self.ny))
+        u, f = _c(u, self.shape), _c(f, self.shape)
         out = np.empty_like(u)
         if self._rl.bpref_born_residual(self._h, _ptr(u), _ptr(f), _ptr(out)):
             raise OracleError(self._rl.bpref_last_error().decode())
         return out
 
     def residual(self, u, f):
-        u, f = _c(u, (self.nx, self.ny)), _c(f, (self.nx, self.ny))
+        u, f = _c(u, self.shape), _c(f, self.shape)
         out = np.empty_like(u)
         if self._rl.bpref_residual(self._h, _ptr(u), _ptr(f), _ptr(out)):
             raise OracleError(self._rl.bpref_last_error().decode())
@@ -386,9 +402,9 @@ class ReferenceProblem(OracleProblem):
 
     def run(self, f, *, map_kind=MAP_SCALAR, gamma=1.0 + 0j, metric=METRIC_EUCLIDEAN, m=None,
             fmt=FMT_NPBS, rtol=1e-6, max_iters=1000, u0=None, n_snap=0) -> RunResult:
-        f = _c(f, (self.nx, self.ny))
-        u0 = None if u0 is None else _c(u0, (self.nx, self.ny))
-        mm = None if m is None else _c(m, (self.nx, self.ny))
+        f = _c(f, self.shape)
+        u0 = None if u0 is None else _c(u0, self.shape)
+        mm = None if m is None else _c(m, self.shape)
         u = np.empty_like(f)
         l2 = np.full(max_iters + 1, np.nan)
         rt = np.full(max_iters + 1, np.nan)

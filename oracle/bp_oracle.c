@@ -168,6 +168,46 @@ static void dst2(int nx, int ny, const bpo_c* in, bpo_c* out) {
     plan_free(&py);
 }
 
+/* 3-D plain sine transform, layout [x][y][z] (z contiguous) */
+static void dst3(int nx, int ny, int nz, const bpo_c* in, bpo_c* out) {
+    dst_plan px, py, pz;
+    plan_init(&px, nx);
+    plan_init(&py, ny);
+    plan_init(&pz, nz);
+    const long plane = (long)ny * nz;
+    if (out != in) memcpy(out, in, sizeof(bpo_c) * (size_t)nx * plane);
+#pragma omp parallel
+    {
+        bpo_c* work = (bpo_c*)malloc(sizeof(bpo_c) * (size_t)(px.L + nx + py.L + ny + pz.L + nz));
+#pragma omp for schedule(static)
+        for (long l = 0; l < (long)nx * ny; ++l)
+            dst1_strided(&pz, out + l * nz, 1, out + l * nz, 1, work);
+#pragma omp for schedule(static)
+        for (long l = 0; l < (long)nx * nz; ++l) {
+            const long x = l / nz, z = l % nz;
+            dst1_strided(&py, out + x * plane + z, nz, out + x * plane + z, nz, work);
+        }
+#pragma omp for schedule(static)
+        for (long l = 0; l < plane; ++l) dst1_strided(&px, out + l, plane, out + l, plane, work);
+        free(work);
+    }
+    plan_free(&px);
+    plan_free(&py);
+    plan_free(&pz);
+}
+
+void bpo_forward_dst3(int nx, int ny, int nz, const double* in_c, double* out_c) {
+    dst3(nx, ny, nz, (const bpo_c*)in_c, (bpo_c*)out_c);
+}
+
+void bpo_inverse_dst3(int nx, int ny, int nz, const double* in_c, double* out_c) {
+    bpo_c* o = (bpo_c*)out_c;
+    dst3(nx, ny, nz, (const bpo_c*)in_c, o);
+    const double s = 8.0 / ((double)(nx + 1) * (ny + 1) * (nz + 1));
+    const long n = (long)nx * ny * nz;
+    for (long i = 0; i < n; ++i) o[i] = s * o[i];
+}
+
 /* forward_transform(DST1): RODFT00 then x0.25 == plain sine sum (proj/src/transforms.cpp:111-118) */
 void bpo_forward_dst(int nx, int ny, const double* in_c, double* out_c) {
     dst2(nx, ny, (const bpo_c*)in_c, (bpo_c*)out_c);
@@ -183,6 +223,18 @@ void bpo_inverse_dst(int nx, int ny, const double* in_c, double* out_c) {
 }
 
 /* ------------------------------------------------------------------ problem */
+
+static long npts(const bpo_problem* p) { return (long)p->nx * p->ny * p->nz; }
+
+static void dstn(const bpo_problem* p, const bpo_c* in, bpo_c* out) {
+    if (p->nz > 1) dst3(p->nx, p->ny, p->nz, in, out);
+    else dst2(p->nx, p->ny, in, out);
+}
+
+static void inverse_n(const bpo_problem* p, const bpo_c* in, bpo_c* out) {
+    if (p->nz > 1) bpo_inverse_dst3(p->nx, p->ny, p->nz, (const double*)in, (double*)out);
+    else bpo_inverse_dst(p->nx, p->ny, (const double*)in, (double*)out);
+}
 
 double bpo_norm2(int n, const double* x) {
     /* serial kernels::norm2sq (proj/src/kernels.cpp:38-42) */
@@ -220,6 +272,7 @@ int bpo_problem_create(int nx, int ny, double lx, double ly, const double* k2_c,
     bpo_problem* p = (bpo_problem*)calloc(1, sizeof *p);
     p->nx = nx;
     p->ny = ny;
+    p->nz = 1;
     p->lx = lx;
     p->ly = ly;
     p->k0 = k0;
@@ -257,6 +310,58 @@ int bpo_problem_create(int nx, int ny, double lx, double ly, const double* k2_c,
     return BPO_OK;
 }
 
+int bpo_problem_create3(int nx, int ny, int nz, double l, const double* k2_c, double k0, double eta,
+                        bpo_problem** out) {
+    *out = NULL;
+    if (nx < 2 || ny < 2 || nz < 2) return fail(BPO_EINVAL, "GridSpec: nx,ny,nz must be >= 2");
+    if (!(l > 0.0)) return fail(BPO_EINVAL, "GridSpec: l must be > 0");
+    if (!(eta > 0.0)) return fail(BPO_EINVAL, "HelmholtzProblem: eta must be > 0");
+    if (nx != ny || ny != nz) return fail(BPO_EINVAL, "3-D grid must be cubic (hx == hy == hz)");
+    const long n = (long)nx * ny * nz;
+    const bpo_c* k2 = (const bpo_c*)k2_c;
+    for (long i = 0; i < n; ++i)
+        if (!isfinite(creal(k2[i])) || !isfinite(cimag(k2[i])))
+            return fail(BPO_EINVAL, "HelmholtzProblem: k2 not finite");
+    bpo_problem* p = (bpo_problem*)calloc(1, sizeof *p);
+    p->nx = nx;
+    p->ny = ny;
+    p->nz = nz;
+    p->lx = l;
+    p->ly = l;
+    p->k0 = k0;
+    p->eta = eta;
+    p->k2 = (bpo_c*)malloc(sizeof(bpo_c) * n);
+    p->v = (bpo_c*)malloc(sizeof(bpo_c) * n);
+    p->lambda = (bpo_c*)malloc(sizeof(bpo_c) * n);
+    memcpy(p->k2, k2, sizeof(bpo_c) * n);
+    const bpo_c shift = k0 * k0 + I * eta;
+    for (long i = 0; i < n; ++i) p->v[i] = p->k2[i] - shift;
+    const double h = l / (nx + 1), a = 4.0 / (h * h);
+    const bpo_c c = -(k0 * k0 + I * eta);
+    double* f1 = (double*)malloc(sizeof(double) * nx);
+    for (int q = 0; q < nx; ++q) {
+        const double sq = sin((q + 1) * kPi / (2.0 * (nx + 1)));
+        f1[q] = a * sq * sq;
+    }
+    double mn = INFINITY, mx = 0.0;
+    for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < ny; ++j)
+            for (int k = 0; k < nz; ++k) {
+                const bpo_c v = ((f1[i] + f1[j]) + f1[k]) + c;
+                p->lambda[((long)i * ny + j) * nz + k] = v;
+                const double av = cabs(v);
+                if (av < mn) mn = av;
+                if (av > mx) mx = av;
+            }
+    free(f1);
+    if (mn < kSymbolDivGuard * mx) {
+        bpo_problem_destroy(p);
+        return fail(BPO_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
+    }
+    *out = p;
+    return BPO_OK;
+}
+
 void bpo_problem_destroy(bpo_problem* p) {
     if (!p) return;
     free(p->k2);
@@ -266,7 +371,27 @@ void bpo_problem_destroy(bpo_problem* p) {
 }
 
 void bpo_problem_symbol(const bpo_problem* p, double* lambda_c) {
-    memcpy(lambda_c, p->lambda, sizeof(bpo_c) * (size_t)p->nx * p->ny);
+    memcpy(lambda_c, p->lambda, sizeof(bpo_c) * (size_t)npts(p));
+}
+
+/* seven-point analogue of kernels::five_point: (6u - six neighbours)/h^2, zero halo */
+static void seven_point(const bpo_c* u, int nx, int ny, int nz, double h2, bpo_c* out) {
+    const double inv = 1.0 / h2;
+    const long plane = (long)ny * nz;
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < ny; ++j)
+            for (int k = 0; k < nz; ++k) {
+                const long c = (long)i * plane + (long)j * nz + k;
+                bpo_c s = 6.0 * u[c];
+                if (i > 0) s -= u[c - plane];
+                if (i < nx - 1) s -= u[c + plane];
+                if (j > 0) s -= u[c - nz];
+                if (j < ny - 1) s -= u[c + nz];
+                if (k > 0) s -= u[c - 1];
+                if (k < nz - 1) s -= u[c + 1];
+                out[c] = s * inv;
+            }
 }
 
 /* kernels::five_point serial (proj/src/kernels.cpp:56-69), zero halo, h2 = hx^2 */
@@ -291,8 +416,9 @@ void bpo_apply_A(const bpo_problem* p, const double* u_c, double* out_c) {
     const bpo_c* u = (const bpo_c*)u_c;
     bpo_c* out = (bpo_c*)out_c;
     const double hx = p->lx / (p->nx + 1);
-    five_point(u, p->nx, p->ny, hx * hx, out);
-    const long n = (long)p->nx * p->ny;
+    if (p->nz > 1) seven_point(u, p->nx, p->ny, p->nz, hx * hx, out);
+    else five_point(u, p->nx, p->ny, hx * hx, out);
+    const long n = npts(p);
     for (long i = 0; i < n; ++i) out[i] -= p->k2[i] * u[i];
 }
 
@@ -300,7 +426,7 @@ void bpo_apply_A(const bpo_problem* p, const double* u_c, double* out_c) {
 void bpo_apply_V(const bpo_problem* p, const double* u_c, double* out_c) {
     const bpo_c* u = (const bpo_c*)u_c;
     bpo_c* out = (bpo_c*)out_c;
-    const long n = (long)p->nx * p->ny;
+    const long n = npts(p);
     for (long i = 0; i < n; ++i) out[i] = u[i] * p->v[i];
 }
 
@@ -308,27 +434,25 @@ void bpo_apply_V(const bpo_problem* p, const double* u_c, double* out_c) {
 void bpo_apply_V_adjoint(const bpo_problem* p, const double* u_c, double* out_c) {
     const bpo_c* u = (const bpo_c*)u_c;
     bpo_c* out = (bpo_c*)out_c;
-    const long n = (long)p->nx * p->ny;
+    const long n = npts(p);
     for (long i = 0; i < n; ++i) out[i] = conj(p->v[i]) * u[i];
 }
 
 /* apply_symbol Multiply (proj/src/symbol.cpp:19-39 with op=Multiply) */
 void bpo_apply_Lref(const bpo_problem* p, const double* u_c, double* out_c) {
-    const int nx = p->nx, ny = p->ny;
-    const long n = (long)nx * ny;
+    const long n = npts(p);
     bpo_c* modes = (bpo_c*)malloc(sizeof(bpo_c) * n);
-    dst2(nx, ny, (const bpo_c*)u_c, modes);
+    dstn(p, (const bpo_c*)u_c, modes);
     for (long i = 0; i < n; ++i) modes[i] *= p->lambda[i];
-    bpo_inverse_dst(nx, ny, (const double*)modes, out_c);
+    inverse_n(p, modes, (bpo_c*)out_c);
     free(modes);
 }
 
 /* apply_symbol Divide (proj/src/symbol.cpp:19-39): forward, guard scan, divide, inverse */
 int bpo_apply_G(const bpo_problem* p, const double* q_c, double* out_c) {
-    const int nx = p->nx, ny = p->ny;
-    const long n = (long)nx * ny;
+    const long n = npts(p);
     bpo_c* modes = (bpo_c*)malloc(sizeof(bpo_c) * n);
-    dst2(nx, ny, (const bpo_c*)q_c, modes);
+    dstn(p, (const bpo_c*)q_c, modes);
     double mn = cabs(p->lambda[0]), mx = mn;
     for (long i = 0; i < n; ++i) {
         const double a = cabs(p->lambda[i]);
@@ -340,14 +464,14 @@ int bpo_apply_G(const bpo_problem* p, const double* q_c, double* out_c) {
         return fail(BPO_ERUNTIME, "apply_symbol: near-zero symbol entry under division");
     }
     for (long i = 0; i < n; ++i) modes[i] /= p->lambda[i];
-    bpo_inverse_dst(nx, ny, (const double*)modes, out_c);
+    inverse_n(p, modes, (bpo_c*)out_c);
     free(modes);
     return BPO_OK;
 }
 
 /* Problem::born_residual = G(V u + f) - u (proj/src/problem.cpp:41-49) */
 int bpo_born_residual(const bpo_problem* p, const double* u_c, const double* f_c, double* out_c) {
-    const long n = (long)p->nx * p->ny;
+    const long n = npts(p);
     bpo_c* vu = (bpo_c*)malloc(sizeof(bpo_c) * n);
     bpo_apply_V(p, u_c, (double*)vu);
     const bpo_c* f = (const bpo_c*)f_c;
@@ -362,7 +486,7 @@ int bpo_born_residual(const bpo_problem* p, const double* u_c, const double* f_c
 
 /* residual = f - A u (proj/src/iterate.cpp:45-50) */
 void bpo_residual(const bpo_problem* p, const double* u_c, const double* f_c, double* out_c) {
-    const long n = (long)p->nx * p->ny;
+    const long n = npts(p);
     bpo_c* au = (bpo_c*)malloc(sizeof(bpo_c) * n);
     bpo_apply_A(p, u_c, (double*)au);
     const bpo_c* f = (const bpo_c*)f_c;
@@ -378,7 +502,7 @@ void bpo_residual(const bpo_problem* p, const double* u_c, const double* f_c, do
  * Osnabrugge-style CBS); it is linear in x like every reference map. */
 static int apply_correction(const bpo_problem* p, const bpo_map* map, const bpo_c* x,
                             const bpo_c* euclid_r, bpo_c* out) {
-    const long n = (long)p->nx * p->ny;
+    const long n = npts(p);
     switch (map->kind) {
         case BPO_MAP_SCALAR: {
             const bpo_c g = map->gamma_re + I * map->gamma_im;
@@ -416,9 +540,9 @@ static int apply_correction(const bpo_problem* p, const bpo_map* map, const bpo_
             if (!map->m) return fail(BPO_EINVAL, "FourierDiag correction: shape mismatch");
             const bpo_c* m = (const bpo_c*)map->m;
             bpo_c* modes = (bpo_c*)malloc(sizeof(bpo_c) * n);
-            dst2(p->nx, p->ny, x, modes);
+            dstn(p, x, modes);
             for (long i = 0; i < n; ++i) modes[i] = modes[i] * m[i];
-            bpo_inverse_dst(p->nx, p->ny, (const double*)modes, (double*)out);
+            inverse_n(p, modes, out);
             free(modes);
             return BPO_OK;
         }
@@ -438,7 +562,7 @@ int bpo_run(const bpo_problem* p, const bpo_map* map, const double* f_c, int for
             bpo_trace* info, double* snapshots, int n_snap) {
     if (!(rtol > 0.0 && rtol < 1.0)) return fail(BPO_EINVAL, "run: rtol must lie in (0,1)");
     if (max_iters < 1) return fail(BPO_EINVAL, "run: max_iters must be >= 1");
-    const long n = (long)p->nx * p->ny;
+    const long n = npts(p);
     const bpo_c* f = (const bpo_c*)f_c;
     const double fnorm = sqrt(norm2sq_c(n, f));
     if (fnorm <= 0.0) return fail(BPO_EINVAL, "run: zero source");

@@ -35,7 +35,7 @@ typedef double _Complex bpo_c;
  * V = k2 - (k0^2 + i eta).  Pattern of proj/src/newton_problem.cpp:17-44 (DST-I symbol,
  * five-point A) combined with proj/src/helmholtz.cpp:11-25 (V, shift). */
 typedef struct {
-    int nx, ny;
+    int nx, ny, nz; /* nz == 1: the reference's 2-D grid; nz > 1: 3-D extension (config c3) */
     double lx, ly;
     double k0, eta;
     bpo_c* k2;      /* nx*ny, damped squared wavenumber */
@@ -60,6 +60,13 @@ void bpo_inverse_dst(int nx, int ny, const double* in_c, double* out_c);
 /* Problem construction / destruction. k2 is complex interleaved nx*ny. */
 int bpo_problem_create(int nx, int ny, double lx, double ly, const double* k2_c, double k0,
                        double eta, bpo_problem** out);
+/* 3-D extension (config c3; no reference counterpart): DST-I along x, y, z
+ * (layout [ix][iy][iz], z contiguous), seven-point stencil, symbol sum of three 1-D factors,
+ * inverse scale 8/((nx+1)(ny+1)(nz+1)).  Requires hx == hy == hz (lx = ly = lz). */
+int bpo_problem_create3(int nx, int ny, int nz, double l, const double* k2_c, double k0, double eta,
+                        bpo_problem** out);
+void bpo_forward_dst3(int nx, int ny, int nz, const double* in_c, double* out_c);
+void bpo_inverse_dst3(int nx, int ny, int nz, const double* in_c, double* out_c);
 void bpo_problem_destroy(bpo_problem* p);
 void bpo_problem_symbol(const bpo_problem* p, double* lambda_c);
 

@@ -27,6 +27,11 @@ class Grid(C.Structure):
                 ("bc", C.c_int32)]
 
 
+class Grid3(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("lx", C.c_double),
+                ("ly", C.c_double), ("lz", C.c_double), ("bc", C.c_int32)]
+
+
 class Map(C.Structure):
     _fields_ = [("kind", C.c_int32), ("gamma_re", C.c_double), ("gamma_im", C.c_double),
                 ("metric", C.c_int32), ("m", _dp)]
@@ -45,7 +50,7 @@ class InstanceSpec(C.Structure):
     _fields_ = [("n", C.c_int32), ("ppw", C.c_double), ("contrast", C.c_double),
                 ("sigma_cells", C.c_double), ("src_sigma_cells", C.c_double),
                 ("n_sources", C.c_int32), ("seed", C.c_uint64), ("sponge_points", C.c_int32),
-                ("sponge_strength", C.c_double), ("eta_factor", C.c_double)]
+                ("sponge_strength", C.c_double), ("eta_factor", C.c_double), ("dim", C.c_int32)]
 
 
 # Every symbol include/bornsweep.h declares (tests/test_abi.py checks the header agrees).
@@ -54,6 +59,8 @@ ABI_FUNCTIONS = {
     "bp_abi_version": (C.c_int, []),
     "bp_problem_create": (C.c_int, [C.POINTER(Grid), C.c_int32, _dp, _dp, _dp, C.c_int32,
                                     C.POINTER(C.c_void_p)]),
+    "bp_problem_create3d": (C.c_int, [C.POINTER(Grid3), C.c_int32, _dp, _dp, _dp, C.c_int32,
+                                      C.POINTER(C.c_void_p)]),
     "bp_problem_destroy": (C.c_int, [C.c_void_p]),
     "bp_problem_batch": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(Grid)]),
     "bp_problem_set_medium": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),

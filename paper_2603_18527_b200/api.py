@@ -140,19 +140,30 @@ class HelmholtzDirichlet:
     five-point pattern of NewtonJacobianProblem (newton_problem.cpp:17-44).
     """
 
-    def __init__(self, k2, k0, eta, lx: float = 1.0, device: int = 0):
+    def __init__(self, k2, k0, eta, lx: float = 1.0, device: int = 0, dim: int = 2):
+        """k2: (batch, nx, ny) -- or (nx, ny) for one member; dim=3: (batch, n, n, n) or
+        (n, n, n), the seven-point 3-D extension (config c3)."""
         k2 = np.asarray(k2, dtype=np.complex128)
-        self.single = k2.ndim == 2
+        self.dim = dim
+        self.single = k2.ndim == dim
         k2 = np.ascontiguousarray(k2.reshape((1,) + k2.shape) if self.single else k2)
-        self.batch, self.nx, self.ny = k2.shape
+        self.batch = k2.shape[0]
+        self.grid_shape = k2.shape[1:]
+        self.nx, self.ny = self.grid_shape[:2]
         k0 = np.ascontiguousarray(np.broadcast_to(np.asarray(k0, np.float64), (self.batch,)))
         eta = np.ascontiguousarray(np.broadcast_to(np.asarray(eta, np.float64), (self.batch,)))
         self.k0, self.eta, self.lx, self.device = k0, eta, lx, device
-        g = N.Grid(self.nx, self.ny, lx, lx, BC_DIRICHLET)
         h = C.c_void_p()
         self._lib = N.lib()
-        _check(self._lib.bp_problem_create(C.byref(g), self.batch, _ptr(k2), _ptr(k0), _ptr(eta),
-                                           device, C.byref(h)))
+        if dim == 3:
+            g3 = N.Grid3(*self.grid_shape, lx, lx, lx, BC_DIRICHLET)
+            rc = self._lib.bp_problem_create3d(C.byref(g3), self.batch, _ptr(k2), _ptr(k0),
+                                               _ptr(eta), device, C.byref(h))
+        else:
+            g = N.Grid(self.nx, self.ny, lx, lx, BC_DIRICHLET)
+            rc = self._lib.bp_problem_create(C.byref(g), self.batch, _ptr(k2), _ptr(k0), _ptr(eta),
+                                             device, C.byref(h))
+        _check(rc)
         self._h = h
 
     # context management / lifetime
@@ -176,18 +187,18 @@ class HelmholtzDirichlet:
 
     @property
     def shape(self):
-        return (self.batch, self.nx, self.ny)
+        return (self.batch,) + tuple(self.grid_shape)
 
     def _field(self, x):
         x = np.asarray(x, dtype=np.complex128)
-        if x.shape == (self.nx, self.ny) and self.batch == 1:
+        if x.shape == tuple(self.grid_shape) and self.batch == 1:
             x = x.reshape(self.shape)
         if x.shape != self.shape:
             raise ValueError(f"field shape {x.shape} does not match problem {self.shape}")
         return np.ascontiguousarray(x)
 
     def _out(self, out):
-        return out.reshape(self.nx, self.ny) if self.single else out
+        return out.reshape(self.grid_shape) if self.single else out
 
     def _unary(self, fn, x):
         x = self._field(x)

@@ -40,16 +40,22 @@ constexpr double kPi = 3.14159265358979323846;
 constexpr double kSymbolDivGuard = 1e-14;  // proj/include/bp/symbol.hpp:24
 
 // ------------------------------------------------------------------ small kernels
+// dense (reference layout, (n-1)^dim per member) -> padded (n^dim per member, zero node at 0)
 __global__ void pack_kernel(const double2* __restrict__ dense, double2* __restrict__ padded,
-                            int batch, int log2n) {
+                            int batch, int log2n, int dim) {
     const int n = 1 << log2n, nd = n - 1;
-    const size_t total = (size_t)batch * n * n;
+    const size_t total = (size_t)batch << (dim * log2n);
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const size_t b = idx >> (2 * log2n);
-        const int i = (int)((idx >> log2n) & (n - 1)), j = (int)(idx & (n - 1));
+        const size_t b = idx >> (dim * log2n);
+        const int j = (int)(idx & (n - 1)), i = (int)((idx >> log2n) & (n - 1));
+        const int x = dim == 3 ? (int)((idx >> (2 * log2n)) & (n - 1)) : 1;
         double2 v = make_double2(0.0, 0.0);
-        if (dense && i > 0 && j > 0) v = dense[(b * nd + (i - 1)) * nd + (j - 1)];
+        if (dense && i > 0 && j > 0 && x > 0) {
+            const size_t plane = dim == 3 ? (size_t)(x - 1) * nd : 0;
+            const size_t per = dim == 3 ? (size_t)nd * nd * nd : (size_t)nd * nd;
+            v = dense[b * per + ((plane + (i - 1)) * nd + (j - 1))];
+        }
         padded[idx] = v;
     }
 }
@@ -57,16 +63,21 @@ __global__ void pack_kernel(const double2* __restrict__ dense, double2* __restri
 // select: per-member ping/pong source (result_buf) when non-null
 __global__ void unpack_kernel(const double2* __restrict__ p0, const double2* __restrict__ p1,
                               const int* __restrict__ select, double2* __restrict__ dense,
-                              int batch, int log2n) {
+                              int batch, int log2n, int dim) {
     const int n = 1 << log2n, nd = n - 1;
-    const size_t total = (size_t)batch * nd * nd;
+    const size_t per = dim == 3 ? (size_t)nd * nd * nd : (size_t)nd * nd;
+    const size_t total = (size_t)batch * per;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const size_t b = idx / ((size_t)nd * nd);
-        const size_t r = idx % ((size_t)nd * nd);
-        const int i = (int)(r / nd) + 1, j = (int)(r % nd) + 1;
+        const size_t b = idx / per;
+        size_t r = idx % per;
+        const int j = (int)(r % nd) + 1;
+        r /= nd;
+        const int i = (int)(r % nd) + 1;
+        const int x = (int)(r / nd) + 1;  // 3-D only
         const double2* src = (select && select[b]) ? p1 : p0;
-        dense[idx] = src[(b << (2 * log2n)) + ((size_t)i << log2n) + j];
+        const size_t line = dim == 3 ? ((size_t)x << log2n) + i : (size_t)i;
+        dense[idx] = src[(b << (dim * log2n)) + (line << log2n) + j];
     }
 }
 
@@ -74,15 +85,17 @@ __global__ void unpack_kernel(const double2* __restrict__ p0, const double2* __r
 __global__ void pointwise_kernel(int op, const double2* __restrict__ u, const double2* __restrict__ k2,
                                  const double2* __restrict__ f, const double* __restrict__ k0sq,
                                  const double* __restrict__ eta, double inv_h2,
-                                 double2* __restrict__ out, int batch, int log2n) {
+                                 double2* __restrict__ out, int batch, int log2n, int dim) {
     const int n = 1 << log2n;
-    const size_t total = (size_t)batch * n * n;
+    const size_t total = (size_t)batch << (dim * log2n);
+    const size_t plane = (size_t)n * n;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
          idx += (size_t)gridDim.x * blockDim.x) {
-        const size_t b = idx >> (2 * log2n);
+        const size_t b = idx >> (dim * log2n);
         const int i = (int)((idx >> log2n) & (n - 1)), j = (int)(idx & (n - 1));
+        const int x = dim == 3 ? (int)((idx >> (2 * log2n)) & (n - 1)) : 1;
         double2 o = make_double2(0.0, 0.0);
-        if (i > 0 && j > 0) {
+        if (i > 0 && j > 0 && x > 0) {
             const double2 uu = u[idx], kk = k2[idx];
             const double2 shift = make_double2(k0sq[b], eta[b]);
             if (op == 1) {
@@ -90,7 +103,11 @@ __global__ void pointwise_kernel(int op, const double2* __restrict__ u, const do
             } else if (op == 2) {
                 o = cmul(cconj(csub(kk, shift)), uu);
             } else {
-                double2 s = cscale(uu, 4.0);
+                double2 s = cscale(uu, dim == 3 ? 6.0 : 4.0);
+                if (dim == 3) {
+                    s = csub(s, u[idx - plane]);
+                    s = csub(s, u[idx + plane]);
+                }
                 s = csub(s, u[idx - n]);
                 s = csub(s, u[idx + n]);
                 s = csub(s, u[idx - 1]);
@@ -104,10 +121,10 @@ __global__ void pointwise_kernel(int op, const double2* __restrict__ u, const do
 }
 
 // per-member sum of |x|^2 over a padded field; partials[b*nchunk + c], deterministic
-__global__ void norm_partial_kernel(const double2* __restrict__ x, int log2n, int nchunk,
+__global__ void norm_partial_kernel(const double2* __restrict__ x, int log2n, int dim, int nchunk,
                                     double* __restrict__ partials) {
     const int b = blockIdx.y, c = blockIdx.x;
-    const size_t per = (size_t)1 << (2 * log2n);
+    const size_t per = (size_t)1 << (dim * log2n);
     const size_t chunk = (per + nchunk - 1) / nchunk;
     const size_t lo = c * chunk, hi = min(per, lo + chunk);
     double s = 0.0;
@@ -163,54 +180,50 @@ int points_per_thread(int log2n) {
     return 16;
 }
 
-cudaError_t launch_row_pp(int log2n, int pp, int mode, const RowArgs& a, cudaStream_t s, bool prep = false) {
-    switch (log2n) {
-        case 3: return launch_row_L3(pp, mode, a, s, prep);
-        case 4: return launch_row_L4(pp, mode, a, s, prep);
-        case 5: return launch_row_L5(pp, mode, a, s, prep);
-        case 6: return launch_row_L6(pp, mode, a, s, prep);
-        case 7: return launch_row_L7(pp, mode, a, s, prep);
-        case 8: return launch_row_L8(pp, mode, a, s, prep);
-        case 9: return launch_row_L9(pp, mode, a, s, prep);
-        case 10: return launch_row_L10(pp, mode, a, s, prep);
-        case 11: return launch_row_L11(pp, mode, a, s, prep);
-        case 12: return launch_row_L12(pp, mode, a, s, prep);
-    }
+#define BS_SIZE_CASES(F, ...)                                                                 \
+    switch (log2n) {                                                                          \
+        case 3: return F##3(__VA_ARGS__);                                                     \
+        case 4: return F##4(__VA_ARGS__);                                                     \
+        case 5: return F##5(__VA_ARGS__);                                                     \
+        case 6: return F##6(__VA_ARGS__);                                                     \
+        case 7: return F##7(__VA_ARGS__);                                                     \
+        case 8: return F##8(__VA_ARGS__);                                                     \
+        case 9: return F##9(__VA_ARGS__);                                                     \
+        case 10: return F##10(__VA_ARGS__);                                                   \
+        case 11: return F##11(__VA_ARGS__);                                                   \
+        case 12: return F##12(__VA_ARGS__);                                                   \
+    }                                                                                         \
     return cudaErrorInvalidValue;
+
+cudaError_t launch_row_pp(int log2n, int pp, int dim, int mode, const RowArgs& a, cudaStream_t s,
+                          bool prep = false) {
+    BS_SIZE_CASES(launch_row_L, pp, dim, mode, a, s, prep)
 }
-cudaError_t launch_col_pp(int log2n, int pp, int mode, const ColArgs& a, cudaStream_t s, bool prep = false) {
-    switch (log2n) {
-        case 3: return launch_col_L3(pp, mode, a, s, prep);
-        case 4: return launch_col_L4(pp, mode, a, s, prep);
-        case 5: return launch_col_L5(pp, mode, a, s, prep);
-        case 6: return launch_col_L6(pp, mode, a, s, prep);
-        case 7: return launch_col_L7(pp, mode, a, s, prep);
-        case 8: return launch_col_L8(pp, mode, a, s, prep);
-        case 9: return launch_col_L9(pp, mode, a, s, prep);
-        case 10: return launch_col_L10(pp, mode, a, s, prep);
-        case 11: return launch_col_L11(pp, mode, a, s, prep);
-        case 12: return launch_col_L12(pp, mode, a, s, prep);
-    }
-    return cudaErrorInvalidValue;
+cudaError_t launch_col_pp(int log2n, int pp, int layout, int mode, const ColArgs& a, cudaStream_t s,
+                          bool prep = false) {
+    BS_SIZE_CASES(launch_col_L, pp, layout, mode, a, s, prep)
 }
 
-cudaError_t launch_row(int log2n, int mode, const RowArgs& a, cudaStream_t s) {
-    return launch_row_pp(log2n, points_per_thread(log2n), mode, a, s);
+cudaError_t launch_row(int log2n, int dim, int mode, const RowArgs& a, cudaStream_t s) {
+    return launch_row_pp(log2n, points_per_thread(log2n), dim, mode, a, s);
 }
-cudaError_t launch_col(int log2n, int mode, const ColArgs& a, cudaStream_t s) {
-    return launch_col_pp(log2n, points_per_thread(log2n), mode, a, s);
+cudaError_t launch_col(int log2n, int layout, int mode, const ColArgs& a, cudaStream_t s) {
+    return launch_col_pp(log2n, points_per_thread(log2n), layout, mode, a, s);
 }
 
-cudaError_t prepare_kernels(int log2n) {
+cudaError_t prepare_kernels(int log2n, int dim) {
     RowArgs a{};
     ColArgs c{};
     cudaError_t e = cudaSuccess;
     for (int pp : {8, 16}) {
         for (int mode : {R_FWD, R_FWD_BORN, R_INV, R_SWEEP, R_OPT_A, R_OPT_B, R_RETA_A, R_RETA_C,
                          R_FD_A, R_FD_B})
-            if (cudaError_t r = launch_row_pp(log2n, pp, mode, a, nullptr, true)) e = r;
-        for (int mode : {C_ONE, C_GREEN, C_LREF, C_FD})
-            if (cudaError_t r = launch_col_pp(log2n, pp, mode, c, nullptr, true)) e = r;
+            if (cudaError_t r = launch_row_pp(log2n, pp, dim, mode, a, nullptr, true)) e = r;
+        for (int mode : {C_ONE, C_GREEN, C_LREF, C_FD}) {
+            if (cudaError_t r = launch_col_pp(log2n, pp, CL_PLANE, mode, c, nullptr, true)) e = r;
+            if (dim == 3)
+                if (cudaError_t r = launch_col_pp(log2n, pp, CL_X3, mode, c, nullptr, true)) e = r;
+        }
     }
     return e;
 }
@@ -227,19 +240,21 @@ std::vector<double> lap_table(int n, double h) {
     return lap;
 }
 
-// Problem ctor -> check_invertible (proj/src/symbol.cpp:102-111)
-int check_symbol(const bp_grid& g, int batch, const double* k0, const double* eta) {
+// Problem ctor -> check_invertible (proj/src/symbol.cpp:102-111); dim 3: a_p + a_q + a_r
+int check_symbol(const bp_grid& g, int dim, int batch, const double* k0, const double* eta) {
     const int n = g.nx + 1;
     std::vector<double> lap = lap_table(n, g.lx / n);
     for (int b = 0; b < batch; ++b) {
         double mn = INFINITY, mx = 0.0;
         const double k0sq = k0[b] * k0[b];
         for (int pp = 1; pp < n; ++pp)
-            for (int qq = 1; qq < n; ++qq) {
-                const double a = std::hypot((lap[pp] + lap[qq]) - k0sq, -eta[b]);
-                mn = std::min(mn, a);
-                mx = std::max(mx, a);
-            }
+            for (int qq = 1; qq < n; ++qq)
+                for (int rr = 1; rr < (dim == 3 ? n : 2); ++rr) {
+                    const double re = dim == 3 ? (lap[pp] + lap[qq]) + lap[rr] : lap[pp] + lap[qq];
+                    const double a = std::hypot(re - k0sq, -eta[b]);
+                    mn = std::min(mn, a);
+                    mx = std::max(mx, a);
+                }
         if (mn < kSymbolDivGuard * mx)
             return set_err(BP_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
     }
@@ -253,9 +268,10 @@ int grid_for(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 16)
 // ------------------------------------------------------------------ handle
 struct bp_problem {
     bp_grid grid{};
-    int batch = 0, device = 0, log2n = 0, n = 0;
-    size_t field = 0;   // padded elements per member (n*n)
-    size_t alloc = 0;   // padded elements per buffer (batch*n*n + n)
+    int batch = 0, device = 0, log2n = 0, n = 0, dim = 2;
+    size_t field = 0;   // padded elements per member (n^dim)
+    size_t alloc = 0;   // padded elements per buffer (batch*n^dim + n^(dim-1): zero halo)
+    size_t dense_pts = 0;  // reference-layout points per member ((n-1)^dim)
     double inv_h2 = 0, green_scale = 0;
     cudaStream_t stream = nullptr;
     // device constants
@@ -369,24 +385,25 @@ int check_problem(const bp_problem* p) {
 
 // dense host -> padded device
 int upload(bp_problem* p, const double* host, double2* dst, bool host_ptr = true) {
-    const size_t nd = (size_t)p->grid.nx * p->grid.ny;
+    const size_t nd = p->dense_pts;
     const size_t bytes = sizeof(double2) * nd * p->batch;
     const double2* src = reinterpret_cast<const double2*>(host);
     if (host_ptr) {
         CU(cudaMemcpyAsync(p->dense, host, bytes, cudaMemcpyHostToDevice, p->stream));
         src = p->dense;
     }
-    pack_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(src, dst, p->batch, p->log2n);
+    pack_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(src, dst, p->batch, p->log2n,
+                                                                       p->dim);
     CU(cudaGetLastError());
     return BP_OK;
 }
 
 int download(bp_problem* p, const double2* p0, const double2* p1, const int* select, double* host,
              bool host_ptr = true) {
-    const size_t nd = (size_t)p->grid.nx * p->grid.ny;
+    const size_t nd = p->dense_pts;
     double2* dst = host_ptr ? p->dense : reinterpret_cast<double2*>(host);
     unpack_kernel<<<grid_for(nd * p->batch), 256, 0, p->stream>>>(p0, p1, select, dst, p->batch,
-                                                                   p->log2n);
+                                                                   p->log2n, p->dim);
     CU(cudaGetLastError());
     if (host_ptr)
         CU(cudaMemcpyAsync(host, p->dense, sizeof(double2) * nd * p->batch, cudaMemcpyDeviceToHost,
@@ -397,10 +414,39 @@ int download(bp_problem* p, const double2* p0, const double2* p1, const int* sel
 int norms(bp_problem* p, const double2* x, double* out) {
     const int nchunk = 64;
     dim3 g(nchunk, p->batch);
-    norm_partial_kernel<<<g, 256, 0, p->stream>>>(x, p->log2n, nchunk, p->norm_part);
+    norm_partial_kernel<<<g, 256, 0, p->stream>>>(x, p->log2n, p->dim, nchunk, p->norm_part);
     norm_final_kernel<<<(p->batch + 127) / 128, 128, 0, p->stream>>>(p->norm_part, nchunk,
                                                                       p->batch, out);
     CU(cudaGetLastError());
+    return BP_OK;
+}
+
+// The transverse part of a transform pair after the row (y / z) pass: in 2-D one column
+// kernel (x-lines); in 3-D the y-lines of every x-plane, the x-lines (where the spectral
+// multiply happens), and the y-lines again.  mode C_ONE = forward transform only (API).
+// Returns the number of kernels launched (negative on error).
+int col_stage(bp_problem* p, const ColArgs& c0, int mode, double scale) {
+    ColArgs c = c0;
+    if (p->dim == 2) {
+        c.planes_per_member = 1;
+        c.scale = scale;
+        return launch_col(p->log2n, CL_PLANE, mode, c, p->stream) == cudaSuccess ? 1 : -1;
+    }
+    c.planes_per_member = p->n;
+    c.scale = 1.0;
+    if (launch_col(p->log2n, CL_PLANE, C_ONE, c, p->stream) != cudaSuccess) return -1;
+    c.scale = scale;
+    if (launch_col(p->log2n, CL_X3, mode, c, p->stream) != cudaSuccess) return -1;
+    if (mode == C_ONE) return 2;
+    c.scale = 1.0;
+    c.planes_per_member = p->n;
+    if (launch_col(p->log2n, CL_PLANE, C_ONE, c, p->stream) != cudaSuccess) return -1;
+    return 3;
+}
+
+int col_stage_checked(bp_problem* p, const ColArgs& c, int mode, double scale) {
+    if (col_stage(p, c, mode, scale) < 0)
+        return set_err(BP_ECUDA, std::string("column stage launch: ") + cudaGetErrorString(cudaGetLastError()));
     return BP_OK;
 }
 
@@ -408,12 +454,12 @@ int norms(bp_problem* p, const double2* x, double* out) {
 int green(bp_problem* p, const double2* in, double2* out, const double2* sub, bool born) {
     RowArgs a = row_args(p);
     a.in = in;
-    CU(launch_row(p->log2n, born ? R_FWD_BORN : R_FWD, a, p->stream));
+    CU(launch_row(p->log2n, p->dim, born ? R_FWD_BORN : R_FWD, a, p->stream));
     ColArgs c = col_args(p);
-    CU(launch_col(p->log2n, C_GREEN, c, p->stream));
+    if (int rc = col_stage_checked(p, c, C_GREEN, p->green_scale)) return rc;
     a.out = out;
     a.sub = sub;
-    CU(launch_row(p->log2n, R_INV, a, p->stream));
+    CU(launch_row(p->log2n, p->dim, R_INV, a, p->stream));
     return BP_OK;
 }
 
@@ -471,13 +517,20 @@ SweepPlan plan_for(const bp_map* map) {
     return s;
 }
 
-// ev (optional): plan.n + 1 events recorded around the launches
+// kernels one sweep launches (a column stage is 3 kernels in 3-D)
+int plan_kernels(const bp_problem* p, const SweepPlan& plan) {
+    int k = 0;
+    for (int s = 0; s < plan.n; ++s) k += plan.row[s] ? 1 : (p->dim == 3 ? 3 : 1);
+    return k;
+}
+
+// ev (optional): plan.n + 1 events recorded around the stages
 int sweep_once(bp_problem* p, const SweepPlan& plan, const RowArgs& a, const ColArgs& c,
                cudaEvent_t* ev) {
     if (ev) CU(cudaEventRecord(ev[0], p->stream));
     for (int k = 0; k < plan.n; ++k) {
-        if (plan.row[k]) CU(launch_row(p->log2n, plan.mode[k], a, p->stream));
-        else CU(launch_col(p->log2n, plan.mode[k], c, p->stream));
+        if (plan.row[k]) CU(launch_row(p->log2n, p->dim, plan.mode[k], a, p->stream));
+        else if (int rc = col_stage_checked(p, c, plan.mode[k], p->green_scale)) return rc;
         if (ev) CU(cudaEventRecord(ev[k + 1], p->stream));
     }
     return BP_OK;
@@ -497,9 +550,9 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     const SweepPlan plan = plan_for(map);
     if (map->kind == BP_MAP_FOURIER_DIAG) {
         // one multiplier for the whole batch, reference mode layout -> padded
-        const size_t bytes = sizeof(double2) * (size_t)p->grid.nx * p->grid.ny;
+        const size_t bytes = sizeof(double2) * p->dense_pts;
         CU(cudaMemcpyAsync(p->dense, map->m, bytes, cudaMemcpyHostToDevice, p->stream));
-        pack_kernel<<<grid_for(p->field), 256, 0, p->stream>>>(p->dense, p->fd, 1, p->log2n);
+        pack_kernel<<<grid_for(p->field), 256, 0, p->stream>>>(p->dense, p->fd, 1, p->log2n, p->dim);
         CU(cudaGetLastError());
     }
 
@@ -525,16 +578,18 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
 
     // q^0 = V u^0 + f -> forward y-DST -> T ; column pass
     a.in = p->u0;
-    CU(launch_row(p->log2n, R_FWD_BORN, a, p->stream));
-    CU(launch_col(p->log2n, C_GREEN, c, p->stream));
+    CU(launch_row(p->log2n, p->dim, R_FWD_BORN, a, p->stream));
+    if (int rc2 = col_stage_checked(p, c, C_GREEN, p->green_scale)) return rc2;
 
-    // kernels launched so far in this run: pack f (+ pack u0), 2x norms (2 each), Green (3),
-    // init_control, 2x fill_nan, initial row + column pass
-    p->stat_launches = 13 + (have_u0 ? 1 : 0);
+    // kernels launched so far in this run: pack f (+ pack u0), 2x norms (2 each), Green
+    // (2 row + column stage), init_control, 2x fill_nan, initial row pass + column stage
+    const int stage = p->dim == 3 ? 3 : 1;
+    p->stat_launches = 8 + 2 * stage + 3 + (have_u0 ? 1 : 0) + (map->kind == BP_MAP_FOURIER_DIAG);
+    const int kps = plan_kernels(p, plan);
     p->stat_row_ms = p->stat_col_ms = 0;
     p->stat_timed = 0;
     const long max_launch = (long)cfg->max_iters + 1;  // launch k records entry k-1
-    const size_t nd = (size_t)p->grid.nx * p->grid.ny;
+    const size_t nd = p->dense_pts;
 
     if (snapshots && n_snap > 0) {
         // u^0
@@ -548,7 +603,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         for (k = 1; k <= max_launch; ++k) {
             rc = sweep_once(p, plan, a, c, nullptr);
             if (rc) return rc;
-            p->stat_launches += plan.n;
+            p->stat_launches += kps;
             if (k < n_snap) {
                 // u^k lives in buffer k&1 for every member still iterating
                 rc = download(p, (k & 1) ? p->u1 : p->u0, nullptr, nullptr,
@@ -574,7 +629,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             }
             if (rc) break;
             launched += kGraphSweeps;
-            p->stat_launches += plan.n * kGraphSweeps;
+            p->stat_launches += (int64_t)kps * kGraphSweeps;
             CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
                                p->stream));
             CU(cudaStreamSynchronize(p->stream));
@@ -615,7 +670,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         while (launched < max_launch) {
             CU(cudaGraphLaunch(p->graph, p->stream));
             launched += kGraphSweeps;
-            p->stat_launches += plan.n * kGraphSweeps;
+            p->stat_launches += (int64_t)kps * kGraphSweeps;
             CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
                                p->stream));
             CU(cudaStreamSynchronize(p->stream));
@@ -684,23 +739,24 @@ extern "C" {
 const char* bp_last_error(void) { return g_err.c_str(); }
 int bp_abi_version(void) { return BP_ABI_VERSION; }
 
-int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, const double* k0,
-                      const double* eta, int32_t device, bp_problem** out) {
-    if (!out) return set_err(BP_EINVAL, "null output handle");
-    *out = nullptr;
-    if (!grid || !k2 || !k0 || !eta) return set_err(BP_EINVAL, "null argument");
-    if (grid->nx < 2 || grid->ny < 2) return set_err(BP_EINVAL, "GridSpec: nx,ny must be >= 2");
-    if (!(grid->lx > 0.0) || !(grid->ly > 0.0)) return set_err(BP_EINVAL, "GridSpec: lx,ly must be > 0");
-    if (batch < 1) return set_err(BP_EINVAL, "batch must be >= 1");
-    if (grid->bc != BP_BC_DIRICHLET)
-        return set_err(BP_ENOTSUP, "only DirichletInterior grids are implemented on the GPU");
+}  // extern "C"
+
+namespace {
+
+// Shared constructor of the 2-D (dim 2) and 3-D (dim 3, cubic) Dirichlet Helmholtz batches.
+int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, const double* k0,
+                const double* eta, int32_t device, bp_problem** out) {
     const int n = grid->nx + 1;
     int log2n = 0;
     while ((1 << log2n) < n) ++log2n;
-    if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > kMaxLog2)
-        return set_err(BP_ENOTSUP, "GPU path needs square grids with nx+1 = 2^k, 8 <= 2^k <= 4096");
+    const int max_log2 = dim == 3 ? kMaxLog2_3d : kMaxLog2;
+    if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > max_log2)
+        return set_err(BP_ENOTSUP, dim == 3
+            ? "GPU path needs cubic grids with n+1 = 2^k, 8 <= 2^k <= 512"
+            : "GPU path needs square grids with nx+1 = 2^k, 8 <= 2^k <= 4096");
     if (grid->lx != grid->ly) return set_err(BP_ENOTSUP, "GPU path needs lx == ly (hx == hy)");
-    const size_t nd = (size_t)grid->nx * grid->ny;
+    size_t nd = (size_t)grid->nx * grid->ny;
+    if (dim == 3) nd *= grid->nx;
     for (int b = 0; b < batch; ++b) {
         if (!(eta[b] > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
         if (!std::isfinite(k0[b])) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
@@ -708,7 +764,7 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
     for (size_t k = 0; k < 2 * nd * batch; ++k)
         if (!std::isfinite(k2[k])) return set_err(BP_EINVAL, "HelmholtzProblem: k2 not finite");
 
-    if (int rc = check_symbol(*grid, batch, k0, eta)) return rc;
+    if (int rc = check_symbol(*grid, dim, batch, k0, eta)) return rc;
     const double h = grid->lx / n;
     std::vector<double> lap = lap_table(n, h);
 
@@ -722,12 +778,14 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
     p->device = device;
     p->log2n = log2n;
     p->n = n;
-    p->field = (size_t)n * n;
-    p->alloc = p->field * batch + n;
+    p->dim = dim;
+    p->field = (size_t)1 << (dim * log2n);
+    p->alloc = p->field * batch + ((size_t)1 << ((dim - 1) * log2n));
+    p->dense_pts = nd;
     p->inv_h2 = 1.0 / (h * h);
-    // 4/((nx+1)(ny+1)) (proj/src/transforms.cpp:99) divided by the gain of the four engine
-    // passes of a Green application (kEngineGain^4 = 256, exact)
-    p->green_scale = 4.0 / ((double)n * n) / (kEngineGain * kEngineGain * kEngineGain * kEngineGain);
+    // 2/(n_i+1) per dimension (proj/src/transforms.cpp:99) divided by the gain of the 2*dim
+    // engine passes of a Green application (kEngineGain^(2 dim), exact)
+    p->green_scale = std::pow(2.0 / n, dim) / std::pow(kEngineGain, 2 * dim);
     auto fail = [&](int code) {
         bp_problem_destroy(p);
         return code;
@@ -737,7 +795,7 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
         cudaError_t _e = (call);                                                                    \
         if (_e != cudaSuccess) return fail(set_err(BP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e))); \
     } while (0)
-    CUF(prepare_kernels(log2n));
+    CUF(prepare_kernels(log2n, dim));
     CUF(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     const size_t fb = sizeof(double2) * p->alloc;
     CUF(cudaMalloc(&p->k2, fb));
@@ -750,7 +808,8 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
     for (double2* buf : {p->k2, p->f, p->u0, p->u1, p->T, p->x, p->y})
         CUF(cudaMemsetAsync(buf, 0, fb, p->stream));
     CUF(cudaMalloc(&p->dense, sizeof(double2) * nd * batch));
-    CUF(cudaMalloc(&p->partial, sizeof(double) * (size_t)batch * n * kPartStride));
+    CUF(cudaMalloc(&p->partial, sizeof(double) * (size_t)batch * ((size_t)1 << ((dim - 1) * log2n)) *
+                                    kPartStride));
     CUF(cudaMalloc(&p->gamma, sizeof(double2) * (size_t)batch));
     CUF(cudaMalloc(&p->fd, sizeof(double2) * p->field));
     CUF(cudaMalloc(&p->norm_part, sizeof(double) * (size_t)batch * 64));
@@ -782,6 +841,41 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
 #undef CUF
     *out = p;
     return BP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, const double* k0,
+                      const double* eta, int32_t device, bp_problem** out) {
+    if (!out) return set_err(BP_EINVAL, "null output handle");
+    *out = nullptr;
+    if (!grid || !k2 || !k0 || !eta) return set_err(BP_EINVAL, "null argument");
+    if (grid->nx < 2 || grid->ny < 2) return set_err(BP_EINVAL, "GridSpec: nx,ny must be >= 2");
+    if (!(grid->lx > 0.0) || !(grid->ly > 0.0)) return set_err(BP_EINVAL, "GridSpec: lx,ly must be > 0");
+    if (batch < 1) return set_err(BP_EINVAL, "batch must be >= 1");
+    if (grid->bc != BP_BC_DIRICHLET)
+        return set_err(BP_ENOTSUP, "only DirichletInterior grids are implemented on the GPU");
+    return create_impl(grid, 2, batch, k2, k0, eta, device, out);
+}
+
+int bp_problem_create3d(const bp_grid3* grid, int32_t batch, const double* k2, const double* k0,
+                        const double* eta, int32_t device, bp_problem** out) {
+    if (!out) return set_err(BP_EINVAL, "null output handle");
+    *out = nullptr;
+    if (!grid || !k2 || !k0 || !eta) return set_err(BP_EINVAL, "null argument");
+    if (grid->nx < 2 || grid->ny < 2 || grid->nz < 2)
+        return set_err(BP_EINVAL, "GridSpec: nx,ny,nz must be >= 2");
+    if (!(grid->lx > 0.0) || !(grid->ly > 0.0) || !(grid->lz > 0.0))
+        return set_err(BP_EINVAL, "GridSpec: lx,ly,lz must be > 0");
+    if (batch < 1) return set_err(BP_EINVAL, "batch must be >= 1");
+    if (grid->bc != BP_BC_DIRICHLET)
+        return set_err(BP_ENOTSUP, "only DirichletInterior grids are implemented on the GPU");
+    if (grid->nz != grid->nx || grid->lz != grid->lx)
+        return set_err(BP_ENOTSUP, "GPU 3-D path needs cubic grids (hx == hy == hz)");
+    const bp_grid g2{grid->nx, grid->ny, grid->lx, grid->ly, grid->bc};
+    return create_impl(&g2, 3, batch, k2, k0, eta, device, out);
 }
 
 int bp_problem_destroy(bp_problem* p) {
@@ -817,7 +911,7 @@ static int pointwise_op(const bp_problem* cp, int op, const double* u, const dou
     if (op == 3)
         if (int rc = upload(p, f, p->f)) return rc;
     pointwise_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(
-        op, p->x, p->k2, p->f, p->k0sq, p->eta, p->inv_h2, p->y, p->batch, p->log2n);
+        op, p->x, p->k2, p->f, p->k0sq, p->eta, p->inv_h2, p->y, p->batch, p->log2n, p->dim);
     CU(cudaGetLastError());
     if (int rc = download(p, p->y, p->y, nullptr, out)) return rc;
     CU(cudaStreamSynchronize(p->stream));
@@ -847,17 +941,18 @@ static int spectral_op(const bp_problem* cp, int which, const double* in, const 
             if (int rc = green(p, p->x, p->y, p->x, true)) return rc;
             break;
         case 2:  // L_ref
-            CU(launch_row(p->log2n, R_FWD, a, p->stream));
-            CU(launch_col(p->log2n, C_LREF, c, p->stream));
+            CU(launch_row(p->log2n, p->dim, R_FWD, a, p->stream));
+            if (int rc = col_stage_checked(p, c, C_LREF, p->green_scale)) return rc;
             a.out = p->y;
-            CU(launch_row(p->log2n, R_INV, a, p->stream));
+            CU(launch_row(p->log2n, p->dim, R_INV, a, p->stream));
             break;
         case 3:  // forward transform (plain sine sums)
-        case 4:  // inverse transform (x 4/((nx+1)(ny+1)))
-            CU(launch_row(p->log2n, R_FWD, a, p->stream));
-            // two engine passes (gain 16) for a 2-D transform
-            c.scale = (which == 3 ? 1.0 : 4.0 / ((double)p->n * p->n)) / (kEngineGain * kEngineGain);
-            CU(launch_col(p->log2n, C_ONE, c, p->stream));
+        case 4:  // inverse transform (x prod 2/(n_i+1), proj/src/transforms.cpp:96-103)
+            CU(launch_row(p->log2n, p->dim, R_FWD, a, p->stream));
+            // dim engine passes (gain 4 each) for a dim-D transform
+            if (int rc = col_stage_checked(p, c, C_ONE,
+                    (which == 3 ? 1.0 : std::pow(2.0 / p->n, p->dim)) / std::pow(kEngineGain, p->dim)))
+                return rc;
             if (int rc = download(p, p->T, p->T, nullptr, out)) return rc;
             CU(cudaStreamSynchronize(p->stream));
             return BP_OK;
@@ -921,14 +1016,14 @@ int bp_problem_stream(const bp_problem* p, void** stream) {
 int bp_problem_set_medium(bp_problem* p, const double* k2, const double* k0, const double* eta) {
     if (int rc = check_problem(p)) return rc;
     if (!k2 || !k0 || !eta) return set_err(BP_EINVAL, "null argument");
-    const size_t nd = (size_t)p->grid.nx * p->grid.ny;
+    const size_t nd = p->dense_pts;
     for (int b = 0; b < p->batch; ++b) {
         if (!(eta[b] > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
         if (!std::isfinite(k0[b])) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
     }
     for (size_t k = 0; k < 2 * nd * p->batch; ++k)
         if (!std::isfinite(k2[k])) return set_err(BP_EINVAL, "HelmholtzProblem: k2 not finite");
-    if (int rc = check_symbol(p->grid, p->batch, k0, eta)) return rc;
+    if (int rc = check_symbol(p->grid, p->dim, p->batch, k0, eta)) return rc;
     DeviceGuard guard(p->device);
     std::vector<double> k0sq(p->batch);
     for (int b = 0; b < p->batch; ++b) k0sq[b] = k0[b] * k0[b];

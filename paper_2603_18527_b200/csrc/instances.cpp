@@ -87,6 +87,36 @@ void smooth(int nx, int ny, double sigma, const double* in, double* out) {
         }
 }
 
+// 3-D separable smoothing (same kernel along z, y, x), zero padding
+void smooth3(int n, double sigma, const double* in, double* out) {
+    const size_t N3 = (size_t)n * n * n;
+    if (sigma <= 0.0) {
+        std::memcpy(out, in, sizeof(double) * N3);
+        return;
+    }
+    const int R = static_cast<int>(std::ceil(4.0 * sigma));
+    std::vector<double> w(2 * R + 1);
+    double ws = 0.0;
+    for (int d = -R; d <= R; ++d) ws += (w[d + R] = std::exp(-0.5 * d * d / (sigma * sigma)));
+    for (double& x : w) x /= ws;
+    std::vector<double> a(in, in + N3), b(N3);
+    const size_t strides[3] = {1, (size_t)n, (size_t)n * n};
+    for (int ax = 0; ax < 3; ++ax) {
+        const size_t st = strides[ax];
+        for (size_t idx = 0; idx < N3; ++idx) {
+            const int pos = static_cast<int>((idx / st) % n);
+            double s = 0.0;
+            for (int d = -R; d <= R; ++d) {
+                const int pp = pos + d;
+                if (pp >= 0 && pp < n) s += w[d + R] * a[idx + (long)d * (long)st];
+            }
+            b[idx] = s;
+        }
+        a.swap(b);
+    }
+    std::memcpy(out, a.data(), sizeof(double) * N3);
+}
+
 // sponge_profile (proj/src/samplers.cpp:130-150)
 void sponge(int nx, int ny, int layer, double strength, double* out) {
     auto ramp = [layer](int dist) {
@@ -122,12 +152,14 @@ void bump(int nx, int ny, double lx, double ly, double cx, double cy, double wid
 void make_one(const bp_instance_spec& s, int64_t index, std::complex<double>* k2,
               std::complex<double>* f, double* k0_out, double* eta_out) {
     const int n = s.n, N = n - 1;
-    const size_t npts = static_cast<size_t>(N) * N;
+    const bool d3 = s.dim == 3;
+    const size_t npts = static_cast<size_t>(N) * N * (d3 ? N : 1);
     const double h = 1.0 / n;
     Rng rng = stream(s.seed, index);
     std::vector<double> noise(npts), g(npts);
     for (double& v : noise) v = rng.normal();
-    smooth(N, N, s.sigma_cells, noise.data(), g.data());
+    if (d3) smooth3(N, s.sigma_cells, noise.data(), g.data());
+    else smooth(N, N, s.sigma_cells, noise.data(), g.data());
     double gmax = 0.0;
     for (double v : g) gmax = std::max(gmax, std::abs(v));
     if (gmax <= 0.0) gmax = 1.0;
@@ -143,7 +175,26 @@ void make_one(const bp_instance_spec& s, int64_t index, std::complex<double>* k2
     const double k0 = ksum / static_cast<double>(npts);
     const int layer = s.sponge_points < 0 ? N / 8 : s.sponge_points;
     std::vector<double> d(npts, 0.0);
-    if (layer > 0 && s.sponge_strength > 0.0) sponge(N, N, layer, s.sponge_strength, d.data());
+    if (layer > 0 && s.sponge_strength > 0.0) {
+        if (d3) {
+            // 3-D analogue of sponge_profile: strength * max over the three axes of the ramp
+            auto ramp = [layer](int dist) {
+                if (dist >= layer) return 0.0;
+                const double t = static_cast<double>(layer - dist) / layer;
+                return t * t;
+            };
+            for (int i = 0; i < N; ++i)
+                for (int j = 0; j < N; ++j)
+                    for (int k = 0; k < N; ++k) {
+                        const double q = std::max(std::max(ramp(std::min(i, N - 1 - i)),
+                                                           ramp(std::min(j, N - 1 - j))),
+                                                  ramp(std::min(k, N - 1 - k)));
+                        d[((size_t)i * N + j) * N + k] = s.sponge_strength * q;
+                    }
+        } else {
+            sponge(N, N, layer, s.sponge_strength, d.data());
+        }
+    }
     // k2 -> k2 (1 + i d)  (proj/src/helmholtz.cpp:67-72); eta rule of helmholtz.cpp:80-85 with
     // the config's factor, floored like HelmholtzOptions::eta_floor.
     double dev = 0.0;
@@ -157,7 +208,29 @@ void make_one(const bp_instance_spec& s, int64_t index, std::complex<double>* k2
     *eta_out = std::max(s.eta_factor * dev, 1e-3);
     std::vector<double> src(npts, 0.0);
     const double width = s.src_sigma_cells * h;
-    if (s.n_sources <= 0) {
+    if (d3) {
+        // unit 3-D Gaussian bump(s): centre, or n_sources seeded uniform positions
+        const int ns = s.n_sources <= 0 ? 1 : s.n_sources;
+        for (int m = 0; m < ns; ++m) {
+            double cx = 0.5, cy = 0.5, cz = 0.5;
+            if (s.n_sources > 0) {
+                cx = rng.uniform();
+                cy = rng.uniform();
+                cz = rng.uniform();
+            }
+            for (int i = 0; i < N; ++i) {
+                const double dx = (i + 1) * h - cx;
+                for (int j = 0; j < N; ++j) {
+                    const double dy = (j + 1) * h - cy;
+                    for (int k = 0; k < N; ++k) {
+                        const double dz = (k + 1) * h - cz;
+                        src[((size_t)i * N + j) * N + k] +=
+                            std::exp(-(dx * dx + dy * dy + dz * dz) / (2.0 * width * width));
+                    }
+                }
+            }
+        }
+    } else if (s.n_sources <= 0) {
         bump(N, N, 1.0, 1.0, 0.5, 0.5, width, 1.0, src.data(), false);
     } else {
         for (int k = 0; k < s.n_sources; ++k) {
@@ -176,7 +249,7 @@ int bp_make_instances(const bp_instance_spec* spec, int64_t first, int32_t count
                       double* f, double* k0, double* eta, int32_t nthreads) {
     if (!spec || spec->n < 3 || !(spec->ppw > 2.0) || spec->contrast < 0.0 || spec->contrast >= 1.0)
         return 1;
-    const size_t npts = static_cast<size_t>(spec->n - 1) * (spec->n - 1);
+    const size_t npts = static_cast<size_t>(spec->n - 1) * (spec->n - 1) * (spec->dim == 3 ? spec->n - 1 : 1);
     auto* K = reinterpret_cast<std::complex<double>*>(k2);
     auto* F = reinterpret_cast<std::complex<double>*>(f);
 #ifdef _OPENMP

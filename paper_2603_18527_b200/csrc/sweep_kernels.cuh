@@ -114,6 +114,7 @@ struct ColArgs {
     const double2* tw;
     const double* sinp;
     const int* status;         // nullable: skip inactive members
+    int planes_per_member;     // CL_PLANE: 1 (2-D) or n (3-D y-lines)
 };
 
 // ------------------------------------------------------------------ helpers
@@ -206,7 +207,10 @@ struct RowGeom {
     static constexpr size_t SMEM = sizeof(double2) * ((size_t)EPB * G::PAD_N + SCRATCH);
 };
 
-template <int LOG2N, int MODE, int NW, int PP>
+// DIM = 2: lines are the rows of each member (x index i, y contiguous), five-point stencil.
+// DIM = 3: lines are the z-lines (x, y) of each member ([x][y][z], z contiguous), seven-point
+//          stencil (the 3-D extension of config c3; no reference counterpart).
+template <int LOG2N, int MODE, int NW, int PP, int DIM = 2>
 __global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? 128 : 80>::value))
 row_kernel(const RowArgs a) {
     using G = Geom<LOG2N, PP>;
@@ -216,14 +220,17 @@ row_kernel(const RowArgs a) {
     using S = RowSpec<MODE>;
     constexpr int N = G::N, P = G::P, T = G::T;
     constexpr int EPB = RG::EPB;
+    constexpr int LLINES = (DIM - 1) * LOG2N;          // log2(lines per member)
+    constexpr size_t PLANE = (size_t)N * N;            // x-stride in 3-D
+    constexpr unsigned VALID_LINES = DIM == 3 ? (unsigned)((N - 1) * (N - 1)) : (unsigned)(N - 1);
     extern __shared__ double2 smem[];
 
     const int t = threadIdx.x % T;
     const int e = threadIdx.x / T;
     const long grow = (long)blockIdx.x * EPB + e;
-    const int b = (int)(grow >> LOG2N);
-    const int i = (int)(grow & (N - 1));
-    bool valid = (b < a.batch) && (i != 0);
+    const int b = (int)(grow >> LLINES);
+    const int i = (int)(grow & ((1L << LLINES) - 1));   // line index within the member
+    bool valid = (b < a.batch) && (i & (N - 1)) != 0 && (DIM == 2 || (i >> LOG2N) != 0);
     int m = 0;  // trace entry this launch belongs to
     if (S::ITER && valid) {
         valid = __ldcg(&a.ctl.status[b]) == ST_ACTIVE;
@@ -233,7 +240,7 @@ row_kernel(const RowArgs a) {
 
     double2* buf = smem + e * G::PAD_N;
     const Pol pol = make_policy((Pol*)nullptr, smem + EPB * G::PAD_N, e);
-    const size_t mem = (size_t)(valid ? b : 0) * N * N;
+    const size_t mem = (size_t)(valid ? b : 0) << (DIM * LOG2N);
     const size_t row = mem + (size_t)(valid ? i : 0) * N;
     const double2 zero = make_double2(0.0, 0.0);
     const double2* ucur = (m & 1) ? a.u1 : a.u0;  // u^m
@@ -253,6 +260,10 @@ row_kernel(const RowArgs a) {
             if constexpr (S::ENTRY) {
                 if (e == 0) prefetch_l2(ucur + row - N, RB);
                 if (e == EPB - 1) prefetch_l2(ucur + row + N, RB);
+                if constexpr (DIM == 3) {
+                    prefetch_l2(ucur + row - PLANE, RB);
+                    prefetch_l2(ucur + row + PLANE, RB);
+                }
             }
             if constexpr (MODE == R_OPT_B) prefetch_l2(a.X + row, RB);
         }
@@ -316,15 +327,27 @@ row_kernel(const RowArgs a) {
             if constexpr (S::ENTRY) {
                 // r^m = f - A u^m (five-point in proj/src/kernels.cpp:56-69 order);
                 // x^m = G q^m - u^m = born_residual (problem.cpp:41-49) = G r^m (key identity)
-                double2 un = zero, us = zero, uw = zero, ue = zero;
+                double2 un = zero, us = zero, uw = zero, ue = zero, ua = zero, ub = zero;
                 if (valid) {
                     un = ucur[row - N + j];
                     us = ucur[row + N + j];
                     if (j > 0) uw = ucur[row + j - 1];
                     if (j + 1 < N) ue = ucur[row + j + 1];
+                    if constexpr (DIM == 3) {
+                        ua = ucur[row - PLANE + j];
+                        ub = ucur[row + PLANE + j];
+                    }
                 }
                 const double2 x = csub(z[mm], u);
-                double2 s = cscale(u, 4.0);
+                double2 s;
+                if constexpr (DIM == 3) {
+                    // seven-point: (6u - x-1 - x+1 - y-1 - y+1 - z-1 - z+1) / h^2
+                    s = cscale(u, 6.0);
+                    s = csub(s, ua);
+                    s = csub(s, ub);
+                } else {
+                    s = cscale(u, 4.0);
+                }
                 s = csub(s, un);
                 s = csub(s, us);
                 s = csub(s, uw);
@@ -409,12 +432,12 @@ row_kernel(const RowArgs a) {
         for (int k = 0; k < S::NPART; ++k) acc[k] = pol.sum(acc[k], t);
         int last = 0;
         if (valid && t == 0) {
-            double* pr = a.ctl.partial + ((size_t)b * N + i) * kPartStride;
+            double* pr = a.ctl.partial + (((size_t)b << LLINES) + i) * kPartStride;
 #pragma unroll
             for (int k = 0; k < S::NPART; ++k) pr[k] = acc[k];
             __threadfence();
             const unsigned old = atomicAdd(&a.ctl.counter[b], 1u);
-            last = (old == (unsigned)(N - 2));
+            last = (old == VALID_LINES - 1u);
         }
         last = pol.bcast0(last, t);
         if (last) {
@@ -422,8 +445,9 @@ row_kernel(const RowArgs a) {
             double s[S::NPART];
 #pragma unroll
             for (int k = 0; k < S::NPART; ++k) s[k] = 0.0;
-            for (int r = 1 + t; r < N; r += T) {
-                const double* pr = a.ctl.partial + ((size_t)b * N + r) * kPartStride;
+            for (int r = t; r < (1 << LLINES); r += T) {
+                if ((r & (N - 1)) == 0 || (DIM == 3 && (r >> LOG2N) == 0)) continue;  // padding lines
+                const double* pr = a.ctl.partial + (((size_t)b << LLINES) + r) * kPartStride;
 #pragma unroll
                 for (int k = 0; k < S::NPART; ++k) s[k] += __ldcg(pr + k);
             }
@@ -448,7 +472,11 @@ struct ColGeom {
     static constexpr size_t SMEM = sizeof(double2) * (C * G::PAD_N + BlockSeg<G::T, C>::SCRATCH);
 };
 
-template <int LOG2N, int MODE, int C, int PP>
+// LAYOUT 0: lines along the slow axis of n x n planes (2-D x-lines; 3-D y-lines of every
+//           x-plane, planes_per_member = n).  LAYOUT 2: 3-D x-lines (stride n^2).
+enum ColLayout { CL_PLANE = 0, CL_X3 = 2 };
+
+template <int LOG2N, int MODE, int C, int PP, int LAYOUT = CL_PLANE>
 __global__ void __launch_bounds__(C * Geom<LOG2N, PP>::T, (MinBlocks<C * Geom<LOG2N, PP>::T, PP >= 16 ? 128 : 64>::value))
 col_kernel(const ColArgs a) {
     using G = Geom<LOG2N, PP>;
@@ -457,30 +485,45 @@ col_kernel(const ColArgs a) {
     extern __shared__ double2 smem[];
     const int c = threadIdx.x % C, t = threadIdx.x / C;
     constexpr int GROUPS = N / C;
-    const int b = blockIdx.x / GROUPS;
+    // line group -> member b, base offset `mem`, line stride LS, and (3-D x-lines) the y index
+    int b, yl = 0;
+    size_t mem;
+    constexpr size_t LS = LAYOUT == CL_X3 ? (size_t)N * N : (size_t)N;
+    if constexpr (LAYOUT == CL_X3) {
+        const int grp = blockIdx.x / GROUPS;  // (member, y)
+        b = grp >> LOG2N;
+        yl = grp & (N - 1);
+        if (yl == 0) return;                   // padding y-plane
+        mem = ((size_t)b << (3 * LOG2N)) + (size_t)yl * N;
+    } else {
+        const int plane = blockIdx.x / GROUPS;
+        b = plane / a.planes_per_member;
+        if (a.planes_per_member > 1 && (plane & (N - 1)) == 0) return;  // padding x-plane (3-D)
+        mem = (size_t)plane * N * N;
+    }
     const int q = (blockIdx.x % GROUPS) * C + c;
     if (a.status && __ldcg(&a.status[b]) != ST_ACTIVE) return;  // uniform per CTA
 
     double2* buf = smem + c * G::PAD_N;
     const BlockSeg<T, C> pol{smem + C * G::PAD_N, c};
-    const size_t mem = (size_t)b * N * N;
     const double2 zero = make_double2(0.0, 0.0);
 
     double2 x[P], xm[P], y[P];
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
-        x[mm] = a.T[mem + (size_t)j * N + q];
-        xm[mm] = (j == 0) ? zero : a.T[mem + (size_t)(N - j) * N + q];
+        x[mm] = a.T[mem + (size_t)j * LS + q];
+        xm[mm] = (j == 0) ? zero : a.T[mem + (size_t)(N - j) * LS + q];
     }
     Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
 
     if constexpr (MODE == C_ONE) {
 #pragma unroll
-        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * N + q] = cscale(y[l], a.scale);
+        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + q] = cscale(y[l], a.scale);
     } else {
         const double k0sq = a.k0sq[b], eta = a.eta[b];
-        const double lq = a.lap[q];
+        // transverse symbol part: a_q (2-D) or a_y + a_z (3-D x-lines)
+        const double lq = LAYOUT == CL_X3 ? a.lap[yl] + a.lap[q] : a.lap[q];
 #pragma unroll
         for (int l = 0; l < P; ++l) {
             const int p = t * P + l;
@@ -489,7 +532,9 @@ col_kernel(const ColArgs a) {
             const double li = -eta;
             double2 w;
             if constexpr (MODE == C_FD) {
-                w = cscale(a.fd[(size_t)p * N + q], a.scale);  // FourierDiag m_pq (correction.cpp:63-68)
+                // FourierDiag m (correction.cpp:63-68), padded mode layout shared by the batch
+                const size_t fi = LAYOUT == CL_X3 ? ((size_t)p * N + yl) * N + q : (size_t)p * N + q;
+                w = cscale(a.fd[fi], a.scale);
             } else if constexpr (MODE == C_GREEN) {
                 const double s = a.scale * __drcp_rn(fma(lr, lr, li * li));
                 w = make_double2(lr * s, -li * s);  // scale / lambda
@@ -509,7 +554,7 @@ col_kernel(const ColArgs a) {
         pol.sync();
         Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
-        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * N + q] = y[l];
+        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + q] = y[l];
     }
 }
 

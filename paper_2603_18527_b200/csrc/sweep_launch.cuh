@@ -14,57 +14,60 @@ struct ColCols {
     static constexpr int value = L <= 9 ? 8 : (L == 10 ? 4 : 2);
 };
 
-template <int L, int MODE, int PP>
+template <int L, int MODE, int PP, int DIM>
 cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
     using RG = RowGeom<L, PP, kRowWarps>;
-    auto k = row_kernel<L, MODE, kRowWarps, PP>;
+    auto k = row_kernel<L, MODE, kRowWarps, PP, DIM>;
     if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
-    const long rows = (long)a.batch << L;
+    const long rows = (long)a.batch << ((DIM - 1) * L);
     const int grid = (int)((rows + RG::EPB - 1) / RG::EPB);
     k<<<grid, kRowWarps * 32, RG::SMEM, s>>>(a);
     return cudaGetLastError();
 }
 
-template <int L, int MODE, int PP>
+template <int L, int MODE, int PP, int LAYOUT>
 cudaError_t launch_col_t(const ColArgs& a, cudaStream_t s, bool prepare) {
     constexpr int C = ColCols<L>::value;
     using CG = ColGeom<L, PP, C>;
-    auto k = col_kernel<L, MODE, C, PP>;
+    auto k = col_kernel<L, MODE, C, PP, LAYOUT>;
     if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
-    const int grid = a.batch * ((1 << L) / C);
+    // CL_PLANE: one CTA per (plane, column group), planes = batch * planes_per_member;
+    // CL_X3: one CTA per (member, y, column group)
+    const long groups = (long)a.batch * (LAYOUT == CL_X3 ? (1L << L) : a.planes_per_member);
+    const int grid = (int)(groups * ((1 << L) / C));
     k<<<grid, CG::THREADS, CG::SMEM, s>>>(a);
     return cudaGetLastError();
 }
 
-template <int L, int PP>
+template <int L, int PP, int DIM = 2>
 cudaError_t launch_row_p(int mode, const RowArgs& a, cudaStream_t s, bool prepare) {
     switch (mode) {
-        case R_FWD: return launch_row_t<L, R_FWD, PP>(a, s, prepare);
-        case R_FWD_BORN: return launch_row_t<L, R_FWD_BORN, PP>(a, s, prepare);
-        case R_INV: return launch_row_t<L, R_INV, PP>(a, s, prepare);
-        case R_SWEEP: return launch_row_t<L, R_SWEEP, PP>(a, s, prepare);
-        case R_OPT_A: return launch_row_t<L, R_OPT_A, PP>(a, s, prepare);
-        case R_OPT_B: return launch_row_t<L, R_OPT_B, PP>(a, s, prepare);
-        case R_RETA_A: return launch_row_t<L, R_RETA_A, PP>(a, s, prepare);
-        case R_RETA_C: return launch_row_t<L, R_RETA_C, PP>(a, s, prepare);
-        case R_FD_A: return launch_row_t<L, R_FD_A, PP>(a, s, prepare);
-        default: return launch_row_t<L, R_FD_B, PP>(a, s, prepare);
+        case R_FWD: return launch_row_t<L, R_FWD, PP, DIM>(a, s, prepare);
+        case R_FWD_BORN: return launch_row_t<L, R_FWD_BORN, PP, DIM>(a, s, prepare);
+        case R_INV: return launch_row_t<L, R_INV, PP, DIM>(a, s, prepare);
+        case R_SWEEP: return launch_row_t<L, R_SWEEP, PP, DIM>(a, s, prepare);
+        case R_OPT_A: return launch_row_t<L, R_OPT_A, PP, DIM>(a, s, prepare);
+        case R_OPT_B: return launch_row_t<L, R_OPT_B, PP, DIM>(a, s, prepare);
+        case R_RETA_A: return launch_row_t<L, R_RETA_A, PP, DIM>(a, s, prepare);
+        case R_RETA_C: return launch_row_t<L, R_RETA_C, PP, DIM>(a, s, prepare);
+        case R_FD_A: return launch_row_t<L, R_FD_A, PP, DIM>(a, s, prepare);
+        default: return launch_row_t<L, R_FD_B, PP, DIM>(a, s, prepare);
     }
 }
 
-template <int L, int PP>
+template <int L, int PP, int LAYOUT = CL_PLANE>
 cudaError_t launch_col_p(int mode, const ColArgs& a, cudaStream_t s, bool prepare) {
     switch (mode) {
-        case C_ONE: return launch_col_t<L, C_ONE, PP>(a, s, prepare);
-        case C_GREEN: return launch_col_t<L, C_GREEN, PP>(a, s, prepare);
-        case C_FD: return launch_col_t<L, C_FD, PP>(a, s, prepare);
-        default: return launch_col_t<L, C_LREF, PP>(a, s, prepare);
+        case C_ONE: return launch_col_t<L, C_ONE, PP, LAYOUT>(a, s, prepare);
+        case C_GREEN: return launch_col_t<L, C_GREEN, PP, LAYOUT>(a, s, prepare);
+        case C_FD: return launch_col_t<L, C_FD, PP, LAYOUT>(a, s, prepare);
+        default: return launch_col_t<L, C_LREF, PP, LAYOUT>(a, s, prepare);
     }
 }
 
-// entry points defined in sweep_L<L>.cu
-cudaError_t launch_row_size(int log2n, int pp, int mode, const RowArgs& a, cudaStream_t s, bool prepare);
-cudaError_t launch_col_size(int log2n, int pp, int mode, const ColArgs& a, cudaStream_t s, bool prepare);
+// 3-D kernels exist for n <= 512 (P = 16)
+constexpr int kMaxLog2_3d = 9;
+
 
 // P = 8 needs T = n/8 <= 256 threads per line; longer lines always use P = 16
 template <int L>
@@ -72,19 +75,31 @@ struct Pp8 {
     static constexpr int value = ((1 << L) / 8 <= 256) ? 8 : 16;
 };
 
-#define BS_DEFINE_SIZE(L)                                                                        \
-    cudaError_t launch_row_L##L(int pp, int mode, const RowArgs& a, cudaStream_t s, bool prep) {  \
-        if (pp == 8) return launch_row_p<L, Pp8<L>::value>(mode, a, s, prep);                    \
-        return launch_row_p<L, 16>(mode, a, s, prep);                                            \
-    }                                                                                            \
-    cudaError_t launch_col_L##L(int pp, int mode, const ColArgs& a, cudaStream_t s, bool prep) {  \
-        if (pp == 8) return launch_col_p<L, Pp8<L>::value>(mode, a, s, prep);                    \
-        return launch_col_p<L, 16>(mode, a, s, prep);                                            \
+#define BS_DEFINE_SIZE(L)                                                                       \
+    cudaError_t launch_row_L##L(int pp, int dim, int mode, const RowArgs& a, cudaStream_t s,     \
+                                bool prep) {                                                    \
+        if (dim == 3) {                                                                         \
+            if constexpr (L <= kMaxLog2_3d) return launch_row_p<L, 16, 3>(mode, a, s, prep);    \
+            return cudaErrorInvalidValue;                                                       \
+        }                                                                                       \
+        if (pp == 8) return launch_row_p<L, Pp8<L>::value>(mode, a, s, prep);                   \
+        return launch_row_p<L, 16>(mode, a, s, prep);                                           \
+    }                                                                                           \
+    cudaError_t launch_col_L##L(int pp, int layout, int mode, const ColArgs& a, cudaStream_t s,  \
+                                bool prep) {                                                    \
+        if (layout == CL_X3) {                                                                  \
+            if constexpr (L <= kMaxLog2_3d) return launch_col_p<L, 16, CL_X3>(mode, a, s, prep); \
+            return cudaErrorInvalidValue;                                                       \
+        }                                                                                       \
+        if (pp == 8) return launch_col_p<L, Pp8<L>::value>(mode, a, s, prep);                   \
+        return launch_col_p<L, 16>(mode, a, s, prep);                                           \
     }
 
-#define BS_DECLARE_SIZE(L)                                                                       \
-    cudaError_t launch_row_L##L(int pp, int mode, const RowArgs& a, cudaStream_t s, bool prep);   \
-    cudaError_t launch_col_L##L(int pp, int mode, const ColArgs& a, cudaStream_t s, bool prep);
+#define BS_DECLARE_SIZE(L)                                                                      \
+    cudaError_t launch_row_L##L(int pp, int dim, int mode, const RowArgs& a, cudaStream_t s,     \
+                                bool prep);                                                     \
+    cudaError_t launch_col_L##L(int pp, int layout, int mode, const ColArgs& a, cudaStream_t s,  \
+                                bool prep);
 
 BS_DECLARE_SIZE(3)
 BS_DECLARE_SIZE(4)

@@ -31,11 +31,12 @@ class InstanceSpec:
     sponge_points: int = -1
     sponge_strength: float = 1.0
     eta_factor: float = 1.01
+    dim: int = 2
 
     def _c(self):
         return N.InstanceSpec(self.n, self.ppw, self.contrast, self.sigma_cells,
                               self.src_sigma_cells, self.n_sources, self.seed, self.sponge_points,
-                              self.sponge_strength, self.eta_factor)
+                              self.sponge_strength, self.eta_factor, self.dim)
 
 
 # BASELINE.json configs (synthetic stand-ins)
@@ -49,14 +50,18 @@ CONFIGS = {
     # c2: one high-frequency 4096x4096 grid, 6 ppw, contrast 0.5, 16 seeded point sources
     "c2": dict(spec=InstanceSpec(n=4096, ppw=6.0, contrast=0.5, n_sources=16), batch=1,
                map="pointwise", rtol=1e-6),
+    # c3: 3-D 256^3 cube (255^3 interior), seven-point, sigma 3 cells, contrast 0.4, 8 ppw
+    "c3": dict(spec=InstanceSpec(n=256, ppw=8.0, contrast=0.4, sigma_cells=3.0, dim=3), batch=1,
+               map="pointwise", rtol=1e-5),
 }
 
 
 def make_instances(spec: InstanceSpec, first: int = 0, count: int = 1, nthreads: int = 0):
-    """(k2, f, k0, eta) for members first..first+count-1: complex (count, N, N) arrays."""
+    """(k2, f, k0, eta) for members first..first+count-1: complex (count, N[, N], N) arrays."""
     nd = spec.n - 1
-    k2 = np.empty((count, nd, nd), np.complex128)
-    f = np.empty((count, nd, nd), np.complex128)
+    shape = (count,) + (nd,) * spec.dim
+    k2 = np.empty(shape, np.complex128)
+    f = np.empty(shape, np.complex128)
     k0 = np.empty(count)
     eta = np.empty(count)
     dp = C.POINTER(C.c_double)

@@ -36,6 +36,13 @@ def dst_golden():
     np.savez_compressed(os.path.join(HERE, "dst_scipy.npz"), **out)
 
 
+def dst3_golden():
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((7, 15, 31)) + 1j * rng.standard_normal((7, 15, 31))
+    y = (sf.dstn(x.real, type=1) + 1j * sf.dstn(x.imag, type=1)) / 8
+    np.savez_compressed(os.path.join(HERE, "dst3_scipy.npz"), x=x, y=y)
+
+
 def rng_golden():
     out = {}
     for seed, idx in [(0, -1), (0, 0), (0, 7), (12345, 3), (2**63 + 5, 63)]:
@@ -92,6 +99,7 @@ def run_golden():
 if __name__ == "__main__":
     Reference.set_mode("serial")
     dst_golden()
+    dst3_golden()
     rng_golden()
     sampler_golden()
     ops_golden()

@@ -205,3 +205,29 @@ def test_live_reference_agrees_with_oracle():
     a = p.run(f, map_kind=MAP_OPTIMAL_SCALAR, metric=1, max_iters=30, rtol=1e-12)
     b = r.run(f, map_kind=MAP_OPTIMAL_SCALAR, metric=1, max_iters=30, rtol=1e-12)
     assert rel(a.u, b.u) < 1e-11
+
+
+def test_3d_oracle_dst_and_identities():
+    """3-D extension of the oracle (config c3): DST-I vs scipy dstn golden (made by
+    tests/golden/make_golden.py), round trip, splitting, Green two-sided inverse, key identity."""
+    g = np.load(os.path.join(GOLDEN, "dst3_scipy.npz"))
+    assert rel(Oracle.forward_dst(g["x"]), g["y"]) < 1e-13
+    rng = np.random.default_rng(11)
+    x = rand_field(rng, (15, 15, 15))
+    assert rel(Oracle.inverse_dst(Oracle.forward_dst(x)), x) < 1e-12
+    import paper_2603_18527_b200 as bs
+    spec = bs.InstanceSpec(n=16, ppw=8.0, contrast=0.4, sigma_cells=2.0, dim=3)
+    k2, f, k0, eta = bs.make_instances(spec, 0, 1)
+    p = OracleProblem(k2[0], k0[0], eta[0])
+    r = rand_field(rng, p.shape)
+    assert rel(p.apply_Lref(r) - p.apply_V(r), p.apply_A(r)) < 1e-12
+    assert rel(p.apply_Lref(p.apply_G(r)), r) < 1e-12
+    lhs = r - p.apply_G(p.apply_V(r))
+    assert np.linalg.norm(lhs - p.apply_G(p.apply_A(r))) / np.linalg.norm(r) < 1e-12
+    # seven-point symbol vs the dense operator at n = 3
+    k2s = np.zeros((3, 3, 3), np.complex128)
+    ps = OracleProblem(k2s, 0.0, 1.0)
+    e = np.eye(27, dtype=np.complex128)
+    A = np.stack([ps.apply_A(e[k].reshape(3, 3, 3)).ravel() for k in range(27)], axis=1)
+    ev = np.sort(np.linalg.eigvalsh(A.real))
+    assert np.abs(np.sort((ps.symbol() + 1j).real.ravel()) - ev).max() < 1e-10 * ev.max()
