@@ -96,6 +96,10 @@ class Oracle:
             lib.bpo_problem_create3.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, _dp,
                                                 C.c_double, C.c_double, C.POINTER(C.c_void_p)]
             lib.bpo_forward_dst3.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
+            lib.bpo_problem_create_periodic.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double,
+                                                        _dp, C.c_double, C.c_double,
+                                                        C.POINTER(C.c_void_p)]
+            lib.bpo_fft2.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
             lib.bpo_inverse_dst3.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
             for name in ("bpo_apply_A", "bpo_apply_V", "bpo_apply_V_adjoint", "bpo_apply_Lref"):
                 getattr(lib, name).argtypes = [C.c_void_p, _dp, _dp]
@@ -160,15 +164,20 @@ class OracleProblem:
 
     backend = "oracle"
 
-    def __init__(self, k2, k0: float, eta: float, lx: float = 1.0, ly: float = 1.0):
-        """k2 of shape (nx, ny) -> the reference's 2-D problem; (nx, ny, nz) -> 3-D extension."""
+    def __init__(self, k2, k0: float, eta: float, lx: float = 1.0, ly: float = 1.0,
+                 periodic: bool = False):
+        """k2 of shape (nx, ny) -> the 2-D Dirichlet problem; (nx, ny, nz) -> 3-D extension;
+        periodic=True -> the reference's own periodic pseudospectral HelmholtzProblem."""
         k2 = _c(k2)
         self.shape = k2.shape
         self.nx, self.ny = k2.shape[:2]
         self.k2, self.k0, self.eta, self.lx, self.ly = k2, float(k0), float(eta), lx, ly
         self._lib = Oracle.lib()
         h = C.c_void_p()
-        if k2.ndim == 3:
+        if periodic:
+            rc = self._lib.bpo_problem_create_periodic(self.nx, self.ny, lx, ly, _ptr(k2), k0, eta,
+                                                       C.byref(h))
+        elif k2.ndim == 3:
             rc = self._lib.bpo_problem_create3(*k2.shape, lx, _ptr(k2), k0, eta, C.byref(h))
         else:
             rc = self._lib.bpo_problem_create(self.nx, self.ny, lx, ly, _ptr(k2), k0, eta, C.byref(h))
@@ -252,6 +261,10 @@ class Reference:
             lib.bpref_last_error.restype = C.c_char_p
             lib.bpref_problem_create.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp,
                                                  C.c_double, C.c_double, C.POINTER(C.c_void_p)]
+            lib.bpref_periodic_create.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp,
+                                                  C.c_double, C.c_double, C.POINTER(C.c_void_p)]
+            lib.bpref_periodic_bench_instance.argtypes = [C.c_int, C.c_double, C.c_double,
+                                                          C.c_uint64, _dp, _dp, _dp, _dp]
             lib.bpref_problem_destroy.argtypes = [C.c_void_p]
             lib.bpref_problem_destroy.restype = None
             lib.bpref_symbol.argtypes = [C.c_void_p, _dp]
@@ -288,6 +301,17 @@ class Reference:
     @classmethod
     def thread_count(cls) -> int:
         return cls.lib().bpref_thread_count()
+
+    @classmethod
+    def periodic_bench_instance(cls, n, ppw, contrast, seed):
+        """The reference's Helmholtz bench instance (make_layered_helmholtz + bump source)."""
+        k2 = np.empty((n, n), np.complex128)
+        f = np.empty((n, n), np.complex128)
+        k0, eta = C.c_double(), C.c_double()
+        if cls.lib().bpref_periodic_bench_instance(n, ppw, contrast, seed, _ptr(k2), _ptr(f),
+                                                   C.byref(k0), C.byref(eta)):
+            raise OracleError(cls.lib().bpref_last_error().decode())
+        return k2, f, k0.value, eta.value
 
     @classmethod
     def sponge_profile(cls, nx, ny, layer, strength=1.0, bc=1):
@@ -348,14 +372,16 @@ class ReferenceProblem(OracleProblem):
 
     backend = "reference"
 
-    def __init__(self, k2, k0: float, eta: float, lx: float = 1.0, ly: float = 1.0):
+    def __init__(self, k2, k0: float, eta: float, lx: float = 1.0, ly: float = 1.0,
+                 periodic: bool = False):
         k2 = _c(k2)
         self.shape = k2.shape
         self.nx, self.ny = k2.shape
         self.k2, self.k0, self.eta, self.lx, self.ly = k2, float(k0), float(eta), lx, ly
         self._rl = Reference.lib()
         h = C.c_void_p()
-        rc = self._rl.bpref_problem_create(self.nx, self.ny, lx, ly, _ptr(k2), k0, eta, C.byref(h))
+        create = self._rl.bpref_periodic_create if periodic else self._rl.bpref_problem_create
+        rc = create(self.nx, self.ny, lx, ly, _ptr(k2), k0, eta, C.byref(h))
         if rc:
             raise (ValueError if rc == 1 else OracleError)(self._rl.bpref_last_error().decode())
         self._h = h

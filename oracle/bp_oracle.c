@@ -208,6 +208,89 @@ void bpo_inverse_dst3(int nx, int ny, int nz, const double* in_c, double* out_c)
     for (long i = 0; i < n; ++i) o[i] = s * o[i];
 }
 
+/* ------------------------------------------------------------------ periodic FFT */
+/* length-n complex DFT, sign -1 forward / +1 backward, unnormalized; radix-2 for powers of two,
+ * direct sum otherwise */
+static void dft1_strided(int n, int sign, const bpo_c* twf, const int* rev, bpo_c* z, long stride,
+                         bpo_c* work) {
+    for (int i = 0; i < n; ++i) work[i] = z[i * stride];
+    if (rev) {
+        for (int i = 0; i < n; ++i) {
+            const int r = rev[i];
+            if (r > i) {
+                bpo_c t = work[i];
+                work[i] = work[r];
+                work[r] = t;
+            }
+        }
+        for (int len = 2; len <= n; len <<= 1) {
+            const int half = len >> 1, step = n / len;
+            for (int s0 = 0; s0 < n; s0 += len)
+                for (int k = 0; k < half; ++k) {
+                    bpo_c w = twf[k * step];
+                    if (sign > 0) w = conj(w);
+                    const bpo_c a = work[s0 + k], b = work[s0 + k + half] * w;
+                    work[s0 + k] = a + b;
+                    work[s0 + k + half] = a - b;
+                }
+        }
+        for (int i = 0; i < n; ++i) z[i * stride] = work[i];
+    } else {
+        for (int k = 0; k < n; ++k) {
+            bpo_c acc = 0;
+            for (int j = 0; j < n; ++j) {
+                bpo_c w = twf[(long)j * k % n];
+                if (sign > 0) w = conj(w);
+                acc += work[j] * w;
+            }
+            z[k * stride] = acc;
+        }
+    }
+}
+
+static void fft_tables(int n, bpo_c** twf, int** rev) {
+    *twf = (bpo_c*)malloc(sizeof(bpo_c) * (size_t)n);
+    for (int k = 0; k < n; ++k) (*twf)[k] = cos(-2.0 * kPi * k / n) + I * sin(-2.0 * kPi * k / n);
+    *rev = NULL;
+    if (is_pow2(n)) {
+        int bits = 0;
+        while ((1 << bits) < n) ++bits;
+        *rev = (int*)malloc(sizeof(int) * (size_t)n);
+        for (int i = 0; i < n; ++i) {
+            int r = 0;
+            for (int b = 0; b < bits; ++b)
+                if (i & (1 << b)) r |= 1 << (bits - 1 - b);
+            (*rev)[i] = r;
+        }
+    }
+}
+
+/* 2-D DFT: forward (sign -1) unnormalized, backward (sign +1) unnormalized */
+static void fft2(int nx, int ny, int sign, const bpo_c* in, bpo_c* out) {
+    bpo_c *twx, *twy;
+    int *rvx, *rvy;
+    fft_tables(nx, &twx, &rvx);
+    fft_tables(ny, &twy, &rvy);
+    if (out != in) memcpy(out, in, sizeof(bpo_c) * (size_t)nx * ny);
+#pragma omp parallel
+    {
+        bpo_c* work = (bpo_c*)malloc(sizeof(bpo_c) * (size_t)(nx > ny ? nx : ny));
+#pragma omp for schedule(static)
+        for (int i = 0; i < nx; ++i) dft1_strided(ny, sign, twy, rvy, out + (long)i * ny, 1, work);
+#pragma omp for schedule(static)
+        for (int j = 0; j < ny; ++j) dft1_strided(nx, sign, twx, rvx, out + j, ny, work);
+        free(work);
+    }
+    free(twx);
+    free(twy);
+    free(rvx);
+    free(rvy);
+}
+
+void bpo_fft2(int nx, int ny, int sign, const double* in_c, double* out_c) {
+    fft2(nx, ny, sign, (const bpo_c*)in_c, (bpo_c*)out_c);
+}
+
 /* forward_transform(DST1): RODFT00 then x0.25 == plain sine sum (proj/src/transforms.cpp:111-118) */
 void bpo_forward_dst(int nx, int ny, const double* in_c, double* out_c) {
     dst2(nx, ny, (const bpo_c*)in_c, (bpo_c*)out_c);
@@ -226,14 +309,24 @@ void bpo_inverse_dst(int nx, int ny, const double* in_c, double* out_c) {
 
 static long npts(const bpo_problem* p) { return (long)p->nx * p->ny * p->nz; }
 
+/* forward_transform / inverse_transform in the problem's basis (transforms.cpp:105-148) */
 static void dstn(const bpo_problem* p, const bpo_c* in, bpo_c* out) {
-    if (p->nz > 1) dst3(p->nx, p->ny, p->nz, in, out);
+    if (p->periodic) fft2(p->nx, p->ny, -1, in, out);
+    else if (p->nz > 1) dst3(p->nx, p->ny, p->nz, in, out);
     else dst2(p->nx, p->ny, in, out);
 }
 
 static void inverse_n(const bpo_problem* p, const bpo_c* in, bpo_c* out) {
-    if (p->nz > 1) bpo_inverse_dst3(p->nx, p->ny, p->nz, (const double*)in, (double*)out);
-    else bpo_inverse_dst(p->nx, p->ny, (const double*)in, (double*)out);
+    if (p->periodic) {
+        fft2(p->nx, p->ny, +1, in, out);
+        const double s = 1.0 / ((double)p->nx * p->ny);
+        const long n = (long)p->nx * p->ny;
+        for (long i = 0; i < n; ++i) out[i] = s * out[i];
+    } else if (p->nz > 1) {
+        bpo_inverse_dst3(p->nx, p->ny, p->nz, (const double*)in, (double*)out);
+    } else {
+        bpo_inverse_dst(p->nx, p->ny, (const double*)in, (double*)out);
+    }
 }
 
 double bpo_norm2(int n, const double* x) {
@@ -307,6 +400,37 @@ int bpo_problem_create(int nx, int ny, double lx, double ly, const double* k2_c,
         return fail(BPO_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
     }
     *out = p;
+    return BPO_OK;
+}
+
+int bpo_problem_create_periodic(int nx, int ny, double lx, double ly, const double* k2_c,
+                                double k0, double eta, bpo_problem** out) {
+    int rc = bpo_problem_create(nx, ny, lx, ly, k2_c, k0, eta, out);
+    if (rc) return rc;
+    bpo_problem* p = *out;
+    p->periodic = 1;
+    /* laplacian_symbol Periodic: |xi|^2 with xi = 2 pi m / L, m in FFT order
+     * (symbol.cpp:58-67, grid.hpp:67-85), shifted by -(k0^2 + i eta) */
+    const bpo_c c = -(k0 * k0 + I * eta);
+    double mn = INFINITY, mx = 0.0;
+    for (int i = 0; i < nx; ++i) {
+        const int mi = (i < (nx + 1) / 2) ? i : i - nx;
+        const double xi = 2.0 * kPi * mi / lx;
+        for (int j = 0; j < ny; ++j) {
+            const int mj = (j < (ny + 1) / 2) ? j : j - ny;
+            const double yj = 2.0 * kPi * mj / ly;
+            const bpo_c v = (xi * xi + yj * yj) + c;
+            p->lambda[(long)i * ny + j] = v;
+            const double a = cabs(v);
+            if (a < mn) mn = a;
+            if (a > mx) mx = a;
+        }
+    }
+    if (mn < kSymbolDivGuard * mx) {
+        bpo_problem_destroy(p);
+        *out = NULL;
+        return fail(BPO_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
+    }
     return BPO_OK;
 }
 
@@ -415,10 +539,28 @@ static void five_point(const bpo_c* u, int nx, int ny, double h2, bpo_c* out) {
 void bpo_apply_A(const bpo_problem* p, const double* u_c, double* out_c) {
     const bpo_c* u = (const bpo_c*)u_c;
     bpo_c* out = (bpo_c*)out_c;
+    const long n = npts(p);
+    if (p->periodic) {
+        /* HelmholtzProblem::apply_A: F^-1(|xi|^2 F u) - k2 u (helmholtz.cpp:27-32) */
+        bpo_c* modes = (bpo_c*)malloc(sizeof(bpo_c) * n);
+        fft2(p->nx, p->ny, -1, u, modes);
+        for (int i = 0; i < p->nx; ++i) {
+            const int mi = (i < (p->nx + 1) / 2) ? i : i - p->nx;
+            const double xi = 2.0 * kPi * mi / p->lx;
+            for (int j = 0; j < p->ny; ++j) {
+                const int mj = (j < (p->ny + 1) / 2) ? j : j - p->ny;
+                const double yj = 2.0 * kPi * mj / p->ly;
+                modes[(long)i * p->ny + j] *= (xi * xi + yj * yj);  /* |xi|^2 */
+            }
+        }
+        inverse_n(p, modes, out);
+        free(modes);
+        for (long i = 0; i < n; ++i) out[i] -= p->k2[i] * u[i];
+        return;
+    }
     const double hx = p->lx / (p->nx + 1);
     if (p->nz > 1) seven_point(u, p->nx, p->ny, p->nz, hx * hx, out);
     else five_point(u, p->nx, p->ny, hx * hx, out);
-    const long n = npts(p);
     for (long i = 0; i < n; ++i) out[i] -= p->k2[i] * u[i];
 }
 

@@ -36,6 +36,7 @@ typedef double _Complex bpo_c;
  * five-point A) combined with proj/src/helmholtz.cpp:11-25 (V, shift). */
 typedef struct {
     int nx, ny, nz; /* nz == 1: the reference's 2-D grid; nz > 1: 3-D extension (config c3) */
+    int periodic;   /* 1: the reference's own HelmholtzProblem (FFT basis, spectral Laplacian) */
     double lx, ly;
     double k0, eta;
     bpo_c* k2;      /* nx*ny, damped squared wavenumber */
@@ -67,6 +68,12 @@ int bpo_problem_create3(int nx, int ny, int nz, double l, const double* k2_c, do
                         bpo_problem** out);
 void bpo_forward_dst3(int nx, int ny, int nz, const double* in_c, double* out_c);
 void bpo_inverse_dst3(int nx, int ny, int nz, const double* in_c, double* out_c);
+/* The reference's periodic pseudospectral HelmholtzProblem (proj/src/helmholtz.cpp:11-53):
+ * A u = F^-1(|xi|^2 F u) - k2 u, L_eta symbol |xi|^2 - (k0^2 + i eta), FFT basis with the
+ * unnormalized forward / 1/(nx ny) inverse of proj/include/bp/transforms.hpp:16-17. */
+int bpo_problem_create_periodic(int nx, int ny, double lx, double ly, const double* k2_c,
+                                double k0, double eta, bpo_problem** out);
+void bpo_fft2(int nx, int ny, int sign, const double* in_c, double* out_c);
 void bpo_problem_destroy(bpo_problem* p);
 void bpo_problem_symbol(const bpo_problem* p, double* lambda_c);
 

@@ -24,6 +24,7 @@
 
 #include "bp/field.hpp"
 #include "bp/grid.hpp"
+#include "bp/helmholtz.hpp"
 #include "bp/kernels.hpp"
 #include "bp/parallel.hpp"
 #include "bp/problem.hpp"
@@ -119,7 +120,7 @@ cplx optimal_scalar(const ComplexField& r, const ComplexField& w) {
     return bp::kernels::dotc(w.data, r.data) / denom;
 }
 
-ComplexField apply_correction(const DirichletHelmholtz& p, const MapDesc& map,
+ComplexField apply_correction(const bp::Problem& p, const MapDesc& map,
                               const ComplexField& x, const ComplexField& euclid_r) {
     ComplexField out(x.grid);
     switch (map.kind) {
@@ -139,16 +140,18 @@ ComplexField apply_correction(const DirichletHelmholtz& p, const MapDesc& map,
             return out;
         }
         case 2: {
-            std::vector<cplx> modes = bp::forward_transform(x, bp::TransformKind::DST1);
+            std::vector<cplx> modes = bp::forward_transform(x, p.kind());
             std::vector<cplx> m(modes.size());
             std::memcpy(static_cast<void*>(m.data()), map.m, sizeof(cplx) * m.size());
             bp::kernels::mul(modes, m, modes);
-            return bp::inverse_transform(modes, x.grid, bp::TransformKind::DST1);
+            return bp::inverse_transform(modes, x.grid, p.kind());
         }
         case 3: {
-            const auto& v = p.v();
+            const auto* dh = dynamic_cast<const DirichletHelmholtz*>(&p);
+            if (!dh) throw std::invalid_argument("pointwise map needs the Dirichlet family");
+            const auto& v = dh->v();
             for (size_t i = 0; i < x.size(); ++i)
-                out.data[i] = (cplx(0.0, 1.0) / p.eta() * v[i]) * x.data[i];
+                out.data[i] = (cplx(0.0, 1.0) / dh->eta() * v[i]) * x.data[i];
             return out;
         }
     }
@@ -162,7 +165,7 @@ struct TraceOut {
     double fnorm_reta;
 };
 
-void run(const DirichletHelmholtz& p, const MapDesc& map, const ComplexField& f, int format,
+void run(const bp::Problem& p, const MapDesc& map, const ComplexField& f, int format,
          double rtol, int max_iters, const ComplexField* u0, ComplexField& u,
          std::vector<double>& l2, std::vector<double>& reta, TraceOut& tr) {
     constexpr double kDivergenceThreshold = 1e8;
@@ -258,10 +261,41 @@ int bpref_problem_create(int nx, int ny, double lx, double ly, const double* k2,
     });
 }
 
-void bpref_problem_destroy(void* p) { delete static_cast<DirichletHelmholtz*>(p); }
+void bpref_problem_destroy(void* p) { delete static_cast<bp::Problem*>(p); }
+
+// The reference's OWN periodic pseudospectral family: bp::HelmholtzProblem (helmholtz.cpp:11-53)
+int bpref_periodic_create(int nx, int ny, double lx, double ly, const double* k2, double k0,
+                          double eta, void** out) {
+    *out = nullptr;
+    return guarded([&] {
+        GridSpec g = bp::make_grid(nx, ny, lx, ly, bp::Bc::Periodic);
+        *out = static_cast<bp::Problem*>(new bp::HelmholtzProblem(g, field_from(g, k2), k0, eta));
+    });
+}
+
+// Instance of the reference's Helmholtz bench family (make_bench_instance, bench.cpp:25-67,
+// restated: bench.cpp needs Eigen): make_layered_helmholtz(n, ppw, contrast,
+// RngState(seed).split("medium")) + gaussian_bump source from split("source").
+int bpref_periodic_bench_instance(int n, double ppw, double contrast, uint64_t seed, double* k2,
+                                  double* f, double* k0, double* eta) {
+    return guarded([&] {
+        bp::RngState rng(seed);
+        bp::RngState rm = rng.split("medium");
+        auto p = bp::make_layered_helmholtz(n, ppw, contrast, rm);
+        field_to(p->k2(), k2);
+        *k0 = p->k0();
+        *eta = p->eta();
+        const GridSpec& g = p->grid();
+        bp::RngState rs = rng.split("source");
+        const double cx = rs.uniform() * g.lx;
+        const double cy = rs.uniform() * g.ly;
+        const double width = (0.05 + 0.10 * rs.uniform()) * g.lx;
+        field_to(bp::to_complex(bp::gaussian_bump(g, cx, cy, width, 1.0)), f);
+    });
+}
 
 int bpref_symbol(void* h, double* out) {
-    auto* p = static_cast<DirichletHelmholtz*>(h);
+    auto* p = static_cast<bp::Problem*>(h);  // L_ref symbol of either family
     std::memcpy(out, p->reference_symbol().values.data(),
                 sizeof(cplx) * p->reference_symbol().values.size());
     return 0;
@@ -269,7 +303,7 @@ int bpref_symbol(void* h, double* out) {
 
 // op: 0 A, 1 V, 2 V^H, 3 Lref, 4 G, 5 forward DST, 6 inverse DST
 int bpref_apply(void* h, int op, const double* in, double* out) {
-    auto* p = static_cast<DirichletHelmholtz*>(h);
+    auto* p = static_cast<bp::Problem*>(h);
     return guarded([&] {
         ComplexField x = field_from(p->grid(), in);
         switch (op) {
@@ -279,13 +313,13 @@ int bpref_apply(void* h, int op, const double* in, double* out) {
             case 3: field_to(p->apply_Lref(x), out); break;
             case 4: field_to(p->apply_G(x), out); break;
             case 5: {
-                auto m = bp::forward_transform(x, bp::TransformKind::DST1);
+                auto m = bp::forward_transform(x, p->kind());
                 std::memcpy(out, m.data(), sizeof(cplx) * m.size());
                 break;
             }
             case 6: {
                 std::vector<cplx> m(x.data);
-                field_to(bp::inverse_transform(m, p->grid(), bp::TransformKind::DST1), out);
+                field_to(bp::inverse_transform(m, p->grid(), p->kind()), out);
                 break;
             }
             default: throw std::invalid_argument("bad op");
@@ -294,14 +328,14 @@ int bpref_apply(void* h, int op, const double* in, double* out) {
 }
 
 int bpref_born_residual(void* h, const double* u, const double* f, double* out) {
-    auto* p = static_cast<DirichletHelmholtz*>(h);
+    auto* p = static_cast<bp::Problem*>(h);
     return guarded([&] {
         field_to(p->born_residual(field_from(p->grid(), u), field_from(p->grid(), f)), out);
     });
 }
 
 int bpref_residual(void* h, const double* u, const double* f, double* out) {
-    auto* p = static_cast<DirichletHelmholtz*>(h);
+    auto* p = static_cast<bp::Problem*>(h);
     return guarded([&] {
         field_to(residual(*p, field_from(p->grid(), u), field_from(p->grid(), f)), out);
     });
@@ -310,7 +344,7 @@ int bpref_residual(void* h, const double* u, const double* f, double* out) {
 int bpref_run(void* h, int map_kind, double g_re, double g_im, int metric, const double* m,
               const double* f, int format, double rtol, int max_iters, const double* u0,
               double* u_out, double* res_l2, double* res_reta, TraceOut* info) {
-    auto* p = static_cast<DirichletHelmholtz*>(h);
+    auto* p = static_cast<bp::Problem*>(h);
     return guarded([&] {
         MapDesc md{map_kind, cplx(g_re, g_im), metric, m};
         ComplexField ff = field_from(p->grid(), f);

@@ -7,6 +7,7 @@ Python mirror of the reference's operator / map / driver API (api.py).
 from .api import (  # noqa: F401
     FourierDiagMap,
     HelmholtzDirichlet,
+    HelmholtzPeriodic,
     IterationConfig,
     IterationTrace,
     OptimalScalarMap,
@@ -19,7 +20,7 @@ from .instances import CONFIGS, InstanceSpec, config_instances, make_instances  
 from . import _native  # noqa: F401
 
 __all__ = [
-    "FourierDiagMap", "HelmholtzDirichlet", "IterationConfig", "IterationTrace", "OptimalScalarMap", "PointwiseMap",
+    "FourierDiagMap", "HelmholtzDirichlet", "HelmholtzPeriodic", "IterationConfig", "IterationTrace", "OptimalScalarMap", "PointwiseMap",
     "RunResult", "ScalarMap", "run", "CONFIGS", "InstanceSpec", "config_instances",
     "make_instances",
 ]

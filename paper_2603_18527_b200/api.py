@@ -140,6 +140,8 @@ class HelmholtzDirichlet:
     five-point pattern of NewtonJacobianProblem (newton_problem.cpp:17-44).
     """
 
+    BC = BC_DIRICHLET
+
     def __init__(self, k2, k0, eta, lx: float = 1.0, device: int = 0, dim: int = 2):
         """k2: (batch, nx, ny) -- or (nx, ny) for one member; dim=3: (batch, n, n, n) or
         (n, n, n), the seven-point 3-D extension (config c3)."""
@@ -160,7 +162,7 @@ class HelmholtzDirichlet:
             rc = self._lib.bp_problem_create3d(C.byref(g3), self.batch, _ptr(k2), _ptr(k0),
                                                _ptr(eta), device, C.byref(h))
         else:
-            g = N.Grid(self.nx, self.ny, lx, lx, BC_DIRICHLET)
+            g = N.Grid(self.nx, self.ny, lx, lx, self.BC)
             rc = self._lib.bp_problem_create(C.byref(g), self.batch, _ptr(k2), _ptr(k0), _ptr(eta),
                                              device, C.byref(h))
         _check(rc)
@@ -250,6 +252,14 @@ class HelmholtzDirichlet:
                                            C.byref(c), C.byref(tm)))
         return {"kernel_launches": la.value, "active_sweeps": sw.value, "row_ms": r.value,
                 "col_ms": c.value, "timed_sweeps": tm.value}
+
+
+class HelmholtzPeriodic(HelmholtzDirichlet):
+    """The reference's own family: bp::HelmholtzProblem (helmholtz.cpp:11-53), periodic
+    pseudospectral, A = F^-1(|xi|^2 F u) - k2 u, FFT basis; nx = ny = 2^k nodes, h = lx/nx.
+    On the GPU the iterate is carried in Fourier space (maps: ScalarMap, FourierDiagMap)."""
+
+    BC = BC_PERIODIC
 
 
 def run(problem: HelmholtzDirichlet, cmap, f, config: IterationConfig | None = None, u0=None,

@@ -85,7 +85,8 @@ __global__ void unpack_kernel(const double2* __restrict__ p0, const double2* __r
 __global__ void pointwise_kernel(int op, const double2* __restrict__ u, const double2* __restrict__ k2,
                                  const double2* __restrict__ f, const double* __restrict__ k0sq,
                                  const double* __restrict__ eta, double inv_h2,
-                                 double2* __restrict__ out, int batch, int log2n, int dim) {
+                                 double2* __restrict__ out, int batch, int log2n, int dim,
+                                 int pad = 1) {
     const int n = 1 << log2n;
     const size_t total = (size_t)batch << (dim * log2n);
     const size_t plane = (size_t)n * n;
@@ -95,7 +96,7 @@ __global__ void pointwise_kernel(int op, const double2* __restrict__ u, const do
         const int i = (int)((idx >> log2n) & (n - 1)), j = (int)(idx & (n - 1));
         const int x = dim == 3 ? (int)((idx >> (2 * log2n)) & (n - 1)) : 1;
         double2 o = make_double2(0.0, 0.0);
-        if (i > 0 && j > 0 && x > 0) {
+        if (!pad || (i > 0 && j > 0 && x > 0)) {
             const double2 uu = u[idx], kk = k2[idx];
             const double2 shift = make_double2(k0sq[b], eta[b]);
             if (op == 1) {
@@ -146,6 +147,16 @@ __global__ void norm_final_kernel(const double* __restrict__ partials, int nchun
     double s = 0.0;
     for (int c = 0; c < nchunk; ++c) s += partials[b * nchunk + c];
     out[b] = sqrt(s);
+}
+
+// y = y - v (and y = f - y when f != null): the periodic A = L_ref - V combination
+__global__ void combine_kernel(double2* __restrict__ y, const double2* __restrict__ v,
+                               const double2* __restrict__ f, size_t total) {
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const double2 a = csub(y[idx], v[idx]);
+        y[idx] = f ? csub(f[idx], a) : a;
+    }
 }
 
 __global__ void init_control_kernel(Control c, int batch) {
@@ -204,6 +215,11 @@ cudaError_t launch_col_pp(int log2n, int pp, int layout, int mode, const ColArgs
     BS_SIZE_CASES(launch_col_L, pp, layout, mode, a, s, prep)
 }
 
+cudaError_t launch_periodic(int log2n, bool row, int mode, const PerArgs& a, cudaStream_t s,
+                            bool prep = false) {
+    BS_SIZE_CASES(launch_periodic_L, row, mode, a, s, prep)
+}
+
 cudaError_t launch_row(int log2n, int dim, int mode, const RowArgs& a, cudaStream_t s) {
     return launch_row_pp(log2n, points_per_thread(log2n), dim, mode, a, s);
 }
@@ -214,7 +230,14 @@ cudaError_t launch_col(int log2n, int layout, int mode, const ColArgs& a, cudaSt
 cudaError_t prepare_kernels(int log2n, int dim) {
     RowArgs a{};
     ColArgs c{};
+    PerArgs pa{};
     cudaError_t e = cudaSuccess;
+    if (dim == 2) {
+        for (int mode : {RP_FWD, RP_FWD_BORN, RP_INV, RP_SWEEP})
+            if (cudaError_t r = launch_periodic(log2n, true, mode, pa, nullptr, true)) e = r;
+        for (int mode : {CP_ONE, CP_GREEN, CP_LREF, CP_SWEEP, CP_INV})
+            if (cudaError_t r = launch_periodic(log2n, false, mode, pa, nullptr, true)) e = r;
+    }
     for (int pp : {8, 16}) {
         for (int mode : {R_FWD, R_FWD_BORN, R_INV, R_SWEEP, R_OPT_A, R_OPT_B, R_RETA_A, R_RETA_C,
                          R_FD_A, R_FD_B})
@@ -269,6 +292,8 @@ int grid_for(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 16)
 struct bp_problem {
     bp_grid grid{};
     int batch = 0, device = 0, log2n = 0, n = 0, dim = 2;
+    bool periodic = false;   // the reference's own HelmholtzProblem (FFT basis, no padding)
+    double* xi2 = nullptr;   // periodic: xi_j^2, FFT order
     size_t field = 0;   // padded elements per member (n^dim)
     size_t alloc = 0;   // padded elements per buffer (batch*n^dim + n^(dim-1): zero halo)
     size_t dense_pts = 0;  // reference-layout points per member ((n-1)^dim)
@@ -392,6 +417,10 @@ int upload(bp_problem* p, const double* host, double2* dst, bool host_ptr = true
         CU(cudaMemcpyAsync(p->dense, host, bytes, cudaMemcpyHostToDevice, p->stream));
         src = p->dense;
     }
+    if (p->periodic) {  // no padding: the dense layout is the device layout
+        CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, p->stream));
+        return BP_OK;
+    }
     pack_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(src, dst, p->batch, p->log2n,
                                                                        p->dim);
     CU(cudaGetLastError());
@@ -402,8 +431,12 @@ int download(bp_problem* p, const double2* p0, const double2* p1, const int* sel
              bool host_ptr = true) {
     const size_t nd = p->dense_pts;
     double2* dst = host_ptr ? p->dense : reinterpret_cast<double2*>(host);
-    unpack_kernel<<<grid_for(nd * p->batch), 256, 0, p->stream>>>(p0, p1, select, dst, p->batch,
-                                                                   p->log2n, p->dim);
+    if (p->periodic) {  // select must be null: the periodic result is produced into p0
+        CU(cudaMemcpyAsync(dst, p0, sizeof(double2) * nd * p->batch, cudaMemcpyDeviceToDevice, p->stream));
+    } else {
+        unpack_kernel<<<grid_for(nd * p->batch), 256, 0, p->stream>>>(p0, p1, select, dst, p->batch,
+                                                                       p->log2n, p->dim);
+    }
     CU(cudaGetLastError());
     if (host_ptr)
         CU(cudaMemcpyAsync(host, p->dense, sizeof(double2) * nd * p->batch, cudaMemcpyDeviceToHost,
@@ -680,13 +713,16 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     return BP_OK;
 }
 
+int finish_run_periodic(bp_problem* p, double* u_out, bool host_ptr);
+
 int finish_run(bp_problem* p, const bp_iter_config* cfg, double* u_out, bool host_ptr,
                double* res_l2, double* res_reta, bp_trace* info) {
     const int B = p->batch;
     Control c = make_control(p);
-    int rc = download(p, p->u0, p->u1, c.result_buf, u_out, host_ptr);
+    int rc = p->periodic ? finish_run_periodic(p, u_out, host_ptr)
+                         : download(p, p->u0, p->u1, c.result_buf, u_out, host_ptr);
     if (rc) return rc;
-    p->stat_launches += 1;  // unpack
+    if (!p->periodic) p->stat_launches += 1;  // unpack
     std::vector<int> iters(B), term(B);
     std::vector<double> f1(B), f2(B);
     CU(cudaMemcpyAsync(iters.data(), c.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, p->stream));
@@ -715,6 +751,185 @@ int finish_run(bp_problem* p, const bp_iter_config* cfg, double* u_out, bool hos
     return BP_OK;
 }
 
+
+// ------------------------------------------------------------------ periodic family (host)
+PerArgs per_args(const bp_problem* p) {
+    PerArgs a{};
+    a.batch = p->batch;
+    a.k0sq = p->k0sq;
+    a.eta = p->eta;
+    a.xi2 = p->xi2;
+    a.k2 = p->k2;
+    a.f = p->f;
+    a.T = p->T;
+    a.U0 = p->u0;
+    a.U1 = p->u1;
+    a.fd = p->fd;
+    a.tw = p->tw;
+    a.scale = 1.0;
+    a.inv_npts = 1.0 / ((double)p->n * p->n);
+    a.map_kind = MK_SCALAR;
+    a.gamma = make_double2(1.0, 0.0);
+    a.ctl = make_control(p);
+    return a;
+}
+
+#define CUP(call) CU(call)
+
+// Green / L_ref / transforms on padded-free periodic fields: in -> out (out - sub)
+int periodic_apply(bp_problem* p, int which, const double2* in, double2* out, const double2* sub) {
+    PerArgs a = per_args(p);
+    const double inv = 1.0 / ((double)p->n * p->n);
+    a.in = in;
+    switch (which) {
+        case 0:  // G q = F^-1(F q / lambda)   (apply_symbol Divide, symbol.cpp:19-39)
+        case 1:  // born: G(V u + f) - u
+        case 2:  // L_ref
+            CUP(launch_periodic(p->log2n, true, which == 1 ? RP_FWD_BORN : RP_FWD, a, p->stream));
+            a.scale = inv;
+            CUP(launch_periodic(p->log2n, false, which == 2 ? CP_LREF : CP_GREEN, a, p->stream));
+            a.out = out;
+            a.sub = sub;
+            CUP(launch_periodic(p->log2n, true, RP_INV, a, p->stream));
+            return BP_OK;
+        case 3:  // forward transform (unnormalised DFT, transforms.hpp:16)
+            CUP(launch_periodic(p->log2n, true, RP_FWD, a, p->stream));
+            a.scale = 1.0;
+            CUP(launch_periodic(p->log2n, false, CP_ONE, a, p->stream));
+            CUP(cudaMemcpyAsync(out, p->T, sizeof(double2) * p->field * p->batch,
+                                cudaMemcpyDeviceToDevice, p->stream));
+            return BP_OK;
+        case 4:  // inverse transform (backward DFT / (nx ny))
+            a.T = const_cast<double2*>(in);
+            a.out = out;
+            CUP(launch_periodic(p->log2n, true, RP_INV, a, p->stream));
+            a.T = out;
+            a.scale = inv;
+            CUP(launch_periodic(p->log2n, false, CP_INV, a, p->stream));
+            return BP_OK;
+    }
+    return set_err(BP_EINVAL, "bad periodic op");
+}
+
+__global__ void select_copy_kernel(const double2* __restrict__ p0, const double2* __restrict__ p1,
+                                   const int* __restrict__ select, double2* __restrict__ out,
+                                   size_t per, int batch) {
+    const size_t total = per * batch;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t b = idx / per;
+        out[idx] = (select && select[b]) ? p1[idx] : p0[idx];
+    }
+}
+
+// bp::run for the periodic family: the iterate lives in Fourier space (U0/U1 ping-pong)
+int run_core_periodic(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool have_u0,
+                      double* snapshots, int n_snap) {
+    const int B = p->batch;
+    PerArgs a = per_args(p);
+    a.ctl.max_iters = cfg->max_iters;
+    a.ctl.rtol = cfg->rtol;
+    a.map_kind = map->kind == BP_MAP_FOURIER_DIAG ? MK_FOURIER_DIAG : MK_SCALAR;
+    a.gamma = make_double2(map->gamma_re, map->gamma_im);
+    if (map->kind == BP_MAP_FOURIER_DIAG) {
+        CU(cudaMemcpyAsync(p->fd, map->m, sizeof(double2) * p->field, cudaMemcpyHostToDevice, p->stream));
+    }
+    // fnorm_l2 = ||f||, fnorm_reta = ||G f||  (iterate.cpp:93,102)
+    if (int rc = norms(p, p->f, p->fnorm_l2)) return rc;
+    if (int rc = periodic_apply(p, 0, p->f, p->y, nullptr)) return rc;
+    if (int rc = norms(p, p->y, p->fnorm_reta)) return rc;
+    std::vector<double> fn(B);
+    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    for (int b = 0; b < B; ++b)
+        if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
+    // U^0 = F u0 (u0 staged in p->x by the caller) or 0
+    if (have_u0) {
+        if (int rc = periodic_apply(p, 3, p->x, p->u0, nullptr)) return rc;
+    } else {
+        CU(cudaMemsetAsync(p->u0, 0, sizeof(double2) * p->alloc, p->stream));
+        CU(cudaMemsetAsync(p->x, 0, sizeof(double2) * p->alloc, p->stream));
+    }
+    CU(cudaMemsetAsync(p->u1, 0, sizeof(double2) * p->alloc, p->stream));
+    init_control_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(a.ctl, B);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_l2, (size_t)B * p->trace_cap);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_reta, (size_t)B * p->trace_cap);
+    CU(cudaGetLastError());
+    // T = F_y q^0, q^0 = V u^0 + f (u^0 physical in p->x)
+    a.in = p->x;
+    CU(launch_periodic(p->log2n, true, RP_FWD_BORN, a, p->stream));
+    p->stat_launches = 16 + (have_u0 ? 2 : 0);
+    p->stat_row_ms = p->stat_col_ms = 0;
+    p->stat_timed = 0;
+    const long max_launch = (long)cfg->max_iters + 1;
+    const size_t nd = p->dense_pts;
+    auto sweep = [&](cudaEvent_t* ev) -> int {
+        if (ev) CU(cudaEventRecord(ev[0], p->stream));
+        CU(launch_periodic(p->log2n, false, CP_SWEEP, a, p->stream));
+        if (ev) CU(cudaEventRecord(ev[1], p->stream));
+        CU(launch_periodic(p->log2n, true, RP_SWEEP, a, p->stream));
+        if (ev) CU(cudaEventRecord(ev[2], p->stream));
+        return BP_OK;
+    };
+    if (snapshots && n_snap > 0) {
+        // u^0 = F^-1 U^0
+        if (int rc = periodic_apply(p, 4, p->u0, p->y, nullptr)) return rc;
+        if (int rc = download(p, p->y, nullptr, nullptr, snapshots)) return rc;
+        for (long k = 1; k <= max_launch; ++k) {
+            if (int rc = sweep(nullptr)) return rc;
+            p->stat_launches += 2;
+            if (k < n_snap) {  // u^k = F^-1 U^k, U^k in buffer k&1
+                if (int rc = periodic_apply(p, 4, (k & 1) ? p->u1 : p->u0, p->y, nullptr)) return rc;
+                if (int rc = download(p, p->y, nullptr, nullptr, snapshots + 2 * nd * B * k)) return rc;
+            }
+            CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
+                               p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            if (*p->host_active == 0) break;
+        }
+        return BP_OK;
+    }
+    std::vector<cudaEvent_t> ev;
+    if (p->timing) {
+        ev.resize(3 * kGraphSweeps);
+        for (auto& e : ev) CU(cudaEventCreate(&e));
+    }
+    long launched = 0;
+    int rc = BP_OK;
+    while (launched < max_launch && rc == BP_OK) {
+        for (int s = 0; s < kGraphSweeps && rc == BP_OK; ++s) rc = sweep(p->timing ? &ev[3 * s] : nullptr);
+        if (rc) break;
+        launched += kGraphSweeps;
+        p->stat_launches += 2 * kGraphSweeps;
+        CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
+                           p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+        if (p->timing) {
+            for (int s = 0; s < kGraphSweeps; ++s) {
+                float c = 0, r = 0;
+                cudaEventElapsedTime(&c, ev[3 * s], ev[3 * s + 1]);
+                cudaEventElapsedTime(&r, ev[3 * s + 1], ev[3 * s + 2]);
+                p->stat_col_ms += c;
+                p->stat_row_ms += r;
+                ++p->stat_timed;
+            }
+        }
+        if (*p->host_active == 0) break;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return rc;
+}
+
+int finish_run_periodic(bp_problem* p, double* u_out, bool host_ptr) {
+    Control c = make_control(p);
+    select_copy_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(
+        p->u0, p->u1, c.result_buf, p->x, p->field, p->batch);
+    CU(cudaGetLastError());
+    if (int rc = periodic_apply(p, 4, p->x, p->y, nullptr)) return rc;  // u = F^-1 U
+    p->stat_launches += 3;
+    return download(p, p->y, nullptr, nullptr, u_out, host_ptr);
+}
+
 int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* cfg) {
     if (int rc = check_problem(p)) return rc;
     if (!map || !cfg) return set_err(BP_EINVAL, "run: null map or config");
@@ -729,6 +944,8 @@ int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* c
     if (map->kind == BP_MAP_OPTIMAL_SCALAR && map->metric != BP_METRIC_EUCLIDEAN &&
         map->metric != BP_METRIC_RETA)
         return set_err(BP_EINVAL, "unknown optimal-scalar metric");
+    if (p->periodic && (map->kind == BP_MAP_OPTIMAL_SCALAR || map->kind == BP_MAP_POINTWISE))
+        return set_err(BP_ENOTSUP, "periodic family on the GPU: scalar and FourierDiag maps only");
     return BP_OK;
 }
 
@@ -744,16 +961,44 @@ int bp_abi_version(void) { return BP_ABI_VERSION; }
 namespace {
 
 // Shared constructor of the 2-D (dim 2) and 3-D (dim 3, cubic) Dirichlet Helmholtz batches.
+// xi_j = 2 pi m_j / L with m_j in FFT order (wavenumbers_1d Periodic, grid.hpp:67-85)
+std::vector<double> xi2_table(int n, double len) {
+    std::vector<double> xi2(n);
+    for (int i = 0; i < n; ++i) {
+        const int m = (i < (n + 1) / 2) ? i : i - n;
+        const double xi = 2.0 * kPi * m / len;
+        xi2[i] = xi * xi;
+    }
+    return xi2;
+}
+
+int check_symbol_periodic(const std::vector<double>& xi2, int batch, const double* k0, const double* eta) {
+    for (int b = 0; b < batch; ++b) {
+        double mn = INFINITY, mx = 0.0;
+        const double k0sq = k0[b] * k0[b];
+        for (double a : xi2)
+            for (double c : xi2) {
+                const double v = std::hypot((a + c) - k0sq, -eta[b]);
+                mn = std::min(mn, v);
+                mx = std::max(mx, v);
+            }
+        if (mn < kSymbolDivGuard * mx)
+            return set_err(BP_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
+    }
+    return BP_OK;
+}
+
 int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, const double* k0,
-                const double* eta, int32_t device, bp_problem** out) {
-    const int n = grid->nx + 1;
+                const double* eta, int32_t device, bp_problem** out, bool periodic = false) {
+    // Dirichlet: n = nx + 1 cells (interior nx); periodic: n = nx nodes (helmholtz.cpp:11-25)
+    const int n = periodic ? grid->nx : grid->nx + 1;
     int log2n = 0;
     while ((1 << log2n) < n) ++log2n;
     const int max_log2 = dim == 3 ? kMaxLog2_3d : kMaxLog2;
     if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > max_log2)
-        return set_err(BP_ENOTSUP, dim == 3
-            ? "GPU path needs cubic grids with n+1 = 2^k, 8 <= 2^k <= 512"
-            : "GPU path needs square grids with nx+1 = 2^k, 8 <= 2^k <= 4096");
+        return set_err(BP_ENOTSUP, periodic ? "GPU periodic path needs square grids with nx = 2^k, 8 <= 2^k <= 4096"
+                                   : dim == 3 ? "GPU path needs cubic grids with n+1 = 2^k, 8 <= 2^k <= 512"
+                                              : "GPU path needs square grids with nx+1 = 2^k, 8 <= 2^k <= 4096");
     if (grid->lx != grid->ly) return set_err(BP_ENOTSUP, "GPU path needs lx == ly (hx == hy)");
     size_t nd = (size_t)grid->nx * grid->ny;
     if (dim == 3) nd *= grid->nx;
@@ -764,7 +1009,12 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     for (size_t k = 0; k < 2 * nd * batch; ++k)
         if (!std::isfinite(k2[k])) return set_err(BP_EINVAL, "HelmholtzProblem: k2 not finite");
 
-    if (int rc = check_symbol(*grid, dim, batch, k0, eta)) return rc;
+    const std::vector<double> xi2 = xi2_table(n, grid->lx);
+    if (periodic) {
+        if (int rc = check_symbol_periodic(xi2, batch, k0, eta)) return rc;
+    } else if (int rc = check_symbol(*grid, dim, batch, k0, eta)) {
+        return rc;
+    }
     const double h = grid->lx / n;
     std::vector<double> lap = lap_table(n, h);
 
@@ -779,6 +1029,7 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     p->log2n = log2n;
     p->n = n;
     p->dim = dim;
+    p->periodic = periodic;
     p->field = (size_t)1 << (dim * log2n);
     p->alloc = p->field * batch + ((size_t)1 << ((dim - 1) * log2n));
     p->dense_pts = nd;
@@ -823,6 +1074,8 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     CUF(cudaMalloc(&p->tw, sizeof(double2) * n));
     CUF(cudaMalloc(&p->sinp, sizeof(double) * n));
     CUF(cudaMalloc(&p->lap, sizeof(double) * n));
+    CUF(cudaMalloc(&p->xi2, sizeof(double) * n));
+    CUF(cudaMemcpyAsync(p->xi2, xi2.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
     std::vector<double> k0sq(batch), tw(2 * n), sinp(n);
     for (int b = 0; b < batch; ++b) k0sq[b] = k0[b] * k0[b];
     for (int k = 0; k < n; ++k) {
@@ -855,8 +1108,10 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
     if (grid->nx < 2 || grid->ny < 2) return set_err(BP_EINVAL, "GridSpec: nx,ny must be >= 2");
     if (!(grid->lx > 0.0) || !(grid->ly > 0.0)) return set_err(BP_EINVAL, "GridSpec: lx,ly must be > 0");
     if (batch < 1) return set_err(BP_EINVAL, "batch must be >= 1");
+    if (grid->bc == BP_BC_PERIODIC)  // the reference's own HelmholtzProblem
+        return create_impl(grid, 2, batch, k2, k0, eta, device, out, true);
     if (grid->bc != BP_BC_DIRICHLET)
-        return set_err(BP_ENOTSUP, "only DirichletInterior grids are implemented on the GPU");
+        return set_err(BP_ENOTSUP, "Neumann grids are not implemented on the GPU");
     return create_impl(grid, 2, batch, k2, k0, eta, device, out);
 }
 
@@ -887,7 +1142,7 @@ int bp_problem_destroy(bp_problem* p) {
                     (void*)p->y, (void*)p->dense, (void*)p->partial, (void*)p->gamma, (void*)p->fd, (void*)p->norm_part,
                     (void*)p->fnorm_l2, (void*)p->fnorm_reta, (void*)p->ctl_int, (void*)p->counter,
                     (void*)p->trace_l2, (void*)p->trace_reta, (void*)p->k0sq, (void*)p->eta,
-                    (void*)p->tw, (void*)p->sinp, (void*)p->lap})
+                    (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2})
         if (q) cudaFree(q);
     if (p->host_active) cudaFreeHost(p->host_active);
     if (p->stream) cudaStreamDestroy(p->stream);
@@ -910,8 +1165,19 @@ static int pointwise_op(const bp_problem* cp, int op, const double* u, const dou
     if (int rc = upload(p, u, p->x)) return rc;
     if (op == 3)
         if (int rc = upload(p, f, p->f)) return rc;
-    pointwise_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(
-        op, p->x, p->k2, p->f, p->k0sq, p->eta, p->inv_h2, p->y, p->batch, p->log2n, p->dim);
+    if (p->periodic && (op == 0 || op == 3)) {
+        // pseudospectral A = L_ref - V (helmholtz.cpp:27-32 computes F^-1(|xi|^2 F u) - k2 u;
+        // equal to roundoff): y = L_ref x, then y -= V x (and f - y for the residual)
+        if (int rc = periodic_apply(p, 2, p->x, p->y, nullptr)) return rc;
+        pointwise_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(
+            1, p->x, p->k2, p->f, p->k0sq, p->eta, p->inv_h2, p->T, p->batch, p->log2n, p->dim, 0);
+        combine_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(
+            p->y, p->T, op == 3 ? p->f : nullptr, p->field * p->batch);
+    } else {
+        pointwise_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(
+            op, p->x, p->k2, p->f, p->k0sq, p->eta, p->inv_h2, p->y, p->batch, p->log2n, p->dim,
+            p->periodic ? 0 : 1);
+    }
     CU(cudaGetLastError());
     if (int rc = download(p, p->y, p->y, nullptr, out)) return rc;
     CU(cudaStreamSynchronize(p->stream));
@@ -929,6 +1195,14 @@ static int spectral_op(const bp_problem* cp, int which, const double* in, const 
     auto* p = const_cast<bp_problem*>(cp);
     DeviceGuard guard(p->device);
     if (int rc = upload(p, in, p->x)) return rc;
+    if (p->periodic) {
+        if (which == 1)
+            if (int rc = upload(p, f, p->f)) return rc;
+        if (int rc = periodic_apply(p, which, p->x, p->y, which == 1 ? p->x : nullptr)) return rc;
+        if (int rc = download(p, p->y, nullptr, nullptr, out)) return rc;
+        CU(cudaStreamSynchronize(p->stream));
+        return BP_OK;
+    }
     RowArgs a = row_args(p);
     ColArgs c = col_args(p);
     a.in = p->x;
@@ -983,9 +1257,11 @@ static int run_impl(const bp_problem* cp, const bp_map* map, const double* f, co
     DeviceGuard guard(p->device);
     if (int rc = ensure_trace(p, cfg->max_iters)) return rc;
     if (int rc = upload(p, f, p->f, host_ptr)) return rc;
-    if (u0)
-        if (int rc = upload(p, u0, p->u0, host_ptr)) return rc;
-    if (int rc = run_core(p, map, cfg, u0 != nullptr, snapshots, n_snap)) return rc;
+    if (u0)  // periodic: the physical u0 is transformed into U^0 by run_core_periodic
+        if (int rc = upload(p, u0, p->periodic ? p->x : p->u0, host_ptr)) return rc;
+    const int rc = p->periodic ? run_core_periodic(p, map, cfg, u0 != nullptr, snapshots, n_snap)
+                               : run_core(p, map, cfg, u0 != nullptr, snapshots, n_snap);
+    if (rc) return rc;
     return finish_run(p, cfg, u_out, host_ptr, res_l2, res_reta, info);
 }
 

@@ -2,6 +2,7 @@
 // sweep_L*.cu, so the instantiations compile in parallel).
 #pragma once
 
+#include "periodic_kernels.cuh"
 #include "sweep_kernels.cuh"
 
 namespace bs {
@@ -65,6 +66,46 @@ cudaError_t launch_col_p(int mode, const ColArgs& a, cudaStream_t s, bool prepar
     }
 }
 
+// ---- periodic family (FFT engine)
+template <int L, int MODE, int PP>
+cudaError_t launch_prow_t(const PerArgs& a, cudaStream_t s, bool prepare) {
+    using RG = RowGeom<L, PP, kRowWarps>;
+    auto k = prow_kernel<L, MODE, kRowWarps, PP>;
+    if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
+    const long rows = (long)a.batch << L;
+    k<<<(int)((rows + RG::EPB - 1) / RG::EPB), kRowWarps * 32, RG::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int L, int MODE, int PP>
+cudaError_t launch_pcol_t(const PerArgs& a, cudaStream_t s, bool prepare) {
+    constexpr int C = ColCols<L>::value;
+    using CG = ColGeom<L, PP, C>;
+    auto k = pcol_kernel<L, MODE, C, PP>;
+    if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
+    k<<<a.batch * ((1 << L) / C), CG::THREADS, CG::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int L>
+cudaError_t launch_periodic_p(bool row, int mode, const PerArgs& a, cudaStream_t s, bool prep) {
+    if (row) {
+        switch (mode) {
+            case RP_FWD: return launch_prow_t<L, RP_FWD, 16>(a, s, prep);
+            case RP_FWD_BORN: return launch_prow_t<L, RP_FWD_BORN, 16>(a, s, prep);
+            case RP_INV: return launch_prow_t<L, RP_INV, 16>(a, s, prep);
+            default: return launch_prow_t<L, RP_SWEEP, 16>(a, s, prep);
+        }
+    }
+    switch (mode) {
+        case CP_ONE: return launch_pcol_t<L, CP_ONE, 16>(a, s, prep);
+        case CP_GREEN: return launch_pcol_t<L, CP_GREEN, 16>(a, s, prep);
+        case CP_LREF: return launch_pcol_t<L, CP_LREF, 16>(a, s, prep);
+        case CP_INV: return launch_pcol_t<L, CP_INV, 16>(a, s, prep);
+        default: return launch_pcol_t<L, CP_SWEEP, 16>(a, s, prep);
+    }
+}
+
 // 3-D kernels exist for n <= 512 (P = 16)
 constexpr int kMaxLog2_3d = 9;
 
@@ -93,13 +134,19 @@ struct Pp8 {
         }                                                                                       \
         if (pp == 8) return launch_col_p<L, Pp8<L>::value>(mode, a, s, prep);                   \
         return launch_col_p<L, 16>(mode, a, s, prep);                                           \
+    }                                                                                           \
+    cudaError_t launch_periodic_L##L(bool row, int mode, const PerArgs& a, cudaStream_t s,      \
+                                     bool prep) {                                               \
+        return launch_periodic_p<L>(row, mode, a, s, prep);                                     \
     }
 
 #define BS_DECLARE_SIZE(L)                                                                      \
     cudaError_t launch_row_L##L(int pp, int dim, int mode, const RowArgs& a, cudaStream_t s,     \
                                 bool prep);                                                     \
     cudaError_t launch_col_L##L(int pp, int layout, int mode, const ColArgs& a, cudaStream_t s,  \
-                                bool prep);
+                                bool prep);                                                     \
+    cudaError_t launch_periodic_L##L(bool row, int mode, const PerArgs& a, cudaStream_t s,      \
+                                     bool prep);
 
 BS_DECLARE_SIZE(3)
 BS_DECLARE_SIZE(4)

@@ -96,6 +96,34 @@ def run_golden():
         print(name, r.iters, r.terminated)
 
 
+def periodic_golden():
+    """The reference's OWN HelmholtzProblem (periodic pseudospectral) on its own bench instance
+    generator (make_layered_helmholtz + bump source, bench.cpp:25-67)."""
+    rng = np.random.default_rng(3)
+    for n, seed in [(32, 5), (64, 7)]:
+        k2, f, k0, eta = Reference.periodic_bench_instance(n, 16.0, 2.0, seed)
+        p = ReferenceProblem(k2, k0, eta, periodic=True)
+        x = rng.standard_normal(k2.shape) + 1j * rng.standard_normal(k2.shape)
+        out = dict(k2=k2, f=f, k0=k0, eta=eta, x=x, A=p.apply_A(x), V=p.apply_V(x),
+                   VH=p.apply_V_adjoint(x), Lref=p.apply_Lref(x), G=p.apply_G(x),
+                   born=p.born_residual(x, f), res=p.residual(x, f), fwd=p.forward_dst(x),
+                   inv=p.inverse_dst(x), symbol=p.symbol())
+        m = 0.8 + 0.1 * (rng.standard_normal(k2.shape) + 1j * rng.standard_normal(k2.shape))
+        out["fd_m"] = m
+        for name, kw in [("scalar", dict(map_kind=MAP_SCALAR, gamma=1.0)),
+                         ("scalar_relaxed", dict(map_kind=MAP_SCALAR, gamma=0.9 + 0.05j)),
+                         ("optl2", dict(map_kind=MAP_OPTIMAL_SCALAR, metric=0)),
+                         ("fd", dict(map_kind=2, m=m))]:
+            r = p.run(f, rtol=1e-8, max_iters=4000, **kw)
+            out[f"run_{name}_u"] = r.u
+            out[f"run_{name}_l2"] = r.res_l2
+            out[f"run_{name}_reta"] = r.res_reta
+            out[f"run_{name}_iters"] = r.iters
+            out[f"run_{name}_term"] = r.terminated
+            print("periodic", n, name, r.iters, r.terminated)
+        np.savez_compressed(os.path.join(HERE, f"ref_periodic_n{n}.npz"), **out)
+
+
 if __name__ == "__main__":
     Reference.set_mode("serial")
     dst_golden()
@@ -104,4 +132,5 @@ if __name__ == "__main__":
     sampler_golden()
     ops_golden()
     run_golden()
+    periodic_golden()
     print("golden fixtures written to", HERE)

@@ -231,3 +231,30 @@ def test_3d_oracle_dst_and_identities():
     A = np.stack([ps.apply_A(e[k].reshape(3, 3, 3)).ravel() for k in range(27)], axis=1)
     ev = np.sort(np.linalg.eigvalsh(A.real))
     assert np.abs(np.sort((ps.symbol() + 1j).real.ravel()) - ev).max() < 1e-10 * ev.max()
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_oracle_periodic_matches_reference_helmholtz(n):
+    """The oracle's periodic family vs the reference's OWN bp::HelmholtzProblem (fixtures from
+    oracle/_ref on the reference's own bench instance generator)."""
+    g = _load(f"ref_periodic_n{n}.npz")
+    p = OracleProblem(g["k2"], float(g["k0"]), float(g["eta"]), periodic=True)
+    x, f = g["x"], g["f"]
+    assert rel(p.symbol(), g["symbol"]) < 1e-15
+    for name, ref in [("apply_A", "A"), ("apply_V", "V"), ("apply_V_adjoint", "VH"),
+                      ("apply_Lref", "Lref"), ("apply_G", "G")]:
+        assert rel(getattr(p, name)(x), g[ref]) < 1e-13, name
+    assert rel(p.born_residual(x, f), g["born"]) < 1e-13
+    assert rel(p.residual(x, f), g["res"]) < 1e-13
+    runs = {"scalar": dict(map_kind=MAP_SCALAR, gamma=1.0),
+            "scalar_relaxed": dict(map_kind=MAP_SCALAR, gamma=0.9 + 0.05j),
+            "optl2": dict(map_kind=MAP_OPTIMAL_SCALAR, metric=0),
+            "fd": dict(map_kind=MAP_FOURIER_DIAG, m=g["fd_m"])}
+    for name, kw in runs.items():
+        r = p.run(f, rtol=1e-8, max_iters=4000, **kw)
+        assert abs(r.iters - int(g[f"run_{name}_iters"])) <= 1, name
+        assert r.terminated == str(g[f"run_{name}_term"])
+        k = min(len(r.res_l2), len(g[f"run_{name}_l2"]))
+        assert np.abs(r.res_l2[:k] - g[f"run_{name}_l2"][:k]).max() < 1e-10
+        if r.iters == int(g[f"run_{name}_iters"]):
+            assert rel(r.u, g[f"run_{name}_u"]) < 1e-9
