@@ -220,6 +220,11 @@ cudaError_t launch_periodic(int log2n, bool row, int mode, const PerArgs& a, cud
     BS_SIZE_CASES(launch_periodic_L, row, mode, a, s, prep)
 }
 
+cudaError_t launch_transposed(int log2n, bool row, int mode, const RowArgs& a, const ColArgs& c,
+                              cudaStream_t s, bool prep = false) {
+    BS_SIZE_CASES(launch_transposed_L, row, mode, a, c, s, prep)
+}
+
 cudaError_t launch_row(int log2n, int dim, int mode, const RowArgs& a, cudaStream_t s) {
     return launch_row_pp(log2n, points_per_thread(log2n), dim, mode, a, s);
 }
@@ -232,6 +237,12 @@ cudaError_t prepare_kernels(int log2n, int dim) {
     ColArgs c{};
     PerArgs pa{};
     cudaError_t e = cudaSuccess;
+    if (dim == 2 && log2n <= 9) {
+        for (int mode : {R_FWD_BORN, R_SWEEP, R_OPT_B, R_RETA_A, R_FD_A, R_FD_B})
+            if (cudaError_t r = launch_transposed(log2n, true, mode, a, c, nullptr, true)) e = r;
+        for (int mode : {C_GREEN, C_FD})
+            if (cudaError_t r = launch_transposed(log2n, false, mode, a, c, nullptr, true)) e = r;
+    }
     if (dim == 2) {
         for (int mode : {RP_FWD, RP_FWD_BORN, RP_INV, RP_SWEEP})
             if (cudaError_t r = launch_periodic(log2n, true, mode, pa, nullptr, true)) e = r;
@@ -293,6 +304,8 @@ struct bp_problem {
     bp_grid grid{};
     int batch = 0, device = 0, log2n = 0, n = 0, dim = 2;
     bool periodic = false;   // the reference's own HelmholtzProblem (FFT basis, no padding)
+    bool transposed = false; // 2-D Dirichlet n <= 512: transposed row -> column handoff (TT)
+    double2* TT = nullptr;
     double* xi2 = nullptr;   // periodic: xi_j^2, FFT order
     size_t field = 0;   // padded elements per member (n^dim)
     size_t alloc = 0;   // padded elements per buffer (batch*n^dim + n^(dim-1): zero halo)
@@ -379,6 +392,7 @@ RowArgs row_args(const bp_problem* p) {
     a.T = p->T;
     a.u0 = p->u0;
     a.u1 = p->u1;
+    a.TT = p->TT;
     a.X = p->x;
     a.tw = p->tw;
     a.sinp = p->sinp;
@@ -396,6 +410,7 @@ ColArgs col_args(const bp_problem* p) {
     c.lap = p->lap;
     c.scale = p->green_scale;
     c.fd = p->fd;
+    c.TT = p->TT;
     c.T = p->T;
     c.tw = p->tw;
     c.sinp = p->sinp;
@@ -562,8 +577,22 @@ int sweep_once(bp_problem* p, const SweepPlan& plan, const RowArgs& a, const Col
                cudaEvent_t* ev) {
     if (ev) CU(cudaEventRecord(ev[0], p->stream));
     for (int k = 0; k < plan.n; ++k) {
-        if (plan.row[k]) CU(launch_row(p->log2n, p->dim, plan.mode[k], a, p->stream));
-        else if (int rc = col_stage_checked(p, c, plan.mode[k], p->green_scale)) return rc;
+        const int md = plan.mode[k];
+        if (p->transposed) {
+            // forward-writing row modes hand the column pass a transposed intermediate
+            const bool fwd = plan.row[k] && md != R_OPT_A && md != R_RETA_C;
+            if (!plan.row[k] || fwd) {
+                ColArgs cc = c;
+                cc.scale = p->green_scale;
+                CU(launch_transposed(p->log2n, plan.row[k], md, a, cc, p->stream));
+            } else {
+                CU(launch_row(p->log2n, p->dim, md, a, p->stream));
+            }
+        } else if (plan.row[k]) {
+            CU(launch_row(p->log2n, p->dim, md, a, p->stream));
+        } else if (int rc = col_stage_checked(p, c, md, p->green_scale)) {
+            return rc;
+        }
         if (ev) CU(cudaEventRecord(ev[k + 1], p->stream));
     }
     return BP_OK;
@@ -611,8 +640,15 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
 
     // q^0 = V u^0 + f -> forward y-DST -> T ; column pass
     a.in = p->u0;
-    CU(launch_row(p->log2n, p->dim, R_FWD_BORN, a, p->stream));
-    if (int rc2 = col_stage_checked(p, c, C_GREEN, p->green_scale)) return rc2;
+    if (p->transposed) {
+        ColArgs cc = c;
+        cc.scale = p->green_scale;
+        CU(launch_transposed(p->log2n, true, R_FWD_BORN, a, cc, p->stream));
+        CU(launch_transposed(p->log2n, false, C_GREEN, a, cc, p->stream));
+    } else {
+        CU(launch_row(p->log2n, p->dim, R_FWD_BORN, a, p->stream));
+        if (int rc2 = col_stage_checked(p, c, C_GREEN, p->green_scale)) return rc2;
+    }
 
     // kernels launched so far in this run: pack f (+ pack u0), 2x norms (2 each), Green
     // (2 row + column stage), init_control, 2x fill_nan, initial row pass + column stage
@@ -1058,6 +1094,15 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     CUF(cudaMalloc(&p->y, fb));
     for (double2* buf : {p->k2, p->f, p->u0, p->u1, p->T, p->x, p->y})
         CUF(cudaMemsetAsync(buf, 0, fb, p->stream));
+    {
+        // opt-in (BP_TRANSPOSED=1): measured equal to the default column pass on B200 (r01)
+        const char* e = std::getenv("BP_TRANSPOSED");
+        p->transposed = dim == 2 && !periodic && log2n <= 9 && e && std::atoi(e) == 1;
+    }
+    if (p->transposed) {
+        CUF(cudaMalloc(&p->TT, fb));
+        CUF(cudaMemsetAsync(p->TT, 0, fb, p->stream));
+    }
     CUF(cudaMalloc(&p->dense, sizeof(double2) * nd * batch));
     CUF(cudaMalloc(&p->partial, sizeof(double) * (size_t)batch * ((size_t)1 << ((dim - 1) * log2n)) *
                                     kPartStride));
@@ -1142,7 +1187,7 @@ int bp_problem_destroy(bp_problem* p) {
                     (void*)p->y, (void*)p->dense, (void*)p->partial, (void*)p->gamma, (void*)p->fd, (void*)p->norm_part,
                     (void*)p->fnorm_l2, (void*)p->fnorm_reta, (void*)p->ctl_int, (void*)p->counter,
                     (void*)p->trace_l2, (void*)p->trace_reta, (void*)p->k0sq, (void*)p->eta,
-                    (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2})
+                    (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2, (void*)p->TT})
         if (q) cudaFree(q);
     if (p->host_active) cudaFreeHost(p->host_active);
     if (p->stream) cudaStreamDestroy(p->stream);

@@ -93,6 +93,7 @@ struct RowArgs {
     double2* out;              // R_INV output (padded)
     const double2* sub;        // R_INV: optional field subtracted from the output
     double2* T;                // intermediate (padded)
+    double2* TT;               // transposed intermediate (TOUT kernels write it, tcol reads it)
     double2* u0;               // iterate ping
     double2* u1;               // iterate pong
     double2* X;                // direction x^m (optimal-scalar / FourierDiag modes)
@@ -110,6 +111,7 @@ struct ColArgs {
     const double* lap;         // (4/h^2) sin^2(j pi / (2n)), j < n
     double scale;              // C_ONE scale / Green normalisation 4/n^2 (/ engine gain)
     const double2* fd;         // C_FD: FourierDiag multiplier, padded n x n (shared by the batch)
+    const double2* TT;         // tcol: transposed input [member][q][i]
     double2* T;
     const double2* tw;
     const double* sinp;
@@ -210,7 +212,9 @@ struct RowGeom {
 // DIM = 2: lines are the rows of each member (x index i, y contiguous), five-point stencil.
 // DIM = 3: lines are the z-lines (x, y) of each member ([x][y][z], z contiguous), seven-point
 //          stencil (the 3-D extension of config c3; no reference counterpart).
-template <int LOG2N, int MODE, int NW, int PP, int DIM = 2>
+// TOUT: write the forward transform transposed ([member][q][i], a.TT) through a CTA-wide
+// shared-memory tile (128-B segments), for the warp-per-line column pass tcol_kernel.
+template <int LOG2N, int MODE, int NW, int PP, int DIM = 2, bool TOUT = false>
 __global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? 128 : 80>::value))
 row_kernel(const RowArgs a) {
     using G = Geom<LOG2N, PP>;
@@ -418,11 +422,26 @@ row_kernel(const RowArgs a) {
         Engine::run(q, qm, y2, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
         for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y2[l];
-        pol.sync();
+        if constexpr (TOUT) {
+            static_assert(DIM == 2 && T <= 32, "transposed handoff: 2-D lines of <= 512");
+            __syncthreads();
+            // tile (EPB rows x N) -> TT[b][q][i]: lanes = 8 consecutive rows x 4 modes
+            const long g0 = (long)blockIdx.x * EPB;
+            for (int k = threadIdx.x; k < EPB * N; k += NW * 32) {
+                const int ee = k % EPB, qq = k / EPB;
+                const long g = g0 + ee;
+                const int bb = (int)(g >> LOG2N);
+                if (bb < a.batch)
+                    a.TT[((size_t)bb << (2 * LOG2N)) + (size_t)qq * N + (g & (N - 1))] =
+                        smem[ee * G::PAD_N + G::pidx(qq)];
+            }
+        } else {
+            pol.sync();
 #pragma unroll
-        for (int mm = 0; mm < P; ++mm) {
-            const int j = t + T * mm;
-            if (valid) a.T[row + j] = buf[G::pidx(j)];
+            for (int mm = 0; mm < P; ++mm) {
+                const int j = t + T * mm;
+                if (valid) a.T[row + j] = buf[G::pidx(j)];
+            }
         }
     }
 
@@ -460,6 +479,85 @@ row_kernel(const RowArgs a) {
                 if constexpr (S::ENTRY) finalize_entry(a.ctl, b, m, s[0], s[1]);
             }
         }
+    }
+}
+
+// ------------------------------------------------------------------ transposed column kernel
+// Warp-per-line x-pass over the transposed intermediate written by the TOUT row kernel: line
+// (member b, mode q) = TT[b][q][0..n), forward x-DST, x w_pq (Green 4/(n^2 lambda) or the
+// FourierDiag m_pq), inverse x-DST, written back row-major T[b][i][q] through a CTA tile.
+template <int LOG2N, int MODE, int NW, int PP>
+__global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? 128 : 80>::value))
+tcol_kernel(const ColArgs a) {
+    using G = Geom<LOG2N, PP>;
+    using RG = RowGeom<LOG2N, PP, NW>;
+    using Pol = typename PolicyFor<G::T>::type;
+    using Engine = DstEngine<LOG2N, PP>;
+    constexpr int N = G::N, P = G::P, T = G::T;
+    constexpr int EPB = RG::EPB;
+    static_assert(T <= 32, "transposed column pass: lines of <= 512");
+    extern __shared__ double2 smem[];
+
+    const int t = threadIdx.x % T;
+    const int e = threadIdx.x / T;
+    const long g = (long)blockIdx.x * EPB + e;
+    const int b = (int)(g >> LOG2N);
+    const int q = (int)(g & (N - 1));
+    bool valid = b < a.batch;
+    if (valid && a.status) valid = __ldcg(&a.status[b]) == ST_ACTIVE;
+    if (!__syncthreads_or(valid)) return;
+    double2* buf = smem + e * G::PAD_N;
+    const Pol pol{};
+    const double2 zero = make_double2(0.0, 0.0);
+    const size_t line = ((size_t)(valid ? b : 0) << (2 * LOG2N)) + (size_t)q * N;
+
+    double2 x[P], xm[P], y[P];
+#pragma unroll
+    for (int mm = 0; mm < P; ++mm) {
+        const int j = t + T * mm;
+        x[mm] = valid ? a.TT[line + j] : zero;
+        xm[mm] = (valid && j != 0) ? a.TT[line + (N - j)] : zero;  // mirror: L1 hit
+    }
+    Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+    {
+        const double k0sq = valid ? a.k0sq[b] : 0.0, eta = valid ? a.eta[b] : 1.0;
+        const double lq = a.lap[q];
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+            const int p = t * P + l;
+            double2 w;
+            if constexpr (MODE == C_FD) {
+                w = cscale(a.fd[(size_t)p * N + q], a.scale);
+            } else {  // C_GREEN: scale / lambda, lambda = (a_p + a_q) - (k0^2 + i eta)
+                const double lr = (a.lap[p] + lq) - k0sq;
+                const double li = -eta;
+                const double s = a.scale * __drcp_rn(fma(lr, lr, li * li));
+                w = make_double2(lr * s, -li * s);
+            }
+            y[l] = (p == 0 || q == 0) ? zero : cmul(y[l], w);
+        }
+    }
+    // contiguous -> stride layout for the inverse transform (+ its mirror by shuffles)
+#pragma unroll
+    for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
+    pol.sync();
+#pragma unroll
+    for (int mm = 0; mm < P; ++mm) x[mm] = buf[G::pidx(t + T * mm)];
+    pol.sync();
+    pol.mirror(x, xm, t, buf, typename G::Pidx{});
+    Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+#pragma unroll
+    for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
+    __syncthreads();
+    // tile (EPB modes x N rows) -> T[b][i][q0 .. q0+EPB)
+    const long g0 = (long)blockIdx.x * EPB;
+    for (int k = threadIdx.x; k < EPB * N; k += NW * 32) {
+        const int ee = k % EPB, ii = k / EPB;
+        const long gg = g0 + ee;
+        const int bb = (int)(gg >> LOG2N);
+        if (bb < a.batch && (!a.status || __ldcg(&a.status[bb]) == ST_ACTIVE))
+            a.T[((size_t)bb << (2 * LOG2N)) + (size_t)ii * N + (gg & (N - 1))] =
+                smem[ee * G::PAD_N + G::pidx(ii)];
     }
 }
 

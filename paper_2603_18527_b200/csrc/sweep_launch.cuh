@@ -15,10 +15,10 @@ struct ColCols {
     static constexpr int value = L <= 9 ? 8 : (L == 10 ? 4 : 2);
 };
 
-template <int L, int MODE, int PP, int DIM>
+template <int L, int MODE, int PP, int DIM, bool TOUT = false>
 cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
     using RG = RowGeom<L, PP, kRowWarps>;
-    auto k = row_kernel<L, MODE, kRowWarps, PP, DIM>;
+    auto k = row_kernel<L, MODE, kRowWarps, PP, DIM, TOUT>;
     if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
     const long rows = (long)a.batch << ((DIM - 1) * L);
     const int grid = (int)((rows + RG::EPB - 1) / RG::EPB);
@@ -64,6 +64,38 @@ cudaError_t launch_col_p(int mode, const ColArgs& a, cudaStream_t s, bool prepar
         case C_FD: return launch_col_t<L, C_FD, PP, LAYOUT>(a, s, prepare);
         default: return launch_col_t<L, C_LREF, PP, LAYOUT>(a, s, prepare);
     }
+}
+
+// ---- transposed 2-D handoff (n <= 512): TOUT row kernels + warp-per-line column pass
+template <int L, int MODE, int PP>
+cudaError_t launch_tcol_t(const ColArgs& a, cudaStream_t s, bool prepare) {
+    using RG = RowGeom<L, PP, kRowWarps>;
+    auto k = tcol_kernel<L, MODE, kRowWarps, PP>;
+    if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
+    const long lines = (long)a.batch << L;
+    k<<<(int)((lines + RG::EPB - 1) / RG::EPB), kRowWarps * 32, RG::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int L>
+cudaError_t launch_transposed_p(bool row, int mode, const RowArgs& a, const ColArgs& c,
+                                cudaStream_t s, bool prep) {
+    if constexpr (Geom<L, 16>::T <= 32) {
+        if (row) {
+            switch (mode) {
+                case R_FWD_BORN: return launch_row_t<L, R_FWD_BORN, 16, 2, true>(a, s, prep);
+                case R_SWEEP: return launch_row_t<L, R_SWEEP, 16, 2, true>(a, s, prep);
+                case R_OPT_B: return launch_row_t<L, R_OPT_B, 16, 2, true>(a, s, prep);
+                case R_RETA_A: return launch_row_t<L, R_RETA_A, 16, 2, true>(a, s, prep);
+                case R_FD_A: return launch_row_t<L, R_FD_A, 16, 2, true>(a, s, prep);
+                case R_FD_B: return launch_row_t<L, R_FD_B, 16, 2, true>(a, s, prep);
+                default: return cudaErrorInvalidValue;
+            }
+        }
+        if (mode == C_FD) return launch_tcol_t<L, C_FD, 16>(c, s, prep);
+        return launch_tcol_t<L, C_GREEN, 16>(c, s, prep);
+    }
+    return cudaErrorInvalidValue;
 }
 
 // ---- periodic family (FFT engine)
@@ -138,6 +170,10 @@ struct Pp8 {
     cudaError_t launch_periodic_L##L(bool row, int mode, const PerArgs& a, cudaStream_t s,      \
                                      bool prep) {                                               \
         return launch_periodic_p<L>(row, mode, a, s, prep);                                     \
+    }                                                                                           \
+    cudaError_t launch_transposed_L##L(bool row, int mode, const RowArgs& a, const ColArgs& c,  \
+                                       cudaStream_t s, bool prep) {                             \
+        return launch_transposed_p<L>(row, mode, a, c, s, prep);                                \
     }
 
 #define BS_DECLARE_SIZE(L)                                                                      \
@@ -146,7 +182,9 @@ struct Pp8 {
     cudaError_t launch_col_L##L(int pp, int layout, int mode, const ColArgs& a, cudaStream_t s,  \
                                 bool prep);                                                     \
     cudaError_t launch_periodic_L##L(bool row, int mode, const PerArgs& a, cudaStream_t s,      \
-                                     bool prep);
+                                     bool prep);                                                \
+    cudaError_t launch_transposed_L##L(bool row, int mode, const RowArgs& a, const ColArgs& c,  \
+                                       cudaStream_t s, bool prep);
 
 BS_DECLARE_SIZE(3)
 BS_DECLARE_SIZE(4)

@@ -374,3 +374,19 @@ def test_config2_grid_first_sweeps(gpu):
     ref = _oracle_run(k2[0], f[0], k0[0], eta[0], bs.PointwiseMap(), 1e-6, K)
     assert res.trace.iters == ref.iters == K
     assert_run_parity(res.trace, res.u, ref)
+
+
+def test_transposed_handoff_matches(gpu, monkeypatch):
+    """The opt-in transposed row->column handoff (BP_TRANSPOSED=1) gives the same iterates."""
+    k2, f, k0, eta = instance(128, batch=2, ppw=10.0, contrast=0.3, seed=9)
+    cfg = bs.IterationConfig(rtol=1e-9, max_iters=400)
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        base = bs.run(p, bs.PointwiseMap(), f, cfg)
+    monkeypatch.setenv("BP_TRANSPOSED", "1")
+    for cmap in (bs.PointwiseMap(), bs.OptimalScalarMap("euclidean"), _fd_map(128)):
+        with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+            tr = bs.run(p, cmap, f, cfg)
+        ref = _oracle_run(k2[0], f[0], k0[0], eta[0], cmap, 1e-9, 400)
+        assert_run_parity(tr.traces[0], tr.u[0], ref)
+        if isinstance(cmap, bs.PointwiseMap):
+            assert rel(tr.u, base.u) < 1e-13
