@@ -121,6 +121,18 @@ int bp_problem_create(const bp_grid* grid, int32_t batch, const double* k2, cons
  * Cubic grids, n+1 = 2^k, 8 <= 2^k <= 512.  All other entry points take the handle. */
 int bp_problem_create3d(const bp_grid3* grid, int32_t batch, const double* k2, const double* k0,
                         const double* eta, int32_t device, bp_problem** out);
+/* Config c4 (convection-diffusion-reaction; no reference problem family -- the spectral layer's
+ * DCT-II/III and Neumann symbol are the reference pieces it uses: transforms.cpp:56-57,120-121,
+ * 142-143, symbol.cpp:81-92).  grid->bc must be BP_BC_NEUMANN (cell-centred, h = lx/nx),
+ * nx = ny = 2^k, 8 <= 2^k <= 4096.  A = -Lap_N + b . grad_upwind + sigma (reflective ghosts),
+ * L_ref = -Lap_N + sigma0, V = L_ref - A.  bx, by, sigma: batch*nx*ny REAL; sigma0: batch.
+ * Every field argument of the entry points below is REAL (nx*ny doubles per member) on a CDR
+ * handle; maps: real BP_MAP_SCALAR only; bp_apply_V_adjoint -> BP_ENOTSUP. */
+int bp_problem_create_cdr(const bp_grid* grid, int32_t batch, const double* bx, const double* by,
+                          const double* sigma, const double* sigma0, int32_t device,
+                          bp_problem** out);
+int bp_problem_set_cdr_medium(bp_problem* p, const double* bx, const double* by,
+                              const double* sigma, const double* sigma0);
 int bp_problem_destroy(bp_problem* p);
 int bp_problem_batch(const bp_problem* p, int32_t* batch, bp_grid* grid);
 /* Replace the media of every member (same grid and batch): equivalent to constructing new

@@ -41,6 +41,23 @@ typedef struct {
 int bp_make_instances(const bp_instance_spec* spec, int64_t first, int32_t count, double* k2,
                       double* f, double* k0, double* eta, int32_t nthreads);
 
+/* Config c4: convection-diffusion-reaction media on the Neumann cell-centred n x n grid
+ * (h = 1/n).  Four seeded white-noise fields (sigma, bx, by, f, in that order) are Gaussian-
+ * smoothed with reflective padding (truncated at 3 sigma) and normalised to unit max-abs:
+ * sigma = smax/2 (1 + g_s) in [0, smax], b = bmax/sqrt(2) (g_x, g_y) (|b| <= bmax), f = g_f;
+ * sigma0 = mean sigma (the reference's CDR default, proj/src/cdr.cpp:215). */
+typedef struct {
+    int32_t n;             /* points per side (cell-centred) */
+    double b_max;          /* 20 */
+    double sigma_max;      /* 50 */
+    double smooth_cells;   /* medium smoothing sigma in cells (<= 0: n/16) */
+    double src_smooth_cells; /* source smoothing sigma in cells (<= 0: n/32) */
+    uint64_t seed;
+} bp_cdr_spec;
+
+int bp_make_cdr_instances(const bp_cdr_spec* spec, int64_t first, int32_t count, double* bx,
+                          double* by, double* sigma, double* sigma0, double* f, int32_t nthreads);
+
 /* The building blocks, exported for the pins in tests/. */
 void bp_rng_normals(uint64_t seed, int64_t index, int32_t count, double* out);
 void bp_rng_uniforms(uint64_t seed, int64_t index, int32_t count, double* out);

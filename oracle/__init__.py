@@ -100,6 +100,9 @@ class Oracle:
                                                         _dp, C.c_double, C.c_double,
                                                         C.POINTER(C.c_void_p)]
             lib.bpo_fft2.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
+            lib.bpo_problem_create_cdr.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp,
+                                                   _dp, _dp, C.c_double, C.POINTER(C.c_void_p)]
+            lib.bpo_dct2.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
             lib.bpo_inverse_dst3.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
             for name in ("bpo_apply_A", "bpo_apply_V", "bpo_apply_V_adjoint", "bpo_apply_Lref"):
                 getattr(lib, name).argtypes = [C.c_void_p, _dp, _dp]
@@ -152,6 +155,14 @@ class Oracle:
         return out
 
     @classmethod
+    def dct2(cls, x, inverse=False):
+        """REDFT10 both axes (inverse: REDFT01 both axes, unnormalised) of a complex array"""
+        x = _c(x)
+        out = np.empty_like(x)
+        cls.lib().bpo_dct2(x.shape[0], x.shape[1], int(inverse), _ptr(x), _ptr(out))
+        return out
+
+    @classmethod
     def dst1_1d(cls, x):
         x = _c(x)
         out = np.empty_like(x)
@@ -184,6 +195,23 @@ class OracleProblem:
         if rc:
             raise (ValueError if rc == 1 else OracleError)(self._lib.bpo_last_error().decode())
         self._h = h
+
+    @classmethod
+    def cdr(cls, bx, by, sigma, sigma0: float, lx: float = 1.0):
+        """Config-c4 convection-diffusion-reaction problem (Neumann, DCT-II, upwind)."""
+        self = cls.__new__(cls)
+        bx, by, sigma = (np.ascontiguousarray(a, np.float64) for a in (bx, by, sigma))
+        self.shape = bx.shape
+        self.nx, self.ny = bx.shape
+        self.k0, self.eta, self.lx, self.ly = 0.0, 1.0, lx, lx
+        self._lib = Oracle.lib()
+        h = C.c_void_p()
+        rc = self._lib.bpo_problem_create_cdr(self.nx, self.ny, lx, lx, _ptr(bx), _ptr(by),
+                                              _ptr(sigma), float(sigma0), C.byref(h))
+        if rc:
+            raise (ValueError if rc == 1 else OracleError)(self._lib.bpo_last_error().decode())
+        self._h = h
+        return self
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -289,6 +317,7 @@ class Reference:
             lib.bpref_rng_uniforms.restype = None
             lib.bpref_laplacian_symbol.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _dp]
             lib.bpref_five_point.argtypes = [_dp, C.c_int, C.c_int, C.c_double, _dp]
+            lib.bpref_dct.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
             lib.bpref_five_point.restype = None
             lib.bpref_thread_count.restype = C.c_int
             cls._lib = lib
@@ -312,6 +341,15 @@ class Reference:
                                                    C.byref(k0), C.byref(eta)):
             raise OracleError(cls.lib().bpref_last_error().decode())
         return k2, f, k0.value, eta.value
+
+    @classmethod
+    def dct(cls, x, inverse=False):
+        """the reference's forward/inverse DCT transform pair on a Neumann grid"""
+        x = _c(x)
+        out = np.empty_like(x)
+        if cls.lib().bpref_dct(x.shape[0], x.shape[1], int(inverse), _ptr(x), _ptr(out)):
+            raise OracleError(cls.lib().bpref_last_error().decode())
+        return out
 
     @classmethod
     def sponge_profile(cls, nx, ny, layer, strength=1.0, bc=1):

@@ -291,6 +291,52 @@ void bpo_fft2(int nx, int ny, int sign, const double* in_c, double* out_c) {
     fft2(nx, ny, sign, (const bpo_c*)in_c, (bpo_c*)out_c);
 }
 
+/* ------------------------------------------------------------------ DCT-II / DCT-III */
+/* REDFT10 Y_k = 2 sum x_j cos(pi (j+1/2) k / n) and REDFT01 Y_k = x_0 + 2 sum_{j>=1} x_j
+ * cos(pi j (k+1/2)/n) via the even/odd extension to a length-4n DFT (real-linear, so complex
+ * inputs transform component-wise). */
+static void dct1_strided(int n, int inverse, const bpo_c* tw4, const int* rev4, bpo_c* x, long stride,
+                         bpo_c* z, bpo_c* work) {
+    const int L = 4 * n;
+    for (int i = 0; i < L; ++i) z[i] = 0;
+    if (!inverse) {
+        for (int j = 0; j < n; ++j) {
+            z[2 * j + 1] = x[j * stride];
+            z[L - 2 * j - 1] = x[j * stride];
+        }
+    } else {
+        for (int j = 0; j < n; ++j) {
+            z[j] = x[j * stride];
+            if (j > 0) z[L - j] = x[j * stride];
+        }
+    }
+    dft1_strided(L, -1, tw4, rev4, z, 1, work);
+    for (int k = 0; k < n; ++k) x[k * stride] = inverse ? z[2 * k + 1] : z[k];
+}
+
+void bpo_dct2(int nx, int ny, int inverse, const double* in_c, double* out_c) {
+    bpo_c* out = (bpo_c*)out_c;
+    if ((const double*)out_c != in_c) memcpy(out, in_c, sizeof(bpo_c) * (size_t)nx * ny);
+    bpo_c *twx, *twy;
+    int *rvx, *rvy;
+    fft_tables(4 * nx, &twx, &rvx);
+    fft_tables(4 * ny, &twy, &rvy);
+    const int L = 4 * (nx > ny ? nx : ny);
+#pragma omp parallel
+    {
+        bpo_c* z = (bpo_c*)malloc(sizeof(bpo_c) * (size_t)L * 2);
+#pragma omp for schedule(static)
+        for (int i = 0; i < nx; ++i) dct1_strided(ny, inverse, twy, rvy, out + (long)i * ny, 1, z, z + L);
+#pragma omp for schedule(static)
+        for (int j = 0; j < ny; ++j) dct1_strided(nx, inverse, twx, rvx, out + j, ny, z, z + L);
+        free(z);
+    }
+    free(twx);
+    free(twy);
+    free(rvx);
+    free(rvy);
+}
+
 /* forward_transform(DST1): RODFT00 then x0.25 == plain sine sum (proj/src/transforms.cpp:111-118) */
 void bpo_forward_dst(int nx, int ny, const double* in_c, double* out_c) {
     dst2(nx, ny, (const bpo_c*)in_c, (bpo_c*)out_c);
@@ -311,13 +357,19 @@ static long npts(const bpo_problem* p) { return (long)p->nx * p->ny * p->nz; }
 
 /* forward_transform / inverse_transform in the problem's basis (transforms.cpp:105-148) */
 static void dstn(const bpo_problem* p, const bpo_c* in, bpo_c* out) {
-    if (p->periodic) fft2(p->nx, p->ny, -1, in, out);
+    if (p->cdr) bpo_dct2(p->nx, p->ny, 0, (const double*)in, (double*)out);
+    else if (p->periodic) fft2(p->nx, p->ny, -1, in, out);
     else if (p->nz > 1) dst3(p->nx, p->ny, p->nz, in, out);
     else dst2(p->nx, p->ny, in, out);
 }
 
 static void inverse_n(const bpo_problem* p, const bpo_c* in, bpo_c* out) {
-    if (p->periodic) {
+    if (p->cdr) {
+        bpo_dct2(p->nx, p->ny, 1, (const double*)in, (double*)out);
+        const double s = 1.0 / (4.0 * (double)p->nx * p->ny);  /* transforms.cpp:100 */
+        const long n = (long)p->nx * p->ny;
+        for (long i = 0; i < n; ++i) out[i] = s * out[i];
+    } else if (p->periodic) {
         fft2(p->nx, p->ny, +1, in, out);
         const double s = 1.0 / ((double)p->nx * p->ny);
         const long n = (long)p->nx * p->ny;
@@ -434,6 +486,74 @@ int bpo_problem_create_periodic(int nx, int ny, double lx, double ly, const doub
     return BPO_OK;
 }
 
+int bpo_problem_create_cdr(int nx, int ny, double lx, double ly, const double* bx,
+                           const double* by, const double* sigma, double sigma0,
+                           bpo_problem** out) {
+    *out = NULL;
+    if (nx < 2 || ny < 2) return fail(BPO_EINVAL, "GridSpec: nx,ny must be >= 2");
+    if (!(lx > 0.0) || !(ly > 0.0)) return fail(BPO_EINVAL, "GridSpec: lx,ly must be > 0");
+    const long n = (long)nx * ny;
+    bpo_problem* p = (bpo_problem*)calloc(1, sizeof *p);
+    p->nx = nx;
+    p->ny = ny;
+    p->nz = 1;
+    p->cdr = 1;
+    p->lx = lx;
+    p->ly = ly;
+    p->sigma0 = sigma0;
+    p->eta = 1.0;
+    p->bx = (double*)malloc(sizeof(double) * n);
+    p->by = (double*)malloc(sizeof(double) * n);
+    p->sigma = (double*)malloc(sizeof(double) * n);
+    memcpy(p->bx, bx, sizeof(double) * n);
+    memcpy(p->by, by, sizeof(double) * n);
+    memcpy(p->sigma, sigma, sizeof(double) * n);
+    p->k2 = (bpo_c*)calloc(n, sizeof(bpo_c));
+    p->v = (bpo_c*)calloc(n, sizeof(bpo_c));
+    p->lambda = (bpo_c*)malloc(sizeof(bpo_c) * n);
+    /* Neumann five-point symbol (symbol.cpp:81-92) + sigma0 */
+    const double hx = lx / nx, hy = ly / ny;
+    const double ax = 4.0 / (hx * hx), ay = 4.0 / (hy * hy);
+    double mn = INFINITY, mx = 0.0;
+    for (int q = 0; q < nx; ++q) {
+        const double sx = sin(q * kPi / (2.0 * nx));
+        for (int r = 0; r < ny; ++r) {
+            const double sy = sin(r * kPi / (2.0 * ny));
+            const double v = (ax * sx * sx + ay * sy * sy) + sigma0;
+            p->lambda[(long)q * ny + r] = v;
+            if (fabs(v) < mn) mn = fabs(v);
+            if (fabs(v) > mx) mx = fabs(v);
+        }
+    }
+    if (mn < kSymbolDivGuard * mx) {
+        bpo_problem_destroy(p);
+        return fail(BPO_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
+    }
+    *out = p;
+    return BPO_OK;
+}
+
+/* c4 operators on complex arrays with zero imaginary part.
+ *   Lap_N u: (sum of reflective-ghost neighbours - 4u)/h^2
+ *   conv u : bx * (upwind x difference) + by * (upwind y difference)   (first-order upwind) */
+static void cdr_parts(const bpo_problem* p, const bpo_c* u, bpo_c* lap, bpo_c* conv) {
+    const int nx = p->nx, ny = p->ny;
+    const double h = p->lx / nx, ih = 1.0 / h, ih2 = 1.0 / (h * h);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < ny; ++j) {
+            const long k = (long)i * ny + j;
+            const bpo_c c = u[k];
+            const bpo_c w = i > 0 ? u[k - ny] : c, e = i < nx - 1 ? u[k + ny] : c;
+            const bpo_c s = j > 0 ? u[k - 1] : c, nn = j < ny - 1 ? u[k + 1] : c;
+            lap[k] = (4.0 * c - w - e - s - nn) * ih2; /* -Lap */
+            const double vx = p->bx[k], vy = p->by[k];
+            const bpo_c dx = vx >= 0.0 ? (c - w) * ih : (e - c) * ih;
+            const bpo_c dy = vy >= 0.0 ? (c - s) * ih : (nn - c) * ih;
+            conv[k] = vx * dx + vy * dy;
+        }
+}
+
 int bpo_problem_create3(int nx, int ny, int nz, double l, const double* k2_c, double k0, double eta,
                         bpo_problem** out) {
     *out = NULL;
@@ -488,6 +608,9 @@ int bpo_problem_create3(int nx, int ny, int nz, double l, const double* k2_c, do
 
 void bpo_problem_destroy(bpo_problem* p) {
     if (!p) return;
+    free(p->bx);
+    free(p->by);
+    free(p->sigma);
     free(p->k2);
     free(p->v);
     free(p->lambda);
@@ -540,6 +663,13 @@ void bpo_apply_A(const bpo_problem* p, const double* u_c, double* out_c) {
     const bpo_c* u = (const bpo_c*)u_c;
     bpo_c* out = (bpo_c*)out_c;
     const long n = npts(p);
+    if (p->cdr) {  /* A u = -Lap_N u + b . grad_up u + sigma u */
+        bpo_c* conv = (bpo_c*)malloc(sizeof(bpo_c) * n);
+        cdr_parts(p, u, out, conv);
+        for (long i = 0; i < n; ++i) out[i] = (out[i] + conv[i]) + p->sigma[i] * u[i];
+        free(conv);
+        return;
+    }
     if (p->periodic) {
         /* HelmholtzProblem::apply_A: F^-1(|xi|^2 F u) - k2 u (helmholtz.cpp:27-32) */
         bpo_c* modes = (bpo_c*)malloc(sizeof(bpo_c) * n);
@@ -569,6 +699,13 @@ void bpo_apply_V(const bpo_problem* p, const double* u_c, double* out_c) {
     const bpo_c* u = (const bpo_c*)u_c;
     bpo_c* out = (bpo_c*)out_c;
     const long n = npts(p);
+    if (p->cdr) {  /* V u = (sigma0 - sigma) u - b . grad_up u */
+        bpo_c* lap = (bpo_c*)malloc(sizeof(bpo_c) * n);
+        cdr_parts(p, u, lap, out);
+        for (long i = 0; i < n; ++i) out[i] = (p->sigma0 - p->sigma[i]) * u[i] - out[i];
+        free(lap);
+        return;
+    }
     for (long i = 0; i < n; ++i) out[i] = u[i] * p->v[i];
 }
 

@@ -37,6 +37,11 @@ typedef double _Complex bpo_c;
 typedef struct {
     int nx, ny, nz; /* nz == 1: the reference's 2-D grid; nz > 1: 3-D extension (config c3) */
     int periodic;   /* 1: the reference's own HelmholtzProblem (FFT basis, spectral Laplacian) */
+    int cdr;        /* 1: config-c4 convection-diffusion-reaction, Neumann cell-centred, DCT-II */
+    double* bx;     /* cdr: velocity (x = first index), real nx*ny */
+    double* by;
+    double* sigma;  /* cdr: reaction, real nx*ny */
+    double sigma0;  /* cdr: reference shift, L0 = -Lap_N + sigma0 */
     double lx, ly;
     double k0, eta;
     bpo_c* k2;      /* nx*ny, damped squared wavenumber */
@@ -74,6 +79,15 @@ void bpo_inverse_dst3(int nx, int ny, int nz, const double* in_c, double* out_c)
 int bpo_problem_create_periodic(int nx, int ny, double lx, double ly, const double* k2_c,
                                 double k0, double eta, bpo_problem** out);
 void bpo_fft2(int nx, int ny, int sign, const double* in_c, double* out_c);
+/* Config c4 (no reference counterpart for the upwind term): Neumann
+ * cell-centred grid (h = lx/nx, x_i = (i+1/2) h, grid.hpp:13-14,31), reflective ghosts,
+ * A u = -Lap_N u + b . grad_upwind u + sigma u, L0 = -Lap_N + sigma0 diagonalised by DCT-II
+ * (symbol.cpp:81-91, transforms.cpp:120-121,142-143: REDFT10 forward, REDFT01 / (4 nx ny)
+ * inverse), V = L0 - A.  Fields are complex arrays with zero imaginary part. */
+int bpo_problem_create_cdr(int nx, int ny, double lx, double ly, const double* bx,
+                           const double* by, const double* sigma, double sigma0,
+                           bpo_problem** out);
+void bpo_dct2(int nx, int ny, int inverse, const double* in_c, double* out_c);
 void bpo_problem_destroy(bpo_problem* p);
 void bpo_problem_symbol(const bpo_problem* p, double* lambda_c);
 

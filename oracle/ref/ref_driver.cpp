@@ -435,6 +435,22 @@ int bpref_laplacian_symbol(int nx, int ny, double lx, double ly, int bc, double*
     });
 }
 
+// The reference's DCT pair on a Neumann grid (transforms.cpp:105-148: REDFT10 forward,
+// REDFT01 x 1/(4 nx ny) inverse)
+int bpref_dct(int nx, int ny, int inverse, const double* in, double* out) {
+    return guarded([&] {
+        GridSpec g = bp::make_grid(nx, ny, 1.0, 1.0, bp::Bc::Neumann);
+        ComplexField x = field_from(g, in);
+        if (!inverse) {
+            auto m = bp::forward_transform(x, bp::TransformKind::DCT);
+            std::memcpy(out, m.data(), sizeof(cplx) * m.size());
+        } else {
+            std::vector<cplx> m(x.data);
+            field_to(bp::inverse_transform(m, g, bp::TransformKind::DCT), out);
+        }
+    });
+}
+
 // Reference kernels for the kernel-level CPU baseline (proj/src/kernels.cpp)
 void bpref_five_point(const double* u, int nx, int ny, double h2, double* out) {
     const size_t n = static_cast<size_t>(nx) * ny;

@@ -5,6 +5,7 @@ metric), rebuilt as hand-written sm_100a CUDA behind a C ABI (include/bornsweep.
 Python mirror of the reference's operator / map / driver API (api.py).
 """
 from .api import (  # noqa: F401
+    CdrNeumann,
     FourierDiagMap,
     HelmholtzDirichlet,
     HelmholtzPeriodic,
@@ -16,11 +17,12 @@ from .api import (  # noqa: F401
     ScalarMap,
     run,
 )
-from .instances import CONFIGS, InstanceSpec, config_instances, make_instances  # noqa: F401
+from .instances import (CONFIGS, CdrSpec, InstanceSpec, config_instances,  # noqa: F401
+                        make_cdr_instances, make_instances)
 from . import _native  # noqa: F401
 
 __all__ = [
-    "FourierDiagMap", "HelmholtzDirichlet", "HelmholtzPeriodic", "IterationConfig", "IterationTrace", "OptimalScalarMap", "PointwiseMap",
+    "CdrNeumann", "FourierDiagMap", "HelmholtzDirichlet", "HelmholtzPeriodic", "IterationConfig", "IterationTrace", "OptimalScalarMap", "PointwiseMap",
     "RunResult", "ScalarMap", "run", "CONFIGS", "InstanceSpec", "config_instances",
-    "make_instances",
+    "make_instances", "CdrSpec", "make_cdr_instances",
 ]

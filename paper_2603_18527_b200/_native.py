@@ -53,6 +53,11 @@ class InstanceSpec(C.Structure):
                 ("sponge_strength", C.c_double), ("eta_factor", C.c_double), ("dim", C.c_int32)]
 
 
+class CdrSpec(C.Structure):
+    _fields_ = [("n", C.c_int32), ("b_max", C.c_double), ("sigma_max", C.c_double),
+                ("smooth_cells", C.c_double), ("src_smooth_cells", C.c_double), ("seed", C.c_uint64)]
+
+
 # Every symbol include/bornsweep.h declares (tests/test_abi.py checks the header agrees).
 ABI_FUNCTIONS = {
     "bp_last_error": (C.c_char_p, []),
@@ -61,6 +66,9 @@ ABI_FUNCTIONS = {
                                     C.POINTER(C.c_void_p)]),
     "bp_problem_create3d": (C.c_int, [C.POINTER(Grid3), C.c_int32, _dp, _dp, _dp, C.c_int32,
                                       C.POINTER(C.c_void_p)]),
+    "bp_problem_create_cdr": (C.c_int, [C.POINTER(Grid), C.c_int32, _dp, _dp, _dp, _dp, C.c_int32,
+                                        C.POINTER(C.c_void_p)]),
+    "bp_problem_set_cdr_medium": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp]),
     "bp_problem_destroy": (C.c_int, [C.c_void_p]),
     "bp_problem_batch": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(Grid)]),
     "bp_problem_set_medium": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
@@ -88,6 +96,8 @@ ABI_FUNCTIONS = {
 HOST_FUNCTIONS = {
     "bp_make_instances": (C.c_int, [C.POINTER(InstanceSpec), C.c_int64, C.c_int32, _dp, _dp, _dp,
                                     _dp, C.c_int32]),
+    "bp_make_cdr_instances": (C.c_int, [C.POINTER(CdrSpec), C.c_int64, C.c_int32, _dp, _dp, _dp,
+                                        _dp, _dp, C.c_int32]),
     "bp_rng_normals": (None, [C.c_uint64, C.c_int64, C.c_int32, _dp]),
     "bp_rng_uniforms": (None, [C.c_uint64, C.c_int64, C.c_int32, _dp]),
     "bp_sponge_profile": (None, [C.c_int32, C.c_int32, C.c_int32, C.c_double, _dp]),

@@ -141,6 +141,7 @@ class HelmholtzDirichlet:
     """
 
     BC = BC_DIRICHLET
+    DTYPE = np.complex128
 
     def __init__(self, k2, k0, eta, lx: float = 1.0, device: int = 0, dim: int = 2):
         """k2: (batch, nx, ny) -- or (nx, ny) for one member; dim=3: (batch, n, n, n) or
@@ -192,7 +193,7 @@ class HelmholtzDirichlet:
         return (self.batch,) + tuple(self.grid_shape)
 
     def _field(self, x):
-        x = np.asarray(x, dtype=np.complex128)
+        x = np.asarray(x, dtype=self.DTYPE)
         if x.shape == tuple(self.grid_shape) and self.batch == 1:
             x = x.reshape(self.shape)
         if x.shape != self.shape:
@@ -262,6 +263,48 @@ class HelmholtzPeriodic(HelmholtzDirichlet):
     BC = BC_PERIODIC
 
 
+class CdrNeumann(HelmholtzDirichlet):
+    """Config c4: convection-diffusion-reaction batch on the Neumann cell-centred grid
+    (h = lx/nx), A = -Lap_N + b . grad_upwind + sigma, L_ref = -Lap_N + sigma0 (DCT-II basis,
+    transforms.cpp:120-121,142-143; symbol.cpp:81-92), V = L_ref - A.  REAL float64 fields
+    (batch, n, n); maps: real ScalarMap.  No reference problem family exists for it (SURVEY.md
+    8(a) a16): the oracle (oracle/bp_oracle.c, bpo_problem_create_cdr) is the parity anchor."""
+
+    BC = BC_NEUMANN
+    DTYPE = np.float64
+
+    def __init__(self, bx, by, sigma, sigma0=None, lx: float = 1.0, device: int = 0):
+        bx = np.asarray(bx, np.float64)
+        self.dim = 2
+        self.single = bx.ndim == 2
+        shape = ((1,) + bx.shape) if self.single else bx.shape
+        bx = np.ascontiguousarray(bx.reshape(shape))
+        by = np.ascontiguousarray(np.asarray(by, np.float64).reshape(shape))
+        sigma = np.ascontiguousarray(np.asarray(sigma, np.float64).reshape(shape))
+        self.batch = shape[0]
+        self.grid_shape = shape[1:]
+        self.nx, self.ny = self.grid_shape
+        if sigma0 is None:  # the reference CDR default sigma0 = mean sigma (cdr.cpp:215)
+            sigma0 = sigma.reshape(self.batch, -1).mean(axis=1)
+        sigma0 = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma0, np.float64), (self.batch,)))
+        self.sigma0, self.lx, self.device = sigma0, lx, device
+        h = C.c_void_p()
+        self._lib = N.lib()
+        g = N.Grid(self.nx, self.ny, lx, lx, BC_NEUMANN)
+        _check(self._lib.bp_problem_create_cdr(C.byref(g), self.batch, _ptr(bx), _ptr(by),
+                                               _ptr(sigma), _ptr(sigma0), device, C.byref(h)))
+        self._h = h
+
+    def set_medium(self, bx, by, sigma, sigma0=None) -> None:
+        bx, by, sigma = self._field(bx), self._field(by), self._field(sigma)
+        if sigma0 is None:
+            sigma0 = sigma.reshape(self.batch, -1).mean(axis=1)
+        sigma0 = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma0, np.float64), (self.batch,)))
+        _check(self._lib.bp_problem_set_cdr_medium(self._h, _ptr(bx), _ptr(by), _ptr(sigma),
+                                                   _ptr(sigma0)))
+        self.sigma0 = sigma0
+
+
 def run(problem: HelmholtzDirichlet, cmap, f, config: IterationConfig | None = None, u0=None,
         n_snap: int = 0) -> RunResult:
     """bp::run (iterate.cpp:88-153) over every member of the batch."""
@@ -277,7 +320,7 @@ def run(problem: HelmholtzDirichlet, cmap, f, config: IterationConfig | None = N
     lib = problem._lib
     snaps = None
     if n_snap:
-        snaps = np.zeros((n_snap,) + problem.shape, np.complex128)
+        snaps = np.zeros((n_snap,) + problem.shape, problem.DTYPE)
         rc = lib.bp_run_snapshots(problem.handle, C.byref(mp), _ptr(f), C.byref(cfg), _ptr(u0),
                                   _ptr(u), _ptr(l2), _ptr(rt), info, _ptr(snaps), n_snap)
     else:

@@ -122,10 +122,9 @@ __global__ void pointwise_kernel(int op, const double2* __restrict__ u, const do
 }
 
 // per-member sum of |x|^2 over a padded field; partials[b*nchunk + c], deterministic
-__global__ void norm_partial_kernel(const double2* __restrict__ x, int log2n, int dim, int nchunk,
+__global__ void norm_partial_kernel(const double2* __restrict__ x, size_t per, int nchunk,
                                     double* __restrict__ partials) {
     const int b = blockIdx.y, c = blockIdx.x;
-    const size_t per = (size_t)1 << (dim * log2n);
     const size_t chunk = (per + nchunk - 1) / nchunk;
     const size_t lo = c * chunk, hi = min(per, lo + chunk);
     double s = 0.0;
@@ -225,6 +224,11 @@ cudaError_t launch_transposed(int log2n, bool row, int mode, const RowArgs& a, c
     BS_SIZE_CASES(launch_transposed_L, row, mode, a, c, s, prep)
 }
 
+cudaError_t launch_cdr(int log2n, bool row, int mode, const CdrArgs& a, cudaStream_t s,
+                       bool prep = false) {
+    BS_SIZE_CASES(launch_cdr_L, row, mode, a, s, prep)
+}
+
 cudaError_t launch_row(int log2n, int dim, int mode, const RowArgs& a, cudaStream_t s) {
     return launch_row_pp(log2n, points_per_thread(log2n), dim, mode, a, s);
 }
@@ -244,6 +248,11 @@ cudaError_t prepare_kernels(int log2n, int dim) {
             if (cudaError_t r = launch_transposed(log2n, false, mode, a, c, nullptr, true)) e = r;
     }
     if (dim == 2) {
+        CdrArgs ca{};
+        for (int mode : {RC_FWD, RC_INV, RC_A, RC_B})
+            if (cudaError_t r = launch_cdr(log2n, true, mode, ca, nullptr, true)) e = r;
+        for (int mode : {CC_ONE, CC_GREEN, CC_INV, CC_LREF})
+            if (cudaError_t r = launch_cdr(log2n, false, mode, ca, nullptr, true)) e = r;
         for (int mode : {RP_FWD, RP_FWD_BORN, RP_INV, RP_SWEEP})
             if (cudaError_t r = launch_periodic(log2n, true, mode, pa, nullptr, true)) e = r;
         for (int mode : {CP_ONE, CP_GREEN, CP_LREF, CP_SWEEP, CP_INV})
@@ -305,6 +314,10 @@ struct bp_problem {
     int batch = 0, device = 0, log2n = 0, n = 0, dim = 2;
     bool periodic = false;   // the reference's own HelmholtzProblem (FFT basis, no padding)
     bool transposed = false; // 2-D Dirichlet n <= 512: transposed row -> column handoff (TT)
+    bool cdr = false;        // config c4: real fields, Neumann, DCT-II, upwind V
+    double *bx = nullptr, *by = nullptr, *sigma = nullptr, *sigma0 = nullptr, *lapn = nullptr,
+           *rnorm2 = nullptr;
+    double2* w4 = nullptr;
     double2* TT = nullptr;
     double* xi2 = nullptr;   // periodic: xi_j^2, FFT order
     size_t field = 0;   // padded elements per member (n^dim)
@@ -462,7 +475,9 @@ int download(bp_problem* p, const double2* p0, const double2* p1, const int* sel
 int norms(bp_problem* p, const double2* x, double* out) {
     const int nchunk = 64;
     dim3 g(nchunk, p->batch);
-    norm_partial_kernel<<<g, 256, 0, p->stream>>>(x, p->log2n, p->dim, nchunk, p->norm_part);
+    // real (CDR) fields are read as pairs: |re|^2 + |im|^2 over half as many double2
+    const size_t per = p->cdr ? p->field / 2 : p->field;
+    norm_partial_kernel<<<g, 256, 0, p->stream>>>(x, per, nchunk, p->norm_part);
     norm_final_kernel<<<(p->batch + 127) / 128, 128, 0, p->stream>>>(p->norm_part, nchunk,
                                                                       p->batch, out);
     CU(cudaGetLastError());
@@ -750,15 +765,17 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
 }
 
 int finish_run_periodic(bp_problem* p, double* u_out, bool host_ptr);
+int finish_run_cdr(bp_problem* p, double* u_out, bool host_ptr);
 
 int finish_run(bp_problem* p, const bp_iter_config* cfg, double* u_out, bool host_ptr,
                double* res_l2, double* res_reta, bp_trace* info) {
     const int B = p->batch;
     Control c = make_control(p);
-    int rc = p->periodic ? finish_run_periodic(p, u_out, host_ptr)
-                         : download(p, p->u0, p->u1, c.result_buf, u_out, host_ptr);
+    int rc = p->cdr        ? finish_run_cdr(p, u_out, host_ptr)
+             : p->periodic ? finish_run_periodic(p, u_out, host_ptr)
+                           : download(p, p->u0, p->u1, c.result_buf, u_out, host_ptr);
     if (rc) return rc;
-    if (!p->periodic) p->stat_launches += 1;  // unpack
+    if (!p->periodic && !p->cdr) p->stat_launches += 1;  // unpack
     std::vector<int> iters(B), term(B);
     std::vector<double> f1(B), f2(B);
     CU(cudaMemcpyAsync(iters.data(), c.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, p->stream));
@@ -966,6 +983,239 @@ int finish_run_periodic(bp_problem* p, double* u_out, bool host_ptr) {
     return download(p, p->y, nullptr, nullptr, u_out, host_ptr);
 }
 
+// ------------------------------------------------------------------ CDR family (config c4, host)
+// Real fp64 fields, n x n per member, no padding (cell-centred Neumann nodes (i+1/2) h).
+CdrArgs cdr_args(const bp_problem* p) {
+    CdrArgs a{};
+    a.batch = p->batch;
+    a.h = p->grid.lx / p->n;
+    a.sigma0 = p->sigma0;
+    a.bx = p->bx;
+    a.by = p->by;
+    a.sigma = p->sigma;
+    a.f = reinterpret_cast<const double*>(p->f);
+    a.T = reinterpret_cast<double*>(p->T);
+    a.u0 = reinterpret_cast<double*>(p->u0);
+    a.u1 = reinterpret_cast<double*>(p->u1);
+    a.rnorm2 = p->rnorm2;
+    a.lapn = p->lapn;
+    a.tw = p->tw;
+    a.w4 = p->w4;
+    a.scale = 1.0;
+    a.gamma = 1.0;
+    a.ctl = make_control(p);
+    return a;
+}
+
+// A u, V u, f - A u, V u + f on real fields (ops 0, 1, 3, 4): the same upwind stencil as the
+// RC_B prologue (cdr_kernels.cuh), elementwise for the operator API
+__global__ void cdr_stencil_kernel(int op, const double* __restrict__ u, const double* __restrict__ f,
+                                   const double* __restrict__ bx, const double* __restrict__ by,
+                                   const double* __restrict__ sigma, const double* __restrict__ sigma0,
+                                   double* __restrict__ out, int batch, int log2n, double h) {
+    const int n = 1 << log2n;
+    const size_t total = (size_t)batch << (2 * log2n);
+    const double ih = 1.0 / h, ih2 = ih * ih;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int b = (int)(idx >> (2 * log2n));
+        const int j = (int)(idx & (n - 1)), i = (int)((idx >> log2n) & (n - 1));
+        const double c = u[idx];
+        const double w = i > 0 ? u[idx - n] : c, e = i < n - 1 ? u[idx + n] : c;
+        const double so = j > 0 ? u[idx - 1] : c, no = j < n - 1 ? u[idx + 1] : c;
+        const double lap = (4.0 * c - w - e - so - no) * ih2;
+        const double vx = bx[idx], vy = by[idx], sg = sigma[idx];
+        const double dx = vx >= 0.0 ? (c - w) * ih : (e - c) * ih;
+        const double dy = vy >= 0.0 ? (c - so) * ih : (no - c) * ih;
+        const double conv = vx * dx + vy * dy;
+        double r;
+        switch (op) {
+            case 0: r = (lap + conv) + sg * c; break;
+            case 1: r = (sigma0[b] - sg) * c - conv; break;
+            case 3: r = f[idx] - ((lap + conv) + sg * c); break;
+            default: r = ((sigma0[b] - sg) * c - conv) + f[idx]; break;
+        }
+        out[idx] = r;
+    }
+}
+
+int cdr_upload(bp_problem* p, const double* src, double2* dst, bool host_ptr = true) {
+    CU(cudaMemcpyAsync(dst, src, sizeof(double) * p->field * p->batch,
+                       host_ptr ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, p->stream));
+    return BP_OK;
+}
+
+int cdr_download(bp_problem* p, const double2* src, double* dst, bool host_ptr = true) {
+    CU(cudaMemcpyAsync(dst, src, sizeof(double) * p->field * p->batch,
+                       host_ptr ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, p->stream));
+    return BP_OK;
+}
+
+// G / L_ref / transforms (transforms.cpp:105-148 with REDFT10 / REDFT01, inverse 1/(4 nx ny))
+//   which 0 G, 2 L_ref, 3 forward transform, 4 inverse transform; out - sub when sub != null
+int cdr_apply(bp_problem* p, int which, const double2* in, double2* out, const double2* sub) {
+    CdrArgs a = cdr_args(p);
+    const double inv = 1.0 / (4.0 * (double)p->n * p->n);
+    a.in = reinterpret_cast<const double*>(in);
+    a.out = reinterpret_cast<double*>(out);
+    a.sub = reinterpret_cast<const double*>(sub);
+    switch (which) {
+        case 0:
+        case 2:
+            CU(launch_cdr(p->log2n, true, RC_FWD, a, p->stream));
+            a.scale = inv;
+            CU(launch_cdr(p->log2n, false, which == 0 ? CC_GREEN : CC_LREF, a, p->stream));
+            a.scale = 1.0;
+            CU(launch_cdr(p->log2n, true, RC_INV, a, p->stream));
+            return BP_OK;
+        case 3:
+            CU(launch_cdr(p->log2n, true, RC_FWD, a, p->stream));
+            CU(launch_cdr(p->log2n, false, CC_ONE, a, p->stream));
+            CU(cudaMemcpyAsync(out, p->T, sizeof(double) * p->field * p->batch,
+                               cudaMemcpyDeviceToDevice, p->stream));
+            return BP_OK;
+        case 4:
+            a.T = const_cast<double*>(a.in);
+            a.sub = nullptr;
+            CU(launch_cdr(p->log2n, true, RC_INV, a, p->stream));
+            a.T = a.out;
+            a.scale = inv;
+            CU(launch_cdr(p->log2n, false, CC_INV, a, p->stream));
+            return BP_OK;
+    }
+    return set_err(BP_EINVAL, "bad CDR op");
+}
+
+int cdr_stencil(bp_problem* p, int op, const double2* u, const double2* f, double2* out) {
+    cdr_stencil_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(
+        op, reinterpret_cast<const double*>(u), reinterpret_cast<const double*>(f), p->bx, p->by,
+        p->sigma, p->sigma0, reinterpret_cast<double*>(out), p->batch, p->log2n, p->grid.lx / p->n);
+    CU(cudaGetLastError());
+    return BP_OK;
+}
+
+// bp::run for the CDR family: sweep m = RC_A (entry m, u^{m+1}), RC_B (r^{m+1}, q^{m+1}, rows),
+// CC_GREEN (columns); the first RC_B + CC_GREEN pair stages q^0.
+int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool have_u0,
+                 double* snapshots, int n_snap) {
+    const int B = p->batch;
+    CdrArgs a = cdr_args(p);
+    a.ctl.max_iters = cfg->max_iters;
+    a.ctl.rtol = cfg->rtol;
+    a.gamma = map->gamma_re;
+    CdrArgs ac = a;
+    ac.scale = 1.0 / (4.0 * (double)p->n * p->n);
+    // fnorm_l2 = ||f||, fnorm_reta = ||G f||  (iterate.cpp:93,102)
+    if (int rc = norms(p, p->f, p->fnorm_l2)) return rc;
+    if (int rc = cdr_apply(p, 0, p->f, p->y, nullptr)) return rc;
+    if (int rc = norms(p, p->y, p->fnorm_reta)) return rc;
+    std::vector<double> fn(B);
+    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    for (int b = 0; b < B; ++b)
+        if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
+    if (!have_u0) CU(cudaMemsetAsync(p->u0, 0, sizeof(double2) * p->alloc, p->stream));
+    CU(cudaMemsetAsync(p->u1, 0, sizeof(double2) * p->alloc, p->stream));
+    init_control_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(a.ctl, B);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_l2, (size_t)B * p->trace_cap);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_reta, (size_t)B * p->trace_cap);
+    CU(cudaGetLastError());
+    CU(launch_cdr(p->log2n, true, RC_B, a, p->stream));
+    CU(launch_cdr(p->log2n, false, CC_GREEN, ac, p->stream));
+    // norms 2x2, G 3, init_control, 2x fill_nan, RC_B + CC_GREEN
+    p->stat_launches = 12;
+    p->stat_row_ms = p->stat_col_ms = 0;
+    p->stat_timed = 0;
+    const long max_launch = (long)cfg->max_iters + 1;
+    const size_t nd = p->field;  // real values per member
+    auto sweep = [&](cudaEvent_t* ev) -> int {
+        if (ev) CU(cudaEventRecord(ev[0], p->stream));
+        CU(launch_cdr(p->log2n, true, RC_A, a, p->stream));
+        CU(launch_cdr(p->log2n, true, RC_B, a, p->stream));
+        if (ev) CU(cudaEventRecord(ev[1], p->stream));
+        CU(launch_cdr(p->log2n, false, CC_GREEN, ac, p->stream));
+        if (ev) CU(cudaEventRecord(ev[2], p->stream));
+        return BP_OK;
+    };
+    auto poll = [&]() -> int {
+        CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+        return BP_OK;
+    };
+    if (snapshots && n_snap > 0) {
+        if (int rc = cdr_download(p, p->u0, snapshots)) return rc;
+        for (long k = 1; k <= max_launch; ++k) {
+            if (int rc = sweep(nullptr)) return rc;
+            p->stat_launches += 3;
+            if (k < n_snap)  // u^k in buffer k & 1
+                if (int rc = cdr_download(p, (k & 1) ? p->u1 : p->u0, snapshots + nd * B * k)) return rc;
+            if (int rc = poll()) return rc;
+            if (*p->host_active == 0) break;
+        }
+        return BP_OK;
+    }
+    if (p->timing) {
+        std::vector<cudaEvent_t> ev(3 * kGraphSweeps);
+        for (auto& e : ev) CU(cudaEventCreate(&e));
+        long launched = 0;
+        int rc = BP_OK;
+        while (launched < max_launch && rc == BP_OK) {
+            for (int s = 0; s < kGraphSweeps && rc == BP_OK; ++s) rc = sweep(&ev[3 * s]);
+            if (rc) break;
+            launched += kGraphSweeps;
+            p->stat_launches += 3 * kGraphSweeps;
+            if ((rc = poll())) break;
+            for (int s = 0; s < kGraphSweeps; ++s) {
+                float r = 0, c = 0;
+                cudaEventElapsedTime(&r, ev[3 * s], ev[3 * s + 1]);
+                cudaEventElapsedTime(&c, ev[3 * s + 1], ev[3 * s + 2]);
+                p->stat_row_ms += r;
+                p->stat_col_ms += c;
+                ++p->stat_timed;
+            }
+            if (*p->host_active == 0) break;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        return rc;
+    }
+    const bool reuse = p->graph && p->graph_map_kind == map->kind && p->graph_gamma.x == map->gamma_re &&
+                       p->graph_max_iters == cfg->max_iters && p->graph_rtol == cfg->rtol;
+    if (!reuse) {
+        if (p->graph) cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+        cudaGraph_t g;
+        CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+        for (int s = 0; s < kGraphSweeps; ++s) sweep(nullptr);
+        CU(cudaStreamEndCapture(p->stream, &g));
+        CU(cudaGraphInstantiate(&p->graph, g, 0));
+        cudaGraphDestroy(g);
+        p->graph_map_kind = map->kind;
+        p->graph_metric = map->metric;
+        p->graph_gamma = make_double2(map->gamma_re, 0.0);
+        p->graph_max_iters = cfg->max_iters;
+        p->graph_rtol = cfg->rtol;
+    }
+    long launched = 0;
+    while (launched < max_launch) {
+        CU(cudaGraphLaunch(p->graph, p->stream));
+        launched += kGraphSweeps;
+        p->stat_launches += 3 * kGraphSweeps;
+        if (int rc = poll()) return rc;
+        if (*p->host_active == 0) break;
+    }
+    return BP_OK;
+}
+
+int finish_run_cdr(bp_problem* p, double* u_out, bool host_ptr) {
+    Control c = make_control(p);
+    // result_buf selects u0 / u1 per member; real fields copied as pairs
+    select_copy_kernel<<<grid_for(p->field * p->batch / 2), 256, 0, p->stream>>>(
+        p->u0, p->u1, c.result_buf, p->x, p->field / 2, p->batch);
+    CU(cudaGetLastError());
+    p->stat_launches += 1;
+    return cdr_download(p, p->x, u_out, host_ptr);
+}
+
 int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* cfg) {
     if (int rc = check_problem(p)) return rc;
     if (!map || !cfg) return set_err(BP_EINVAL, "run: null map or config");
@@ -980,6 +1230,8 @@ int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* c
     if (map->kind == BP_MAP_OPTIMAL_SCALAR && map->metric != BP_METRIC_EUCLIDEAN &&
         map->metric != BP_METRIC_RETA)
         return set_err(BP_EINVAL, "unknown optimal-scalar metric");
+    if (p->cdr && (map->kind != BP_MAP_SCALAR || map->gamma_im != 0.0))
+        return set_err(BP_ENOTSUP, "CDR family on the GPU: real scalar maps only");
     if (p->periodic && (map->kind == BP_MAP_OPTIMAL_SCALAR || map->kind == BP_MAP_POINTWISE))
         return set_err(BP_ENOTSUP, "periodic family on the GPU: scalar and FourierDiag maps only");
     return BP_OK;
@@ -1141,6 +1393,131 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     return BP_OK;
 }
 
+// Config c4 handle: Neumann cell-centred n x n (h = lx/n), L0 = -Lap_N + sigma0 diagonalised by
+// DCT-II (symbol.cpp:81-92), V = (sigma0 - sigma) - b . grad_upwind.  Real fields.
+int check_cdr_medium(const bp_problem* p, const double* bx, const double* by, const double* sigma,
+                     const double* sigma0) {
+    const size_t tot = p->field * p->batch;
+    for (size_t k = 0; k < tot; ++k)
+        if (!std::isfinite(bx[k]) || !std::isfinite(by[k]) || !std::isfinite(sigma[k]))
+            return set_err(BP_EINVAL, "CDR medium not finite");
+    const double h = p->grid.lx / p->n;
+    std::vector<double> lapn(p->n);
+    for (int k = 0; k < p->n; ++k) {
+        const double s = std::sin(k * kPi / (2.0 * p->n));
+        lapn[k] = 4.0 / (h * h) * s * s;
+    }
+    for (int b = 0; b < p->batch; ++b) {
+        const double s0 = sigma0[b];
+        if (!std::isfinite(s0)) return set_err(BP_EINVAL, "CDR: sigma0 not finite");
+        // apply_symbol's guard (symbol.cpp:23-31) over lambda_pq = a_p + a_q + sigma0; the a_k
+        // are non-negative and increasing, so sigma0 >= 0 puts the extremes at the corners
+        double mn, mx;
+        if (s0 >= 0.0) {
+            mn = s0;
+            mx = 2.0 * lapn[p->n - 1] + s0;
+        } else {
+            mn = INFINITY;
+            mx = 0.0;
+            for (int i = 0; i < p->n; ++i)
+                for (int j = 0; j < p->n; ++j) {
+                    const double v = std::fabs(lapn[i] + lapn[j] + s0);
+                    mn = std::min(mn, v);
+                    mx = std::max(mx, v);
+                }
+        }
+        if (mn < kSymbolDivGuard * mx)
+            return set_err(BP_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
+    }
+    return BP_OK;
+}
+
+int upload_cdr_medium(bp_problem* p, const double* bx, const double* by, const double* sigma,
+                      const double* sigma0) {
+    const size_t bytes = sizeof(double) * p->field * p->batch;
+    CU(cudaMemcpyAsync(p->bx, bx, bytes, cudaMemcpyHostToDevice, p->stream));
+    CU(cudaMemcpyAsync(p->by, by, bytes, cudaMemcpyHostToDevice, p->stream));
+    CU(cudaMemcpyAsync(p->sigma, sigma, bytes, cudaMemcpyHostToDevice, p->stream));
+    CU(cudaMemcpyAsync(p->sigma0, sigma0, sizeof(double) * p->batch, cudaMemcpyHostToDevice, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    return BP_OK;
+}
+
+int create_cdr_impl(const bp_grid* grid, int32_t batch, const double* bx, const double* by,
+                    const double* sigma, const double* sigma0, int32_t device, bp_problem** out) {
+    const int n = grid->nx;
+    int log2n = 0;
+    while ((1 << log2n) < n) ++log2n;
+    if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > kMaxLog2)
+        return set_err(BP_ENOTSUP, "GPU CDR path needs square Neumann grids with nx = 2^k, 8 <= 2^k <= 4096");
+    if (grid->lx != grid->ly) return set_err(BP_ENOTSUP, "GPU path needs lx == ly (hx == hy)");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return set_err(BP_ECUDA, "no such CUDA device");
+    DeviceGuard guard(device);
+    auto* p = new bp_problem();
+    p->grid = *grid;
+    p->batch = batch;
+    p->device = device;
+    p->log2n = log2n;
+    p->n = n;
+    p->dim = 2;
+    p->cdr = true;
+    p->field = (size_t)n * n;
+    p->alloc = p->field * batch / 2;  // in double2 units (real fields)
+    p->dense_pts = p->field;
+    auto fail = [&](int code) {
+        bp_problem_destroy(p);
+        return code;
+    };
+    if (int rc = check_cdr_medium(p, bx, by, sigma, sigma0)) return fail(rc);
+#define CUF(call)                                                                                   \
+    do {                                                                                            \
+        cudaError_t _e = (call);                                                                    \
+        if (_e != cudaSuccess) return fail(set_err(BP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e))); \
+    } while (0)
+    CUF(prepare_kernels(log2n, 2));
+    CUF(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    const size_t fb = sizeof(double) * p->field * batch;
+    for (double2** buf : {&p->f, &p->u0, &p->u1, &p->T, &p->x, &p->y}) {
+        CUF(cudaMalloc(buf, fb));
+        CUF(cudaMemsetAsync(*buf, 0, fb, p->stream));
+    }
+    for (double** buf : {&p->bx, &p->by, &p->sigma}) CUF(cudaMalloc(buf, fb));
+    CUF(cudaMalloc(&p->sigma0, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->rnorm2, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->partial, sizeof(double) * (size_t)batch * n * kPartStride));
+    CUF(cudaMalloc(&p->gamma, sizeof(double2) * (size_t)batch));
+    CUF(cudaMalloc(&p->norm_part, sizeof(double) * (size_t)batch * 64));
+    CUF(cudaMalloc(&p->fnorm_l2, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->fnorm_reta, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->ctl_int, sizeof(int) * (5 * (size_t)batch + 1)));
+    CUF(cudaMalloc(&p->counter, sizeof(unsigned) * batch));
+    CUF(cudaMemsetAsync(p->counter, 0, sizeof(unsigned) * batch, p->stream));
+    CUF(cudaMallocHost(&p->host_active, sizeof(int)));
+    CUF(cudaMalloc(&p->tw, sizeof(double2) * n));
+    CUF(cudaMalloc(&p->w4, sizeof(double2) * n));
+    CUF(cudaMalloc(&p->lapn, sizeof(double) * n));
+    const double h = grid->lx / n;
+    std::vector<double> tw(2 * n), w4(2 * n), lapn(n);
+    for (int k = 0; k < n; ++k) {
+        tw[2 * k] = std::cos(2.0 * kPi * k / n);
+        tw[2 * k + 1] = -std::sin(2.0 * kPi * k / n);
+        w4[2 * k] = std::cos(kPi * k / (2.0 * n));
+        w4[2 * k + 1] = -std::sin(kPi * k / (2.0 * n));
+        const double s = std::sin(k * kPi / (2.0 * n));
+        lapn[k] = 4.0 / (h * h) * s * s;  // symbol.cpp:81-92 (per axis)
+    }
+    CUF(cudaMemcpyAsync(p->tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->w4, w4.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->lapn, lapn.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
+    if (int rc = upload_cdr_medium(p, bx, by, sigma, sigma0)) return fail(rc);
+    if (int rc = ensure_trace(p, 1000)) return fail(rc);
+#undef CUF
+    *out = p;
+    return BP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1178,6 +1555,28 @@ int bp_problem_create3d(const bp_grid3* grid, int32_t batch, const double* k2, c
     return create_impl(&g2, 3, batch, k2, k0, eta, device, out);
 }
 
+int bp_problem_create_cdr(const bp_grid* grid, int32_t batch, const double* bx, const double* by,
+                          const double* sigma, const double* sigma0, int32_t device, bp_problem** out) {
+    if (!out) return set_err(BP_EINVAL, "null output handle");
+    *out = nullptr;
+    if (!grid || !bx || !by || !sigma || !sigma0) return set_err(BP_EINVAL, "null argument");
+    if (grid->nx < 2 || grid->ny < 2) return set_err(BP_EINVAL, "GridSpec: nx,ny must be >= 2");
+    if (!(grid->lx > 0.0) || !(grid->ly > 0.0)) return set_err(BP_EINVAL, "GridSpec: lx,ly must be > 0");
+    if (batch < 1) return set_err(BP_EINVAL, "batch must be >= 1");
+    if (grid->bc != BP_BC_NEUMANN) return set_err(BP_EINVAL, "CDR problems live on Neumann grids");
+    return create_cdr_impl(grid, batch, bx, by, sigma, sigma0, device, out);
+}
+
+int bp_problem_set_cdr_medium(bp_problem* p, const double* bx, const double* by, const double* sigma,
+                              const double* sigma0) {
+    if (int rc = check_problem(p)) return rc;
+    if (!p->cdr) return set_err(BP_EINVAL, "not a CDR problem");
+    if (!bx || !by || !sigma || !sigma0) return set_err(BP_EINVAL, "null argument");
+    if (int rc = check_cdr_medium(p, bx, by, sigma, sigma0)) return rc;
+    DeviceGuard guard(p->device);
+    return upload_cdr_medium(p, bx, by, sigma, sigma0);
+}
+
 int bp_problem_destroy(bp_problem* p) {
     if (!p) return BP_OK;
     DeviceGuard guard(p->device);
@@ -1187,7 +1586,9 @@ int bp_problem_destroy(bp_problem* p) {
                     (void*)p->y, (void*)p->dense, (void*)p->partial, (void*)p->gamma, (void*)p->fd, (void*)p->norm_part,
                     (void*)p->fnorm_l2, (void*)p->fnorm_reta, (void*)p->ctl_int, (void*)p->counter,
                     (void*)p->trace_l2, (void*)p->trace_reta, (void*)p->k0sq, (void*)p->eta,
-                    (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2, (void*)p->TT})
+                    (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2, (void*)p->TT,
+                    (void*)p->bx, (void*)p->by, (void*)p->sigma, (void*)p->sigma0, (void*)p->lapn,
+                    (void*)p->rnorm2, (void*)p->w4})
         if (q) cudaFree(q);
     if (p->host_active) cudaFreeHost(p->host_active);
     if (p->stream) cudaStreamDestroy(p->stream);
@@ -1207,6 +1608,16 @@ static int pointwise_op(const bp_problem* cp, int op, const double* u, const dou
     if (!u || !out || (op == 3 && !f)) return set_err(BP_EINVAL, "null field");
     auto* p = const_cast<bp_problem*>(cp);
     DeviceGuard guard(p->device);
+    if (p->cdr) {
+        if (op == 2) return set_err(BP_ENOTSUP, "CDR family: V is not normal; no adjoint on the GPU");
+        if (int rc = cdr_upload(p, u, p->x)) return rc;
+        if (op == 3)
+            if (int rc = cdr_upload(p, f, p->f)) return rc;
+        if (int rc = cdr_stencil(p, op, p->x, p->f, p->y)) return rc;
+        if (int rc = cdr_download(p, p->y, out)) return rc;
+        CU(cudaStreamSynchronize(p->stream));
+        return BP_OK;
+    }
     if (int rc = upload(p, u, p->x)) return rc;
     if (op == 3)
         if (int rc = upload(p, f, p->f)) return rc;
@@ -1239,6 +1650,19 @@ static int spectral_op(const bp_problem* cp, int which, const double* in, const 
     if (!in || !out || (which == 1 && !f)) return set_err(BP_EINVAL, "null field");
     auto* p = const_cast<bp_problem*>(cp);
     DeviceGuard guard(p->device);
+    if (p->cdr) {
+        if (int rc = cdr_upload(p, in, p->x)) return rc;
+        if (which == 1) {  // born residual G(V u + f) - u
+            if (int rc = cdr_upload(p, f, p->f)) return rc;
+            if (int rc = cdr_stencil(p, 4, p->x, p->f, p->y)) return rc;
+            if (int rc = cdr_apply(p, 0, p->y, p->y, p->x)) return rc;
+        } else if (int rc = cdr_apply(p, which, p->x, p->y, nullptr)) {
+            return rc;
+        }
+        if (int rc = cdr_download(p, p->y, out)) return rc;
+        CU(cudaStreamSynchronize(p->stream));
+        return BP_OK;
+    }
     if (int rc = upload(p, in, p->x)) return rc;
     if (p->periodic) {
         if (which == 1)
@@ -1301,6 +1725,13 @@ static int run_impl(const bp_problem* cp, const bp_map* map, const double* f, co
     auto* p = const_cast<bp_problem*>(cp);
     DeviceGuard guard(p->device);
     if (int rc = ensure_trace(p, cfg->max_iters)) return rc;
+    if (p->cdr) {
+        if (int rc = cdr_upload(p, f, p->f, host_ptr)) return rc;
+        if (u0)
+            if (int rc = cdr_upload(p, u0, p->u0, host_ptr)) return rc;
+        if (int rc = run_core_cdr(p, map, cfg, u0 != nullptr, snapshots, n_snap)) return rc;
+        return finish_run(p, cfg, u_out, host_ptr, res_l2, res_reta, info);
+    }
     if (int rc = upload(p, f, p->f, host_ptr)) return rc;
     if (u0)  // periodic: the physical u0 is transformed into U^0 by run_core_periodic
         if (int rc = upload(p, u0, p->periodic ? p->x : p->u0, host_ptr)) return rc;
@@ -1336,6 +1767,7 @@ int bp_problem_stream(const bp_problem* p, void** stream) {
 
 int bp_problem_set_medium(bp_problem* p, const double* k2, const double* k0, const double* eta) {
     if (int rc = check_problem(p)) return rc;
+    if (p->cdr) return set_err(BP_EINVAL, "CDR problem: use bp_problem_set_cdr_medium");
     if (!k2 || !k0 || !eta) return set_err(BP_EINVAL, "null argument");
     const size_t nd = p->dense_pts;
     for (int b = 0; b < p->batch; ++b) {

@@ -241,9 +241,94 @@ void make_one(const bp_instance_spec& s, int64_t index, std::complex<double>* k2
     for (size_t i = 0; i < npts; ++i) f[i] = std::complex<double>(src[i], 0.0);
 }
 
+// Separable Gaussian smoothing with reflective (cell-centred Neumann) padding, truncated at
+// 3 sigma, unit-sum weights.
+void smooth_reflect(int n, double sigma, const double* in, double* out) {
+    const size_t N2 = (size_t)n * n;
+    if (sigma <= 0.0) {
+        std::memcpy(out, in, sizeof(double) * N2);
+        return;
+    }
+    const int R = static_cast<int>(std::ceil(3.0 * sigma));
+    std::vector<double> w(2 * R + 1);
+    double ws = 0.0;
+    for (int d = -R; d <= R; ++d) ws += (w[d + R] = std::exp(-0.5 * d * d / (sigma * sigma)));
+    for (double& x : w) x /= ws;
+    auto refl = [n](int i) {
+        while (i < 0 || i >= n) i = i < 0 ? -i - 1 : 2 * n - i - 1;
+        return i;
+    };
+    // 1-D pass along contiguous lines through a reflected, padded copy (vectorisable dot)
+    auto pass = [&](const double* src, double* dst) {
+        std::vector<double> ext(n + 2 * R);
+        for (int i = 0; i < n; ++i) {
+            const double* line = src + (size_t)i * n;
+            for (int k = 0; k < n + 2 * R; ++k) ext[k] = line[refl(k - R)];
+            double* o = dst + (size_t)i * n;
+            for (int j = 0; j < n; ++j) {
+                const double* e = ext.data() + j;
+                double acc = 0.0;
+                for (int d = 0; d <= 2 * R; ++d) acc += w[d] * e[d];
+                o[j] = acc;
+            }
+        }
+    };
+    auto transpose = [n](const double* a, double* b) {
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) b[(size_t)j * n + i] = a[(size_t)i * n + j];
+    };
+    std::vector<double> t1(N2), t2(N2);
+    pass(in, t1.data());
+    transpose(t1.data(), t2.data());
+    pass(t2.data(), t1.data());
+    transpose(t1.data(), out);
+}
+
+void make_cdr_one(const bp_cdr_spec& s, int64_t index, double* bx, double* by, double* sigma,
+                  double* sigma0, double* f) {
+    const int n = s.n;
+    const size_t N2 = (size_t)n * n;
+    Rng rng = stream(s.seed, index);
+    const double sm = s.smooth_cells > 0 ? s.smooth_cells : n / 16.0;
+    const double sf = s.src_smooth_cells > 0 ? s.src_smooth_cells : n / 32.0;
+    double* outs[4] = {sigma, bx, by, f};
+    std::vector<double> noise(N2);
+    for (int k = 0; k < 4; ++k) {
+        for (double& v : noise) v = rng.normal();
+        smooth_reflect(n, k == 3 ? sf : sm, noise.data(), outs[k]);
+        double mx = 0.0;
+        for (size_t i = 0; i < N2; ++i) mx = std::max(mx, std::abs(outs[k][i]));
+        if (mx <= 0.0) mx = 1.0;
+        for (size_t i = 0; i < N2; ++i) outs[k][i] /= mx;
+    }
+    const double bs = s.b_max / std::sqrt(2.0);
+    double ssum = 0.0;
+    for (size_t i = 0; i < N2; ++i) {
+        sigma[i] = 0.5 * s.sigma_max * (1.0 + sigma[i]);
+        ssum += sigma[i];
+        bx[i] *= bs;
+        by[i] *= bs;
+    }
+    *sigma0 = ssum / static_cast<double>(N2);
+}
+
 }  // namespace
 
 extern "C" {
+
+int bp_make_cdr_instances(const bp_cdr_spec* spec, int64_t first, int32_t count, double* bx,
+                          double* by, double* sigma, double* sigma0, double* f, int32_t nthreads) {
+    if (!spec || spec->n < 4 || spec->b_max < 0.0 || spec->sigma_max < 0.0) return 1;
+    const size_t N2 = (size_t)spec->n * spec->n;
+#ifdef _OPENMP
+    const int nt = nthreads > 0 ? nthreads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic) num_threads(nt)
+#endif
+    for (int b = 0; b < count; ++b)
+        make_cdr_one(*spec, first + b, bx + N2 * b, by + N2 * b, sigma + N2 * b, sigma0 + b, f + N2 * b);
+    (void)nthreads;
+    return 0;
+}
 
 int bp_make_instances(const bp_instance_spec* spec, int64_t first, int32_t count, double* k2,
                       double* f, double* k0, double* eta, int32_t nthreads) {

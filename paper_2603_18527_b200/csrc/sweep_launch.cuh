@@ -2,6 +2,7 @@
 // sweep_L*.cu, so the instantiations compile in parallel).
 #pragma once
 
+#include "cdr_kernels.cuh"
 #include "periodic_kernels.cuh"
 #include "sweep_kernels.cuh"
 
@@ -98,6 +99,45 @@ cudaError_t launch_transposed_p(bool row, int mode, const RowArgs& a, const ColA
     return cudaErrorInvalidValue;
 }
 
+// ---- config c4 (CDR, DCT engine, real packed pairs)
+template <int L, int MODE>
+cudaError_t launch_crow_t(const CdrArgs& a, cudaStream_t s, bool prepare) {
+    using RG = RowGeom<L, 16, kRowWarps>;
+    auto k = crow_kernel<L, MODE, kRowWarps, 16>;
+    if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
+    const long pairs = (long)a.batch << (L - 1);
+    k<<<(int)((pairs + RG::EPB - 1) / RG::EPB), kRowWarps * 32, RG::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int L, int MODE>
+cudaError_t launch_ccol_t(const CdrArgs& a, cudaStream_t s, bool prepare) {
+    constexpr int C = ColCols<L>::value >= 8 ? 4 : ColCols<L>::value;  // column pairs per CTA
+    using CG = ColGeom<L, 16, C>;
+    auto k = ccol_kernel<L, MODE, C, 16>;
+    if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
+    k<<<a.batch * ((1 << L) / (2 * C)), CG::THREADS, CG::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int L>
+cudaError_t launch_cdr_p(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep) {
+    if (row) {
+        switch (mode) {
+            case RC_FWD: return launch_crow_t<L, RC_FWD>(a, s, prep);
+            case RC_INV: return launch_crow_t<L, RC_INV>(a, s, prep);
+            case RC_A: return launch_crow_t<L, RC_A>(a, s, prep);
+            default: return launch_crow_t<L, RC_B>(a, s, prep);
+        }
+    }
+    switch (mode) {
+        case CC_ONE: return launch_ccol_t<L, CC_ONE>(a, s, prep);
+        case CC_INV: return launch_ccol_t<L, CC_INV>(a, s, prep);
+        case CC_LREF: return launch_ccol_t<L, CC_LREF>(a, s, prep);
+        default: return launch_ccol_t<L, CC_GREEN>(a, s, prep);
+    }
+}
+
 // ---- periodic family (FFT engine)
 template <int L, int MODE, int PP>
 cudaError_t launch_prow_t(const PerArgs& a, cudaStream_t s, bool prepare) {
@@ -174,6 +214,9 @@ struct Pp8 {
     cudaError_t launch_transposed_L##L(bool row, int mode, const RowArgs& a, const ColArgs& c,  \
                                        cudaStream_t s, bool prep) {                             \
         return launch_transposed_p<L>(row, mode, a, c, s, prep);                                \
+    }                                                                                           \
+    cudaError_t launch_cdr_L##L(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep) { \
+        return launch_cdr_p<L>(row, mode, a, s, prep);                                          \
     }
 
 #define BS_DECLARE_SIZE(L)                                                                      \
@@ -184,7 +227,8 @@ struct Pp8 {
     cudaError_t launch_periodic_L##L(bool row, int mode, const PerArgs& a, cudaStream_t s,      \
                                      bool prep);                                                \
     cudaError_t launch_transposed_L##L(bool row, int mode, const RowArgs& a, const ColArgs& c,  \
-                                       cudaStream_t s, bool prep);
+                                       cudaStream_t s, bool prep);                              \
+    cudaError_t launch_cdr_L##L(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep);
 
 BS_DECLARE_SIZE(3)
 BS_DECLARE_SIZE(4)

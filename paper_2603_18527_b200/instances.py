@@ -75,6 +75,43 @@ def make_instances(spec: InstanceSpec, first: int = 0, count: int = 1, nthreads:
 
 
 def config_instances(name: str, first: int = 0, count: int | None = None, **overrides):
+    if name == "c4":
+        spec = replace(CONFIGS["c4"]["spec"], **overrides) if overrides else CONFIGS["c4"]["spec"]
+        return make_cdr_instances(spec, first, CONFIGS["c4"]["batch"] if count is None else count)
     cfg = CONFIGS[name]
     spec = replace(cfg["spec"], **overrides) if overrides else cfg["spec"]
     return make_instances(spec, first, cfg["batch"] if count is None else count)
+
+
+@dataclass(frozen=True)
+class CdrSpec:
+    """Config c4 media (include/bornsweep_instances.h bp_cdr_spec)."""
+    n: int = 1024
+    b_max: float = 20.0
+    sigma_max: float = 50.0
+    smooth_cells: float = 0.0
+    src_smooth_cells: float = 0.0
+    seed: int = 0
+
+    def _c(self):
+        return N.CdrSpec(self.n, self.b_max, self.sigma_max, self.smooth_cells,
+                         self.src_smooth_cells, self.seed)
+
+
+CONFIGS["c4"] = dict(spec=CdrSpec(n=1024), batch=32, map="scalar", rtol=1e-8)
+
+
+def make_cdr_instances(spec: CdrSpec, first: int = 0, count: int = 1, nthreads: int = 0):
+    """(bx, by, sigma, sigma0, f): real (count, n, n) arrays and sigma0 (count)."""
+    n = spec.n
+    arrs = [np.empty((count, n, n)) for _ in range(4)]
+    s0 = np.empty(count)
+    dp = C.POINTER(C.c_double)
+    s = spec._c()
+    rc = N.host_lib().bp_make_cdr_instances(C.byref(s), first, count, arrs[0].ctypes.data_as(dp),
+                                            arrs[1].ctypes.data_as(dp), arrs[2].ctypes.data_as(dp),
+                                            s0.ctypes.data_as(dp), arrs[3].ctypes.data_as(dp), nthreads)
+    if rc:
+        raise ValueError(f"invalid CDR spec {spec}")
+    bx, by, sigma, f = arrs
+    return bx, by, sigma, s0, f

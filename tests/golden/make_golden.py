@@ -6,6 +6,9 @@
                         to the reference's forward convention (x0.25, proj/src/transforms.cpp:117)
 * ref_rng.npz        -- RngState normals / uniforms from the reference's own rng.hpp
 * ref_samplers.npz   -- sponge_profile / gaussian_bump from the reference's samplers.cpp
+* ref_dct.npz        -- the reference's DCT-II / DCT-III transform pair (Neumann grids,
+                        transforms.cpp:105-148) and Neumann five-point symbol (symbol.cpp:81-92),
+                        plus scipy.fft.dctn(type=2/3) of the same real inputs (config c4)
 * ref_ops_n{16,32}.npz, ref_run_*.npz
                      -- operator outputs and run() trajectories produced by the reference's own
                         L1-L3 code (oracle/_ref) on instances from libbornsweep_host.so
@@ -124,8 +127,27 @@ def periodic_golden():
         np.savez_compressed(os.path.join(HERE, f"ref_periodic_n{n}.npz"), **out)
 
 
+def dct_golden():
+    rng = np.random.default_rng(44)
+    out = {}
+    for nx, ny in [(16, 12), (16, 16), (32, 32), (64, 64)]:
+        x = rng.standard_normal((nx, ny)) + 1j * rng.standard_normal((nx, ny))
+        out[f"x_{nx}x{ny}"] = x
+        out[f"fwd_{nx}x{ny}"] = Reference.dct(x)
+        out[f"inv_{nx}x{ny}"] = Reference.dct(x, inverse=True)
+        out[f"scipy2_{nx}x{ny}"] = sf.dctn(x.real, type=2)
+        out[f"scipy3_{nx}x{ny}"] = sf.dctn(x.real, type=3)
+    for n, lx in [(32, 1.0), (64, 2.0)]:
+        out[f"symbol_n{n}"] = Reference.laplacian_symbol(n, n, lx, lx, bc=2)
+    np.savez_compressed(os.path.join(HERE, "ref_dct.npz"), **out)
+
+
 if __name__ == "__main__":
     Reference.set_mode("serial")
+    if sys.argv[1:] == ["dct"]:
+        dct_golden()
+        sys.exit(0)
+    dct_golden()
     dst_golden()
     dst3_golden()
     rng_golden()
