@@ -42,7 +42,14 @@ WORKLOADS = {
     "c0": "c0: 1 x 127^2 Dirichlet Helmholtz CBS, contrast 0.3, 10 ppw, sponge N/8, rtol 1e-6",
     "c1": "c1: 64 x 511^2 Dirichlet Helmholtz CBS batch, contrast 0.5, 8 ppw, sponge N/8, rtol 1e-6",
     "c2": "c2: 1 x 4095^2 Dirichlet Helmholtz CBS, contrast 0.5, 6 ppw, 16 point sources, rtol 1e-6",
+    "c4": "c4: 32 x 1024^2 Neumann convection-diffusion-reaction (upwind, DCT-II), real fp64, "
+          "scalar gamma 1, rtol 1e-8",
 }
+# c4 (real fp64): RC_A T,u in + u out = 24 B/pt; RC_B u,bx,by,sigma,f in + T out = 48 B/pt;
+# CC_GREEN T in + T out = 16 B/pt
+CDR_ROW_BYTES_PER_PT = 72
+CDR_COL_BYTES_PER_PT = 16
+CDR_SWEEP_BYTES_PER_PT = 88
 UNIT = "Gpts/s"
 ROW_BYTES_PER_PT = 96     # row kernel: T in, u in, k2 in, f in, u out, T out (16 B each)
 COL_BYTES_PER_PT = 32     # column kernel: T in, T out
@@ -137,12 +144,52 @@ def cpu_baseline(k2, f, k0, eta, sweeps, threads):
     return done * nd * nd / dt / 1e9, dt, kind, sample
 
 
+def cpu_baseline_cdr(bx, by, sigma, s0, f, sweeps, threads):
+    """c4 has no reference problem family: the plain-C port (oracle/bp_oracle.c) on the host,
+    OpenMP inside each transform / stencil, members one after another."""
+    from oracle import Oracle, OracleProblem
+    Oracle.set_threads(threads)
+    n = bx.shape[1]
+    t0 = time.perf_counter()
+    done = 0
+    for b in range(bx.shape[0]):
+        done += OracleProblem.cdr(bx[b], by[b], sigma[b], s0[b]).run(
+            f[b] + 0j, rtol=1e-8, max_iters=sweeps).iters
+    dt = time.perf_counter() - t0
+    sample = (f"{bx.shape[0]} c4 member(s) x {sweeps} sweeps of {n}x{n} (full bp::run incl. setup), "
+              f"plain-C port, OpenMP over grid lines, {threads} threads")
+    return done * n * n / dt / 1e9, dt, "port", sample
+
+
 def run_reference_arm(args):
     rank, _, world = dist_env()
     if rank != 0:
         return 0
     import paper_2603_18527_b200 as bs
     cores = os.cpu_count() or 1
+    if args.config == "c4":
+        bx, by, sg, s0, f = bs.config_instances("c4", 0, 1)
+        sweeps = max(1, args.ref_sweeps)
+        for _ in range(args.warmup):
+            cpu_baseline_cdr(bx, by, sg, s0, f, sweeps, cores)
+        times = []
+        for _ in range(args.steps):
+            v, dt, kind, sample = cpu_baseline_cdr(bx, by, sg, s0, f, sweeps, cores)
+            times.append(dt)
+        value = float(len(times) * sweeps * 1024 * 1024 / np.sum(times) / 1e9)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded c4 media)", "impl": "reference",
+            "config": {"workload": "c4", "grid": "1024x1024", "batch_sample": 1,
+                       "sweeps_per_step": sweeps, "parallelism": "OpenMP inside the port"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
     members = min(cores, 64)
     k2, f, k0, eta = bs.config_instances("c1", 0, members)
     sweeps = args.ref_sweeps
@@ -214,14 +261,24 @@ def run_ours(args):
     cfgd = bs.CONFIGS[args.config]
     total = args.batch if args.config == "c1" else cfgd["batch"]
     first, per = shard_members(total, world, rank)
-    k2, f, k0, eta = bs.config_instances(args.config, first, per)
-    nd = k2.shape[1]
+    cdr = args.config == "c4"
+    if cdr:
+        bx, by, sg, s0, f = bs.config_instances("c4", first, per)
+        nd = bx.shape[1]
+        row_b, col_b, sweep_b = CDR_ROW_BYTES_PER_PT, CDR_COL_BYTES_PER_PT, CDR_SWEEP_BYTES_PER_PT
+    else:
+        k2, f, k0, eta = bs.config_instances(args.config, first, per)
+        nd = k2.shape[1]
+        row_b, col_b, sweep_b = ROW_BYTES_PER_PT, COL_BYTES_PER_PT, SWEEP_BYTES_PER_PT
     pts = nd * nd
     cmap = {"pointwise": bs.PointwiseMap(), "scalar": bs.ScalarMap(1.0),
             "optimal_l2": bs.OptimalScalarMap("euclidean")}[args.map or cfgd["map"]]
-    cfg = bs.IterationConfig(rtol=1e-6, max_iters=args.sweeps)
+    cfg = bs.IterationConfig(rtol=cfgd.get("rtol", 1e-6) if cdr else 1e-6, max_iters=args.sweeps)
 
-    prob = bs.HelmholtzDirichlet(k2, k0, eta, device=local_rank)
+    if cdr:
+        prob = bs.CdrNeumann(bx, by, sg, s0, device=local_rank)
+    else:
+        prob = bs.HelmholtzDirichlet(k2, k0, eta, device=local_rank)
     stream = torch.cuda.ExternalStream(prob.stream, device=local_rank)
     f_dev = torch.from_numpy(f).to(f"cuda:{local_rank}")
     u_dev = torch.empty_like(f_dev)
@@ -288,27 +345,34 @@ def run_ours(args):
     work = sum_over_ranks(float(sweeps_done * pts))
     value = work / (elapsed_ms * 1e-3) / 1e9
     value_instrumented = sum_over_ranks(float(inst_sweeps * pts)) / (inst_ms * 1e-3) / 1e9
-    # per-launch kernel durations (row / column kernels; each launch covers the rank's batch)
-    row_avg = row_ms / max(timed, 1)
-    col_avg = col_ms / max(timed, 1)
+    # per-launch kernel durations, normalised to a launch over the whole (active) batch: the
+    # event time of every launch (including the early-exit launches after members converged)
+    # divided by the member-sweeps done, times the members per launch
+    full_launches = max(inst_sweeps, 1) / per
+    row_avg = row_ms / full_launches
+    col_avg = col_ms / full_launches
     pts_per_launch = per * pts
     peak, peak_src = measured_peak()
-    row_gbs = ROW_BYTES_PER_PT * pts_per_launch / (row_avg * 1e-3) / 1e9
-    col_gbs = COL_BYTES_PER_PT * pts_per_launch / (col_avg * 1e-3) / 1e9
-    sweep_gbs = SWEEP_BYTES_PER_PT * pts_per_launch / ((row_avg + col_avg) * 1e-3) / 1e9
-    traffic, traffic_src = load_traffic()
+    row_gbs = row_b * pts_per_launch / (row_avg * 1e-3) / 1e9
+    col_gbs = col_b * pts_per_launch / (col_avg * 1e-3) / 1e9
+    sweep_gbs = sweep_b * pts_per_launch / ((row_avg + col_avg) * 1e-3) / 1e9
+    traffic, traffic_src = load_traffic() if args.config == "c1" else (None, None)
 
     # ------------------------------------------------------------------ e2e through host buffers
-    pin_k2 = torch.empty(k2.shape, dtype=torch.complex128, pin_memory=True)
-    pin_f = torch.empty(f.shape, dtype=torch.complex128, pin_memory=True)
-    pin_u = torch.empty(f.shape, dtype=torch.complex128, pin_memory=True)
-    pin_k2.numpy()[...] = k2
-    pin_f.numpy()[...] = f
-    k2h, fh, uh = pin_k2.numpy(), pin_f.numpy(), pin_u.numpy()
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64 if cdr else torch.complex128, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    fh, uh = pinned(f), pinned(np.zeros_like(f))
+    if cdr:
+        medium = [pinned(a) for a in (bx, by, sg)] + [s0]
+    else:
+        medium = [pinned(k2), k0, eta]
     prob.set_kernel_timing(False)
 
     def step_e2e():
-        prob.set_medium(k2h, k0, eta)
+        prob.set_medium(*medium)
         rc = lib.bp_run(prob.handle, C.byref(mp), fh.ctypes.data_as(dp), C.byref(cc), None,
                         uh.ctypes.data_as(dp), l2.ctypes.data_as(dp), rt.ctypes.data_as(dp), info)
         if rc:
@@ -330,15 +394,20 @@ def run_ours(args):
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     e2e_value = sum_over_ranks(float(e2e_sweeps * pts)) / (e2e_ms * 1e-3) / 1e9
-    h2d = int(k2h.nbytes + fh.nbytes + k0.nbytes + eta.nbytes) * world
+    h2d = int(sum(a.nbytes for a in medium) + fh.nbytes) * world
     d2h = int(uh.nbytes + l2.nbytes + rt.nbytes + per * C.sizeof(N.Trace)) * world
 
     # ------------------------------------------------------------------ CPU baseline (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
-        m = min(cores, per)
-        v, dt, kind, sample = cpu_baseline(k2[:m], f[:m], k0[:m], eta[:m], args.cpu_sweeps, cores)
+        if cdr:
+            m = min(8, per)
+            v, dt, kind, sample = cpu_baseline_cdr(bx[:m], by[:m], sg[:m], s0[:m], f[:m],
+                                                   args.cpu_sweeps_c4, cores)
+        else:
+            m = min(cores, per)
+            v, dt, kind, sample = cpu_baseline(k2[:m], f[:m], k0[:m], eta[:m], args.cpu_sweeps, cores)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
                "seconds": round(dt, 3)}
 
@@ -348,25 +417,29 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded RngState media + centre Gaussian-bump sources, BASELINE c1 construction)",
+            "data": ("synthetic (seeded c4 media: smoothed noise b, sigma, f)" if cdr else
+                     "synthetic (seeded RngState media + centre Gaussian-bump sources, BASELINE c1 construction)"),
             "config": {"workload": WORKLOADS[args.config] + f"; map {args.map or cfgd['map']}",
-                       "grid": f"{nd}x{nd} (n={nd + 1}, h=1/{nd + 1})", "global_batch": total,
+                       "grid": (f"{nd}x{nd} Neumann cell-centred (h=1/{nd})" if cdr else
+                                f"{nd}x{nd} (n={nd + 1}, h=1/{nd + 1})"), "global_batch": total,
                        "members_per_gpu": per, "sweeps_per_step": args.sweeps,
                        "parallelism": f"batch-shard x{world}",
                        "l2": "no flush needed: ~1.7 GB working set per step >> 126 MB L2"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "bp_problem_set_medium + bp_run with pinned host buffers"},
-            "roofline": {"bound": "hbm", "kernel": f"row_kernel<{int(np.log2(nd + 1))},R_SWEEP>",
+            "roofline": {"bound": "hbm",
+                         "kernel": (f"crow_kernel<{int(np.log2(nd))},RC_A> + crow_kernel<{int(np.log2(nd))},RC_B>"
+                                    if cdr else f"row_kernel<{int(np.log2(nd + 1))},R_SWEEP>"),
                          "achieved": row_gbs, "peak": peak, "unit": "GB/s", "frac": row_gbs / peak,
                          "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": ROW_BYTES_PER_PT * pts_per_launch,
+                         "algorithmic_bytes_per_launch": row_b * pts_per_launch,
                          "avg_launch_ms": row_avg,
                          "column_kernel": {"achieved": col_gbs, "frac": col_gbs / peak,
                                            "avg_launch_ms": col_avg,
-                                           "algorithmic_bytes_per_launch": COL_BYTES_PER_PT * pts_per_launch},
+                                           "algorithmic_bytes_per_launch": col_b * pts_per_launch},
                          "sweep": {"achieved": sweep_gbs, "frac": sweep_gbs / peak,
-                                   "bytes_per_pt": SWEEP_BYTES_PER_PT,
+                                   "bytes_per_pt": sweep_b,
                                    "gpts_per_s_kernels_only": pts_per_launch / ((row_avg + col_avg) * 1e-3) / 1e9}},
             "cpu_baseline": cpu,
             "gpu_launches": int(sum_over_ranks(float(launches))),
@@ -386,12 +459,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=64, help="members of config c1 (whole job)")
-    ap.add_argument("--config", choices=["c0", "c1", "c2"], default="c1",
+    ap.add_argument("--config", choices=["c0", "c1", "c2", "c4"], default="c1",
                     help="workload; the headline metric is quoted on c1 (BASELINE.json configs[1])")
     ap.add_argument("--map", choices=["pointwise", "scalar", "optimal_l2"], default=None,
                     help="correction map (default: the config's canonical map)")
     ap.add_argument("--sweeps", type=int, default=127, help="sweeps per step (max_iters)")
-    ap.add_argument("--cpu-sweeps", type=int, default=100)
+    ap.add_argument("--cpu-sweeps", type=int, default=300)
+    ap.add_argument("--cpu-sweeps-c4", type=int, default=30)
     ap.add_argument("--ref-sweeps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -171,6 +171,15 @@ __global__ void init_control_kernel(Control c, int batch) {
     if (b == 0) *c.n_active = batch;
 }
 
+// any non-finite entry -> *flag = 1 (medium validation on the device: the host loop over a
+// c1 / c4 batch costs tens of ms per set_medium)
+__global__ void nonfinite_kernel(const double* __restrict__ x, size_t n, int* flag) {
+    int bad = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
 __global__ void fill_nan_kernel(double* p, size_t n) {
     for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
          k += (size_t)gridDim.x * blockDim.x)
@@ -345,6 +354,7 @@ struct bp_problem {
     double *trace_l2 = nullptr, *trace_reta = nullptr;
     int trace_cap = 0;
     int* host_active = nullptr;  // pinned
+    int* dflag = nullptr;        // device flag of nonfinite_kernel
     // graph cache
     cudaGraphExec_t graph = nullptr;
     int graph_map_kind = -1;
@@ -436,8 +446,32 @@ int check_problem(const bp_problem* p) {
     return BP_OK;
 }
 
+int upload(bp_problem* p, const double* host, double2* dst, bool host_ptr = true);
+
+// true when the n doubles at dev (device memory) are all finite; synchronises the stream
+int all_finite(bp_problem* p, const double* dev, size_t n, bool* ok) {
+    CU(cudaMemsetAsync(p->dflag, 0, sizeof(int), p->stream));
+    nonfinite_kernel<<<grid_for(n), 256, 0, p->stream>>>(dev, n, p->dflag);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(p->host_active, p->dflag, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    *ok = *p->host_active == 0;
+    return BP_OK;
+}
+
+// dense host k2 -> validated (finite) -> padded device k2 (HelmholtzProblem ctor's check,
+// helmholtz.cpp:18-20, done on the staged copy)
+int upload_k2_checked(bp_problem* p, const double* host) {
+    const size_t nd = p->dense_pts;
+    CU(cudaMemcpyAsync(p->dense, host, sizeof(double2) * nd * p->batch, cudaMemcpyHostToDevice, p->stream));
+    bool ok = false;
+    if (int rc = all_finite(p, reinterpret_cast<const double*>(p->dense), 2 * nd * p->batch, &ok)) return rc;
+    if (!ok) return set_err(BP_EINVAL, "HelmholtzProblem: k2 not finite");
+    return upload(p, reinterpret_cast<const double*>(p->dense), p->k2, false);
+}
+
 // dense host -> padded device
-int upload(bp_problem* p, const double* host, double2* dst, bool host_ptr = true) {
+int upload(bp_problem* p, const double* host, double2* dst, bool host_ptr) {
     const size_t nd = p->dense_pts;
     const size_t bytes = sizeof(double2) * nd * p->batch;
     const double2* src = reinterpret_cast<const double2*>(host);
@@ -1294,8 +1328,6 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
         if (!(eta[b] > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
         if (!std::isfinite(k0[b])) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
     }
-    for (size_t k = 0; k < 2 * nd * batch; ++k)
-        if (!std::isfinite(k2[k])) return set_err(BP_EINVAL, "HelmholtzProblem: k2 not finite");
 
     const std::vector<double> xi2 = xi2_table(n, grid->lx);
     if (periodic) {
@@ -1366,6 +1398,7 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     CUF(cudaMalloc(&p->ctl_int, sizeof(int) * (5 * (size_t)batch + 1)));
     CUF(cudaMalloc(&p->counter, sizeof(unsigned) * batch));
     CUF(cudaMallocHost(&p->host_active, sizeof(int)));
+    CUF(cudaMalloc(&p->dflag, sizeof(int)));
     CUF(cudaMalloc(&p->k0sq, sizeof(double) * batch));
     CUF(cudaMalloc(&p->eta, sizeof(double) * batch));
     CUF(cudaMalloc(&p->tw, sizeof(double2) * n));
@@ -1385,7 +1418,7 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     CUF(cudaMemcpyAsync(p->tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->sinp, sinp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->lap, lap.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
-    if (int rc = upload(p, k2, p->k2)) return fail(rc);
+    if (int rc = upload_k2_checked(p, k2)) return fail(rc);
     CUF(cudaStreamSynchronize(p->stream));
     if (int rc = ensure_trace(p, 1000)) return fail(rc);
 #undef CUF
@@ -1397,10 +1430,6 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
 // DCT-II (symbol.cpp:81-92), V = (sigma0 - sigma) - b . grad_upwind.  Real fields.
 int check_cdr_medium(const bp_problem* p, const double* bx, const double* by, const double* sigma,
                      const double* sigma0) {
-    const size_t tot = p->field * p->batch;
-    for (size_t k = 0; k < tot; ++k)
-        if (!std::isfinite(bx[k]) || !std::isfinite(by[k]) || !std::isfinite(sigma[k]))
-            return set_err(BP_EINVAL, "CDR medium not finite");
     const double h = p->grid.lx / p->n;
     std::vector<double> lapn(p->n);
     for (int k = 0; k < p->n; ++k) {
@@ -1434,10 +1463,21 @@ int check_cdr_medium(const bp_problem* p, const double* bx, const double* by, co
 
 int upload_cdr_medium(bp_problem* p, const double* bx, const double* by, const double* sigma,
                       const double* sigma0) {
-    const size_t bytes = sizeof(double) * p->field * p->batch;
-    CU(cudaMemcpyAsync(p->bx, bx, bytes, cudaMemcpyHostToDevice, p->stream));
-    CU(cudaMemcpyAsync(p->by, by, bytes, cudaMemcpyHostToDevice, p->stream));
-    CU(cudaMemcpyAsync(p->sigma, sigma, bytes, cudaMemcpyHostToDevice, p->stream));
+    // staged through the scratch fields (T, x, y) and validated there, so a rejected medium
+    // leaves the handle's current one intact
+    const size_t n = p->field * p->batch, bytes = sizeof(double) * n;
+    double* st[3] = {reinterpret_cast<double*>(p->T), reinterpret_cast<double*>(p->x),
+                     reinterpret_cast<double*>(p->y)};
+    const double* src[3] = {bx, by, sigma};
+    double* dst[3] = {p->bx, p->by, p->sigma};
+    for (int i = 0; i < 3; ++i)
+        CU(cudaMemcpyAsync(st[i], src[i], bytes, cudaMemcpyHostToDevice, p->stream));
+    bool ok = true;
+    for (int i = 0; i < 3 && ok; ++i)
+        if (int rc = all_finite(p, st[i], n, &ok)) return rc;
+    if (!ok) return set_err(BP_EINVAL, "CDR medium not finite");
+    for (int i = 0; i < 3; ++i)
+        CU(cudaMemcpyAsync(dst[i], st[i], bytes, cudaMemcpyDeviceToDevice, p->stream));
     CU(cudaMemcpyAsync(p->sigma0, sigma0, sizeof(double) * p->batch, cudaMemcpyHostToDevice, p->stream));
     CU(cudaStreamSynchronize(p->stream));
     return BP_OK;
@@ -1495,6 +1535,7 @@ int create_cdr_impl(const bp_grid* grid, int32_t batch, const double* bx, const 
     CUF(cudaMalloc(&p->counter, sizeof(unsigned) * batch));
     CUF(cudaMemsetAsync(p->counter, 0, sizeof(unsigned) * batch, p->stream));
     CUF(cudaMallocHost(&p->host_active, sizeof(int)));
+    CUF(cudaMalloc(&p->dflag, sizeof(int)));
     CUF(cudaMalloc(&p->tw, sizeof(double2) * n));
     CUF(cudaMalloc(&p->w4, sizeof(double2) * n));
     CUF(cudaMalloc(&p->lapn, sizeof(double) * n));
@@ -1588,7 +1629,7 @@ int bp_problem_destroy(bp_problem* p) {
                     (void*)p->trace_l2, (void*)p->trace_reta, (void*)p->k0sq, (void*)p->eta,
                     (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2, (void*)p->TT,
                     (void*)p->bx, (void*)p->by, (void*)p->sigma, (void*)p->sigma0, (void*)p->lapn,
-                    (void*)p->rnorm2, (void*)p->w4})
+                    (void*)p->rnorm2, (void*)p->w4, (void*)p->dflag})
         if (q) cudaFree(q);
     if (p->host_active) cudaFreeHost(p->host_active);
     if (p->stream) cudaStreamDestroy(p->stream);
@@ -1769,20 +1810,21 @@ int bp_problem_set_medium(bp_problem* p, const double* k2, const double* k0, con
     if (int rc = check_problem(p)) return rc;
     if (p->cdr) return set_err(BP_EINVAL, "CDR problem: use bp_problem_set_cdr_medium");
     if (!k2 || !k0 || !eta) return set_err(BP_EINVAL, "null argument");
-    const size_t nd = p->dense_pts;
     for (int b = 0; b < p->batch; ++b) {
         if (!(eta[b] > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
         if (!std::isfinite(k0[b])) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
     }
-    for (size_t k = 0; k < 2 * nd * p->batch; ++k)
-        if (!std::isfinite(k2[k])) return set_err(BP_EINVAL, "HelmholtzProblem: k2 not finite");
-    if (int rc = check_symbol(p->grid, p->dim, p->batch, k0, eta)) return rc;
+    if (p->periodic) {
+        if (int rc = check_symbol_periodic(xi2_table(p->n, p->grid.lx), p->batch, k0, eta)) return rc;
+    } else if (int rc = check_symbol(p->grid, p->dim, p->batch, k0, eta)) {
+        return rc;
+    }
     DeviceGuard guard(p->device);
+    if (int rc = upload_k2_checked(p, k2)) return rc;  // validated before anything is replaced
     std::vector<double> k0sq(p->batch);
     for (int b = 0; b < p->batch; ++b) k0sq[b] = k0[b] * k0[b];
     CU(cudaMemcpyAsync(p->k0sq, k0sq.data(), sizeof(double) * p->batch, cudaMemcpyHostToDevice, p->stream));
     CU(cudaMemcpyAsync(p->eta, eta, sizeof(double) * p->batch, cudaMemcpyHostToDevice, p->stream));
-    if (int rc = upload(p, k2, p->k2)) return rc;
     CU(cudaStreamSynchronize(p->stream));
     return BP_OK;
 }

@@ -94,6 +94,29 @@ struct DctEngine {
         }
         pol.sync();
     }
+
+    // REDFT01 of a packed pair whose spectrum Y already sits in buf (natural order)
+    template <class Pol>
+    __device__ __forceinline__ static void dct3_smem(double2 (&x)[P], int t, double2* buf,
+                                                     const double2* __restrict__ tw,
+                                                     const double2* __restrict__ w4, const Pol& pol) {
+        double2 v[P];
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            const int k = t + T * m;
+            const double2 w = cconj(__ldg(&w4[k]));
+            const double2 ym = k ? buf[G::pidx(N - k)] : make_double2(0.0, 0.0);
+            v[m] = cmul(w, csub(buf[G::pidx(k)], mul_pi(ym)));
+        }
+        pol.sync();
+        fft_to_smem<true>(v, t, buf, tw, pol);
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            const int j = t + T * m;
+            x[m] = cconj(buf[G::pidx((j & 1) ? N - 1 - (j >> 1) : (j >> 1))]);
+        }
+        pol.sync();
+    }
 };
 
 enum CRowMode { RC_FWD = 0, RC_INV = 1, RC_A = 2, RC_B = 3 };
@@ -154,6 +177,26 @@ crow_kernel(const CdrArgs a) {
     const double2 zero = make_double2(0.0, 0.0);
     double acc = 0.0;
 
+    // Everything an engine reads sits in two adjacent rows (+ a halo row each side for the
+    // RC_B stencil): one bulk L2 prefetch per array puts all of it in flight at once; the loads
+    // below (RC_B stencil, RC_A u after the transform) then hit L2.
+    const double* ucur = (m & 1) ? a.u1 : a.u0;
+    const bool firstA = (2 * pr == 0), lastB = (2 * pr + 1 == N - 1);
+    if ((MODE == RC_A || MODE == RC_B) && valid && t == 0) {
+        constexpr unsigned R2 = 2 * N * sizeof(double);
+        prefetch_l2(ucur + rowA, R2);
+        if constexpr (MODE == RC_A) {
+            prefetch_l2(a.T + rowA, R2);
+        } else {
+            prefetch_l2(a.bx + rowA, R2);
+            prefetch_l2(a.by + rowA, R2);
+            prefetch_l2(a.sigma + rowA, R2);
+            prefetch_l2(a.f + rowA, R2);
+            if (!firstA) prefetch_l2(ucur + rowA - N, R2 / 2);
+            if (!lastB) prefetch_l2(ucur + rowB + N, R2 / 2);
+        }
+    }
+
     double2 q[P];
     if constexpr (MODE == RC_INV || MODE == RC_A) {
         double2 y[P], ym[P], z[P];
@@ -176,7 +219,6 @@ crow_kernel(const CdrArgs a) {
                 }
             } else {
                 // RC_A: z = G q^m (scaled in CC); x = z - u^m; u^{m+1} = u^m + gamma x
-                const double* ucur = (m & 1) ? a.u1 : a.u0;
                 double* unext = (m & 1) ? a.u0 : a.u1;
                 const double2 u = valid ? make_double2(ucur[rowA + j], ucur[rowB + j]) : zero;
                 const double2 x = csub(z[mm], u);
@@ -197,41 +239,54 @@ crow_kernel(const CdrArgs a) {
             }
         } else {
             // RC_B on u^m (m = sweep[b]): r = f - A u, q = V u + f, A = -Lap_N + conv + sigma,
-            // V = (sigma0 - sigma) - conv; reflective ghosts (cell-centred Neumann)
-            const double* uc = (m & 1) ? a.u1 : a.u0;
-            const double ih = 1.0 / a.h, ih2 = ih * ih;
-            const double s0 = valid ? a.sigma0[b] : 0.0;
-            const bool firstA = (2 * pr == 0), lastB = (2 * pr + 1 == N - 1);
+            // V = (sigma0 - sigma) - conv; reflective ghosts (cell-centred Neumann).  The pair's
+            // own values go through shared memory for the y-neighbours (j -+ 1); rows A and B
+            // are each other's x-neighbour, so only the halo rows come from global memory.
 #pragma unroll
             for (int mm = 0; mm < P; ++mm) {
                 const int j = t + T * mm;
+                q[mm] = valid ? make_double2(ucur[rowA + j], ucur[rowB + j]) : zero;
+                buf[G::pidx(j)] = q[mm];
+            }
+            pol.sync();
+            const double ih = 1.0 / a.h, ih2 = ih * ih;
+            const double s0 = valid ? a.sigma0[b] : 0.0;
+#pragma unroll
+            for (int mm = 0; mm < P; ++mm) {
+                const int j = t + T * mm;
+                const double2 c = q[mm];
+                const double2 so = j > 0 ? buf[G::pidx(j - 1)] : c;
+                const double2 no = j + 1 < N ? buf[G::pidx(j + 1)] : c;
+                double wA = c.x, eB = c.y, vx[2] = {0, 0}, vy[2] = {0, 0}, sg[2] = {0, 0}, ff[2] = {0, 0};
+                if (valid) {
+                    if (!firstA) wA = ucur[rowA - N + j];
+                    if (!lastB) eB = ucur[rowB + N + j];
+#pragma unroll
+                    for (int s = 0; s < 2; ++s) {
+                        const size_t o = (s ? rowB : rowA) + j;
+                        vx[s] = a.bx[o];
+                        vy[s] = a.by[o];
+                        sg[s] = a.sigma[o];
+                        ff[s] = a.f[o];
+                    }
+                }
                 double res[2], qq[2];
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
-                    const size_t row = s == 0 ? rowA : rowB;
-                    double c = 0, w = 0, e2 = 0, so = 0, no = 0, vx = 0, vy = 0, sg = 0, ff = 0;
-                    if (valid) {
-                        c = uc[row + j];
-                        // x-neighbours (rows): reflective at the first / last row
-                        w = (s == 0 && firstA) ? c : uc[row - N + j];
-                        e2 = (s == 1 && lastB) ? c : uc[row + N + j];
-                        so = j > 0 ? uc[row + j - 1] : c;
-                        no = j + 1 < N ? uc[row + j + 1] : c;
-                        vx = a.bx[row + j];
-                        vy = a.by[row + j];
-                        sg = a.sigma[row + j];
-                        ff = a.f[row + j];
-                    }
-                    const double lap = (4.0 * c - w - e2 - so - no) * ih2;  // -Lap_N u
-                    const double dx = vx >= 0.0 ? (c - w) * ih : (e2 - c) * ih;
-                    const double dy = vy >= 0.0 ? (c - so) * ih : (no - c) * ih;
-                    const double conv = vx * dx + vy * dy;
-                    res[s] = ff - ((lap + conv) + sg * c);
-                    qq[s] = ((s0 - sg) * c - conv) + ff;
+                    const double cv = s ? c.y : c.x;
+                    const double w = s ? c.x : wA, e2 = s ? eB : c.y;
+                    const double sv = s ? so.y : so.x, nv = s ? no.y : no.x;
+                    const double lap = (4.0 * cv - w - e2 - sv - nv) * ih2;  // -Lap_N u
+                    const double dx = vx[s] >= 0.0 ? (cv - w) * ih : (e2 - cv) * ih;
+                    const double dy = vy[s] >= 0.0 ? (cv - sv) * ih : (nv - cv) * ih;
+                    const double conv = vx[s] * dx + vy[s] * dy;
+                    res[s] = ff[s] - ((lap + conv) + sg[s] * cv);
+                    qq[s] = ((s0 - sg[s]) * cv - conv) + ff[s];
                 }
                 acc += res[0] * res[0] + res[1] * res[1];
                 q[mm] = make_double2(qq[0], qq[1]);
             }
+            pol.sync();  // buf is the transform's workspace next
         }
     }
 
@@ -282,7 +337,8 @@ ccol_kernel(const CdrArgs a) {
     using Eng = DctEngine<LOG2N, PP>;
     constexpr int N = G::N, P = G::P, T = G::T;
     extern __shared__ double2 smem[];
-    const int c = threadIdx.x % C, t = threadIdx.x / C;
+    int c, t;
+    col_thread_map<G::T, C>(t, c);
     constexpr int GROUPS = N / (2 * C);  // C packed column pairs per CTA
     const int b = blockIdx.x / GROUPS;
     const int q0 = (blockIdx.x % GROUPS) * 2 * C + 2 * c;  // real columns q0, q0 + 1
@@ -330,14 +386,7 @@ ccol_kernel(const CdrArgs a) {
                 buf[G::pidx(p)] = y[mm];
             }
             pol.sync();
-            double2 ym[P];
-#pragma unroll
-            for (int mm = 0; mm < P; ++mm) {
-                const int k = t + T * mm;
-                ym[mm] = k ? buf[G::pidx(N - k)] : make_double2(0.0, 0.0);
-            }
-            pol.sync();
-            Eng::dct3(y, ym, x, t, buf, a.tw, a.w4, pol);
+            Eng::dct3_smem(x, t, buf, a.tw, a.w4, pol);
 #pragma unroll
             for (int mm = 0; mm < P; ++mm) Tp[col + (size_t)(t + T * mm) * LS] = x[mm];
         }

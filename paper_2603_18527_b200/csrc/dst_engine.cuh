@@ -325,6 +325,25 @@ struct BlockSeg {
     }
 };
 
+// Thread -> (engine c, engine thread t) for the column kernels (C engines per CTA, T threads
+// each).  Global coalescing wants the C engines (adjacent columns) side by side in a warp; the
+// shared-memory side wants each 8-lane phase of a 16-B access inside ONE engine, where the pidx
+// padding makes the accesses conflict-free.  With C in {2, 4}: lane = (t mod 32/C) + (32/C) c,
+// so a warp still covers C adjacent columns x 32/C rows.  C = 8 keeps c fastest (a phase is 8
+// engines at one t; the odd engine stride PAD_N keeps those conflict-free).
+template <int T, int C>
+__device__ __forceinline__ void col_thread_map(int& t, int& c) {
+    constexpr int LPE = 32 / C;
+    if constexpr ((C == 2 || C == 4) && T >= LPE) {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        c = lane / LPE;
+        t = lane % LPE + LPE * w;
+    } else {
+        c = threadIdx.x % C;
+        t = threadIdx.x / C;
+    }
+}
+
 // ------------------------------------------------------------------ the engine
 template <int LOG2N, int PP = 16>
 struct DstEngine {

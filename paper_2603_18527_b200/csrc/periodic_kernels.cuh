@@ -163,7 +163,8 @@ pcol_kernel(const PerArgs a) {
     using Engine = FftEngine<LOG2N, PP>;
     constexpr int N = G::N, P = G::P, T = G::T;
     extern __shared__ double2 smem[];
-    const int c = threadIdx.x % C, t = threadIdx.x / C;
+    int c, t;
+    col_thread_map<G::T, C>(t, c);
     constexpr int GROUPS = N / C;
     const int b = blockIdx.x / GROUPS;
     const int q = (blockIdx.x % GROUPS) * C + c;

@@ -581,7 +581,8 @@ col_kernel(const ColArgs a) {
     using Engine = DstEngine<LOG2N, PP>;
     constexpr int N = G::N, P = G::P, T = G::T;
     extern __shared__ double2 smem[];
-    const int c = threadIdx.x % C, t = threadIdx.x / C;
+    int c, t;
+    col_thread_map<G::T, C>(t, c);
     constexpr int GROUPS = N / C;
     // line group -> member b, base offset `mem`, line stride LS, and (3-D x-lines) the y index
     int b, yl = 0;

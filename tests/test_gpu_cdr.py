@@ -139,5 +139,21 @@ def test_cdr_errors(gpu):
             bs.run(p, bs.ScalarMap(1.0 + 0.5j), f)
         with pytest.raises(ValueError):
             bs.run(p, bs.ScalarMap(1.0), np.zeros((1, 32, 32)))
+        before = bs.run(p, bs.ScalarMap(1.0), f)
         with pytest.raises(ValueError):
             p.set_medium(z, z, z + np.nan, 1.0)
+        after = bs.run(p, bs.ScalarMap(1.0), f)  # the rejected medium replaced nothing
+        assert np.array_equal(before.u, after.u)
+
+
+def test_cdr_set_medium_equals_fresh_handle(gpu):
+    bx, by, sigma, s0, f = media(64, 2, seed=21)
+    bx2, by2, sigma2, s02, _ = media(64, 2, seed=22)
+    cfg = bs.IterationConfig("cbs", 1e-8, 300)
+    with bs.CdrNeumann(bx, by, sigma, s0) as p:
+        bs.run(p, bs.ScalarMap(1.0), f, cfg)
+        p.set_medium(bx2, by2, sigma2, s02)
+        swapped = bs.run(p, bs.ScalarMap(1.0), f, cfg)
+    with bs.CdrNeumann(bx2, by2, sigma2, s02) as q:
+        fresh = bs.run(q, bs.ScalarMap(1.0), f, cfg)
+    assert np.array_equal(swapped.u, fresh.u)

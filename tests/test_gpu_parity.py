@@ -302,6 +302,28 @@ def test_errors_follow_reference(gpu):
         bs.HelmholtzDirichlet(bad, k0, eta)
 
 
+def test_rejected_medium_leaves_handle_intact(gpu):
+    """set_medium validates the new k2 on the device before replacing anything: a rejected
+    medium leaves the previous one (and its run result) in place."""
+    k2, f, k0, eta = instance(32, batch=2, seed=12)
+    cfg = bs.IterationConfig(rtol=1e-6, max_iters=300)
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        before = bs.run(p, bs.ScalarMap(1.0), f, cfg)
+        bad = k2.copy()
+        bad[1, 5, 7] = np.inf
+        with pytest.raises(ValueError, match="finite"):
+            p.set_medium(bad, k0 * 1.1, eta * 2.0)
+        after = bs.run(p, bs.ScalarMap(1.0), f, cfg)
+        assert np.array_equal(before.u, after.u)
+        # an accepted medium takes effect (same as a fresh handle)
+        k2b, _, k0b, etab = instance(32, batch=2, seed=13)
+        p.set_medium(k2b, k0b, etab)
+        swapped = bs.run(p, bs.ScalarMap(1.0), f, cfg)
+    with bs.HelmholtzDirichlet(k2b, k0b, etab) as q:
+        fresh = bs.run(q, bs.ScalarMap(1.0), f, cfg)
+    assert np.array_equal(swapped.u, fresh.u)
+
+
 def test_cbs_equals_npbs_on_gpu(gpu):
     k2, f, k0, eta = instance(64, ppw=10.0, contrast=0.3, seed=1)
     with bs.HelmholtzDirichlet(k2, k0, eta) as p:

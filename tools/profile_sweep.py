@@ -17,6 +17,13 @@ ap.add_argument("--members", type=int, default=64)
 ap.add_argument("--sweeps", type=int, default=4)
 ap.add_argument("--config", default="c1")
 args = ap.parse_args()
+if args.config == "c4":
+    bx, by, sg, s0, f = bs.config_instances("c4", 0, args.members)
+    with bs.CdrNeumann(bx, by, sg, s0) as p:
+        p.set_kernel_timing(True)
+        r = bs.run(p, bs.ScalarMap(1.0), f, bs.IterationConfig(rtol=1e-8, max_iters=args.sweeps))
+        print("iters", [t.iters for t in r.traces[:4]], p.last_run_stats())
+    sys.exit(0)
 k2, f, k0, eta = bs.config_instances(args.config, 0, args.members)
 with bs.HelmholtzDirichlet(k2, k0, eta) as p:
     cmap = bs.PointwiseMap() if args.config == "c1" else bs.ScalarMap(1.0)
