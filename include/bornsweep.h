@@ -133,6 +133,9 @@ int bp_problem_create_cdr(const bp_grid* grid, int32_t batch, const double* bx, 
                           bp_problem** out);
 int bp_problem_set_cdr_medium(bp_problem* p, const double* bx, const double* by,
                               const double* sigma, const double* sigma0);
+/* Launch every later call of this handle on `stream` (a cudaStream_t owned by the caller, e.g.
+ * the framework's current stream, so collectives issued on it are ordered with the kernels). */
+int bp_problem_set_stream(bp_problem* p, void* stream);
 int bp_problem_destroy(bp_problem* p);
 int bp_problem_batch(const bp_problem* p, int32_t* batch, bp_grid* grid);
 /* Replace the media of every member (same grid and batch): equivalent to constructing new
@@ -182,6 +185,47 @@ int bp_run_snapshots(const bp_problem* p, const bp_map* map, const double* f,
 int bp_set_kernel_timing(bp_problem* p, int32_t enable);
 int bp_last_run_stats(const bp_problem* p, int64_t* kernel_launches, int64_t* active_sweeps,
                       double* row_kernel_ms, double* col_kernel_ms, int64_t* timed_sweeps);
+
+/* ---- slab decomposition of ONE 2-D Dirichlet grid over nranks GPUs (config c2).
+ * Rank r owns padded rows [r R, (r+1) R), R = (nx+1)/nranks.  The y-DSTs (rows) are local; the
+ * x-DSTs need full columns, so the row side writes T blocked by destination rank
+ * ([nranks][R][R]: the all-to-all send buffer) and the column pass runs on the received
+ * [nranks][R][R] = n x R column block.  The driver (paper_2603_18527_b200/slab.py) runs, per
+ * sweep: halo exchange of u^m's edge rows -> BP_SLAB_SWEEP -> all-reduce sums[0..1] ->
+ * BP_SLAB_FINALIZE (the termination test of iterate.cpp:134-150 on identical sums on every
+ * rank) -> all-to-all t_rows -> t_cols -> BP_SLAB_COL -> all-to-all back.  Scalar and pointwise
+ * maps; bp_run semantics otherwise. */
+enum {
+    BP_SLAB_FWD_F = 0,     /* t_rows <- y-DST of f; sums[0] = local ||f||^2 */
+    BP_SLAB_COL = 1,       /* t_cols: x-DST, x Green weights, inverse x-DST (in place) */
+    BP_SLAB_INV_NORM = 2,  /* y <- inverse y-DST of t_rows; sums[1] = local ||y||^2 */
+    BP_SLAB_INIT = 3,      /* a0 = ||f||, a1 = ||G f|| (global), cfg: control + traces reset */
+    BP_SLAB_FWD_BORN = 4,  /* t_rows <- y-DST of V u^0 + f */
+    BP_SLAB_SWEEP = 5,     /* fused sweep; sums[0..1] = local entry sums */
+    BP_SLAB_FINALIZE = 6   /* trace entry + termination from the all-reduced sums */
+};
+typedef struct {
+    int32_t rank, nranks, rows, row0, n;
+    int64_t block_elems;           /* R*R complex per destination rank */
+    void* t_rows;                  /* device [nranks][R][R] complex128 */
+    void* t_cols;                  /* device [nranks][R][R] complex128 */
+    void* sums;                    /* device double[4] */
+    void* u_first[2];              /* device: first / last owned row of u ping (0) and pong (1) */
+    void* u_last[2];
+    void* u_halo_lo[2];            /* device: halo rows (row0 - 1, row0 + R) */
+    void* u_halo_hi[2];
+    void* stream;
+} bp_slab_view_t;
+int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const double* k2, double k0,
+                   double eta, int32_t device, bp_problem** out);
+int bp_slab_view(const bp_problem* p, bp_slab_view_t* v);
+/* f, u0: the FULL dense nx*ny fields (host); u0 may be null */
+int bp_slab_set_fields(bp_problem* p, const double* f, const double* u0);
+int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter_config* cfg,
+                  double a0, double a1);
+int bp_slab_active(bp_problem* p, int32_t* n_active);
+/* writes this rank's rows of the dense nx*ny result into u_dense; traces as bp_run */
+int bp_slab_result(bp_problem* p, double* u_dense, double* res_l2, double* res_reta, bp_trace* info);
 
 #ifdef __cplusplus
 }

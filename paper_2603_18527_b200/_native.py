@@ -46,6 +46,14 @@ class Trace(C.Structure):
                 ("fnorm_reta", C.c_double)]
 
 
+class SlabView(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("rows", C.c_int32), ("row0", C.c_int32),
+                ("n", C.c_int32), ("block_elems", C.c_int64), ("t_rows", C.c_void_p),
+                ("t_cols", C.c_void_p), ("sums", C.c_void_p), ("u_first", C.c_void_p * 2),
+                ("u_last", C.c_void_p * 2), ("u_halo_lo", C.c_void_p * 2),
+                ("u_halo_hi", C.c_void_p * 2), ("stream", C.c_void_p)]
+
+
 class InstanceSpec(C.Structure):
     _fields_ = [("n", C.c_int32), ("ppw", C.c_double), ("contrast", C.c_double),
                 ("sigma_cells", C.c_double), ("src_sigma_cells", C.c_double),
@@ -69,6 +77,15 @@ ABI_FUNCTIONS = {
     "bp_problem_create_cdr": (C.c_int, [C.POINTER(Grid), C.c_int32, _dp, _dp, _dp, _dp, C.c_int32,
                                         C.POINTER(C.c_void_p)]),
     "bp_problem_set_cdr_medium": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp]),
+    "bp_problem_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "bp_slab_create": (C.c_int, [C.POINTER(Grid), C.c_int32, C.c_int32, _dp, C.c_double, C.c_double,
+                                 C.c_int32, C.POINTER(C.c_void_p)]),
+    "bp_slab_view": (C.c_int, [C.c_void_p, C.POINTER(SlabView)]),
+    "bp_slab_set_fields": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "bp_slab_stage": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Map), C.POINTER(IterConfig),
+                                C.c_double, C.c_double]),
+    "bp_slab_active": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    "bp_slab_result": (C.c_int, [C.c_void_p, _dp, _dp, _dp, C.POINTER(Trace)]),
     "bp_problem_destroy": (C.c_int, [C.c_void_p]),
     "bp_problem_batch": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(Grid)]),
     "bp_problem_set_medium": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),

@@ -140,12 +140,12 @@ __global__ void norm_partial_kernel(const double2* __restrict__ x, size_t per, i
 }
 
 __global__ void norm_final_kernel(const double* __restrict__ partials, int nchunk, int batch,
-                                  double* __restrict__ out) {
+                                  double* __restrict__ out, int squared) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= batch) return;
     double s = 0.0;
     for (int c = 0; c < nchunk; ++c) s += partials[b * nchunk + c];
-    out[b] = sqrt(s);
+    out[b] = squared ? s : sqrt(s);
 }
 
 // y = y - v (and y = f - y when f != null): the periodic A = L_ref - V combination
@@ -327,6 +327,15 @@ struct bp_problem {
     double *bx = nullptr, *by = nullptr, *sigma = nullptr, *sigma0 = nullptr, *lapn = nullptr,
            *rnorm2 = nullptr;
     double2* w4 = nullptr;
+    // slab decomposition (one rank's x-slab of a distributed 2-D grid, batch 1)
+    int slab_log2 = 0, slab_rank = 0, slab_nranks = 1, row0 = 0;
+    double2 *u_alloc0 = nullptr, *u_alloc1 = nullptr;  // u with one halo row each side
+    double2* Tc = nullptr;                              // column-side block
+    double* slab_sums = nullptr;
+    bool slab_running = false;
+    int slab_max_iters = 1000;
+    double slab_rtol = 1e-6;
+    bool own_stream = true;
     double2* TT = nullptr;
     double* xi2 = nullptr;   // periodic: xi_j^2, FFT order
     size_t field = 0;   // padded elements per member (n^dim)
@@ -506,14 +515,14 @@ int download(bp_problem* p, const double2* p0, const double2* p1, const int* sel
     return BP_OK;
 }
 
-int norms(bp_problem* p, const double2* x, double* out) {
+int norms(bp_problem* p, const double2* x, double* out, bool squared = false) {
     const int nchunk = 64;
     dim3 g(nchunk, p->batch);
     // real (CDR) fields are read as pairs: |re|^2 + |im|^2 over half as many double2
     const size_t per = p->cdr ? p->field / 2 : p->field;
     norm_partial_kernel<<<g, 256, 0, p->stream>>>(x, per, nchunk, p->norm_part);
     norm_final_kernel<<<(p->batch + 127) / 128, 128, 0, p->stream>>>(p->norm_part, nchunk,
-                                                                      p->batch, out);
+                                                                      p->batch, out, squared);
     CU(cudaGetLastError());
     return BP_OK;
 }
@@ -800,16 +809,25 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
 
 int finish_run_periodic(bp_problem* p, double* u_out, bool host_ptr);
 int finish_run_cdr(bp_problem* p, double* u_out, bool host_ptr);
+int finish_run_traces(bp_problem* p, const bp_iter_config* cfg, double* res_l2, double* res_reta,
+                      bp_trace* info);
 
 int finish_run(bp_problem* p, const bp_iter_config* cfg, double* u_out, bool host_ptr,
                double* res_l2, double* res_reta, bp_trace* info) {
-    const int B = p->batch;
     Control c = make_control(p);
     int rc = p->cdr        ? finish_run_cdr(p, u_out, host_ptr)
              : p->periodic ? finish_run_periodic(p, u_out, host_ptr)
                            : download(p, p->u0, p->u1, c.result_buf, u_out, host_ptr);
     if (rc) return rc;
     if (!p->periodic && !p->cdr) p->stat_launches += 1;  // unpack
+    return finish_run_traces(p, cfg, res_l2, res_reta, info);
+}
+
+// iteration counts, terminations, norms and the trace vectors of the last run -> host
+int finish_run_traces(bp_problem* p, const bp_iter_config* cfg, double* res_l2, double* res_reta,
+                      bp_trace* info) {
+    const int B = p->batch;
+    Control c = make_control(p);
     std::vector<int> iters(B), term(B);
     std::vector<double> f1(B), f2(B);
     CU(cudaMemcpyAsync(iters.data(), c.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, p->stream));
@@ -1559,6 +1577,314 @@ int create_cdr_impl(const bp_grid* grid, int32_t batch, const double* bx, const 
     return BP_OK;
 }
 
+
+// ------------------------------------------------------------------ slab decomposition (host)
+// One rank's x-slab of a distributed 2-D Dirichlet grid (config c2 across GPUs, SURVEY.md
+// 8(e)).  The driver (paper_2603_18527_b200/slab.py) sequences the stages below with the
+// collectives between them: all-to-all of the blocked row-side T (t_rows) into the column-side
+// block (t_cols) and back, the u halo-row exchange, and the all-reduce of the two trace sums.
+
+__global__ void slab_finalize_kernel(Control c, const double* sums) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && c.status[0] == ST_ACTIVE)
+        finalize_entry(c, 0, c.sweep[0], sums[0], sums[1]);
+}
+
+// dense reference rows (nx*ny interior, x slow) -> padded slab rows [row0, row0 + R) (host)
+void pack_slab_host(const double* dense, int n, int row0, int R, std::vector<double2>& out) {
+    out.assign((size_t)R * n, make_double2(0.0, 0.0));
+    const int nd = n - 1;
+    for (int i = 0; i < R; ++i) {
+        const int x = row0 + i;
+        if (x < 1 || x > nd) continue;
+        const double* src = dense + 2 * (size_t)(x - 1) * nd;
+        for (int y = 1; y < n; ++y) out[(size_t)i * n + y] = make_double2(src[2 * (y - 1)], src[2 * (y - 1) + 1]);
+    }
+}
+
+RowArgs slab_row_args(const bp_problem* p) {
+    RowArgs a = row_args(p);
+    a.slab_log2 = p->slab_log2;
+    a.row0 = p->row0;
+    a.slab_sums = p->slab_sums;
+    return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bp_problem_set_stream(bp_problem* p, void* stream) {
+    if (int rc = check_problem(p)) return rc;
+    DeviceGuard guard(p->device);
+    CU(cudaStreamSynchronize(p->stream));
+    if (p->own_stream) CU(cudaStreamDestroy(p->stream));
+    p->stream = (cudaStream_t)stream;
+    p->own_stream = false;
+    return BP_OK;
+}
+
+int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const double* k2, double k0,
+                   double eta, int32_t device, bp_problem** out) {
+    if (!out) return set_err(BP_EINVAL, "null output handle");
+    *out = nullptr;
+    if (!grid || !k2) return set_err(BP_EINVAL, "null argument");
+    if (grid->bc != BP_BC_DIRICHLET) return set_err(BP_ENOTSUP, "slab decomposition: Dirichlet grids only");
+    if (nranks < 1 || (nranks & (nranks - 1)) || rank < 0 || rank >= nranks)
+        return set_err(BP_EINVAL, "slab decomposition: nranks must be a power of two, 0 <= rank < nranks");
+    const int n = grid->nx + 1;
+    int log2n = 0;
+    while ((1 << log2n) < n) ++log2n;
+    if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > kMaxLog2)
+        return set_err(BP_ENOTSUP, "GPU path needs square grids with nx+1 = 2^k, 8 <= 2^k <= 4096");
+    if (grid->lx != grid->ly) return set_err(BP_ENOTSUP, "GPU path needs lx == ly (hx == hy)");
+    const int R = n / nranks;
+    if (R < 8) return set_err(BP_ENOTSUP, "slab decomposition: at least 8 rows per rank");
+    if (!(eta > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
+    if (!std::isfinite(k0)) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
+    if (int rc = check_symbol(*grid, 2, 1, &k0, &eta)) return rc;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return set_err(BP_ECUDA, "no such CUDA device");
+    DeviceGuard guard(device);
+    auto* p = new bp_problem();
+    p->grid = *grid;
+    p->batch = 1;
+    p->device = device;
+    p->log2n = log2n;
+    p->n = n;
+    p->dim = 2;
+    p->slab_nranks = nranks;
+    p->slab_rank = rank;
+    p->slab_log2 = 0;
+    while ((1 << p->slab_log2) < R) ++p->slab_log2;
+    p->row0 = rank * R;
+    p->field = (size_t)R * n;
+    p->alloc = p->field;
+    p->dense_pts = (size_t)grid->nx * grid->ny;
+    const double h = grid->lx / n;
+    p->inv_h2 = 1.0 / (h * h);
+    p->green_scale = std::pow(2.0 / n, 2) / std::pow(kEngineGain, 4);
+    auto fail = [&](int code) {
+        bp_problem_destroy(p);
+        return code;
+    };
+#define CUF(call)                                                                                   \
+    do {                                                                                            \
+        cudaError_t _e = (call);                                                                    \
+        if (_e != cudaSuccess) return fail(set_err(BP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e))); \
+    } while (0)
+    CUF(prepare_kernels(log2n, 2));
+    {
+        ColArgs c{};
+        CUF(launch_col_pp(log2n, 16, CL_SLAB, C_GREEN, c, nullptr, true));
+        CUF(launch_col_pp(log2n, 16, CL_SLAB, C_ONE, c, nullptr, true));
+    }
+    CUF(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    const size_t fb = sizeof(double2) * p->field, ub = sizeof(double2) * (p->field + 2 * (size_t)n);
+    for (double2** buf : {&p->k2, &p->f, &p->T, &p->Tc, &p->x, &p->y}) {
+        CUF(cudaMalloc(buf, fb));
+        CUF(cudaMemsetAsync(*buf, 0, fb, p->stream));
+    }
+    for (double2** buf : {&p->u_alloc0, &p->u_alloc1}) {
+        CUF(cudaMalloc(buf, ub));
+        CUF(cudaMemsetAsync(*buf, 0, ub, p->stream));
+    }
+    p->u0 = p->u_alloc0 + n;
+    p->u1 = p->u_alloc1 + n;
+    CUF(cudaMalloc(&p->slab_sums, sizeof(double) * 4));
+    CUF(cudaMemsetAsync(p->slab_sums, 0, sizeof(double) * 4, p->stream));
+    CUF(cudaMalloc(&p->partial, sizeof(double) * (size_t)R * kPartStride));
+    CUF(cudaMalloc(&p->gamma, sizeof(double2)));
+    CUF(cudaMalloc(&p->norm_part, sizeof(double) * 64));
+    CUF(cudaMalloc(&p->fnorm_l2, sizeof(double)));
+    CUF(cudaMalloc(&p->fnorm_reta, sizeof(double)));
+    CUF(cudaMalloc(&p->ctl_int, sizeof(int) * 6));
+    CUF(cudaMemsetAsync(p->ctl_int, 0, sizeof(int) * 6, p->stream));
+    CUF(cudaMalloc(&p->counter, sizeof(unsigned)));
+    CUF(cudaMemsetAsync(p->counter, 0, sizeof(unsigned), p->stream));
+    CUF(cudaMallocHost(&p->host_active, sizeof(int)));
+    CUF(cudaMalloc(&p->dflag, sizeof(int)));
+    CUF(cudaMalloc(&p->k0sq, sizeof(double)));
+    CUF(cudaMalloc(&p->eta, sizeof(double)));
+    CUF(cudaMalloc(&p->tw, sizeof(double2) * n));
+    CUF(cudaMalloc(&p->sinp, sizeof(double) * n));
+    CUF(cudaMalloc(&p->lap, sizeof(double) * n));
+    std::vector<double> lap = lap_table(n, h), tw(2 * n), sinp(n);
+    for (int k = 0; k < n; ++k) {
+        tw[2 * k] = std::cos(2.0 * kPi * k / n);
+        tw[2 * k + 1] = -std::sin(2.0 * kPi * k / n);
+        sinp[k] = std::sin(kPi * k / n);
+    }
+    const double k0sq = k0 * k0;
+    CUF(cudaMemcpyAsync(p->k0sq, &k0sq, sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->eta, &eta, sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->sinp, sinp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->lap, lap.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
+    std::vector<double2> rows;
+    pack_slab_host(k2, n, p->row0, R, rows);
+    CUF(cudaMemcpyAsync(p->k2, rows.data(), fb, cudaMemcpyHostToDevice, p->stream));
+    bool ok = false;
+    if (int rc = all_finite(p, reinterpret_cast<const double*>(p->k2), 2 * p->field, &ok)) return fail(rc);
+    if (!ok) return fail(set_err(BP_EINVAL, "HelmholtzProblem: k2 not finite"));
+    if (int rc = ensure_trace(p, 1000)) return fail(rc);
+#undef CUF
+    *out = p;
+    return BP_OK;
+}
+
+int bp_slab_view(const bp_problem* p, bp_slab_view_t* v) {
+    if (int rc = check_problem(p)) return rc;
+    if (!p->slab_log2 || !v) return set_err(BP_EINVAL, "not a slab problem");
+    const int n = p->n, R = 1 << p->slab_log2;
+    v->rank = p->slab_rank;
+    v->nranks = p->slab_nranks;
+    v->rows = R;
+    v->row0 = p->row0;
+    v->n = n;
+    v->block_elems = (int64_t)R * R;
+    v->t_rows = p->T;
+    v->t_cols = p->Tc;
+    v->sums = p->slab_sums;
+    for (int k = 0; k < 2; ++k) {
+        double2* u = k ? p->u1 : p->u0;
+        v->u_first[k] = u;
+        v->u_last[k] = u + (size_t)(R - 1) * n;
+        v->u_halo_lo[k] = u - n;
+        v->u_halo_hi[k] = u + (size_t)R * n;
+    }
+    v->stream = p->stream;
+    return BP_OK;
+}
+
+int bp_slab_set_fields(bp_problem* p, const double* f, const double* u0) {
+    if (int rc = check_problem(p)) return rc;
+    if (!p->slab_log2 || !f) return set_err(BP_EINVAL, "slab: null field or not a slab problem");
+    DeviceGuard guard(p->device);
+    const int R = 1 << p->slab_log2;
+    const size_t fb = sizeof(double2) * p->field, ub = sizeof(double2) * (p->field + 2 * (size_t)p->n);
+    std::vector<double2> rows;
+    pack_slab_host(f, p->n, p->row0, R, rows);
+    CU(cudaMemcpyAsync(p->f, rows.data(), fb, cudaMemcpyHostToDevice, p->stream));
+    CU(cudaMemsetAsync(p->u_alloc0, 0, ub, p->stream));
+    if (u0) {
+        pack_slab_host(u0, p->n, p->row0, R, rows);
+        CU(cudaMemcpyAsync(p->u0, rows.data(), fb, cudaMemcpyHostToDevice, p->stream));
+    }
+    CU(cudaStreamSynchronize(p->stream));  // the staging vector goes out of scope
+    return BP_OK;
+}
+
+int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter_config* cfg,
+                  double a0, double a1) {
+    if (int rc = check_problem(p)) return rc;
+    if (!p->slab_log2) return set_err(BP_EINVAL, "not a slab problem");
+    DeviceGuard guard(p->device);
+    RowArgs a = slab_row_args(p);
+    a.ctl.max_iters = p->slab_max_iters;
+    a.ctl.rtol = p->slab_rtol;
+    switch (stage) {
+        case BP_SLAB_FWD_F:  // T <- y-DST of f; sums[0] = local ||f||^2
+            a.in = p->f;
+            CU(launch_row(p->log2n, 2, R_FWD, a, p->stream));
+            return norms(p, p->f, p->slab_sums, true);
+        case BP_SLAB_COL: {  // column pass on the rank's n x R block
+            ColArgs c = col_args(p);
+            c.T = p->Tc;
+            c.slab_cols = 1 << p->slab_log2;
+            c.col0 = p->slab_rank * c.slab_cols;
+            c.scale = p->green_scale;
+            c.status = p->slab_running ? a.ctl.status : nullptr;
+            CU(launch_col_pp(p->log2n, 16, CL_SLAB, C_GREEN, c, p->stream));
+            return BP_OK;
+        }
+        case BP_SLAB_INV_NORM:  // y <- inverse y-DST of T; sums[1] = local ||y||^2
+            a.out = p->y;
+            a.sub = nullptr;
+            CU(launch_row(p->log2n, 2, R_INV, a, p->stream));
+            return norms(p, p->y, p->slab_sums + 1, true);
+        case BP_SLAB_INIT: {  // a0 = ||f||, a1 = ||G f|| (global); cfg: rtol / max_iters
+            if (!cfg) return set_err(BP_EINVAL, "slab init: null config");
+            if (!(cfg->rtol > 0.0 && cfg->rtol < 1.0)) return set_err(BP_EINVAL, "run: rtol must lie in (0,1)");
+            if (cfg->max_iters < 1) return set_err(BP_EINVAL, "run: max_iters must be >= 1");
+            if (!(a0 > 0.0)) return set_err(BP_EINVAL, "run: zero source");
+            if (int rc = ensure_trace(p, cfg->max_iters)) return rc;
+            p->slab_max_iters = cfg->max_iters;
+            p->slab_rtol = cfg->rtol;
+            a = slab_row_args(p);
+            CU(cudaMemcpyAsync(p->fnorm_l2, &a0, sizeof(double), cudaMemcpyHostToDevice, p->stream));
+            CU(cudaMemcpyAsync(p->fnorm_reta, &a1, sizeof(double), cudaMemcpyHostToDevice, p->stream));
+            CU(cudaMemsetAsync(p->u_alloc1, 0, sizeof(double2) * (p->field + 2 * (size_t)p->n), p->stream));
+            init_control_kernel<<<1, 128, 0, p->stream>>>(a.ctl, 1);
+            fill_nan_kernel<<<grid_for((size_t)p->trace_cap), 256, 0, p->stream>>>(p->trace_l2, p->trace_cap);
+            fill_nan_kernel<<<grid_for((size_t)p->trace_cap), 256, 0, p->stream>>>(p->trace_reta, p->trace_cap);
+            CU(cudaGetLastError());
+            CU(cudaStreamSynchronize(p->stream));  // a0 / a1 are host stack values
+            p->slab_running = true;
+            return BP_OK;
+        }
+        case BP_SLAB_FWD_BORN:  // T <- y-DST of V u^0 + f
+            a.in = p->u0;
+            CU(launch_row(p->log2n, 2, R_FWD_BORN, a, p->stream));
+            return BP_OK;
+        case BP_SLAB_SWEEP:  // fused scalar / pointwise sweep; sums[0..1] = local entry sums
+            if (!map || (map->kind != BP_MAP_SCALAR && map->kind != BP_MAP_POINTWISE))
+                return set_err(BP_ENOTSUP, "slab decomposition: scalar and pointwise maps only");
+            a.map_kind = map->kind;
+            a.gamma = make_double2(map->gamma_re, map->gamma_im);
+            CU(launch_row(p->log2n, 2, R_SWEEP, a, p->stream));
+            return BP_OK;
+        case BP_SLAB_FINALIZE:  // sums hold the all-reduced entry sums
+            slab_finalize_kernel<<<1, 32, 0, p->stream>>>(a.ctl, p->slab_sums);
+            CU(cudaGetLastError());
+            return BP_OK;
+    }
+    return set_err(BP_EINVAL, "unknown slab stage");
+}
+
+int bp_slab_active(bp_problem* p, int32_t* n_active) {
+    if (int rc = check_problem(p)) return rc;
+    if (!n_active) return set_err(BP_EINVAL, "null output");
+    DeviceGuard guard(p->device);
+    Control c = make_control(p);
+    CU(cudaMemcpyAsync(p->host_active, c.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    *n_active = *p->host_active;
+    return BP_OK;
+}
+
+int bp_slab_result(bp_problem* p, double* u_dense, double* res_l2, double* res_reta, bp_trace* info) {
+    if (int rc = check_problem(p)) return rc;
+    if (!p->slab_log2 || !u_dense) return set_err(BP_EINVAL, "slab: null output or not a slab problem");
+    DeviceGuard guard(p->device);
+    Control c = make_control(p);
+    int rb = 0;
+    CU(cudaMemcpyAsync(&rb, c.result_buf, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    const int n = p->n, R = 1 << p->slab_log2, nd = n - 1;
+    std::vector<double2> rows((size_t)R * n);
+    CU(cudaMemcpyAsync(rows.data(), rb ? p->u1 : p->u0, sizeof(double2) * rows.size(), cudaMemcpyDeviceToHost,
+                       p->stream));
+    bp_iter_config cfg{BP_FMT_NPBS, p->slab_rtol, p->slab_max_iters};
+    bp_trace tr{};
+    if (int rc = finish_run_traces(p, &cfg, res_l2, res_reta, &tr)) return rc;
+    if (info) *info = tr;
+    for (int i = 0; i < R; ++i) {
+        const int x = p->row0 + i;
+        if (x < 1 || x > nd) continue;
+        double* dst = u_dense + 2 * (size_t)(x - 1) * nd;
+        for (int y = 1; y < n; ++y) {
+            dst[2 * (y - 1)] = rows[(size_t)i * n + y].x;
+            dst[2 * (y - 1) + 1] = rows[(size_t)i * n + y].y;
+        }
+    }
+    p->slab_running = false;
+    return BP_OK;
+}
+
+}  // extern "C"
+
+namespace {
 }  // namespace
 
 extern "C" {
@@ -1623,16 +1949,18 @@ int bp_problem_destroy(bp_problem* p) {
     DeviceGuard guard(p->device);
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->graph) cudaGraphExecDestroy(p->graph);
+    if (p->u_alloc0) p->u0 = p->u_alloc0;
+    if (p->u_alloc1) p->u1 = p->u_alloc1;
     for (void* q : {(void*)p->k2, (void*)p->f, (void*)p->u0, (void*)p->u1, (void*)p->T, (void*)p->x,
                     (void*)p->y, (void*)p->dense, (void*)p->partial, (void*)p->gamma, (void*)p->fd, (void*)p->norm_part,
                     (void*)p->fnorm_l2, (void*)p->fnorm_reta, (void*)p->ctl_int, (void*)p->counter,
                     (void*)p->trace_l2, (void*)p->trace_reta, (void*)p->k0sq, (void*)p->eta,
                     (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2, (void*)p->TT,
                     (void*)p->bx, (void*)p->by, (void*)p->sigma, (void*)p->sigma0, (void*)p->lapn,
-                    (void*)p->rnorm2, (void*)p->w4, (void*)p->dflag})
+                    (void*)p->rnorm2, (void*)p->w4, (void*)p->dflag, (void*)p->Tc, (void*)p->slab_sums})
         if (q) cudaFree(q);
     if (p->host_active) cudaFreeHost(p->host_active);
-    if (p->stream) cudaStreamDestroy(p->stream);
+    if (p->stream && p->own_stream) cudaStreamDestroy(p->stream);
     delete p;
     return BP_OK;
 }

@@ -102,6 +102,14 @@ struct RowArgs {
     int map_kind;
     double2 gamma;
     Control ctl;
+    // x-slab of a grid distributed over ranks (2-D, batch 1; 0 = whole members): the launch
+    // covers 2^slab_log2 rows starting at global row row0; u / k2 / f hold those rows (u with
+    // one halo row on each side), T is blocked [dest rank][row][col within the dest's block]
+    // for the all-to-all, and ENTRY modes write their per-slab sums to slab_sums instead of
+    // finalising (the driver all-reduces them and launches finalize_kernel)
+    int slab_log2;
+    int row0;
+    double* slab_sums;
 };
 
 struct ColArgs {
@@ -117,6 +125,8 @@ struct ColArgs {
     const double* sinp;
     const int* status;         // nullable: skip inactive members
     int planes_per_member;     // CL_PLANE: 1 (2-D) or n (3-D y-lines)
+    int slab_cols;             // CL_SLAB: columns held by this rank (n x slab_cols block, row stride slab_cols)
+    int col0;                  // CL_SLAB: global index of the first of them
 };
 
 // ------------------------------------------------------------------ helpers
@@ -232,9 +242,11 @@ row_kernel(const RowArgs a) {
     const int t = threadIdx.x % T;
     const int e = threadIdx.x / T;
     const long grow = (long)blockIdx.x * EPB + e;
-    const int b = (int)(grow >> LLINES);
-    const int i = (int)(grow & ((1L << LLINES) - 1));   // line index within the member
-    bool valid = (b < a.batch) && (i & (N - 1)) != 0 && (DIM == 2 || (i >> LOG2N) != 0);
+    const int lsh = (DIM == 2 && a.slab_log2) ? a.slab_log2 : LLINES;  // log2(lines per member)
+    const int b = (int)(grow >> lsh);
+    const int i = (int)(grow & ((1L << lsh) - 1));      // line index within the member (slab)
+    const int ig = (DIM == 2 && a.slab_log2) ? a.row0 + i : i;  // global line index
+    bool valid = (b < a.batch) && (ig & (N - 1)) != 0 && (DIM == 2 || (i >> LOG2N) != 0);
     int m = 0;  // trace entry this launch belongs to
     if (S::ITER && valid) {
         valid = __ldcg(&a.ctl.status[b]) == ST_ACTIVE;
@@ -244,8 +256,14 @@ row_kernel(const RowArgs a) {
 
     double2* buf = smem + e * G::PAD_N;
     const Pol pol = make_policy((Pol*)nullptr, smem + EPB * G::PAD_N, e);
-    const size_t mem = (size_t)(valid ? b : 0) << (DIM * LOG2N);
+    const size_t mem = (size_t)(valid ? b : 0) << (lsh + LOG2N);
     const size_t row = mem + (size_t)(valid ? i : 0) * N;
+    // T element (this line, column j): row-major, or blocked by destination rank on a slab
+    const int sl = DIM == 2 ? a.slab_log2 : 0;
+    auto tix = [&](int j) -> size_t {
+        if (sl == 0) return row + j;
+        return mem + ((size_t)(j >> sl) << (2 * sl)) + ((size_t)(valid ? i : 0) << sl) + (j & ((1 << sl) - 1));
+    };
     const double2 zero = make_double2(0.0, 0.0);
     const double2* ucur = (m & 1) ? a.u1 : a.u0;  // u^m
     double2* unext = (m & 1) ? a.u0 : a.u1;       // u^{m+1}
@@ -283,8 +301,8 @@ row_kernel(const RowArgs a) {
 #pragma unroll
         for (int mm = 0; mm < P; ++mm) {
             const int j = t + T * mm;
-            x[mm] = valid ? a.T[row + j] : zero;
-            xm[mm] = (valid && j != 0) ? a.T[row + (N - j)] : zero;  // mirror: L1 hit
+            x[mm] = valid ? a.T[tix(j)] : zero;
+            xm[mm] = (valid && j != 0) ? a.T[tix(N - j)] : zero;  // mirror: L1 hit
         }
         Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
@@ -440,7 +458,7 @@ row_kernel(const RowArgs a) {
 #pragma unroll
             for (int mm = 0; mm < P; ++mm) {
                 const int j = t + T * mm;
-                if (valid) a.T[row + j] = buf[G::pidx(j)];
+                if (valid) a.T[tix(j)] = buf[G::pidx(j)];
             }
         }
     }
@@ -451,12 +469,13 @@ row_kernel(const RowArgs a) {
         for (int k = 0; k < S::NPART; ++k) acc[k] = pol.sum(acc[k], t);
         int last = 0;
         if (valid && t == 0) {
-            double* pr = a.ctl.partial + (((size_t)b << LLINES) + i) * kPartStride;
+            double* pr = a.ctl.partial + (((size_t)b << lsh) + i) * kPartStride;
 #pragma unroll
             for (int k = 0; k < S::NPART; ++k) pr[k] = acc[k];
             __threadfence();
             const unsigned old = atomicAdd(&a.ctl.counter[b], 1u);
-            last = (old == VALID_LINES - 1u);
+            const unsigned nvalid = sl ? (1u << sl) - (a.row0 == 0 ? 1u : 0u) : VALID_LINES;
+            last = (old == nvalid - 1u);
         }
         last = pol.bcast0(last, t);
         if (last) {
@@ -464,9 +483,10 @@ row_kernel(const RowArgs a) {
             double s[S::NPART];
 #pragma unroll
             for (int k = 0; k < S::NPART; ++k) s[k] = 0.0;
-            for (int r = t; r < (1 << LLINES); r += T) {
-                if ((r & (N - 1)) == 0 || (DIM == 3 && (r >> LOG2N) == 0)) continue;  // padding lines
-                const double* pr = a.ctl.partial + (((size_t)b << LLINES) + r) * kPartStride;
+            for (int r = t; r < (1 << lsh); r += T) {
+                const int rg = sl ? a.row0 + r : r;
+                if ((rg & (N - 1)) == 0 || (DIM == 3 && (r >> LOG2N) == 0)) continue;  // padding lines
+                const double* pr = a.ctl.partial + (((size_t)b << lsh) + r) * kPartStride;
 #pragma unroll
                 for (int k = 0; k < S::NPART; ++k) s[k] += __ldcg(pr + k);
             }
@@ -476,7 +496,14 @@ row_kernel(const RowArgs a) {
                 a.ctl.counter[b] = 0u;
                 if constexpr (MODE == R_OPT_A) finalize_gamma(a.ctl, b, s[2], s[3], s[4]);
                 if constexpr (MODE == R_RETA_C) finalize_gamma(a.ctl, b, s[0], s[1], s[2]);
-                if constexpr (S::ENTRY) finalize_entry(a.ctl, b, m, s[0], s[1]);
+                if constexpr (S::ENTRY) {
+                    if (sl) {  // slab: partial sums of this rank, finalised after the all-reduce
+                        a.slab_sums[2 * b] = s[0];
+                        a.slab_sums[2 * b + 1] = s[1];
+                    } else {
+                        finalize_entry(a.ctl, b, m, s[0], s[1]);
+                    }
+                }
             }
         }
     }
@@ -572,7 +599,9 @@ struct ColGeom {
 
 // LAYOUT 0: lines along the slow axis of n x n planes (2-D x-lines; 3-D y-lines of every
 //           x-plane, planes_per_member = n).  LAYOUT 2: 3-D x-lines (stride n^2).
-enum ColLayout { CL_PLANE = 0, CL_X3 = 2 };
+//           CL_SLAB: 2-D x-lines of the n x slab_cols column block a rank holds after the
+//           all-to-all of a slab-decomposed grid (row stride slab_cols, global column col0 + q).
+enum ColLayout { CL_PLANE = 0, CL_X3 = 2, CL_SLAB = 3 };
 
 template <int LOG2N, int MODE, int C, int PP, int LAYOUT = CL_PLANE>
 __global__ void __launch_bounds__(C * Geom<LOG2N, PP>::T, (MinBlocks<C * Geom<LOG2N, PP>::T, PP >= 16 ? 128 : 64>::value))
@@ -585,10 +614,16 @@ col_kernel(const ColArgs a) {
     col_thread_map<G::T, C>(t, c);
     constexpr int GROUPS = N / C;
     // line group -> member b, base offset `mem`, line stride LS, and (3-D x-lines) the y index
-    int b, yl = 0;
+    int b, yl = 0, qa;
     size_t mem;
-    constexpr size_t LS = LAYOUT == CL_X3 ? (size_t)N * N : (size_t)N;
-    if constexpr (LAYOUT == CL_X3) {
+    size_t LS = LAYOUT == CL_X3 ? (size_t)N * N : (size_t)N;
+    if constexpr (LAYOUT == CL_SLAB) {
+        const int groups = a.slab_cols / C;
+        b = blockIdx.x / groups;
+        qa = (blockIdx.x % groups) * C + c;  // column within the block (address)
+        LS = (size_t)a.slab_cols;
+        mem = (size_t)b * N * a.slab_cols;
+    } else if constexpr (LAYOUT == CL_X3) {
         const int grp = blockIdx.x / GROUPS;  // (member, y)
         b = grp >> LOG2N;
         yl = grp & (N - 1);
@@ -600,7 +635,13 @@ col_kernel(const ColArgs a) {
         if (a.planes_per_member > 1 && (plane & (N - 1)) == 0) return;  // padding x-plane (3-D)
         mem = (size_t)plane * N * N;
     }
-    const int q = (blockIdx.x % GROUPS) * C + c;
+    int q;  // global column index (symbol, Dirichlet zero column)
+    if constexpr (LAYOUT == CL_SLAB) {
+        q = a.col0 + qa;
+    } else {
+        q = (blockIdx.x % GROUPS) * C + c;
+        qa = q;
+    }
     if (a.status && __ldcg(&a.status[b]) != ST_ACTIVE) return;  // uniform per CTA
 
     double2* buf = smem + c * G::PAD_N;
@@ -611,14 +652,14 @@ col_kernel(const ColArgs a) {
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
-        x[mm] = a.T[mem + (size_t)j * LS + q];
-        xm[mm] = (j == 0) ? zero : a.T[mem + (size_t)(N - j) * LS + q];
+        x[mm] = a.T[mem + (size_t)j * LS + qa];
+        xm[mm] = (j == 0) ? zero : a.T[mem + (size_t)(N - j) * LS + qa];
     }
     Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
 
     if constexpr (MODE == C_ONE) {
 #pragma unroll
-        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + q] = cscale(y[l], a.scale);
+        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + qa] = cscale(y[l], a.scale);
     } else {
         const double k0sq = a.k0sq[b], eta = a.eta[b];
         // transverse symbol part: a_q (2-D) or a_y + a_z (3-D x-lines)
@@ -653,7 +694,7 @@ col_kernel(const ColArgs a) {
         pol.sync();
         Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
-        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + q] = y[l];
+        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + qa] = y[l];
     }
 }
 

@@ -21,7 +21,7 @@ cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
     using RG = RowGeom<L, PP, kRowWarps>;
     auto k = row_kernel<L, MODE, kRowWarps, PP, DIM, TOUT>;
     if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
-    const long rows = (long)a.batch << ((DIM - 1) * L);
+    const long rows = (long)a.batch << ((DIM == 2 && a.slab_log2) ? a.slab_log2 : (DIM - 1) * L);
     const int grid = (int)((rows + RG::EPB - 1) / RG::EPB);
     k<<<grid, kRowWarps * 32, RG::SMEM, s>>>(a);
     return cudaGetLastError();
@@ -35,8 +35,11 @@ cudaError_t launch_col_t(const ColArgs& a, cudaStream_t s, bool prepare) {
     if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
     // CL_PLANE: one CTA per (plane, column group), planes = batch * planes_per_member;
     // CL_X3: one CTA per (member, y, column group)
+    // CL_SLAB: one CTA per (member, column group of the rank's block)
     const long groups = (long)a.batch * (LAYOUT == CL_X3 ? (1L << L) : a.planes_per_member);
-    const int grid = (int)(groups * ((1 << L) / C));
+    const int grid = LAYOUT == CL_SLAB ? (int)((long)a.batch * (a.slab_cols / C))
+                                       : (int)(groups * ((1 << L) / C));
+    if (LAYOUT == CL_SLAB && (a.slab_cols % C) != 0) return cudaErrorInvalidValue;
     k<<<grid, CG::THREADS, CG::SMEM, s>>>(a);
     return cudaGetLastError();
 }
@@ -202,6 +205,11 @@ struct Pp8 {
                                 bool prep) {                                                    \
         if (layout == CL_X3) {                                                                  \
             if constexpr (L <= kMaxLog2_3d) return launch_col_p<L, 16, CL_X3>(mode, a, s, prep); \
+            return cudaErrorInvalidValue;                                                       \
+        }                                                                                       \
+        if (layout == CL_SLAB) {                                                                \
+            if (mode == C_ONE) return launch_col_t<L, C_ONE, 16, CL_SLAB>(a, s, prep);          \
+            if (mode == C_GREEN) return launch_col_t<L, C_GREEN, 16, CL_SLAB>(a, s, prep);      \
             return cudaErrorInvalidValue;                                                       \
         }                                                                                       \
         if (pp == 8) return launch_col_p<L, Pp8<L>::value>(mode, a, s, prep);                   \

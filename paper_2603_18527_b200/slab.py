@@ -1,0 +1,238 @@
+"""Slab decomposition of ONE 2-D Dirichlet grid over several GPUs (config c2).
+
+Rank r owns the padded rows [r R, (r+1) R) of the n x n grid, R = n / nranks.  A sweep needs
+the y-DSTs (rows: local), the x-DSTs (columns: every rank's rows) and the five-point stencil
+(one halo row from each neighbour), so the driver below runs, per sweep m:
+
+    halo exchange of u^m's edge rows                         (point-to-point, 2 rows)
+    BP_SLAB_SWEEP     inverse y-DST, entry sums, update, next source, forward y-DST
+    all-reduce of the two entry sums                          (2 doubles)
+    BP_SLAB_FINALIZE  trace entry m + termination test (identical on every rank)
+    all-to-all        t_rows [dest][R][R] -> t_cols [src][R][R] = the n x R column block
+    BP_SLAB_COL       x-DST, x Green weights, inverse x-DST
+    all-to-all        back
+
+which is bp::run (proj/src/iterate.cpp:88-153) with the transposes of the distributed
+transform.  The driver is written against two small interfaces so the same host logic runs
+
+  * on GPUs: `SlabPart` (the C-ABI slab handle, include/bornsweep.h bp_slab_*) with
+    `DistComm` (torch.distributed, NCCL) -- one part per process, or with `LocalComm` -- several
+    parts in one process exchanging by device copies (how the GPU tests exercise nranks > 1 on
+    one device without ranks waiting on each other);
+  * on CPUs in the tests: a numpy stand-in part with `DistComm` over gloo (world size 2).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .api import BC_DIRICHLET, TERMINATION, IterationConfig, IterationTrace, ScalarMap, _check, _ptr
+
+FWD_F, COL, INV_NORM, INIT, FWD_BORN, SWEEP, FINALIZE = range(7)
+POLL_SWEEPS = 16
+
+
+class _DevPtr:
+    """__cuda_array_interface__ over a device pointer (zero-copy torch.as_tensor)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _dev_tensor(ptr, shape, typestr, device):
+    import torch
+    return torch.as_tensor(_DevPtr(ptr, shape, typestr), device=f"cuda:{device}")
+
+
+class SlabPart:
+    """One rank's x-slab on a GPU (bp_slab_create).  k2: the FULL dense (nx, ny) medium."""
+
+    def __init__(self, k2, k0: float, eta: float, rank: int, nranks: int, lx: float = 1.0,
+                 device: int = 0):
+        import torch
+        k2 = np.ascontiguousarray(np.asarray(k2, np.complex128))
+        self.nx, self.ny = k2.shape
+        self.rank, self.nranks, self.device = rank, nranks, device
+        self._lib = N.lib()
+        h = C.c_void_p()
+        g = N.Grid(self.nx, self.ny, lx, lx, BC_DIRICHLET)
+        _check(self._lib.bp_slab_create(C.byref(g), rank, nranks, _ptr(k2), float(k0), float(eta),
+                                        device, C.byref(h)))
+        self._h = h
+        # launch on the framework's current stream: the collectives are ordered with the kernels
+        stream = torch.cuda.current_stream(device).cuda_stream
+        _check(self._lib.bp_problem_set_stream(self._h, C.c_void_p(stream)))
+        v = N.SlabView()
+        _check(self._lib.bp_slab_view(self._h, C.byref(v)))
+        self.rows, self.row0, self.n = v.rows, v.row0, v.n
+        R, n, d = v.rows, v.n, device
+        self.t_rows = _dev_tensor(v.t_rows, (nranks, R, R), "<c16", d)
+        self.t_cols = _dev_tensor(v.t_cols, (nranks, R, R), "<c16", d)
+        self.sums = _dev_tensor(v.sums, (4,), "<f8", d)
+        self.u_first = [_dev_tensor(v.u_first[k], (n,), "<c16", d) for k in range(2)]
+        self.u_last = [_dev_tensor(v.u_last[k], (n,), "<c16", d) for k in range(2)]
+        self.u_halo_lo = [_dev_tensor(v.u_halo_lo[k], (n,), "<c16", d) for k in range(2)]
+        self.u_halo_hi = [_dev_tensor(v.u_halo_hi[k], (n,), "<c16", d) for k in range(2)]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.bp_problem_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def set_fields(self, f, u0=None):
+        f = np.ascontiguousarray(np.asarray(f, np.complex128))
+        u0 = None if u0 is None else np.ascontiguousarray(np.asarray(u0, np.complex128))
+        _check(self._lib.bp_slab_set_fields(self._h, _ptr(f), _ptr(u0)))
+
+    def stage(self, code: int, cmap=None, config: IterationConfig | None = None, a0=0.0, a1=0.0):
+        mp = cmap._c() if cmap is not None else None
+        cfg = config._c() if config is not None else None
+        _check(self._lib.bp_slab_stage(self._h, code, C.byref(mp) if mp is not None else None,
+                                       C.byref(cfg) if cfg is not None else None, float(a0), float(a1)))
+
+    def host_sums(self) -> np.ndarray:
+        return self.sums.cpu().numpy().copy()
+
+    def active(self) -> int:
+        n = C.c_int32()
+        _check(self._lib.bp_slab_active(self._h, C.byref(n)))
+        return n.value
+
+    def result(self, u_dense: np.ndarray, max_iters: int) -> IterationTrace:
+        l2 = np.empty(max_iters + 1)
+        rt = np.empty(max_iters + 1)
+        info = N.Trace()
+        _check(self._lib.bp_slab_result(self._h, _ptr(u_dense), _ptr(l2), _ptr(rt), C.byref(info)))
+        k = info.iters + 1
+        return IterationTrace(l2[:k].copy(), rt[:k].copy(), info.iters, TERMINATION[info.terminated],
+                              info.fnorm_l2, info.fnorm_reta)
+
+
+# ---------------------------------------------------------------------------- exchanges
+class LocalComm:
+    """Every part in this process (rank order): exchanges are tensor copies on one stream."""
+
+    def transpose(self, parts, forward: bool):
+        P = len(parts)
+        for d in range(P):
+            for s in range(P):
+                if forward:
+                    parts[d].t_cols[s].copy_(parts[s].t_rows[d])
+                else:
+                    parts[s].t_rows[d].copy_(parts[d].t_cols[s])
+
+    def allreduce(self, parts, k: int = 2):
+        total = parts[0].sums[:k].clone()
+        for p in parts[1:]:
+            total += p.sums[:k]
+        for p in parts:
+            p.sums[:k].copy_(total)
+
+    def halo(self, parts, buf: int):
+        for r, p in enumerate(parts):
+            if r > 0:
+                p.u_halo_lo[buf].copy_(parts[r - 1].u_last[buf])
+            if r + 1 < len(parts):
+                p.u_halo_hi[buf].copy_(parts[r + 1].u_first[buf])
+
+
+class DistComm:
+    """One part per process; torch.distributed collectives (NCCL on GPUs, gloo on CPUs)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    @staticmethod
+    def _real(t):
+        import torch
+        return torch.view_as_real(t).reshape(-1)
+
+    def transpose(self, parts, forward: bool):
+        (p,) = parts
+        src, dst = (p.t_rows, p.t_cols) if forward else (p.t_cols, p.t_rows)
+        self.dist.all_to_all_single(self._real(dst), self._real(src), group=self.group)
+
+    def allreduce(self, parts, k: int = 2):
+        (p,) = parts
+        buf = p.sums[:k].clone()
+        self.dist.all_reduce(buf, group=self.group)
+        p.sums[:k].copy_(buf)
+
+    def halo(self, parts, buf: int):
+        (p,) = parts
+        ops = []
+        dist, r, W = self.dist, self.rank, self.world
+        if r > 0:
+            ops.append(dist.P2POp(dist.isend, self._real(p.u_first[buf]), r - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, self._real(p.u_halo_lo[buf]), r - 1, self.group))
+        if r + 1 < W:
+            ops.append(dist.P2POp(dist.isend, self._real(p.u_last[buf]), r + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, self._real(p.u_halo_hi[buf]), r + 1, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+
+# ---------------------------------------------------------------------------- driver
+@dataclass
+class SlabResult:
+    u: np.ndarray            # dense (nx, ny): the rows of the local parts filled
+    trace: IterationTrace
+    sweeps_launched: int
+
+
+def run_slab(parts, comm, cmap, f, config: IterationConfig | None = None, u0=None) -> SlabResult:
+    """bp::run (iterate.cpp:88-153) on a slab-decomposed grid; every rank gets the same trace."""
+    config = config or IterationConfig()
+    cmap = cmap if cmap is not None else ScalarMap(1.0)
+
+    def col_pass():
+        comm.transpose(parts, True)
+        for p in parts:
+            p.stage(COL)
+        comm.transpose(parts, False)
+
+    for p in parts:
+        p.set_fields(f, u0)
+    # ||f|| and ||G f|| (iterate.cpp:93,102) through the distributed transform
+    for p in parts:
+        p.stage(FWD_F)
+    col_pass()
+    for p in parts:
+        p.stage(INV_NORM)
+    comm.allreduce(parts)
+    s = parts[0].host_sums()
+    fn, gn = math.sqrt(max(s[0], 0.0)), math.sqrt(max(s[1], 0.0))
+    for p in parts:
+        p.stage(INIT, config=config, a0=fn, a1=gn)
+        p.stage(FWD_BORN)
+    col_pass()
+    launched = 0
+    for k in range(config.max_iters + 1):
+        comm.halo(parts, k & 1)
+        for p in parts:
+            p.stage(SWEEP, cmap=cmap)
+        comm.allreduce(parts)
+        for p in parts:
+            p.stage(FINALIZE)
+        col_pass()
+        launched += 1
+        if (k + 1) % POLL_SWEEPS == 0 or k == config.max_iters:
+            if parts[0].active() == 0:
+                break
+    u = np.zeros((parts[0].nx, parts[0].ny), np.complex128)
+    trace = None
+    for p in parts:
+        trace = p.result(u, config.max_iters)
+    return SlabResult(u, trace, launched)

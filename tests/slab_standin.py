@@ -1,0 +1,172 @@
+"""CPU stand-in for one rank's slab part (the interface of paper_2603_18527_b200.slab.SlabPart)
+so the slab driver's host logic -- partition, blocked all-to-all layout, halo exchange,
+all-reduced sums, identical termination on every rank -- runs under gloo on CPUs.
+
+Same stage semantics as the CUDA slab stages (include/bornsweep.h BP_SLAB_*), computed with
+scipy's DST-I (== FFTW RODFT00): forward = plain sine sum (transforms.cpp:117), Green weights
+4/(n^2 lambda) (symbol.cpp:69-80, transforms.cpp:99), termination restating iterate.cpp:134-150.
+Test infrastructure only."""
+import math
+
+import numpy as np
+import scipy.fft as sf
+import torch
+
+from paper_2603_18527_b200.api import TERMINATION, IterationTrace
+from paper_2603_18527_b200.slab import COL, FINALIZE, FWD_BORN, FWD_F, INIT, INV_NORM, SWEEP
+
+
+def _sine(a):
+    """plain sine sum over the interior (index 1..n-1) along the last axis of padded rows"""
+    out = np.zeros_like(a)
+    out[..., 1:] = 0.5 * sf.dst(a[..., 1:], type=1, axis=-1)
+    return out
+
+
+class NumpySlabPart:
+    def __init__(self, k2, k0, eta, rank, nranks, lx=1.0):
+        k2 = np.asarray(k2, np.complex128)
+        self.nx, self.ny = k2.shape
+        n = self.nx + 1
+        R = n // nranks
+        self.n, self.rows, self.rank, self.nranks, self.row0 = n, R, rank, nranks, rank * R
+        self.h = lx / n
+        self.k0sq, self.eta = k0 * k0, eta
+        self.k2 = self._pack(k2)
+        self.V = self.k2 - (self.k0sq + 1j * eta)
+        j = np.arange(n)
+        self.lap = 4.0 / self.h ** 2 * np.sin(j * np.pi / (2 * n)) ** 2
+        self._T = np.zeros((nranks, R, R), np.complex128)
+        self._Tc = np.zeros((nranks, R, R), np.complex128)
+        self._sums = np.zeros(4)
+        self._u = [np.zeros((R + 2, n), np.complex128) for _ in range(2)]
+        self.t_rows, self.t_cols = torch.from_numpy(self._T), torch.from_numpy(self._Tc)
+        self.sums = torch.from_numpy(self._sums)
+        self.u_first = [torch.from_numpy(u[1]) for u in self._u]
+        self.u_last = [torch.from_numpy(u[R]) for u in self._u]
+        self.u_halo_lo = [torch.from_numpy(u[0]) for u in self._u]
+        self.u_halo_hi = [torch.from_numpy(u[R + 1]) for u in self._u]
+        self.f = np.zeros((R, n), np.complex128)
+        self.y = np.zeros((R, n), np.complex128)
+        self.valid = (self.row0 + np.arange(R)) % n != 0
+
+    def _pack(self, dense):
+        out = np.zeros((self.rows, self.n), np.complex128)
+        for i in range(self.rows):
+            x = self.row0 + i
+            if 1 <= x <= self.nx:
+                out[i, 1:] = dense[x - 1]
+        return out
+
+    # blocked [dest][row][col in block] <-> rows x n
+    def _block(self, rows):
+        R, P = self.rows, self.nranks
+        self._T[...] = rows.reshape(R, P, R).transpose(1, 0, 2)
+
+    def _unblock(self):
+        R, P = self.rows, self.nranks
+        return self._T.transpose(1, 0, 2).reshape(R, P * R).copy()
+
+    def set_fields(self, f, u0=None):
+        self.f = self._pack(np.asarray(f, np.complex128))
+        self._u[0][...] = 0
+        if u0 is not None:
+            self._u[0][1:self.rows + 1] = self._pack(np.asarray(u0, np.complex128))
+
+    def host_sums(self):
+        return self._sums.copy()
+
+    def _finalize(self, s0, s1):
+        m = self.sweep
+        rel, rel_reta = math.sqrt(s0) / self.fn, math.sqrt(s1) / self.gn
+        self.l2[m], self.rt[m] = rel, rel_reta
+        term = -1
+        if m == 0:
+            if rel <= self.rtol:
+                term = 0
+        else:
+            if not math.isfinite(rel) or rel > 1e8:
+                term = 2
+            elif rel <= self.rtol:
+                term = 0
+            elif m + 1 > 20:
+                past = self.l2[m - 20]
+                if abs(past - rel) < 1e-14 * max(1.0, past):
+                    term = 3
+        if term < 0 and m >= self.max_iters:
+            term = 1
+        if term >= 0:
+            self.iters, self.term, self.result_buf, self.status = m, term, m & 1, 1
+        self.sweep = m + 1
+
+    def stage(self, code, cmap=None, config=None, a0=0.0, a1=0.0):
+        R, n = self.rows, self.n
+        if code == FWD_F:
+            self._block(_sine(self.f))
+            self._sums[0] = np.sum(np.abs(self.f) ** 2)
+        elif code == COL:
+            if getattr(self, "status", 0) != 0:
+                return
+            M = self._Tc.reshape(n, R)
+            q = self.rank * R + np.arange(R)
+            X = _sine(M.T)  # x-DST of every column
+            lam = self.lap[None, :] + self.lap[q][:, None] - (self.k0sq + 1j * self.eta)
+            w = 4.0 / (n * n) / lam
+            w[:, 0] = 0
+            w[q == 0, :] = 0
+            M[...] = _sine(X * w).T
+        elif code == INV_NORM:
+            self.y = _sine(self._unblock()) * self.valid[:, None]
+            self._sums[1] = np.sum(np.abs(self.y) ** 2)
+        elif code == INIT:
+            if not a0 > 0:
+                raise ValueError("run: zero source")
+            self.fn, self.gn = a0, a1
+            self.rtol, self.max_iters = config.rtol, config.max_iters
+            self.l2 = np.full(config.max_iters + 1, np.nan)
+            self.rt = np.full(config.max_iters + 1, np.nan)
+            self.status, self.sweep = 0, 0
+            self._u[1][...] = 0
+        elif code == FWD_BORN:
+            u = self._u[0][1:R + 1]
+            self._block(_sine(self.V * u + self.f))
+        elif code == SWEEP:
+            if self.status != 0:
+                return
+            m = self.sweep
+            ua = self._u[m & 1]
+            u = ua[1:R + 1]
+            z = _sine(self._unblock())
+            un, us = ua[0:R], ua[2:R + 2]
+            uw = np.zeros_like(u)
+            uw[:, 1:] = u[:, :-1]
+            ue = np.zeros_like(u)
+            ue[:, :-1] = u[:, 1:]
+            s = 4.0 * u - un - us - uw - ue
+            r = self.f - (s / self.h ** 2 - self.k2 * u)
+            x = z - u
+            mask = self.valid[:, None] & (np.arange(n) != 0)[None, :]
+            self._sums[0] = np.sum((np.abs(r) ** 2)[mask])
+            self._sums[1] = np.sum((np.abs(x) ** 2)[mask])
+            g = 1j / self.eta * self.V if cmap.__class__.__name__ == "PointwiseMap" else complex(cmap.gamma)
+            unew = u + g * x
+            unew[:, 0] = 0
+            nxt = self._u[(m + 1) & 1][1:R + 1]
+            nxt[self.valid] = unew[self.valid]
+            self._block(_sine(self.V * nxt + self.f))
+        elif code == FINALIZE:
+            if self.status == 0:
+                self._finalize(self._sums[0], self._sums[1])
+
+    def active(self):
+        return 1 if self.status == 0 else 0
+
+    def result(self, u_dense, max_iters):
+        rows = self._u[self.result_buf][1:self.rows + 1]
+        for i in range(self.rows):
+            x = self.row0 + i
+            if 1 <= x <= self.nx:
+                u_dense[x - 1] = rows[i, 1:]
+        k = self.iters + 1
+        return IterationTrace(self.l2[:k].copy(), self.rt[:k].copy(), self.iters, TERMINATION[self.term],
+                              self.fn, self.gn)

@@ -1,0 +1,86 @@
+"""Slab-decomposed grids on the GPU (bp_slab_* kernels: blocked row-side T, CL_SLAB column
+pass, halo rows, per-slab sums finalised after the reduction).  nranks parts live in ONE
+process on one device and exchange through device copies (LocalComm) -- the same driver and
+the same kernels a multi-GPU run uses with NCCL (DistComm), without ranks waiting on each
+other on a shared GPU."""
+import numpy as np
+import pytest
+
+import paper_2603_18527_b200 as bs
+from oracle import MAP_POINTWISE, MAP_SCALAR, OracleProblem
+from paper_2603_18527_b200.slab import LocalComm, SlabPart, run_slab
+
+pytestmark = pytest.mark.gpu
+FIELD_TOL = 1e-10
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def instance(n, seed=3, **kw):
+    spec = bs.InstanceSpec(n=n, ppw=10.0, contrast=0.3, sigma_cells=3.0, seed=seed, **kw)
+    k2, f, k0, eta = bs.make_instances(spec, 0, 1)
+    return k2[0], f[0], float(k0[0]), float(eta[0])
+
+
+def parts_for(k2, k0, eta, nranks):
+    return [SlabPart(k2, k0, eta, r, nranks) for r in range(nranks)]
+
+
+@pytest.mark.parametrize("n,nranks", [(64, 1), (64, 2), (64, 8), (256, 4), (512, 2)])
+@pytest.mark.parametrize("cmap", [bs.ScalarMap(1.0), bs.PointwiseMap()], ids=["scalar", "pointwise"])
+def test_slab_run_matches_oracle(gpu, n, nranks, cmap):
+    k2, f, k0, eta = instance(n)
+    cfg = bs.IterationConfig(rtol=1e-7, max_iters=4000)
+    parts = parts_for(k2, k0, eta, nranks)
+    res = run_slab(parts, LocalComm(), cmap, f, cfg)
+    p = OracleProblem(k2, k0, eta)
+    kind = MAP_POINTWISE if isinstance(cmap, bs.PointwiseMap) else MAP_SCALAR
+    ref = p.run(f, map_kind=kind, gamma=getattr(cmap, "gamma", 1.0), rtol=1e-7, max_iters=4000)
+    assert res.trace.terminated == ref.terminated
+    assert abs(res.trace.iters - ref.iters) <= 1
+    assert rel(res.u, ref.u) < FIELD_TOL
+    k = min(res.trace.iters, ref.iters) + 1
+    np.testing.assert_allclose(res.trace.res_l2_rel[:k], ref.res_l2[:k], rtol=1e-9, atol=1e-13)
+    np.testing.assert_allclose(res.trace.res_reta_rel[:k], ref.res_reta[:k], rtol=1e-9, atol=1e-13)
+
+
+def test_slab_matches_single_gpu_path(gpu):
+    """Same grid through the single-GPU handle and through 4 slabs: same trajectory."""
+    k2, f, k0, eta = instance(256, seed=7)
+    cfg = bs.IterationConfig(rtol=1e-6, max_iters=60)
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        one = bs.run(p, bs.PointwiseMap(), f, cfg)
+    res = run_slab(parts_for(k2, k0, eta, 4), LocalComm(), bs.PointwiseMap(), f, cfg)
+    assert res.trace.iters == one.trace.iters
+    assert rel(res.u, one.u) < 1e-12
+    np.testing.assert_allclose(res.trace.res_l2_rel, one.trace.res_l2_rel, rtol=1e-11)
+
+
+def test_slab_config2_grid_first_sweeps(gpu):
+    """c2's 4095^2 grid in 2 and 4 slabs, 12 sweeps: equal to the single-GPU path."""
+    cfgd = bs.CONFIGS["c2"]
+    k2, f, k0, eta = bs.config_instances("c2", 0, 1)
+    cfg = bs.IterationConfig(rtol=1e-6, max_iters=12)
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        one = bs.run(p, bs.PointwiseMap() if cfgd["map"] == "pointwise" else bs.ScalarMap(1.0), f, cfg)
+    cmap = bs.PointwiseMap() if cfgd["map"] == "pointwise" else bs.ScalarMap(1.0)
+    for nranks in (2, 4):
+        res = run_slab(parts_for(k2[0], float(k0[0]), float(eta[0]), nranks), LocalComm(), cmap, f[0], cfg)
+        assert res.trace.iters == one.trace.iters == 12
+        assert rel(res.u, one.u[0]) < 1e-12
+        np.testing.assert_allclose(res.trace.res_l2_rel, one.trace.res_l2_rel, rtol=1e-11)
+
+
+def test_slab_errors(gpu):
+    k2, f, k0, eta = instance(64)
+    with pytest.raises(NotImplementedError):
+        SlabPart(k2, k0, eta, 0, 16)  # 4 rows per rank
+    with pytest.raises(ValueError):
+        SlabPart(k2, k0, eta, 0, 3)
+    parts = parts_for(k2, k0, eta, 2)
+    with pytest.raises(ValueError, match="zero source"):
+        run_slab(parts, LocalComm(), bs.ScalarMap(1.0), np.zeros_like(f))
+    with pytest.raises(NotImplementedError):
+        run_slab(parts, LocalComm(), bs.OptimalScalarMap(), f)

@@ -1,0 +1,118 @@
+"""Slab decomposition host logic (paper_2603_18527_b200/slab.py) on CPUs: the driver with the
+numpy stand-in part (tests/slab_standin.py) -- in one process (LocalComm, 1/2/4 parts) and as
+two gloo ranks (DistComm) -- against the single-grid oracle run (iterate.cpp:88-153)."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import paper_2603_18527_b200 as bs  # noqa: E402
+from oracle import MAP_POINTWISE, MAP_SCALAR, OracleProblem  # noqa: E402
+from paper_2603_18527_b200.slab import DistComm, LocalComm, run_slab  # noqa: E402
+from slab_standin import NumpySlabPart  # noqa: E402
+
+FIELD_TOL = 1e-10
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def instance(n, seed=3):
+    spec = bs.InstanceSpec(n=n, ppw=10.0, contrast=0.3, sigma_cells=3.0, seed=seed)
+    k2, f, k0, eta = bs.make_instances(spec, 0, 1)
+    return k2[0], f[0], float(k0[0]), float(eta[0])
+
+
+def oracle_run(k2, f, k0, eta, cmap, rtol, max_iters, u0=None):
+    p = OracleProblem(k2, k0, eta)
+    if isinstance(cmap, bs.PointwiseMap):
+        return p.run(f, map_kind=MAP_POINTWISE, rtol=rtol, max_iters=max_iters, u0=u0)
+    return p.run(f, map_kind=MAP_SCALAR, gamma=cmap.gamma, rtol=rtol, max_iters=max_iters, u0=u0)
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4])
+@pytest.mark.parametrize("cmap", [bs.ScalarMap(1.0), bs.PointwiseMap()], ids=["scalar", "pointwise"])
+def test_local_slab_driver_matches_oracle(nranks, cmap):
+    k2, f, k0, eta = instance(32)
+    cfg = bs.IterationConfig(rtol=1e-8, max_iters=3000)
+    parts = [NumpySlabPart(k2, k0, eta, r, nranks) for r in range(nranks)]
+    res = run_slab(parts, LocalComm(), cmap, f, cfg)
+    ref = oracle_run(k2, f, k0, eta, cmap, 1e-8, 3000)
+    assert res.trace.terminated == ref.terminated == "converged"
+    assert abs(res.trace.iters - ref.iters) <= 1
+    assert rel(res.u, ref.u) < FIELD_TOL
+    k = min(res.trace.iters, ref.iters) + 1
+    np.testing.assert_allclose(res.trace.res_l2_rel[:k], ref.res_l2[:k], rtol=1e-9, atol=1e-13)
+    np.testing.assert_allclose(res.trace.res_reta_rel[:k], ref.res_reta[:k], rtol=1e-9, atol=1e-13)
+
+
+def test_local_slab_driver_warm_start_and_max_iters():
+    k2, f, k0, eta = instance(32, seed=5)
+    u0 = 1e-3 * (np.random.default_rng(2).standard_normal(k2.shape) + 0j)
+    parts = [NumpySlabPart(k2, k0, eta, r, 2) for r in range(2)]
+    res = run_slab(parts, LocalComm(), bs.ScalarMap(1.0), f, bs.IterationConfig(rtol=1e-8, max_iters=7), u0=u0)
+    ref = oracle_run(k2, f, k0, eta, bs.ScalarMap(1.0), 1e-8, 7, u0=u0)
+    assert res.trace.terminated == ref.terminated == "max_iters"
+    assert res.trace.iters == ref.iters == 7
+    assert rel(res.u, ref.u) < FIELD_TOL
+
+
+def test_local_slab_zero_source_raises():
+    k2, f, k0, eta = instance(16)
+    parts = [NumpySlabPart(k2, k0, eta, r, 2) for r in range(2)]
+    with pytest.raises(ValueError, match="zero source"):
+        run_slab(parts, LocalComm(), bs.ScalarMap(1.0), np.zeros_like(f))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from slab_standin import NumpySlabPart as Part
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        k2, f, k0, eta = instance(32)
+        part = Part(k2, k0, eta, rank, world)
+        res = run_slab([part], DistComm(), bs.PointwiseMap(), f, bs.IterationConfig(rtol=1e-8, max_iters=3000))
+        q.put((rank, part.row0, part.rows, res.u, res.trace.iters, res.trace.terminated,
+               res.trace.res_l2_rel, res.sweeps_launched))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_slab_matches_oracle():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = sorted([q.get(timeout=300) for _ in procs], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    k2, f, k0, eta = instance(32)
+    ref = oracle_run(k2, f, k0, eta, bs.PointwiseMap(), 1e-8, 3000)
+    u = np.zeros_like(ref.u)
+    for rank, row0, rows, ur, iters, term, l2, launched in results:
+        lo, hi = max(row0 - 1, 0), min(row0 + rows - 1, k2.shape[0])
+        u[lo:hi] = ur[lo:hi]  # each rank filled only its own rows
+        assert term == ref.terminated == "converged"
+        assert abs(iters - ref.iters) <= 1
+    # both ranks saw the same trace and stopped at the same sweep
+    assert results[0][4] == results[1][4] and results[0][7] == results[1][7]
+    assert np.array_equal(results[0][6], results[1][6])
+    assert rel(u, ref.u) < FIELD_TOL
