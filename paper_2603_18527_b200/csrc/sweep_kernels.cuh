@@ -224,7 +224,9 @@ struct RowGeom {
 //          stencil (the 3-D extension of config c3; no reference counterpart).
 // TOUT: write the forward transform transposed ([member][q][i], a.TT) through a CTA-wide
 // shared-memory tile (128-B segments), for the warp-per-line column pass tcol_kernel.
-template <int LOG2N, int MODE, int NW, int PP, int DIM = 2, bool TOUT = false>
+// SLAB: the launch covers one rank's x-slab (RowArgs::slab_log2 / row0 / slab_sums); a separate
+// instantiation so the whole-member path keeps its compile-time indexing.
+template <int LOG2N, int MODE, int NW, int PP, int DIM = 2, bool TOUT = false, bool SLAB = false>
 __global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? 128 : 80>::value))
 row_kernel(const RowArgs a) {
     using G = Geom<LOG2N, PP>;
@@ -242,10 +244,11 @@ row_kernel(const RowArgs a) {
     const int t = threadIdx.x % T;
     const int e = threadIdx.x / T;
     const long grow = (long)blockIdx.x * EPB + e;
-    const int lsh = (DIM == 2 && a.slab_log2) ? a.slab_log2 : LLINES;  // log2(lines per member)
+    static_assert(!SLAB || (DIM == 2 && !TOUT), "slabs: 2-D row-major handoff only");
+    const int lsh = SLAB ? a.slab_log2 : LLINES;        // log2(lines per member)
     const int b = (int)(grow >> lsh);
     const int i = (int)(grow & ((1L << lsh) - 1));      // line index within the member (slab)
-    const int ig = (DIM == 2 && a.slab_log2) ? a.row0 + i : i;  // global line index
+    const int ig = SLAB ? a.row0 + i : i;               // global line index
     bool valid = (b < a.batch) && (ig & (N - 1)) != 0 && (DIM == 2 || (i >> LOG2N) != 0);
     int m = 0;  // trace entry this launch belongs to
     if (S::ITER && valid) {
@@ -259,9 +262,9 @@ row_kernel(const RowArgs a) {
     const size_t mem = (size_t)(valid ? b : 0) << (lsh + LOG2N);
     const size_t row = mem + (size_t)(valid ? i : 0) * N;
     // T element (this line, column j): row-major, or blocked by destination rank on a slab
-    const int sl = DIM == 2 ? a.slab_log2 : 0;
+    const int sl = SLAB ? a.slab_log2 : 0;
     auto tix = [&](int j) -> size_t {
-        if (sl == 0) return row + j;
+        if constexpr (!SLAB) return row + j;
         return mem + ((size_t)(j >> sl) << (2 * sl)) + ((size_t)(valid ? i : 0) << sl) + (j & ((1 << sl) - 1));
     };
     const double2 zero = make_double2(0.0, 0.0);
@@ -474,7 +477,7 @@ row_kernel(const RowArgs a) {
             for (int k = 0; k < S::NPART; ++k) pr[k] = acc[k];
             __threadfence();
             const unsigned old = atomicAdd(&a.ctl.counter[b], 1u);
-            const unsigned nvalid = sl ? (1u << sl) - (a.row0 == 0 ? 1u : 0u) : VALID_LINES;
+            const unsigned nvalid = SLAB ? (1u << sl) - (a.row0 == 0 ? 1u : 0u) : VALID_LINES;
             last = (old == nvalid - 1u);
         }
         last = pol.bcast0(last, t);
@@ -484,7 +487,7 @@ row_kernel(const RowArgs a) {
 #pragma unroll
             for (int k = 0; k < S::NPART; ++k) s[k] = 0.0;
             for (int r = t; r < (1 << lsh); r += T) {
-                const int rg = sl ? a.row0 + r : r;
+                const int rg = SLAB ? a.row0 + r : r;
                 if ((rg & (N - 1)) == 0 || (DIM == 3 && (r >> LOG2N) == 0)) continue;  // padding lines
                 const double* pr = a.ctl.partial + (((size_t)b << lsh) + r) * kPartStride;
 #pragma unroll
@@ -497,7 +500,7 @@ row_kernel(const RowArgs a) {
                 if constexpr (MODE == R_OPT_A) finalize_gamma(a.ctl, b, s[2], s[3], s[4]);
                 if constexpr (MODE == R_RETA_C) finalize_gamma(a.ctl, b, s[0], s[1], s[2]);
                 if constexpr (S::ENTRY) {
-                    if (sl) {  // slab: partial sums of this rank, finalised after the all-reduce
+                    if constexpr (SLAB) {  // partial sums of this rank, finalised after the all-reduce
                         a.slab_sums[2 * b] = s[0];
                         a.slab_sums[2 * b + 1] = s[1];
                     } else {

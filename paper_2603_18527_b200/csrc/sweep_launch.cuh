@@ -16,12 +16,22 @@ struct ColCols {
     static constexpr int value = L <= 9 ? 8 : (L == 10 ? 4 : 2);
 };
 
-template <int L, int MODE, int PP, int DIM, bool TOUT = false>
+template <int L, int MODE, int PP, int DIM, bool TOUT = false, bool SLAB = false>
 cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
     using RG = RowGeom<L, PP, kRowWarps>;
-    auto k = row_kernel<L, MODE, kRowWarps, PP, DIM, TOUT>;
+    // slab launches (2-D, row-major handoff, the modes the slab driver uses) -> SLAB instance
+    constexpr bool SLAB_OK = DIM == 2 && !TOUT && PP == 16 &&
+                             (MODE == R_FWD || MODE == R_FWD_BORN || MODE == R_INV || MODE == R_SWEEP);
+    if constexpr (SLAB_OK && !SLAB) {
+        if (a.slab_log2 || prepare) {
+            const cudaError_t e = launch_row_t<L, MODE, PP, DIM, false, true>(a, s, prepare);
+            if (!prepare || e != cudaSuccess) return e;
+        }
+    }
+    if (!SLAB && a.slab_log2 && !prepare) return cudaErrorInvalidValue;
+    auto k = row_kernel<L, MODE, kRowWarps, PP, DIM, TOUT, SLAB>;
     if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
-    const long rows = (long)a.batch << ((DIM == 2 && a.slab_log2) ? a.slab_log2 : (DIM - 1) * L);
+    const long rows = (long)a.batch << (SLAB ? a.slab_log2 : (DIM - 1) * L);
     const int grid = (int)((rows + RG::EPB - 1) / RG::EPB);
     k<<<grid, kRowWarps * 32, RG::SMEM, s>>>(a);
     return cudaGetLastError();
