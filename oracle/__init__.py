@@ -318,6 +318,14 @@ class Reference:
             lib.bpref_laplacian_symbol.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _dp]
             lib.bpref_five_point.argtypes = [_dp, C.c_int, C.c_int, C.c_double, _dp]
             lib.bpref_dct.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
+            lib.bpref_save_field.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, _dp]
+            lib.bpref_load_field.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, _dp]
+            lib.bpref_export_csv.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, _dp]
+            lib.bpref_save_problem_helmholtz.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int,
+                                                         C.c_double, C.c_double, _dp, C.c_double,
+                                                         C.c_double]
+            lib.bpref_load_problem_helmholtz.argtypes = [C.c_char_p] + [C.POINTER(C.c_int)] * 2 + \
+                [C.POINTER(C.c_double)] * 4 + [_dp, C.c_int]
             lib.bpref_five_point.restype = None
             lib.bpref_thread_count.restype = C.c_int
             cls._lib = lib
@@ -341,6 +349,50 @@ class Reference:
                                                    C.byref(k0), C.byref(eta)):
             raise OracleError(cls.lib().bpref_last_error().decode())
         return k2, f, k0.value, eta.value
+
+    # ---- the reference's file formats (field.cpp, problem_io.cpp)
+    @classmethod
+    def _chk(cls, rc):
+        if rc:
+            raise OracleError(cls.lib().bpref_last_error().decode())
+
+    @classmethod
+    def save_field(cls, path, a):
+        a = np.asarray(a)
+        cx = int(np.iscomplexobj(a))
+        a = np.ascontiguousarray(a, np.complex128 if cx else np.float64)
+        cls._chk(cls.lib().bpref_save_field(os.fsencode(path), a.shape[0], a.shape[1], cx, _ptr(a)))
+
+    @classmethod
+    def load_field(cls, path, nx, ny, complex_=True):
+        out = np.empty((nx, ny), np.complex128 if complex_ else np.float64)
+        cls._chk(cls.lib().bpref_load_field(os.fsencode(path), nx, ny, int(complex_), _ptr(out)))
+        return out
+
+    @classmethod
+    def export_csv(cls, path, a):
+        a = np.asarray(a)
+        cx = int(np.iscomplexobj(a))
+        a = np.ascontiguousarray(a, np.complex128 if cx else np.float64)
+        cls._chk(cls.lib().bpref_export_csv(os.fsencode(path), a.shape[0], a.shape[1], cx, _ptr(a)))
+
+    @classmethod
+    def save_problem_helmholtz(cls, directory, stem, k2, k0, eta, lx=1.0, ly=1.0):
+        k2 = _c(k2)
+        cls._chk(cls.lib().bpref_save_problem_helmholtz(os.fsencode(directory), stem.encode(),
+                                                         k2.shape[0], k2.shape[1], lx, ly, _ptr(k2),
+                                                         k0, eta))
+
+    @classmethod
+    def load_problem_helmholtz(cls, path, cap=1 << 22):
+        nx, ny = C.c_int(), C.c_int()
+        lx, ly, k0, eta = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        buf = np.empty(cap, np.complex128)
+        cls._chk(cls.lib().bpref_load_problem_helmholtz(os.fsencode(path), C.byref(nx), C.byref(ny),
+                                                         C.byref(lx), C.byref(ly), C.byref(k0),
+                                                         C.byref(eta), _ptr(buf), cap))
+        return dict(nx=nx.value, ny=ny.value, lx=lx.value, ly=ly.value, k0=k0.value, eta=eta.value,
+                    k2=buf[:nx.value * ny.value].reshape(nx.value, ny.value).copy())
 
     @classmethod
     def dct(cls, x, inverse=False):

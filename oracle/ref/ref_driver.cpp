@@ -28,6 +28,7 @@
 #include "bp/kernels.hpp"
 #include "bp/parallel.hpp"
 #include "bp/problem.hpp"
+#include "bp/problem_io.hpp"
 #include "bp/rng.hpp"
 #include "bp/samplers.hpp"
 #include "bp/symbol.hpp"
@@ -456,6 +457,77 @@ void bpref_five_point(const double* u, int nx, int ny, double h2, double* out) {
     const size_t n = static_cast<size_t>(nx) * ny;
     bp::kernels::five_point(std::span<const cplx>(reinterpret_cast<const cplx*>(u), n), nx, ny,
                             h2, std::span<cplx>(reinterpret_cast<cplx*>(out), n));
+}
+
+// ---- BPFD field / problem I/O (field.cpp:37-133, problem_io.cpp:16-95): the reference's own
+// writers and readers, for the byte-exact pins of the project's native I/O (tests/)
+int bpref_save_field(const char* path, int nx, int ny, int dtype, const double* data) {
+    return guarded([&] {
+        GridSpec g = bp::make_grid(nx, ny, 1.0, 1.0, bp::Bc::Periodic);
+        if (dtype == 1) {
+            bp::save_field(path, field_from(g, data));
+        } else {
+            bp::RealField f(g);
+            std::memcpy(f.data.data(), data, sizeof(double) * f.data.size());
+            bp::save_field(path, f);
+        }
+    });
+}
+
+int bpref_load_field(const char* path, int nx, int ny, int dtype, double* out) {
+    return guarded([&] {
+        if (dtype == 1) {
+            ComplexField f = bp::load_complex_field(path, bp::Bc::Periodic, 1.0, 1.0);
+            if (f.grid.nx != nx || f.grid.ny != ny) throw std::invalid_argument("shape");
+            field_to(f, out);
+        } else {
+            bp::RealField f = bp::load_real_field(path, bp::Bc::Periodic, 1.0, 1.0);
+            if (f.grid.nx != nx || f.grid.ny != ny) throw std::invalid_argument("shape");
+            std::memcpy(out, f.data.data(), sizeof(double) * f.data.size());
+        }
+    });
+}
+
+int bpref_export_csv(const char* path, int nx, int ny, int dtype, const double* data) {
+    return guarded([&] {
+        GridSpec g = bp::make_grid(nx, ny, 1.0, 1.0, bp::Bc::Periodic);
+        if (dtype == 1) {
+            bp::export_csv(path, field_from(g, data));
+        } else {
+            bp::RealField f(g);
+            std::memcpy(f.data.data(), data, sizeof(double) * f.data.size());
+            bp::export_csv(path, f);
+        }
+    });
+}
+
+// save_problem of the reference's own HelmholtzProblem (periodic) -> manifest + k2 file
+int bpref_save_problem_helmholtz(const char* dir, const char* stem, int nx, int ny, double lx,
+                                 double ly, const double* k2, double k0, double eta) {
+    return guarded([&] {
+        GridSpec g = bp::make_grid(nx, ny, lx, ly, bp::Bc::Periodic);
+        bp::HelmholtzProblem p(g, field_from(g, k2), k0, eta);
+        bp::save_problem(dir, stem, p);
+    });
+}
+
+// load_problem of a helmholtz manifest -> grid, k0, eta, k2 (nx*ny complex)
+int bpref_load_problem_helmholtz(const char* path, int* nx, int* ny, double* lx, double* ly,
+                                 double* k0, double* eta, double* k2, int cap) {
+    return guarded([&] {
+        bp::ProblemPtr p = bp::load_problem(path);
+        const auto* h = dynamic_cast<const bp::HelmholtzProblem*>(p.get());
+        if (!h) throw std::invalid_argument("not a helmholtz manifest");
+        const GridSpec& g = h->grid();
+        *nx = g.nx;
+        *ny = g.ny;
+        *lx = g.lx;
+        *ly = g.ly;
+        *k0 = h->k0();
+        *eta = h->eta();
+        if ((long)g.nx * g.ny > cap) throw std::invalid_argument("capacity");
+        field_to(h->k2(), k2);
+    });
 }
 
 }  // extern "C"

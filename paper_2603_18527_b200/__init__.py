@@ -19,7 +19,7 @@ from .api import (  # noqa: F401
 )
 from .instances import (CONFIGS, CdrSpec, InstanceSpec, config_instances,  # noqa: F401
                         make_cdr_instances, make_instances)
-from . import _native  # noqa: F401
+from . import _native, bpfd, slab  # noqa: F401
 
 __all__ = [
     "CdrNeumann", "FourierDiagMap", "HelmholtzDirichlet", "HelmholtzPeriodic", "IterationConfig", "IterationTrace", "OptimalScalarMap", "PointwiseMap",

@@ -121,6 +121,14 @@ HOST_FUNCTIONS = {
     "bp_gaussian_bump": (None, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
                                 C.c_double, C.c_double, C.c_double, _dp]),
     "bp_gaussian_smooth": (None, [C.c_int32, C.c_int32, C.c_double, _dp, _dp]),
+    # include/bornsweep_io.h
+    "bp_io_last_error": (C.c_char_p, []),
+    "bp_bpfd_save": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _dp]),
+    "bp_bpfd_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                               C.POINTER(C.c_int32)]),
+    "bp_bpfd_load": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _dp]),
+    "bp_csv_export": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _dp]),
+    "bp_trace_csv_write": (C.c_int, [C.c_char_p, C.c_int32, _dp, _dp]),
 }
 
 _lib = None

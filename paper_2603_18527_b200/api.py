@@ -156,6 +156,7 @@ class HelmholtzDirichlet:
         k0 = np.ascontiguousarray(np.broadcast_to(np.asarray(k0, np.float64), (self.batch,)))
         eta = np.ascontiguousarray(np.broadcast_to(np.asarray(eta, np.float64), (self.batch,)))
         self.k0, self.eta, self.lx, self.device = k0, eta, lx, device
+        self.k2 = k2  # host copy of the media (save_problem)
         h = C.c_void_p()
         self._lib = N.lib()
         if dim == 3:
@@ -235,7 +236,7 @@ class HelmholtzDirichlet:
         k0 = np.ascontiguousarray(np.broadcast_to(np.asarray(k0, np.float64), (self.batch,)))
         eta = np.ascontiguousarray(np.broadcast_to(np.asarray(eta, np.float64), (self.batch,)))
         _check(self._lib.bp_problem_set_medium(self._h, _ptr(k2), _ptr(k0), _ptr(eta)))
-        self.k0, self.eta = k0, eta
+        self.k0, self.eta, self.k2 = k0, eta, k2
 
     @property
     def stream(self) -> int:
@@ -288,6 +289,7 @@ class CdrNeumann(HelmholtzDirichlet):
             sigma0 = sigma.reshape(self.batch, -1).mean(axis=1)
         sigma0 = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma0, np.float64), (self.batch,)))
         self.sigma0, self.lx, self.device = sigma0, lx, device
+        self.bx, self.by, self.sigma = bx, by, sigma  # host copies (save_problem)
         h = C.c_void_p()
         self._lib = N.lib()
         g = N.Grid(self.nx, self.ny, lx, lx, BC_NEUMANN)
@@ -302,7 +304,7 @@ class CdrNeumann(HelmholtzDirichlet):
         sigma0 = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma0, np.float64), (self.batch,)))
         _check(self._lib.bp_problem_set_cdr_medium(self._h, _ptr(bx), _ptr(by), _ptr(sigma),
                                                    _ptr(sigma0)))
-        self.sigma0 = sigma0
+        self.sigma0, self.bx, self.by, self.sigma = sigma0, bx, by, sigma
 
 
 def run(problem: HelmholtzDirichlet, cmap, f, config: IterationConfig | None = None, u0=None,

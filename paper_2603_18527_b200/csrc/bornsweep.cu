@@ -299,6 +299,14 @@ int check_symbol(const bp_grid& g, int dim, int batch, const double* k0, const d
     for (int b = 0; b < batch; ++b) {
         double mn = INFINITY, mx = 0.0;
         const double k0sq = k0[b] * k0[b];
+        {
+            // |lambda| >= eta everywhere and the largest |lambda| sits at an extreme mode sum:
+            // when eta alone clears the guard the scan below cannot fail (the common case)
+            const double lo = dim == 3 ? (lap[1] + lap[1]) + lap[1] : lap[1] + lap[1];
+            const double hi = dim == 3 ? (lap[n - 1] + lap[n - 1]) + lap[n - 1] : lap[n - 1] + lap[n - 1];
+            const double mx0 = std::hypot(std::max(std::fabs(lo - k0sq), std::fabs(hi - k0sq)), eta[b]);
+            if (std::fabs(eta[b]) >= kSymbolDivGuard * mx0 * (1.0 + 1e-12)) continue;
+        }
         for (int pp = 1; pp < n; ++pp)
             for (int qq = 1; qq < n; ++qq)
                 for (int rr = 1; rr < (dim == 3 ? n : 2); ++rr) {
@@ -1313,9 +1321,15 @@ std::vector<double> xi2_table(int n, double len) {
 }
 
 int check_symbol_periodic(const std::vector<double>& xi2, int batch, const double* k0, const double* eta) {
+    const double xmax = *std::max_element(xi2.begin(), xi2.end());
+    const double xmin = *std::min_element(xi2.begin(), xi2.end());
     for (int b = 0; b < batch; ++b) {
         double mn = INFINITY, mx = 0.0;
         const double k0sq = k0[b] * k0[b];
+        {
+            const double mx0 = std::hypot(std::max(std::fabs((xmin + xmin) - k0sq), std::fabs((xmax + xmax) - k0sq)), eta[b]);
+            if (std::fabs(eta[b]) >= kSymbolDivGuard * mx0 * (1.0 + 1e-12)) continue;  // see check_symbol
+        }
         for (double a : xi2)
             for (double c : xi2) {
                 const double v = std::hypot((a + c) - k0sq, -eta[b]);

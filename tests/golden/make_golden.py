@@ -9,6 +9,8 @@
 * ref_dct.npz        -- the reference's DCT-II / DCT-III transform pair (Neumann grids,
                         transforms.cpp:105-148) and Neumann five-point symbol (symbol.cpp:81-92),
                         plus scipy.fft.dctn(type=2/3) of the same real inputs (config c4)
+* ref_io/            -- BPFD field files, CSV exports and a helmholtz problem manifest written by
+                        the reference's own field.cpp / problem_io.cpp (io_inputs.npz: the data)
 * ref_ops_n{16,32}.npz, ref_run_*.npz
                      -- operator outputs and run() trajectories produced by the reference's own
                         L1-L3 code (oracle/_ref) on instances from libbornsweep_host.so
@@ -142,11 +144,28 @@ def dct_golden():
     np.savez_compressed(os.path.join(HERE, "ref_dct.npz"), **out)
 
 
+def io_golden():
+    d = os.path.join(HERE, "ref_io")
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng(77)
+    fc = rng.standard_normal((5, 7)) + 1j * rng.standard_normal((5, 7))
+    fr = rng.standard_normal((6, 4))
+    fr[0, 0], fr[1, 1] = 1.0, 1e-300  # formatting edge cases in the CSV
+    k2, f, k0, eta = Reference.periodic_bench_instance(16, 8.0, 1.0, 3)
+    Reference.save_field(os.path.join(d, "field_c.bpfd"), fc)
+    Reference.save_field(os.path.join(d, "field_r.bpfd"), fr)
+    Reference.export_csv(os.path.join(d, "field_c.csv"), fc)
+    Reference.export_csv(os.path.join(d, "field_r.csv"), fr)
+    Reference.save_problem_helmholtz(d, "helm", k2, k0, eta)
+    np.savez_compressed(os.path.join(HERE, "io_inputs.npz"), fc=fc, fr=fr, k2=k2, f=f, k0=k0, eta=eta)
+
+
 if __name__ == "__main__":
     Reference.set_mode("serial")
-    if sys.argv[1:] == ["dct"]:
-        dct_golden()
+    if sys.argv[1:] in (["dct"], ["io"]):
+        {"dct": dct_golden, "io": io_golden}[sys.argv[1]]()
         sys.exit(0)
+    io_golden()
     dct_golden()
     dst_golden()
     dst3_golden()

@@ -102,9 +102,11 @@ def test_c_abi_library_exports_every_declared_symbol():
 
 
 def test_instances_header_symbols_exported():
-    text = open(os.path.join(ROOT, "include", "bornsweep_instances.h")).read()
-    declared = set(re.findall(r"^(?:int|void)\s+(bp_\w+)\s*\(", text, flags=re.M))
-    assert declared == set(N.HOST_FUNCTIONS)
+    declared = set()
+    for h in ("bornsweep_instances.h", "bornsweep_io.h"):  # both live in libbornsweep_host.so
+        text = open(os.path.join(ROOT, "include", h)).read()
+        declared |= set(re.findall(r"^(?:int|void|const char\*)\s+(bp_\w+)\s*\(", text, flags=re.M))
+    assert declared == set(N.HOST_FUNCTIONS), declared ^ set(N.HOST_FUNCTIONS)
     for name in declared:
         assert hasattr(N.host_lib(), name)
 
