@@ -389,6 +389,16 @@ struct DstEngine {
 
     // x[m] = x_{t+Tm}, xm[m] = x_{N-t-Tm} (mirror; must be 0 where the index is N).
     // On return y[l] = Y_{tP+l}.  buf: this engine's padded smem line (G::PAD_N double2).
+    // DST-I pre-processing of one element: y_j = 2 sin(pi j/N)(x_j + x_{N-j}) + (x_j - x_{N-j})
+    // with 2 sin(pi j/N) = st cos(2 pi m/P') + ct sin(...) for j = t + T m (kCS16 table)
+    __device__ __forceinline__ static double2 pre(double2 x, double2 xm, int m, double st, double ct) {
+        constexpr int STEP = 16 / P;
+        const double s = fma(st, kCS16[m * STEP].c, ct * kCS16[m * STEP].s);
+        const double2 a = cadd(x, xm);
+        const double2 d = csub(x, xm);
+        return make_double2(fma(s, a.x, d.x), fma(s, a.y, d.y));
+    }
+
     template <class Pol>
     __device__ __forceinline__ static void run(const double2 (&x)[P], const double2 (&xm)[P], double2 (&y)[P],
                                                int t, double2* buf, const double2* __restrict__ tw,
@@ -401,13 +411,34 @@ struct DstEngine {
 #pragma unroll
         for (int m = 0; m < P; ++m) {
             const int j = t + T * m;
-            constexpr int STEP = 16 / P;
-            const double s = fma(st, kCS16[m * STEP].c, ct * kCS16[m * STEP].s);
-            const double2 a = cadd(x[m], xm[m]);
-            const double2 d = csub(x[m], xm[m]);
-            v[m] = (j == 0) ? make_double2(0.0, 0.0)
-                            : make_double2(fma(s, a.x, d.x), fma(s, a.y, d.y));
+            v[m] = (j == 0) ? make_double2(0.0, 0.0) : pre(x[m], xm[m], m, st, ct);
         }
+        transform(v, y, t, buf, tw, pol);
+    }
+
+    // Same transform with the line already in buf (natural order at pidx(j)): the mirror
+    // x_{N-j} is read from shared memory as each element is pre-processed, so neither the
+    // line nor its mirror has to be held in registers.  v: scratch of P registers.
+    template <class Pol>
+    __device__ __forceinline__ static void run_smem(double2 (&v)[P], double2 (&y)[P], int t, double2* buf,
+                                                    const double2* __restrict__ tw,
+                                                    const double* __restrict__ sinp, const Pol& pol) {
+        const double st = 2.0 * __ldg(&sinp[t]), ct = 2.0 * __ldg(&sinp[t + H]);
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            const int j = t + T * m;
+            const double2 x = buf[G::pidx(j)];
+            const double2 xm = buf[G::pidx((N - j) & (N - 1))];
+            v[m] = (j == 0) ? make_double2(0.0, 0.0) : pre(x, xm, m, st, ct);
+        }
+        pol.sync();
+        transform(v, y, t, buf, tw, pol);
+    }
+
+    // first Stockham pass (radix P in registers), the remaining passes, fused post-processing
+    template <class Pol>
+    __device__ __forceinline__ static void transform(double2 (&v)[P], double2 (&y)[P], int t, double2* buf,
+                                                     const double2* __restrict__ tw, const Pol& pol) {
         Dft<P>::template run<1>(v);
 #pragma unroll
         for (int r = 0; r < P; ++r) buf[G::pidx(t * P + r)] = v[r];

@@ -21,6 +21,9 @@
 #ifndef BS_SHFL_MIRROR
 #define BS_SHFL_MIRROR 1
 #endif
+#ifndef BS_COL_SMEM_MIRROR
+#define BS_COL_SMEM_MIRROR 1
+#endif
 
 namespace bs {
 
@@ -651,14 +654,28 @@ col_kernel(const ColArgs a) {
     const BlockSeg<T, C> pol{smem + C * G::PAD_N, c};
     const double2 zero = make_double2(0.0, 0.0);
 
-    double2 x[P], xm[P], y[P];
+    double2 x[P], y[P];
+#if BS_COL_SMEM_MIRROR
+    // the column goes through shared memory; the pre-processing reads x_j and x_{N-j} there
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
-        x[mm] = a.T[mem + (size_t)j * LS + qa];
-        xm[mm] = (j == 0) ? zero : a.T[mem + (size_t)(N - j) * LS + qa];
+        buf[G::pidx(j)] = a.T[mem + (size_t)j * LS + qa];
     }
-    Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+    pol.sync();
+    Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
+#else
+    {
+        double2 xm[P];
+#pragma unroll
+        for (int mm = 0; mm < P; ++mm) {
+            const int j = t + T * mm;
+            x[mm] = a.T[mem + (size_t)j * LS + qa];
+            xm[mm] = (j == 0) ? zero : a.T[mem + (size_t)(N - j) * LS + qa];
+        }
+        Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+    }
+#endif
 
     if constexpr (MODE == C_ONE) {
 #pragma unroll
@@ -688,14 +705,7 @@ col_kernel(const ColArgs a) {
             buf[G::pidx(p)] = v;
         }
         pol.sync();
-#pragma unroll
-        for (int mm = 0; mm < P; ++mm) {
-            const int j = t + T * mm;
-            x[mm] = buf[G::pidx(j)];
-            xm[mm] = (j == 0) ? zero : buf[G::pidx(N - j)];
-        }
-        pol.sync();
-        Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+        Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
         for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + qa] = y[l];
     }
