@@ -24,6 +24,9 @@
 #ifndef BS_COL_SMEM_MIRROR
 #define BS_COL_SMEM_MIRROR 1
 #endif
+#ifndef BS_ROW_SMEM
+#define BS_ROW_SMEM 1
+#endif
 
 namespace bs {
 
@@ -297,13 +300,36 @@ row_kernel(const RowArgs a) {
         }
     }
 
-    double2 q[P];                    // source of the forward transform
     double acc[S::NPART > 0 ? S::NPART : 1] = {};
+    // shared-memory staging pays off for multi-warp lines (n >= 1024) and the 3-D stencil;
+    // single-warp 2-D lines keep the register path (measured, r01)
+    constexpr bool RSM = BS_ROW_SMEM && (T > 32 || DIM == 3);
+    double2 q[P];                    // register path: source of the forward transform
+    double2 z[P];                    // register path: G q
 
-    // ---- inverse y-DST of the column-pass output, staged to the stride layout
-    double2 z[P];
+    // ---- inverse y-DST of the column-pass output, staged to the stride layout.  BS_ROW_SMEM:
+    // the T row goes through shared memory (pre-processing reads x_j and x_{N-j} there) and
+    // G q stays there in natural order for the element-wise phase, which writes the next
+    // source into the same slots (same thread, same j): neither the line, its mirror, G q nor
+    // the next source occupies registers, so the element-wise loads can be kept in flight.
     if constexpr (S::INV) {
-        double2 x[P], xm[P], y[P];
+        double2 y[P];
+        if constexpr (RSM) {
+#pragma unroll
+            for (int mm = 0; mm < P; ++mm) {
+                const int j = t + T * mm;
+                buf[G::pidx(j)] = valid ? a.T[tix(j)] : zero;
+            }
+            pol.sync();
+            {
+                double2 v[P];
+                Engine::run_smem(v, y, t, buf, a.tw, a.sinp, pol);
+            }
+#pragma unroll
+            for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
+            pol.sync();
+        } else {
+        double2 x[P], xm[P];
 #pragma unroll
         for (int mm = 0; mm < P; ++mm) {
             const int j = t + T * mm;
@@ -317,28 +343,31 @@ row_kernel(const RowArgs a) {
 #pragma unroll
         for (int mm = 0; mm < P; ++mm) z[mm] = buf[G::pidx(t + T * mm)];
         pol.sync();
+        }
     }
 
     // ---- element-wise phase
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
+        const double2 zz = !S::INV ? zero : RSM ? buf[G::pidx(j)] : z[mm];
+        double2 qv = zero;
         if constexpr (MODE == R_INV) {
-            double2 o = z[mm];
+            double2 o = zz;
             if (a.sub) o = csub(o, valid ? a.sub[row + j] : zero);
             if (valid) a.out[row + j] = (j == 0) ? zero : o;
         } else if constexpr (MODE == R_FWD) {
             const double2 v = valid ? a.in[row + j] : zero;
-            q[mm] = (j == 0) ? zero : v;
+            qv = (j == 0) ? zero : v;
         } else if constexpr (MODE == R_FWD_BORN) {
             const double2 v = valid ? a.in[row + j] : zero;
             const double2 V = csub(valid ? a.k2[row + j] : zero, shift);
             const double2 o = cadd(cmul(v, V), valid ? a.f[row + j] : zero);  // mul(u, v) + f
-            q[mm] = (j == 0) ? zero : o;
+            qv = (j == 0) ? zero : o;
         } else if constexpr (MODE == R_RETA_C) {
             // z = G V x: w = x - G V x (correction.cpp:38-44); gamma = <w, x> / <w, w>
             const double2 x = valid ? a.X[row + j] : zero;
-            const double2 w = csub(x, z[mm]);
+            const double2 w = csub(x, zz);
             if (j != 0) {
                 acc[0] += w.x * x.x + w.y * x.y;  // Re conj(w) x
                 acc[1] += w.x * x.y - w.y * x.x;  // Im conj(w) x
@@ -366,7 +395,7 @@ row_kernel(const RowArgs a) {
                         ub = ucur[row + PLANE + j];
                     }
                 }
-                const double2 x = csub(z[mm], u);
+                const double2 x = csub(zz, u);
                 double2 s;
                 if constexpr (DIM == 3) {
                     // seven-point: (6u - x-1 - x+1 - y-1 - y+1 - z-1 - z+1) / h^2
@@ -391,7 +420,7 @@ row_kernel(const RowArgs a) {
                     double2 unew = cadd(u, cmul(g, x));
                     if (j == 0) unew = zero;
                     if (valid) unext[row + j] = unew;
-                    q[mm] = cadd(cmul(V, unew), f);
+                    qv = cadd(cmul(V, unew), f);
                 } else if constexpr (MODE == R_OPT_A) {
                     // w = A x = (L_ref - V) G r = r - V x (key identity; the reference applies
                     // A by stencil, correction.cpp:33-36 -- equal to roundoff)
@@ -404,9 +433,9 @@ row_kernel(const RowArgs a) {
                     if (valid) a.X[row + j] = (j == 0) ? zero : x;
                 } else if constexpr (MODE == R_RETA_A) {
                     if (valid) a.X[row + j] = (j == 0) ? zero : x;
-                    q[mm] = (j == 0) ? zero : cmul(x, V);  // apply_V(x)
+                    qv = (j == 0) ? zero : cmul(x, V);  // apply_V(x)
                 } else {  // R_FD_A: forward transform of the direction itself
-                    q[mm] = (j == 0) ? zero : x;
+                    qv = (j == 0) ? zero : x;
                 }
             } else {
                 // R_OPT_B: u' = u + gamma x ; R_FD_B: u' = u + du (du = z)
@@ -416,20 +445,32 @@ row_kernel(const RowArgs a) {
                     const double2 g = valid ? a.ctl.gamma[b] : zero;
                     du = cmul(g, x);  // kernels::scale(x, gamma)
                 } else {
-                    du = z[mm];
+                    du = zz;
                 }
                 double2 unew = cadd(u, du);
                 if (j == 0) unew = zero;
                 if (valid) unext[row + j] = unew;
-                q[mm] = cadd(cmul(V, unew), f);
+                qv = cadd(cmul(V, unew), f);
             }
+        }
+        if constexpr (S::FWD) {
+            if constexpr (RSM) buf[G::pidx(j)] = qv;  // the slot this thread read G q from
+            else q[mm] = qv;
         }
     }
     if constexpr (MODE == R_INV) return;
 
     // ---- forward y-DST of q (mirror by warp shuffles, or shared memory for multi-warp rows)
     if constexpr (S::FWD) {
-        double2 qm[P], y2[P];
+        double2 y2[P];
+        if constexpr (RSM) {
+        pol.sync();
+        {
+            double2 v[P];
+            Engine::run_smem(v, y2, t, buf, a.tw, a.sinp, pol);
+        }
+        } else {
+        double2 qm[P];
 #if BS_SHFL_MIRROR
         pol.mirror(q, qm, t, buf, typename G::Pidx{});
 #else
@@ -444,6 +485,7 @@ row_kernel(const RowArgs a) {
         pol.sync();
 #endif
         Engine::run(q, qm, y2, t, buf, a.tw, a.sinp, pol);
+        }
 #pragma unroll
         for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y2[l];
         if constexpr (TOUT) {
@@ -655,8 +697,10 @@ col_kernel(const ColArgs a) {
     const double2 zero = make_double2(0.0, 0.0);
 
     double2 x[P], y[P];
-#if BS_COL_SMEM_MIRROR
-    // the column goes through shared memory; the pre-processing reads x_j and x_{N-j} there
+    // n >= 512: the column goes through shared memory and the pre-processing reads x_j and
+    // x_{N-j} there (no mirror registers); shorter lines keep the register path (measured, r01)
+    constexpr bool CSM = BS_COL_SMEM_MIRROR && LOG2N >= 9;
+    if constexpr (CSM) {
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
@@ -664,8 +708,7 @@ col_kernel(const ColArgs a) {
     }
     pol.sync();
     Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
-#else
-    {
+    } else {
         double2 xm[P];
 #pragma unroll
         for (int mm = 0; mm < P; ++mm) {
@@ -675,7 +718,6 @@ col_kernel(const ColArgs a) {
         }
         Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
     }
-#endif
 
     if constexpr (MODE == C_ONE) {
 #pragma unroll
@@ -705,7 +747,19 @@ col_kernel(const ColArgs a) {
             buf[G::pidx(p)] = v;
         }
         pol.sync();
-        Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
+        if constexpr (CSM) {
+            Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
+        } else {
+            double2 xm[P];
+#pragma unroll
+            for (int mm = 0; mm < P; ++mm) {
+                const int j = t + T * mm;
+                x[mm] = buf[G::pidx(j)];
+                xm[mm] = (j == 0) ? zero : buf[G::pidx(N - j)];
+            }
+            pol.sync();
+            Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
+        }
 #pragma unroll
         for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + qa] = y[l];
     }
