@@ -238,6 +238,11 @@ cudaError_t launch_cdr(int log2n, bool row, int mode, const CdrArgs& a, cudaStre
     BS_SIZE_CASES(launch_cdr_L, row, mode, a, s, prep)
 }
 
+cudaError_t launch_mixed(int log2n, const RowArgs& ra, const ColArgs& ca, cudaStream_t s,
+                         bool prep = false) {
+    BS_SIZE_CASES(launch_mixed_L, ra, ca, s, prep)
+}
+
 cudaError_t launch_row(int log2n, int dim, int mode, const RowArgs& a, cudaStream_t s) {
     return launch_row_pp(log2n, points_per_thread(log2n), dim, mode, a, s);
 }
@@ -256,6 +261,7 @@ cudaError_t prepare_kernels(int log2n, int dim) {
         for (int mode : {C_GREEN, C_FD})
             if (cudaError_t r = launch_transposed(log2n, false, mode, a, c, nullptr, true)) e = r;
     }
+    if (dim == 2) launch_mixed(log2n, a, c, nullptr, true);  // sizes without a mixed kernel: ignored
     if (dim == 2) {
         CdrArgs ca{};
         for (int mode : {RC_FWD, RC_INV, RC_A, RC_B})
@@ -375,6 +381,7 @@ struct bp_problem {
     // graph cache
     cudaGraphExec_t graph = nullptr;
     int graph_map_kind = -1;
+    bool graph_mixed = false;
     int graph_metric = -1;
     double2 graph_gamma{};
     int graph_max_iters = -1;
@@ -455,6 +462,46 @@ ColArgs col_args(const bp_problem* p) {
     c.tw = p->tw;
     c.sinp = p->sinp;
     c.status = nullptr;
+    return c;
+}
+
+// Arguments restricted to members [b0, b0 + nb) of the batch (the half-batches of the mixed
+// pipeline): every per-member array is offset, n_active stays shared.
+RowArgs row_args_range(const RowArgs& a0, const bp_problem* p, int b0, int nb) {
+    RowArgs a = a0;
+    const size_t fo = (size_t)b0 * p->field;
+    a.batch = nb;
+    a.k0sq += b0;
+    a.eta += b0;
+    a.k2 += fo;
+    a.f += fo;
+    a.T += fo;
+    a.u0 += fo;
+    a.u1 += fo;
+    if (a.X) a.X += fo;
+    Control& c = a.ctl;
+    c.status += b0;
+    c.sweep += b0;
+    c.iters += b0;
+    c.term += b0;
+    c.result_buf += b0;
+    c.counter += b0;
+    c.partial += ((size_t)b0 << (p->log2n * (p->dim - 1))) * kPartStride;
+    c.gamma += b0;
+    c.fnorm_l2 += b0;
+    c.fnorm_reta += b0;
+    c.trace_l2 += (size_t)b0 * c.trace_stride;
+    c.trace_reta += (size_t)b0 * c.trace_stride;
+    return a;
+}
+
+ColArgs col_args_range(const ColArgs& c0, const bp_problem* p, int b0, int nb) {
+    ColArgs c = c0;
+    c.batch = nb;
+    c.k0sq += b0;
+    c.eta += b0;
+    c.T += (size_t)b0 * p->field;
+    if (c.status) c.status += b0;
     return c;
 }
 
@@ -664,6 +711,45 @@ int sweep_once(bp_problem* p, const SweepPlan& plan, const RowArgs& a, const Col
     return BP_OK;
 }
 
+// Mixed pipeline (scalar / pointwise maps, 2-D, batch >= 2): the batch is split into halves A
+// and B; one "pipelined sweep" is two mixed launches, [rows(A) + columns(B)] then
+// [columns(A) + rows(B)] (mixed_kernel), so every launch co-runs an HBM-bound row pass with an
+// FP64-bound column pass.  B runs half a sweep behind A; per member the kernel sequence is
+// unchanged.  Opt-in (BP_MIXED=1): measured equal to the two-launch sweep on c1 (619 vs
+// 613 us per sweep, r01) -- both roles are latency-bound per warp, so co-running them on an
+// SM halves each role's warps without freeing a shared resource.
+bool mixed_enabled(const bp_problem* p, const bp_map* map) {
+    const char* e = std::getenv("BP_MIXED");
+    if (!(e && e[0] == '1') || p->dim != 2 || p->batch < 2 || p->transposed || p->periodic || p->cdr || p->slab_log2)
+        return false;
+    if (map->kind != BP_MAP_SCALAR && map->kind != BP_MAP_POINTWISE) return false;
+    return launch_mixed(p->log2n, RowArgs{}, ColArgs{}, nullptr, true) == cudaSuccess;
+}
+
+struct MixedHalves {
+    RowArgs ra, rb;
+    ColArgs ca, cb;
+};
+
+MixedHalves mixed_halves(const bp_problem* p, const RowArgs& a, const ColArgs& c) {
+    const int h = p->batch / 2;
+    ColArgs c2 = c;  // what col_stage sets for a 2-D C_GREEN launch
+    c2.planes_per_member = 1;
+    c2.scale = p->green_scale;
+    return {row_args_range(a, p, 0, h), row_args_range(a, p, h, p->batch - h),
+            col_args_range(c2, p, 0, h), col_args_range(c2, p, h, p->batch - h)};
+}
+
+// one pipelined sweep; ev (optional): 3 events around the two launches
+int mixed_sweep(bp_problem* p, const MixedHalves& mh, cudaEvent_t* ev) {
+    if (ev) CU(cudaEventRecord(ev[0], p->stream));
+    CU(launch_mixed(p->log2n, mh.ra, mh.cb, p->stream));
+    if (ev) CU(cudaEventRecord(ev[1], p->stream));
+    CU(launch_mixed(p->log2n, mh.rb, mh.ca, p->stream));
+    if (ev) CU(cudaEventRecord(ev[2], p->stream));
+    return BP_OK;
+}
+
 // The driver: bp::run over the batch.  f_dev/u0_dev padded device fields already staged.
 int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool have_u0,
              double* snapshots, int n_snap) {
@@ -713,7 +799,12 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         CU(launch_transposed(p->log2n, false, C_GREEN, a, cc, p->stream));
     } else {
         CU(launch_row(p->log2n, p->dim, R_FWD_BORN, a, p->stream));
-        if (int rc2 = col_stage_checked(p, c, C_GREEN, p->green_scale)) return rc2;
+    }
+    const bool mixed = !(snapshots && n_snap > 0) && mixed_enabled(p, map);
+    const MixedHalves mh = mixed ? mixed_halves(p, a, c) : MixedHalves{};
+    if (!p->transposed) {
+        // mixed pipeline: only half A's first column pass here (B's runs in the first launch)
+        if (int rc2 = col_stage_checked(p, mixed ? mh.ca : c, C_GREEN, p->green_scale)) return rc2;
     }
 
     // kernels launched so far in this run: pack f (+ pack u0), 2x norms (2 each), Green
@@ -750,6 +841,35 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             CU(cudaStreamSynchronize(p->stream));
             if (*p->host_active == 0) break;
         }
+    } else if (p->timing && mixed) {
+        // instrumented mixed path: events around each mixed launch (charged to row_ms; the
+        // column work runs inside the same launches)
+        std::vector<cudaEvent_t> ev(3 * kGraphSweeps);
+        for (auto& e : ev) CU(cudaEventCreate(&e));
+        long launched = 0;
+        while (launched < max_launch) {
+            for (int s = 0; s < kGraphSweeps; ++s) {
+                rc = mixed_sweep(p, mh, &ev[3 * s]);
+                if (rc) break;
+            }
+            if (rc) break;
+            launched += kGraphSweeps;
+            p->stat_launches += (int64_t)2 * kGraphSweeps;
+            CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
+                               p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            for (int s = 0; s < kGraphSweeps; ++s) {
+                for (int k = 0; k < 2; ++k) {
+                    float ms = 0;
+                    cudaEventElapsedTime(&ms, ev[3 * s + k], ev[3 * s + k + 1]);
+                    p->stat_row_ms += ms;
+                }
+                ++p->stat_timed;
+            }
+            if (*p->host_active == 0) break;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (rc) return rc;
     } else if (p->timing) {
         // instrumented path: CUDA events around every row / column launch on the handle's
         // stream, polled once per kGraphSweeps sweeps (same cadence as the graph path)
@@ -782,7 +902,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         if (rc) return rc;
     } else {
         // graph of kGraphSweeps sweeps, replayed until every member terminated
-        const bool reuse = p->graph && p->graph_map_kind == map->kind &&
+        const bool reuse = p->graph && p->graph_map_kind == map->kind && p->graph_mixed == mixed &&
                            p->graph_metric == map->metric &&
                            p->graph_gamma.x == map->gamma_re && p->graph_gamma.y == map->gamma_im &&
                            p->graph_max_iters == cfg->max_iters && p->graph_rtol == cfg->rtol;
@@ -791,11 +911,15 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             p->graph = nullptr;
             cudaGraph_t g;
             CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-            for (int s = 0; s < kGraphSweeps; ++s) sweep_once(p, plan, a, c, nullptr);
+            for (int s = 0; s < kGraphSweeps; ++s) {
+                if (mixed) mixed_sweep(p, mh, nullptr);
+                else sweep_once(p, plan, a, c, nullptr);
+            }
             CU(cudaStreamEndCapture(p->stream, &g));
             CU(cudaGraphInstantiate(&p->graph, g, 0));
             cudaGraphDestroy(g);
             p->graph_map_kind = map->kind;
+            p->graph_mixed = mixed;
             p->graph_metric = map->metric;
             p->graph_gamma = a.gamma;
             p->graph_max_iters = cfg->max_iters;

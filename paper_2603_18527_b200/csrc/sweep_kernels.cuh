@@ -27,6 +27,28 @@
 #ifndef BS_ROW_SMEM
 #define BS_ROW_SMEM 1
 #endif
+// element-wise phase of the row kernel: operands (u, k2, f, stencil neighbours) are loaded
+// BS_EW_PD elements ahead of their use, so a warp keeps several row segments in flight
+// instead of waiting one L2 round trip per element (r01 ncu: 65 % of the long-scoreboard
+// stalls were the stencil operands consumed right after their loads)
+#ifndef BS_EW_PD
+#define BS_EW_PD 2
+#endif
+// shared-memory staging of G q / the next source also for single-warp 2-D rows (frees the
+// 64 registers of z[] / q[] for the prefetched operands)
+// register budget of the row kernel (128: 2 CTAs of 8 warps per SM; 85: 3 CTAs)
+#ifndef BS_ROW_REGS
+#define BS_ROW_REGS 128
+#endif
+// column kernels with warp-private engines (col_group_w) for lines of 32 threads (r01:
+// 277 vs 246 us on c1 -- the engines' own stride patterns conflict where the c-fastest map
+// of col_group does not; kept for experiments, off)
+#ifndef BS_COL_WARP
+#define BS_COL_WARP 0
+#endif
+#ifndef BS_RSM_ALL
+#define BS_RSM_ALL 1
+#endif
 
 namespace bs {
 
@@ -232,9 +254,10 @@ struct RowGeom {
 // shared-memory tile (128-B segments), for the warp-per-line column pass tcol_kernel.
 // SLAB: the launch covers one rank's x-slab (RowArgs::slab_log2 / row0 / slab_sums); a separate
 // instantiation so the whole-member path keeps its compile-time indexing.
-template <int LOG2N, int MODE, int NW, int PP, int DIM = 2, bool TOUT = false, bool SLAB = false>
-__global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? 128 : 80>::value))
-row_kernel(const RowArgs a) {
+// One group of EPB lines (the work of one CTA).  `staged`: the group's operands are already
+// in L2 (skip the per-line prefetch).
+template <int LOG2N, int MODE, int NW, int PP, int DIM, bool TOUT, bool SLAB>
+__device__ __forceinline__ void row_group(const RowArgs& a, const long grp, const bool staged) {
     using G = Geom<LOG2N, PP>;
     using RG = RowGeom<LOG2N, PP, NW>;
     using Pol = typename PolicyFor<G::T>::type;
@@ -249,13 +272,32 @@ row_kernel(const RowArgs a) {
 
     const int t = threadIdx.x % T;
     const int e = threadIdx.x / T;
-    const long grow = (long)blockIdx.x * EPB + e;
+    const long grow = grp * EPB + e;
     static_assert(!SLAB || (DIM == 2 && !TOUT), "slabs: 2-D row-major handoff only");
     const int lsh = SLAB ? a.slab_log2 : LLINES;        // log2(lines per member)
     const int b = (int)(grow >> lsh);
     const int i = (int)(grow & ((1L << lsh) - 1));      // line index within the member (slab)
     const int ig = SLAB ? a.row0 + i : i;               // global line index
     bool valid = (b < a.batch) && (ig & (N - 1)) != 0 && (DIM == 2 || (i >> LOG2N) != 0);
+    // shared-memory staging of the inverse transform's input (see RSM below)
+    constexpr bool RSM = BS_ROW_SMEM && (T > 32 || DIM == 3 || (BS_RSM_ALL && S::ITER));
+    // The T line is loaded before the member's status / sweep counter are known (they are
+    // an L2 round trip of their own): the two latencies overlap instead of adding up.  A
+    // terminated member's line is loaded and dropped (16 B/pt, its CTA then exits).
+    double2 xT[(S::INV && RSM) ? P : 1];
+    if constexpr (S::INV && RSM) {
+        const int sl0 = SLAB ? a.slab_log2 : 0;
+        const size_t mem0 = (size_t)(valid ? b : 0) << (lsh + LOG2N);
+        const size_t row0 = mem0 + (size_t)(valid ? i : 0) * N;
+#pragma unroll
+        for (int mm = 0; mm < P; ++mm) {
+            const int j = t + T * mm;
+            size_t ix = row0 + j;
+            if constexpr (SLAB)
+                ix = mem0 + ((size_t)(j >> sl0) << (2 * sl0)) + ((size_t)(valid ? i : 0) << sl0) + (j & ((1 << sl0) - 1));
+            xT[mm] = valid ? a.T[ix] : make_double2(0.0, 0.0);
+        }
+    }
     int m = 0;  // trace entry this launch belongs to
     if (S::ITER && valid) {
         valid = __ldcg(&a.ctl.status[b]) == ST_ACTIVE;
@@ -280,10 +322,12 @@ row_kernel(const RowArgs a) {
     const double eta = valid ? a.eta[b] : 1.0;
     const double2 shift = make_double2(k0sq, eta);
 
+    // Stage the element-wise operands of this row (and the stencil halo rows at the CTA's
+    // edges) into L2 while the transform runs: the loads after the engine then hit L2.
+    // Issued after the T row's own loads so those do not queue behind the prefetches.
+    auto prefetch_row = [&]() {
     if constexpr (S::ITER && MODE != R_RETA_C) {
-        // Stage the element-wise operands of this row (and the stencil halo rows at the CTA's
-        // edges) into L2 while the transform runs: the loads after the engine then hit L2.
-        if (valid && t == 0) {
+        if (valid && t == 0 && !staged) {
             constexpr unsigned RB = N * sizeof(double2);
             prefetch_l2(ucur + row, RB);
             prefetch_l2(a.k2 + row, RB);
@@ -299,11 +343,12 @@ row_kernel(const RowArgs a) {
             if constexpr (MODE == R_OPT_B) prefetch_l2(a.X + row, RB);
         }
     }
+    };
+    if constexpr (!S::INV) prefetch_row();
 
     double acc[S::NPART > 0 ? S::NPART : 1] = {};
     // shared-memory staging pays off for multi-warp lines (n >= 1024) and the 3-D stencil;
     // single-warp 2-D lines keep the register path (measured, r01)
-    constexpr bool RSM = BS_ROW_SMEM && (T > 32 || DIM == 3);
     double2 q[P];                    // register path: source of the forward transform
     double2 z[P];                    // register path: G q
 
@@ -315,11 +360,9 @@ row_kernel(const RowArgs a) {
     if constexpr (S::INV) {
         double2 y[P];
         if constexpr (RSM) {
+            prefetch_row();
 #pragma unroll
-            for (int mm = 0; mm < P; ++mm) {
-                const int j = t + T * mm;
-                buf[G::pidx(j)] = valid ? a.T[tix(j)] : zero;
-            }
+            for (int mm = 0; mm < P; ++mm) buf[G::pidx(t + T * mm)] = valid ? xT[mm] : zero;
             pol.sync();
             {
                 double2 v[P];
@@ -336,6 +379,7 @@ row_kernel(const RowArgs a) {
             x[mm] = valid ? a.T[tix(j)] : zero;
             xm[mm] = (valid && j != 0) ? a.T[tix(N - j)] : zero;  // mirror: L1 hit
         }
+        prefetch_row();
         Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
         for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
@@ -347,9 +391,45 @@ row_kernel(const RowArgs a) {
     }
 
     // ---- element-wise phase
+    // operands of element mm, issued BS_EW_PD elements ahead (iterate modes)
+    struct Opnd {
+        double2 u, k2, f, un, us, uw, ue, ua, ub, x;
+    };
+    constexpr bool PIPE = S::ITER && MODE != R_RETA_C;
+    auto load_op = [&](int mm) {
+        Opnd o;
+        o.u = o.k2 = o.f = o.un = o.us = o.uw = o.ue = o.ua = o.ub = o.x = zero;
+        const int j = t + T * mm;
+        if (valid) {
+            o.u = ucur[row + j];
+            o.k2 = a.k2[row + j];
+            o.f = a.f[row + j];
+            if constexpr (S::ENTRY) {
+                o.un = ucur[row - N + j];
+                o.us = ucur[row + N + j];
+                if (j > 0) o.uw = ucur[row + j - 1];
+                if (j + 1 < N) o.ue = ucur[row + j + 1];
+                if constexpr (DIM == 3) {
+                    o.ua = ucur[row - PLANE + j];
+                    o.ub = ucur[row + PLANE + j];
+                }
+            }
+            if constexpr (MODE == R_OPT_B) o.x = a.X[row + j];
+        }
+        return o;
+    };
+    constexpr int PD = PIPE ? (BS_EW_PD < P ? BS_EW_PD : P) : 0;
+    Opnd ops[P];
+    if constexpr (PIPE) {
+#pragma unroll
+        for (int mm = 0; mm < PD; ++mm) ops[mm] = load_op(mm);
+    }
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
+        if constexpr (PIPE) {
+            if (mm + PD < P) ops[mm + PD] = load_op(mm + PD);
+        }
         const double2 zz = !S::INV ? zero : RSM ? buf[G::pidx(j)] : z[mm];
         double2 qv = zero;
         if constexpr (MODE == R_INV) {
@@ -374,27 +454,13 @@ row_kernel(const RowArgs a) {
                 acc[2] += cnorm(w);
             }
         } else {
-            double2 u = zero, k2 = zero, f = zero;
-            if (valid) {
-                u = ucur[row + j];
-                k2 = a.k2[row + j];
-                f = a.f[row + j];
-            }
+            const Opnd& op = ops[mm];
+            const double2 u = op.u, k2 = op.k2, f = op.f;
             const double2 V = csub(k2, shift);
             if constexpr (S::ENTRY) {
                 // r^m = f - A u^m (five-point in proj/src/kernels.cpp:56-69 order);
                 // x^m = G q^m - u^m = born_residual (problem.cpp:41-49) = G r^m (key identity)
-                double2 un = zero, us = zero, uw = zero, ue = zero, ua = zero, ub = zero;
-                if (valid) {
-                    un = ucur[row - N + j];
-                    us = ucur[row + N + j];
-                    if (j > 0) uw = ucur[row + j - 1];
-                    if (j + 1 < N) ue = ucur[row + j + 1];
-                    if constexpr (DIM == 3) {
-                        ua = ucur[row - PLANE + j];
-                        ub = ucur[row + PLANE + j];
-                    }
-                }
+                const double2 un = op.un, us = op.us, uw = op.uw, ue = op.ue, ua = op.ua, ub = op.ub;
                 const double2 x = csub(zz, u);
                 double2 s;
                 if constexpr (DIM == 3) {
@@ -441,7 +507,7 @@ row_kernel(const RowArgs a) {
                 // R_OPT_B: u' = u + gamma x ; R_FD_B: u' = u + du (du = z)
                 double2 du;
                 if constexpr (MODE == R_OPT_B) {
-                    const double2 x = valid ? a.X[row + j] : zero;
+                    const double2 x = op.x;
                     const double2 g = valid ? a.ctl.gamma[b] : zero;
                     du = cmul(g, x);  // kernels::scale(x, gamma)
                 } else {
@@ -492,7 +558,7 @@ row_kernel(const RowArgs a) {
             static_assert(DIM == 2 && T <= 32, "transposed handoff: 2-D lines of <= 512");
             __syncthreads();
             // tile (EPB rows x N) -> TT[b][q][i]: lanes = 8 consecutive rows x 4 modes
-            const long g0 = (long)blockIdx.x * EPB;
+            const long g0 = grp * EPB;
             for (int k = threadIdx.x; k < EPB * N; k += NW * 32) {
                 const int ee = k % EPB, qq = k / EPB;
                 const long g = g0 + ee;
@@ -555,6 +621,14 @@ row_kernel(const RowArgs a) {
             }
         }
     }
+}
+
+template <int LOG2N, int MODE, int NW, int PP, int DIM = 2, bool TOUT = false, bool SLAB = false>
+__global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? BS_ROW_REGS : 80>::value))
+row_kernel(const RowArgs a) {
+    // (a persistent variant looping over groups with next-group L2 prefetch measured 23-48 %
+    // slower on c1, r01: the hardware's CTA scheduling is kept)
+    row_group<LOG2N, MODE, NW, PP, DIM, TOUT, SLAB>(a, blockIdx.x, false);
 }
 
 // ------------------------------------------------------------------ transposed column kernel
@@ -651,12 +725,107 @@ struct ColGeom {
 //           all-to-all of a slab-decomposed grid (row stride slab_cols, global column col0 + q).
 enum ColLayout { CL_PLANE = 0, CL_X3 = 2, CL_SLAB = 3 };
 
-template <int LOG2N, int MODE, int C, int PP, int LAYOUT = CL_PLANE>
-__global__ void __launch_bounds__(C * Geom<LOG2N, PP>::T, (MinBlocks<C * Geom<LOG2N, PP>::T, PP >= 16 ? 128 : 64>::value))
-col_kernel(const ColArgs a) {
+// Column group with warp-private engines (lines of T <= 32 threads): the CTA stages its C
+// columns into C shared-memory lines with coalesced row-segment loads, each engine (one warp
+// or warp segment) transforms its own line with warp-level sync and shuffle scans (no CTA
+// barriers, no shared-memory scan inside the transforms), and the CTA stores the lines back
+// with the same row-segment pattern.  Two CTA barriers per group in total.
+template <int LOG2N, int MODE, int C, int PP, int LAYOUT>
+__device__ __forceinline__ void col_group_w(const ColArgs& a, const int bid) {
     using G = Geom<LOG2N, PP>;
     using Engine = DstEngine<LOG2N, PP>;
     constexpr int N = G::N, P = G::P, T = G::T;
+    static_assert(T <= 32, "warp-private column engines");
+    constexpr int THREADS = C * T;
+    extern __shared__ double2 smem[];
+    const int e = threadIdx.x / T, t = threadIdx.x % T;  // engine e = column q0 + e
+    constexpr int GROUPS = N / C;
+    int b, yl = 0, qa0;
+    size_t mem;
+    size_t LS = LAYOUT == CL_X3 ? (size_t)N * N : (size_t)N;
+    if constexpr (LAYOUT == CL_SLAB) {
+        const int groups = a.slab_cols / C;
+        b = bid / groups;
+        qa0 = (bid % groups) * C;
+        LS = (size_t)a.slab_cols;
+        mem = (size_t)b * N * a.slab_cols;
+    } else if constexpr (LAYOUT == CL_X3) {
+        const int grp = bid / GROUPS;
+        b = grp >> LOG2N;
+        yl = grp & (N - 1);
+        if (yl == 0) return;
+        mem = ((size_t)b << (3 * LOG2N)) + (size_t)yl * N;
+        qa0 = (bid % GROUPS) * C;
+    } else {
+        const int plane = bid / GROUPS;
+        b = plane / a.planes_per_member;
+        if (a.planes_per_member > 1 && (plane & (N - 1)) == 0) return;
+        mem = (size_t)plane * N * N;
+        qa0 = (bid % GROUPS) * C;
+    }
+    const int q = (LAYOUT == CL_SLAB ? a.col0 : 0) + qa0 + e;  // global column of this engine
+    if (a.status && __ldcg(&a.status[b]) != ST_ACTIVE) return;  // uniform per CTA
+    const double2 zero = make_double2(0.0, 0.0);
+
+    // coalesced staging: consecutive threads = consecutive columns of one row (C*16-B segments);
+    // line stride PAD_N is odd in 16-B units, so the C lines of one row hit distinct banks
+#pragma unroll
+    for (int k0 = 0; k0 < C * N; k0 += THREADS) {
+        const int k = k0 + threadIdx.x, j = k / C, cc = k % C;
+        smem[cc * G::PAD_N + G::pidx(j)] = a.T[mem + (size_t)j * LS + qa0 + cc];
+    }
+    __syncthreads();
+    double2* buf = smem + e * G::PAD_N;
+    const WarpSeg<T> pol{};
+    double2 x[P], y[P];
+    Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
+    if constexpr (MODE == C_ONE) {
+#pragma unroll
+        for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = cscale(y[l], a.scale);
+    } else {
+        const double k0sq = a.k0sq[b], eta = a.eta[b];
+        const double lq = LAYOUT == CL_X3 ? a.lap[yl] + a.lap[q] : a.lap[q];
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+            const int p = t * P + l;
+            // lambda = (a_p + a_q) - (k0^2 + i eta)   (symbol.cpp:69-80 + shift_symbol :97-100)
+            const double lr = (a.lap[p] + lq) - k0sq;
+            const double li = -eta;
+            double2 w;
+            if constexpr (MODE == C_FD) {
+                const size_t fi = LAYOUT == CL_X3 ? ((size_t)p * N + yl) * N + q : (size_t)p * N + q;
+                w = cscale(a.fd[fi], a.scale);
+            } else if constexpr (MODE == C_GREEN) {
+                const double s = a.scale * __drcp_rn(fma(lr, lr, li * li));
+                w = make_double2(lr * s, -li * s);  // scale / lambda
+            } else {
+                w = make_double2(lr * a.scale, li * a.scale);  // scale * lambda
+            }
+            buf[G::pidx(p)] = (p == 0 || q == 0) ? zero : cmul(y[l], w);
+        }
+        pol.sync();
+        Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
+#pragma unroll
+        for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k0 = 0; k0 < C * N; k0 += THREADS) {
+        const int k = k0 + threadIdx.x, j = k / C, cc = k % C;
+        a.T[mem + (size_t)j * LS + qa0 + cc] = smem[cc * G::PAD_N + G::pidx(j)];
+    }
+}
+
+// One CTA's column group (bid = the CTA index of the column launch).
+template <int LOG2N, int MODE, int C, int PP, int LAYOUT>
+__device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
+    using G = Geom<LOG2N, PP>;
+    using Engine = DstEngine<LOG2N, PP>;
+    constexpr int N = G::N, P = G::P, T = G::T;
+    if constexpr (BS_COL_WARP && G::T == 32) {
+        col_group_w<LOG2N, MODE, C, PP, LAYOUT>(a, bid);
+        return;
+    }
     extern __shared__ double2 smem[];
     int c, t;
     col_thread_map<G::T, C>(t, c);
@@ -667,18 +836,18 @@ col_kernel(const ColArgs a) {
     size_t LS = LAYOUT == CL_X3 ? (size_t)N * N : (size_t)N;
     if constexpr (LAYOUT == CL_SLAB) {
         const int groups = a.slab_cols / C;
-        b = blockIdx.x / groups;
-        qa = (blockIdx.x % groups) * C + c;  // column within the block (address)
+        b = bid / groups;
+        qa = (bid % groups) * C + c;  // column within the block (address)
         LS = (size_t)a.slab_cols;
         mem = (size_t)b * N * a.slab_cols;
     } else if constexpr (LAYOUT == CL_X3) {
-        const int grp = blockIdx.x / GROUPS;  // (member, y)
+        const int grp = bid / GROUPS;  // (member, y)
         b = grp >> LOG2N;
         yl = grp & (N - 1);
         if (yl == 0) return;                   // padding y-plane
         mem = ((size_t)b << (3 * LOG2N)) + (size_t)yl * N;
     } else {
-        const int plane = blockIdx.x / GROUPS;
+        const int plane = bid / GROUPS;
         b = plane / a.planes_per_member;
         if (a.planes_per_member > 1 && (plane & (N - 1)) == 0) return;  // padding x-plane (3-D)
         mem = (size_t)plane * N * N;
@@ -687,7 +856,7 @@ col_kernel(const ColArgs a) {
     if constexpr (LAYOUT == CL_SLAB) {
         q = a.col0 + qa;
     } else {
-        q = (blockIdx.x % GROUPS) * C + c;
+        q = (bid % GROUPS) * C + c;
         qa = q;
     }
     if (a.status && __ldcg(&a.status[b]) != ST_ACTIVE) return;  // uniform per CTA
@@ -762,6 +931,43 @@ col_kernel(const ColArgs a) {
         }
 #pragma unroll
         for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + qa] = y[l];
+    }
+}
+
+template <int LOG2N, int MODE, int C, int PP, int LAYOUT = CL_PLANE>
+__global__ void __launch_bounds__(C * Geom<LOG2N, PP>::T, (MinBlocks<C * Geom<LOG2N, PP>::T, PP >= 16 ? 128 : 64>::value))
+col_kernel(const ColArgs a) {
+    col_group<LOG2N, MODE, C, PP, LAYOUT>(a, blockIdx.x);
+}
+
+// ------------------------------------------------------------------ mixed (pipelined) kernel
+// One launch = the fused row pass (R_SWEEP) of one half of the batch AND the column pass
+// (C_GREEN) of the other half, CTAs interleaved 1:1 so every SM co-runs both roles: the row
+// role streams HBM (96 B/pt) while the column role is FP64/issue-bound (32 B/pt), so each
+// fills the other's idle resource.  The halves alternate roles launch by launch (the column
+// half is half a sweep behind); per member the launch sequence is the plain R_SWEEP, C_GREEN
+// alternation, so results are bit-identical to the two-launch sweep.
+template <int LOG2N, int NW, int PP, int C>
+struct MixedGeom {
+    static constexpr int THREADS = NW * 32;
+    static_assert(THREADS == C * Geom<LOG2N, PP>::T, "row and column CTAs of equal size");
+    static constexpr size_t SMEM = RowGeom<LOG2N, PP, NW>::SMEM > ColGeom<LOG2N, PP, C>::SMEM
+                                       ? RowGeom<LOG2N, PP, NW>::SMEM
+                                       : ColGeom<LOG2N, PP, C>::SMEM;
+};
+
+template <int LOG2N, int NW, int PP, int C>
+__global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? 128 : 80>::value))
+mixed_kernel(const RowArgs ra, const ColArgs ca, const int nrow, const int ncol) {
+    const int bid = blockIdx.x;
+    const int m = nrow < ncol ? nrow : ncol;
+    if (bid < 2 * m) {
+        if (bid & 1) col_group<LOG2N, C_GREEN, C, PP, CL_PLANE>(ca, bid >> 1);
+        else row_group<LOG2N, R_SWEEP, NW, PP, 2, false, false>(ra, bid >> 1, false);
+    } else if (nrow > ncol) {
+        row_group<LOG2N, R_SWEEP, NW, PP, 2, false, false>(ra, bid - m, false);
+    } else {
+        col_group<LOG2N, C_GREEN, C, PP, CL_PLANE>(ca, bid - m);
     }
 }
 

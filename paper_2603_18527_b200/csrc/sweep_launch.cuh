@@ -191,6 +191,24 @@ cudaError_t launch_periodic_p(bool row, int mode, const PerArgs& a, cudaStream_t
     }
 }
 
+// ---- mixed launch: R_SWEEP rows of one half-batch + C_GREEN columns of the other (2-D, P = 16)
+template <int L>
+cudaError_t launch_mixed_t(const RowArgs& ra, const ColArgs& ca, cudaStream_t s, bool prepare) {
+    constexpr int C = ColCols<L>::value;
+    if constexpr (kRowWarps * 32 == C * Geom<L, 16>::T) {
+        using MG = MixedGeom<L, kRowWarps, 16, C>;
+        using RG = RowGeom<L, 16, kRowWarps>;
+        auto k = mixed_kernel<L, kRowWarps, 16, C>;
+        if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG::SMEM);
+        const int nrow = (int)((((long)ra.batch << L) + RG::EPB - 1) / RG::EPB);
+        const int ncol = ca.batch * ((1 << L) / C);
+        if (nrow + ncol == 0) return cudaSuccess;
+        k<<<nrow + ncol, MG::THREADS, MG::SMEM, s>>>(ra, ca, nrow, ncol);
+        return cudaGetLastError();
+    }
+    return cudaErrorInvalidValue;
+}
+
 // 3-D kernels exist for n <= 512 (P = 16)
 constexpr int kMaxLog2_3d = 9;
 
@@ -235,6 +253,9 @@ struct Pp8 {
     }                                                                                           \
     cudaError_t launch_cdr_L##L(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep) { \
         return launch_cdr_p<L>(row, mode, a, s, prep);                                          \
+    }                                                                                           \
+    cudaError_t launch_mixed_L##L(const RowArgs& ra, const ColArgs& ca, cudaStream_t s, bool prep) { \
+        return launch_mixed_t<L>(ra, ca, s, prep);                                              \
     }
 
 #define BS_DECLARE_SIZE(L)                                                                      \
@@ -246,7 +267,8 @@ struct Pp8 {
                                      bool prep);                                                \
     cudaError_t launch_transposed_L##L(bool row, int mode, const RowArgs& a, const ColArgs& c,  \
                                        cudaStream_t s, bool prep);                              \
-    cudaError_t launch_cdr_L##L(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep);
+    cudaError_t launch_cdr_L##L(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep); \
+    cudaError_t launch_mixed_L##L(const RowArgs& ra, const ColArgs& ca, cudaStream_t s, bool prep);
 
 BS_DECLARE_SIZE(3)
 BS_DECLARE_SIZE(4)

@@ -412,3 +412,25 @@ def test_transposed_handoff_matches(gpu, monkeypatch):
         assert_run_parity(tr.traces[0], tr.u[0], ref)
         if isinstance(cmap, bs.PointwiseMap):
             assert rel(tr.u, base.u) < 1e-13
+
+
+@pytest.mark.parametrize("n", [512, 1024])
+def test_mixed_pipeline_matches(gpu, monkeypatch, n):
+    """The opt-in mixed pipeline (BP_MIXED=1: one launch = rows of one half-batch + columns of
+    the other) gives the same members, traces and termination sweeps; an odd batch
+    makes the halves unequal (1 + 2 members)."""
+    k2, f, k0, eta = instance(n, batch=3, ppw=60.0, contrast=0.1, seed=11)
+    f[2] *= -1e2
+    cfg = bs.IterationConfig(rtol=1e-5, max_iters=300)
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        base = bs.run(p, bs.PointwiseMap(), f, cfg)
+    monkeypatch.setenv("BP_MIXED", "1")
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        mixed = bs.run(p, bs.PointwiseMap(), f, cfg)
+    for b in range(3):
+        assert mixed.traces[b].iters == base.traces[b].iters
+        assert mixed.traces[b].terminated == base.traces[b].terminated
+        # same arithmetic; the mixed kernel is a separate compilation (FMA contraction may
+        # differ), so roundoff-level agreement rather than bit identity
+        assert rel(mixed.u[b], base.u[b]) < 1e-12
+        assert np.allclose(mixed.traces[b].res_l2_rel, base.traces[b].res_l2_rel, rtol=1e-10, atol=0)

@@ -13,7 +13,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 agg, sass, fn_tot = {}, [], {}
 cur_file, cur_fn, cur_line = "", "", ""
 for r in csv.reader(io.StringIO(out)):
-    if not r:
+    if len(r) < 2:
         continue
     if r[0] == "File Path":
         cur_file = r[1].split("/")[-1]
