@@ -37,6 +37,8 @@ int set_err(int code, const std::string& msg) {
 
 constexpr int kGraphSweeps = 16;
 constexpr double kPi = 3.14159265358979323846;
+// sinp table: 2 sin(pi j/n) for the table-driven engine (BS_TW_TABLE), sin(pi j/n) otherwise
+constexpr double kSinScale = BS_TW_TABLE ? 2.0 : 1.0;
 constexpr double kSymbolDivGuard = 1e-14;  // proj/include/bp/symbol.hpp:24
 
 // ------------------------------------------------------------------ small kernels
@@ -1567,7 +1569,7 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     for (int k = 0; k < n; ++k) {
         tw[2 * k] = std::cos(2.0 * kPi * k / n);
         tw[2 * k + 1] = -std::sin(2.0 * kPi * k / n);
-        sinp[k] = std::sin(kPi * k / n);
+        sinp[k] = kSinScale * std::sin(kPi * k / n);
     }
     CUF(cudaMemcpyAsync(p->k0sq, k0sq.data(), sizeof(double) * batch, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->eta, eta, sizeof(double) * batch, cudaMemcpyHostToDevice, p->stream));
@@ -1851,7 +1853,7 @@ int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const doub
     for (int k = 0; k < n; ++k) {
         tw[2 * k] = std::cos(2.0 * kPi * k / n);
         tw[2 * k + 1] = -std::sin(2.0 * kPi * k / n);
-        sinp[k] = std::sin(kPi * k / n);
+        sinp[k] = kSinScale * std::sin(kPi * k / n);
     }
     const double k0sq = k0 * k0;
     CUF(cudaMemcpyAsync(p->k0sq, &k0sq, sizeof(double), cudaMemcpyHostToDevice, p->stream));

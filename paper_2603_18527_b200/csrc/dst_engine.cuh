@@ -26,6 +26,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Opt-in (measured slower, r01: c1 row 463 vs 365 us, c4 +13 %): twiddles and the
+// pre-processing sines read from the device tables (tw, sinp: L1-resident,
+// one load each) instead of being built by in-register complex multiplications: r01 ncu showed
+// FP64 as the binding pipe, and the multiplication chains also serialised each butterfly.
+#ifndef BS_TW_TABLE
+#define BS_TW_TABLE 0
+#endif
+
 namespace bs {
 
 constexpr double kEngineGain = 4.0;  // each engine pass returns 4 x the plain sine sum
@@ -366,7 +374,13 @@ struct DstEngine {
                 const int jm = jj % NS;
                 // exp(-2 pi i jm r / (NS R)) = w^r with w = tw[jm N/(NS R)]: one load per butterfly
                 double2 pw[R];
+#if BS_TW_TABLE
+                pw[0] = make_double2(1.0, 0.0);
+#pragma unroll
+                for (int r = 1; r < R; ++r) pw[r] = __ldg(&tw[jm * r * (N / (NS * R))]);
+#else
                 twiddle_powers<R>(__ldg(&tw[jm * (N / (NS * R))]), pw);
+#endif
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     double2 x = buf[G::pidx(jj + r * STRIDE_IN)];
@@ -398,6 +412,22 @@ struct DstEngine {
         const double2 d = csub(x, xm);
         return make_double2(fma(s, a.x, d.x), fma(s, a.y, d.y));
     }
+    // same with s = 2 sin(pi j/N) given
+    __device__ __forceinline__ static double2 pre_s(double2 x, double2 xm, double s) {
+        const double2 a = cadd(x, xm);
+        const double2 d = csub(x, xm);
+        return make_double2(fma(s, a.x, d.x), fma(s, a.y, d.y));
+    }
+    // 2 sin(pi j/N) for j = t + T m (sinp holds 2 sin(pi j/N), j < N)
+    __device__ __forceinline__ static double sin2(const double* __restrict__ sinp, int t, int m, double st,
+                                                  double ct) {
+#if BS_TW_TABLE
+        return __ldg(&sinp[t + T * m]);
+#else
+        constexpr int STEP = 16 / P;
+        return fma(st, kCS16[m * STEP].c, ct * kCS16[m * STEP].s);
+#endif
+    }
 
     template <class Pol>
     __device__ __forceinline__ static void run(const double2 (&x)[P], const double2 (&xm)[P], double2 (&y)[P],
@@ -407,11 +437,11 @@ struct DstEngine {
         double2 v[P];
         // 2 sin(pi t/N), 2 cos(pi t/N): the engine computes 4x the sine sum (the 1/2 factors
         // of pre- and post-processing are folded into the caller's scale, exact powers of 2)
-        const double st = 2.0 * __ldg(&sinp[t]), ct = 2.0 * __ldg(&sinp[t + H]);
+        const double st = BS_TW_TABLE ? 0.0 : 2.0 * __ldg(&sinp[t]), ct = BS_TW_TABLE ? 0.0 : 2.0 * __ldg(&sinp[t + H]);
 #pragma unroll
         for (int m = 0; m < P; ++m) {
             const int j = t + T * m;
-            v[m] = (j == 0) ? make_double2(0.0, 0.0) : pre(x[m], xm[m], m, st, ct);
+            v[m] = (j == 0) ? make_double2(0.0, 0.0) : pre_s(x[m], xm[m], sin2(sinp, t, m, st, ct));
         }
         transform(v, y, t, buf, tw, pol);
     }
@@ -423,13 +453,13 @@ struct DstEngine {
     __device__ __forceinline__ static void run_smem(double2 (&v)[P], double2 (&y)[P], int t, double2* buf,
                                                     const double2* __restrict__ tw,
                                                     const double* __restrict__ sinp, const Pol& pol) {
-        const double st = 2.0 * __ldg(&sinp[t]), ct = 2.0 * __ldg(&sinp[t + H]);
+        const double st = BS_TW_TABLE ? 0.0 : 2.0 * __ldg(&sinp[t]), ct = BS_TW_TABLE ? 0.0 : 2.0 * __ldg(&sinp[t + H]);
 #pragma unroll
         for (int m = 0; m < P; ++m) {
             const int j = t + T * m;
             const double2 x = buf[G::pidx(j)];
             const double2 xm = buf[G::pidx((N - j) & (N - 1))];
-            v[m] = (j == 0) ? make_double2(0.0, 0.0) : pre(x, xm, m, st, ct);
+            v[m] = (j == 0) ? make_double2(0.0, 0.0) : pre_s(x, xm, sin2(sinp, t, m, st, ct));
         }
         pol.sync();
         transform(v, y, t, buf, tw, pol);
@@ -451,12 +481,18 @@ struct DstEngine {
         // --- fused final radix-2 pass + DST-I post-processing + prefix sum
         constexpr int K = P / 2;  // k values per thread: k = t*K + i
         double2 ev[K], od[K];     // Y_2k and S_k
+#if !BS_TW_TABLE
         const double2 w0 = __ldg(&tw[t * K]), w1 = __ldg(&tw[1]);
         double2 w = w0;           // exp(-2 pi i k/N), stepped by exp(-2 pi i/N)
+#endif
 #pragma unroll
         for (int i = 0; i < K; ++i) {
             const int k = t * K + i;
+#if BS_TW_TABLE
+            const double2 w = __ldg(&tw[k]);
+#else
             if (i > 0) w = cmul(w, w1);
+#endif
             const double2 a = buf[G::pidx(k)];
             const double2 b = cmul(buf[G::pidx(k + H)], w);
             const double2 Wk = cadd(a, b);

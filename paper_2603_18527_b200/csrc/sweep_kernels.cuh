@@ -160,6 +160,24 @@ struct ColArgs {
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
 
+// 1/x for the Green weights (x = |lambda|^2 > 0): hardware approximation + two Newton steps
+// (quadratic: ~2^-22 -> 2^-88), branch-free; __drcp_rn adds a correctly-rounded fix-up path.
+#ifndef BS_FAST_RCP
+#define BS_FAST_RCP 1
+#endif
+__device__ __forceinline__ double rcp_green(double x) {
+#if BS_FAST_RCP
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+#else
+    return __drcp_rn(x);
+#endif
+}
+
 // TMA bulk prefetch of a contiguous range into L2 (sm_90+: cp.async.bulk.prefetch.L2).
 // bytes: multiple of 16, address 16-B aligned.  Fire-and-forget, no registers held.
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
@@ -680,7 +698,7 @@ tcol_kernel(const ColArgs a) {
             } else {  // C_GREEN: scale / lambda, lambda = (a_p + a_q) - (k0^2 + i eta)
                 const double lr = (a.lap[p] + lq) - k0sq;
                 const double li = -eta;
-                const double s = a.scale * __drcp_rn(fma(lr, lr, li * li));
+                const double s = a.scale * rcp_green(fma(lr, lr, li * li));
                 w = make_double2(lr * s, -li * s);
             }
             y[l] = (p == 0 || q == 0) ? zero : cmul(y[l], w);
@@ -796,7 +814,7 @@ __device__ __forceinline__ void col_group_w(const ColArgs& a, const int bid) {
                 const size_t fi = LAYOUT == CL_X3 ? ((size_t)p * N + yl) * N + q : (size_t)p * N + q;
                 w = cscale(a.fd[fi], a.scale);
             } else if constexpr (MODE == C_GREEN) {
-                const double s = a.scale * __drcp_rn(fma(lr, lr, li * li));
+                const double s = a.scale * rcp_green(fma(lr, lr, li * li));
                 w = make_double2(lr * s, -li * s);  // scale / lambda
             } else {
                 w = make_double2(lr * a.scale, li * a.scale);  // scale * lambda
@@ -907,7 +925,7 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
                 const size_t fi = LAYOUT == CL_X3 ? ((size_t)p * N + yl) * N + q : (size_t)p * N + q;
                 w = cscale(a.fd[fi], a.scale);
             } else if constexpr (MODE == C_GREEN) {
-                const double s = a.scale * __drcp_rn(fma(lr, lr, li * li));
+                const double s = a.scale * rcp_green(fma(lr, lr, li * li));
                 w = make_double2(lr * s, -li * s);  // scale / lambda
             } else {
                 w = make_double2(lr * a.scale, li * a.scale);  // scale * lambda
