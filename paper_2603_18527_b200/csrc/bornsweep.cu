@@ -808,6 +808,16 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         // mixed pipeline: only half A's first column pass here (B's runs in the first launch)
         if (int rc2 = col_stage_checked(p, mixed ? mh.ca : c, C_GREEN, p->green_scale)) return rc2;
     }
+    // scalar / pointwise 2-D sweeps: the column pass finalises the entry the row pass before
+    // it reduced (RowArgs::defer_final / ColArgs::finalize); not for the initial column pass
+    // (n >= 64: the column CTA has at least one full warp for finalize_member's shuffles)
+    if (!mixed && !p->transposed && p->dim == 2 && p->log2n >= 6 && plan.n == 2 && plan.row[0] &&
+        plan.mode[0] == R_SWEEP && !plan.row[1] && plan.mode[1] == C_GREEN) {
+        a.defer_final = 1;
+        c.finalize = 1;
+        c.fin_lsh = p->log2n;
+        c.ctl = a.ctl;
+    }
 
     // kernels launched so far in this run: pack f (+ pack u0), 2x norms (2 each), Green
     // (2 row + column stage), init_control, 2x fill_nan, initial row pass + column stage

@@ -138,6 +138,10 @@ struct RowArgs {
     int slab_log2;
     int row0;
     double* slab_sums;
+    // R_SWEEP (2-D whole members): store the per-row partials only; the NEXT launch (the
+    // column pass, ColArgs::finalize) sums them and records entry m -- no fence / atomic /
+    // last-row wait at the end of every row (r01 ncu: ~13 % of the long-scoreboard stalls)
+    int defer_final;
 };
 
 struct ColArgs {
@@ -155,6 +159,12 @@ struct ColArgs {
     int planes_per_member;     // CL_PLANE: 1 (2-D) or n (3-D y-lines)
     int slab_cols;             // CL_SLAB: columns held by this rank (n x slab_cols block, row stride slab_cols)
     int col0;                  // CL_SLAB: global index of the first of them
+    // finalize != 0 (2-D CL_PLANE): the first CTA of each member sums the per-row partials of
+    // the preceding R_SWEEP launch (RowArgs::defer_final) and records its trace entry +
+    // termination test (finalize_entry); ctl as in RowArgs, log2 rows per member = fin_lsh
+    int finalize;
+    int fin_lsh;
+    Control ctl;
 };
 
 // ------------------------------------------------------------------ helpers
@@ -599,6 +609,16 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     if constexpr (S::NPART > 0) {
 #pragma unroll
         for (int k = 0; k < S::NPART; ++k) acc[k] = pol.sum(acc[k], t);
+        if constexpr (MODE == R_SWEEP && !SLAB) {
+            if (a.defer_final) {  // finalised by the next launch (col_group, ColArgs::finalize)
+                if (valid && t == 0) {
+                    double* pr = a.ctl.partial + (((size_t)b << lsh) + i) * kPartStride;
+#pragma unroll
+                    for (int k = 0; k < S::NPART; ++k) pr[k] = acc[k];
+                }
+                return;
+            }
+        }
         int last = 0;
         if (valid && t == 0) {
             double* pr = a.ctl.partial + (((size_t)b << lsh) + i) * kPartStride;
@@ -743,6 +763,28 @@ struct ColGeom {
 //           all-to-all of a slab-decomposed grid (row stride slab_cols, global column col0 + q).
 enum ColLayout { CL_PLANE = 0, CL_X3 = 2, CL_SLAB = 3 };
 
+// Deferred finalisation of trace entry m for member b (ColArgs::finalize): one warp sums the
+// per-row partials of the preceding R_SWEEP launch in the row kernel's own order (lane r over
+// rows r, r+32, ...; xor-shuffle tree) and runs finalize_entry.  Visibility of the partials
+// is given by the launch boundary.
+__device__ __forceinline__ void finalize_member(const ColArgs& a, int b, int nlines) {
+    const int lane = threadIdx.x & 31;
+    const int m = __ldcg(&a.ctl.sweep[b]);
+    double s0 = 0.0, s1 = 0.0;
+    const double* base = a.ctl.partial + ((size_t)b << a.fin_lsh) * kPartStride;
+    for (int r = lane; r < nlines; r += 32) {
+        if (r == 0) continue;  // Dirichlet padding line
+        s0 += __ldcg(base + (size_t)r * kPartStride);
+        s1 += __ldcg(base + (size_t)r * kPartStride + 1);
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, d);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, d);
+    }
+    if (lane == 0) finalize_entry(a.ctl, b, m, s0, s1);
+}
+
 // Column group with warp-private engines (lines of T <= 32 threads): the CTA stages its C
 // columns into C shared-memory lines with coalesced row-segment loads, each engine (one warp
 // or warp segment) transforms its own line with warp-level sync and shuffle scans (no CTA
@@ -782,7 +824,14 @@ __device__ __forceinline__ void col_group_w(const ColArgs& a, const int bid) {
         qa0 = (bid % GROUPS) * C;
     }
     const int q = (LAYOUT == CL_SLAB ? a.col0 : 0) + qa0 + e;  // global column of this engine
-    if (a.status && __ldcg(&a.status[b]) != ST_ACTIVE) return;  // uniform per CTA
+    if (a.status) {
+        const bool active = __ldcg(&a.status[b]) == ST_ACTIVE;  // read before finalising
+        if constexpr (LAYOUT == CL_PLANE) {
+            if (a.finalize && active && a.planes_per_member == 1 && (bid % GROUPS) == 0 && threadIdx.x < 32)
+                finalize_member(a, b, 1 << a.fin_lsh);
+        }
+        if (!active) return;  // uniform per CTA
+    }
     const double2 zero = make_double2(0.0, 0.0);
 
     // coalesced staging: consecutive threads = consecutive columns of one row (C*16-B segments);
@@ -877,7 +926,14 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
         q = (bid % GROUPS) * C + c;
         qa = q;
     }
-    if (a.status && __ldcg(&a.status[b]) != ST_ACTIVE) return;  // uniform per CTA
+    if (a.status) {
+        const bool active = __ldcg(&a.status[b]) == ST_ACTIVE;  // read before finalising
+        if constexpr (LAYOUT == CL_PLANE) {
+            if (a.finalize && active && a.planes_per_member == 1 && (bid % GROUPS) == 0 && threadIdx.x < 32)
+                finalize_member(a, b, 1 << a.fin_lsh);
+        }
+        if (!active) return;  // uniform per CTA
+    }
 
     double2* buf = smem + c * G::PAD_N;
     const BlockSeg<T, C> pol{smem + C * G::PAD_N, c};
