@@ -112,8 +112,15 @@ class ClockSampler:
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        pw = []
+        for r in self.rows:
+            try:
+                pw.append(float(r[2]))
+            except ValueError:
+                pass
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "power_w": float(np.median(pw)) if pw else None,
                 "reasons": reasons, "samples": len(self.rows)}
 
 

@@ -323,7 +323,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
             size_t ix = row0 + j;
             if constexpr (SLAB)
                 ix = mem0 + ((size_t)(j >> sl0) << (2 * sl0)) + ((size_t)(valid ? i : 0) << sl0) + (j & ((1 << sl0) - 1));
-            xT[mm] = valid ? a.T[ix] : make_double2(0.0, 0.0);
+            xT[mm] = a.T[ix];  // in bounds for every thread (mem0/row0 clamped)
         }
     }
     int m = 0;  // trace entry this launch belongs to
@@ -335,8 +335,12 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
 
     double2* buf = smem + e * G::PAD_N;
     const Pol pol = make_policy((Pol*)nullptr, smem + EPB * G::PAD_N, e);
+    // invalid lines (padding, inactive, past the batch) are clamped to a line whose stencil
+    // neighbours are in bounds, so the element-wise loads need no predicates or zero fills;
+    // their results are never stored or summed
+    constexpr int ISAFE = SLAB ? 0 : (DIM == 3 ? N + 1 : 1);
     const size_t mem = (size_t)(valid ? b : 0) << (lsh + LOG2N);
-    const size_t row = mem + (size_t)(valid ? i : 0) * N;
+    const size_t row = mem + (size_t)(valid ? i : ISAFE) * N;
     // T element (this line, column j): row-major, or blocked by destination rank on a slab
     const int sl = SLAB ? a.slab_log2 : 0;
     auto tix = [&](int j) -> size_t {
@@ -390,7 +394,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         if constexpr (RSM) {
             prefetch_row();
 #pragma unroll
-            for (int mm = 0; mm < P; ++mm) buf[G::pidx(t + T * mm)] = valid ? xT[mm] : zero;
+            for (int mm = 0; mm < P; ++mm) buf[G::pidx(t + T * mm)] = xT[mm];  // invalid lines: discarded
             pol.sync();
             {
                 double2 v[P];
@@ -425,25 +429,26 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     };
     constexpr bool PIPE = S::ITER && MODE != R_RETA_C;
     auto load_op = [&](int mm) {
+        // unpredicated: `row` is clamped for invalid lines; uw at j = 0 reads the previous
+        // line's last element (its result is discarded: j = 0 is the Dirichlet node) and ue at
+        // j = n-1 reads the next line's zero node (the five-point zero halo, as before)
         Opnd o;
-        o.u = o.k2 = o.f = o.un = o.us = o.uw = o.ue = o.ua = o.ub = o.x = zero;
+        o.un = o.us = o.uw = o.ue = o.ua = o.ub = o.x = zero;
         const int j = t + T * mm;
-        if (valid) {
-            o.u = ucur[row + j];
-            o.k2 = a.k2[row + j];
-            o.f = a.f[row + j];
-            if constexpr (S::ENTRY) {
-                o.un = ucur[row - N + j];
-                o.us = ucur[row + N + j];
-                if (j > 0) o.uw = ucur[row + j - 1];
-                if (j + 1 < N) o.ue = ucur[row + j + 1];
-                if constexpr (DIM == 3) {
-                    o.ua = ucur[row - PLANE + j];
-                    o.ub = ucur[row + PLANE + j];
-                }
+        o.u = ucur[row + j];
+        o.k2 = a.k2[row + j];
+        o.f = a.f[row + j];
+        if constexpr (S::ENTRY) {
+            o.un = ucur[row - N + j];
+            o.us = ucur[row + N + j];
+            o.uw = ucur[row + j - 1];
+            o.ue = ucur[row + j + 1];
+            if constexpr (DIM == 3) {
+                o.ua = ucur[row - PLANE + j];
+                o.ub = ucur[row + PLANE + j];
             }
-            if constexpr (MODE == R_OPT_B) o.x = a.X[row + j];
         }
+        if constexpr (MODE == R_OPT_B) o.x = a.X[row + j];
         return o;
     };
     constexpr int PD = PIPE ? (BS_EW_PD < P ? BS_EW_PD : P) : 0;

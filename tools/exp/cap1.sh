@@ -1,0 +1,4 @@
+for v in main twtab; do
+  if [ $v = main ]; then export BP_LIB_PATH=; else export BP_LIB_PATH=variants/$v/libbornsweep.so; fi
+  python bench.py --no-cpu --steps 40 --warmup 3 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['value'],3), d['clocks'], round(d['roofline']['avg_launch_ms'],4), round(d['roofline']['column_kernel']['avg_launch_ms'],4))"
+done
