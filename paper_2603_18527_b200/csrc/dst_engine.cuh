@@ -162,6 +162,26 @@ struct Geom {
     struct Pidx {
         __device__ __forceinline__ int operator()(int i) const { return pidx(i); }
     };
+    // Split addressing: pidx(x + k) = pidx(x) + pidx(k) whenever 8 | k and (x mod 64) +
+    // (k mod 64) < 64.  With the per-thread base px = pidx(x) computed once and k a constant
+    // of an unrolled loop, every access becomes [base + immediate] (the compiler cannot prove
+    // the split itself and otherwise recomputes i + i/8 + i/64 per access: ~10 % of all
+    // instructions, r01 ncu).  x64max: an upper bound of x mod 64 over the threads; both
+    // branches compute the same index, the condition folds at compile time.
+    __device__ __forceinline__ static int padd(int x, int px, int x64max, int k) {
+        return ((k & 7) == 0 && (k & 63) + x64max < 64) ? px + pidx(k) : pidx(x + k);
+    }
+    // pidx(x + r) for x = 0 mod 8, (x mod 64) + r < 64 (block layout t*P + r, P in {8, 16})
+    __device__ __forceinline__ static int psmall(int px, int r) { return px + r + (r >> 3); }
+    static constexpr int TM64 = (T < 64 ? T : 64) - 1;  // bound of t mod 64, t < T
+    // element t + T m of the stride layout (bt = pidx(t))
+    __device__ __forceinline__ static int at_stride(int t, int bt, int m) {
+        return T >= 8 ? padd(t, bt, TM64, T * m) : pidx(t + T * m);
+    }
+    // element t P + l of the block layout (bp = pidx(t P))
+    __device__ __forceinline__ static int at_block(int t, int bp, int l) {
+        return (P == 8 || P == 16) ? psmall(bp, l) : pidx(t * P + l);
+    }
 };
 
 // Stockham pass list: product of radices == N/2; first radix == P; radices <= P.
@@ -370,6 +390,7 @@ struct DstEngine {
             constexpr int V = P / R;  // butterflies per thread
             constexpr int STRIDE_IN = N / R;
             double2 v[P];
+            const int bt = G::pidx(t);
 #pragma unroll
             for (int b = 0; b < V; ++b) {
                 const int jj = t + T * b;
@@ -385,19 +406,27 @@ struct DstEngine {
 #endif
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    double2 x = buf[G::pidx(jj + r * STRIDE_IN)];
+                    // jj + r STRIDE_IN = t + (T b + r STRIDE_IN), a multiple of T added
+                    double2 x = buf[G::at_stride(t, bt, b + r * (STRIDE_IN / T))];
                     if (r > 0) x = cmul(x, pw[r]);
                     v[b * R + r] = x;
                 }
                 Dft<R>::template run<1>(&v[b * R]);
             }
             pol.sync();
+            // write index base(b) + r NS with base(b) = (jj/NS) NS R + jj%NS, jj = t + T b:
+            // = wt + K(b) for the per-thread wt below (t < T, T and NS powers of 2)
+            constexpr int Q = NS > T ? NS / T : 1;
+            const int wt = NS <= T ? (t / NS) * NS * R + t % NS : t;
+            const int pwt = G::pidx(wt);
+            // bound of wt mod 64 over t < T
+            constexpr int W64 = NS <= T ? ((NS * R) % 64 == 0 ? (NS < 64 ? NS : 64) - 1 : 63)
+                                        : G::TM64;
 #pragma unroll
             for (int b = 0; b < V; ++b) {
-                const int jj = t + T * b;
-                const int base = (jj / NS) * NS * R + (jj % NS);
+                const int kb = NS <= T ? T * R * b : (b / Q) * NS * R + T * (b % Q);
 #pragma unroll
-                for (int r = 0; r < R; ++r) buf[G::pidx(base + r * NS)] = v[b * R + r];
+                for (int r = 0; r < R; ++r) buf[G::padd(wt, pwt, W64, kb + r * NS)] = v[b * R + r];
             }
             pol.sync();
         }
@@ -456,11 +485,15 @@ struct DstEngine {
                                                     const double2* __restrict__ tw,
                                                     const double* __restrict__ sinp, const Pol& pol) {
         const double st = BS_TW_TABLE ? 0.0 : 2.0 * __ldg(&sinp[t]), ct = BS_TW_TABLE ? 0.0 : 2.0 * __ldg(&sinp[t + H]);
+        // x_{N-j}, j = t + T m: (T - t) + T (P-1-m) for t > 0; T (P-m) (its own slot P-m)
+        // for t = 0 (the split needs T - t < T, so lane 0 takes a direct constant index)
+        const int bt = G::pidx(t), tm = (T - t) & (T - 1), btm = G::pidx(tm);
 #pragma unroll
         for (int m = 0; m < P; ++m) {
             const int j = t + T * m;
-            const double2 x = buf[G::pidx(j)];
-            const double2 xm = buf[G::pidx((N - j) & (N - 1))];
+            const double2 x = buf[G::at_stride(t, bt, m)];
+            const int mi = t == 0 ? G::pidx((N - T * m) & (N - 1)) : G::at_stride(tm, btm, P - 1 - m);
+            const double2 xm = buf[mi];
             v[m] = (j == 0) ? make_double2(0.0, 0.0) : pre_s(x, xm, sin2(sinp, t, m, st, ct));
         }
         pol.sync();
@@ -472,8 +505,9 @@ struct DstEngine {
     __device__ __forceinline__ static void transform(double2 (&v)[P], double2 (&y)[P], int t, double2* buf,
                                                      const double2* __restrict__ tw, const Pol& pol) {
         Dft<P>::template run<1>(v);
+        const int bp = G::pidx(t * P);
 #pragma unroll
-        for (int r = 0; r < P; ++r) buf[G::pidx(t * P + r)] = v[r];
+        for (int r = 0; r < P; ++r) buf[G::at_block(t, bp, r)] = v[r];
         pol.sync();
         // --- remaining passes up to length N/2 (radix-2 last pass fused below)
         pass<PS::R2, P>(buf, t, tw, pol);
@@ -483,6 +517,11 @@ struct DstEngine {
         // --- fused final radix-2 pass + DST-I post-processing + prefix sum
         constexpr int K = P / 2;  // k values per thread: k = t*K + i
         double2 ev[K], od[K];     // Y_2k and S_k
+        // split bases (K = 8): k = 8t + i -> pidx(8t) + i; H - k, N - k -> pidx(H - 8t) for
+        // i = 0, pidx(H - 8t - 8) + 8 - i otherwise (same for N); H a multiple of 64 (N >= 128)
+        constexpr bool KS = K == 8 && H % 64 == 0;
+        const int pk = G::pidx(t * K), ph0 = G::pidx(H - t * K), ph1 = G::pidx(H - t * K - K);
+        const int pn0 = G::pidx((N - t * K) & (N - 1)), pn1 = G::pidx(N - t * K - K);
 #if !BS_TW_TABLE
         const double2 w0 = __ldg(&tw[t * K]), w1 = __ldg(&tw[1]);
         double2 w = w0;           // exp(-2 pi i k/N), stepped by exp(-2 pi i/N)
@@ -495,16 +534,16 @@ struct DstEngine {
 #else
             if (i > 0) w = cmul(w, w1);
 #endif
-            const double2 a = buf[G::pidx(k)];
-            const double2 b = cmul(buf[G::pidx(k + H)], w);
+            const double2 a = buf[KS ? pk + i : G::pidx(k)];
+            const double2 b = cmul(buf[KS ? pk + i + G::pidx(H) : G::pidx(k + H)], w);
             const double2 Wk = cadd(a, b);
             if (k == 0) {
                 ev[i] = make_double2(0.0, 0.0);
                 od[i] = Wk;
             } else {
                 // W_{N-k} = a_{H-k} - w^{H-k} b_{H-k},  w^{H-k} = -conj(w^k)
-                const double2 a2 = buf[G::pidx(H - k)];
-                const double2 b2 = buf[G::pidx(N - k)];
+                const double2 a2 = buf[KS ? (i == 0 ? ph0 : ph1 + K - i) : G::pidx(H - k)];
+                const double2 b2 = buf[KS ? (i == 0 ? pn0 : pn1 + K - i) : G::pidx(N - k)];
                 const double2 Wnk = cadd(a2, cmul(b2, cconj(w)));
                 const double2 dif = csub(Wk, Wnk);
                 ev[i] = make_double2(-dif.y, dif.x);  // i (Wk - Wnk)

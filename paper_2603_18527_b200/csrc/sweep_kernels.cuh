@@ -394,14 +394,14 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         if constexpr (RSM) {
             prefetch_row();
 #pragma unroll
-            for (int mm = 0; mm < P; ++mm) buf[G::pidx(t + T * mm)] = xT[mm];  // invalid lines: discarded
+            for (int mm = 0; mm < P; ++mm) buf[G::at_stride(t, G::pidx(t), mm)] = xT[mm];  // invalid lines: discarded
             pol.sync();
             {
                 double2 v[P];
                 Engine::run_smem(v, y, t, buf, a.tw, a.sinp, pol);
             }
 #pragma unroll
-            for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
+            for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y[l];
             pol.sync();
         } else {
         double2 x[P], xm[P];
@@ -414,10 +414,10 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         prefetch_row();
         Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
-        for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
+        for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y[l];
         pol.sync();
 #pragma unroll
-        for (int mm = 0; mm < P; ++mm) z[mm] = buf[G::pidx(t + T * mm)];
+        for (int mm = 0; mm < P; ++mm) z[mm] = buf[G::at_stride(t, G::pidx(t), mm)];
         pol.sync();
         }
     }
@@ -463,7 +463,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         if constexpr (PIPE) {
             if (mm + PD < P) ops[mm + PD] = load_op(mm + PD);
         }
-        const double2 zz = !S::INV ? zero : RSM ? buf[G::pidx(j)] : z[mm];
+        const double2 zz = !S::INV ? zero : RSM ? buf[G::at_stride(t, G::pidx(t), mm)] : z[mm];
         double2 qv = zero;
         if constexpr (MODE == R_INV) {
             double2 o = zz;
@@ -553,7 +553,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
             }
         }
         if constexpr (S::FWD) {
-            if constexpr (RSM) buf[G::pidx(j)] = qv;  // the slot this thread read G q from
+            if constexpr (RSM) buf[G::at_stride(t, G::pidx(t), mm)] = qv;  // the slot this thread read G q from
             else q[mm] = qv;
         }
     }
@@ -574,7 +574,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         pol.mirror(q, qm, t, buf, typename G::Pidx{});
 #else
 #pragma unroll
-        for (int mm = 0; mm < P; ++mm) buf[G::pidx(t + T * mm)] = q[mm];
+        for (int mm = 0; mm < P; ++mm) buf[G::at_stride(t, G::pidx(t), mm)] = q[mm];
         pol.sync();
 #pragma unroll
         for (int mm = 0; mm < P; ++mm) {
@@ -586,7 +586,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         Engine::run(q, qm, y2, t, buf, a.tw, a.sinp, pol);
         }
 #pragma unroll
-        for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y2[l];
+        for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y2[l];
         if constexpr (TOUT) {
             static_assert(DIM == 2 && T <= 32, "transposed handoff: 2-D lines of <= 512");
             __syncthreads();
@@ -605,7 +605,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
 #pragma unroll
             for (int mm = 0; mm < P; ++mm) {
                 const int j = t + T * mm;
-                if (valid) a.T[tix(j)] = buf[G::pidx(j)];
+                if (valid) a.T[tix(j)] = buf[G::at_stride(t, G::pidx(t), mm)];
             }
         }
     }
@@ -731,15 +731,15 @@ tcol_kernel(const ColArgs a) {
     }
     // contiguous -> stride layout for the inverse transform (+ its mirror by shuffles)
 #pragma unroll
-    for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
+    for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y[l];
     pol.sync();
 #pragma unroll
-    for (int mm = 0; mm < P; ++mm) x[mm] = buf[G::pidx(t + T * mm)];
+    for (int mm = 0; mm < P; ++mm) x[mm] = buf[G::at_stride(t, G::pidx(t), mm)];
     pol.sync();
     pol.mirror(x, xm, t, buf, typename G::Pidx{});
     Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
-    for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
+    for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y[l];
     __syncthreads();
     // tile (EPB modes x N rows) -> T[b][i][q0 .. q0+EPB)
     const long g0 = (long)blockIdx.x * EPB;
@@ -853,7 +853,7 @@ __device__ __forceinline__ void col_group_w(const ColArgs& a, const int bid) {
     Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
     if constexpr (MODE == C_ONE) {
 #pragma unroll
-        for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = cscale(y[l], a.scale);
+        for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = cscale(y[l], a.scale);
     } else {
         const double k0sq = a.k0sq[b], eta = a.eta[b];
         const double lq = LAYOUT == CL_X3 ? a.lap[yl] + a.lap[q] : a.lap[q];
@@ -878,7 +878,7 @@ __device__ __forceinline__ void col_group_w(const ColArgs& a, const int bid) {
         pol.sync();
         Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
 #pragma unroll
-        for (int l = 0; l < P; ++l) buf[G::pidx(t * P + l)] = y[l];
+        for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y[l];
     }
     __syncthreads();
 #pragma unroll
@@ -952,7 +952,7 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
-        buf[G::pidx(j)] = a.T[mem + (size_t)j * LS + qa];
+        buf[G::at_stride(t, G::pidx(t), mm)] = a.T[mem + (size_t)j * LS + qa];
     }
     pol.sync();
     Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
@@ -992,7 +992,7 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
                 w = make_double2(lr * a.scale, li * a.scale);  // scale * lambda
             }
             const double2 v = (p == 0 || q == 0) ? zero : cmul(y[l], w);
-            buf[G::pidx(p)] = v;
+            buf[G::at_block(t, G::pidx(t * P), l)] = v;
         }
         pol.sync();
         if constexpr (CSM) {
