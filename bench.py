@@ -244,7 +244,7 @@ def run_ours(args):
 
     rank, local_rank, world = dist_env()
     torch.cuda.set_device(local_rank)
-    if world > 1 or (args.slab and args.config == "c2"):
+    if world > 1 or (args.slab and args.config in ("c2", "c3")):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29531")
         os.environ.setdefault("RANK", str(rank))
@@ -269,7 +269,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
-    if args.config == "c2" and (world > 1 or args.slab):
+    if args.config in ("c2", "c3") and (world > 1 or args.slab):
         rc = run_slab_bench(args, bs, rank, local_rank, world, barrier, max_over_ranks)
         dist.destroy_process_group()
         return rc
@@ -477,14 +477,17 @@ def run_ours(args):
 
 
 def run_slab_bench(args, bs, rank, local_rank, world, barrier, max_over_ranks):
-    """c2 on N GPUs: ONE 4095^2 grid slab-decomposed over the ranks: per sweep
-    a halo exchange, an all-reduce of 2 doubles and two all-to-alls of the transform
-    intermediate (NCCL through torch.distributed).  Total work fixed ("scaling": "strong")."""
+    """c2 / c3 on N GPUs: ONE 4095^2 (255^3) grid slab-decomposed over the ranks (SURVEY.md
+    8(e)): per sweep a halo exchange (rows / x-planes), an all-reduce of 2 doubles and two
+    all-to-alls of the transform intermediate (NCCL through torch.distributed; 3-D: over
+    y-blocks, the z- and y-lines stay local).  Total work fixed ("scaling": "strong")."""
     import torch
 
     from paper_2603_18527_b200.slab import DistComm, SlabPart, run_slab
-    k2, f, k0, eta = bs.config_instances("c2", 0, 1)
+    cname = args.config
+    k2, f, k0, eta = bs.config_instances(cname, 0, 1)
     nd = k2.shape[1]
+    dim = k2.ndim - 1
     part = SlabPart(k2[0], float(k0[0]), float(eta[0]), rank, world, device=local_rank)
     comm = DistComm()
     cmap = bs.PointwiseMap()
@@ -507,10 +510,11 @@ def run_slab_bench(args, bs, rank, local_rank, world, barrier, max_over_ranks):
         torch.cuda.synchronize()
         barrier()
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
-    pts = nd * nd
+    pts = nd ** dim
+    bpp = SWEEP_BYTES_PER_PT if dim == 2 else 192  # 128 (2-D), 192 (3-D)
     value = sweeps * pts / (elapsed_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
-    per_rank_gbs = SWEEP_BYTES_PER_PT * pts / world * sweeps / (elapsed_ms * 1e-3) / 1e9
+    per_rank_gbs = bpp * pts / world * sweeps / (elapsed_ms * 1e-3) / 1e9
     part.close()
     if rank == 0:
         fb = int(f[0].nbytes)
@@ -518,20 +522,23 @@ def run_slab_bench(args, bs, rank, local_rank, world, barrier, max_over_ranks):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded RngState medium, 16 seeded point sources, BASELINE c2 construction)",
-            "config": {"workload": WORKLOADS["c2"] + "; map pointwise; slab-decomposed",
-                       "grid": f"{nd}x{nd} (n={nd + 1})", "global_batch": 1,
-                       "rows_per_gpu": (nd + 1) // world, "sweeps_per_step": args.sweeps,
+            "data": ("synthetic (seeded RngState medium, 16 seeded point sources, BASELINE c2 construction)"
+                     if dim == 2 else "synthetic (seeded RngState 3-D medium, centre bump, BASELINE c3 construction)"),
+            "config": {"workload": WORKLOADS[cname] + "; map pointwise; slab-decomposed",
+                       "grid": "x".join([str(nd)] * dim) + f" (n={nd + 1})", "global_batch": 1,
+                       ("rows_per_gpu" if dim == 2 else "x_planes_per_gpu"): (nd + 1) // world,
+                       "sweeps_per_step": args.sweeps,
                        "parallelism": f"x-slab x{world}: halo p2p + all-reduce + 2 all-to-all per sweep (NCCL)",
-                       "l2": "no flush needed: ~1.3 GB working set >> 126 MB L2"},
+                       "l2": "no flush needed: >1 GB working set >> 126 MB L2"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": fb, "d2h_bytes_per_step": fb,
                     "path": "run_slab from host fields (set_fields + result inside every step)"},
             "roofline": {"bound": "hbm", "kernel": "whole sweep per rank (row + column + collectives)",
                          "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
                          "frac": per_rank_gbs / peak, "traffic": None, "peak_source": peak_src,
-                         "bytes_per_pt": SWEEP_BYTES_PER_PT},
+                         "bytes_per_pt": bpp},
             "cpu_baseline": None,
-            "gpu_launches": int(sweeps * 3 * world),
+            # per sweep and rank: row + column + finalize (3-D: + two y-line launches)
+            "gpu_launches": int(sweeps * (3 if dim == 2 else 5) * world),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -554,7 +561,7 @@ def main():
     ap.add_argument("--cpu-sweeps-c4", type=int, default=30)
     ap.add_argument("--ref-sweeps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--slab", action="store_true", help="c2: slab-decomposed path even at N=1")
+    ap.add_argument("--slab", action="store_true", help="c2 / c3: slab-decomposed path even at N=1")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

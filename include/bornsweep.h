@@ -215,9 +215,20 @@ typedef struct {
     void* u_halo_lo[2];            /* device: halo rows (row0 - 1, row0 + R) */
     void* u_halo_hi[2];
     void* stream;
+    int32_t dim;                   /* 2, or 3 for bp_slab_create3d */
+    int64_t halo_elems;            /* complex elements of one halo row (2-D) / x-plane (3-D) */
 } bp_slab_view_t;
 int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const double* k2, double k0,
                    double eta, int32_t device, bp_problem** out);
+/* 3-D slabs (config c3 over several GPUs; the 3-D extension has no reference counterpart):
+ * rank r owns the x-planes [r R, (r+1) R) of the cubic grid, R = n / nranks.  z-lines (the row
+ * kernel) and y-lines are local; the x-lines follow an all-to-all over y-blocks: t_rows is
+ * [dest][x_local][y_local][z] (R*R*n per destination), t_cols after the exchange the rank's
+ * y-block for every x.  The SWEEP / FWD_F / FWD_BORN stages end with the local y-DSTs, SWEEP /
+ * INV_NORM start with the inverse ones, so the stage protocol above is unchanged.  k2, and the
+ * fields of bp_slab_set_fields / bp_slab_result, are FULL dense nx^3 arrays. */
+int bp_slab_create3d(const bp_grid3* grid, int32_t rank, int32_t nranks, const double* k2, double k0,
+                     double eta, int32_t device, bp_problem** out);
 int bp_slab_view(const bp_problem* p, bp_slab_view_t* v);
 /* f, u0: the FULL dense nx*ny fields (host); u0 may be null */
 int bp_slab_set_fields(bp_problem* p, const double* f, const double* u0);

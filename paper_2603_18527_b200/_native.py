@@ -51,7 +51,8 @@ class SlabView(C.Structure):
                 ("n", C.c_int32), ("block_elems", C.c_int64), ("t_rows", C.c_void_p),
                 ("t_cols", C.c_void_p), ("sums", C.c_void_p), ("u_first", C.c_void_p * 2),
                 ("u_last", C.c_void_p * 2), ("u_halo_lo", C.c_void_p * 2),
-                ("u_halo_hi", C.c_void_p * 2), ("stream", C.c_void_p)]
+                ("u_halo_hi", C.c_void_p * 2), ("stream", C.c_void_p), ("dim", C.c_int32),
+                ("halo_elems", C.c_int64)]
 
 
 class InstanceSpec(C.Structure):
@@ -80,6 +81,8 @@ ABI_FUNCTIONS = {
     "bp_problem_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "bp_slab_create": (C.c_int, [C.POINTER(Grid), C.c_int32, C.c_int32, _dp, C.c_double, C.c_double,
                                  C.c_int32, C.POINTER(C.c_void_p)]),
+    "bp_slab_create3d": (C.c_int, [C.POINTER(Grid3), C.c_int32, C.c_int32, _dp, C.c_double, C.c_double,
+                                   C.c_int32, C.POINTER(C.c_void_p)]),
     "bp_slab_view": (C.c_int, [C.c_void_p, C.POINTER(SlabView)]),
     "bp_slab_set_fields": (C.c_int, [C.c_void_p, _dp, _dp]),
     "bp_slab_stage": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Map), C.POINTER(IterConfig),

@@ -1740,15 +1740,64 @@ __global__ void slab_finalize_kernel(Control c, const double* sums) {
 }
 
 // dense reference rows (nx*ny interior, x slow) -> padded slab rows [row0, row0 + R) (host)
-void pack_slab_host(const double* dense, int n, int row0, int R, std::vector<double2>& out) {
-    out.assign((size_t)R * n, make_double2(0.0, 0.0));
+// dense reference layout -> the rank's padded rows (2-D: [R][n]) / x-planes (3-D: [R][n][n])
+void pack_slab_host(const double* dense, int n, int row0, int R, std::vector<double2>& out, int dim = 2) {
+    const size_t line = dim == 3 ? (size_t)n * n : (size_t)n;
+    out.assign((size_t)R * line, make_double2(0.0, 0.0));
     const int nd = n - 1;
     for (int i = 0; i < R; ++i) {
         const int x = row0 + i;
         if (x < 1 || x > nd) continue;
-        const double* src = dense + 2 * (size_t)(x - 1) * nd;
-        for (int y = 1; y < n; ++y) out[(size_t)i * n + y] = make_double2(src[2 * (y - 1)], src[2 * (y - 1) + 1]);
+        if (dim == 2) {
+            const double* src = dense + 2 * (size_t)(x - 1) * nd;
+            for (int y = 1; y < n; ++y) out[(size_t)i * n + y] = make_double2(src[2 * (y - 1)], src[2 * (y - 1) + 1]);
+            continue;
+        }
+        for (int y = 1; y < n; ++y) {
+            const double* src = dense + 2 * ((size_t)(x - 1) * nd + (y - 1)) * nd;
+            double2* dst = out.data() + ((size_t)i * n + y) * n;
+            for (int z = 1; z < n; ++z) dst[z] = make_double2(src[2 * (z - 1)], src[2 * (z - 1) + 1]);
+        }
     }
+}
+
+// inverse of pack_slab_host for the rank's own rows / planes
+void unpack_slab_host(const std::vector<double2>& rows, int n, int row0, int R, double* dense, int dim) {
+    const int nd = n - 1;
+    for (int i = 0; i < R; ++i) {
+        const int x = row0 + i;
+        if (x < 1 || x > nd) continue;
+        if (dim == 2) {
+            double* dst = dense + 2 * (size_t)(x - 1) * nd;
+            for (int y = 1; y < n; ++y) {
+                dst[2 * (y - 1)] = rows[(size_t)i * n + y].x;
+                dst[2 * (y - 1) + 1] = rows[(size_t)i * n + y].y;
+            }
+            continue;
+        }
+        for (int y = 1; y < n; ++y) {
+            double* dst = dense + 2 * ((size_t)(x - 1) * nd + (y - 1)) * nd;
+            const double2* src = rows.data() + ((size_t)i * n + y) * n;
+            for (int z = 1; z < n; ++z) {
+                dst[2 * (z - 1)] = src[z].x;
+                dst[2 * (z - 1) + 1] = src[z].y;
+            }
+        }
+    }
+}
+
+size_t slab_halo(const bp_problem* p) { return p->dim == 3 ? (size_t)p->n * p->n : (size_t)p->n; }
+
+// 3-D slabs: the local y-lines of the rank's x-planes in the dest-blocked T layout (CL_YBLK)
+int slab_ylines(bp_problem* p, const Control& ctl) {
+    ColArgs c = col_args(p);
+    c.T = p->T;
+    c.batch = 1;
+    c.slab_log2 = p->slab_log2;
+    c.scale = 1.0;
+    c.status = p->slab_running ? ctl.status : nullptr;
+    CU(launch_col_pp(p->log2n, 16, CL_YBLK, C_ONE, c, p->stream));
+    return BP_OK;
 }
 
 RowArgs slab_row_args(const bp_problem* p) {
@@ -1773,8 +1822,8 @@ int bp_problem_set_stream(bp_problem* p, void* stream) {
     return BP_OK;
 }
 
-int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const double* k2, double k0,
-                   double eta, int32_t device, bp_problem** out) {
+static int slab_create_impl(const bp_grid* grid, int dim, int32_t rank, int32_t nranks, const double* k2,
+                            double k0, double eta, int32_t device, bp_problem** out) {
     if (!out) return set_err(BP_EINVAL, "null output handle");
     *out = nullptr;
     if (!grid || !k2) return set_err(BP_EINVAL, "null argument");
@@ -1784,14 +1833,15 @@ int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const doub
     const int n = grid->nx + 1;
     int log2n = 0;
     while ((1 << log2n) < n) ++log2n;
-    if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > kMaxLog2)
-        return set_err(BP_ENOTSUP, "GPU path needs square grids with nx+1 = 2^k, 8 <= 2^k <= 4096");
+    if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > (dim == 3 ? kMaxLog2_3d : kMaxLog2))
+        return set_err(BP_ENOTSUP, dim == 3 ? "GPU 3-D path needs cubic grids with n+1 = 2^k, 8 <= 2^k <= 512"
+                                            : "GPU path needs square grids with nx+1 = 2^k, 8 <= 2^k <= 4096");
     if (grid->lx != grid->ly) return set_err(BP_ENOTSUP, "GPU path needs lx == ly (hx == hy)");
     const int R = n / nranks;
     if (R < 8) return set_err(BP_ENOTSUP, "slab decomposition: at least 8 rows per rank");
     if (!(eta > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
     if (!std::isfinite(k0)) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
-    if (int rc = check_symbol(*grid, 2, 1, &k0, &eta)) return rc;
+    if (int rc = check_symbol(*grid, dim, 1, &k0, &eta)) return rc;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
         return set_err(BP_ECUDA, "no such CUDA device");
@@ -1802,18 +1852,19 @@ int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const doub
     p->device = device;
     p->log2n = log2n;
     p->n = n;
-    p->dim = 2;
+    p->dim = dim;
     p->slab_nranks = nranks;
     p->slab_rank = rank;
     p->slab_log2 = 0;
     while ((1 << p->slab_log2) < R) ++p->slab_log2;
     p->row0 = rank * R;
-    p->field = (size_t)R * n;
+    const size_t halo = dim == 3 ? (size_t)n * n : (size_t)n;  // one row / x-plane
+    p->field = (size_t)R * halo;
     p->alloc = p->field;
-    p->dense_pts = (size_t)grid->nx * grid->ny;
+    p->dense_pts = (size_t)grid->nx * grid->ny * (dim == 3 ? grid->nx : 1);
     const double h = grid->lx / n;
     p->inv_h2 = 1.0 / (h * h);
-    p->green_scale = std::pow(2.0 / n, 2) / std::pow(kEngineGain, 4);
+    p->green_scale = std::pow(2.0 / n, dim) / std::pow(kEngineGain, 2 * dim);
     auto fail = [&](int code) {
         bp_problem_destroy(p);
         return code;
@@ -1823,14 +1874,15 @@ int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const doub
         cudaError_t _e = (call);                                                                    \
         if (_e != cudaSuccess) return fail(set_err(BP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e))); \
     } while (0)
-    CUF(prepare_kernels(log2n, 2));
+    CUF(prepare_kernels(log2n, dim));
     {
         ColArgs c{};
         CUF(launch_col_pp(log2n, 16, CL_SLAB, C_GREEN, c, nullptr, true));
         CUF(launch_col_pp(log2n, 16, CL_SLAB, C_ONE, c, nullptr, true));
+        if (dim == 3) CUF(launch_col_pp(log2n, 16, CL_YBLK, C_ONE, c, nullptr, true));
     }
     CUF(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-    const size_t fb = sizeof(double2) * p->field, ub = sizeof(double2) * (p->field + 2 * (size_t)n);
+    const size_t fb = sizeof(double2) * p->field, ub = sizeof(double2) * (p->field + 2 * halo);
     for (double2** buf : {&p->k2, &p->f, &p->T, &p->Tc, &p->x, &p->y}) {
         CUF(cudaMalloc(buf, fb));
         CUF(cudaMemsetAsync(*buf, 0, fb, p->stream));
@@ -1839,11 +1891,11 @@ int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const doub
         CUF(cudaMalloc(buf, ub));
         CUF(cudaMemsetAsync(*buf, 0, ub, p->stream));
     }
-    p->u0 = p->u_alloc0 + n;
-    p->u1 = p->u_alloc1 + n;
+    p->u0 = p->u_alloc0 + halo;
+    p->u1 = p->u_alloc1 + halo;
     CUF(cudaMalloc(&p->slab_sums, sizeof(double) * 4));
     CUF(cudaMemsetAsync(p->slab_sums, 0, sizeof(double) * 4, p->stream));
-    CUF(cudaMalloc(&p->partial, sizeof(double) * (size_t)R * kPartStride));
+    CUF(cudaMalloc(&p->partial, sizeof(double) * (size_t)R * (dim == 3 ? n : 1) * kPartStride));
     CUF(cudaMalloc(&p->gamma, sizeof(double2)));
     CUF(cudaMalloc(&p->norm_part, sizeof(double) * 64));
     CUF(cudaMalloc(&p->fnorm_l2, sizeof(double)));
@@ -1872,7 +1924,7 @@ int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const doub
     CUF(cudaMemcpyAsync(p->sinp, sinp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->lap, lap.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
     std::vector<double2> rows;
-    pack_slab_host(k2, n, p->row0, R, rows);
+    pack_slab_host(k2, n, p->row0, R, rows, dim);
     CUF(cudaMemcpyAsync(p->k2, rows.data(), fb, cudaMemcpyHostToDevice, p->stream));
     bool ok = false;
     if (int rc = all_finite(p, reinterpret_cast<const double*>(p->k2), 2 * p->field, &ok)) return fail(rc);
@@ -1881,6 +1933,23 @@ int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const doub
 #undef CUF
     *out = p;
     return BP_OK;
+}
+
+int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const double* k2, double k0,
+                   double eta, int32_t device, bp_problem** out) {
+    return slab_create_impl(grid, 2, rank, nranks, k2, k0, eta, device, out);
+}
+
+int bp_slab_create3d(const bp_grid3* grid, int32_t rank, int32_t nranks, const double* k2, double k0,
+                     double eta, int32_t device, bp_problem** out) {
+    if (!out) return set_err(BP_EINVAL, "null output handle");
+    *out = nullptr;
+    if (!grid || !k2) return set_err(BP_EINVAL, "null argument");
+    if (grid->nx < 2 || grid->ny < 2 || grid->nz < 2) return set_err(BP_EINVAL, "GridSpec: nx,ny,nz must be >= 2");
+    if (grid->nz != grid->nx || grid->lz != grid->lx)
+        return set_err(BP_ENOTSUP, "GPU 3-D path needs cubic grids (hx == hy == hz)");
+    const bp_grid g2{grid->nx, grid->ny, grid->lx, grid->ly, grid->bc};
+    return slab_create_impl(&g2, 3, rank, nranks, k2, k0, eta, device, out);
 }
 
 int bp_slab_view(const bp_problem* p, bp_slab_view_t* v) {
@@ -1892,18 +1961,21 @@ int bp_slab_view(const bp_problem* p, bp_slab_view_t* v) {
     v->rows = R;
     v->row0 = p->row0;
     v->n = n;
-    v->block_elems = (int64_t)R * R;
+    const size_t halo = slab_halo(p);
+    v->block_elems = (int64_t)R * R * (p->dim == 3 ? n : 1);
     v->t_rows = p->T;
     v->t_cols = p->Tc;
     v->sums = p->slab_sums;
     for (int k = 0; k < 2; ++k) {
         double2* u = k ? p->u1 : p->u0;
         v->u_first[k] = u;
-        v->u_last[k] = u + (size_t)(R - 1) * n;
-        v->u_halo_lo[k] = u - n;
-        v->u_halo_hi[k] = u + (size_t)R * n;
+        v->u_last[k] = u + (size_t)(R - 1) * halo;
+        v->u_halo_lo[k] = u - halo;
+        v->u_halo_hi[k] = u + (size_t)R * halo;
     }
     v->stream = p->stream;
+    v->dim = p->dim;
+    v->halo_elems = (int64_t)halo;
     return BP_OK;
 }
 
@@ -1912,13 +1984,13 @@ int bp_slab_set_fields(bp_problem* p, const double* f, const double* u0) {
     if (!p->slab_log2 || !f) return set_err(BP_EINVAL, "slab: null field or not a slab problem");
     DeviceGuard guard(p->device);
     const int R = 1 << p->slab_log2;
-    const size_t fb = sizeof(double2) * p->field, ub = sizeof(double2) * (p->field + 2 * (size_t)p->n);
+    const size_t fb = sizeof(double2) * p->field, ub = sizeof(double2) * (p->field + 2 * slab_halo(p));
     std::vector<double2> rows;
-    pack_slab_host(f, p->n, p->row0, R, rows);
+    pack_slab_host(f, p->n, p->row0, R, rows, p->dim);
     CU(cudaMemcpyAsync(p->f, rows.data(), fb, cudaMemcpyHostToDevice, p->stream));
     CU(cudaMemsetAsync(p->u_alloc0, 0, ub, p->stream));
     if (u0) {
-        pack_slab_host(u0, p->n, p->row0, R, rows);
+        pack_slab_host(u0, p->n, p->row0, R, rows, p->dim);
         CU(cudaMemcpyAsync(p->u0, rows.data(), fb, cudaMemcpyHostToDevice, p->stream));
     }
     CU(cudaStreamSynchronize(p->stream));  // the staging vector goes out of scope
@@ -1933,25 +2005,32 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
     RowArgs a = slab_row_args(p);
     a.ctl.max_iters = p->slab_max_iters;
     a.ctl.rtol = p->slab_rtol;
+    const int dim = p->dim;
+    const bool d3 = dim == 3;  // 3-D: local y-lines after the forward / before the inverse rows
     switch (stage) {
-        case BP_SLAB_FWD_F:  // T <- y-DST of f; sums[0] = local ||f||^2
+        case BP_SLAB_FWD_F:  // T <- y-DST of f (3-D: z then y); sums[0] = local ||f||^2
             a.in = p->f;
-            CU(launch_row(p->log2n, 2, R_FWD, a, p->stream));
+            CU(launch_row(p->log2n, dim, R_FWD, a, p->stream));
+            if (d3)
+                if (int rc = slab_ylines(p, a.ctl)) return rc;
             return norms(p, p->f, p->slab_sums, true);
-        case BP_SLAB_COL: {  // column pass on the rank's n x R block
+        case BP_SLAB_COL: {  // column (x-line) pass on the rank's received block
             ColArgs c = col_args(p);
             c.T = p->Tc;
-            c.slab_cols = 1 << p->slab_log2;
-            c.col0 = p->slab_rank * c.slab_cols;
+            c.slab_cols = (1 << p->slab_log2) * (d3 ? p->n : 1);  // 3-D: (y, z) pairs
+            c.col0 = p->slab_rank * (1 << p->slab_log2);
+            c.slab3 = d3;
             c.scale = p->green_scale;
             c.status = p->slab_running ? a.ctl.status : nullptr;
             CU(launch_col_pp(p->log2n, 16, CL_SLAB, C_GREEN, c, p->stream));
             return BP_OK;
         }
         case BP_SLAB_INV_NORM:  // y <- inverse y-DST of T; sums[1] = local ||y||^2
+            if (d3)
+                if (int rc = slab_ylines(p, a.ctl)) return rc;
             a.out = p->y;
             a.sub = nullptr;
-            CU(launch_row(p->log2n, 2, R_INV, a, p->stream));
+            CU(launch_row(p->log2n, dim, R_INV, a, p->stream));
             return norms(p, p->y, p->slab_sums + 1, true);
         case BP_SLAB_INIT: {  // a0 = ||f||, a1 = ||G f|| (global); cfg: rtol / max_iters
             if (!cfg) return set_err(BP_EINVAL, "slab init: null config");
@@ -1964,7 +2043,7 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
             a = slab_row_args(p);
             CU(cudaMemcpyAsync(p->fnorm_l2, &a0, sizeof(double), cudaMemcpyHostToDevice, p->stream));
             CU(cudaMemcpyAsync(p->fnorm_reta, &a1, sizeof(double), cudaMemcpyHostToDevice, p->stream));
-            CU(cudaMemsetAsync(p->u_alloc1, 0, sizeof(double2) * (p->field + 2 * (size_t)p->n), p->stream));
+            CU(cudaMemsetAsync(p->u_alloc1, 0, sizeof(double2) * (p->field + 2 * slab_halo(p)), p->stream));
             init_control_kernel<<<1, 128, 0, p->stream>>>(a.ctl, 1);
             fill_nan_kernel<<<grid_for((size_t)p->trace_cap), 256, 0, p->stream>>>(p->trace_l2, p->trace_cap);
             fill_nan_kernel<<<grid_for((size_t)p->trace_cap), 256, 0, p->stream>>>(p->trace_reta, p->trace_cap);
@@ -1975,14 +2054,18 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
         }
         case BP_SLAB_FWD_BORN:  // T <- y-DST of V u^0 + f
             a.in = p->u0;
-            CU(launch_row(p->log2n, 2, R_FWD_BORN, a, p->stream));
+            CU(launch_row(p->log2n, dim, R_FWD_BORN, a, p->stream));
+            if (d3) return slab_ylines(p, a.ctl);
             return BP_OK;
         case BP_SLAB_SWEEP:  // fused scalar / pointwise sweep; sums[0..1] = local entry sums
             if (!map || (map->kind != BP_MAP_SCALAR && map->kind != BP_MAP_POINTWISE))
                 return set_err(BP_ENOTSUP, "slab decomposition: scalar and pointwise maps only");
             a.map_kind = map->kind;
             a.gamma = make_double2(map->gamma_re, map->gamma_im);
-            CU(launch_row(p->log2n, 2, R_SWEEP, a, p->stream));
+            if (d3)
+                if (int rc = slab_ylines(p, a.ctl)) return rc;
+            CU(launch_row(p->log2n, dim, R_SWEEP, a, p->stream));
+            if (d3) return slab_ylines(p, a.ctl);
             return BP_OK;
         case BP_SLAB_FINALIZE:  // sums hold the all-reduced entry sums
             slab_finalize_kernel<<<1, 32, 0, p->stream>>>(a.ctl, p->slab_sums);
@@ -2011,23 +2094,15 @@ int bp_slab_result(bp_problem* p, double* u_dense, double* res_l2, double* res_r
     int rb = 0;
     CU(cudaMemcpyAsync(&rb, c.result_buf, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
     CU(cudaStreamSynchronize(p->stream));
-    const int n = p->n, R = 1 << p->slab_log2, nd = n - 1;
-    std::vector<double2> rows((size_t)R * n);
+    const int n = p->n, R = 1 << p->slab_log2;
+    std::vector<double2> rows(p->field);
     CU(cudaMemcpyAsync(rows.data(), rb ? p->u1 : p->u0, sizeof(double2) * rows.size(), cudaMemcpyDeviceToHost,
                        p->stream));
     bp_iter_config cfg{BP_FMT_NPBS, p->slab_rtol, p->slab_max_iters};
     bp_trace tr{};
     if (int rc = finish_run_traces(p, &cfg, res_l2, res_reta, &tr)) return rc;
     if (info) *info = tr;
-    for (int i = 0; i < R; ++i) {
-        const int x = p->row0 + i;
-        if (x < 1 || x > nd) continue;
-        double* dst = u_dense + 2 * (size_t)(x - 1) * nd;
-        for (int y = 1; y < n; ++y) {
-            dst[2 * (y - 1)] = rows[(size_t)i * n + y].x;
-            dst[2 * (y - 1) + 1] = rows[(size_t)i * n + y].y;
-        }
-    }
+    unpack_slab_host(rows, n, p->row0, R, u_dense, p->dim);
     p->slab_running = false;
     return BP_OK;
 }

@@ -165,6 +165,11 @@ struct ColArgs {
     int finalize;
     int fin_lsh;
     Control ctl;
+    // 3-D slabs: CL_YBLK y-lines of the rank's R = 2^slab_log2 x-planes in the blocked layout
+    // of t_index<DIM = 3, SLAB>; CL_SLAB with slab3 != 0: the received block's columns are
+    // (y, z) pairs (slab_cols = R n), symbol a_y + a_z
+    int slab_log2;
+    int slab3;
 };
 
 // ------------------------------------------------------------------ helpers
@@ -284,6 +289,25 @@ struct RowGeom {
 // instantiation so the whole-member path keeps its compile-time indexing.
 // One group of EPB lines (the work of one CTA).  `staged`: the group's operands are already
 // in L2 (skip the per-line prefetch).
+// Element j of line i (of the member starting at `mem`) in the intermediate T: row-major for
+// whole members; on a slab (batch 1) blocked by the destination rank of the all-to-all --
+// 2-D: [dest = j >> sl][row i][j mod R]; 3-D (line i = (xl, y), xl the local x-plane):
+// [dest = y >> sl][xl][y mod R][z = j], i.e. the rank owning y-block `dest` receives its
+// x-lines contiguous (slab.py / bp_slab_*).
+template <int LOG2N, int DIM, bool SLAB>
+__device__ __forceinline__ size_t t_index(int sl, size_t mem, int i, int j) {
+    constexpr int N = 1 << LOG2N;
+    if constexpr (!SLAB) {
+        return mem + (size_t)i * N + j;
+    } else if constexpr (DIM == 2) {
+        return mem + ((size_t)(j >> sl) << (2 * sl)) + ((size_t)i << sl) + (j & ((1 << sl) - 1));
+    } else {
+        const int xl = i >> LOG2N, y = i & (N - 1);
+        const size_t blk = ((size_t)(y >> sl) << sl) + xl;
+        return mem + (((blk << sl) + (size_t)(y & ((1 << sl) - 1))) << LOG2N) + j;
+    }
+}
+
 template <int LOG2N, int MODE, int NW, int PP, int DIM, bool TOUT, bool SLAB>
 __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, const bool staged) {
     using G = Geom<LOG2N, PP>;
@@ -301,12 +325,14 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     const int t = threadIdx.x % T;
     const int e = threadIdx.x / T;
     const long grow = grp * EPB + e;
-    static_assert(!SLAB || (DIM == 2 && !TOUT), "slabs: 2-D row-major handoff only");
-    const int lsh = SLAB ? a.slab_log2 : LLINES;        // log2(lines per member)
+    static_assert(!SLAB || !TOUT, "slabs: row-major handoff only");
+    // log2(lines per member or slab): a slab holds 2^slab_log2 rows (2-D) / x-planes (3-D)
+    const int lsh = SLAB ? a.slab_log2 + (DIM - 2) * LOG2N : LLINES;
     const int b = (int)(grow >> lsh);
     const int i = (int)(grow & ((1L << lsh) - 1));      // line index within the member (slab)
-    const int ig = SLAB ? a.row0 + i : i;               // global line index
-    bool valid = (b < a.batch) && (ig & (N - 1)) != 0 && (DIM == 2 || (i >> LOG2N) != 0);
+    // global x index of the line (2-D: the row; 3-D: the plane) and its Dirichlet padding
+    const int xg = (SLAB ? a.row0 : 0) + (DIM == 2 ? i : (i >> LOG2N));
+    bool valid = (b < a.batch) && (xg & (N - 1)) != 0 && (DIM == 2 || (i & (N - 1)) != 0);
     // shared-memory staging of the inverse transform's input (see RSM below)
     constexpr bool RSM = BS_ROW_SMEM && (T > 32 || DIM == 3 || (BS_RSM_ALL && S::ITER));
     // The T line is loaded before the member's status / sweep counter are known (they are
@@ -316,15 +342,10 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     if constexpr (S::INV && RSM) {
         const int sl0 = SLAB ? a.slab_log2 : 0;
         const size_t mem0 = (size_t)(valid ? b : 0) << (lsh + LOG2N);
-        const size_t row0 = mem0 + (size_t)(valid ? i : 0) * N;
+        const int i0 = valid ? i : 0;
 #pragma unroll
-        for (int mm = 0; mm < P; ++mm) {
-            const int j = t + T * mm;
-            size_t ix = row0 + j;
-            if constexpr (SLAB)
-                ix = mem0 + ((size_t)(j >> sl0) << (2 * sl0)) + ((size_t)(valid ? i : 0) << sl0) + (j & ((1 << sl0) - 1));
-            xT[mm] = a.T[ix];  // in bounds for every thread (mem0/row0 clamped)
-        }
+        for (int mm = 0; mm < P; ++mm)  // in bounds for every thread (member / line clamped)
+            xT[mm] = a.T[t_index<LOG2N, DIM, SLAB>(sl0, mem0, i0, t + T * mm)];
     }
     int m = 0;  // trace entry this launch belongs to
     if (S::ITER && valid) {
@@ -345,7 +366,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     const int sl = SLAB ? a.slab_log2 : 0;
     auto tix = [&](int j) -> size_t {
         if constexpr (!SLAB) return row + j;
-        return mem + ((size_t)(j >> sl) << (2 * sl)) + ((size_t)(valid ? i : 0) << sl) + (j & ((1 << sl) - 1));
+        return t_index<LOG2N, DIM, SLAB>(sl, mem, valid ? i : 0, j);
     };
     const double2 zero = make_double2(0.0, 0.0);
     const double2* ucur = (m & 1) ? a.u1 : a.u0;  // u^m
@@ -631,7 +652,8 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
             for (int k = 0; k < S::NPART; ++k) pr[k] = acc[k];
             __threadfence();
             const unsigned old = atomicAdd(&a.ctl.counter[b], 1u);
-            const unsigned nvalid = SLAB ? (1u << sl) - (a.row0 == 0 ? 1u : 0u) : VALID_LINES;
+            const unsigned nvalid = SLAB ? ((1u << sl) - (a.row0 == 0 ? 1u : 0u)) * (DIM == 3 ? N - 1u : 1u)
+                                         : VALID_LINES;
             last = (old == nvalid - 1u);
         }
         last = pol.bcast0(last, t);
@@ -642,7 +664,9 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
             for (int k = 0; k < S::NPART; ++k) s[k] = 0.0;
             for (int r = t; r < (1 << lsh); r += T) {
                 const int rg = SLAB ? a.row0 + r : r;
-                if ((rg & (N - 1)) == 0 || (DIM == 3 && (r >> LOG2N) == 0)) continue;  // padding lines
+                if (DIM == 2 ? (rg & (N - 1)) == 0
+                             : ((r & (N - 1)) == 0 || (((SLAB ? a.row0 : 0) + (r >> LOG2N)) & (N - 1)) == 0))
+                    continue;  // padding lines
                 const double* pr = a.ctl.partial + (((size_t)b << lsh) + r) * kPartStride;
 #pragma unroll
                 for (int k = 0; k < S::NPART; ++k) s[k] += __ldcg(pr + k);
@@ -766,7 +790,8 @@ struct ColGeom {
 //           x-plane, planes_per_member = n).  LAYOUT 2: 3-D x-lines (stride n^2).
 //           CL_SLAB: 2-D x-lines of the n x slab_cols column block a rank holds after the
 //           all-to-all of a slab-decomposed grid (row stride slab_cols, global column col0 + q).
-enum ColLayout { CL_PLANE = 0, CL_X3 = 2, CL_SLAB = 3 };
+//           CL_YBLK: 3-D slab y-lines on the dest-blocked layout (t_index<3, true>).
+enum ColLayout { CL_PLANE = 0, CL_X3 = 2, CL_SLAB = 3, CL_YBLK = 4 };
 
 // Deferred finalisation of trace entry m for member b (ColArgs::finalize): one warp sums the
 // per-row partials of the preceding R_SWEEP launch in the row kernel's own order (lane r over
@@ -906,7 +931,13 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
     int b, yl = 0, qa;
     size_t mem;
     size_t LS = LAYOUT == CL_X3 ? (size_t)N * N : (size_t)N;
-    if constexpr (LAYOUT == CL_SLAB) {
+    int xl = 0;  // CL_YBLK: local x-plane
+    if constexpr (LAYOUT == CL_YBLK) {
+        b = 0;
+        xl = bid / GROUPS;
+        qa = (bid % GROUPS) * C + c;  // z
+        mem = 0;
+    } else if constexpr (LAYOUT == CL_SLAB) {
         const int groups = a.slab_cols / C;
         b = bid / groups;
         qa = (bid % groups) * C + c;  // column within the block (address)
@@ -925,12 +956,30 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
         mem = (size_t)plane * N * N;
     }
     int q;  // global column index (symbol, Dirichlet zero column)
+    double lq3 = 0.0;  // 3-D slab columns: a_y + a_z
     if constexpr (LAYOUT == CL_SLAB) {
         q = a.col0 + qa;
+        if (a.slab3) {
+            const int yq = a.col0 + (qa >> LOG2N), zq = qa & (N - 1);
+            q = (yq == 0 || zq == 0) ? 0 : 1;  // only the Dirichlet test uses q below
+            lq3 = a.lap[yq] + a.lap[zq];
+        }
+    } else if constexpr (LAYOUT == CL_YBLK) {
+        q = qa;
     } else {
         q = (bid % GROUPS) * C + c;
         qa = q;
     }
+    // element j of this thread's line
+    const int sly = LAYOUT == CL_YBLK ? a.slab_log2 : 0;
+    auto gidx = [&](int j) -> size_t {
+        if constexpr (LAYOUT == CL_YBLK) {
+            const size_t blk = ((size_t)(j >> sly) << sly) + xl;
+            return (((blk << sly) + (size_t)(j & ((1 << sly) - 1))) << LOG2N) + qa;
+        } else {
+            return mem + (size_t)j * LS + qa;
+        }
+    };
     if (a.status) {
         const bool active = __ldcg(&a.status[b]) == ST_ACTIVE;  // read before finalising
         if constexpr (LAYOUT == CL_PLANE) {
@@ -952,7 +1001,7 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
-        buf[G::at_stride(t, G::pidx(t), mm)] = a.T[mem + (size_t)j * LS + qa];
+        buf[G::at_stride(t, G::pidx(t), mm)] = a.T[gidx(j)];
     }
     pol.sync();
     Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
@@ -961,19 +1010,19 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
 #pragma unroll
         for (int mm = 0; mm < P; ++mm) {
             const int j = t + T * mm;
-            x[mm] = a.T[mem + (size_t)j * LS + qa];
-            xm[mm] = (j == 0) ? zero : a.T[mem + (size_t)(N - j) * LS + qa];
+            x[mm] = a.T[gidx(j)];
+            xm[mm] = (j == 0) ? zero : a.T[gidx(N - j)];
         }
         Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
     }
 
     if constexpr (MODE == C_ONE) {
 #pragma unroll
-        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + qa] = cscale(y[l], a.scale);
+        for (int l = 0; l < P; ++l) a.T[gidx(t * P + l)] = cscale(y[l], a.scale);
     } else {
         const double k0sq = a.k0sq[b], eta = a.eta[b];
         // transverse symbol part: a_q (2-D) or a_y + a_z (3-D x-lines)
-        const double lq = LAYOUT == CL_X3 ? a.lap[yl] + a.lap[q] : a.lap[q];
+        const double lq = LAYOUT == CL_X3 ? a.lap[yl] + a.lap[q] : (LAYOUT == CL_SLAB && a.slab3) ? lq3 : a.lap[q];
 #pragma unroll
         for (int l = 0; l < P; ++l) {
             const int p = t * P + l;
@@ -1009,7 +1058,7 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
             Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
         }
 #pragma unroll
-        for (int l = 0; l < P; ++l) a.T[mem + (size_t)(t * P + l) * LS + qa] = y[l];
+        for (int l = 0; l < P; ++l) a.T[gidx(t * P + l)] = y[l];
     }
 }
 

@@ -20,7 +20,7 @@ template <int L, int MODE, int PP, int DIM, bool TOUT = false, bool SLAB = false
 cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
     using RG = RowGeom<L, PP, kRowWarps>;
     // slab launches (2-D, row-major handoff, the modes the slab driver uses) -> SLAB instance
-    constexpr bool SLAB_OK = DIM == 2 && !TOUT && PP == 16 &&
+    constexpr bool SLAB_OK = !TOUT && PP == 16 &&
                              (MODE == R_FWD || MODE == R_FWD_BORN || MODE == R_INV || MODE == R_SWEEP);
     if constexpr (SLAB_OK && !SLAB) {
         if (a.slab_log2 || prepare) {
@@ -31,7 +31,7 @@ cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
     if (!SLAB && a.slab_log2 && !prepare) return cudaErrorInvalidValue;
     auto k = row_kernel<L, MODE, kRowWarps, PP, DIM, TOUT, SLAB>;
     if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
-    const long rows = (long)a.batch << (SLAB ? a.slab_log2 : (DIM - 1) * L);
+    const long rows = (long)a.batch << (SLAB ? a.slab_log2 + (DIM - 2) * L : (DIM - 1) * L);
     const int grid = (int)((rows + RG::EPB - 1) / RG::EPB);
     k<<<grid, kRowWarps * 32, RG::SMEM, s>>>(a);
     return cudaGetLastError();
@@ -46,7 +46,9 @@ cudaError_t launch_col_t(const ColArgs& a, cudaStream_t s, bool prepare) {
     // CL_PLANE: one CTA per (plane, column group), planes = batch * planes_per_member;
     // CL_X3: one CTA per (member, y, column group)
     // CL_SLAB: one CTA per (member, column group of the rank's block)
-    const long groups = (long)a.batch * (LAYOUT == CL_X3 ? (1L << L) : a.planes_per_member);
+    // CL_YBLK: one CTA per (local x-plane, column group); batch 1
+    const long groups = LAYOUT == CL_YBLK ? (1L << a.slab_log2)
+                                          : (long)a.batch * (LAYOUT == CL_X3 ? (1L << L) : a.planes_per_member);
     const int grid = LAYOUT == CL_SLAB ? (int)((long)a.batch * (a.slab_cols / C))
                                        : (int)(groups * ((1 << L) / C));
     if (LAYOUT == CL_SLAB && (a.slab_cols % C) != 0) return cudaErrorInvalidValue;
@@ -238,6 +240,11 @@ struct Pp8 {
         if (layout == CL_SLAB) {                                                                \
             if (mode == C_ONE) return launch_col_t<L, C_ONE, 16, CL_SLAB>(a, s, prep);          \
             if (mode == C_GREEN) return launch_col_t<L, C_GREEN, 16, CL_SLAB>(a, s, prep);      \
+            return cudaErrorInvalidValue;                                                       \
+        }                                                                                       \
+        if (layout == CL_YBLK) {                                                                \
+            if constexpr (L <= kMaxLog2_3d)                                                     \
+                if (mode == C_ONE) return launch_col_t<L, C_ONE, 16, CL_YBLK>(a, s, prep);      \
             return cudaErrorInvalidValue;                                                       \
         }                                                                                       \
         if (pp == 8) return launch_col_p<L, Pp8<L>::value>(mode, a, s, prep);                   \

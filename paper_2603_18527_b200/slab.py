@@ -50,19 +50,26 @@ def _dev_tensor(ptr, shape, typestr, device):
 
 
 class SlabPart:
-    """One rank's x-slab on a GPU (bp_slab_create).  k2: the FULL dense (nx, ny) medium."""
+    """One rank's x-slab on a GPU (bp_slab_create / bp_slab_create3d).  k2: the FULL dense
+    (nx, ny) or (nx, ny, nz) medium; a 3-D medium gives x-plane slabs (config c3)."""
 
     def __init__(self, k2, k0: float, eta: float, rank: int, nranks: int, lx: float = 1.0,
                  device: int = 0):
         import torch
         k2 = np.ascontiguousarray(np.asarray(k2, np.complex128))
-        self.nx, self.ny = k2.shape
+        self.shape = k2.shape
+        self.nx, self.ny = k2.shape[:2]
         self.rank, self.nranks, self.device = rank, nranks, device
         self._lib = N.lib()
         h = C.c_void_p()
-        g = N.Grid(self.nx, self.ny, lx, lx, BC_DIRICHLET)
-        _check(self._lib.bp_slab_create(C.byref(g), rank, nranks, _ptr(k2), float(k0), float(eta),
-                                        device, C.byref(h)))
+        if k2.ndim == 3:
+            g3 = N.Grid3(*k2.shape, lx, lx, lx, BC_DIRICHLET)
+            _check(self._lib.bp_slab_create3d(C.byref(g3), rank, nranks, _ptr(k2), float(k0), float(eta),
+                                              device, C.byref(h)))
+        else:
+            g = N.Grid(self.nx, self.ny, lx, lx, BC_DIRICHLET)
+            _check(self._lib.bp_slab_create(C.byref(g), rank, nranks, _ptr(k2), float(k0), float(eta),
+                                            device, C.byref(h)))
         self._h = h
         # launch on the framework's current stream: the collectives are ordered with the kernels
         stream = torch.cuda.current_stream(device).cuda_stream
@@ -70,14 +77,15 @@ class SlabPart:
         v = N.SlabView()
         _check(self._lib.bp_slab_view(self._h, C.byref(v)))
         self.rows, self.row0, self.n = v.rows, v.row0, v.n
-        R, n, d = v.rows, v.n, device
-        self.t_rows = _dev_tensor(v.t_rows, (nranks, R, R), "<c16", d)
-        self.t_cols = _dev_tensor(v.t_cols, (nranks, R, R), "<c16", d)
+        R, n, d, hl = v.rows, v.n, device, v.halo_elems
+        # per destination: R x R (2-D) / R x R x n (3-D) complex, flattened
+        self.t_rows = _dev_tensor(v.t_rows, (nranks, v.block_elems), "<c16", d)
+        self.t_cols = _dev_tensor(v.t_cols, (nranks, v.block_elems), "<c16", d)
         self.sums = _dev_tensor(v.sums, (4,), "<f8", d)
-        self.u_first = [_dev_tensor(v.u_first[k], (n,), "<c16", d) for k in range(2)]
-        self.u_last = [_dev_tensor(v.u_last[k], (n,), "<c16", d) for k in range(2)]
-        self.u_halo_lo = [_dev_tensor(v.u_halo_lo[k], (n,), "<c16", d) for k in range(2)]
-        self.u_halo_hi = [_dev_tensor(v.u_halo_hi[k], (n,), "<c16", d) for k in range(2)]
+        self.u_first = [_dev_tensor(v.u_first[k], (hl,), "<c16", d) for k in range(2)]
+        self.u_last = [_dev_tensor(v.u_last[k], (hl,), "<c16", d) for k in range(2)]
+        self.u_halo_lo = [_dev_tensor(v.u_halo_lo[k], (hl,), "<c16", d) for k in range(2)]
+        self.u_halo_hi = [_dev_tensor(v.u_halo_hi[k], (hl,), "<c16", d) for k in range(2)]
 
     def close(self):
         if getattr(self, "_h", None):
@@ -187,7 +195,7 @@ class DistComm:
 # ---------------------------------------------------------------------------- driver
 @dataclass
 class SlabResult:
-    u: np.ndarray            # dense (nx, ny): the rows of the local parts filled
+    u: np.ndarray            # dense (nx, ny[, nz]): the rows / planes of the local parts filled
     trace: IterationTrace
     sweeps_launched: int
 
@@ -231,7 +239,7 @@ def run_slab(parts, comm, cmap, f, config: IterationConfig | None = None, u0=Non
         if (k + 1) % POLL_SWEEPS == 0 or k == config.max_iters:
             if parts[0].active() == 0:
                 break
-    u = np.zeros((parts[0].nx, parts[0].ny), np.complex128)
+    u = np.zeros(parts[0].shape, np.complex128)
     trace = None
     for p in parts:
         trace = p.result(u, config.max_iters)

@@ -27,6 +27,7 @@ class NumpySlabPart:
     def __init__(self, k2, k0, eta, rank, nranks, lx=1.0):
         k2 = np.asarray(k2, np.complex128)
         self.nx, self.ny = k2.shape
+        self.shape = k2.shape
         n = self.nx + 1
         R = n // nranks
         self.n, self.rows, self.rank, self.nranks, self.row0 = n, R, rank, nranks, rank * R
@@ -167,6 +168,139 @@ class NumpySlabPart:
             x = self.row0 + i
             if 1 <= x <= self.nx:
                 u_dense[x - 1] = rows[i, 1:]
+        k = self.iters + 1
+        return IterationTrace(self.l2[:k].copy(), self.rt[:k].copy(), self.iters, TERMINATION[self.term],
+                              self.fn, self.gn)
+
+
+def _sine_ax(a, axis):
+    """plain sine sum over the interior (index 1..n-1) along `axis` of padded data"""
+    a = np.moveaxis(a, axis, -1)
+    out = np.zeros_like(a)
+    out[..., 1:] = 0.5 * sf.dst(a[..., 1:], type=1, axis=-1)
+    return np.moveaxis(out, -1, axis)
+
+
+class NumpySlabPart3(NumpySlabPart):
+    """3-D x-plane slab (bp_slab_create3d): planes [R][y][z]; t_rows = [dest][x_local][y_local][z]
+    (dest = y-block); the SWEEP / FWD_* stages end with the y-DST, SWEEP / INV_NORM start with
+    the inverse one; COL = x-DST, x 8/(n^3 lambda), inverse x-DST on the received y-block."""
+
+    def __init__(self, k2, k0, eta, rank, nranks, lx=1.0):
+        k2 = np.asarray(k2, np.complex128)
+        self.shape = k2.shape
+        self.nx, self.ny = k2.shape[:2]
+        n = self.nx + 1
+        R = n // nranks
+        self.n, self.rows, self.rank, self.nranks, self.row0 = n, R, rank, nranks, rank * R
+        self.h = lx / n
+        self.k0sq, self.eta = k0 * k0, eta
+        self.k2 = self._pack(k2)
+        self.V = self.k2 - (self.k0sq + 1j * eta)
+        j = np.arange(n)
+        self.lap = 4.0 / self.h ** 2 * np.sin(j * np.pi / (2 * n)) ** 2
+        self._T = np.zeros((nranks, R * R * n), np.complex128)
+        self._Tc = np.zeros((nranks, R * R * n), np.complex128)
+        self._sums = np.zeros(4)
+        self._u = [np.zeros((R + 2, n, n), np.complex128) for _ in range(2)]
+        self.t_rows, self.t_cols = torch.from_numpy(self._T), torch.from_numpy(self._Tc)
+        self.sums = torch.from_numpy(self._sums)
+        self.u_first = [torch.from_numpy(u[1]) for u in self._u]
+        self.u_last = [torch.from_numpy(u[R]) for u in self._u]
+        self.u_halo_lo = [torch.from_numpy(u[0]) for u in self._u]
+        self.u_halo_hi = [torch.from_numpy(u[R + 1]) for u in self._u]
+        self.f = np.zeros((R, n, n), np.complex128)
+        self.y = np.zeros((R, n, n), np.complex128)
+        self.valid = (self.row0 + np.arange(R)) % n != 0
+
+    def _pack(self, dense):
+        out = np.zeros((self.rows, self.n, self.n), np.complex128)
+        for i in range(self.rows):
+            x = self.row0 + i
+            if 1 <= x <= self.nx:
+                out[i, 1:, 1:] = dense[x - 1]
+        return out
+
+    def _block(self, planes):  # z- then y-DST'd planes -> [dest][xl][yb][z]
+        R, P, n = self.rows, self.nranks, self.n
+        self._T[...] = planes.reshape(R, P, R, n).transpose(1, 0, 2, 3).reshape(P, -1)
+
+    def _unblock(self):
+        R, P, n = self.rows, self.nranks, self.n
+        return self._T.reshape(P, R, R, n).transpose(1, 0, 2, 3).reshape(R, P * R, n).copy()
+
+    @staticmethod
+    def _yz(planes):
+        return _sine_ax(_sine_ax(planes, 2), 1)
+
+    def set_fields(self, f, u0=None):
+        self.f = self._pack(np.asarray(f, np.complex128))
+        self._u[0][...] = 0
+        if u0 is not None:
+            self._u[0][1:self.rows + 1] = self._pack(np.asarray(u0, np.complex128))
+
+    def stage(self, code, cmap=None, config=None, a0=0.0, a1=0.0):
+        R, n = self.rows, self.n
+        if code == FWD_F:
+            self._block(self._yz(self.f))
+            self._sums[0] = np.sum(np.abs(self.f) ** 2)
+        elif code == COL:
+            if getattr(self, "status", 0) != 0:
+                return
+            M = self._Tc.reshape(n, R, n)  # (x, y_local, z)
+            yq = self.rank * R + np.arange(R)
+            lam = (self.lap[:, None, None] + self.lap[yq][None, :, None] + self.lap[None, None, :]
+                   - (self.k0sq + 1j * self.eta))
+            w = 8.0 / n ** 3 / lam
+            w[0], w[:, :, 0] = 0, 0
+            w[:, yq == 0, :] = 0
+            M[...] = _sine_ax(_sine_ax(M, 0) * w, 0)
+        elif code == INV_NORM:
+            self.y = self._yz(self._unblock()) * self.valid[:, None, None]
+            self._sums[1] = np.sum(np.abs(self.y) ** 2)
+        elif code in (INIT, FINALIZE):
+            super().stage(code, cmap, config, a0, a1)
+            if code == INIT:
+                self._u[1][...] = 0
+        elif code == FWD_BORN:
+            u = self._u[0][1:R + 1]
+            self._block(self._yz(self.V * u + self.f))
+        elif code == SWEEP:
+            if self.status != 0:
+                return
+            m = self.sweep
+            ua = self._u[m & 1]
+            u = ua[1:R + 1]
+            z = self._yz(self._unblock())
+            s = 6.0 * u - ua[0:R] - ua[2:R + 2]
+            for ax in (1, 2):
+                lo = np.zeros_like(u)
+                hi = np.zeros_like(u)
+                sl = [slice(None)] * 3
+                sl[ax] = slice(1, None)
+                sr = [slice(None)] * 3
+                sr[ax] = slice(None, -1)
+                lo[tuple(sl)] = u[tuple(sr)]
+                hi[tuple(sr)] = u[tuple(sl)]
+                s = s - lo - hi
+            r = self.f - (s / self.h ** 2 - self.k2 * u)
+            x = z - u
+            mask = self.valid[:, None, None] & (np.arange(n) != 0)[None, :, None] & (np.arange(n) != 0)[None, None, :]
+            self._sums[0] = np.sum((np.abs(r) ** 2)[mask])
+            self._sums[1] = np.sum((np.abs(x) ** 2)[mask])
+            g = 1j / self.eta * self.V if cmap.__class__.__name__ == "PointwiseMap" else complex(cmap.gamma)
+            unew = u + g * x
+            unew[:, 0, :], unew[:, :, 0] = 0, 0
+            nxt = self._u[(m + 1) & 1][1:R + 1]
+            nxt[self.valid] = unew[self.valid]
+            self._block(self._yz(self.V * nxt + self.f))
+
+    def result(self, u_dense, max_iters):
+        planes = self._u[self.result_buf][1:self.rows + 1]
+        for i in range(self.rows):
+            x = self.row0 + i
+            if 1 <= x <= self.nx:
+                u_dense[x - 1] = planes[i, 1:, 1:]
         k = self.iters + 1
         return IterationTrace(self.l2[:k].copy(), self.rt[:k].copy(), self.iters, TERMINATION[self.term],
                               self.fn, self.gn)

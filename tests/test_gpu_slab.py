@@ -84,3 +84,42 @@ def test_slab_errors(gpu):
         run_slab(parts, LocalComm(), bs.ScalarMap(1.0), np.zeros_like(f))
     with pytest.raises(NotImplementedError):
         run_slab(parts, LocalComm(), bs.OptimalScalarMap(), f)
+
+
+# ---------------------------------------------------------------------------- 3-D slabs (c3)
+def inst3(n, seed=0, ppw=10.0, contrast=0.3):
+    spec = bs.InstanceSpec(n=n, ppw=ppw, contrast=contrast, sigma_cells=3.0, seed=seed, dim=3)
+    k2, f, k0, eta = bs.make_instances(spec, 0, 1)
+    return k2[0], f[0], float(k0[0]), float(eta[0])
+
+
+@pytest.mark.parametrize("n,nranks", [(32, 1), (32, 2), (32, 4), (64, 8)])
+@pytest.mark.parametrize("cmap", [bs.ScalarMap(1.0), bs.PointwiseMap()], ids=["scalar", "pointwise"])
+def test_slab3d_run_matches_oracle(gpu, n, nranks, cmap):
+    """x-plane slabs of a 3-D grid (z-lines and y-lines local, x-lines after the y-block
+    all-to-all) against the plain-C oracle's 3-D run: iterations +-1, u within 1e-10."""
+    k2, f, k0, eta = inst3(n, seed=n + nranks)
+    cfg = bs.IterationConfig(rtol=1e-7, max_iters=2000)
+    res = run_slab([SlabPart(k2, k0, eta, r, nranks) for r in range(nranks)], LocalComm(), cmap, f, cfg)
+    kind = MAP_POINTWISE if isinstance(cmap, bs.PointwiseMap) else MAP_SCALAR
+    ref = OracleProblem(k2, k0, eta).run(f, map_kind=kind, gamma=getattr(cmap, "gamma", 1.0), rtol=1e-7,
+                                         max_iters=2000)
+    assert res.trace.terminated == ref.terminated
+    assert abs(res.trace.iters - ref.iters) <= 1
+    assert rel(res.u, ref.u) < FIELD_TOL
+    k = min(res.trace.iters, ref.iters) + 1
+    np.testing.assert_allclose(res.trace.res_l2_rel[:k], ref.res_l2[:k], rtol=1e-9, atol=1e-13)
+
+
+def test_slab3d_matches_single_gpu_path(gpu):
+    """A 128^3 grid through the single-GPU 3-D handle and through 2 and 4 slabs."""
+    k2, f, k0, eta = inst3(128, seed=5, ppw=8.0, contrast=0.4)
+    cfg = bs.IterationConfig(rtol=1e-6, max_iters=30)
+    with bs.HelmholtzDirichlet(k2[None], np.array([k0]), np.array([eta]), dim=3) as p:
+        one = bs.run(p, bs.PointwiseMap(), f[None], cfg)
+    for nranks in (2, 4):
+        res = run_slab([SlabPart(k2, k0, eta, r, nranks) for r in range(nranks)], LocalComm(),
+                       bs.PointwiseMap(), f, cfg)
+        assert res.trace.iters == one.trace.iters == 30
+        assert rel(res.u, one.u[0]) < 1e-12
+        np.testing.assert_allclose(res.trace.res_l2_rel, one.trace.res_l2_rel, rtol=1e-11)

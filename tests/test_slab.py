@@ -12,7 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import paper_2603_18527_b200 as bs  # noqa: E402
 from oracle import MAP_POINTWISE, MAP_SCALAR, OracleProblem  # noqa: E402
 from paper_2603_18527_b200.slab import DistComm, LocalComm, run_slab  # noqa: E402
-from slab_standin import NumpySlabPart  # noqa: E402
+from slab_standin import NumpySlabPart, NumpySlabPart3  # noqa: E402
 
 FIELD_TOL = 1e-10
 
@@ -76,14 +76,33 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def instance3(n, seed=2):
+    spec = bs.InstanceSpec(n=n, ppw=10.0, contrast=0.3, sigma_cells=3.0, seed=seed, dim=3)
+    k2, f, k0, eta = bs.make_instances(spec, 0, 1)
+    return k2[0], f[0], float(k0[0]), float(eta[0])
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4])
+def test_local_slab3d_driver_matches_oracle(nranks):
+    """3-D x-plane slabs (bp_slab_create3d protocol: y-block all-to-all, halo planes)."""
+    k2, f, k0, eta = instance3(16)
+    parts = [NumpySlabPart3(k2, k0, eta, r, nranks) for r in range(nranks)]
+    res = run_slab(parts, LocalComm(), bs.PointwiseMap(), f, bs.IterationConfig(rtol=1e-8, max_iters=3000))
+    ref = oracle_run(k2, f, k0, eta, bs.PointwiseMap(), 1e-8, 3000)
+    assert res.trace.terminated == ref.terminated == "converged"
+    assert abs(res.trace.iters - ref.iters) <= 1
+    assert rel(res.u, ref.u) < FIELD_TOL
+
+
+def _worker(rank, world, port, q, dim=2):
     import torch.distributed as dist
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-    from slab_standin import NumpySlabPart as Part
+    from slab_standin import NumpySlabPart, NumpySlabPart3
+    Part = NumpySlabPart3 if dim == 3 else NumpySlabPart
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        k2, f, k0, eta = instance(32)
+        k2, f, k0, eta = instance3(16) if dim == 3 else instance(32)
         part = Part(k2, k0, eta, rank, world)
         res = run_slab([part], DistComm(), bs.PointwiseMap(), f, bs.IterationConfig(rtol=1e-8, max_iters=3000))
         q.put((rank, part.row0, part.rows, res.u, res.trace.iters, res.trace.terminated,
@@ -92,19 +111,20 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_gloo_slab_matches_oracle():
+@pytest.mark.parametrize("dim", [2, 3])
+def test_two_rank_gloo_slab_matches_oracle(dim):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, dim)) for r in range(2)]
     for p in procs:
         p.start()
     results = sorted([q.get(timeout=300) for _ in procs], key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    k2, f, k0, eta = instance(32)
+    k2, f, k0, eta = instance3(16) if dim == 3 else instance(32)
     ref = oracle_run(k2, f, k0, eta, bs.PointwiseMap(), 1e-8, 3000)
     u = np.zeros_like(ref.u)
     for rank, row0, rows, ur, iters, term, l2, launched in results:
