@@ -489,7 +489,7 @@ def run_slab_bench(args, bs, rank, local_rank, world, barrier, max_over_ranks):
     nd = k2.shape[1]
     dim = k2.ndim - 1
     part = SlabPart(k2[0], float(k0[0]), float(eta[0]), rank, world, device=local_rank)
-    comm = DistComm()
+    comm = DistComm(fused=args.fused)
     cmap = bs.PointwiseMap()
     cfg = bs.IterationConfig(rtol=1e-6, max_iters=args.sweeps)
     stream = torch.cuda.current_stream(local_rank)
@@ -500,19 +500,30 @@ def run_slab_bench(args, bs, rank, local_rank, world, barrier, max_over_ranks):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    sweeps = 0
-    with ClockSampler(local_rank) as clocks:
+    def timed(resident: bool):
+        sweeps = 0
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            sweeps += run_slab([part], comm, cmap, f[0], cfg).sweeps_launched
+            # value: f resident in HBM (staged by the warm-up), no result download;
+            # e2e: host fields staged and the result + traces fetched inside every step
+            sweeps += run_slab([part], comm, cmap, f[0], cfg, stage_fields=not resident,
+                               fetch=not resident).sweeps_launched
         ev1.record(stream)
         ev1.synchronize()
         torch.cuda.synchronize()
         barrier()
-    elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
+        return sweeps, max_over_ranks(ev0.elapsed_time(ev1))
+
+    with ClockSampler(local_rank) as clocks:
+        sweeps, elapsed_ms = timed(True)
+    sweeps_e2e, elapsed_e2e = timed(False)
     pts = nd ** dim
     bpp = SWEEP_BYTES_PER_PT if dim == 2 else 192  # 128 (2-D), 192 (3-D)
     value = sweeps * pts / (elapsed_ms * 1e-3) / 1e9
+    value_e2e = sweeps_e2e * pts / (elapsed_e2e * 1e-3) / 1e9
     peak, peak_src = measured_peak()
     per_rank_gbs = bpp * pts / world * sweeps / (elapsed_ms * 1e-3) / 1e9
     part.close()
@@ -528,9 +539,11 @@ def run_slab_bench(args, bs, rank, local_rank, world, barrier, max_over_ranks):
                        "grid": "x".join([str(nd)] * dim) + f" (n={nd + 1})", "global_batch": 1,
                        ("rows_per_gpu" if dim == 2 else "x_planes_per_gpu"): (nd + 1) // world,
                        "sweeps_per_step": args.sweeps,
-                       "parallelism": f"x-slab x{world}: halo p2p + all-reduce + 2 all-to-all per sweep (NCCL)",
+                       "parallelism": (f"x-slab x{world}: halo p2p + all-reduce + exchange fused into the kernels' "
+                                       "stores over symmetric (NVLink peer) memory + 2 fences per sweep" if args.fused else
+                                       f"x-slab x{world}: halo p2p + all-reduce + 2 all-to-all per sweep (NCCL)"),
                        "l2": "no flush needed: >1 GB working set >> 126 MB L2"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": fb, "d2h_bytes_per_step": fb,
+            "e2e": {"value": value_e2e, "unit": UNIT, "h2d_bytes_per_step": fb, "d2h_bytes_per_step": fb,
                     "path": "run_slab from host fields (set_fields + result inside every step)"},
             "roofline": {"bound": "hbm", "kernel": "whole sweep per rank (row + column + collectives)",
                          "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
@@ -562,6 +575,8 @@ def main():
     ap.add_argument("--ref-sweeps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slab", action="store_true", help="c2 / c3: slab-decomposed path even at N=1")
+    ap.add_argument("--fused", action="store_true",
+                    help="c2 / c3 slabs: exchange fused into the kernels' stores (symmetric memory)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -202,7 +202,8 @@ enum {
     BP_SLAB_INIT = 3,      /* a0 = ||f||, a1 = ||G f|| (global), cfg: control + traces reset */
     BP_SLAB_FWD_BORN = 4,  /* t_rows <- y-DST of V u^0 + f */
     BP_SLAB_SWEEP = 5,     /* fused sweep; sums[0..1] = local entry sums */
-    BP_SLAB_FINALIZE = 6   /* trace entry + termination from the all-reduced sums */
+    BP_SLAB_FINALIZE = 6,  /* trace entry + termination from the all-reduced sums */
+    BP_SLAB_ZERO_U = 7     /* u^0 <- 0 on the device (a cold start without re-staging f) */
 };
 typedef struct {
     int32_t rank, nranks, rows, row0, n;
@@ -229,6 +230,17 @@ int bp_slab_create(const bp_grid* grid, int32_t rank, int32_t nranks, const doub
  * fields of bp_slab_set_fields / bp_slab_result, are FULL dense nx^3 arrays. */
 int bp_slab_create3d(const bp_grid3* grid, int32_t rank, int32_t nranks, const double* k2, double k0,
                      double eta, int32_t device, bp_problem** out);
+/* Fused exchange (nranks <= 8): the kernel that produces the forward transform's blocks (2-D:
+ * the row kernel; 3-D: the forward y-lines) stores block d straight into rank d's t_cols, and
+ * the column kernel stores its results straight into the source ranks' t_rows -- the two
+ * all-to-alls become the kernels' own epilogues (same-device parts, or NVLink peer memory
+ * mapped into this process).  peer_t_cols / peer_t_rows: nranks device pointers valid on this
+ * device (this rank's own entries included).  local_t_rows / local_t_cols (nullable): buffers
+ * to use as this rank's t_rows / t_cols instead of its own (e.g. symmetric-memory allocations;
+ * block_elems * nranks complex each).  The driver then only orders the stages across ranks
+ * (no transposes).  enable = 0 restores the plain exchange. */
+int bp_slab_set_exchange(bp_problem* p, int32_t enable, void* local_t_rows, void* local_t_cols,
+                         void* const* peer_t_cols, void* const* peer_t_rows);
 int bp_slab_view(const bp_problem* p, bp_slab_view_t* v);
 /* f, u0: the FULL dense nx*ny fields (host); u0 may be null */
 int bp_slab_set_fields(bp_problem* p, const double* f, const double* u0);

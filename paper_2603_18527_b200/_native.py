@@ -84,6 +84,8 @@ ABI_FUNCTIONS = {
     "bp_slab_create3d": (C.c_int, [C.POINTER(Grid3), C.c_int32, C.c_int32, _dp, C.c_double, C.c_double,
                                    C.c_int32, C.POINTER(C.c_void_p)]),
     "bp_slab_view": (C.c_int, [C.c_void_p, C.POINTER(SlabView)]),
+    "bp_slab_set_exchange": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                       C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "bp_slab_set_fields": (C.c_int, [C.c_void_p, _dp, _dp]),
     "bp_slab_stage": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Map), C.POINTER(IterConfig),
                                 C.c_double, C.c_double]),

@@ -349,6 +349,11 @@ struct bp_problem {
     double2* Tc = nullptr;                              // column-side block
     double* slab_sums = nullptr;
     bool slab_running = false;
+    // fused exchange (bp_slab_set_exchange)
+    bool xchg_on = false;
+    double2* xchg_cols[kMaxXchg]{};  // peers' t_cols (receive side of the forward exchange)
+    double2* xchg_rows[kMaxXchg]{};  // peers' t_rows (receive side of the inverse exchange)
+    double2 *own_T = nullptr, *own_Tc = nullptr;  // the handle's allocations (freed on destroy)
     int slab_max_iters = 1000;
     double slab_rtol = 1e-6;
     bool own_stream = true;
@@ -1788,14 +1793,20 @@ void unpack_slab_host(const std::vector<double2>& rows, int n, int row0, int R, 
 
 size_t slab_halo(const bp_problem* p) { return p->dim == 3 ? (size_t)p->n * p->n : (size_t)p->n; }
 
-// 3-D slabs: the local y-lines of the rank's x-planes in the dest-blocked T layout (CL_YBLK)
-int slab_ylines(bp_problem* p, const Control& ctl) {
+// 3-D slabs: the local y-lines of the rank's x-planes in the dest-blocked T layout (CL_YBLK);
+// forward = the launch before the exchange (fused: stores into the peers' t_cols)
+int slab_ylines(bp_problem* p, const Control& ctl, bool forward = false) {
     ColArgs c = col_args(p);
     c.T = p->T;
     c.batch = 1;
     c.slab_log2 = p->slab_log2;
     c.scale = 1.0;
     c.status = p->slab_running ? ctl.status : nullptr;
+    if (forward && p->xchg_on) {
+        c.xchg_on = 1;
+        c.xchg_rank = p->slab_rank;
+        for (int r = 0; r < p->slab_nranks; ++r) c.xchg[r] = p->xchg_cols[r];
+    }
     CU(launch_col_pp(p->log2n, 16, CL_YBLK, C_ONE, c, p->stream));
     return BP_OK;
 }
@@ -1805,6 +1816,11 @@ RowArgs slab_row_args(const bp_problem* p) {
     a.slab_log2 = p->slab_log2;
     a.row0 = p->row0;
     a.slab_sums = p->slab_sums;
+    if (p->xchg_on && p->dim == 2) {  // 2-D: the row kernel's forward stores are the exchange
+        a.xchg_on = 1;
+        a.xchg_rank = p->slab_rank;
+        for (int r = 0; r < p->slab_nranks; ++r) a.xchg[r] = p->xchg_cols[r];
+    }
     return a;
 }
 
@@ -1979,6 +1995,35 @@ int bp_slab_view(const bp_problem* p, bp_slab_view_t* v) {
     return BP_OK;
 }
 
+int bp_slab_set_exchange(bp_problem* p, int32_t enable, void* local_t_rows, void* local_t_cols,
+                         void* const* peer_t_cols, void* const* peer_t_rows) {
+    if (int rc = check_problem(p)) return rc;
+    if (!p->slab_log2) return set_err(BP_EINVAL, "not a slab problem");
+    DeviceGuard guard(p->device);
+    CU(cudaStreamSynchronize(p->stream));
+    if (!p->own_T) {
+        p->own_T = p->T;
+        p->own_Tc = p->Tc;
+    }
+    if (!enable) {
+        p->xchg_on = false;
+        p->T = p->own_T;
+        p->Tc = p->own_Tc;
+        return BP_OK;
+    }
+    if (p->slab_nranks > kMaxXchg) return set_err(BP_ENOTSUP, "fused exchange: at most 8 ranks");
+    if (!peer_t_cols || !peer_t_rows) return set_err(BP_EINVAL, "fused exchange: null peer pointer arrays");
+    for (int r = 0; r < p->slab_nranks; ++r) {
+        if (!peer_t_cols[r] || !peer_t_rows[r]) return set_err(BP_EINVAL, "fused exchange: null peer pointer");
+        p->xchg_cols[r] = static_cast<double2*>(peer_t_cols[r]);
+        p->xchg_rows[r] = static_cast<double2*>(peer_t_rows[r]);
+    }
+    p->T = local_t_rows ? static_cast<double2*>(local_t_rows) : p->own_T;
+    p->Tc = local_t_cols ? static_cast<double2*>(local_t_cols) : p->own_Tc;
+    p->xchg_on = true;
+    return BP_OK;
+}
+
 int bp_slab_set_fields(bp_problem* p, const double* f, const double* u0) {
     if (int rc = check_problem(p)) return rc;
     if (!p->slab_log2 || !f) return set_err(BP_EINVAL, "slab: null field or not a slab problem");
@@ -2012,7 +2057,7 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
             a.in = p->f;
             CU(launch_row(p->log2n, dim, R_FWD, a, p->stream));
             if (d3)
-                if (int rc = slab_ylines(p, a.ctl)) return rc;
+                if (int rc = slab_ylines(p, a.ctl, true)) return rc;
             return norms(p, p->f, p->slab_sums, true);
         case BP_SLAB_COL: {  // column (x-line) pass on the rank's received block
             ColArgs c = col_args(p);
@@ -2022,6 +2067,12 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
             c.slab3 = d3;
             c.scale = p->green_scale;
             c.status = p->slab_running ? a.ctl.status : nullptr;
+            if (p->xchg_on) {  // results straight into the source ranks' t_rows
+                c.xchg_on = 1;
+                c.xchg_rank = p->slab_rank;
+                c.xchg_log2r = p->slab_log2;
+                for (int r = 0; r < p->slab_nranks; ++r) c.xchg[r] = p->xchg_rows[r];
+            }
             CU(launch_col_pp(p->log2n, 16, CL_SLAB, C_GREEN, c, p->stream));
             return BP_OK;
         }
@@ -2055,7 +2106,7 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
         case BP_SLAB_FWD_BORN:  // T <- y-DST of V u^0 + f
             a.in = p->u0;
             CU(launch_row(p->log2n, dim, R_FWD_BORN, a, p->stream));
-            if (d3) return slab_ylines(p, a.ctl);
+            if (d3) return slab_ylines(p, a.ctl, true);
             return BP_OK;
         case BP_SLAB_SWEEP:  // fused scalar / pointwise sweep; sums[0..1] = local entry sums
             if (!map || (map->kind != BP_MAP_SCALAR && map->kind != BP_MAP_POINTWISE))
@@ -2065,7 +2116,10 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
             if (d3)
                 if (int rc = slab_ylines(p, a.ctl)) return rc;
             CU(launch_row(p->log2n, dim, R_SWEEP, a, p->stream));
-            if (d3) return slab_ylines(p, a.ctl);
+            if (d3) return slab_ylines(p, a.ctl, true);
+            return BP_OK;
+        case BP_SLAB_ZERO_U:
+            CU(cudaMemsetAsync(p->u_alloc0, 0, sizeof(double2) * (p->field + 2 * slab_halo(p)), p->stream));
             return BP_OK;
         case BP_SLAB_FINALIZE:  // sums hold the all-reduced entry sums
             slab_finalize_kernel<<<1, 32, 0, p->stream>>>(a.ctl, p->slab_sums);
@@ -2176,6 +2230,10 @@ int bp_problem_destroy(bp_problem* p) {
     if (p->graph) cudaGraphExecDestroy(p->graph);
     if (p->u_alloc0) p->u0 = p->u_alloc0;
     if (p->u_alloc1) p->u1 = p->u_alloc1;
+    if (p->own_T) {  // external exchange buffers (bp_slab_set_exchange) are not ours to free
+        p->T = p->own_T;
+        p->Tc = p->own_Tc;
+    }
     for (void* q : {(void*)p->k2, (void*)p->f, (void*)p->u0, (void*)p->u1, (void*)p->T, (void*)p->x,
                     (void*)p->y, (void*)p->dense, (void*)p->partial, (void*)p->gamma, (void*)p->fd, (void*)p->norm_part,
                     (void*)p->fnorm_l2, (void*)p->fnorm_reta, (void*)p->ctl_int, (void*)p->counter,

@@ -91,6 +91,8 @@ struct RowSpec {
     static constexpr bool UPDATE = MODE == R_SWEEP || MODE == R_OPT_B || MODE == R_FD_B;
 };
 
+constexpr int kMaxXchg = 8;  // ranks of a fused-exchange slab group
+
 struct Control {
     int* status;          // [batch]
     int* sweep;           // [batch] next trace entry to record
@@ -142,6 +144,13 @@ struct RowArgs {
     // column pass, ColArgs::finalize) sums them and records entry m -- no fence / atomic /
     // last-row wait at the end of every row (r01 ncu: ~13 % of the long-scoreboard stalls)
     int defer_final;
+    // Fused exchange on a slab (xchg_on): the forward transform's blocks are stored straight
+    // into the destination ranks' receive buffers (xchg[d] = rank d's t_cols, mapped on this
+    // device: same-device parts or NVLink peer memory) at block `xchg_rank` -- the forward
+    // all-to-all becomes part of the row kernel's epilogue.
+    int xchg_on;
+    int xchg_rank;
+    double2* xchg[kMaxXchg];
 };
 
 struct ColArgs {
@@ -170,6 +179,12 @@ struct ColArgs {
     // (y, z) pairs (slab_cols = R n), symbol a_y + a_z
     int slab_log2;
     int slab3;
+    // fused inverse exchange (CL_SLAB): line element j belongs to source rank j >> xchg_log2r;
+    // it is stored into that rank's t_rows (xchg[src]) at block xchg_rank
+    int xchg_on;
+    int xchg_rank;
+    int xchg_log2r;
+    double2* xchg[kMaxXchg];
 };
 
 // ------------------------------------------------------------------ helpers
@@ -626,7 +641,19 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
 #pragma unroll
             for (int mm = 0; mm < P; ++mm) {
                 const int j = t + T * mm;
-                if (valid) a.T[tix(j)] = buf[G::at_stride(t, G::pidx(t), mm)];
+                if (valid) {
+                    const double2 v = buf[G::at_stride(t, G::pidx(t), mm)];
+                    size_t ix = tix(j);
+                    if constexpr (SLAB) {
+                        if (a.xchg_on) {  // block d -> rank d's receive buffer, at block xchg_rank
+                            const int lb = 2 * sl + (DIM - 2) * LOG2N;  // log2 elements per block
+                            const size_t d = ix >> lb;
+                            a.xchg[d][((size_t)a.xchg_rank << lb) + (ix & ((1ull << lb) - 1))] = v;
+                            continue;
+                        }
+                    }
+                    a.T[ix] = v;
+                }
             }
         }
     }
@@ -980,6 +1007,27 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
             return mem + (size_t)j * LS + qa;
         }
     };
+    // output element j: in place, or (fused inverse exchange, CL_SLAB) into the source rank's
+    // t_rows at block xchg_rank -- row j & (R-1) of that block, same column
+    // (CL_YBLK forward y-lines of a 3-D slab: the dest-blocked element goes to rank d's t_cols,
+    // like the 2-D row kernel's fused store)
+    auto st_out = [&](int j, double2 v) {
+        if constexpr (LAYOUT == CL_SLAB) {
+            if (a.xchg_on) {
+                const int rr = a.xchg_log2r;
+                a.xchg[j >> rr][((size_t)a.xchg_rank << rr) * LS + (size_t)(j & ((1 << rr) - 1)) * LS + qa] = v;
+                return;
+            }
+        } else if constexpr (LAYOUT == CL_YBLK) {
+            if (a.xchg_on) {
+                const size_t ix = gidx(j);
+                const int lb = 2 * sly + LOG2N;  // log2 elements per destination block
+                a.xchg[ix >> lb][((size_t)a.xchg_rank << lb) + (ix & ((1ull << lb) - 1))] = v;
+                return;
+            }
+        }
+        a.T[gidx(j)] = v;
+    };
     if (a.status) {
         const bool active = __ldcg(&a.status[b]) == ST_ACTIVE;  // read before finalising
         if constexpr (LAYOUT == CL_PLANE) {
@@ -1018,7 +1066,7 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
 
     if constexpr (MODE == C_ONE) {
 #pragma unroll
-        for (int l = 0; l < P; ++l) a.T[gidx(t * P + l)] = cscale(y[l], a.scale);
+        for (int l = 0; l < P; ++l) st_out(t * P + l, cscale(y[l], a.scale));
     } else {
         const double k0sq = a.k0sq[b], eta = a.eta[b];
         // transverse symbol part: a_q (2-D) or a_y + a_z (3-D x-lines)
@@ -1058,7 +1106,7 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
             Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
         }
 #pragma unroll
-        for (int l = 0; l < P; ++l) a.T[gidx(t * P + l)] = y[l];
+        for (int l = 0; l < P; ++l) st_out(t * P + l, y[l]);
     }
 }
 

@@ -13,7 +13,7 @@ import scipy.fft as sf
 import torch
 
 from paper_2603_18527_b200.api import TERMINATION, IterationTrace
-from paper_2603_18527_b200.slab import COL, FINALIZE, FWD_BORN, FWD_F, INIT, INV_NORM, SWEEP
+from paper_2603_18527_b200.slab import COL, FINALIZE, FWD_BORN, FWD_F, INIT, INV_NORM, SWEEP, ZERO_U
 
 
 def _sine(a):
@@ -158,6 +158,8 @@ class NumpySlabPart:
         elif code == FINALIZE:
             if self.status == 0:
                 self._finalize(self._sums[0], self._sums[1])
+        elif code == ZERO_U:
+            self._u[0][...] = 0
 
     def active(self):
         return 1 if self.status == 0 else 0
@@ -258,7 +260,7 @@ class NumpySlabPart3(NumpySlabPart):
         elif code == INV_NORM:
             self.y = self._yz(self._unblock()) * self.valid[:, None, None]
             self._sums[1] = np.sum(np.abs(self.y) ** 2)
-        elif code in (INIT, FINALIZE):
+        elif code in (INIT, FINALIZE, ZERO_U):
             super().stage(code, cmap, config, a0, a1)
             if code == INIT:
                 self._u[1][...] = 0
