@@ -379,8 +379,8 @@ ccol_kernel(const CdrArgs a) {
             for (int mm = 0; mm < P; ++mm) {
                 const int p = t + T * mm;
                 const double lre = (a.lapn[p] + la) + s0, lim = (a.lapn[p] + lb) + s0;
-                if constexpr (MODE == CC_GREEN)
-                    y[mm] = make_double2(y[mm].x * (a.scale / lre), y[mm].y * (a.scale / lim));
+                if constexpr (MODE == CC_GREEN)  // lambda >= sigma0 > 0: reciprocal + Newton
+                    y[mm] = make_double2(y[mm].x * (a.scale * rcp_green(lre)), y[mm].y * (a.scale * rcp_green(lim)));
                 else
                     y[mm] = make_double2(y[mm].x * (a.scale * lre), y[mm].y * (a.scale * lim));
                 buf[G::pidx(p)] = y[mm];

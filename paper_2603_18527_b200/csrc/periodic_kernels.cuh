@@ -205,14 +205,14 @@ pcol_kernel(const PerArgs a) {
             const double lr = (a.xi2[p] + xq) - k0sq;
             const double li = -eta;
             if constexpr (MODE == CP_GREEN) {
-                const double s = a.scale * __drcp_rn(fma(lr, lr, li * li));
+                const double s = a.scale * rcp_green(fma(lr, lr, li * li));
                 x[m] = cmul(y[m], make_double2(lr * s, -li * s));
             } else if constexpr (MODE == CP_LREF) {
                 x[m] = cmul(y[m], make_double2(lr * a.scale, li * a.scale));
             } else {  // CP_SWEEP
                 const size_t idx = mem + (size_t)p * N + q;
                 const double2 U = Ucur[idx];
-                const double inv = __drcp_rn(fma(lr, lr, li * li));
+                const double inv = rcp_green(fma(lr, lr, li * li));
                 const double2 ginv = make_double2(lr * inv, -li * inv);      // 1/lambda
                 const double2 xs = csub(cmul(y[m], ginv), U);                // r_bs^
                 const double2 rs = csub(y[m], cmul(make_double2(lr, li), U)); // r^
