@@ -9,16 +9,28 @@
 namespace bs {
 
 constexpr int kRowWarps = 8;   // warps per row-kernel CTA
+// experiment knobs (r01: 4-warp row CTAs equal, 4-column n = 512 column CTAs 47 % slower)
+#ifndef BS_ROW_NW
+#define BS_ROW_NW 8            // warps per CTA of the Dirichlet row kernel for single-warp lines
+#endif
+#ifndef BS_COLC9
+#define BS_COLC9 8             // columns per column-kernel CTA for n = 512
+#endif
+template <int L, int PP>
+struct RowWarps {
+    static constexpr int value = Geom<L, PP>::T <= 32 ? BS_ROW_NW : kRowWarps;
+};
 // columns per column-kernel CTA: 8 (128-B row segments) while a CTA of 8 lines fits; long
 // lines (n >= 1024) hold fewer columns per CTA so the shared-memory lines still fit
 template <int L>
 struct ColCols {
-    static constexpr int value = L <= 9 ? 8 : (L == 10 ? 4 : 2);
+    static constexpr int value = L == 9 ? BS_COLC9 : L <= 8 ? 8 : (L == 10 ? 4 : 2);
 };
 
 template <int L, int MODE, int PP, int DIM, bool TOUT = false, bool SLAB = false>
 cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
-    using RG = RowGeom<L, PP, kRowWarps>;
+    constexpr int NWR = RowWarps<L, PP>::value;
+    using RG = RowGeom<L, PP, NWR>;
     // slab launches (2-D, row-major handoff, the modes the slab driver uses) -> SLAB instance
     constexpr bool SLAB_OK = !TOUT && PP == 16 &&
                              (MODE == R_FWD || MODE == R_FWD_BORN || MODE == R_INV || MODE == R_SWEEP);
@@ -29,11 +41,11 @@ cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
         }
     }
     if (!SLAB && a.slab_log2 && !prepare) return cudaErrorInvalidValue;
-    auto k = row_kernel<L, MODE, kRowWarps, PP, DIM, TOUT, SLAB>;
+    auto k = row_kernel<L, MODE, NWR, PP, DIM, TOUT, SLAB>;
     if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
     const long rows = (long)a.batch << (SLAB ? a.slab_log2 + (DIM - 2) * L : (DIM - 1) * L);
     const int grid = (int)((rows + RG::EPB - 1) / RG::EPB);
-    k<<<grid, kRowWarps * 32, RG::SMEM, s>>>(a);
+    k<<<grid, NWR * 32, RG::SMEM, s>>>(a);
     return cudaGetLastError();
 }
 
