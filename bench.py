@@ -190,8 +190,9 @@ def run_reference_arm(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded c4 media)", "impl": "reference",
-            "config": {"workload": "c4", "grid": "1024x1024", "batch_sample": 1,
-                       "sweeps_per_step": sweeps, "parallelism": "OpenMP inside the port"},
+            "config": {"workload": WORKLOADS["c4"] + "; map scalar", "grid": "1024x1024 Neumann cell-centred (h=1/1024)",
+                       "global_batch": 32, "batch_sample": 1, "sweeps_per_step": sweeps,
+                       "parallelism": "OpenMP inside the port"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -215,8 +216,10 @@ def run_reference_arm(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded RngState media, BASELINE.json c1 construction)",
         "impl": "reference",
-        "config": {"workload": "c1", "grid": "511x511", "batch_sample": members,
-                   "sweeps_per_step": sweeps, "parallelism": "OpenMP over members"},
+        # the GPU arm's config (same workload, grid, batch); the CPU step is a bounded sample
+        "config": {"workload": WORKLOADS["c1"] + "; map pointwise", "grid": "511x511 (n=512, h=1/512)",
+                   "global_batch": 64, "batch_sample": members, "sweeps_per_step": sweeps,
+                   "parallelism": f"OpenMP over members, {cores} threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -572,7 +575,9 @@ def main():
     ap.add_argument("--sweeps", type=int, default=127, help="sweeps per step (max_iters)")
     ap.add_argument("--cpu-sweeps", type=int, default=300)
     ap.add_argument("--cpu-sweeps-c4", type=int, default=30)
-    ap.add_argument("--ref-sweeps", type=int, default=2)
+    # sweeps per reference-arm step: enough that the run's setup (||f||, ||G f||: two
+    # transform pairs) does not dominate the CPU sample (~1.3 s per step on 16 cores)
+    ap.add_argument("--ref-sweeps", type=int, default=20)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slab", action="store_true", help="c2 / c3: slab-decomposed path even at N=1")
     ap.add_argument("--fused", action="store_true",
