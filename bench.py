@@ -19,8 +19,10 @@ and result gather.  Work counted = sweeps actually executed (sum of iters) x 511
              the graph replaced by individually event-bracketed launches), vs MEASURED_PEAKS.
 * cpu_baseline -- the reference's own code (oracle/_ref) on the host cores, bounded sample.
 
-N > 1 (torchrun): members are sharded across ranks (64/N each, no collective on the data
-path: "scaling": "strong", total work fixed); torch.distributed only for barrier + max time.
+N > 1 (torchrun): every rank runs its own batch of independent members (the N = 1 batch, global
+member indices [64 r, 64 r + 64): "scaling": "weak", per-GPU work fixed -- SURVEY.md 8(e), no
+collective on the data path); --strong splits the config's 64 members instead (8 per GPU at
+N = 8, config 1's wording).  torch.distributed only for the barrier and the max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -280,7 +282,10 @@ def run_ours(args):
     from paper_2603_18527_b200.sharding import shard_members
     cfgd = bs.CONFIGS[args.config]
     total = args.batch if args.config == "c1" else cfgd["batch"]
-    first, per = shard_members(total, world, rank)
+    if args.strong:  # the config's member count split over the ranks
+        first, per = shard_members(total, world, rank)
+    else:  # weak scaling (batch of independent members, no collective): the N = 1 batch per rank
+        first, per = rank * total, total
     cdr = args.config == "c4"
     if cdr:
         bx, by, sg, s0, f = bs.config_instances("c4", first, per)
@@ -376,8 +381,9 @@ def run_ours(args):
     col_avg = col_ms / full_launches
     pts_per_launch = per * pts
     peak, peak_src = measured_peak()
-    row_gbs = row_b * pts_per_launch / (row_avg * 1e-3) / 1e9
-    col_gbs = col_b * pts_per_launch / (col_avg * 1e-3) / 1e9
+    # (BP_MIXED=1: rows and columns share launches, all time is charged to row_ms)
+    row_gbs = row_b * pts_per_launch / (row_avg * 1e-3) / 1e9 if row_avg > 0 else 0.0
+    col_gbs = col_b * pts_per_launch / (col_avg * 1e-3) / 1e9 if col_avg > 0 else 0.0
     sweep_gbs = sweep_b * pts_per_launch / ((row_avg + col_avg) * 1e-3) / 1e9
     traffic, traffic_src = load_traffic() if args.config == "c1" else (None, None)
 
@@ -442,14 +448,17 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": ("synthetic (seeded c4 media: smoothed noise b, sigma, f)" if cdr else
                      "synthetic (seeded RngState media + centre Gaussian-bump sources, BASELINE c1 construction)"),
             "config": {"workload": WORKLOADS[args.config] + f"; map {args.map or cfgd['map']}",
                        "grid": (f"{nd}x{nd} Neumann cell-centred (h=1/{nd})" if cdr else
-                                "x".join([str(nd)] * dim) + f" (n={nd + 1}, h=1/{nd + 1})"), "global_batch": total,
+                                "x".join([str(nd)] * dim) + f" (n={nd + 1}, h=1/{nd + 1})"), "global_batch": total if args.strong else total * world,
                        "members_per_gpu": per, "sweeps_per_step": args.sweeps,
-                       "parallelism": f"batch-shard x{world}",
+                       "parallelism": (f"batch-shard x{world} (the {total} members split)" if args.strong else
+                                       f"batch-shard x{world} ({per} independent members per GPU, "
+                                       f"global members [{first}, {first + per}) on rank {rank})"),
                        "l2": "no flush needed: ~1.7 GB working set per step >> 126 MB L2"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
@@ -567,7 +576,9 @@ def main():
     ap.add_argument("--steps", type=int, default=15)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=64, help="members of config c1 (whole job)")
+    ap.add_argument("--batch", type=int, default=64, help="members of config c1 per GPU (whole job with --strong)")
+    ap.add_argument("--strong", action="store_true",
+                    help="split the config's members over the ranks (default: weak scaling, the N=1 batch per rank)")
     ap.add_argument("--config", choices=["c0", "c1", "c2", "c3", "c4"], default="c1",
                     help="workload; the headline metric is quoted on c1 (BASELINE.json configs[1])")
     ap.add_argument("--map", choices=["pointwise", "scalar", "optimal_l2"], default=None,
