@@ -186,6 +186,28 @@ int bp_set_kernel_timing(bp_problem* p, int32_t enable);
 int bp_last_run_stats(const bp_problem* p, int64_t* kernel_launches, int64_t* active_sweeps,
                       double* row_kernel_ms, double* col_kernel_ms, int64_t* timed_sweeps);
 
+/* ---- overlapped solves (serving pattern; the reference solves one batch at a time and waits,
+ * proj/src/bench.cpp:143-151).  A pipeline owns `depth` handles of one shape (created by the
+ * caller, destroyed by the caller after bp_pipeline_destroy), each driven by its own host worker
+ * thread on the handle's own stream.  bp_pipeline_submit enqueues one job on the next slot
+ * (round robin) and returns at once; a job is exactly bp_problem_set_medium (k2 != NULL) or
+ * bp_problem_set_cdr_medium (bx != NULL) followed by bp_run on that slot, so while one slot
+ * sweeps, the next uploads its media/sources and the previous downloads its iterates.  All host
+ * buffers of a job must stay valid until bp_pipeline_wait returns; pinned buffers let the copies
+ * run under the other slots' sweeps.  bp_pipeline_wait blocks until every submitted job
+ * finished and returns the first job error (message in bp_last_error, prefixed by the slot). */
+typedef struct {
+    const double *k2, *k0, *eta;               /* Dirichlet / periodic Helmholtz media */
+    const double *bx, *by, *sigma, *sigma0;    /* CDR media (config c4) */
+} bp_medium;
+typedef struct bp_pipeline bp_pipeline;
+int bp_pipeline_create(bp_problem* const* slots, int32_t depth, bp_pipeline** out);
+int bp_pipeline_submit(bp_pipeline* pl, const bp_medium* medium, const bp_map* map, const double* f,
+                       const bp_iter_config* cfg, const double* u0, double* u_out, double* res_l2,
+                       double* res_reta, bp_trace* info, int32_t* slot_out);
+int bp_pipeline_wait(bp_pipeline* pl);
+int bp_pipeline_destroy(bp_pipeline* pl);
+
 /* ---- slab decomposition of ONE 2-D Dirichlet grid over nranks GPUs (config c2).
  * Rank r owns padded rows [r R, (r+1) R), R = (nx+1)/nranks.  The y-DSTs (rows) are local; the
  * x-DSTs need full columns, so the row side writes T blocked by destination rank

@@ -12,6 +12,7 @@ from .api import (  # noqa: F401
     IterationConfig,
     IterationTrace,
     OptimalScalarMap,
+    Pipeline,
     PointwiseMap,
     RunResult,
     ScalarMap,
@@ -22,7 +23,7 @@ from .instances import (CONFIGS, CdrSpec, InstanceSpec, config_instances,  # noq
 from . import _native, bpfd, slab  # noqa: F401
 
 __all__ = [
-    "CdrNeumann", "FourierDiagMap", "HelmholtzDirichlet", "HelmholtzPeriodic", "IterationConfig", "IterationTrace", "OptimalScalarMap", "PointwiseMap",
+    "CdrNeumann", "FourierDiagMap", "HelmholtzDirichlet", "HelmholtzPeriodic", "IterationConfig", "IterationTrace", "OptimalScalarMap", "Pipeline", "PointwiseMap",
     "RunResult", "ScalarMap", "run", "CONFIGS", "InstanceSpec", "config_instances",
     "make_instances", "CdrSpec", "make_cdr_instances",
 ]

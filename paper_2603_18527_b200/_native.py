@@ -55,6 +55,11 @@ class SlabView(C.Structure):
                 ("halo_elems", C.c_int64)]
 
 
+class Medium(C.Structure):
+    _fields_ = [("k2", _dp), ("k0", _dp), ("eta", _dp), ("bx", _dp), ("by", _dp), ("sigma", _dp),
+                ("sigma0", _dp)]
+
+
 class InstanceSpec(C.Structure):
     _fields_ = [("n", C.c_int32), ("ppw", C.c_double), ("contrast", C.c_double),
                 ("sigma_cells", C.c_double), ("src_sigma_cells", C.c_double),
@@ -111,6 +116,12 @@ ABI_FUNCTIONS = {
     "bp_run_snapshots": (C.c_int, [C.c_void_p, C.POINTER(Map), _dp, C.POINTER(IterConfig), _dp,
                                    _dp, _dp, _dp, C.POINTER(Trace), _dp, C.c_int32]),
     "bp_set_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+    "bp_pipeline_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_void_p)]),
+    "bp_pipeline_submit": (C.c_int, [C.c_void_p, C.POINTER(Medium), C.POINTER(Map), _dp,
+                                     C.POINTER(IterConfig), _dp, _dp, _dp, _dp, C.POINTER(Trace),
+                                     C.POINTER(C.c_int32)]),
+    "bp_pipeline_wait": (C.c_int, [C.c_void_p]),
+    "bp_pipeline_destroy": (C.c_int, [C.c_void_p]),
     "bp_last_run_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                     _dp, _dp, C.POINTER(C.c_int64)]),
 }

@@ -338,3 +338,103 @@ def run(problem: HelmholtzDirichlet, cmap, f, config: IterationConfig | None = N
     if snaps is not None and problem.single:
         snaps = snaps[:, 0]
     return RunResult(problem._out(u), traces, snaps)
+
+
+class Pipeline:
+    """Overlapped solves over ``depth`` problem handles of one shape (bp_pipeline_*): each
+    ``submit`` is ``set_medium`` (when a medium is given) + ``run`` on the next slot, executed by
+    that slot's native worker thread on the slot's own stream, so the PCIe copies of one job run
+    under the sweeps of the others.  The reference solves one batch at a time
+    (proj/src/bench.cpp:143-151); every job's result is bit-identical to calling
+    ``problem.set_medium(...)`` + ``run(problem, ...)`` directly.
+
+    ``submit`` returns a handle; ``wait()`` blocks for every submitted job and returns their
+    RunResults in submission order.  Host buffers are held until then (pass pinned arrays for
+    overlapped copies)."""
+
+    def __init__(self, problems):
+        self.problems = list(problems)
+        if not self.problems:
+            raise ValueError("Pipeline needs at least one problem handle")
+        p0 = self.problems[0]
+        for p in self.problems[1:]:
+            if type(p) is not type(p0) or p.shape != p0.shape:
+                raise ValueError("Pipeline slots must be problems of one family and shape")
+        self._lib = N.lib()
+        hs = (C.c_void_p * len(self.problems))(*[p.handle for p in self.problems])
+        h = C.c_void_p()
+        _check(self._lib.bp_pipeline_create(hs, len(self.problems), C.byref(h)))
+        self._h = h
+        self._jobs = []
+
+    def submit(self, cmap, f, config: IterationConfig | None = None, medium=None, u0=None,
+               u_out=None) -> int:
+        """medium: None (keep the slot's medium), (k2, k0, eta) for Helmholtz problems or
+        (bx, by, sigma[, sigma0]) for CdrNeumann.  u_out: optional preallocated (pinned) output
+        of the problem's shape.  Returns the job index into wait()'s list."""
+        config = config or IterationConfig()
+        p = self.problems[0]
+        f = p._field(f)
+        u0 = None if u0 is None else p._field(u0)
+        u = np.empty_like(f) if u_out is None else u_out
+        if u.shape != f.shape or u.dtype != f.dtype or not u.flags["C_CONTIGUOUS"]:
+            raise ValueError("u_out must be a C-contiguous array of the problem's shape and dtype")
+        keep = []
+        md = N.Medium()
+        if medium is not None:
+            if isinstance(p, CdrNeumann):
+                bx, by, sg = (p._field(a) for a in medium[:3])
+                s0 = medium[3] if len(medium) > 3 and medium[3] is not None else \
+                    sg.reshape(p.batch, -1).mean(axis=1)
+                s0 = np.ascontiguousarray(np.broadcast_to(np.asarray(s0, np.float64), (p.batch,)))
+                md.bx, md.by, md.sigma, md.sigma0 = _ptr(bx), _ptr(by), _ptr(sg), _ptr(s0)
+                keep += [bx, by, sg, s0]
+            else:
+                k2 = p._field(medium[0])
+                k0 = np.ascontiguousarray(np.broadcast_to(np.asarray(medium[1], np.float64), (p.batch,)))
+                eta = np.ascontiguousarray(np.broadcast_to(np.asarray(medium[2], np.float64), (p.batch,)))
+                md.k2, md.k0, md.eta = _ptr(k2), _ptr(k0), _ptr(eta)
+                keep += [k2, k0, eta]
+        stride = config.max_iters + 1
+        l2 = np.empty((p.batch, stride))
+        rt = np.empty((p.batch, stride))
+        info = (N.Trace * p.batch)()
+        mp, cfg = cmap._c(), config._c()
+        slot = C.c_int32()
+        _check(self._lib.bp_pipeline_submit(self._h, C.byref(md), C.byref(mp), _ptr(f), C.byref(cfg),
+                                            _ptr(u0), _ptr(u), _ptr(l2), _ptr(rt), info,
+                                            C.byref(slot)))
+        self._jobs.append((slot.value, u, l2, rt, info, keep + [f, u0, md, mp, cfg, cmap]))
+        return len(self._jobs) - 1
+
+    def wait(self) -> list:
+        """Block until every submitted job finished; RunResults in submission order."""
+        rc = self._lib.bp_pipeline_wait(self._h)
+        jobs, self._jobs = self._jobs, []
+        _check(rc)
+        out = []
+        for slot, u, l2, rt, info, _ in jobs:
+            p = self.problems[slot]
+            traces = []
+            for b in range(p.batch):
+                k = info[b].iters + 1
+                traces.append(IterationTrace(l2[b, :k].copy(), rt[b, :k].copy(), info[b].iters,
+                                             TERMINATION[info[b].terminated], info[b].fnorm_l2,
+                                             info[b].fnorm_reta))
+            out.append(RunResult(p._out(u), traces, None))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.bp_pipeline_wait(self._h)
+            self._lib.bp_pipeline_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        self.close()

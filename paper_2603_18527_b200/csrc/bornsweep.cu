@@ -1445,6 +1445,9 @@ extern "C" {
 const char* bp_last_error(void) { return g_err.c_str(); }
 int bp_abi_version(void) { return BP_ABI_VERSION; }
 
+// for the host-side pipeline TU (pipeline.cpp): set this thread's bp_last_error() message
+int bp_internal_set_error(int code, const char* msg) { return set_err(code, msg ? msg : ""); }
+
 }  // extern "C"
 
 namespace {

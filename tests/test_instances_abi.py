@@ -120,3 +120,17 @@ def test_sm100a_code_in_library():
         pytest.skip("cuobjdump absent")
     out = subprocess.run([tool, "--list-elf", N.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_pipeline_argument_errors_without_gpu():
+    """bp_pipeline_* validate their arguments before any CUDA call (BP_EINVAL + message)."""
+    lib = N.lib()
+    out = C.c_void_p()
+    assert lib.bp_pipeline_create(None, 2, C.byref(out)) == 1
+    assert "null" in N.last_error()
+    slots = (C.c_void_p * 2)(None, None)
+    assert lib.bp_pipeline_create(slots, 2, C.byref(out)) == 1
+    assert "slot" in N.last_error()
+    assert lib.bp_pipeline_create(slots, 0, C.byref(out)) == 1
+    assert lib.bp_pipeline_wait(None) == 1
+    assert lib.bp_pipeline_destroy(None) == 0
