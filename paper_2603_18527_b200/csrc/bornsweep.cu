@@ -1256,6 +1256,10 @@ int cdr_download(bp_problem* p, const double2* src, double* dst, bool host_ptr =
 //   which 0 G, 2 L_ref, 3 forward transform, 4 inverse transform; out - sub when sub != null
 int cdr_apply(bp_problem* p, int which, const double2* in, double2* out, const double2* sub) {
     CdrArgs a = cdr_args(p);
+    // operator applications act on every member: the column kernel's skip of terminated
+    // members (ctl.status) belongs to the sweep only -- left set, a member that terminated in
+    // the handle's previous run kept its forward transform here (||G f|| of the next run wrong)
+    a.ctl.status = nullptr;
     const double inv = 1.0 / (4.0 * (double)p->n * p->n);
     a.in = reinterpret_cast<const double*>(in);
     a.out = reinterpret_cast<double*>(out);

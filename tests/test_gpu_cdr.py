@@ -157,3 +157,21 @@ def test_cdr_set_medium_equals_fresh_handle(gpu):
     with bs.CdrNeumann(bx2, by2, sigma2, s02) as q:
         fresh = bs.run(q, bs.ScalarMap(1.0), f, cfg)
     assert np.array_equal(swapped.u, fresh.u)
+
+
+def test_cdr_repeated_runs_and_operators_after_run(gpu):
+    """A second run on the same handle reproduces the first bit for bit (incl. ||G f|| and the
+    R_eta trace), and apply_G after a run still acts on every member (regression: the column
+    kernel skipped members the previous run had terminated)."""
+    bx, by, sigma, s0, f = media(64, 2, seed=5)
+    cfg = bs.IterationConfig("cbs", 1e-8, 200)
+    with bs.CdrNeumann(bx, by, sigma, s0) as p:
+        g0 = p.apply_G(f)
+        r1 = bs.run(p, bs.ScalarMap(1.0), f, cfg)
+        r2 = bs.run(p, bs.ScalarMap(1.0), f, cfg)
+        g1 = p.apply_G(f)
+    assert np.array_equal(g0, g1)
+    assert np.array_equal(r1.u, r2.u)
+    for t1, t2 in zip(r1.traces, r2.traces):
+        assert t1.fnorm_reta == t2.fnorm_reta and abs(t1.res_reta_rel[0] - 1.0) < 1e-14
+        assert np.array_equal(t1.res_reta_rel, t2.res_reta_rel)
