@@ -1110,8 +1110,11 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
     }
 }
 
+#ifndef BS_COL_REGS
+#define BS_COL_REGS 128  // register budget the column kernel's launch bounds are sized for (P = 16)
+#endif
 template <int LOG2N, int MODE, int C, int PP, int LAYOUT = CL_PLANE>
-__global__ void __launch_bounds__(C * Geom<LOG2N, PP>::T, (MinBlocks<C * Geom<LOG2N, PP>::T, PP >= 16 ? 128 : 64>::value))
+__global__ void __launch_bounds__(C * Geom<LOG2N, PP>::T, (MinBlocks<C * Geom<LOG2N, PP>::T, PP >= 16 ? BS_COL_REGS : 64>::value))
 col_kernel(const ColArgs a) {
     col_group<LOG2N, MODE, C, PP, LAYOUT>(a, blockIdx.x);
 }

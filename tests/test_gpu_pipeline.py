@@ -11,6 +11,8 @@ pytestmark = pytest.mark.gpu
 
 
 def _same(ra, rb):
+    for t in ra.traces:  # r^0 = f: entry 0 of the R_eta trace is 1 (iterate.cpp:93-102)
+        assert abs(t.res_reta_rel[0] - 1.0) < 1e-12
     assert np.array_equal(ra.u, rb.u)
     for ta, tb in zip(ra.traces, rb.traces):
         assert ta.iters == tb.iters and ta.terminated == tb.terminated
