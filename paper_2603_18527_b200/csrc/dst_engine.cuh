@@ -480,7 +480,12 @@ struct DstEngine {
     // Same transform with the line already in buf (natural order at pidx(j)): the mirror
     // x_{N-j} is read from shared memory as each element is pre-processed, so neither the
     // line nor its mirror has to be held in registers.  v: scratch of P registers.
-    template <class Pol>
+    // DENSE: the line sits UNPADDED in buf (x_j at buf[j]).  The mirror reads of one 8-lane
+    // phase, x_{N-t-Tm} for 8 consecutive t, are 8 consecutive elements that straddle an 8-block
+    // boundary; under the pidx padding every such phase is a 2-way bank conflict (91 % of the
+    // row kernel's excess wavefronts, r01c), unpadded any 8 consecutive elements hit 8 distinct
+    // 16-byte bank groups.  The passes after the pre-processing use the padded layout as before.
+    template <bool DENSE = false, class Pol>
     __device__ __forceinline__ static void run_smem(double2 (&v)[P], double2 (&y)[P], int t, double2* buf,
                                                     const double2* __restrict__ tw,
                                                     const double* __restrict__ sinp, const Pol& pol) {
@@ -491,8 +496,9 @@ struct DstEngine {
 #pragma unroll
         for (int m = 0; m < P; ++m) {
             const int j = t + T * m;
-            const double2 x = buf[G::at_stride(t, bt, m)];
-            const int mi = t == 0 ? G::pidx((N - T * m) & (N - 1)) : G::at_stride(tm, btm, P - 1 - m);
+            const double2 x = DENSE ? buf[j] : buf[G::at_stride(t, bt, m)];
+            const int mi = DENSE ? ((N - j) & (N - 1))
+                                 : t == 0 ? G::pidx((N - T * m) & (N - 1)) : G::at_stride(tm, btm, P - 1 - m);
             const double2 xm = buf[mi];
             v[m] = (j == 0) ? make_double2(0.0, 0.0) : pre_s(x, xm, sin2(sinp, t, m, st, ct));
         }

@@ -430,11 +430,11 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         if constexpr (RSM) {
             prefetch_row();
 #pragma unroll
-            for (int mm = 0; mm < P; ++mm) buf[G::at_stride(t, G::pidx(t), mm)] = xT[mm];  // invalid lines: discarded
+            for (int mm = 0; mm < P; ++mm) buf[t + T * mm] = xT[mm];  // unpadded (run_smem<true>); invalid lines: discarded
             pol.sync();
             {
                 double2 v[P];
-                Engine::run_smem(v, y, t, buf, a.tw, a.sinp, pol);
+                Engine::template run_smem<true>(v, y, t, buf, a.tw, a.sinp, pol);
             }
 #pragma unroll
             for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y[l];
