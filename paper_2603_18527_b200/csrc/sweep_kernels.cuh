@@ -1049,10 +1049,10 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
-        buf[G::at_stride(t, G::pidx(t), mm)] = a.T[gidx(j)];
+        buf[j] = a.T[gidx(j)];  // unpadded: conflict-free mirror reads in run_smem<true>
     }
     pol.sync();
-    Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
+    Engine::template run_smem<true>(x, y, t, buf, a.tw, a.sinp, pol);
     } else {
         double2 xm[P];
 #pragma unroll
