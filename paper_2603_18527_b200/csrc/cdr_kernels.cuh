@@ -340,8 +340,9 @@ ccol_kernel(const CdrArgs a) {
     int c, t;
     col_thread_map<G::T, C>(t, c);
     constexpr int GROUPS = N / (2 * C);  // C packed column pairs per CTA
-    const int b = blockIdx.x / GROUPS;
-    const int q0 = (blockIdx.x % GROUPS) * 2 * C + 2 * c;  // real columns q0, q0 + 1
+    const int bid = BS_COL_REVERSE && a.batch > 1 ? gridDim.x - 1 - blockIdx.x : blockIdx.x;  // (col_kernel)
+    const int b = bid / GROUPS;
+    const int q0 = (bid % GROUPS) * 2 * C + 2 * c;  // real columns q0, q0 + 1
     if (a.ctl.status && __ldcg(&a.ctl.status[b]) != ST_ACTIVE) return;
     double2* buf = smem + c * G::PAD_N;
     const BlockSeg<T, C> pol{smem + C * G::PAD_N, c};

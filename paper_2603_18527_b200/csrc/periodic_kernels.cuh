@@ -166,8 +166,9 @@ pcol_kernel(const PerArgs a) {
     int c, t;
     col_thread_map<G::T, C>(t, c);
     constexpr int GROUPS = N / C;
-    const int b = blockIdx.x / GROUPS;
-    const int q = (blockIdx.x % GROUPS) * C + c;
+    const int bid = BS_COL_REVERSE && a.batch > 1 ? gridDim.x - 1 - blockIdx.x : blockIdx.x;  // (col_kernel)
+    const int b = bid / GROUPS;
+    const int q = (bid % GROUPS) * C + c;
     int mstep = 0;
     if constexpr (MODE == CP_SWEEP) {
         if (__ldcg(&a.ctl.status[b]) != ST_ACTIVE) return;  // uniform per CTA
@@ -243,7 +244,7 @@ pcol_kernel(const PerArgs a) {
                     r += red[0][k];
                     xx += red[1][k];
                 }
-                const int g = blockIdx.x % GROUPS;
+                const int g = bid % GROUPS;
                 double* pr = a.ctl.partial + ((size_t)b * N + g) * kPartStride;
                 pr[0] = r;
                 pr[1] = xx;
