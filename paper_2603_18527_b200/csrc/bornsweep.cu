@@ -393,6 +393,11 @@ struct bp_problem {
     double2 graph_gamma{};
     int graph_max_iters = -1;
     double graph_rtol = -1;
+    // compute hooks (bp_internal_set_compute_hooks; the pipeline's FIFO compute turn): called
+    // around the sweeps of a run, after its uploads were enqueued and before its downloads
+    void (*hook_pre)(void*) = nullptr;
+    void (*hook_post)(void*) = nullptr;
+    void* hook_ctx = nullptr;
     // instrumentation
     bool timing = false;
     int64_t stat_launches = 0, stat_sweeps = 0, stat_timed = 0;
@@ -1451,6 +1456,14 @@ int bp_abi_version(void) { return BP_ABI_VERSION; }
 
 // for the host-side pipeline TU (pipeline.cpp): set this thread's bp_last_error() message
 int bp_internal_set_error(int code, const char* msg) { return set_err(code, msg ? msg : ""); }
+// for pipeline.cpp: hooks run around the sweeps of every later run on this handle (null: none)
+int bp_internal_set_compute_hooks(bp_problem* p, void (*pre)(void*), void (*post)(void*), void* ctx) {
+    if (int rc = check_problem(p)) return rc;
+    p->hook_pre = pre;
+    p->hook_post = post;
+    p->hook_ctx = ctx;
+    return BP_OK;
+}
 
 }  // extern "C"
 
@@ -2376,6 +2389,20 @@ int bp_inverse_transform(const bp_problem* p, const double* modes, double* field
     return spectral_op(p, 4, modes, nullptr, field);
 }
 
+// Holds the handle's compute turn (if hooks are set) from construction to release().
+struct ComputeTurn {
+    bp_problem* p;
+    bool held;
+    explicit ComputeTurn(bp_problem* pp) : p(pp), held(pp->hook_pre != nullptr) {
+        if (held) p->hook_pre(p->hook_ctx);
+    }
+    void release() {
+        if (held) p->hook_post(p->hook_ctx);
+        held = false;
+    }
+    ~ComputeTurn() { release(); }
+};
+
 static int run_impl(const bp_problem* cp, const bp_map* map, const double* f, const bp_iter_config* cfg,
                     const double* u0, double* u_out, double* res_l2, double* res_reta, bp_trace* info,
                     bool host_ptr, double* snapshots, int n_snap) {
@@ -2388,15 +2415,19 @@ static int run_impl(const bp_problem* cp, const bp_map* map, const double* f, co
         if (int rc = cdr_upload(p, f, p->f, host_ptr)) return rc;
         if (u0)
             if (int rc = cdr_upload(p, u0, p->u0, host_ptr)) return rc;
+        ComputeTurn turn(p);
         if (int rc = run_core_cdr(p, map, cfg, u0 != nullptr, snapshots, n_snap)) return rc;
+        turn.release();
         return finish_run(p, cfg, u_out, host_ptr, res_l2, res_reta, info);
     }
     if (int rc = upload(p, f, p->f, host_ptr)) return rc;
     if (u0)  // periodic: the physical u0 is transformed into U^0 by run_core_periodic
         if (int rc = upload(p, u0, p->periodic ? p->x : p->u0, host_ptr)) return rc;
+    ComputeTurn turn(p);
     const int rc = p->periodic ? run_core_periodic(p, map, cfg, u0 != nullptr, snapshots, n_snap)
                                : run_core(p, map, cfg, u0 != nullptr, snapshots, n_snap);
     if (rc) return rc;
+    turn.release();
     return finish_run(p, cfg, u_out, host_ptr, res_l2, res_reta, info);
 }
 

@@ -7,7 +7,11 @@
 // handle's own non-blocking stream: while slot s sweeps, slot s+1 uploads the next batch and the
 // previous slot downloads its result, so in steady state the copy engines run under the sweeps.
 // Every job is exactly bp_problem_set_medium / bp_problem_set_cdr_medium + bp_run on its slot;
-// results are bit-identical to calling those two entry points directly.
+// results are bit-identical to calling those two entry points directly.  The sweeps themselves
+// take FIFO turns (a ticket per job, handed over through compute hooks the run calls after its
+// uploads were enqueued and before its downloads), so only the copies overlap: two solves never
+// share the SMs, and the pipeline's throughput is the single-handle sweep rate minus the copy
+// time it could not hide.
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
@@ -18,8 +22,11 @@
 
 #include "bornsweep.h"
 
-// defined in bornsweep.cu: sets the calling thread's bp_last_error() message
+// defined in bornsweep.cu: sets the calling thread's bp_last_error() message; installs the
+// hooks a run calls around its sweeps
 extern "C" int bp_internal_set_error(int code, const char* msg);
+extern "C" int bp_internal_set_compute_hooks(bp_problem* p, void (*pre)(void*), void (*post)(void*),
+                                             void* ctx);
 
 namespace {
 
@@ -33,12 +40,17 @@ struct Job {
     double* res_l2;
     double* res_reta;
     bp_trace* info;
+    int64_t ticket;  // submission order = compute order
 };
 
 struct Slot {
     bp_problem* p = nullptr;
     std::thread worker;
     std::deque<Job> queue;
+    // compute-turn state of the slot's running job (guarded by bp_pipeline::m)
+    bp_pipeline* pl = nullptr;
+    int64_t ticket = -1;
+    bool turn_done = false;
 };
 
 }  // namespace
@@ -50,11 +62,30 @@ struct bp_pipeline {
     bool stop = false;
     int64_t pending = 0;  // submitted and not finished
     int next = 0;
+    int64_t next_ticket = 0;   // assigned at submit
+    int64_t compute_turn = 0;  // ticket whose sweeps may run now
+    std::condition_variable cv_turn;
     int err_code = BP_OK;
     std::string err_msg;
 };
 
 namespace {
+
+void turn_acquire(void* ctx) {
+    auto* sl = static_cast<Slot*>(ctx);
+    std::unique_lock<std::mutex> lk(sl->pl->m);
+    sl->pl->cv_turn.wait(lk, [&] { return sl->pl->compute_turn == sl->ticket; });
+}
+
+void turn_release(void* ctx) {
+    auto* sl = static_cast<Slot*>(ctx);
+    {
+        std::lock_guard<std::mutex> lk(sl->pl->m);
+        ++sl->pl->compute_turn;
+        sl->turn_done = true;
+    }
+    sl->pl->cv_turn.notify_all();
+}
 
 int run_job(bp_problem* p, const Job& j) {
     const bp_medium& md = j.medium;
@@ -74,8 +105,14 @@ void worker_loop(bp_pipeline* pl, int s) {
             pl->cv_work.wait(lk, [&] { return pl->stop || !pl->slots[s].queue.empty(); });
             if (pl->slots[s].queue.empty()) return;  // stop requested and nothing left
             job = pl->slots[s].queue.front();
+            pl->slots[s].ticket = job.ticket;
+            pl->slots[s].turn_done = false;
         }
         const int rc = run_job(pl->slots[s].p, job);
+        if (!pl->slots[s].turn_done) {  // failed before its sweeps: pass the turn on in order
+            turn_acquire(&pl->slots[s]);
+            turn_release(&pl->slots[s]);
+        }
         const std::string msg = rc ? std::string(bp_last_error()) : std::string();
         {
             std::lock_guard<std::mutex> lk(pl->m);
@@ -99,9 +136,23 @@ int bp_pipeline_create(bp_problem* const* slots, int32_t depth, bp_pipeline** ou
     *out = nullptr;
     for (int s = 0; s < depth; ++s)
         if (!slots[s]) return bp_internal_set_error(BP_EINVAL, "pipeline: null slot handle");
+    for (int s = 0; s < depth; ++s)
+        for (int r = 0; r < s; ++r)
+            if (slots[r] == slots[s])  // one worker thread per handle
+                return bp_internal_set_error(BP_EINVAL, "pipeline: the same handle in two slots");
     auto* pl = new bp_pipeline;
     pl->slots.resize(depth);
-    for (int s = 0; s < depth; ++s) pl->slots[s].p = slots[s];
+    for (int s = 0; s < depth; ++s) {
+        pl->slots[s].p = slots[s];
+        pl->slots[s].pl = pl;
+    }
+    for (int s = 0; s < depth; ++s) {
+        if (int rc = bp_internal_set_compute_hooks(slots[s], turn_acquire, turn_release, &pl->slots[s])) {
+            for (int r = 0; r < s; ++r) bp_internal_set_compute_hooks(slots[r], nullptr, nullptr, nullptr);
+            delete pl;
+            return rc;
+        }
+    }
     for (int s = 0; s < depth; ++s) pl->slots[s].worker = std::thread(worker_loop, pl, s);
     *out = pl;
     return BP_OK;
@@ -127,6 +178,7 @@ int bp_pipeline_submit(bp_pipeline* pl, const bp_medium* medium, const bp_map* m
         std::lock_guard<std::mutex> lk(pl->m);
         s = pl->next;
         pl->next = (pl->next + 1) % (int)pl->slots.size();
+        j.ticket = pl->next_ticket++;
         pl->slots[s].queue.push_back(j);
         ++pl->pending;
     }
@@ -153,6 +205,7 @@ int bp_pipeline_destroy(bp_pipeline* pl) {
     pl->cv_work.notify_all();
     for (auto& s : pl->slots)
         if (s.worker.joinable()) s.worker.join();
+    for (auto& s : pl->slots) bp_internal_set_compute_hooks(s.p, nullptr, nullptr, nullptr);
     delete pl;
     return BP_OK;
 }
