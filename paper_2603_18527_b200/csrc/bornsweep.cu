@@ -608,6 +608,7 @@ int col_stage(bp_problem* p, const ColArgs& c0, int mode, double scale) {
     c.planes_per_member = p->n;
     c.scale = 1.0;
     if (launch_col(p->log2n, CL_PLANE, C_ONE, c, p->stream) != cudaSuccess) return -1;
+    c.finalize = 0;  // deferred finalisation (3-D) belongs to the first launch only
     c.scale = scale;
     if (launch_col(p->log2n, CL_X3, mode, c, p->stream) != cudaSuccess) return -1;
     if (mode == C_ONE) return 2;
@@ -821,11 +822,14 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     // scalar / pointwise 2-D sweeps: the column pass finalises the entry the row pass before
     // it reduced (RowArgs::defer_final / ColArgs::finalize); not for the initial column pass
     // (n >= 64: the column CTA has at least one full warp for finalize_member's shuffles)
-    if (!mixed && !p->transposed && p->dim == 2 && p->log2n >= 6 && plan.n == 2 && plan.row[0] &&
-        plan.mode[0] == R_SWEEP && !plan.row[1] && plan.mode[1] == C_GREEN) {
+    // 3-D: the first (y-line) launch of the column stage finalises, the whole CTA summing the
+    // n^2 line partials (finalize_member3; col_stage clears the flag for the other two)
+    if (!mixed && !p->transposed && (p->dim == 2 || p->dim == 3) && p->log2n >= 6 && plan.n == 2 &&
+        plan.row[0] && plan.mode[0] == R_SWEEP && !plan.row[1] && plan.mode[1] == C_GREEN) {
         a.defer_final = 1;
         c.finalize = 1;
-        c.fin_lsh = p->log2n;
+        c.fin_lsh = (p->dim - 1) * p->log2n;
+        c.fin_step = row_lines_per_cta(p->log2n, points_per_thread(p->log2n));
         c.ctl = a.ctl;
     }
 

@@ -173,6 +173,7 @@ struct ColArgs {
     // termination test (finalize_entry); ctl as in RowArgs, log2 rows per member = fin_lsh
     int finalize;
     int fin_lsh;
+    int fin_step;  // 3-D: lines per row CTA (one partial per row CTA, finalize_member3)
     Control ctl;
     // 3-D slabs: CL_YBLK y-lines of the rank's R = 2^slab_log2 x-planes in the blocked layout
     // of t_index<DIM = 3, SLAB>; CL_SLAB with slab3 != 0: the received block's columns are
@@ -664,7 +665,27 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         for (int k = 0; k < S::NPART; ++k) acc[k] = pol.sum(acc[k], t);
         if constexpr (MODE == R_SWEEP && !SLAB) {
             if (a.defer_final) {  // finalised by the next launch (col_group, ColArgs::finalize)
-                if (valid && t == 0) {
+                if constexpr (DIM == 3) {
+                    // one partial per CTA (its EPB lines summed in engine order), stored in the
+                    // slot of the CTA's first line: n^2 / EPB values for the finalising CTA
+                    __shared__ double cpart[EPB][2];
+                    if (t == 0) {
+                        cpart[e][0] = valid ? acc[0] : 0.0;
+                        cpart[e][1] = valid ? acc[1] : 0.0;
+                    }
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        double s0 = 0.0, s1 = 0.0;
+                        for (int k = 0; k < EPB; ++k) {
+                            s0 += cpart[k][0];
+                            s1 += cpart[k][1];
+                        }
+                        const long g0 = grp * EPB;  // first line of the CTA (members hold whole CTAs)
+                        double* pr = a.ctl.partial + (size_t)g0 * kPartStride;
+                        pr[0] = s0;
+                        pr[1] = s1;
+                    }
+                } else if (valid && t == 0) {
                     double* pr = a.ctl.partial + (((size_t)b << lsh) + i) * kPartStride;
 #pragma unroll
                     for (int k = 0; k < S::NPART; ++k) pr[k] = acc[k];
@@ -820,6 +841,18 @@ struct ColGeom {
 //           CL_YBLK: 3-D slab y-lines on the dest-blocked layout (t_index<3, true>).
 enum ColLayout { CL_PLANE = 0, CL_X3 = 2, CL_SLAB = 3, CL_YBLK = 4 };
 
+#ifndef BS_COL_REVERSE
+#define BS_COL_REVERSE 1
+#endif
+// One plane (a single 2-D grid, c2) has no member/plane order to exploit: kept forward
+// (measured: c2 column 490 us forward vs 512 reversed; c1 -1 %, c3 -1 %, c4 -7 % reversed).
+template <int LAYOUT>
+__device__ __forceinline__ bool col_reversed(const ColArgs& a) {
+    const bool one_plane = (LAYOUT == CL_PLANE && (long)a.batch * a.planes_per_member == 1) ||
+                           (LAYOUT == CL_SLAB && a.batch == 1);
+    return BS_COL_REVERSE && !one_plane;
+}
+
 // Deferred finalisation of trace entry m for member b (ColArgs::finalize): one warp sums the
 // per-row partials of the preceding R_SWEEP launch in the row kernel's own order (lane r over
 // rows r, r+32, ...; xor-shuffle tree) and runs finalize_entry.  Visibility of the partials
@@ -840,6 +873,46 @@ __device__ __forceinline__ void finalize_member(const ColArgs& a, int b, int nli
         s1 += __shfl_xor_sync(0xffffffffu, s1, d);
     }
     if (lane == 0) finalize_entry(a.ctl, b, m, s0, s1);
+}
+
+// 3-D variant (ColArgs::finalize on the first y-line launch of the column stage): the whole CTA
+// sums the member's per-row-CTA partials -- lane-strided, then a fixed-order warp and CTA
+// tree -- and thread 0 runs finalize_entry.  Previously the 3-D row
+// kernel's last engine did this alone (16 lanes over 65536 lines at n = 256): a ~600 us
+// single-SM tail on a ~340 us launch (ncu sm__cycles_active min 650 K vs max 1.81 M, r01c).
+// The row kernel leaves one partial per row CTA (a.fin_step lines, padding lines contributing 0)
+// in the slot of the CTA's first line; CTAs of the padding x-plane 0 exit without one.
+template <int LOG2N>
+__device__ __forceinline__ void finalize_member3(const ColArgs& a, int b) {
+    constexpr int N = 1 << LOG2N;
+    __shared__ double red[2][32];
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, w = tid >> 5;
+    const int m = __ldcg(&a.ctl.sweep[b]);
+    double s0 = 0.0, s1 = 0.0;
+    const double* base = a.ctl.partial + ((size_t)b << (2 * LOG2N)) * kPartStride;
+    const int step = a.fin_step;
+    for (int r = N + tid * step; r < N * N; r += nthr * step) {  // from x-plane 1
+        s0 += __ldcg(base + (size_t)r * kPartStride);
+        s1 += __ldcg(base + (size_t)r * kPartStride + 1);
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, d);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, d);
+    }
+    if (lane == 0) {
+        red[0][w] = s0;
+        red[1][w] = s1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int k = 0; k < (nthr + 31) / 32; ++k) {
+            t0 += red[0][k];
+            t1 += red[1][k];
+        }
+        finalize_entry(a.ctl, b, m, t0, t1);
+    }
 }
 
 // Column group with warp-private engines (lines of T <= 32 threads): the CTA stages its C
@@ -886,6 +959,11 @@ __device__ __forceinline__ void col_group_w(const ColArgs& a, const int bid) {
         if constexpr (LAYOUT == CL_PLANE) {
             if (a.finalize && active && a.planes_per_member == 1 && (bid % GROUPS) == 0 && threadIdx.x < 32)
                 finalize_member(a, b, 1 << a.fin_lsh);
+            if (a.finalize && active && a.planes_per_member > 1) {  // 3-D (see col_group)
+                const int pim = (bid / GROUPS) & (N - 1), g = bid % GROUPS;
+                if (col_reversed<LAYOUT>(a) ? (pim == N - 1 && g == GROUPS - 1) : (pim == 1 && g == 0))
+                    finalize_member3<LOG2N>(a, b);
+            }
         }
         if (!active) return;  // uniform per CTA
     }
@@ -1033,6 +1111,13 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
         if constexpr (LAYOUT == CL_PLANE) {
             if (a.finalize && active && a.planes_per_member == 1 && (bid % GROUPS) == 0 && threadIdx.x < 32)
                 finalize_member(a, b, 1 << a.fin_lsh);
+            if (a.finalize && active && a.planes_per_member > 1) {
+                // 3-D: the member's first-dispatched CTA (reversed order: its last valid plane
+                // and group; forward: plane 1, group 0) finalises -- CTA-uniform condition
+                const int pim = (bid / GROUPS) & (N - 1), g = bid % GROUPS;
+                if (col_reversed<LAYOUT>(a) ? (pim == N - 1 && g == GROUPS - 1) : (pim == 1 && g == 0))
+                    finalize_member3<LOG2N>(a, b);
+            }
         }
         if (!active) return;  // uniform per CTA
     }
@@ -1110,9 +1195,6 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
     }
 }
 
-#ifndef BS_COL_REVERSE
-#define BS_COL_REVERSE 1
-#endif
 #ifndef BS_COL_REGS
 #define BS_COL_REGS 128  // register budget the column kernel's launch bounds are sized for (P = 16)
 #endif
@@ -1123,12 +1205,7 @@ col_kernel(const ColArgs a) {
     // CTAs by increasing index, so the column pass starts on the last members the row pass
     // wrote (their T still in L2) and ends on the first ones, which the next row pass then
     // reads first, again from L2: each handoff reuses the L2-resident tail of the other pass.
-    // One plane (a single 2-D grid, c2) has no member/plane order to exploit: kept forward
-    // (measured: c2 column 490 us forward vs 512 reversed; c1 -1 %, c3 -1 %, c4 -7 % reversed).
-    const bool one_plane = (LAYOUT == CL_PLANE && (long)a.batch * a.planes_per_member == 1) ||
-                           (LAYOUT == CL_SLAB && a.batch == 1);
-    const bool rev = BS_COL_REVERSE && !one_plane;
-    col_group<LOG2N, MODE, C, PP, LAYOUT>(a, rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
+    col_group<LOG2N, MODE, C, PP, LAYOUT>(a, col_reversed<LAYOUT>(a) ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
 }
 
 // ------------------------------------------------------------------ mixed (pipelined) kernel

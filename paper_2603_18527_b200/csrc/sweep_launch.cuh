@@ -27,6 +27,13 @@ struct ColCols {
     static constexpr int value = L == 9 ? BS_COLC9 : L <= 8 ? 8 : (L == 10 ? 4 : 2);
 };
 
+// lines per Dirichlet row-kernel CTA (RowGeom::EPB of the launched instance), for the host
+inline int row_lines_per_cta(int log2n, int pp) {
+    const int n = 1 << log2n, p = (n / 2) < pp ? (n / 2) : pp, t = n / p;
+    const int nw = t <= 32 ? BS_ROW_NW : kRowWarps;
+    return nw * 32 / t;
+}
+
 template <int L, int MODE, int PP, int DIM, bool TOUT = false, bool SLAB = false>
 cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
     constexpr int NWR = RowWarps<L, PP>::value;

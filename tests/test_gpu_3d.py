@@ -87,3 +87,32 @@ def test_config3_first_sweeps(gpu):
     assert res.trace.iters == ref.iters == K
     np.testing.assert_allclose(res.trace.res_l2_rel, ref.res_l2, rtol=1e-8)
     assert rel(res.u, ref.u) < FIELD_TOL
+
+
+@pytest.mark.parametrize("n", [64, 128])
+def test_3d_batch_deferred_finalisation(gpu, n):
+    """3-D batches: the trace entry is finalised by the first column launch from one partial per
+    row CTA (finalize_member3).  Members terminate independently, each bit-identical to its
+    single-member run, and the iteration counts / first iterates agree with the oracle."""
+    Oracle.set_threads(os.cpu_count() or 8)
+    k2, f, k0, eta = inst3(n, batch=3, seed=7, contrast=0.3, ppw=10.0)
+    cfg = bs.IterationConfig(rtol=1e-5, max_iters=3000 if n == 64 else 6)
+    with bs.HelmholtzDirichlet(k2, k0, eta, dim=3) as p:
+        res = bs.run(p, bs.PointwiseMap(), f, cfg)
+    for b in range(3):
+        with bs.HelmholtzDirichlet(k2[b:b + 1], k0[b:b + 1], eta[b:b + 1], dim=3) as q:
+            one = bs.run(q, bs.PointwiseMap(), f[b:b + 1], cfg)
+        assert np.array_equal(res.u[b], one.u[0])
+        assert res.traces[b].iters == one.traces[0].iters
+        assert np.array_equal(res.traces[b].res_l2_rel, one.traces[0].res_l2_rel)
+        assert np.array_equal(res.traces[b].res_reta_rel, one.traces[0].res_reta_rel)
+    ref = OracleProblem(k2[0], k0[0], eta[0]).run(f[0], map_kind=MAP_POINTWISE, rtol=1e-5,
+                                                   max_iters=cfg.max_iters)
+    t = res.traces[0]
+    assert t.terminated == ref.terminated
+    assert abs(t.iters - ref.iters) <= 1
+    k = min(t.iters, ref.iters) + 1
+    np.testing.assert_allclose(t.res_l2_rel[:k], ref.res_l2[:k], rtol=1e-8)
+    np.testing.assert_allclose(t.res_reta_rel[:k], ref.res_reta[:k], rtol=1e-8)
+    if t.iters == ref.iters:
+        assert rel(res.u[0], ref.u) < FIELD_TOL
