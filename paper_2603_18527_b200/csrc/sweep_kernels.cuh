@@ -704,6 +704,58 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
                                          : VALID_LINES;
             last = (old == nvalid - 1u);
         }
+        if constexpr (DIM == 3) {
+            // 3-D: the member's n^2 line partials are summed by the whole last CTA (a CTA holds
+            // lines of one member once 2^lsh >= EPB) -- one engine of 16 lanes took ~600 us
+            // at n = 256 (single-SM tail, r01c); strided per thread, fixed-order tree
+            if ((1L << lsh) >= EPB) {
+                if (!__syncthreads_or(last)) return;
+                __threadfence();
+                __shared__ double red[S::NPART][32];
+                double s[S::NPART];
+#pragma unroll
+                for (int k = 0; k < S::NPART; ++k) s[k] = 0.0;
+                for (int r = threadIdx.x; r < (1 << lsh); r += blockDim.x) {
+                    if ((r & (N - 1)) == 0 || (((SLAB ? a.row0 : 0) + (r >> LOG2N)) & (N - 1)) == 0)
+                        continue;  // padding lines
+                    const double* pr = a.ctl.partial + (((size_t)b << lsh) + r) * kPartStride;
+#pragma unroll
+                    for (int k = 0; k < S::NPART; ++k) s[k] += __ldcg(pr + k);
+                }
+#pragma unroll
+                for (int k = 0; k < S::NPART; ++k) {
+#pragma unroll
+                    for (int d = 16; d >= 1; d >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], d);
+                }
+                if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+                    for (int k = 0; k < S::NPART; ++k) red[k][threadIdx.x >> 5] = s[k];
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+#pragma unroll
+                    for (int k = 0; k < S::NPART; ++k) {
+                        s[k] = 0.0;
+                        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s[k] += red[k][w];
+                    }
+                    a.ctl.counter[b] = 0u;
+                    if constexpr (MODE == R_OPT_A) finalize_gamma(a.ctl, b, s[2], s[3], s[4]);
+                    if constexpr (MODE == R_RETA_C) finalize_gamma(a.ctl, b, s[0], s[1], s[2]);
+                    if constexpr (S::ENTRY) {
+                        if constexpr (SLAB) {
+                            a.slab_sums[2 * b] = s[0];
+                            a.slab_sums[2 * b + 1] = s[1];
+                        } else {
+                            // m of this member (thread 0's own line may be a padding line, for
+                            // which m was not read); the counter is advanced only here
+                            const int mb = __ldcg(&a.ctl.sweep[b]) - (S::POST ? 1 : 0);
+                            finalize_entry(a.ctl, b, mb, s[0], s[1]);
+                        }
+                    }
+                }
+                return;
+            }
+        }
         last = pol.bcast0(last, t);
         if (last) {
             __threadfence();
