@@ -1026,13 +1026,13 @@ __device__ __forceinline__ void col_group_w(const ColArgs& a, const int bid) {
 #pragma unroll
     for (int k0 = 0; k0 < C * N; k0 += THREADS) {
         const int k = k0 + threadIdx.x, j = k / C, cc = k % C;
-        smem[cc * G::PAD_N + G::pidx(j)] = a.T[mem + (size_t)j * LS + qa0 + cc];
+        smem[cc * G::PAD_N + j] = a.T[mem + (size_t)j * LS + qa0 + cc];  // unpadded (run_smem<true>)
     }
     __syncthreads();
     double2* buf = smem + e * G::PAD_N;
     const WarpSeg<T> pol{};
     double2 x[P], y[P];
-    Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
+    Engine::template run_smem<true>(x, y, t, buf, a.tw, a.sinp, pol);
     if constexpr (MODE == C_ONE) {
 #pragma unroll
         for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = cscale(y[l], a.scale);
