@@ -12,6 +12,7 @@
 #pragma once
 
 #include <complex>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -90,6 +91,14 @@ class GpuHelmholtzDirichlet {
     GpuHelmholtzDirichlet& operator=(const GpuHelmholtzDirichlet&) = delete;
     ~GpuHelmholtzDirichlet() { bp_problem_destroy(h_); }
 
+    // swap in new media of the same grid / batch (bp_problem_set_medium)
+    void set_medium(const Field& k2, const std::vector<double>& k0, const std::vector<double>& eta) {
+        if (k2.size() != static_cast<size_t>(batch_) * n_ * n_ || k0.size() != static_cast<size_t>(batch_) ||
+            eta.size() != k0.size())
+            throw std::invalid_argument("set_medium: field grid mismatch");
+        check(bp_problem_set_medium(h_, reinterpret_cast<const double*>(k2.data()), k0.data(), eta.data()));
+    }
+
     int batch() const { return batch_; }
     int n() const { return n_; }
     const bp_problem* handle() const { return h_; }
@@ -127,9 +136,7 @@ class GpuHelmholtzDirichlet {
     bp_problem* h_ = nullptr;
 };
 
-// bp::run (proj/src/iterate.cpp:88-153) over every member of the batch
-inline RunResult run(const GpuHelmholtzDirichlet& p, const CorrectionMap& map, const Field& f,
-                     const IterationConfig& cfg = {}, const Field* u0 = nullptr) {
+inline bp_map to_c_map(const CorrectionMap& map) {
     bp_map m{};
     std::visit(
         [&](const auto& mm) {
@@ -146,6 +153,31 @@ inline RunResult run(const GpuHelmholtzDirichlet& p, const CorrectionMap& map, c
             }
         },
         map);
+    return m;
+}
+
+inline std::vector<IterationTrace> make_traces(int batch, size_t stride, const std::vector<double>& l2,
+                                               const std::vector<double>& reta,
+                                               const std::vector<bp_trace>& info) {
+    std::vector<IterationTrace> out;
+    for (int b = 0; b < batch; ++b) {
+        IterationTrace t;
+        const size_t k = static_cast<size_t>(info[b].iters) + 1;
+        t.res_l2_rel.assign(l2.begin() + b * stride, l2.begin() + b * stride + k);
+        t.res_reta_rel.assign(reta.begin() + b * stride, reta.begin() + b * stride + k);
+        t.iters = info[b].iters;
+        t.terminated = static_cast<Termination>(info[b].terminated);
+        t.fnorm_l2 = info[b].fnorm_l2;
+        t.fnorm_reta = info[b].fnorm_reta;
+        out.push_back(std::move(t));
+    }
+    return out;
+}
+
+// bp::run (proj/src/iterate.cpp:88-153) over every member of the batch
+inline RunResult run(const GpuHelmholtzDirichlet& p, const CorrectionMap& map, const Field& f,
+                     const IterationConfig& cfg = {}, const Field* u0 = nullptr) {
+    const bp_map m = to_c_map(map);
     bp_iter_config c{static_cast<int32_t>(cfg.format), cfg.rtol, cfg.max_iters};
     const int B = p.batch();
     const size_t stride = static_cast<size_t>(cfg.max_iters) + 1;
@@ -156,18 +188,80 @@ inline RunResult run(const GpuHelmholtzDirichlet& p, const CorrectionMap& map, c
     check(bp_run(p.handle(), &m, reinterpret_cast<const double*>(f.data()), &c,
                  u0 ? reinterpret_cast<const double*>(u0->data()) : nullptr,
                  reinterpret_cast<double*>(res.u.data()), l2.data(), reta.data(), info.data()));
-    for (int b = 0; b < B; ++b) {
-        IterationTrace t;
-        const size_t k = static_cast<size_t>(info[b].iters) + 1;
-        t.res_l2_rel.assign(l2.begin() + b * stride, l2.begin() + b * stride + k);
-        t.res_reta_rel.assign(reta.begin() + b * stride, reta.begin() + b * stride + k);
-        t.iters = info[b].iters;
-        t.terminated = static_cast<Termination>(info[b].terminated);
-        t.fnorm_l2 = info[b].fnorm_l2;
-        t.fnorm_reta = info[b].fnorm_reta;
-        res.trace.push_back(std::move(t));
-    }
+    res.trace = make_traces(B, stride, l2, reta, info);
     return res;
 }
+
+// Overlapped solves over several handles of one shape (bp_pipeline_*; the reference solves one
+// batch at a time, proj/src/bench.cpp:143-151): submit() enqueues set_medium (when k2 is given)
+// + run on the next slot and returns; wait() returns the results in submission order.  The
+// fields passed to submit() must stay alive until wait(); the slots must outlive the pipeline.
+class GpuPipeline {
+  public:
+    explicit GpuPipeline(const std::vector<GpuHelmholtzDirichlet*>& slots) : slots_(slots) {
+        std::vector<bp_problem*> hs;
+        for (auto* s : slots_) hs.push_back(const_cast<bp_problem*>(s->handle()));
+        check(bp_pipeline_create(hs.data(), static_cast<int32_t>(hs.size()), &pl_));
+    }
+    GpuPipeline(const GpuPipeline&) = delete;
+    GpuPipeline& operator=(const GpuPipeline&) = delete;
+    ~GpuPipeline() {
+        bp_pipeline_wait(pl_);
+        bp_pipeline_destroy(pl_);
+    }
+
+    size_t submit(const CorrectionMap& map, const Field& f, const IterationConfig& cfg = {},
+                  const Field* k2 = nullptr, const std::vector<double>* k0 = nullptr,
+                  const std::vector<double>* eta = nullptr) {
+        auto j = std::make_unique<Job>();
+        const int B = slots_.front()->batch();
+        j->stride = static_cast<size_t>(cfg.max_iters) + 1;
+        j->l2.resize(B * j->stride);
+        j->reta.resize(B * j->stride);
+        j->info.resize(B);
+        j->u.resize(f.size());
+        bp_medium md{};
+        if (k2) {
+            if (!k0 || !eta) throw std::invalid_argument("pipeline submit: k2 needs k0 and eta");
+            md.k2 = reinterpret_cast<const double*>(k2->data());
+            md.k0 = k0->data();
+            md.eta = eta->data();
+        }
+        const bp_map m = to_c_map(map);
+        const bp_iter_config c{static_cast<int32_t>(cfg.format), cfg.rtol, cfg.max_iters};
+        check(bp_pipeline_submit(pl_, &md, &m, reinterpret_cast<const double*>(f.data()), &c, nullptr,
+                                 reinterpret_cast<double*>(j->u.data()), j->l2.data(), j->reta.data(),
+                                 j->info.data(), &j->slot));
+        jobs_.push_back(std::move(j));
+        return jobs_.size() - 1;
+    }
+
+    std::vector<RunResult> wait() {
+        const int rc = bp_pipeline_wait(pl_);
+        std::vector<std::unique_ptr<Job>> jobs;
+        jobs.swap(jobs_);
+        check(rc);
+        std::vector<RunResult> out;
+        for (auto& j : jobs) {
+            RunResult r;
+            r.u = std::move(j->u);
+            r.trace = make_traces(slots_[j->slot]->batch(), j->stride, j->l2, j->reta, j->info);
+            out.push_back(std::move(r));
+        }
+        return out;
+    }
+
+  private:
+    struct Job {  // heap-held: the worker threads write into these buffers until wait()
+        int32_t slot = 0;
+        size_t stride = 0;
+        Field u;
+        std::vector<double> l2, reta;
+        std::vector<bp_trace> info;
+    };
+    std::vector<GpuHelmholtzDirichlet*> slots_;
+    bp_pipeline* pl_ = nullptr;
+    std::vector<std::unique_ptr<Job>> jobs_;
+};
 
 }  // namespace bornsweep

@@ -22,6 +22,7 @@ def test_cpp_mirror_matches_python_api(gpu):
     k2, f, k0, eta = bs.make_instances(spec, 0, 2)
     with bs.HelmholtzDirichlet(k2, k0, eta) as p:
         res = bs.run(p, bs.ScalarMap(1.0), f, bs.IterationConfig(rtol=1e-6, max_iters=5000))
+    assert [l for l in lines if l.startswith("pipe")] == [f"pipe {j} same" for j in range(3)]
     for b, line in enumerate(lines[:2]):
         mb, iters, term, last, csum = line.split()
         assert int(mb) == b

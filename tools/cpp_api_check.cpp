@@ -30,6 +30,21 @@ int main(int argc, char** argv) {
             std::printf("%d %d %d %.17g %.17g\n", b, r.trace[b].iters,
                         static_cast<int>(r.trace[b].terminated), r.trace[b].res_l2_rel.back(), s);
         }
+        // overlapped solves: a two-slot pipeline gives the direct run bit for bit
+        {
+            bornsweep::GpuHelmholtzDirichlet p2(nd, k2, k0, eta);
+            bornsweep::GpuPipeline pipe({&p, &p2});
+            for (int j = 0; j < 3; ++j) pipe.submit(bornsweep::ScalarMap{}, f, cfg, &k2, &k0, &eta);
+            const auto rs = pipe.wait();
+            for (size_t j = 0; j < rs.size(); ++j) {
+                bool same = rs[j].u == r.u;
+                for (int b = 0; b < batch; ++b)
+                    same = same && rs[j].trace[b].iters == r.trace[b].iters &&
+                           rs[j].trace[b].res_l2_rel == r.trace[b].res_l2_rel &&
+                           rs[j].trace[b].res_reta_rel == r.trace[b].res_reta_rel;
+                std::printf("pipe %zu %s\n", j, same ? "same" : "DIFFERENT");
+            }
+        }
         // error mapping: zero source -> std::invalid_argument, like bp::run
         try {
             bornsweep::run(p, bornsweep::ScalarMap{}, bornsweep::Field(f.size()), cfg);
