@@ -230,6 +230,22 @@ def test_config1_members_truncated(gpu):
         assert_run_parity(res.traces[b], res.u[b], ref)
 
 
+@pytest.mark.slow
+def test_config1_member_full_length(gpu):
+    """BASELINE config 1, member 1 (511^2, pointwise map) solved to rtol 1e-6: the GPU and the
+    oracle take the same number of sweeps (4708 with this seed) and end on the same iterate."""
+    Oracle.set_threads(os.cpu_count() or 8)
+    k2, f, k0, eta = bs.config_instances("c1", 1, 1)
+    cfg = bs.IterationConfig(rtol=1e-6, max_iters=20000)
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        res = bs.run(p, bs.PointwiseMap(), f, cfg)
+    ref = _oracle_run(k2[0], f[0], k0[0], eta[0], bs.PointwiseMap(), 1e-6, 20000)
+    t = res.traces[0]
+    assert t.terminated == ref.terminated == "converged"
+    assert t.iters == ref.iters
+    assert np.linalg.norm(res.u[0] - ref.u) / np.linalg.norm(ref.u) < 1e-10
+
+
 def test_batch_members_independent(gpu):
     """Each member of a batch iterates and terminates on its own: a batch run equals the
     members run one at a time (bit-for-bit: same kernels, same reduction order)."""
