@@ -316,7 +316,9 @@ struct BarSeg {
 // scan read (lanes = t) are bank-conflict free.
 template <int T, int E>
 struct BlockSeg {
-    static constexpr int SCRATCH = T * (E + 1);  // double2
+    static constexpr int CH = (T + 31) / 32;  // 32-wide chunks per engine
+    // scan scratch + the chunk totals of the parallel scan (T >= 64: one warp per chunk)
+    static constexpr int SCRATCH = T * (E + 1) + (CH > 1 ? E * CH : 0);  // double2
     double2* scratch;
     int e;
     __device__ __forceinline__ static int sidx(int ee, int tt) { return tt * (E + 1) + ee; }
@@ -324,6 +326,33 @@ struct BlockSeg {
     __device__ __forceinline__ double2 exclusive_scan(double2 v, int t) const {
         scratch[sidx(e, t)] = v;
         __syncthreads();
+        if constexpr (CH > 1 && (T % 32) == 0) {
+            // long lines: the CTA has exactly E * CH warps (C * T threads), one per 32-value
+            // chunk; each scans its chunk, the chunk totals are combined afterwards in the same
+            // order as the sequential carry (bit-identical; the serial version kept 14 of 16
+            // warps waiting at the barrier on c2's 4096-point columns)
+            double2* tot = scratch + T * (E + 1);
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            const int ee = warp / CH, c = warp % CH, tt = c * 32 + lane;
+            const double2 x = scratch[sidx(ee, tt)];
+            double2 incl = x;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const double ux = __shfl_up_sync(0xffffffffu, incl.x, d);
+                const double uy = __shfl_up_sync(0xffffffffu, incl.y, d);
+                if (lane >= d) {
+                    incl.x += ux;
+                    incl.y += uy;
+                }
+            }
+            scratch[sidx(ee, tt)] = csub(incl, x);
+            if (lane == 31) tot[ee * CH + c] = incl;
+            __syncthreads();
+            double2 carry = make_double2(0.0, 0.0);
+            const int cm = t >> 5;
+            for (int k = 0; k < cm; ++k) carry = cadd(carry, tot[e * CH + k]);
+            return cadd(carry, scratch[sidx(e, t)]);
+        }
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         const int nwarps = (blockDim.x + 31) >> 5;
         constexpr int CH = (T + 31) / 32;  // 32-wide chunks per engine

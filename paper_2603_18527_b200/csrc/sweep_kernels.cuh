@@ -43,6 +43,9 @@
 // column kernels with warp-private engines (col_group_w) for lines of 32 threads (r01:
 // 277 vs 246 us on c1 -- the engines' own stride patterns conflict where the c-fastest map
 // of col_group does not; kept for experiments, off)
+#ifndef BS_COL_LD256
+#define BS_COL_LD256 1  // 256-bit paired-column loads in the 2-column (n >= 2048) column kernel
+#endif
 #ifndef BS_COL_WARP
 #define BS_COL_WARP 0
 #endif
@@ -1183,10 +1186,30 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
     // x_{N-j} there (no mirror registers); shorter lines keep the register path (measured, r01)
     constexpr bool CSM = BS_COL_SMEM_MIRROR && LOG2N >= 9;
     if constexpr (CSM) {
+    if constexpr (LAYOUT == CL_PLANE && C == 2 && BS_COL_LD256) {
+        // two columns per CTA (n >= 2048): each thread loads BOTH columns of a row with one
+        // 256-bit load (LDG.E.ENL2.256; the pair is 32-B aligned, q0 even) and splits them into
+        // the two engines' lines -- half the load instructions of the per-engine map, whose warp
+        // requests touch 16 rows x 32 B each (lg_throttle-bound on c2, r01c)
+        const size_t pair0 = mem + (size_t)((bid % GROUPS) * C);
+        double2* buf0 = smem;
+        double2* buf1 = smem + G::PAD_N;
+#pragma unroll
+        for (int k = 0; k < N / (C * T); ++k) {
+            const int r = threadIdx.x + C * T * k;
+            const double* src = reinterpret_cast<const double*>(a.T + pair0 + (size_t)r * N);
+            double v0, v1, v2, v3;
+            asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(v0), "=d"(v1), "=d"(v2), "=d"(v3) : "l"(src));
+            buf0[r] = make_double2(v0, v1);
+            buf1[r] = make_double2(v2, v3);
+        }
+    } else {
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
         buf[j] = a.T[gidx(j)];  // unpadded: conflict-free mirror reads in run_smem<true>
+    }
     }
     pol.sync();
     Engine::template run_smem<true>(x, y, t, buf, a.tw, a.sinp, pol);
