@@ -46,6 +46,9 @@
 #ifndef BS_COL_LD256
 #define BS_COL_LD256 1  // 256-bit paired-column loads in the 2-column (n >= 2048) column kernel
 #endif
+#ifndef BS_COL_WIDE
+#define BS_COL_WIDE 1  // warp-contiguous engines + named barriers for 2-column CTAs (n >= 2048)
+#endif
 #ifndef BS_COL_WARP
 #define BS_COL_WARP 0
 #endif
@@ -1084,8 +1087,17 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
         return;
     }
     extern __shared__ double2 smem[];
+    // WIDE (two 2048/4096-point columns per CTA): warp-contiguous engines synchronised by their
+    // own named barriers (the engines no longer wait for each other at every pass), the CTA
+    // loading and storing both columns of a row with 256-bit accesses through shared memory
+    constexpr bool WIDE = BS_COL_WIDE && BS_COL_LD256 && LAYOUT == CL_PLANE && C == 2 && T > 32 && (T % 32) == 0;
     int c, t;
-    col_thread_map<G::T, C>(t, c);
+    if constexpr (WIDE) {
+        c = threadIdx.x / T;
+        t = threadIdx.x % T;
+    } else {
+        col_thread_map<G::T, C>(t, c);
+    }
     constexpr int GROUPS = N / C;
     // line group -> member b, base offset `mem`, line stride LS, and (3-D x-lines) the y index
     int b, yl = 0, qa;
@@ -1178,8 +1190,27 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
     }
 
     double2* buf = smem + c * G::PAD_N;
-    const BlockSeg<T, C> pol{smem + C * G::PAD_N, c};
+    auto make_pol = [&]() {
+        if constexpr (WIDE) return BarSeg<T>{smem + C * G::PAD_N + c * (T / 32), 1 + c};
+        else return BlockSeg<T, C>{smem + C * G::PAD_N, c};
+    };
+    const auto pol = make_pol();
     const double2 zero = make_double2(0.0, 0.0);
+    const size_t pair0 = mem + (size_t)((bid % GROUPS) * C);  // (row 0, first column) of the CTA
+    // WIDE: y (block layout, this thread's P outputs) -> both lines -> 256-bit row-pair stores
+    auto store_wide = [&](const double2 (&v)[P]) {
+#pragma unroll
+        for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = v[l];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < N / (C * T); ++k) {
+            const int r = threadIdx.x + C * T * k;
+            const double2 v0 = smem[G::pidx(r)], v1 = smem[G::PAD_N + G::pidx(r)];
+            double* dst = reinterpret_cast<double*>(a.T + pair0 + (size_t)r * N);
+            asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(dst), "d"(v0.x), "d"(v0.y),
+                         "d"(v1.x), "d"(v1.y) : "memory");
+        }
+    };
 
     double2 x[P], y[P];
     // n >= 512: the column goes through shared memory and the pre-processing reads x_j and
@@ -1191,7 +1222,6 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
         // 256-bit load (LDG.E.ENL2.256; the pair is 32-B aligned, q0 even) and splits them into
         // the two engines' lines -- half the load instructions of the per-engine map, whose warp
         // requests touch 16 rows x 32 B each (lg_throttle-bound on c2, r01c)
-        const size_t pair0 = mem + (size_t)((bid % GROUPS) * C);
         double2* buf0 = smem;
         double2* buf1 = smem + G::PAD_N;
 #pragma unroll
@@ -1204,14 +1234,15 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
             buf0[r] = make_double2(v0, v1);
             buf1[r] = make_double2(v2, v3);
         }
+        __syncthreads();  // both lines were filled by the whole CTA
     } else {
 #pragma unroll
     for (int mm = 0; mm < P; ++mm) {
         const int j = t + T * mm;
         buf[j] = a.T[gidx(j)];  // unpadded: conflict-free mirror reads in run_smem<true>
     }
-    }
     pol.sync();
+    }
     Engine::template run_smem<true>(x, y, t, buf, a.tw, a.sinp, pol);
     } else {
         double2 xm[P];
@@ -1225,8 +1256,14 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
     }
 
     if constexpr (MODE == C_ONE) {
+        if constexpr (WIDE) {
 #pragma unroll
-        for (int l = 0; l < P; ++l) st_out(t * P + l, cscale(y[l], a.scale));
+            for (int l = 0; l < P; ++l) y[l] = cscale(y[l], a.scale);
+            store_wide(y);
+        } else {
+#pragma unroll
+            for (int l = 0; l < P; ++l) st_out(t * P + l, cscale(y[l], a.scale));
+        }
     } else {
         const double k0sq = a.k0sq[b], eta = a.eta[b];
         // transverse symbol part: a_q (2-D) or a_y + a_z (3-D x-lines)
@@ -1265,8 +1302,12 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
             pol.sync();
             Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
         }
+        if constexpr (WIDE) {
+            store_wide(y);
+        } else {
 #pragma unroll
-        for (int l = 0; l < P; ++l) st_out(t * P + l, y[l]);
+            for (int l = 0; l < P; ++l) st_out(t * P + l, y[l]);
+        }
     }
 }
 
