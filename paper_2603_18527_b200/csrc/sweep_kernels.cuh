@@ -46,6 +46,9 @@
 #ifndef BS_COL_LD256
 #define BS_COL_LD256 1  // 256-bit paired-column loads in the 2-column (n >= 2048) column kernel
 #endif
+#ifndef BS_ROW_FWD_DENSE
+#define BS_ROW_FWD_DENSE 1
+#endif
 #ifndef BS_COL_WIDE
 #define BS_COL_WIDE 1  // warp-contiguous engines + named barriers for 2-column CTAs (n >= 2048)
 #endif
@@ -357,6 +360,8 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     bool valid = (b < a.batch) && (xg & (N - 1)) != 0 && (DIM == 2 || (i & (N - 1)) != 0);
     // shared-memory staging of the inverse transform's input (see RSM below)
     constexpr bool RSM = BS_ROW_SMEM && (T > 32 || DIM == 3 || (BS_RSM_ALL && S::ITER));
+    // forward transform's staged line unpadded too (warp-private engines only, see below)
+    constexpr bool FWD_DENSE = BS_ROW_FWD_DENSE && RSM && T <= 32;
     // The T line is loaded before the member's status / sweep counter are known (they are
     // an L2 round trip of their own): the two latencies overlap instead of adding up.  A
     // terminated member's line is loaded and dropped (16 B/pt, its CTA then exits).
@@ -596,7 +601,18 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
             }
         }
         if constexpr (S::FWD) {
-            if constexpr (RSM) buf[G::at_stride(t, G::pidx(t), mm)] = qv;  // the slot this thread read G q from
+            if constexpr (RSM) {
+                if constexpr (FWD_DENSE) {
+                    // unpadded next source (run_smem<true>: conflict-free mirror reads).  Slot j
+                    // can only alias the padded G q slot of an element j' <= j, i.e. of this
+                    // iteration or an earlier one: the warp sync orders every lane's G q read of
+                    // this iteration before any lane's write (one engine never spans warps here)
+                    __syncwarp();
+                    buf[t + T * mm] = qv;
+                } else {
+                    buf[G::at_stride(t, G::pidx(t), mm)] = qv;  // the slot this thread read G q from
+                }
+            }
             else q[mm] = qv;
         }
     }
@@ -609,7 +625,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         pol.sync();
         {
             double2 v[P];
-            Engine::run_smem(v, y2, t, buf, a.tw, a.sinp, pol);
+            Engine::template run_smem<FWD_DENSE>(v, y2, t, buf, a.tw, a.sinp, pol);
         }
         } else {
         double2 qm[P];
