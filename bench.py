@@ -154,6 +154,21 @@ def cpu_baseline(k2, f, k0, eta, sweeps, threads):
     return done * nd * nd / dt / 1e9, dt, kind, sample
 
 
+def cpu_oracle_parallel(k2, f, k0, eta, sweeps, threads):
+    """SURVEY.md 8(d) mode (ii), "oracle-parallel": the plain-C port on ONE member with OpenMP
+    inside every transform / element-wise pass (the reference never threads its FFTW plans,
+    transforms.cpp:39-65).  Returns (Gpts/s, seconds, sample)."""
+    from oracle import MAP_POINTWISE, Oracle, OracleProblem
+    nd = k2.shape[1]
+    Oracle.set_threads(threads)
+    t0 = time.perf_counter()
+    done = OracleProblem(k2[0], k0[0], eta[0]).run(f[0], map_kind=MAP_POINTWISE, rtol=1e-30,
+                                                   max_iters=sweeps).iters
+    dt = time.perf_counter() - t0
+    return done * nd * nd / dt / 1e9, dt, (f"1 member x {done} sweeps of {nd}x{nd}, plain-C port, "
+                                           f"OpenMP over transform lines, {threads} threads")
+
+
 def cpu_baseline_cdr(bx, by, sigma, s0, f, sweeps, threads):
     """c4 has no reference problem family: the plain-C port (oracle/bp_oracle.c) on the host,
     OpenMP inside each transform / stencil, members one after another."""
@@ -463,6 +478,11 @@ def run_ours(args):
             v, dt, kind, sample = cpu_baseline(k2[:m], f[:m], k0[:m], eta[:m], sw, cores)
         cpu = None if v is None else {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                                       "sample": sample, "seconds": round(dt, 3)}
+        if cpu is not None and not cdr and dim == 2 and args.config != "c2":
+            # mode (ii) next to the reference-faithful mode (i) above
+            v2, dt2, sample2 = cpu_oracle_parallel(k2, f, k0, eta, 60, cores)
+            cpu["oracle_parallel"] = {"value": v2, "unit": UNIT, "cores": cores, "kind": "port",
+                                      "sample": sample2, "seconds": round(dt2, 3)}
 
     prob.close()
     if rank == 0:
