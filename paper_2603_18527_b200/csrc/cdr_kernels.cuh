@@ -20,6 +20,10 @@
 
 #include "periodic_kernels.cuh"
 
+#ifndef BS_CDR_PD
+#define BS_CDR_PD 1  // RC_B operand prefetch distance (measured c4 RC_A+RC_B: 0 -> 620, 1 -> 570, 2 -> 657 us)
+#endif
+
 namespace bs {
 
 template <int LOG2N, int PP = 16>
@@ -251,25 +255,46 @@ crow_kernel(const CdrArgs a) {
             pol.sync();
             const double ih = 1.0 / a.h, ih2 = ih * ih;
             const double s0 = valid ? a.sigma0[b] : 0.0;
+            // global operands of element mm, issued CDR_PD elements ahead of their use (like the
+            // Dirichlet row kernel's element-wise pipeline); halo rows of the boundary pairs
+            // are replaced by the reflective ghosts at use
+            struct Op {
+                double w, e, vx[2], vy[2], sg[2], ff[2];
+            };
+            auto load_op = [&](int mm) {
+                Op o{};
+                if (valid) {
+                    const int j = t + T * mm;
+                    o.w = firstA ? 0.0 : ucur[rowA - N + j];
+                    o.e = lastB ? 0.0 : ucur[rowB + N + j];
+#pragma unroll
+                    for (int s = 0; s < 2; ++s) {
+                        const size_t ix = (s ? rowB : rowA) + j;
+                        o.vx[s] = a.bx[ix];
+                        o.vy[s] = a.by[ix];
+                        o.sg[s] = a.sigma[ix];
+                        o.ff[s] = a.f[ix];
+                    }
+                }
+                return o;
+            };
+            constexpr int PD = BS_CDR_PD < P ? BS_CDR_PD : P;
+            Op ops[P];
+#pragma unroll
+            for (int mm = 0; mm < PD; ++mm) ops[mm] = load_op(mm);
 #pragma unroll
             for (int mm = 0; mm < P; ++mm) {
+                if (mm + PD < P) ops[mm + PD] = load_op(mm + PD);
                 const int j = t + T * mm;
                 const double2 c = q[mm];
                 const double2 so = j > 0 ? buf[G::pidx(j - 1)] : c;
                 const double2 no = j + 1 < N ? buf[G::pidx(j + 1)] : c;
-                double wA = c.x, eB = c.y, vx[2] = {0, 0}, vy[2] = {0, 0}, sg[2] = {0, 0}, ff[2] = {0, 0};
-                if (valid) {
-                    if (!firstA) wA = ucur[rowA - N + j];
-                    if (!lastB) eB = ucur[rowB + N + j];
-#pragma unroll
-                    for (int s = 0; s < 2; ++s) {
-                        const size_t o = (s ? rowB : rowA) + j;
-                        vx[s] = a.bx[o];
-                        vy[s] = a.by[o];
-                        sg[s] = a.sigma[o];
-                        ff[s] = a.f[o];
-                    }
-                }
+                const Op& op = ops[mm];
+                const double wA = (valid && !firstA) ? op.w : c.x, eB = (valid && !lastB) ? op.e : c.y;
+                const double* vx = op.vx;
+                const double* vy = op.vy;
+                const double* sg = op.sg;
+                const double* ff = op.ff;
                 double res[2], qq[2];
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
