@@ -19,10 +19,10 @@ and result gather.  Work counted = sweeps actually executed (sum of iters) x 511
              the graph replaced by individually event-bracketed launches), vs MEASURED_PEAKS.
 * cpu_baseline -- the reference's own code (oracle/_ref) on the host cores, bounded sample.
 
-N > 1 (torchrun): every rank runs its own batch of independent members (the N = 1 batch, global
-member indices [64 r, 64 r + 64): "scaling": "weak", per-GPU work fixed -- SURVEY.md 8(e), no
-collective on the data path); --strong splits the config's 64 members instead (8 per GPU at
-N = 8, config 1's wording).  torch.distributed only for the barrier and the max-over-ranks time.
+N > 1 (torchrun): the config's 64 members are split over the ranks (8 per GPU at N = 8, config
+1's wording; "scaling": "strong"), independent members with no collective on the data path
+(SURVEY.md 8(e)); --weak gives every rank its own N = 1 batch (global members [64 r, 64 r + 64)).
+torch.distributed only for the barrier and the max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -130,13 +130,15 @@ def cpu_baseline(k2, f, k0, eta, sweeps, threads):
     """The reference's own code (oracle/_ref: proj/src sources + FFTW shim + restated run) on
     the host: OpenMP over members like proj/src/bench.cpp:143, each member iterated `sweeps`
     times.  Returns (Gpts/s, seconds, kind, sample)."""
-    from oracle import MAP_POINTWISE, Reference, Oracle, OracleProblem
+    from oracle import MAP_POINTWISE, Reference, ReferenceBatch, Oracle, OracleProblem
     nd = k2.shape[1]
     if Reference.available():
+        batch = ReferenceBatch(k2, k0, eta)  # Problem construction outside the timed sample
         t0 = time.perf_counter()
-        _, _, _, info = Reference.run_batch(k2, k0, eta, f, map_kind=MAP_POINTWISE, rtol=1e-6,
-                                            max_iters=sweeps, nthreads=threads)
+        _, _, _, info = batch.run(f, map_kind=MAP_POINTWISE, rtol=1e-6, max_iters=sweeps,
+                                  nthreads=threads)
         dt = time.perf_counter() - t0
+        batch.close()
         done = sum(i for i, _ in info)
         kind = "reference"
     else:  # the plain-C port
@@ -148,9 +150,9 @@ def cpu_baseline(k2, f, k0, eta, sweeps, threads):
                                                             max_iters=sweeps).iters
         dt = time.perf_counter() - t0
         kind = "port"
-    sample = (f"{k2.shape[0]} members x {sweeps} sweeps of {nd}x{nd} (full bp::run incl. "
-              f"setup), OpenMP over members, {threads} threads; transforms through the project "
-              f"FFTW-API shim (FFTW absent)")
+    sample = (f"{k2.shape[0]} members x {sweeps} sweeps of {nd}x{nd} (bp::run incl. its setup, "
+              f"Problem construction excluded), OpenMP over members, {threads} threads; transforms "
+              f"through the project FFTW-API shim (radix-4 Stockham, not FFTW: FFTW is absent)")
     return done * nd * nd / dt / 1e9, dt, kind, sample
 
 
@@ -186,59 +188,79 @@ def cpu_baseline_cdr(bx, by, sigma, s0, f, sweeps, threads):
     return done * n * n / dt / 1e9, dt, "port", sample
 
 
+def workload_config(name: str, map_name: str, total: int, nd: int, dim: int = 2) -> dict:
+    """The bench line's `config`: the workload only, identical in both arms (the arm-specific
+    execution details go to the line's `step` / `parallelism` keys)."""
+    grid = (f"{nd}x{nd} Neumann cell-centred (h=1/{nd})" if name == "c4" else
+            "x".join([str(nd)] * dim) + f" (n={nd + 1}, h=1/{nd + 1})")
+    return {"workload": WORKLOADS[name] + f"; map {map_name}", "grid": grid, "global_batch": total,
+            "l2": "no flush needed: the per-step working set (>1 GB) >> 126 MB L2"}
+
+
 def run_reference_arm(args):
+    """The reference's own CPU path on the host cores: oracle/_ref --
+    proj/src compiled in place with the project's FFTW-API shim (FFTW is absent) and the
+    Eigen-free restatement of run / apply_correction.  Inputs come from the reference's own
+    RngState / samplers (oracle/instances.py); nothing of the product package is imported.
+    The members' Problem objects are built once before timing; a step is one bp::run of every
+    member limited to --ref-sweeps sweeps, OpenMP over members (proj/src/bench.cpp:143-151)."""
     rank, _, world = dist_env()
     if rank != 0:
         return 0
-    import paper_2603_18527_b200 as bs
+    from oracle import MAP_POINTWISE, Oracle, OracleProblem, Reference, ReferenceBatch
+    from oracle.instances import cdr_c4, helmholtz_c1
     cores = os.cpu_count() or 1
     if args.config == "c4":
-        bx, by, sg, s0, f = bs.config_instances("c4", 0, 1)
+        # c4 has no reference problem family (SURVEY.md 8(a) a16): the plain-C port stands in
+        m = min(8, 32)
+        bx, by, sg, s0, f = cdr_c4(0, m)
         sweeps = max(1, args.ref_sweeps)
-        for _ in range(args.warmup):
-            cpu_baseline_cdr(bx, by, sg, s0, f, sweeps, cores)
-        times = []
-        for _ in range(args.steps):
-            v, dt, kind, sample = cpu_baseline_cdr(bx, by, sg, s0, f, sweeps, cores)
-            times.append(dt)
-        value = float(len(times) * sweeps * 1024 * 1024 / np.sum(times) / 1e9)
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded c4 media)", "impl": "reference",
-            "config": {"workload": WORKLOADS["c4"] + "; map scalar", "grid": "1024x1024 Neumann cell-centred (h=1/1024)",
-                       "global_batch": 32, "batch_sample": 1, "sweeps_per_step": sweeps,
-                       "parallelism": "OpenMP inside the port"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line), flush=True)
-        return 0
-    members = min(cores, 64)
-    k2, f, k0, eta = bs.config_instances("c1", 0, members)
-    sweeps = args.ref_sweeps
+        Oracle.set_threads(cores)
+        probs = [OracleProblem.cdr(bx[b], by[b], sg[b], s0[b]) for b in range(m)]
+
+        def step():
+            return sum(probs[b].run(f[b] + 0j, rtol=1e-8, max_iters=sweeps).iters for b in range(m))
+        n, kind = 1024, "port"
+        sample = (f"{m} of the 32 c4 members x {sweeps} sweeps of 1024x1024 per step, plain-C port "
+                  f"(oracle/bp_oracle.c; the reference has no CDR problem family), OpenMP over grid "
+                  f"lines, {cores} threads")
+        cfg = workload_config("c4", "scalar", 32, 1024)
+    else:
+        if not Reference.available():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbpref.so not built"}))
+            return 0
+        members = 64
+        k2, f, k0, eta = helmholtz_c1(0, members)
+        batch = ReferenceBatch(k2, k0, eta)  # Problem construction: outside the timed region
+        sweeps = max(1, args.ref_sweeps)
+
+        def step():
+            _, _, _, info = batch.run(f, map_kind=MAP_POINTWISE, rtol=1e-6, max_iters=sweeps,
+                                      nthreads=cores)
+            return sum(i for i, _ in info)
+        n, kind = 511, "reference"
+        sample = (f"all 64 c1 members x {sweeps} sweeps of 511x511 per step (bp::run per member: "
+                  f"its setup ||f||, ||G f|| included, Problem construction excluded), OpenMP over "
+                  f"members, {cores} threads; transforms through the project FFTW-API shim "
+                  f"(radix-4 Stockham, not FFTW: FFTW is absent)")
+        cfg = workload_config("c1", "pointwise", 64, 511)
     for _ in range(args.warmup):
-        cpu_baseline(k2, f, k0, eta, sweeps, cores)
-    vals, times = [], []
+        step()
+    done, times = 0, []
     for _ in range(args.steps):
-        v, dt, kind, sample = cpu_baseline(k2, f, k0, eta, sweeps, cores)
-        vals.append(v)
-        times.append(dt)
-    value = float(np.sum([members * sweeps * 511 * 511 for _ in times]) / np.sum(times) / 1e9)
+        t0 = time.perf_counter()
+        done += step()
+        times.append(time.perf_counter() - t0)
+    value = float(done * n * n / np.sum(times) / 1e9)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded RngState media, BASELINE.json c1 construction)",
-        "impl": "reference",
-        # the GPU arm's config (same workload, grid, batch); the CPU step is a bounded sample
-        "config": {"workload": WORKLOADS["c1"] + "; map pointwise", "grid": "511x511 (n=512, h=1/512)",
-                   "global_batch": 64, "batch_sample": members, "sweeps_per_step": sweeps,
-                   "parallelism": f"OpenMP over members, {cores} threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": sample},
+        "data": "synthetic (seeded RngState media from the reference's own samplers, BASELINE construction)",
+        "impl": "reference", "config": cfg,
+        "step": {"sweeps_per_member": sweeps, "member_sweeps": done // max(1, args.steps)},
+        "parallelism": f"host CPU, {cores} threads",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -493,14 +515,13 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64",
             "data": ("synthetic (seeded c4 media: smoothed noise b, sigma, f)" if cdr else
                      "synthetic (seeded RngState media + centre Gaussian-bump sources, BASELINE c1 construction)"),
-            "config": {"workload": WORKLOADS[args.config] + f"; map {args.map or cfgd['map']}",
-                       "grid": (f"{nd}x{nd} Neumann cell-centred (h=1/{nd})" if cdr else
-                                "x".join([str(nd)] * dim) + f" (n={nd + 1}, h=1/{nd + 1})"), "global_batch": total if args.strong else total * world,
-                       "members_per_gpu": per, "sweeps_per_step": args.sweeps,
-                       "parallelism": (f"batch-shard x{world} (the {total} members split)" if args.strong else
-                                       f"batch-shard x{world} ({per} independent members per GPU, "
-                                       f"global members [{first}, {first + per}) on rank {rank})"),
-                       "l2": "no flush needed: ~1.7 GB working set per step >> 126 MB L2"},
+            "config": workload_config(args.config, args.map or cfgd["map"],
+                                      total if args.strong else total * world, nd, dim),
+            "step": {"sweeps_per_member": args.sweeps, "members_per_gpu": per},
+            "parallelism": (f"batch-shard x{world} (the {total} members split, members [{first}, "
+                            f"{first + per}) on rank {rank})" if args.strong else
+                            f"batch-shard x{world} ({per} independent members per GPU, "
+                            f"global members [{first}, {first + per}) on rank {rank})"),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": (f"bs.Pipeline depth {depth} (bp_pipeline_*: set_medium + bp_run per step, "
@@ -619,9 +640,10 @@ def main():
     ap.add_argument("--steps", type=int, default=15)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=64, help="members of config c1 per GPU (whole job with --strong)")
-    ap.add_argument("--strong", action="store_true",
-                    help="split the config's members over the ranks (default: weak scaling, the N=1 batch per rank)")
+    ap.add_argument("--batch", type=int, default=64, help="members of config c1 (whole job; per GPU with --weak)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank runs the N=1 batch of independent members (default: "
+                         "the config's members split over the ranks, BASELINE c1 'sharded 8 per GPU at 8 GPUs')")
     ap.add_argument("--config", choices=["c0", "c1", "c2", "c3", "c4"], default="c1",
                     help="workload; the headline metric is quoted on c1 (BASELINE.json configs[1])")
     ap.add_argument("--map", choices=["pointwise", "scalar", "optimal_l2"], default=None,
@@ -631,7 +653,7 @@ def main():
     ap.add_argument("--cpu-sweeps-c4", type=int, default=30)
     # sweeps per reference-arm step: enough that the run's setup (||f||, ||G f||: two
     # transform pairs) does not dominate the CPU sample (~1.3 s per step on 16 cores)
-    ap.add_argument("--ref-sweeps", type=int, default=20)
+    ap.add_argument("--ref-sweeps", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-depth", type=int, default=2,
                     help="handles in the e2e bs.Pipeline (1 = set_medium + bp_run, serial)")
@@ -639,6 +661,7 @@ def main():
     ap.add_argument("--fused", action="store_true",
                     help="c2 / c3 slabs: exchange fused into the kernels' stores (symmetric memory)")
     args = ap.parse_args()
+    args.strong = not args.weak
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":

@@ -306,6 +306,10 @@ class Reference:
                                             _dp, _dp, _dp, C.c_int, C.c_double, C.c_double,
                                             C.c_int, _dp, C.c_int, C.c_double, C.c_int, _dp, _dp,
                                             _dp, C.POINTER(_Trace), C.c_int]
+            lib.bpref_run_handles.argtypes = [C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_double,
+                                              C.c_double, C.c_int, _dp, C.c_long, C.c_int,
+                                              C.c_double, C.c_int, _dp, _dp, _dp,
+                                              C.POINTER(_Trace), C.c_int]
             lib.bpref_set_mode.argtypes = [C.c_int]
             lib.bpref_set_mode.restype = None
             lib.bpref_sponge_profile.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _dp]
@@ -454,6 +458,53 @@ class Reference:
                                        max_iters, _ptr(u), _ptr(l2), _ptr(rt), tr, nthreads)
         if rc:
             raise OracleError(cls.lib().bpref_last_error().decode())
+        return u, l2, rt, [(t.iters, TERM_NAMES[t.terminated]) for t in tr]
+
+
+class ReferenceBatch:
+    """Reference problems of a batch created ONCE (the reference's Problem constructors), then
+    run repeatedly with OpenMP over members (bpref_run_handles, the sample-parallel loop of
+    proj/src/bench.cpp:143-151): the bench's reference arm times only the runs."""
+
+    def __init__(self, k2, k0, eta, lx: float = 1.0, ly: float = 1.0):
+        k2 = _c(k2)
+        self.batch, self.nx, self.ny = k2.shape
+        lib = Reference.lib()
+        self.handles = (C.c_void_p * self.batch)()
+        for b in range(self.batch):
+            h = C.c_void_p()
+            if lib.bpref_problem_create(self.nx, self.ny, lx, ly, _ptr(k2[b]), float(k0[b]),
+                                        float(eta[b]), C.byref(h)):
+                raise OracleError(lib.bpref_last_error().decode())
+            self.handles[b] = h
+
+    def close(self):
+        lib = Reference.lib()
+        for b in range(self.batch):
+            if self.handles[b]:
+                lib.bpref_problem_destroy(self.handles[b])
+                self.handles[b] = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, f, *, map_kind=MAP_SCALAR, gamma=1.0 + 0j, metric=0, fmt=FMT_NPBS, rtol=1e-6,
+            max_iters=1000, nthreads=None):
+        f = _c(f)
+        u = np.empty_like(f)
+        l2 = np.full((self.batch, max_iters + 1), np.nan)
+        rt = np.full((self.batch, max_iters + 1), np.nan)
+        tr = (_Trace * self.batch)()
+        g = complex(gamma)
+        rc = Reference.lib().bpref_run_handles(self.batch, self.handles, map_kind, g.real, g.imag,
+                                               metric, _ptr(f), self.nx * self.ny, fmt, rtol,
+                                               max_iters, _ptr(u), _ptr(l2), _ptr(rt), tr,
+                                               nthreads or os.cpu_count())
+        if rc:
+            raise OracleError(Reference.lib().bpref_last_error().decode())
         return u, l2, rt, [(t.iters, TERM_NAMES[t.terminated]) for t in tr]
 
 

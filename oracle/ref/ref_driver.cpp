@@ -395,6 +395,32 @@ int bpref_run_batch(int nx, int ny, double lx, double ly, int batch, const doubl
     return rc;
 }
 
+// Pre-created problems (bpref_problem_create), OpenMP over members like bpref_run_batch: the
+// bench's reference arm creates its problems once, outside the timed region, and times only
+// the runs (problem setup = the reference's Problem constructor, not part of bp::run).
+int bpref_run_handles(int batch, void* const* handles, int map_kind, double g_re, double g_im,
+                      int metric, const double* f, long member_stride, int format, double rtol,
+                      int max_iters, double* u_out, double* res_l2, double* res_reta,
+                      TraceOut* info, int nthreads) {
+    int rc = 0;
+    const bp::parallel::Mode saved = bp::parallel::mode();
+    if (nthreads > 1) bp::parallel::set_mode(bp::parallel::Mode::Serial);
+#pragma omp parallel for schedule(dynamic) num_threads(nthreads)
+    for (int b = 0; b < batch; ++b) {
+        const int r = bpref_run(handles[b], map_kind, g_re, g_im, metric, nullptr,
+                                f + 2 * member_stride * b, format, rtol, max_iters, nullptr,
+                                u_out + 2 * member_stride * b,
+                                res_l2 + static_cast<long>(max_iters + 1) * b,
+                                res_reta + static_cast<long>(max_iters + 1) * b, info + b);
+        if (r) {
+#pragma omp critical
+            rc = r;
+        }
+    }
+    bp::parallel::set_mode(saved);
+    return rc;
+}
+
 // ---- the reference's own samplers and RNG (proj/src/samplers.cpp, proj/include/bp/rng.hpp),
 // exposed so the project's instance generator can be pinned against them.
 int bpref_sponge_profile(int nx, int ny, int bc, int layer, double strength, double* out) {
