@@ -26,8 +26,11 @@
  *   holds the message.  Numerical failure is NOT an error: it is reported through
  *   bp_trace.terminated exactly like bp::Termination (proj/include/bp/iterate.hpp:20).
  *
- * Threading: a problem handle is immutable after creation (like bp::Problem, problem.hpp:14-15);
- * concurrent calls on distinct handles are safe, each handle owns its stream.
+ * Threading: concurrent calls on distinct handles are safe, each handle owns its stream and
+ * workspaces.  Unlike bp::Problem (problem.hpp:14-15) a handle is NOT reentrant: every call,
+ * the bp_apply_* operators included, uses the handle's device workspaces, so one handle must
+ * not be used from two threads at once -- nor directly while a pipeline job runs on it
+ * (bp_pipeline_*; a direct call between jobs is fine).
  */
 #ifndef BORNSWEEP_H
 #define BORNSWEEP_H
@@ -60,11 +63,17 @@ typedef struct {
 } bp_grid;
 
 /* CorrectionMap variants (proj/include/bp/correction.hpp:16-40) plus the diagonal
- * relaxation gamma(x) = (i/eta) V(x) ("scalar/diagonal relaxation"). */
+ * relaxation gamma(x) = (i/eta) V(x) ("scalar/diagonal relaxation").
+ * Supported on the GPU (bp_run):
+ *   SCALAR          every family and path (CDR: real gamma only)
+ *   OPTIMAL_SCALAR  Dirichlet 2-D / 3-D and periodic, both metrics; not on slabs or CDR
+ *   FOURIER_DIAG    Dirichlet 2-D / 3-D and periodic; not on slabs or CDR
+ *   POINTWISE       Dirichlet 2-D / 3-D, single device and slabs (a Dirichlet-family map)
+ * anything else returns BP_ENOTSUP. */
 enum {
     BP_MAP_SCALAR = 0,         /* ScalarMap{gamma}                                      */
-    BP_MAP_OPTIMAL_SCALAR = 1, /* OptimalScalarMap{metric}             (BP_ENOTSUP yet) */
-    BP_MAP_FOURIER_DIAG = 2,   /* FourierDiagMap{m}                    (BP_ENOTSUP yet) */
+    BP_MAP_OPTIMAL_SCALAR = 1, /* OptimalScalarMap{metric}                              */
+    BP_MAP_FOURIER_DIAG = 2,   /* FourierDiagMap{m}                                     */
     BP_MAP_POINTWISE = 3       /* gamma(x) = (i/eta) V(x), Osnabrugge-style CBS          */
 };
 enum { BP_METRIC_EUCLIDEAN = 0, BP_METRIC_RETA = 1 }; /* bp::OptMetric */
@@ -76,7 +85,9 @@ typedef struct {
     const double* m;           /* BP_MAP_FOURIER_DIAG: nx*ny complex (host) */
 } bp_map;
 
-/* bp::IterFormat / IterationConfig (proj/include/bp/iterate.hpp:12-18) */
+/* bp::IterFormat / IterationConfig (proj/include/bp/iterate.hpp:12-18).  DIRECT (direction
+ * = r, iterate.cpp:118-123) runs on the single-device Helmholtz families (Dirichlet, periodic);
+ * slabs and CDR take CBS / NPBS only (BP_ENOTSUP). */
 enum { BP_FMT_DIRECT = 0, BP_FMT_CBS = 1, BP_FMT_NPBS = 2 };
 typedef struct {
     int32_t format;   /* default BP_FMT_NPBS */

@@ -361,11 +361,12 @@ class Pipeline:
             if type(p) is not type(p0) or p.shape != p0.shape:
                 raise ValueError("Pipeline slots must be problems of one family and shape")
         self._lib = N.lib()
+        self._h = None
+        self._jobs = []
         hs = (C.c_void_p * len(self.problems))(*[p.handle for p in self.problems])
         h = C.c_void_p()
         _check(self._lib.bp_pipeline_create(hs, len(self.problems), C.byref(h)))
         self._h = h
-        self._jobs = []
 
     def submit(self, cmap, f, config: IterationConfig | None = None, medium=None, u0=None,
                u_out=None) -> int:

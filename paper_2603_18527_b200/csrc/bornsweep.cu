@@ -270,9 +270,9 @@ cudaError_t prepare_kernels(int log2n, int dim) {
             if (cudaError_t r = launch_cdr(log2n, true, mode, ca, nullptr, true)) e = r;
         for (int mode : {CC_ONE, CC_GREEN, CC_INV, CC_LREF})
             if (cudaError_t r = launch_cdr(log2n, false, mode, ca, nullptr, true)) e = r;
-        for (int mode : {RP_FWD, RP_FWD_BORN, RP_INV, RP_SWEEP})
+        for (int mode : {RP_FWD, RP_FWD_BORN, RP_INV, RP_SWEEP, RP_OPT_B, RP_RETA_B})
             if (cudaError_t r = launch_periodic(log2n, true, mode, pa, nullptr, true)) e = r;
-        for (int mode : {CP_ONE, CP_GREEN, CP_LREF, CP_SWEEP, CP_INV})
+        for (int mode : {CP_ONE, CP_GREEN, CP_LREF, CP_SWEEP, CP_INV, CP_OPT_A, CP_OPT_C, CP_RETA_C})
             if (cudaError_t r = launch_periodic(log2n, false, mode, pa, nullptr, true)) e = r;
     }
     for (int pp : {8, 16}) {
@@ -390,6 +390,7 @@ struct bp_problem {
     int graph_map_kind = -1;
     bool graph_mixed = false;
     int graph_metric = -1;
+    int graph_format = -1;
     double2 graph_gamma{};
     int graph_max_iters = -1;
     double graph_rtol = -1;
@@ -664,11 +665,16 @@ struct SweepPlan {
     }
 };
 
-SweepPlan plan_for(const bp_map* map) {
+SweepPlan plan_for(const bp_map* map, int format) {
     SweepPlan s;
     switch (map->kind) {
         case BP_MAP_OPTIMAL_SCALAR:
-            if (map->metric == BP_METRIC_RETA) {
+            if (map->metric != BP_METRIC_RETA && format == BP_FMT_DIRECT) {
+                // Direct + Euclidean: w = A r = L_ref r - V r (R_FD_A stores r, C_LREF, R_RETA_C)
+                s.add(true, R_FD_A);
+                s.add(false, C_LREF);
+                s.add(true, R_RETA_C);
+            } else if (map->metric == BP_METRIC_RETA) {
                 s.add(true, R_RETA_A);
                 s.add(false, C_GREEN);
                 s.add(true, R_RETA_C);
@@ -772,9 +778,11 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     a.ctl.rtol = cfg->rtol;
     a.map_kind = map->kind;
     a.gamma = make_double2(map->gamma_re, map->gamma_im);
+    a.direct = cfg->format == BP_FMT_DIRECT;
+    a.lw = a.direct && map->kind == BP_MAP_OPTIMAL_SCALAR && map->metric != BP_METRIC_RETA;
     ColArgs c = col_args(p);
     c.status = a.ctl.status;
-    const SweepPlan plan = plan_for(map);
+    const SweepPlan plan = plan_for(map, cfg->format);
     if (map->kind == BP_MAP_FOURIER_DIAG) {
         // one multiplier for the whole batch, reference mode layout -> padded
         const size_t bytes = sizeof(double2) * p->dense_pts;
@@ -929,7 +937,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     } else {
         // graph of kGraphSweeps sweeps, replayed until every member terminated
         const bool reuse = p->graph && p->graph_map_kind == map->kind && p->graph_mixed == mixed &&
-                           p->graph_metric == map->metric &&
+                           p->graph_metric == map->metric && p->graph_format == cfg->format &&
                            p->graph_gamma.x == map->gamma_re && p->graph_gamma.y == map->gamma_im &&
                            p->graph_max_iters == cfg->max_iters && p->graph_rtol == cfg->rtol;
         if (!reuse) {
@@ -947,6 +955,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             p->graph_map_kind = map->kind;
             p->graph_mixed = mixed;
             p->graph_metric = map->metric;
+            p->graph_format = cfg->format;
             p->graph_gamma = a.gamma;
             p->graph_max_iters = cfg->max_iters;
             p->graph_rtol = cfg->rtol;
@@ -1094,6 +1103,11 @@ int run_core_periodic(bp_problem* p, const bp_map* map, const bp_iter_config* cf
     a.ctl.rtol = cfg->rtol;
     a.map_kind = map->kind == BP_MAP_FOURIER_DIAG ? MK_FOURIER_DIAG : MK_SCALAR;
     a.gamma = make_double2(map->gamma_re, map->gamma_im);
+    a.direct = cfg->format == BP_FMT_DIRECT;
+    const bool opt = map->kind == BP_MAP_OPTIMAL_SCALAR;
+    a.metric_reta = opt && map->metric == BP_METRIC_RETA;
+    a.D = p->x;   // OptimalScalar: spectral direction (x is free once the run has started)
+    a.T2 = p->y;  // OptimalScalar (Euclidean): second intermediate (snapshots reuse y between sweeps)
     if (map->kind == BP_MAP_FOURIER_DIAG) {
         CU(cudaMemcpyAsync(p->fd, map->m, sizeof(double2) * p->field, cudaMemcpyHostToDevice, p->stream));
     }
@@ -1126,9 +1140,22 @@ int run_core_periodic(bp_problem* p, const bp_map* map, const bp_iter_config* cf
     p->stat_timed = 0;
     const long max_launch = (long)cfg->max_iters + 1;
     const size_t nd = p->dense_pts;
+    // launches per sweep: scalar / FourierDiag 2; OptimalScalar 4 (Euclidean) or 5 (R_eta)
+    const int per_sweep = opt ? (a.metric_reta ? 5 : 4) : 2;
     auto sweep = [&](cudaEvent_t* ev) -> int {
         if (ev) CU(cudaEventRecord(ev[0], p->stream));
-        CU(launch_periodic(p->log2n, false, CP_SWEEP, a, p->stream));
+        if (opt) {
+            CU(launch_periodic(p->log2n, false, CP_OPT_A, a, p->stream));
+            if (a.metric_reta) {
+                CU(launch_periodic(p->log2n, true, RP_RETA_B, a, p->stream));
+                CU(launch_periodic(p->log2n, false, CP_RETA_C, a, p->stream));
+            } else {
+                CU(launch_periodic(p->log2n, true, RP_OPT_B, a, p->stream));
+            }
+            CU(launch_periodic(p->log2n, false, CP_OPT_C, a, p->stream));
+        } else {
+            CU(launch_periodic(p->log2n, false, CP_SWEEP, a, p->stream));
+        }
         if (ev) CU(cudaEventRecord(ev[1], p->stream));
         CU(launch_periodic(p->log2n, true, RP_SWEEP, a, p->stream));
         if (ev) CU(cudaEventRecord(ev[2], p->stream));
@@ -1140,7 +1167,7 @@ int run_core_periodic(bp_problem* p, const bp_map* map, const bp_iter_config* cf
         if (int rc = download(p, p->y, nullptr, nullptr, snapshots)) return rc;
         for (long k = 1; k <= max_launch; ++k) {
             if (int rc = sweep(nullptr)) return rc;
-            p->stat_launches += 2;
+            p->stat_launches += per_sweep;
             if (k < n_snap) {  // u^k = F^-1 U^k, U^k in buffer k&1
                 if (int rc = periodic_apply(p, 4, (k & 1) ? p->u1 : p->u0, p->y, nullptr)) return rc;
                 if (int rc = download(p, p->y, nullptr, nullptr, snapshots + 2 * nd * B * k)) return rc;
@@ -1163,7 +1190,7 @@ int run_core_periodic(bp_problem* p, const bp_map* map, const bp_iter_config* cf
         for (int s = 0; s < kGraphSweeps && rc == BP_OK; ++s) rc = sweep(p->timing ? &ev[3 * s] : nullptr);
         if (rc) break;
         launched += kGraphSweeps;
-        p->stat_launches += 2 * kGraphSweeps;
+        p->stat_launches += per_sweep * kGraphSweeps;
         CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
                            p->stream));
         CU(cudaStreamSynchronize(p->stream));
@@ -1435,8 +1462,11 @@ int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* c
     if (!map || !cfg) return set_err(BP_EINVAL, "run: null map or config");
     if (!(cfg->rtol > 0.0 && cfg->rtol < 1.0)) return set_err(BP_EINVAL, "run: rtol must lie in (0,1)");
     if (cfg->max_iters < 1) return set_err(BP_EINVAL, "run: max_iters must be >= 1");
-    if (cfg->format != BP_FMT_NPBS && cfg->format != BP_FMT_CBS)
-        return set_err(BP_ENOTSUP, "run: only the CBS / NPBS formats are implemented on the GPU");
+    if (cfg->format != BP_FMT_NPBS && cfg->format != BP_FMT_CBS && cfg->format != BP_FMT_DIRECT)
+        return set_err(BP_EINVAL, "run: unknown iteration format");
+    if (cfg->format == BP_FMT_DIRECT && (p->cdr || p->slab_log2 || p->slab_nranks > 1))
+        return set_err(BP_ENOTSUP, "run: the Direct format is implemented for the Helmholtz families "
+                                   "(Dirichlet, periodic) on one device");
     if (map->kind < BP_MAP_SCALAR || map->kind > BP_MAP_POINTWISE)
         return set_err(BP_EINVAL, "unknown correction map");
     if (map->kind == BP_MAP_FOURIER_DIAG && !map->m)
@@ -1446,8 +1476,9 @@ int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* c
         return set_err(BP_EINVAL, "unknown optimal-scalar metric");
     if (p->cdr && (map->kind != BP_MAP_SCALAR || map->gamma_im != 0.0))
         return set_err(BP_ENOTSUP, "CDR family on the GPU: real scalar maps only");
-    if (p->periodic && (map->kind == BP_MAP_OPTIMAL_SCALAR || map->kind == BP_MAP_POINTWISE))
-        return set_err(BP_ENOTSUP, "periodic family on the GPU: scalar and FourierDiag maps only");
+    if (p->periodic && map->kind == BP_MAP_POINTWISE)
+        return set_err(BP_ENOTSUP, "periodic family: the pointwise (i/eta) V map is defined for the "
+                                   "Dirichlet family only");
     return BP_OK;
 }
 
@@ -1463,6 +1494,8 @@ int bp_internal_set_error(int code, const char* msg) { return set_err(code, msg 
 // for pipeline.cpp: hooks run around the sweeps of every later run on this handle (null: none)
 int bp_internal_set_compute_hooks(bp_problem* p, void (*pre)(void*), void (*post)(void*), void* ctx) {
     if (int rc = check_problem(p)) return rc;
+    if (pre && p->hook_pre)  // one pipeline per handle: a second one would mix the tickets
+        return set_err(BP_EINVAL, "pipeline: the handle is already a slot of another pipeline");
     p->hook_pre = pre;
     p->hook_post = post;
     p->hook_ctx = ctx;

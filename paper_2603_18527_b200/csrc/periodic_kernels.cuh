@@ -10,6 +10,18 @@
 //   col kernel  (64 B/pt)  T -> forward x-FFT = Q^; U^m in; x^, r^ partials; U^{m+1} out;
 //                          inverse x-FFT of U^{m+1} / (nx ny) -> T; entry m + termination
 //   row kernel  (64 B/pt)  T -> inverse y-FFT = u^{m+1}; q = V u^{m+1} + f -> forward y-FFT -> T
+// OptimalScalar (correction.cpp:22-48) needs its gamma from a global reduction before the update,
+// so a sweep becomes (Euclidean metric, w = A d):
+//   CP_OPT_A (col)  Q^; x^, r^; entry m; D^ = direction (x^ or, Direct format, r^) stored;
+//                   T = F_x^-1 D^, T2 = F_x^-1 (r^ or lambda D^) (both / (nx ny))
+//   RP_OPT_B (row)  d = F_y^-1 T, s = F_y^-1 T2 (= r, or L_ref d); w = s - V d (key identity
+//                   A x = r - V x, or A r = L_ref r - V r); <w, r>, |w|^2 -> gamma (last CTA)
+//   CP_OPT_C (col)  U^{m+1} = U^m + gamma D^; T = F_x^-1 U^{m+1} / (nx ny)
+//   RP_SWEEP (row)  as the scalar sweep
+// and for the R_eta metric (w = d - G V d, gamma = <w, d> / |w|^2, correction.cpp:38-44):
+//   CP_OPT_A (T only), RP_RETA_B (row: d = F_y^-1 T; F_y (V d) -> T),
+//   CP_RETA_C (col: (V d)^ = F_x T; w^ = D^ - (V d)^ / lambda; <w, d>, |w|^2 by Parseval ->
+//   gamma), CP_OPT_C, RP_SWEEP.
 // Transforms follow proj/include/bp/transforms.hpp:16-17: unnormalised forward DFT, inverse
 // with 1/(nx ny).  Grids are n x n, n = 2^k, no padding (every node is a degree of freedom).
 #pragma once
@@ -66,8 +78,9 @@ struct FftEngine {
     }
 };
 
-enum PRowMode { RP_FWD = 0, RP_FWD_BORN = 1, RP_INV = 2, RP_SWEEP = 3 };
-enum PColMode { CP_ONE = 0, CP_GREEN = 1, CP_LREF = 2, CP_SWEEP = 3, CP_INV = 4 };
+enum PRowMode { RP_FWD = 0, RP_FWD_BORN = 1, RP_INV = 2, RP_SWEEP = 3, RP_OPT_B = 4, RP_RETA_B = 5 };
+enum PColMode { CP_ONE = 0, CP_GREEN = 1, CP_LREF = 2, CP_SWEEP = 3, CP_INV = 4, CP_OPT_A = 5,
+                CP_OPT_C = 6, CP_RETA_C = 7 };
 
 struct PerArgs {
     int batch;
@@ -88,8 +101,48 @@ struct PerArgs {
     double inv_npts;           // 1 / (nx ny)
     int map_kind;              // MK_SCALAR / MK_FOURIER_DIAG
     double2 gamma;
+    int direct;                // IterFormat::Direct: direction = r (iterate.cpp:122), else r_bs
+    int metric_reta;           // OptimalScalar metric R_eta (CP_OPT_A writes T only)
+    double2* D;                // OptimalScalar: spectral direction D^ (CP_OPT_A -> CP_OPT_C / CP_RETA_C)
+    double2* T2;               // OptimalScalar (Euclidean): second intermediate (r, or L_ref d)
     Control ctl;
 };
+
+// Fixed-order CTA sum of NP per-thread values, then the member's CTAs are combined by its
+// last-arriving CTA (atomic counter; partial slots [b][slot]): `fin(sums)` runs on one thread
+// of that CTA.  Deterministic: the per-CTA partials are summed in slot order.
+template <int NP, int NTHR, class Fin>
+__device__ __forceinline__ void member_reduce(const Control& c, int b, int slot, int nslots, int slot_stride,
+                                              const double (&v)[NP], Fin fin) {
+    __shared__ double red[NP][NTHR];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) red[k][threadIdx.x] = v[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double* pr = c.partial + ((size_t)b * slot_stride + slot) * kPartStride;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            double s = 0.0;
+            for (int i = 0; i < NTHR; ++i) s += red[k][i];
+            pr[k] = s;
+        }
+        __threadfence();
+        const unsigned old = atomicAdd(&c.counter[b], 1u);
+        if (old == (unsigned)(nslots - 1)) {
+            __threadfence();
+            double s[NP];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) s[k] = 0.0;
+            for (int i = 0; i < nslots; ++i) {
+                const double* pk = c.partial + ((size_t)b * slot_stride + i) * kPartStride;
+#pragma unroll
+                for (int k = 0; k < NP; ++k) s[k] += __ldcg(pk + k);
+            }
+            c.counter[b] = 0u;
+            fin(s);
+        }
+    }
+}
 
 // ------------------------------------------------------------------ row kernel (y lines)
 template <int LOG2N, int MODE, int NW, int PP>
@@ -108,7 +161,10 @@ prow_kernel(const PerArgs a) {
     const long grow = (long)blockIdx.x * EPB + e;
     const int b = (int)(grow >> LOG2N);
     bool valid = b < a.batch;
-    if (MODE == RP_SWEEP && valid) valid = __ldcg(&a.ctl.status[b]) == ST_ACTIVE;
+    constexpr bool ITER = MODE == RP_SWEEP || MODE == RP_OPT_B || MODE == RP_RETA_B;
+    if (ITER && valid) valid = __ldcg(&a.ctl.status[b]) == ST_ACTIVE;
+    // (RP_OPT_B reduces over the member's rows: a CTA exits only when none of its rows is
+    // active, so every row of an active member reaches the counter)
     if (!__syncthreads_or(valid)) return;
     double2* buf = smem + e * G::PAD_N;
     const Pol pol = make_policy((Pol*)nullptr, smem + EPB * G::PAD_N, e);
@@ -117,7 +173,69 @@ prow_kernel(const PerArgs a) {
     const double2 shift = make_double2(valid ? a.k0sq[b] : 0.0, valid ? a.eta[b] : 1.0);
 
     double2 q[P];
-    if constexpr (MODE == RP_INV || MODE == RP_SWEEP) {
+    if constexpr (MODE == RP_OPT_B) {
+        // d = F_y^-1 T, s = F_y^-1 T2 (physical; the column pass applied 1/(nx ny)); w = s - V d
+        double2 x[P], d[P], sv[P];
+#pragma unroll
+        for (int m = 0; m < P; ++m) x[m] = a.T[row + t + T * m];
+        Engine::template run<true>(x, d, t, buf, a.tw, pol);
+#pragma unroll
+        for (int m = 0; m < P; ++m) x[m] = a.T2[row + t + T * m];
+        Engine::template run<true>(x, sv, t, buf, a.tw, pol);
+        double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            const int j = t + T * m;
+            const double2 V = csub(a.k2[row + j], shift);
+            const double2 w = csub(sv[m], cmul(V, d[m]));
+            const double2 r = a.direct ? d[m] : sv[m];   // the Euclidean residual r
+            acc[0] += w.x * r.x + w.y * r.y;              // Re conj(w) r   (kernels::dotc)
+            acc[1] += w.x * r.y - w.y * r.x;              // Im conj(w) r
+            acc[2] += cnorm(w);                           // |w|^2          (kernels::norm2sq)
+        }
+        // per-row partials (engine-wide fixed-order sums); the member's last row sums its n
+        // row partials in row order (lanes strided, fixed tree) and finalises gamma.  A CTA may
+        // hold rows of several members (small n), so the reduction is per row, not per CTA.
+        const int i = (int)(grow & (N - 1));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] = pol.sum(acc[k], t);
+        int last = 0;
+        if (valid && t == 0) {
+            double* pr = a.ctl.partial + ((size_t)b * N + i) * kPartStride;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) pr[k] = acc[k];
+            __threadfence();
+            last = atomicAdd(&a.ctl.counter[b], 1u) == (unsigned)(N - 1);
+        }
+        last = pol.bcast0(last, t);
+        if (last) {
+            __threadfence();
+            double sm[3] = {0.0, 0.0, 0.0};
+            for (int r = t; r < N; r += T) {
+                const double* pr = a.ctl.partial + ((size_t)b * N + r) * kPartStride;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) sm[k] += __ldcg(pr + k);
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) sm[k] = pol.sum(sm[k], t);
+            if (t == 0) {
+                a.ctl.counter[b] = 0u;
+                finalize_gamma(a.ctl, b, sm[0], sm[1], sm[2]);
+            }
+        }
+        return;
+    } else if constexpr (MODE == RP_RETA_B) {
+        // d = F_y^-1 T (physical); V d -> forward y-FFT -> T (for G V d)
+        double2 x[P], d[P];
+#pragma unroll
+        for (int m = 0; m < P; ++m) x[m] = a.T[row + t + T * m];
+        Engine::template run<true>(x, d, t, buf, a.tw, pol);
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            const int j = t + T * m;
+            q[m] = cmul(d[m], csub(a.k2[row + j], shift));  // apply_V(d)
+        }
+    } else if constexpr (MODE == RP_INV || MODE == RP_SWEEP) {
         double2 x[P], z[P];
 #pragma unroll
         for (int m = 0; m < P; ++m) x[m] = valid ? a.T[row + t + T * m] : zero;
@@ -170,28 +288,69 @@ pcol_kernel(const PerArgs a) {
     const int b = bid / GROUPS;
     const int q = (bid % GROUPS) * C + c;
     int mstep = 0;
-    if constexpr (MODE == CP_SWEEP) {
+    constexpr bool ITER = MODE == CP_SWEEP || MODE == CP_OPT_A || MODE == CP_OPT_C || MODE == CP_RETA_C;
+    if constexpr (ITER) {
         if (__ldcg(&a.ctl.status[b]) != ST_ACTIVE) return;  // uniform per CTA
-        mstep = __ldcg(&a.ctl.sweep[b]);
+        // entry m of this sweep; CP_OPT_C / CP_RETA_C run after CP_OPT_A recorded it
+        mstep = __ldcg(&a.ctl.sweep[b]) - ((MODE == CP_OPT_C || MODE == CP_RETA_C) ? 1 : 0);
     }
     double2* buf = smem + c * G::PAD_N;
     const BlockSeg<T, C> pol{smem + C * G::PAD_N, c};
     const size_t mem = (size_t)b * N * N;
 
     double2 x[P], y[P];
+    if constexpr (MODE != CP_OPT_C) {
 #pragma unroll
-    for (int m = 0; m < P; ++m) x[m] = a.T[mem + (size_t)(t + T * m) * N + q];
+        for (int m = 0; m < P; ++m) x[m] = a.T[mem + (size_t)(t + T * m) * N + q];
+    }
     if constexpr (MODE == CP_INV) {
         Engine::template run<true>(x, y, t, buf, a.tw, pol);
 #pragma unroll
         for (int m = 0; m < P; ++m) a.T[mem + (size_t)(t + T * m) * N + q] = cscale(y[m], a.scale);
         return;
-    } else {
+    } else if constexpr (MODE != CP_OPT_C) {
         Engine::template run<false>(x, y, t, buf, a.tw, pol);
     }
     if constexpr (MODE == CP_ONE) {
 #pragma unroll
         for (int m = 0; m < P; ++m) a.T[mem + (size_t)(t + T * m) * N + q] = cscale(y[m], a.scale);
+        return;
+    } else if constexpr (MODE == CP_OPT_C) {
+        // U^{m+1} = U^m + gamma D^ (kernels::scale + add); T = F_x^-1 U^{m+1} / (nx ny)
+        const double2* Ucur = (mstep & 1) ? a.U1 : a.U0;
+        double2* Unext = (mstep & 1) ? a.U0 : a.U1;
+        const double2 g = a.ctl.gamma[b];
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            const size_t idx = mem + (size_t)(t + T * m) * N + q;
+            const double2 Un = cadd(Ucur[idx], cmul(g, a.D[idx]));
+            Unext[idx] = Un;
+            x[m] = Un;
+        }
+        Engine::template run<true>(x, y, t, buf, a.tw, pol);
+#pragma unroll
+        for (int m = 0; m < P; ++m) a.T[mem + (size_t)(t + T * m) * N + q] = cscale(y[m], a.inv_npts);
+        return;
+    } else if constexpr (MODE == CP_RETA_C) {
+        // y = (V d)^; w^ = D^ - (V d)^ / lambda (= F(d - G V d)); Parseval: <w, d>, |w|^2 carry
+        // the same 1/(nx ny) factor, which cancels in gamma = <w, d> / |w|^2
+        const double k0sq = a.k0sq[b], eta = a.eta[b];
+        const double xq = a.xi2[q];
+        double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            const int p = t + T * m;
+            const double lr = (a.xi2[p] + xq) - k0sq, li = -eta;
+            const double inv = rcp_green(fma(lr, lr, li * li));
+            const double2 D = a.D[mem + (size_t)p * N + q];
+            const double2 w = csub(D, cmul(y[m], make_double2(lr * inv, -li * inv)));
+            acc[0] += w.x * D.x + w.y * D.y;
+            acc[1] += w.x * D.y - w.y * D.x;
+            acc[2] += cnorm(w);
+        }
+        member_reduce<3, C * T>(a.ctl, b, bid % GROUPS, GROUPS, N, acc, [&](const double (&s)[3]) {
+            finalize_gamma(a.ctl, b, s[0], s[1], s[2]);
+        });
         return;
     } else {
         const double k0sq = a.k0sq[b], eta = a.eta[b];
@@ -210,7 +369,7 @@ pcol_kernel(const PerArgs a) {
                 x[m] = cmul(y[m], make_double2(lr * s, -li * s));
             } else if constexpr (MODE == CP_LREF) {
                 x[m] = cmul(y[m], make_double2(lr * a.scale, li * a.scale));
-            } else {  // CP_SWEEP
+            } else {  // CP_SWEEP, CP_OPT_A
                 const size_t idx = mem + (size_t)p * N + q;
                 const double2 U = Ucur[idx];
                 const double inv = rcp_green(fma(lr, lr, li * li));
@@ -219,20 +378,36 @@ pcol_kernel(const PerArgs a) {
                 const double2 rs = csub(y[m], cmul(make_double2(lr, li), U)); // r^
                 s_x += cnorm(xs);
                 s_r += cnorm(rs);
-                double2 g = a.gamma;
-                if (a.map_kind == MK_FOURIER_DIAG) g = a.fd[(size_t)p * N + q];
-                const double2 Un = cadd(U, cmul(g, xs));
-                Unext[idx] = Un;
-                x[m] = Un;
+                const double2 dir = a.direct ? rs : xs;  // iterate.cpp:118-123 direction
+                if constexpr (MODE == CP_OPT_A) {
+                    a.D[idx] = dir;
+                    x[m] = dir;
+                    // second line: r^ (Euclidean, NPBS) or L_ref d^ = lambda r^ (Direct)
+                    y[m] = a.direct ? cmul(make_double2(lr, li), rs) : rs;
+                } else {
+                    double2 g = a.gamma;
+                    if (a.map_kind == MK_FOURIER_DIAG) g = a.fd[(size_t)p * N + q];
+                    const double2 Un = cadd(U, cmul(g, dir));
+                    Unext[idx] = Un;
+                    x[m] = Un;
+                }
+            }
+        }
+        if constexpr (MODE == CP_OPT_A) {
+            if (!a.metric_reta) {  // T2 = F_x^-1 (second line) / (nx ny)
+                double2 y2[P];
+                Engine::template run<true>(y, y2, t, buf, a.tw, pol);
+#pragma unroll
+                for (int m = 0; m < P; ++m) a.T2[mem + (size_t)(t + T * m) * N + q] = cscale(y2[m], a.inv_npts);
             }
         }
         // inverse x-FFT -> T (scaled so the row kernel's inverse y-FFT is the physical field)
         Engine::template run<true>(x, y, t, buf, a.tw, pol);
-        const double osc = MODE == CP_SWEEP ? a.inv_npts : 1.0;
+        const double osc = (MODE == CP_SWEEP || MODE == CP_OPT_A) ? a.inv_npts : 1.0;
 #pragma unroll
         for (int m = 0; m < P; ++m) a.T[mem + (size_t)(t + T * m) * N + q] = cscale(y[m], osc);
 
-        if constexpr (MODE == CP_SWEEP) {
+        if constexpr (MODE == CP_SWEEP || MODE == CP_OPT_A) {
             // CTA partial sums (fixed order), last CTA of the member finalises entry mstep
             __shared__ double red[2][C * T];
             red[0][threadIdx.x] = s_r;

@@ -71,14 +71,21 @@ struct bp_pipeline {
 
 namespace {
 
+// The slot whose worker runs on this thread.  The compute hooks act only there: a direct
+// bp_run / bp_run_device on a slot handle from any other thread (while the pipeline exists)
+// runs without taking a turn instead of waiting for a ticket that is not its own.
+thread_local const Slot* tl_worker_slot = nullptr;
+
 void turn_acquire(void* ctx) {
     auto* sl = static_cast<Slot*>(ctx);
+    if (tl_worker_slot != sl) return;
     std::unique_lock<std::mutex> lk(sl->pl->m);
     sl->pl->cv_turn.wait(lk, [&] { return sl->pl->compute_turn == sl->ticket; });
 }
 
 void turn_release(void* ctx) {
     auto* sl = static_cast<Slot*>(ctx);
+    if (tl_worker_slot != sl) return;
     {
         std::lock_guard<std::mutex> lk(sl->pl->m);
         ++sl->pl->compute_turn;
@@ -98,6 +105,7 @@ int run_job(bp_problem* p, const Job& j) {
 }
 
 void worker_loop(bp_pipeline* pl, int s) {
+    tl_worker_slot = &pl->slots[s];
     for (;;) {
         Job job;
         {

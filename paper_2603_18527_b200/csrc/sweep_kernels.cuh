@@ -140,6 +140,13 @@ struct RowArgs {
     const double* sinp;        // sin(pi j/n), j < n
     int map_kind;
     double2 gamma;
+    // IterFormat::Direct (iterate.cpp:118-123): the direction is the residual r^m itself
+    // instead of r_bs^m = G r^m (CBS / NPBS)
+    int direct;
+    // Direct format + OptimalScalar (Euclidean): w = A r = L_ref r - V r.  R_FD_A also stores
+    // the direction into X and R_RETA_C forms w = (L_ref r) - V r from its inverse transform
+    // of the C_LREF column pass instead of w = x - G V x
+    int lw;
     Control ctl;
     // x-slab of a grid distributed over ranks (2-D, batch 1; 0 = whole members): the launch
     // covers 2^slab_log2 rows starting at global row row0; u / k2 / f hold those rows (u with
@@ -401,6 +408,9 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     const double k0sq = valid ? a.k0sq[b] : 0.0;
     const double eta = valid ? a.eta[b] : 1.0;
     const double2 shift = make_double2(k0sq, eta);
+    // pointwise map gamma(x) = (i/eta) V(x): one division per line, not one per element (the
+    // unrolled element loop otherwise carried an FP64 divide + slow-path call per element)
+    const double inv_eta = 1.0 / eta;
 
     // Stage the element-wise operands of this row (and the stencil halo rows at the CTA's
     // edges) into L2 while the transform runs: the loads after the engine then hit L2.
@@ -528,7 +538,9 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         } else if constexpr (MODE == R_RETA_C) {
             // z = G V x: w = x - G V x (correction.cpp:38-44); gamma = <w, x> / <w, w>
             const double2 x = valid ? a.X[row + j] : zero;
-            const double2 w = csub(x, zz);
+            // R_eta metric: w = x - G V x; Direct + Euclidean: w = L_ref x - V x (= A x)
+            const double2 w = a.lw ? csub(zz, cmul(csub(valid ? a.k2[row + j] : zero, shift), x))
+                                   : csub(x, zz);
             if (j != 0) {
                 acc[0] += w.x * x.x + w.y * x.y;  // Re conj(w) x
                 acc[1] += w.x * x.y - w.y * x.x;  // Im conj(w) x
@@ -561,16 +573,19 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
                     acc[0] += cnorm(r);
                     acc[1] += cnorm(x);
                 }
+                // direction of the update (iterate.cpp:118-123): r (Direct) or r_bs = G r
+                const double2 d = a.direct ? r : x;
                 if constexpr (MODE == R_SWEEP) {
                     double2 g = a.gamma;
-                    if (a.map_kind == MK_POINTWISE) g = cscale(mul_pi(V), 1.0 / eta);  // (i/eta) V
-                    double2 unew = cadd(u, cmul(g, x));
+                    if (a.map_kind == MK_POINTWISE) g = cscale(mul_pi(V), inv_eta);  // (i/eta) V
+                    double2 unew = cadd(u, cmul(g, d));
                     if (j == 0) unew = zero;
                     if (valid) unext[row + j] = unew;
                     qv = cadd(cmul(V, unew), f);
                 } else if constexpr (MODE == R_OPT_A) {
                     // w = A x = (L_ref - V) G r = r - V x (key identity; the reference applies
                     // A by stencil, correction.cpp:33-36 -- equal to roundoff)
+                    // (NPBS / CBS only: Direct + Euclidean takes the R_FD_A / C_LREF plan)
                     const double2 w = csub(r, cmul(V, x));
                     if (j != 0) {
                         acc[2] += w.x * r.x + w.y * r.y;
@@ -579,10 +594,11 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
                     }
                     if (valid) a.X[row + j] = (j == 0) ? zero : x;
                 } else if constexpr (MODE == R_RETA_A) {
-                    if (valid) a.X[row + j] = (j == 0) ? zero : x;
-                    qv = (j == 0) ? zero : cmul(x, V);  // apply_V(x)
+                    if (valid) a.X[row + j] = (j == 0) ? zero : d;
+                    qv = (j == 0) ? zero : cmul(d, V);  // apply_V(d)
                 } else {  // R_FD_A: forward transform of the direction itself
-                    qv = (j == 0) ? zero : x;
+                    if (a.lw && valid) a.X[row + j] = (j == 0) ? zero : d;
+                    qv = (j == 0) ? zero : d;
                 }
             } else {
                 // R_OPT_B: u' = u + gamma x ; R_FD_B: u' = u + du (du = z)

@@ -200,6 +200,8 @@ cudaError_t launch_periodic_p(bool row, int mode, const PerArgs& a, cudaStream_t
             case RP_FWD: return launch_prow_t<L, RP_FWD, 16>(a, s, prep);
             case RP_FWD_BORN: return launch_prow_t<L, RP_FWD_BORN, 16>(a, s, prep);
             case RP_INV: return launch_prow_t<L, RP_INV, 16>(a, s, prep);
+            case RP_OPT_B: return launch_prow_t<L, RP_OPT_B, 16>(a, s, prep);
+            case RP_RETA_B: return launch_prow_t<L, RP_RETA_B, 16>(a, s, prep);
             default: return launch_prow_t<L, RP_SWEEP, 16>(a, s, prep);
         }
     }
@@ -208,6 +210,9 @@ cudaError_t launch_periodic_p(bool row, int mode, const PerArgs& a, cudaStream_t
         case CP_GREEN: return launch_pcol_t<L, CP_GREEN, 16>(a, s, prep);
         case CP_LREF: return launch_pcol_t<L, CP_LREF, 16>(a, s, prep);
         case CP_INV: return launch_pcol_t<L, CP_INV, 16>(a, s, prep);
+        case CP_OPT_A: return launch_pcol_t<L, CP_OPT_A, 16>(a, s, prep);
+        case CP_OPT_C: return launch_pcol_t<L, CP_OPT_C, 16>(a, s, prep);
+        case CP_RETA_C: return launch_pcol_t<L, CP_RETA_C, 16>(a, s, prep);
         default: return launch_pcol_t<L, CP_SWEEP, 16>(a, s, prep);
     }
 }

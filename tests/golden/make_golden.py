@@ -26,7 +26,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-from oracle import MAP_OPTIMAL_SCALAR, MAP_POINTWISE, MAP_SCALAR, Reference, ReferenceProblem  # noqa: E402
+from oracle import (FMT_DIRECT, MAP_OPTIMAL_SCALAR, MAP_POINTWISE, MAP_SCALAR, Reference,  # noqa: E402
+                    ReferenceProblem)
 import paper_2603_18527_b200 as bs  # noqa: E402
 
 
@@ -129,6 +130,51 @@ def periodic_golden():
         np.savez_compressed(os.path.join(HERE, f"ref_periodic_n{n}.npz"), **out)
 
 
+def round2_golden():
+    """Round-2 fixtures (new files only; the round-1 fixtures are left as committed).
+    ref_periodic_more.npz -- the reference's OWN periodic HelmholtzProblem (n = 32 instance of
+        ref_periodic_n32.npz): OptimalScalar with the R_eta metric, and the Direct format
+        (iterate.cpp:118-123) with OptimalScalar (Euclidean) and a small scalar gamma.
+    ref_direct.npz -- the Direct format on the Dirichlet five-point family (n = 16 / 32
+        instances of run_golden): scalar, pointwise, OptimalScalar (both metrics), FourierDiag."""
+    g = np.load(os.path.join(HERE, "ref_periodic_n32.npz"))
+    p = ReferenceProblem(g["k2"], float(g["k0"]), float(g["eta"]), periodic=True)
+    out = {}
+    cases = {"optreta": dict(map_kind=MAP_OPTIMAL_SCALAR, metric=1, rtol=1e-8, max_iters=4000),
+             "direct_optl2": dict(map_kind=MAP_OPTIMAL_SCALAR, metric=0, fmt=FMT_DIRECT, rtol=1e-3,
+                                  max_iters=300),
+             "direct_scalar": dict(map_kind=MAP_SCALAR, gamma=2e-5, fmt=FMT_DIRECT, rtol=1e-3,
+                                   max_iters=200)}
+    for name, kw in cases.items():
+        r = p.run(g["f"], **kw)
+        for k, v in dict(u=r.u, l2=r.res_l2, reta=r.res_reta, iters=r.iters, term=r.terminated).items():
+            out[f"run_{name}_{k}"] = v
+        print("periodic", name, r.iters, r.terminated)
+    np.savez_compressed(os.path.join(HERE, "ref_periodic_more.npz"), **out)
+
+    out = {}
+    rng = np.random.default_rng(5)
+    for n in (16, 32):
+        spec = bs.InstanceSpec(n=n, ppw=8.0, contrast=0.4, sigma_cells=2.0)
+        k2, f, k0, eta = bs.make_instances(spec, 0, 1)
+        out[f"n{n}_k2"], out[f"n{n}_f"], out[f"n{n}_k0"], out[f"n{n}_eta"] = k2[0], f[0], k0[0], eta[0]
+        p = ReferenceProblem(k2[0], k0[0], eta[0])
+        m = 0.5 + 0.05 * (rng.standard_normal(k2[0].shape) + 1j * rng.standard_normal(k2[0].shape))
+        out[f"n{n}_fd_m"] = m
+        cases = {"optl2": dict(map_kind=MAP_OPTIMAL_SCALAR, metric=0),
+                 "optreta": dict(map_kind=MAP_OPTIMAL_SCALAR, metric=1),
+                 "scalar": dict(map_kind=MAP_SCALAR, gamma=1.0 / (8.0 * n * n)),
+                 "pointwise": dict(map_kind=MAP_POINTWISE),
+                 "fd": dict(map_kind=2, m=m * (1.0 / (8.0 * n * n)))}
+        for name, kw in cases.items():
+            r = p.run(f[0], fmt=FMT_DIRECT, rtol=1e-4, max_iters=150, **kw)
+            for k, v in dict(u=r.u, l2=r.res_l2, reta=r.res_reta, iters=r.iters,
+                             term=r.terminated).items():
+                out[f"n{n}_{name}_{k}"] = v
+            print("direct", n, name, r.iters, r.terminated)
+    np.savez_compressed(os.path.join(HERE, "ref_direct.npz"), **out)
+
+
 def dct_golden():
     rng = np.random.default_rng(44)
     out = {}
@@ -162,8 +208,8 @@ def io_golden():
 
 if __name__ == "__main__":
     Reference.set_mode("serial")
-    if sys.argv[1:] in (["dct"], ["io"]):
-        {"dct": dct_golden, "io": io_golden}[sys.argv[1]]()
+    if sys.argv[1:] in (["dct"], ["io"], ["round2"]):
+        {"dct": dct_golden, "io": io_golden, "round2": round2_golden}[sys.argv[1]]()
         sys.exit(0)
     io_golden()
     dct_golden()
@@ -174,4 +220,5 @@ if __name__ == "__main__":
     ops_golden()
     run_golden()
     periodic_golden()
+    round2_golden()
     print("golden fixtures written to", HERE)

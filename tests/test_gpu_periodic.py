@@ -8,7 +8,7 @@ import pytest
 
 from conftest import GOLDEN
 import paper_2603_18527_b200 as bs
-from oracle import MAP_FOURIER_DIAG, MAP_SCALAR, Oracle, OracleProblem
+from oracle import MAP_FOURIER_DIAG, MAP_OPTIMAL_SCALAR, MAP_SCALAR, Oracle, OracleProblem
 
 pytestmark = pytest.mark.gpu
 FIELD_TOL = 1e-10
@@ -36,11 +36,13 @@ def test_periodic_operators_match_reference(gpu, n):
 
 
 @pytest.mark.parametrize("n", [32, 64])
-@pytest.mark.parametrize("name", ["scalar", "scalar_relaxed", "fd"])
+@pytest.mark.parametrize("name", ["scalar", "scalar_relaxed", "fd", "optl2"])
 def test_periodic_runs_match_reference(gpu, n, name):
+    # optl2: OptimalScalarMap{Euclidean}, the reference's own default CBS map on its own family
+    # (proj/src/bench.cpp:140-141, correction.cpp:22-48)
     g = np.load(os.path.join(GOLDEN, f"ref_periodic_n{n}.npz"))
     cmap = {"scalar": bs.ScalarMap(1.0), "scalar_relaxed": bs.ScalarMap(0.9 + 0.05j),
-            "fd": bs.FourierDiagMap(g["fd_m"])}[name]
+            "fd": bs.FourierDiagMap(g["fd_m"]), "optl2": bs.OptimalScalarMap("euclidean")}[name]
     with bs.HelmholtzPeriodic(g["k2"], float(g["k0"]), float(g["eta"])) as p:
         res = bs.run(p, cmap, g["f"], bs.IterationConfig(rtol=1e-8, max_iters=4000))
     tr, iters = res.trace, int(g[f"run_{name}_iters"])
@@ -91,10 +93,48 @@ def test_periodic_per_iterate_and_warm_start(gpu):
     np.testing.assert_allclose(res.trace.res_l2_rel, ref.res_l2, rtol=1e-8)
 
 
+@pytest.mark.parametrize("name", ["optreta", "direct_optl2", "direct_scalar"])
+def test_periodic_more_runs_match_reference(gpu, name):
+    """OptimalScalar with the R_eta metric and the Direct format (direction = r,
+    iterate.cpp:118-123) on the reference's periodic family, vs the reference's own run()."""
+    g = np.load(os.path.join(GOLDEN, "ref_periodic_n32.npz"))
+    h = np.load(os.path.join(GOLDEN, "ref_periodic_more.npz"))
+    cmap, cfg = {
+        "optreta": (bs.OptimalScalarMap("reta"), bs.IterationConfig(rtol=1e-8, max_iters=4000)),
+        "direct_optl2": (bs.OptimalScalarMap("euclidean"),
+                         bs.IterationConfig(format="direct", rtol=1e-3, max_iters=300)),
+        "direct_scalar": (bs.ScalarMap(2e-5), bs.IterationConfig(format="direct", rtol=1e-3, max_iters=200)),
+    }[name]
+    with bs.HelmholtzPeriodic(g["k2"], float(g["k0"]), float(g["eta"])) as p:
+        res = bs.run(p, cmap, g["f"], cfg)
+    tr, iters = res.trace, int(h[f"run_{name}_iters"])
+    assert tr.terminated == str(h[f"run_{name}_term"])
+    assert abs(tr.iters - iters) <= 1
+    k = min(tr.iters, iters) + 1
+    np.testing.assert_allclose(tr.res_l2_rel[:k], h[f"run_{name}_l2"][:k], rtol=1e-8, atol=1e-13)
+    np.testing.assert_allclose(tr.res_reta_rel[:k], h[f"run_{name}_reta"][:k], rtol=1e-8, atol=1e-13)
+    if tr.iters == iters:
+        assert rel(res.u, h[f"run_{name}_u"]) < FIELD_TOL
+
+
+def test_periodic_optimal_scalar_per_iterate_vs_oracle(gpu):
+    """Per-iterate u^m of the periodic OptimalScalar runs (both metrics) vs the plain-C oracle."""
+    g = np.load(os.path.join(GOLDEN, "ref_periodic_n64.npz"))
+    K = 25
+    o = OracleProblem(g["k2"], float(g["k0"]), float(g["eta"]), periodic=True)
+    for metric, mk in (("euclidean", 0), ("reta", 1)):
+        with bs.HelmholtzPeriodic(g["k2"], float(g["k0"]), float(g["eta"])) as p:
+            res = bs.run(p, bs.OptimalScalarMap(metric), g["f"], bs.IterationConfig(rtol=1e-12, max_iters=K),
+                         n_snap=K + 1)
+        ref = o.run(g["f"], map_kind=MAP_OPTIMAL_SCALAR, metric=mk, rtol=1e-12, max_iters=K, n_snap=K + 1)
+        assert res.trace.iters == ref.iters == K
+        assert not np.any(res.snapshots[0])  # u^0 = 0
+        for m in range(1, K + 1):
+            assert rel(res.snapshots[m], ref.snapshots[m]) < FIELD_TOL, (metric, m)
+
+
 def test_periodic_unsupported_maps_raise(gpu):
     g = np.load(os.path.join(GOLDEN, "ref_periodic_n32.npz"))
     with bs.HelmholtzPeriodic(g["k2"], float(g["k0"]), float(g["eta"])) as p:
-        with pytest.raises(NotImplementedError):
-            bs.run(p, bs.OptimalScalarMap(), g["f"])
-        with pytest.raises(NotImplementedError):
+        with pytest.raises(NotImplementedError):  # a Dirichlet-family map (PAPER.md:207)
             bs.run(p, bs.PointwiseMap(), g["f"])

@@ -87,3 +87,29 @@ def test_pipeline_reports_job_errors(gpu):
         assert r.traces[0].iters > 0
     for p in slots:
         p.close()
+
+
+def test_direct_run_on_a_slot_handle_and_second_pipeline(gpu):
+    """A direct bs.run on a slot handle between jobs (another thread than the slot's worker)
+    does not take a compute turn (it used to wait forever for a ticket); a handle cannot be a
+    slot of two pipelines at once."""
+    import threading
+    k2, f, k0, eta = bs.make_instances(bs.InstanceSpec(n=32, ppw=8.0, contrast=0.3), 0, 2)
+    cfg = bs.IterationConfig(rtol=1e-6, max_iters=60)
+    slots = [bs.HelmholtzDirichlet(k2, k0, eta) for _ in range(2)]
+    with bs.Pipeline(slots) as pipe:
+        pipe.submit(bs.ScalarMap(1.0), f, cfg)
+        (first,) = pipe.wait()
+        out = {}
+        th = threading.Thread(target=lambda: out.setdefault("r", bs.run(slots[0], bs.ScalarMap(1.0), f, cfg)))
+        th.start()
+        th.join(timeout=60)
+        assert not th.is_alive(), "direct bp_run on a pipeline slot hung"
+        _same(out["r"], first)
+        with pytest.raises(ValueError, match="already a slot"):
+            bs.Pipeline(slots)
+        pipe.submit(bs.ScalarMap(1.0), f, cfg)  # the pipeline still works afterwards
+        (again,) = pipe.wait()
+        _same(again, first)
+    for p in slots:
+        p.close()
