@@ -245,6 +245,10 @@ cudaError_t launch_mixed(int log2n, const RowArgs& ra, const ColArgs& ca, cudaSt
     BS_SIZE_CASES(launch_mixed_L, ra, ca, s, prep)
 }
 
+cudaError_t launch_tri(int log2n, int layout, const ColArgs& a, cudaStream_t s, bool prep = false) {
+    BS_SIZE_CASES(launch_tri_L, layout, a, s, prep)
+}
+
 cudaError_t launch_row(int log2n, int dim, int mode, const RowArgs& a, cudaStream_t s) {
     return launch_row_pp(log2n, points_per_thread(log2n), dim, mode, a, s);
 }
@@ -264,6 +268,8 @@ cudaError_t prepare_kernels(int log2n, int dim) {
             if (cudaError_t r = launch_transposed(log2n, false, mode, a, c, nullptr, true)) e = r;
     }
     if (dim == 2) launch_mixed(log2n, a, c, nullptr, true);  // sizes without a mixed kernel: ignored
+    if (log2n >= 6)
+        if (cudaError_t r = launch_tri(log2n, dim == 3 ? CL_X3 : CL_PLANE, c, nullptr, true)) e = r;
     if (dim == 2) {
         CdrArgs ca{};
         for (int mode : {RC_FWD, RC_INV, RC_A, RC_B})
@@ -276,7 +282,7 @@ cudaError_t prepare_kernels(int log2n, int dim) {
             if (cudaError_t r = launch_periodic(log2n, false, mode, pa, nullptr, true)) e = r;
     }
     for (int pp : {8, 16}) {
-        for (int mode : {R_FWD, R_FWD_BORN, R_INV, R_SWEEP, R_OPT_A, R_OPT_B, R_RETA_A, R_RETA_C,
+        for (int mode : {R_FWD, R_FWD_BORN, R_INV, R_SWEEP, R_SWEEP_D, R_OPT_A, R_OPT_B, R_RETA_A, R_RETA_C,
                          R_FD_A, R_FD_B})
             if (cudaError_t r = launch_row_pp(log2n, pp, dim, mode, a, nullptr, true)) e = r;
         for (int mode : {C_ONE, C_GREEN, C_LREF, C_FD}) {
@@ -363,6 +369,10 @@ struct bp_problem {
     size_t alloc = 0;   // padded elements per buffer (batch*n^dim + n^(dim-1): zero halo)
     size_t dense_pts = 0;  // reference-layout points per member ((n-1)^dim)
     double inv_h2 = 0, green_scale = 0;
+    // Green column pass as a tridiagonal x-solve (tri_kernels.cuh): pivot tables per
+    // (member, line), rebuilt whenever k0 / eta change; null = transform route
+    double2* tri = nullptr;
+    double tri_scale = 0;
     cudaStream_t stream = nullptr;
     // device constants
     double2* k2 = nullptr;
@@ -470,6 +480,8 @@ ColArgs col_args(const bp_problem* p) {
     c.lap = p->lap;
     c.scale = p->green_scale;
     c.fd = p->fd;
+    c.tri = p->tri;
+    c.tri_scale = p->tri_scale;
     c.TT = p->TT;
     c.T = p->T;
     c.tw = p->tw;
@@ -604,6 +616,8 @@ int col_stage(bp_problem* p, const ColArgs& c0, int mode, double scale) {
     if (p->dim == 2) {
         c.planes_per_member = 1;
         c.scale = scale;
+        if (mode == C_GREEN && p->tri && scale == p->green_scale)
+            return launch_tri(p->log2n, CL_PLANE, c, p->stream) == cudaSuccess ? 1 : -1;
         return launch_col(p->log2n, CL_PLANE, mode, c, p->stream) == cudaSuccess ? 1 : -1;
     }
     c.planes_per_member = p->n;
@@ -611,7 +625,11 @@ int col_stage(bp_problem* p, const ColArgs& c0, int mode, double scale) {
     if (launch_col(p->log2n, CL_PLANE, C_ONE, c, p->stream) != cudaSuccess) return -1;
     c.finalize = 0;  // deferred finalisation (3-D) belongs to the first launch only
     c.scale = scale;
-    if (launch_col(p->log2n, CL_X3, mode, c, p->stream) != cudaSuccess) return -1;
+    if (mode == C_GREEN && p->tri && scale == p->green_scale) {
+        if (launch_tri(p->log2n, CL_X3, c, p->stream) != cudaSuccess) return -1;
+    } else if (launch_col(p->log2n, CL_X3, mode, c, p->stream) != cudaSuccess) {
+        return -1;
+    }
     if (mode == C_ONE) return 2;
     c.scale = 1.0;
     c.planes_per_member = p->n;
@@ -635,6 +653,18 @@ int green(bp_problem* p, const double2* in, double2* out, const double2* sub, bo
     a.out = out;
     a.sub = sub;
     CU(launch_row(p->log2n, p->dim, R_INV, a, p->stream));
+    return BP_OK;
+}
+
+// (Re)build the tridiagonal pivot tables from the device k0^2 / eta (stream-ordered after
+// their upload)
+int build_tri(bp_problem* p) {
+    if (!p->tri) return BP_OK;
+    const double h = p->grid.lx / p->n;
+    const long lines = (long)p->batch << ((p->dim - 1) * p->log2n);
+    tri_setup_kernel<<<(int)((lines + 127) / 128), 128, 0, p->stream>>>(p->lap, p->k0sq, p->eta, h * h, p->batch,
+                                                                       p->log2n, p->dim, p->tri);
+    CU(cudaGetLastError());
     return BP_OK;
 }
 
@@ -691,7 +721,7 @@ SweepPlan plan_for(const bp_map* map, int format) {
             s.add(false, C_GREEN);
             break;
         default:  // scalar gamma or pointwise gamma(x): one fused row pass
-            s.add(true, R_SWEEP);
+            s.add(true, format == BP_FMT_DIRECT ? R_SWEEP_D : R_SWEEP);
             s.add(false, C_GREEN);
     }
     return s;
@@ -833,7 +863,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     // 3-D: the first (y-line) launch of the column stage finalises, the whole CTA summing the
     // n^2 line partials (finalize_member3; col_stage clears the flag for the other two)
     if (!mixed && !p->transposed && (p->dim == 2 || p->dim == 3) && p->log2n >= 6 && plan.n == 2 &&
-        plan.row[0] && plan.mode[0] == R_SWEEP && !plan.row[1] && plan.mode[1] == C_GREEN) {
+        plan.row[0] && (plan.mode[0] == R_SWEEP || plan.mode[0] == R_SWEEP_D) && !plan.row[1] && plan.mode[1] == C_GREEN) {
         a.defer_final = 1;
         c.finalize = 1;
         c.fin_lsh = (p->dim - 1) * p->log2n;
@@ -1648,6 +1678,17 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     CUF(cudaMemcpyAsync(p->tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->sinp, sinp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->lap, lap.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
+    {
+        // Green column pass: tridiagonal x-solve for the Dirichlet family, n >= 64 (2-D columns,
+        // 3-D x-lines; BP_COL_DST=1 keeps the transform route)
+        const char* e = std::getenv("BP_COL_DST");
+        if (!periodic && log2n >= 6 && !(e && e[0] == '1')) {
+            const size_t lines = (size_t)batch << ((dim - 1) * log2n);
+            CUF(cudaMalloc(&p->tri, sizeof(double2) * lines * (kTriP + n / kTriP)));
+            p->tri_scale = 8.0 * n * h * h * p->green_scale;
+            if (int rc = build_tri(p)) return fail(rc);
+        }
+    }
     if (int rc = upload_k2_checked(p, k2)) return fail(rc);
     CUF(cudaStreamSynchronize(p->stream));
     if (int rc = ensure_trace(p, 1000)) return fail(rc);
@@ -2297,7 +2338,8 @@ int bp_problem_destroy(bp_problem* p) {
                     (void*)p->trace_l2, (void*)p->trace_reta, (void*)p->k0sq, (void*)p->eta,
                     (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2, (void*)p->TT,
                     (void*)p->bx, (void*)p->by, (void*)p->sigma, (void*)p->sigma0, (void*)p->lapn,
-                    (void*)p->rnorm2, (void*)p->w4, (void*)p->dflag, (void*)p->Tc, (void*)p->slab_sums})
+                    (void*)p->rnorm2, (void*)p->w4, (void*)p->dflag, (void*)p->Tc, (void*)p->slab_sums,
+                    (void*)p->tri})
         if (q) cudaFree(q);
     if (p->host_active) cudaFreeHost(p->host_active);
     if (p->stream && p->own_stream) cudaStreamDestroy(p->stream);
@@ -2511,6 +2553,7 @@ int bp_problem_set_medium(bp_problem* p, const double* k2, const double* k0, con
     for (int b = 0; b < p->batch; ++b) k0sq[b] = k0[b] * k0[b];
     CU(cudaMemcpyAsync(p->k0sq, k0sq.data(), sizeof(double) * p->batch, cudaMemcpyHostToDevice, p->stream));
     CU(cudaMemcpyAsync(p->eta, eta, sizeof(double) * p->batch, cudaMemcpyHostToDevice, p->stream));
+    if (int rc = build_tri(p)) return rc;
     CU(cudaStreamSynchronize(p->stream));
     return BP_OK;
 }

@@ -78,6 +78,7 @@ enum RowMode {
     R_RETA_C = 7,    // T -> inverse = G V x; w = x - G V x; <w,x>, |w|^2 -> gamma
     R_FD_A = 8,      // entry m; x = r_bs -> forward -> T (for the FourierDiag multiply)
     R_FD_B = 9,      // T -> inverse = du; u' = u + du; q = V u' + f -> forward -> T
+    R_SWEEP_D = 10,  // R_SWEEP with IterFormat::Direct: the update direction is r^m itself
 };
 enum ColMode { C_ONE = 0, C_GREEN = 1, C_LREF = 2, C_FD = 3 };
 enum Status { ST_ACTIVE = 0, ST_DONE = 1 };
@@ -86,18 +87,19 @@ constexpr int kPartStride = 8;  // doubles of per-row partial sums
 
 template <int MODE>
 struct RowSpec {
-    static constexpr bool INV = MODE == R_INV || MODE == R_SWEEP || MODE == R_OPT_A ||
+    static constexpr bool SWEEP = MODE == R_SWEEP || MODE == R_SWEEP_D;
+    static constexpr bool INV = MODE == R_INV || SWEEP || MODE == R_OPT_A ||
                                 MODE == R_RETA_A || MODE == R_RETA_C || MODE == R_FD_A || MODE == R_FD_B;
-    static constexpr bool FWD = MODE == R_FWD || MODE == R_FWD_BORN || MODE == R_SWEEP ||
+    static constexpr bool FWD = MODE == R_FWD || MODE == R_FWD_BORN || SWEEP ||
                                 MODE == R_OPT_B || MODE == R_RETA_A || MODE == R_FD_A || MODE == R_FD_B;
     // records trace entry m = sweep[b] (and the termination test)
-    static constexpr bool ENTRY = MODE == R_SWEEP || MODE == R_OPT_A || MODE == R_RETA_A || MODE == R_FD_A;
+    static constexpr bool ENTRY = SWEEP || MODE == R_OPT_A || MODE == R_RETA_A || MODE == R_FD_A;
     // runs after the entry of this sweep was recorded: m = sweep[b] - 1
     static constexpr bool POST = MODE == R_OPT_B || MODE == R_RETA_C || MODE == R_FD_B;
     static constexpr bool ITER = ENTRY || POST;
     static constexpr bool GAMMA = MODE == R_OPT_A || MODE == R_RETA_C;  // reduces a gamma
     static constexpr int NPART = MODE == R_OPT_A ? 5 : MODE == R_RETA_C ? 3 : ENTRY ? 2 : 0;
-    static constexpr bool UPDATE = MODE == R_SWEEP || MODE == R_OPT_B || MODE == R_FD_B;
+    static constexpr bool UPDATE = SWEEP || MODE == R_OPT_B || MODE == R_FD_B;
 };
 
 constexpr int kMaxXchg = 8;  // ranks of a fused-exchange slab group
@@ -202,7 +204,19 @@ struct ColArgs {
     int xchg_rank;
     int xchg_log2r;
     double2* xchg[kMaxXchg];
+    // C_GREEN as a tridiagonal x-solve (tri_kernels.cuh): pivot tables per (member, line) and
+    // the scale that makes it equal the transform route (8 n h^2 x scale)
+    const double2* tri;
+    double tri_scale;
 };
+
+// 1/eta of the pointwise map hoisted out of the row kernel's element loop: measured slower on
+// c1 (r02: 337.5 vs 329.5 us per row launch) -- the hoisted reciprocal stays live through the
+// unrolled loop and pushes the 128-register kernel into spills, which cost more than the
+// per-element divide
+#ifndef BS_INV_ETA_HOIST
+#define BS_INV_ETA_HOIST 0
+#endif
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ double2 ldcg2(const double2* p) { return __ldcg(p); }
@@ -410,7 +424,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     const double2 shift = make_double2(k0sq, eta);
     // pointwise map gamma(x) = (i/eta) V(x): one division per line, not one per element (the
     // unrolled element loop otherwise carried an FP64 divide + slow-path call per element)
-    const double inv_eta = 1.0 / eta;
+    [[maybe_unused]] const double inv_eta = BS_INV_ETA_HOIST ? 1.0 / eta : 0.0;
 
     // Stage the element-wise operands of this row (and the stencil halo rows at the CTA's
     // edges) into L2 while the transform runs: the loads after the engine then hit L2.
@@ -574,10 +588,16 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
                     acc[1] += cnorm(x);
                 }
                 // direction of the update (iterate.cpp:118-123): r (Direct) or r_bs = G r
-                const double2 d = a.direct ? r : x;
-                if constexpr (MODE == R_SWEEP) {
+                // (a compile-time choice: a runtime select kept r and x live together and made
+                // the c1 row kernel spill, 328 -> 368 us)
+                const double2 d = MODE == R_SWEEP_D ? r : (MODE == R_SWEEP ? x : (a.direct ? r : x));
+                if constexpr (RowSpec<MODE>::SWEEP) {
                     double2 g = a.gamma;
+#if BS_INV_ETA_HOIST
                     if (a.map_kind == MK_POINTWISE) g = cscale(mul_pi(V), inv_eta);  // (i/eta) V
+#else
+                    if (a.map_kind == MK_POINTWISE) g = cscale(mul_pi(V), 1.0 / eta);
+#endif
                     double2 unew = cadd(u, cmul(g, d));
                     if (j == 0) unew = zero;
                     if (valid) unext[row + j] = unew;
@@ -701,7 +721,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     if constexpr (S::NPART > 0) {
 #pragma unroll
         for (int k = 0; k < S::NPART; ++k) acc[k] = pol.sum(acc[k], t);
-        if constexpr (MODE == R_SWEEP && !SLAB) {
+        if constexpr (RowSpec<MODE>::SWEEP && !SLAB) {
             if (a.defer_final) {  // finalised by the next launch (col_group, ColArgs::finalize)
                 if constexpr (DIM == 3) {
                     // one partial per CTA (its EPB lines summed in engine order), stored in the

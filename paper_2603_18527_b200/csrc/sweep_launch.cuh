@@ -5,6 +5,7 @@
 #include "cdr_kernels.cuh"
 #include "periodic_kernels.cuh"
 #include "sweep_kernels.cuh"
+#include "tri_kernels.cuh"
 
 namespace bs {
 
@@ -82,6 +83,7 @@ cudaError_t launch_row_p(int mode, const RowArgs& a, cudaStream_t s, bool prepar
         case R_FWD_BORN: return launch_row_t<L, R_FWD_BORN, PP, DIM>(a, s, prepare);
         case R_INV: return launch_row_t<L, R_INV, PP, DIM>(a, s, prepare);
         case R_SWEEP: return launch_row_t<L, R_SWEEP, PP, DIM>(a, s, prepare);
+        case R_SWEEP_D: return launch_row_t<L, R_SWEEP_D, PP, DIM>(a, s, prepare);
         case R_OPT_A: return launch_row_t<L, R_OPT_A, PP, DIM>(a, s, prepare);
         case R_OPT_B: return launch_row_t<L, R_OPT_B, PP, DIM>(a, s, prepare);
         case R_RETA_A: return launch_row_t<L, R_RETA_A, PP, DIM>(a, s, prepare);
@@ -99,6 +101,31 @@ cudaError_t launch_col_p(int mode, const ColArgs& a, cudaStream_t s, bool prepar
         case C_FD: return launch_col_t<L, C_FD, PP, LAYOUT>(a, s, prepare);
         default: return launch_col_t<L, C_LREF, PP, LAYOUT>(a, s, prepare);
     }
+}
+
+// ---- Green column pass as a tridiagonal x-solve (n >= 64): persistent CTAs, one per
+// resident slot (occupancy queried once per instance)
+template <int L, int LAYOUT>
+cudaError_t launch_tri_t(const ColArgs& a, cudaStream_t s, bool prepare) {
+    if constexpr (L >= 6) {
+        using TG = TriGeom<L>;
+        using TT = TriTile<L>;
+        auto k = tri_kernel<L, LAYOUT>;
+        if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TT::SMEM);
+        static int slots = [&] {
+            int dev = 0, sms = 0, per = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, TG::THREADS, TT::SMEM);
+            return sms * (per > 0 ? per : 1);
+        }();
+        const long tiles = (long)a.batch * (LAYOUT == CL_X3 ? (1L << L) : 1L) * ((1 << L) / TG::C);
+        const int grid = (int)(tiles < slots ? tiles : slots);
+        if (grid == 0) return cudaSuccess;
+        k<<<grid, TG::THREADS, TT::SMEM, s>>>(a);
+        return cudaGetLastError();
+    }
+    return cudaErrorInvalidValue;
 }
 
 // ---- transposed 2-D handoff (n <= 512): TOUT row kernels + warp-per-line column pass
@@ -287,6 +314,12 @@ struct Pp8 {
     }                                                                                           \
     cudaError_t launch_mixed_L##L(const RowArgs& ra, const ColArgs& ca, cudaStream_t s, bool prep) { \
         return launch_mixed_t<L>(ra, ca, s, prep);                                              \
+    }                                                                                           \
+    cudaError_t launch_tri_L##L(int layout, const ColArgs& a, cudaStream_t s, bool prep) {     \
+        if (layout == CL_PLANE) return launch_tri_t<L, CL_PLANE>(a, s, prep);                   \
+        if constexpr (L <= kMaxLog2_3d)                                                         \
+            if (layout == CL_X3) return launch_tri_t<L, CL_X3>(a, s, prep);                     \
+        return cudaErrorInvalidValue;                                                           \
     }
 
 #define BS_DECLARE_SIZE(L)                                                                      \
@@ -299,7 +332,8 @@ struct Pp8 {
     cudaError_t launch_transposed_L##L(bool row, int mode, const RowArgs& a, const ColArgs& c,  \
                                        cudaStream_t s, bool prep);                              \
     cudaError_t launch_cdr_L##L(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep); \
-    cudaError_t launch_mixed_L##L(const RowArgs& ra, const ColArgs& ca, cudaStream_t s, bool prep);
+    cudaError_t launch_mixed_L##L(const RowArgs& ra, const ColArgs& ca, cudaStream_t s, bool prep); \
+    cudaError_t launch_tri_L##L(int layout, const ColArgs& a, cudaStream_t s, bool prep);
 
 BS_DECLARE_SIZE(3)
 BS_DECLARE_SIZE(4)

@@ -1,0 +1,355 @@
+// tri_kernels.cuh -- the Green column pass as a batched Toeplitz tridiagonal solve (sm_100a).
+//
+// The Dirichlet symbol is separable and its x factor a_p = (4/h^2) sin^2(p pi / 2n)
+// (proj/src/symbol.cpp:69-80) is exactly the spectrum of the three-point second difference
+// with zero ends.  After the row pass has taken y into the DST basis, the column pass
+//     forward x-DST -> x 1/lambda_pq -> inverse x-DST           (symbol.cpp:19-39, Divide)
+// is therefore, column q by column q, the solve
+//     (-D_xx + a_q - k0^2 - i eta) z = r,   z_0 = z_n = 0,
+// i.e. h^2-scaled: d z_i - z_{i-1} - z_{i+1} = h^2 r_i with d = 2 + h^2 (a_q - k0^2 - i eta).
+// Same operator, O(n) work per column instead of two length-n transforms: ~20 FP64
+// instructions per point instead of ~80, and the column never leaves registers except for a
+// handful of boundary values.  d lies off the real segment [-2, 2] (eta > 0), so the
+// elimination needs no pivoting and is backward stable.
+//
+// Parallel algorithm (one thread = one segment of P = 16 consecutive rows of one column):
+//   row 16s of each segment is a separator X_s (X_0 = z_0 = 0, X_S = z_n = 0); rows
+//   16s+1 .. 16s+15 are the segment interior, a 15 x 15 Toeplitz system with the separators
+//   as boundary values.  With p_k the LU pivots 1/u_k of that system (u_1 = d,
+//   u_k = d - p_{k-1}), delta = p_15 and gamma = prod p_k (the corner entries of its inverse):
+//     1. each thread eliminates its interior downwards and upwards (zero boundaries) ->
+//        zp_15, zp_1;
+//     2. the separators satisfy the reduced Toeplitz system
+//          (d - 2 delta) X_s - gamma (X_{s-1} + X_{s+1}) = h^2 r_{16s} + zp^{s-1}_15 + zp^s_1,
+//        solved by its own LU pivots pr_s as two first-order linear recurrences, each an
+//        affine-map scan across the segments (warp shuffles; chunk carries through shared
+//        memory for n >= 1024);
+//     3. each thread re-runs its elimination with the separators added and back-substitutes.
+// The pivot tables (p_1..p_15, gamma, pr_1..pr_{S-1} per column and member) depend on the
+// medium only through (k0, eta): tri_setup_kernel builds them when the medium is set.
+// Deterministic: fixed operation order, batch members independent (bit-identical to single
+// runs).
+#pragma once
+
+#include "sweep_kernels.cuh"
+
+namespace bs {
+
+constexpr int kTriP = 16;  // rows per segment
+#ifndef TRI_THREADS
+#define TRI_THREADS 256  // threads per CTA (n < 4096)
+#endif
+#ifndef TRI_REV
+#define TRI_REV 1
+#endif
+#ifndef TRI_PF
+#define TRI_PF 0  // tiles prefetched into L2 ahead of the shared-memory prefetch
+#endif
+
+template <int LOG2N>
+struct TriGeom {
+    static constexpr int N = 1 << LOG2N;
+    static constexpr int S = N / kTriP;                  // segments per column
+    static constexpr int C = S >= TRI_THREADS ? 2 : TRI_THREADS / S;  // columns per CTA
+    static constexpr int THREADS = C * S;
+    static constexpr int CW = C < 8 ? C : 8;             // columns side by side in a warp (16*CW-B rows)
+    static constexpr int SPW = 32 / CW;                  // segments per warp (load phase)
+    static constexpr int WPG = S / SPW;                  // warps per column group
+    static constexpr int TS = 16 + S;                    // table entries per column (double2)
+    // shared-memory row pitches, odd in 16-B units: the CW columns a warp reads at one index
+    // land on distinct bank groups (pitch TS = 48 put all 8 on one group: 8-way conflicts)
+    static constexpr int TSP = TS + 1;
+    static constexpr int SP = S + 1;
+    static constexpr int LPC = S < 32 ? S : 32;          // lanes per column (reduced phase)
+    static constexpr int CH = S / LPC;                   // warps per column (reduced phase)
+    static_assert(S >= SPW, "tridiagonal column pass needs n >= 64");
+};
+
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {  // a*b + c
+    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+
+// Pivot tables, one thread per (member, line).  Lines: 2-D columns q (a_t = a_q); 3-D x-lines
+// (y, z) (a_t = a_y + a_z).  Entry layout per line: [0..14] p_1..p_15, [15] gamma,
+// [16 + s] pr_s (pr_0 = 0).  Dirichlet zero lines (q = 0; y = 0 or z = 0) get zeros.
+static __global__ void tri_setup_kernel(const double* __restrict__ lap, const double* __restrict__ k0sq,
+                                 const double* __restrict__ eta, double h2, int batch, int log2n,
+                                 int dim, double2* __restrict__ tab) {
+    const int n = 1 << log2n, S = n / kTriP, TS = 16 + S;
+    const long lines = (long)batch << ((dim - 1) * log2n);
+    const long idx = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (idx >= lines) return;
+    const int b = (int)(idx >> ((dim - 1) * log2n));
+    const long l = idx & ((1L << ((dim - 1) * log2n)) - 1);
+    double2* t = tab + idx * TS;
+    bool zero;
+    double at;
+    if (dim == 2) {
+        zero = l == 0;
+        at = lap[l];
+    } else {
+        const int y = (int)(l >> log2n), z = (int)(l & (n - 1));
+        zero = y == 0 || z == 0;
+        at = lap[y] + lap[z];
+    }
+    if (zero) {
+        for (int k = 0; k < TS; ++k) t[k] = make_double2(0.0, 0.0);
+        return;
+    }
+    const double dr = 2.0 + h2 * (at - k0sq[b]), di = -h2 * eta[b];
+    auto rcp = [](double x, double y) {
+        const double den = x * x + y * y;
+        return make_double2(x / den, -y / den);
+    };
+    double2 p = rcp(dr, di), g = p;
+    t[0] = p;
+    for (int k = 1; k < kTriP - 1; ++k) {
+        p = rcp(dr - p.x, di - p.y);
+        g = cmul(g, p);
+        t[k] = p;
+    }
+    t[15] = g;
+    // reduced system: D X_s - gamma (X_{s-1} + X_{s+1}); u_1 = D, u_s = D - gamma^2 pr_{s-1}
+    const double2 D = make_double2(dr - 2.0 * p.x, di - 2.0 * p.y);
+    const double2 g2 = cmul(g, g);
+    t[16] = make_double2(0.0, 0.0);
+    double2 pr = make_double2(0.0, 0.0);
+    for (int s = 1; s < S; ++s) {
+        const double2 gp = cmul(g2, pr);
+        pr = rcp(D.x - gp.x, D.y - gp.y);
+        t[16 + s] = pr;
+    }
+}
+
+// cp.async (16 B, L2 only) global -> shared
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Tile = C adjacent lines (columns) of one plane, all n rows.  Shared-memory tile layout:
+// element (row r, column c) at e + e / (16 C), e = r C + c -- one pad slot per 16 rows, so the
+// 16-row segments a warp reads (SPW segments x CW columns per load) fall on distinct bank
+// groups for every C.
+template <int LOG2N>
+struct TriTile {
+    using G = TriGeom<LOG2N>;
+    static constexpr int TB = G::C * G::N + G::N / kTriP;   // tile buffer (double2)
+    static constexpr size_t SMEM =
+        sizeof(double2) * ((size_t)TB + 2 * (size_t)G::C * G::TSP + 3 * (size_t)G::C * G::SP + 2 * (size_t)G::C * G::CH);
+    __device__ __forceinline__ static int sidx(int r, int c) {
+        const int e = r * G::C + c;
+        return e + e / (kTriP * G::C);
+    }
+};
+
+// Line-tile addressing per layout.  CL_PLANE (2-D): tile (b, q0): lines = columns q0..q0+C-1
+// of member b, row stride n, table lines b n + q.  CL_X3 (3-D x-lines): tile (b, y, z0): lines
+// (y, z0..z0+C-1), row (= x) stride n^2, table lines (b n + y) n + z; the padding y-plane is
+// skipped (its lines are the Dirichlet zero).
+template <int LOG2N, int LAYOUT>
+struct TriLines {
+    static constexpr int N = 1 << LOG2N, C = TriGeom<LOG2N>::C, GROUPS = N / C;
+    int b, q0, yl;
+    size_t base, tline;
+    bool skip;
+    __device__ __forceinline__ static long count(const ColArgs& a) {
+        return LAYOUT == CL_X3 ? (long)a.batch * N * GROUPS : (long)a.batch * GROUPS;
+    }
+    static constexpr size_t LS = LAYOUT == CL_X3 ? (size_t)N * N : (size_t)N;
+    __device__ __forceinline__ TriLines(long t) {
+        q0 = (int)(t % GROUPS) * C;
+        if constexpr (LAYOUT == CL_X3) {
+            const long g = t / GROUPS;  // (b, y)
+            b = (int)(g >> LOG2N);
+            yl = (int)(g & (N - 1));
+            base = ((size_t)b << (3 * LOG2N)) + (size_t)yl * N + q0;
+            tline = (size_t)g * N + q0;
+            skip = yl == 0;
+        } else {
+            b = (int)(t / GROUPS);
+            yl = 0;
+            base = ((size_t)b << (2 * LOG2N)) + q0;
+            tline = (size_t)b * N + q0;
+            skip = false;
+        }
+    }
+};
+
+// Persistent CTAs over the line tiles (grid = resident CTAs).  Per tile: its n x C values and
+// pivot table were prefetched by cp.async while the previous tile was solved; the CTA copies
+// them into registers, immediately prefetches the next tile into the same buffer, solves, and
+// stores straight from registers.  Load phase mapping: warp w, lane l -> column
+// (w / WPG) CW + l mod CW, segment (w mod WPG) SPW + l / CW.  Reduced phase: thread t ->
+// column t / S, segment t mod S (a column's segments on consecutive lanes).
+template <int LOG2N, int LAYOUT>
+__global__ void __launch_bounds__(TriGeom<LOG2N>::THREADS, TriGeom<LOG2N>::THREADS >= 512 ? 1 : 2)
+tri_kernel(const ColArgs a) {
+    using G = TriGeom<LOG2N>;
+    using TT = TriTile<LOG2N>;
+    using TL = TriLines<LOG2N, LAYOUT>;
+    constexpr int N = G::N, S = G::S, C = G::C, TS = G::TS, TSP = G::TSP, SP = G::SP, LPC = G::LPC,
+                  CH = G::CH;
+    static_assert(LAYOUT == CL_PLANE || LAYOUT == CL_X3, "layout");
+    extern __shared__ double2 sm[];
+    double2* tbuf = sm;                    // [TB] tile
+    double2* tabs = tbuf + TT::TB;         // [2][C][TSP] pivot tables (double-buffered)
+    double2* red = tabs + 2 * C * TSP;     // [C][SP] h^2 r_sep + zp_1
+    double2* zl = red + C * SP;            // [C][SP] zp_15
+    double2* xs = zl + C * SP;             // [C][SP] separators (X_S = 0 at [S])
+    double2* tot = xs + C * SP;            // [C][CH] chunk maps (A, B)
+
+    const long ntiles = TL::count(a);
+    // reversed order on multi-plane launches: start on the row pass's L2-resident tail
+    const bool rev = TRI_REV && col_reversed<LAYOUT == CL_X3 ? CL_PLANE : LAYOUT>(a);
+    auto tile_at = [&](long k) { return rev ? ntiles - 1 - k : k; };
+    auto issue = [&](long k, int tb) {
+        const TL ln(tile_at(k));
+        const double2* src = a.T + ln.base;
+#pragma unroll 4
+        for (int e = threadIdx.x; e < C * N; e += G::THREADS)
+            cp_async16(tbuf + e + e / (kTriP * C), src + (size_t)(e / C) * TL::LS + (e % C));
+        const double2* ts = a.tri + ln.tline * TS;
+        double2* td = tabs + tb * C * TSP;
+        for (int k2 = threadIdx.x; k2 < C * TS; k2 += G::THREADS) cp_async16(td + (k2 / TS) * TSP + k2 % TS, ts + k2);
+    };
+
+    // L2 prefetch of a tile's rows (fire-and-forget: keeps DRAM busy TRI_PF tiles ahead without
+    // holding shared memory or registers)
+    auto prefetch = [&](long k) {
+        const TL ln(tile_at(k));
+        for (int r = threadIdx.x; r < N; r += G::THREADS)
+            prefetch_l2(a.T + ln.base + (size_t)r * TL::LS, C * sizeof(double2));
+    };
+
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int c = (w / G::WPG) * G::CW + lane % G::CW;
+    const int s = (w % G::WPG) * G::SPW + lane / G::CW;
+    const int cr = threadIdx.x / S, sr = threadIdx.x % S, ls = sr % LPC, ch = sr / LPC;
+    const double2 zero = make_double2(0.0, 0.0);
+    const double sc = a.tri_scale;
+
+    long k = blockIdx.x;
+    if (k < ntiles) issue(k, 0);
+    cp_async_commit();
+#pragma unroll 1
+    for (int j = 1; j <= TRI_PF; ++j)
+        if (k + j * gridDim.x < ntiles) prefetch(k + j * gridDim.x);
+    for (int it = 0; k < ntiles; k += gridDim.x, ++it) {
+        // member status: issued before the tile wait so its round trip overlaps it
+        const int stv = a.status ? __ldcg(&a.status[TL(tile_at(k)).b]) : (int)ST_ACTIVE;
+        cp_async_wait_all();
+        __syncthreads();
+        double2 v[kTriP];
+#pragma unroll
+        for (int i = 0; i < kTriP; ++i) v[i] = tbuf[TT::sidx(kTriP * s + i, c)];
+        __syncthreads();  // tile buffer free: prefetch the next tile under this one's solve
+        if (k + gridDim.x < ntiles) issue(k + gridDim.x, (it + 1) & 1);
+        cp_async_commit();
+        if (TRI_PF > 0 && k + (TRI_PF + 1) * (long)gridDim.x < ntiles) prefetch(k + (TRI_PF + 1) * (long)gridDim.x);
+
+        const long t = tile_at(k);
+        const TL ln(t);
+        if (ln.skip) continue;
+        if (a.status) {
+            const bool active = stv == ST_ACTIVE;  // read before finalising
+            if constexpr (LAYOUT == CL_PLANE)
+                if (a.finalize && active && ln.q0 == 0 && threadIdx.x < 32) finalize_member(a, ln.b, 1 << a.fin_lsh);
+            if (!active) continue;  // uniform per CTA
+        }
+        const double2* tab = tabs + (it & 1) * C * TSP;
+
+        // 1. zero-boundary eliminations of the interior, downwards and upwards (shared pivots)
+        const double2* pt = tab + c * TSP;
+        {
+            double2 yd = v[1], yu = v[kTriP - 1];
+#pragma unroll
+            for (int j = 1; j < kTriP - 1; ++j) {
+                const double2 p = pt[j - 1];
+                yd = cfma(p, yd, v[1 + j]);
+                yu = cfma(p, yu, v[kTriP - 1 - j]);
+            }
+            const double2 p15 = pt[kTriP - 2];
+            zl[c * SP + s] = cmul(p15, yd);
+            red[c * SP + s] = cfma(p15, yu, v[0]);
+        }
+        __syncthreads();
+
+        // 2. reduced system: forward recurrence y_s = gamma pr_{s-1} y_{s-1} + rr_s, then
+        //    X_s = gamma pr_s X_{s+1} + pr_s y_s, each as an inclusive affine-map scan
+        {
+            const double2* tr = tab + cr * TSP;
+            const double2 gam = tr[15];
+            const double2 prs = tr[16 + sr];
+            const double2 prm = sr > 0 ? tr[16 + sr - 1] : zero;
+            double2 A = cmul(gam, prm);
+            double2 B = sr > 0 ? cadd(red[cr * SP + sr], zl[cr * SP + sr - 1]) : zero;
+#pragma unroll
+            for (int d = 1; d < LPC; d <<= 1) {
+                const double ax = __shfl_up_sync(0xffffffffu, A.x, d, LPC), ay = __shfl_up_sync(0xffffffffu, A.y, d, LPC);
+                const double bx = __shfl_up_sync(0xffffffffu, B.x, d, LPC), by = __shfl_up_sync(0xffffffffu, B.y, d, LPC);
+                if (ls >= d) {
+                    B = cfma(A, make_double2(bx, by), B);
+                    A = cmul(A, make_double2(ax, ay));
+                }
+            }
+            double2 y = B;
+            if constexpr (CH > 1) {
+                if (ls == LPC - 1) {
+                    tot[(cr * CH + ch) * 2] = A;
+                    tot[(cr * CH + ch) * 2 + 1] = B;
+                }
+                __syncthreads();
+                double2 yc = zero;  // y at the end of the previous chunk
+                for (int j = 0; j < ch; ++j) yc = cfma(tot[(cr * CH + j) * 2], yc, tot[(cr * CH + j) * 2 + 1]);
+                y = cfma(A, yc, B);
+                __syncthreads();  // tot reused below
+            }
+            A = cmul(gam, prs);
+            B = cmul(prs, y);
+#pragma unroll
+            for (int d = 1; d < LPC; d <<= 1) {
+                const double ax = __shfl_down_sync(0xffffffffu, A.x, d, LPC), ay = __shfl_down_sync(0xffffffffu, A.y, d, LPC);
+                const double bx = __shfl_down_sync(0xffffffffu, B.x, d, LPC), by = __shfl_down_sync(0xffffffffu, B.y, d, LPC);
+                if (ls + d < LPC) {
+                    B = cfma(A, make_double2(bx, by), B);
+                    A = cmul(A, make_double2(ax, ay));
+                }
+            }
+            double2 X = B;
+            if constexpr (CH > 1) {
+                if (ls == 0) {
+                    tot[(cr * CH + ch) * 2] = A;
+                    tot[(cr * CH + ch) * 2 + 1] = B;
+                }
+                __syncthreads();
+                double2 xc = zero;  // X at the start of the next chunk
+                for (int j = CH - 1; j > ch; --j) xc = cfma(tot[(cr * CH + j) * 2], xc, tot[(cr * CH + j) * 2 + 1]);
+                X = cfma(A, xc, B);
+            }
+            xs[cr * SP + sr] = X;
+            if (sr == S - 1) xs[cr * SP + S] = zero;
+        }
+        __syncthreads();
+
+        // 3. elimination with the separators as boundary values, back substitution, store
+        const double2 xl = xs[c * SP + s], xr = xs[c * SP + s + 1];
+        v[1] = cadd(v[1], xl);
+#pragma unroll
+        for (int i = 2; i < kTriP; ++i) v[i] = cfma(pt[i - 2], v[i - 1], v[i]);
+        v[kTriP - 1] = cmul(pt[kTriP - 2], cadd(v[kTriP - 1], xr));
+#pragma unroll
+        for (int i = kTriP - 2; i >= 1; --i) v[i] = cmul(pt[i - 1], cadd(v[i], v[i + 1]));
+        v[0] = xl;
+        // Dirichlet zero line (q = 0; 3-D: z = 0): its table is zero, store zeros explicitly
+        const bool zc = ln.q0 + c == 0;
+        double2* col = a.T + ln.base + (size_t)(kTriP * s) * TL::LS + c;
+#pragma unroll
+        for (int i = 0; i < kTriP; ++i) col[(size_t)i * TL::LS] = zc ? zero : cscale(v[i], sc);
+    }
+    cp_async_wait_all();
+}
+
+}  // namespace bs

@@ -1,0 +1,108 @@
+"""Green column pass as a tridiagonal x-solve (csrc/tri_kernels.cuh) against the transform
+route (BP_COL_DST=1: forward x-DST, x 1/lambda, inverse x-DST -- proj/src/symbol.cpp:19-39)
+and against the CPU oracle.
+
+Both routes apply the same operator G = L_eta^{-1} (the x factor of the Dirichlet five-point
+symbol, symbol.cpp:69-80, is the spectrum of the three-point second difference); they differ
+only in rounding.  Tolerances: one operator application 1e-13 relative L2 (OP_TOL of
+test_gpu_parity.py), iterates 1e-10 (north_star)."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2603_18527_b200 as bs
+from oracle import MAP_POINTWISE, OracleProblem
+
+pytestmark = pytest.mark.gpu
+
+OP_TOL = 1e-13
+FIELD_TOL = 1e-10
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def handle(k2, k0, eta, dst):
+    old = os.environ.get("BP_COL_DST")
+    os.environ["BP_COL_DST"] = "1" if dst else "0"
+    try:
+        return bs.HelmholtzDirichlet(k2, k0, eta)
+    finally:
+        if old is None:
+            del os.environ["BP_COL_DST"]
+        else:
+            os.environ["BP_COL_DST"] = old
+
+
+@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024, 2048, 4096])
+def test_green_tri_matches_transform_route(gpu, n):
+    batch = 2 if n <= 1024 else 1
+    k2, f, k0, eta = bs.make_instances(bs.InstanceSpec(n=n, ppw=8.0, contrast=0.5, seed=n), 0, batch)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(k2.shape) + 1j * rng.standard_normal(k2.shape)
+    with handle(k2, k0, eta, True) as pd, handle(k2, k0, eta, False) as pt:
+        gd, gt = pd.apply_G(x), pt.apply_G(x)
+    for b in range(batch):
+        assert rel(gt[b], gd[b]) < OP_TOL, (n, b, rel(gt[b], gd[b]))
+
+
+@pytest.mark.parametrize("n", [64, 256])
+def test_green_tri_matches_oracle(gpu, n):
+    k2, f, k0, eta = bs.make_instances(bs.InstanceSpec(n=n, ppw=10.0, contrast=0.3, seed=7), 0, 2)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(k2.shape) + 1j * rng.standard_normal(k2.shape)
+    with handle(k2, k0, eta, False) as p:
+        g = p.apply_G(x)
+    for b in range(2):
+        assert rel(g[b], OracleProblem(k2[b], k0[b], eta[b]).apply_G(x[b])) < OP_TOL
+
+
+@pytest.mark.parametrize("eta_scale", [1e-4, 1e-2, 1.0, 1e3])
+def test_green_tri_weak_and_strong_damping(gpu, eta_scale):
+    """d = 2 + h^2 (a_q - k0^2 - i eta) close to the real segment [-2, 2] (weak damping: slowly
+    converging pivots, long-range coupling across segments) and far from it (strong damping:
+    gamma -> 0, decoupled segments)."""
+    n = 512
+    k2, f, k0, eta = bs.make_instances(bs.InstanceSpec(n=n, ppw=8.0, contrast=0.5, seed=11), 0, 1)
+    eta = eta * eta_scale
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(k2.shape) + 1j * rng.standard_normal(k2.shape)
+    try:
+        pd = handle(k2, k0, eta, True)
+    except RuntimeError:
+        pytest.skip("symbol guard rejects this eta")
+    with pd, handle(k2, k0, eta, False) as pt:
+        gd, gt = pd.apply_G(x), pt.apply_G(x)
+    # the transform route's own rounding grows with the conditioning ~ max|lambda| / eta
+    assert rel(gt[0], gd[0]) < max(OP_TOL, 1e-15 / min(eta_scale, 1.0)), rel(gt[0], gd[0])
+
+
+def test_run_tri_iterates_match_transform_route(gpu):
+    """Per-iterate u^m of the pointwise-map sweep (c1 construction at n = 256) through both
+    column routes, and against the oracle."""
+    n, sweeps = 256, 24
+    k2, f, k0, eta = bs.make_instances(bs.InstanceSpec(n=n, ppw=8.0, contrast=0.5, seed=2), 0, 2)
+    cfg = bs.IterationConfig(rtol=1e-30, max_iters=sweeps)
+    with handle(k2, k0, eta, True) as pd, handle(k2, k0, eta, False) as pt:
+        sd = bs.run(pd, bs.PointwiseMap(), f, cfg, n_snap=sweeps + 1).snapshots
+        st = bs.run(pt, bs.PointwiseMap(), f, cfg, n_snap=sweeps + 1).snapshots
+    for m in range(1, sweeps + 1):
+        for b in range(2):
+            assert rel(st[m][b], sd[m][b]) < 1e-12, (m, b)
+    ref = OracleProblem(k2[0], k0[0], eta[0]).run(f[0], map_kind=MAP_POINTWISE, rtol=1e-30,
+                                                  max_iters=sweeps, n_snap=sweeps + 1)
+    for m in range(1, sweeps + 1):
+        assert rel(st[m][0], ref.snapshots[m]) < FIELD_TOL, m
+
+
+def test_set_medium_rebuilds_tri_tables(gpu):
+    n = 128
+    k2a, _, k0a, etaa = bs.make_instances(bs.InstanceSpec(n=n, ppw=8.0, contrast=0.5, seed=1), 0, 2)
+    k2b, _, k0b, etab = bs.make_instances(bs.InstanceSpec(n=n, ppw=6.0, contrast=0.3, seed=9), 0, 2)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(k2a.shape) + 1j * rng.standard_normal(k2a.shape)
+    with handle(k2a, k0a, etaa, False) as p, handle(k2b, k0b, etab, False) as q:
+        p.set_medium(k2b, k0b, etab)
+        assert np.array_equal(p.apply_G(x), q.apply_G(x))
