@@ -1,11 +1,12 @@
 """Condense gpurun_out/ ncu artefacts into the tracked profiles/ summaries.
 
-    python tools/make_profile_summary.py <round-tag> <launches.csv> <full.ncu-rep>
+    python tools/make_profile_summary.py <round-tag> <config> <launches.csv | -> <full.ncu-rep>
 
 Writes profiles/<tag>_launches.md (per-kernel launch counts and device-time shares of the
 `ncu --metrics gpu__time_duration.sum` pass over bench.py), profiles/<tag>_ncu_full.md (key
-`--set full` metrics of the sweep kernels) and profiles/ncu_summary.json (dram bytes per launch
-of the row / column sweep kernels, read by bench.py for roofline.traffic)."""
+`--set full` metrics of the sweep kernels) and updates profiles/ncu_summary.json: per config,
+dram bytes per launch of the sweep's row kernel ("row") and column kernel ("col"), read by
+bench.py for roofline.traffic."""
 import collections
 import csv
 import io
@@ -15,7 +16,7 @@ import re
 import subprocess
 import sys
 
-tag, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3]
+tag, config, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 out_dir = os.path.join(ROOT, "profiles")
 os.makedirs(out_dir, exist_ok=True)
@@ -27,7 +28,7 @@ def short(name):
 
 
 # ---- launch list
-rows = [r for r in csv.reader(open(launches)) if len(r) > 14 and r[0].isdigit()]
+rows = [] if launches == "-" else [r for r in csv.reader(open(launches)) if len(r) > 14 and r[0].isdigit()]
 agg = collections.OrderedDict()
 for r in rows:
     k = short(r[4])
@@ -35,8 +36,9 @@ for r in rows:
     c, s = agg.get(k, (0, 0.0))
     agg[k] = (c + 1, s + t)
 total = sum(s for _, s in agg.values())
-with open(os.path.join(out_dir, f"{tag}_launches.md"), "w") as fh:
-    fh.write(f"# {tag}: kernel launch list of `python bench.py --no-cpu` under\n"
+for _ in [0] if rows else []:
+  with open(os.path.join(out_dir, f"{tag}_launches.md"), "w") as fh:
+    fh.write(f"# {tag} ({config}): kernel launch list of `python bench.py --no-cpu` under\n"
              f"`ncu --metrics gpu__time_duration.sum --clock-control none -c 3000`\n\n"
              f"Cold-cache, serialised per-launch times: compare SHARES, not absolutes.\n"
              f"{len(rows)} launches captured.\n\n| kernel | launches | total ms | mean us | share |\n|---|---|---|---|---|\n")
@@ -62,7 +64,7 @@ WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "DRAM r
         ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier / issue")]
 summary = {}
 with open(os.path.join(out_dir, f"{tag}_ncu_full.md"), "w") as fh:
-    fh.write(f"# {tag}: `ncu --set full` of the sweep kernels (tools/profile_sweep.py, c1: 64 x 511^2)\n\n")
+    fh.write(f"# {tag}: `ncu --set full` of the {config} sweep kernels (tools/profile_sweep.py --config {config})\n\n")
     for r in raw[2:]:
         name = r[hdr.index("Kernel Name")]
         fh.write(f"## `{name}`\n\n| metric | value |\n|---|---|\n")
@@ -77,14 +79,24 @@ with open(os.path.join(out_dir, f"{tag}_ncu_full.md"), "w") as fh:
         def to_bytes(v):
             x, u = float(v[0].replace(",", "")), v[1]
             return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-        if "row_kernel" in name and ", 3," in name:
-            summary["row_kernel"] = {"kernel": name, "dram_bytes_per_launch":
-                                     to_bytes(vals["dram__bytes_read.sum"]) + to_bytes(vals["dram__bytes_write.sum"]),
-                                     "duration": " ".join(vals["gpu__time_duration.sum"])}
-        if "col_kernel" in name and ", 1," in name:
-            summary["col_kernel"] = {"kernel": name, "dram_bytes_per_launch":
-                                     to_bytes(vals["dram__bytes_read.sum"]) + to_bytes(vals["dram__bytes_write.sum"]),
-                                     "duration": " ".join(vals["gpu__time_duration.sum"])}
-summary["source"] = f"profiles/{tag}_ncu_full.md (ncu --set full, 64 members x 511^2 per launch)"
-json.dump(summary, open(os.path.join(out_dir, "ncu_summary.json"), "w"), indent=1)
+        entry = {"kernel": name, "dram_bytes_per_launch":
+                 to_bytes(vals["dram__bytes_read.sum"]) + to_bytes(vals["dram__bytes_write.sum"]),
+                 "duration": " ".join(vals["gpu__time_duration.sum"])}
+        # the sweep's row pass (R_SWEEP, or the c4 RC_A/RC_B pair) and its column pass
+        if re.search(r"row_kernel<\d+, 3,|crow_kernel<\d+, 2,|prow_kernel", name):
+            summary["row"] = entry
+        if re.search(r"crow_kernel<\d+, 3,", name):
+            summary["row_b"] = entry
+        if re.search(r"tri_kernel|col_kernel<\d+, 1,|ccol_kernel<\d+, 1,", name):
+            summary.setdefault("col", entry)
+summary["source"] = f"profiles/{tag}_ncu_full.md (ncu --set full --clock-control none, tools/profile_sweep.py --config {config})"
+path = os.path.join(out_dir, "ncu_summary.json")
+try:
+    doc = json.load(open(path))
+    if "row_kernel" in doc:  # r01 layout (c1 only)
+        doc = {}
+except Exception:
+    doc = {}
+doc[config] = summary
+json.dump(doc, open(path, "w"), indent=1)
 print(json.dumps(summary, indent=1))
