@@ -267,13 +267,14 @@ def run_reference_arm(args):
     return 0
 
 
-def load_traffic():
-    """dram bytes per row-kernel launch from the committed ncu summary (profiles/), if any."""
+def load_traffic(config):
+    """dram bytes per launch of the config's dominant (row) kernel from the committed ncu
+    summary (profiles/ncu_summary.json, tools/make_profile_summary.py), if captured."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
-            d = json.load(fh)
-        return d["row_kernel"]["dram_bytes_per_launch"], os.path.relpath(path, ROOT)
+            d = json.load(fh)[config]
+        return d["row"]["dram_bytes_per_launch"], f"{os.path.relpath(path, ROOT)} ({d['source']})"
     except Exception:
         return None, None
 
@@ -418,11 +419,10 @@ def run_ours(args):
     col_avg = col_ms / full_launches
     pts_per_launch = per * pts
     peak, peak_src = measured_peak()
-    # (BP_MIXED=1: rows and columns share launches, all time is charged to row_ms)
     row_gbs = row_b * pts_per_launch / (row_avg * 1e-3) / 1e9 if row_avg > 0 else 0.0
     col_gbs = col_b * pts_per_launch / (col_avg * 1e-3) / 1e9 if col_avg > 0 else 0.0
     sweep_gbs = sweep_b * pts_per_launch / ((row_avg + col_avg) * 1e-3) / 1e9
-    traffic, traffic_src = load_traffic() if args.config == "c1" else (None, None)
+    traffic, traffic_src = load_traffic(args.config)
 
     # ------------------------------------------------------------------ e2e through host buffers
     def pinned(a):
@@ -602,6 +602,14 @@ def run_slab_bench(args, bs, rank, local_rank, world, barrier, max_over_ranks):
     value_e2e = sweeps_e2e * pts / (elapsed_e2e * 1e-3) / 1e9
     peak, peak_src = measured_peak()
     per_rank_gbs = bpp * pts / world * sweeps / (elapsed_ms * 1e-3) / 1e9
+    # NVLink traffic per rank and sweep: the two transposes move the rank's
+    # (P-1)/P off-rank share of its n^dim/P points, 16 B each way, plus the u halo (one row /
+    # x-plane from each neighbour); the 1-element fences / 2-double all-reduce are negligible
+    halo_elems = nd ** (dim - 1)
+    nbr = (1 if rank in (0, world - 1) else 2) if world > 1 else 0
+    nvl_bytes = (2 * 16 * (pts / world) * (world - 1) / world + 16 * halo_elems * nbr) if world > 1 else 0.0
+    nvl_gbs = nvl_bytes * sweeps / (elapsed_ms * 1e-3) / 1e9
+    nvl_peak = 900.0  # NVLink 5, GB/s per direction per GPU (B200 HGX, NVSwitch)
     part.close()
     if rank == 0:
         fb = int(f[0].nbytes)
@@ -615,6 +623,7 @@ def run_slab_bench(args, bs, rank, local_rank, world, barrier, max_over_ranks):
                        "grid": "x".join([str(nd)] * dim) + f" (n={nd + 1})", "global_batch": 1,
                        ("rows_per_gpu" if dim == 2 else "x_planes_per_gpu"): (nd + 1) // world,
                        "sweeps_per_step": args.sweeps,
+                       "graph": "sweep loop captured as a CUDA graph of 16 sweeps (kernels + NCCL collectives)",
                        "parallelism": (f"x-slab x{world}: halo p2p + all-reduce + exchange fused into the kernels' "
                                        "stores over symmetric (NVLink peer) memory + 2 fences per sweep" if args.fused else
                                        f"x-slab x{world}: halo p2p + all-reduce + 2 all-to-all per sweep (NCCL)"),
@@ -624,7 +633,11 @@ def run_slab_bench(args, bs, rank, local_rank, world, barrier, max_over_ranks):
             "roofline": {"bound": "hbm", "kernel": "whole sweep per rank (row + column + collectives)",
                          "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
                          "frac": per_rank_gbs / peak, "traffic": None, "peak_source": peak_src,
-                         "bytes_per_pt": bpp},
+                         "bytes_per_pt": bpp,
+                         "nvlink": {"bytes_per_sweep_per_rank": nvl_bytes, "achieved": nvl_gbs,
+                                    "peak": nvl_peak, "unit": "GB/s", "frac": nvl_gbs / nvl_peak,
+                                    "peak_source": "nominal NVLink 5 per-direction bandwidth (900 GB/s); "
+                                                   "0 at N=1 (no off-rank traffic)"}},
             "cpu_baseline": None,
             # per sweep and rank: row + column + finalize (3-D: + two y-line launches)
             "gpu_launches": int(sweeps * (3 if dim == 2 else 5) * world),

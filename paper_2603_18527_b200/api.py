@@ -143,9 +143,12 @@ class HelmholtzDirichlet:
     BC = BC_DIRICHLET
     DTYPE = np.complex128
 
-    def __init__(self, k2, k0, eta, lx: float = 1.0, device: int = 0, dim: int = 2):
+    def __init__(self, k2, k0, eta, lx: float = 1.0, device: int = 0, dim: int = 2,
+                 ly: float | None = None):
         """k2: (batch, nx, ny) -- or (nx, ny) for one member; dim=3: (batch, n, n, n) or
-        (n, n, n), the seven-point 3-D extension (config c3)."""
+        (n, n, n), the seven-point 3-D extension (config c3).  Grids with nx + 1 = ny + 1 = 2^k
+        and lx == ly run the fused power-of-two kernels; any other 2-D Dirichlet shape runs the
+        any-shape path (generic_kernels.cuh: radix-2 / Bluestein line transforms)."""
         k2 = np.asarray(k2, dtype=np.complex128)
         self.dim = dim
         self.single = k2.ndim == dim
@@ -156,6 +159,7 @@ class HelmholtzDirichlet:
         k0 = np.ascontiguousarray(np.broadcast_to(np.asarray(k0, np.float64), (self.batch,)))
         eta = np.ascontiguousarray(np.broadcast_to(np.asarray(eta, np.float64), (self.batch,)))
         self.k0, self.eta, self.lx, self.device = k0, eta, lx, device
+        self.ly = lx if ly is None else ly
         self.k2 = k2  # host copy of the media (save_problem)
         h = C.c_void_p()
         self._lib = N.lib()
@@ -164,7 +168,7 @@ class HelmholtzDirichlet:
             rc = self._lib.bp_problem_create3d(C.byref(g3), self.batch, _ptr(k2), _ptr(k0),
                                                _ptr(eta), device, C.byref(h))
         else:
-            g = N.Grid(self.nx, self.ny, lx, lx, self.BC)
+            g = N.Grid(self.nx, self.ny, lx, self.ly, self.BC)
             rc = self._lib.bp_problem_create(C.byref(g), self.batch, _ptr(k2), _ptr(k0), _ptr(eta),
                                              device, C.byref(h))
         _check(rc)

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -16,6 +17,7 @@
 
 #include "bornsweep.h"
 #include "sweep_launch.cuh"
+#include "generic_kernels.cuh"
 
 using namespace bs;
 
@@ -37,8 +39,8 @@ int set_err(int code, const std::string& msg) {
 
 constexpr int kGraphSweeps = 16;
 constexpr double kPi = 3.14159265358979323846;
-// sinp table: 2 sin(pi j/n) for the table-driven engine (BS_TW_TABLE), sin(pi j/n) otherwise
-constexpr double kSinScale = BS_TW_TABLE ? 2.0 : 1.0;
+// sinp table: sin(pi j/n)
+constexpr double kSinScale = 1.0;
 constexpr double kSymbolDivGuard = 1e-14;  // proj/include/bp/symbol.hpp:24
 
 // ------------------------------------------------------------------ small kernels
@@ -230,19 +232,9 @@ cudaError_t launch_periodic(int log2n, bool row, int mode, const PerArgs& a, cud
     BS_SIZE_CASES(launch_periodic_L, row, mode, a, s, prep)
 }
 
-cudaError_t launch_transposed(int log2n, bool row, int mode, const RowArgs& a, const ColArgs& c,
-                              cudaStream_t s, bool prep = false) {
-    BS_SIZE_CASES(launch_transposed_L, row, mode, a, c, s, prep)
-}
-
 cudaError_t launch_cdr(int log2n, bool row, int mode, const CdrArgs& a, cudaStream_t s,
                        bool prep = false) {
     BS_SIZE_CASES(launch_cdr_L, row, mode, a, s, prep)
-}
-
-cudaError_t launch_mixed(int log2n, const RowArgs& ra, const ColArgs& ca, cudaStream_t s,
-                         bool prep = false) {
-    BS_SIZE_CASES(launch_mixed_L, ra, ca, s, prep)
 }
 
 cudaError_t launch_tri(int log2n, int layout, const ColArgs& a, cudaStream_t s, bool prep = false) {
@@ -261,13 +253,6 @@ cudaError_t prepare_kernels(int log2n, int dim) {
     ColArgs c{};
     PerArgs pa{};
     cudaError_t e = cudaSuccess;
-    if (dim == 2 && log2n <= 9) {
-        for (int mode : {R_FWD_BORN, R_SWEEP, R_OPT_B, R_RETA_A, R_FD_A, R_FD_B})
-            if (cudaError_t r = launch_transposed(log2n, true, mode, a, c, nullptr, true)) e = r;
-        for (int mode : {C_GREEN, C_FD})
-            if (cudaError_t r = launch_transposed(log2n, false, mode, a, c, nullptr, true)) e = r;
-    }
-    if (dim == 2) launch_mixed(log2n, a, c, nullptr, true);  // sizes without a mixed kernel: ignored
     if (log2n >= 6)
         if (cudaError_t r = launch_tri(log2n, dim == 3 ? CL_X3 : CL_PLANE, c, nullptr, true)) e = r;
     if (dim == 2) {
@@ -339,12 +324,18 @@ int grid_for(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 16)
 
 }  // namespace
 
+// Line-transform plan of the any-shape path (generic_kernels.cuh): DFT length n, FFT length L
+// (n itself when a power of two, else the Bluestein convolution length), device tables.
+struct GLinePlan {
+    int n = 0, L = 0, lg = 0;
+    double2 *chirp = nullptr, *filt = nullptr, *tw = nullptr;
+};
+
 // ------------------------------------------------------------------ handle
 struct bp_problem {
     bp_grid grid{};
     int batch = 0, device = 0, log2n = 0, n = 0, dim = 2;
     bool periodic = false;   // the reference's own HelmholtzProblem (FFT basis, no padding)
-    bool transposed = false; // 2-D Dirichlet n <= 512: transposed row -> column handoff (TT)
     bool cdr = false;        // config c4: real fields, Neumann, DCT-II, upwind V
     double *bx = nullptr, *by = nullptr, *sigma = nullptr, *sigma0 = nullptr, *lapn = nullptr,
            *rnorm2 = nullptr;
@@ -363,7 +354,6 @@ struct bp_problem {
     int slab_max_iters = 1000;
     double slab_rtol = 1e-6;
     bool own_stream = true;
-    double2* TT = nullptr;
     double* xi2 = nullptr;   // periodic: xi_j^2, FFT order
     size_t field = 0;   // padded elements per member (n^dim)
     size_t alloc = 0;   // padded elements per buffer (batch*n^dim + n^(dim-1): zero halo)
@@ -373,6 +363,12 @@ struct bp_problem {
     // (member, line), rebuilt whenever k0 / eta change; null = transform route
     double2* tri = nullptr;
     double tri_scale = 0;
+    // any-shape 2-D Dirichlet handle (nx, ny not of the form 2^k - 1, or nx != ny): dense nx x ny
+    // layout, line transforms by radix-2 / Bluestein (generic_kernels.cuh)
+    bool generic = false;
+    int gnx = 0, gny = 0;
+    GLinePlan gplan_x, gplan_y;
+    double *gax = nullptr, *gay = nullptr, *gpart = nullptr;
     cudaStream_t stream = nullptr;
     // device constants
     double2* k2 = nullptr;
@@ -398,7 +394,6 @@ struct bp_problem {
     // graph cache
     cudaGraphExec_t graph = nullptr;
     int graph_map_kind = -1;
-    bool graph_mixed = false;
     int graph_metric = -1;
     int graph_format = -1;
     double2 graph_gamma{};
@@ -462,7 +457,6 @@ RowArgs row_args(const bp_problem* p) {
     a.T = p->T;
     a.u0 = p->u0;
     a.u1 = p->u1;
-    a.TT = p->TT;
     a.X = p->x;
     a.tw = p->tw;
     a.sinp = p->sinp;
@@ -482,51 +476,11 @@ ColArgs col_args(const bp_problem* p) {
     c.fd = p->fd;
     c.tri = p->tri;
     c.tri_scale = p->tri_scale;
-    c.TT = p->TT;
+
     c.T = p->T;
     c.tw = p->tw;
     c.sinp = p->sinp;
     c.status = nullptr;
-    return c;
-}
-
-// Arguments restricted to members [b0, b0 + nb) of the batch (the half-batches of the mixed
-// pipeline): every per-member array is offset, n_active stays shared.
-RowArgs row_args_range(const RowArgs& a0, const bp_problem* p, int b0, int nb) {
-    RowArgs a = a0;
-    const size_t fo = (size_t)b0 * p->field;
-    a.batch = nb;
-    a.k0sq += b0;
-    a.eta += b0;
-    a.k2 += fo;
-    a.f += fo;
-    a.T += fo;
-    a.u0 += fo;
-    a.u1 += fo;
-    if (a.X) a.X += fo;
-    Control& c = a.ctl;
-    c.status += b0;
-    c.sweep += b0;
-    c.iters += b0;
-    c.term += b0;
-    c.result_buf += b0;
-    c.counter += b0;
-    c.partial += ((size_t)b0 << (p->log2n * (p->dim - 1))) * kPartStride;
-    c.gamma += b0;
-    c.fnorm_l2 += b0;
-    c.fnorm_reta += b0;
-    c.trace_l2 += (size_t)b0 * c.trace_stride;
-    c.trace_reta += (size_t)b0 * c.trace_stride;
-    return a;
-}
-
-ColArgs col_args_range(const ColArgs& c0, const bp_problem* p, int b0, int nb) {
-    ColArgs c = c0;
-    c.batch = nb;
-    c.k0sq += b0;
-    c.eta += b0;
-    c.T += (size_t)b0 * p->field;
-    if (c.status) c.status += b0;
     return c;
 }
 
@@ -568,7 +522,7 @@ int upload(bp_problem* p, const double* host, double2* dst, bool host_ptr) {
         CU(cudaMemcpyAsync(p->dense, host, bytes, cudaMemcpyHostToDevice, p->stream));
         src = p->dense;
     }
-    if (p->periodic) {  // no padding: the dense layout is the device layout
+    if (p->periodic || p->generic) {  // no padding: the dense layout is the device layout
         CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, p->stream));
         return BP_OK;
     }
@@ -584,6 +538,9 @@ int download(bp_problem* p, const double2* p0, const double2* p1, const int* sel
     double2* dst = host_ptr ? p->dense : reinterpret_cast<double2*>(host);
     if (p->periodic) {  // select must be null: the periodic result is produced into p0
         CU(cudaMemcpyAsync(dst, p0, sizeof(double2) * nd * p->batch, cudaMemcpyDeviceToDevice, p->stream));
+    } else if (p->generic) {
+        gen_select_kernel<<<grid_for(nd * p->batch), 256, 0, p->stream>>>(p0, p1 ? p1 : p0, select, dst,
+                                                                          (long)nd, p->batch);
     } else {
         unpack_kernel<<<grid_for(nd * p->batch), 256, 0, p->stream>>>(p0, p1, select, dst, p->batch,
                                                                        p->log2n, p->dim);
@@ -661,11 +618,173 @@ int green(bp_problem* p, const double2* in, double2* out, const double2* sub, bo
 int build_tri(bp_problem* p) {
     if (!p->tri) return BP_OK;
     const double h = p->grid.lx / p->n;
+    if (p->cdr) {
+        const long cols = (long)p->batch << p->log2n;
+        tri_setup_neumann_kernel<<<(int)((cols + 127) / 128), 128, 0, p->stream>>>(p->lapn, p->sigma0, h * h,
+                                                                                 p->batch, p->log2n, p->tri);
+        CU(cudaGetLastError());
+        return BP_OK;
+    }
     const long lines = (long)p->batch << ((p->dim - 1) * p->log2n);
     tri_setup_kernel<<<(int)((lines + 127) / 128), 128, 0, p->stream>>>(p->lap, p->k0sq, p->eta, h * h, p->batch,
                                                                        p->log2n, p->dim, p->tri);
     CU(cudaGetLastError());
     return BP_OK;
+}
+
+// ------------------------------------------------------------------ any-shape path (host)
+// In-place iterative radix-2 FFT on the host (plan setup only: the Bluestein filter spectrum).
+void host_fft(std::vector<std::complex<double>>& a) {
+    const size_t L = a.size();
+    for (size_t i = 1, j = 0; i < L; ++i) {
+        size_t bit = L >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    for (size_t len = 2; len <= L; len <<= 1) {
+        for (size_t i = 0; i < L; i += len)
+            for (size_t k = 0; k < len / 2; ++k) {
+                const std::complex<double> w = std::polar(1.0, -2.0 * kPi * (double)k / (double)len);
+                const std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w;
+                a[i + k] = u + v;
+                a[i + k + len / 2] = u - v;
+            }
+    }
+}
+
+int make_gplan(int n, GLinePlan& pl) {
+    pl.n = n;
+    int L = 1;
+    const bool pow2 = (n & (n - 1)) == 0;
+    while (L < (pow2 ? n : 2 * n - 1)) L <<= 1;
+    if (L > 8192) return set_err(BP_ENOTSUP, "any-shape path: line transforms up to 4096 points");
+    pl.L = L;
+    pl.lg = 0;
+    while ((1 << pl.lg) < L) ++pl.lg;
+    std::vector<double2> tw(std::max(1, L / 2));
+    for (int k = 0; k < L / 2; ++k) tw[k] = make_double2(std::cos(2.0 * kPi * k / L), -std::sin(2.0 * kPi * k / L));
+    CU(cudaMalloc(&pl.tw, sizeof(double2) * tw.size()));
+    CU(cudaMemcpy(pl.tw, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
+    if (L != n) {
+        // c_j = exp(-i pi j^2 / n), the exponent reduced mod 2n in integers (exact angles)
+        std::vector<double2> ch(n);
+        std::vector<std::complex<double>> b(L, 0.0);
+        for (int j = 0; j < n; ++j) {
+            const double ang = kPi * (double)(((long long)j * j) % (2LL * n)) / n;
+            ch[j] = make_double2(std::cos(ang), -std::sin(ang));
+            b[j] = std::complex<double>(std::cos(ang), std::sin(ang));  // b_j = conj(c_j)
+            if (j) b[L - j] = b[j];
+        }
+        host_fft(b);
+        std::vector<double2> fl(L);
+        for (int k = 0; k < L; ++k) fl[k] = make_double2(b[k].real(), b[k].imag());
+        CU(cudaMalloc(&pl.chirp, sizeof(double2) * n));
+        CU(cudaMalloc(&pl.filt, sizeof(double2) * L));
+        CU(cudaMemcpy(pl.chirp, ch.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(pl.filt, fl.data(), sizeof(double2) * L, cudaMemcpyHostToDevice));
+    }
+    return BP_OK;
+}
+
+void free_gplan(GLinePlan& pl) {
+    for (double2* q : {pl.chirp, pl.filt, pl.tw})
+        if (q) cudaFree(q);
+    pl = GLinePlan{};
+}
+
+GenArgs gen_args(const bp_problem* p) {
+    GenArgs g{};
+    g.batch = p->batch;
+    g.nx = p->gnx;
+    g.ny = p->gny;
+    g.inv_h2 = p->inv_h2;
+    g.k2 = p->k2;
+    g.k0sq = p->k0sq;
+    g.eta = p->eta;
+    g.ax = p->gax;
+    g.ay = p->gay;
+    g.gscale = 4.0 / ((double)(p->gnx + 1) * (p->gny + 1));
+    return g;
+}
+
+// DST-I (mode GL_DST) of every y-line (axis 0) or x-line (axis 1) of the dense batch
+int gen_lines(bp_problem* p, int axis, const double2* in, double2* out, double scale) {
+    const GLinePlan& pl = axis == 0 ? p->gplan_y : p->gplan_x;
+    GLineArgs a{};
+    a.in = in;
+    a.out = out;
+    a.n = pl.n;
+    a.L = pl.L;
+    a.lgL = pl.lg;
+    const long per = (long)p->gnx * p->gny;
+    if (axis == 0) {
+        a.lines = (long)p->batch * p->gnx;
+        a.lpm = p->gnx;
+        a.lstride = p->gny;
+        a.estride = 1;
+    } else {
+        a.lines = (long)p->batch * p->gny;
+        a.lpm = p->gny;
+        a.lstride = 1;
+        a.estride = p->gny;
+    }
+    a.mstride = per;
+    a.chirp = pl.chirp;
+    a.filt = pl.filt;
+    a.tw = pl.tw;
+    a.scale = scale;
+    const int smem = (int)(sizeof(double2) * (pl.n + std::max(pl.L, pl.n / 2 + 256)));
+    static bool attr = [] {
+        cudaFuncSetAttribute(gline_kernel<GL_DST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        return true;
+    }();
+    (void)attr;
+    gline_kernel<GL_DST><<<(unsigned)a.lines, 256, smem, p->stream>>>(a);
+    CU(cudaGetLastError());
+    return BP_OK;
+}
+
+// 2-D DST-I (plain sine sums, transforms.hpp:18-20) of a dense batch, x scale
+int gen_dst2(bp_problem* p, const double2* in, double2* out, double scale) {
+    if (int rc = gen_lines(p, 0, in, out, 1.0)) return rc;
+    return gen_lines(p, 1, out, out, scale);
+}
+
+// G (divide) / L_ref (multiply): S^-1 diag(lambda^-+1) S with S^-1 = 4/((nx+1)(ny+1)) S
+int gen_spectral(bp_problem* p, bool divide, const double2* in, double2* out) {
+    const GenArgs g = gen_args(p);
+    if (int rc = gen_dst2(p, in, p->T, 1.0)) return rc;
+    gen_symbol_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(g, divide ? 1 : 0, g.gscale, p->T);
+    CU(cudaGetLastError());
+    return gen_dst2(p, p->T, out, 1.0);
+}
+
+// Problem ctor guard (symbol.cpp:102-111) over the any-shape symbol
+int check_symbol_generic(const std::vector<double>& ax, const std::vector<double>& ay, int batch,
+                         const double* k0, const double* eta) {
+    for (int b = 0; b < batch; ++b) {
+        const double k0sq = k0[b] * k0[b];
+        double mn = INFINITY, mx = 0.0;
+        for (double a : ax)
+            for (double c : ay) {
+                const double v = std::hypot((a + c) - k0sq, -eta[b]);
+                mn = std::min(mn, v);
+                mx = std::max(mx, v);
+            }
+        if (mn < kSymbolDivGuard * mx)
+            return set_err(BP_ERUNTIME, "symbol has a (near-)zero entry; reference operator not invertible");
+    }
+    return BP_OK;
+}
+
+std::vector<double> gen_lap(int n, double h) {  // (4/h^2) sin^2((p+1) pi / (2(n+1))), p < n
+    std::vector<double> a(n);
+    for (int p2 = 0; p2 < n; ++p2) {
+        const double sx = std::sin((p2 + 1) * kPi / (2.0 * (n + 1)));
+        a[p2] = 4.0 / (h * h) * sx * sx;
+    }
+    return a;
 }
 
 int ensure_trace(bp_problem* p, int max_iters) {
@@ -740,62 +859,13 @@ int sweep_once(bp_problem* p, const SweepPlan& plan, const RowArgs& a, const Col
     if (ev) CU(cudaEventRecord(ev[0], p->stream));
     for (int k = 0; k < plan.n; ++k) {
         const int md = plan.mode[k];
-        if (p->transposed) {
-            // forward-writing row modes hand the column pass a transposed intermediate
-            const bool fwd = plan.row[k] && md != R_OPT_A && md != R_RETA_C;
-            if (!plan.row[k] || fwd) {
-                ColArgs cc = c;
-                cc.scale = p->green_scale;
-                CU(launch_transposed(p->log2n, plan.row[k], md, a, cc, p->stream));
-            } else {
-                CU(launch_row(p->log2n, p->dim, md, a, p->stream));
-            }
-        } else if (plan.row[k]) {
+        if (plan.row[k]) {
             CU(launch_row(p->log2n, p->dim, md, a, p->stream));
         } else if (int rc = col_stage_checked(p, c, md, p->green_scale)) {
             return rc;
         }
         if (ev) CU(cudaEventRecord(ev[k + 1], p->stream));
     }
-    return BP_OK;
-}
-
-// Mixed pipeline (scalar / pointwise maps, 2-D, batch >= 2): the batch is split into halves A
-// and B; one "pipelined sweep" is two mixed launches, [rows(A) + columns(B)] then
-// [columns(A) + rows(B)] (mixed_kernel), so every launch co-runs an HBM-bound row pass with an
-// FP64-bound column pass.  B runs half a sweep behind A; per member the kernel sequence is
-// unchanged.  Opt-in (BP_MIXED=1): measured equal to the two-launch sweep on c1 (619 vs
-// 613 us per sweep, r01) -- both roles are latency-bound per warp, so co-running them on an
-// SM halves each role's warps without freeing a shared resource.
-bool mixed_enabled(const bp_problem* p, const bp_map* map) {
-    const char* e = std::getenv("BP_MIXED");
-    if (!(e && e[0] == '1') || p->dim != 2 || p->batch < 2 || p->transposed || p->periodic || p->cdr || p->slab_log2)
-        return false;
-    if (map->kind != BP_MAP_SCALAR && map->kind != BP_MAP_POINTWISE) return false;
-    return launch_mixed(p->log2n, RowArgs{}, ColArgs{}, nullptr, true) == cudaSuccess;
-}
-
-struct MixedHalves {
-    RowArgs ra, rb;
-    ColArgs ca, cb;
-};
-
-MixedHalves mixed_halves(const bp_problem* p, const RowArgs& a, const ColArgs& c) {
-    const int h = p->batch / 2;
-    ColArgs c2 = c;  // what col_stage sets for a 2-D C_GREEN launch
-    c2.planes_per_member = 1;
-    c2.scale = p->green_scale;
-    return {row_args_range(a, p, 0, h), row_args_range(a, p, h, p->batch - h),
-            col_args_range(c2, p, 0, h), col_args_range(c2, p, h, p->batch - h)};
-}
-
-// one pipelined sweep; ev (optional): 3 events around the two launches
-int mixed_sweep(bp_problem* p, const MixedHalves& mh, cudaEvent_t* ev) {
-    if (ev) CU(cudaEventRecord(ev[0], p->stream));
-    CU(launch_mixed(p->log2n, mh.ra, mh.cb, p->stream));
-    if (ev) CU(cudaEventRecord(ev[1], p->stream));
-    CU(launch_mixed(p->log2n, mh.rb, mh.ca, p->stream));
-    if (ev) CU(cudaEventRecord(ev[2], p->stream));
     return BP_OK;
 }
 
@@ -843,26 +913,14 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
 
     // q^0 = V u^0 + f -> forward y-DST -> T ; column pass
     a.in = p->u0;
-    if (p->transposed) {
-        ColArgs cc = c;
-        cc.scale = p->green_scale;
-        CU(launch_transposed(p->log2n, true, R_FWD_BORN, a, cc, p->stream));
-        CU(launch_transposed(p->log2n, false, C_GREEN, a, cc, p->stream));
-    } else {
-        CU(launch_row(p->log2n, p->dim, R_FWD_BORN, a, p->stream));
-    }
-    const bool mixed = !(snapshots && n_snap > 0) && mixed_enabled(p, map);
-    const MixedHalves mh = mixed ? mixed_halves(p, a, c) : MixedHalves{};
-    if (!p->transposed) {
-        // mixed pipeline: only half A's first column pass here (B's runs in the first launch)
-        if (int rc2 = col_stage_checked(p, mixed ? mh.ca : c, C_GREEN, p->green_scale)) return rc2;
-    }
+    CU(launch_row(p->log2n, p->dim, R_FWD_BORN, a, p->stream));
+    if (int rc2 = col_stage_checked(p, c, C_GREEN, p->green_scale)) return rc2;
     // scalar / pointwise 2-D sweeps: the column pass finalises the entry the row pass before
     // it reduced (RowArgs::defer_final / ColArgs::finalize); not for the initial column pass
     // (n >= 64: the column CTA has at least one full warp for finalize_member's shuffles)
     // 3-D: the first (y-line) launch of the column stage finalises, the whole CTA summing the
     // n^2 line partials (finalize_member3; col_stage clears the flag for the other two)
-    if (!mixed && !p->transposed && (p->dim == 2 || p->dim == 3) && p->log2n >= 6 && plan.n == 2 &&
+    if ((p->dim == 2 || p->dim == 3) && p->log2n >= 6 && plan.n == 2 &&
         plan.row[0] && (plan.mode[0] == R_SWEEP || plan.mode[0] == R_SWEEP_D) && !plan.row[1] && plan.mode[1] == C_GREEN) {
         a.defer_final = 1;
         c.finalize = 1;
@@ -905,35 +963,6 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             CU(cudaStreamSynchronize(p->stream));
             if (*p->host_active == 0) break;
         }
-    } else if (p->timing && mixed) {
-        // instrumented mixed path: events around each mixed launch (charged to row_ms; the
-        // column work runs inside the same launches)
-        std::vector<cudaEvent_t> ev(3 * kGraphSweeps);
-        for (auto& e : ev) CU(cudaEventCreate(&e));
-        long launched = 0;
-        while (launched < max_launch) {
-            for (int s = 0; s < kGraphSweeps; ++s) {
-                rc = mixed_sweep(p, mh, &ev[3 * s]);
-                if (rc) break;
-            }
-            if (rc) break;
-            launched += kGraphSweeps;
-            p->stat_launches += (int64_t)2 * kGraphSweeps;
-            CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
-                               p->stream));
-            CU(cudaStreamSynchronize(p->stream));
-            for (int s = 0; s < kGraphSweeps; ++s) {
-                for (int k = 0; k < 2; ++k) {
-                    float ms = 0;
-                    cudaEventElapsedTime(&ms, ev[3 * s + k], ev[3 * s + k + 1]);
-                    p->stat_row_ms += ms;
-                }
-                ++p->stat_timed;
-            }
-            if (*p->host_active == 0) break;
-        }
-        for (auto& e : ev) cudaEventDestroy(e);
-        if (rc) return rc;
     } else if (p->timing) {
         // instrumented path: CUDA events around every row / column launch on the handle's
         // stream, polled once per kGraphSweeps sweeps (same cadence as the graph path)
@@ -966,7 +995,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         if (rc) return rc;
     } else {
         // graph of kGraphSweeps sweeps, replayed until every member terminated
-        const bool reuse = p->graph && p->graph_map_kind == map->kind && p->graph_mixed == mixed &&
+        const bool reuse = p->graph && p->graph_map_kind == map->kind &&
                            p->graph_metric == map->metric && p->graph_format == cfg->format &&
                            p->graph_gamma.x == map->gamma_re && p->graph_gamma.y == map->gamma_im &&
                            p->graph_max_iters == cfg->max_iters && p->graph_rtol == cfg->rtol;
@@ -975,15 +1004,11 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             p->graph = nullptr;
             cudaGraph_t g;
             CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-            for (int s = 0; s < kGraphSweeps; ++s) {
-                if (mixed) mixed_sweep(p, mh, nullptr);
-                else sweep_once(p, plan, a, c, nullptr);
-            }
+            for (int s = 0; s < kGraphSweeps; ++s) sweep_once(p, plan, a, c, nullptr);
             CU(cudaStreamEndCapture(p->stream, &g));
             CU(cudaGraphInstantiate(&p->graph, g, 0));
             cudaGraphDestroy(g);
             p->graph_map_kind = map->kind;
-            p->graph_mixed = mixed;
             p->graph_metric = map->metric;
             p->graph_format = cfg->format;
             p->graph_gamma = a.gamma;
@@ -997,6 +1022,67 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             p->stat_launches += (int64_t)kps * kGraphSweeps;
             CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
                                p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            if (*p->host_active == 0) break;
+        }
+    }
+    return BP_OK;
+}
+
+// bp::run on an any-shape handle: per sweep q = V u^m + f (members still active), z = G q (four
+// line-transform launches + the spectral divide), then one element-wise pass (entry sums, u^{m+1})
+// and the device-side entry / termination record -- the same Control protocol as the fused
+// path (ping-pong u, entry m finalised after u^m, result_buf), polled every kGraphSweeps sweeps.
+int run_core_generic(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool have_u0,
+                     double* snapshots, int n_snap) {
+    const int B = p->batch;
+    const GenArgs g = gen_args(p);
+    Control c = make_control(p);
+    c.max_iters = cfg->max_iters;
+    c.rtol = cfg->rtol;
+    if (int rc = norms(p, p->f, p->fnorm_l2)) return rc;
+    if (int rc = gen_spectral(p, true, p->f, p->y)) return rc;
+    if (int rc = norms(p, p->y, p->fnorm_reta)) return rc;
+    std::vector<double> fn(B);
+    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    for (int b = 0; b < B; ++b)
+        if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
+    if (!have_u0) CU(cudaMemsetAsync(p->u0, 0, sizeof(double2) * p->alloc, p->stream));
+    CU(cudaMemsetAsync(p->u1, 0, sizeof(double2) * p->alloc, p->stream));
+    init_control_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(c, B);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_l2, (size_t)B * p->trace_cap);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_reta, (size_t)B * p->trace_cap);
+    CU(cudaGetLastError());
+    const int nchunk = 64;
+    const double2 gamma = make_double2(map->gamma_re, map->gamma_im);
+    const int direct = cfg->format == BP_FMT_DIRECT;
+    const size_t nd = p->dense_pts;
+    // hx != hy: five_point (hx^2 only, kernels.cpp:56-69) and the two-spacing symbol differ, the
+    // key identity ||G r|| = ||G(V u + f) - u|| no longer holds -- apply G to r explicitly
+    const bool exact_reta = std::fabs(p->grid.lx / (p->gnx + 1) - p->grid.ly / (p->gny + 1)) >
+                            1e-15 * (p->grid.lx / (p->gnx + 1));
+    if (snapshots && n_snap > 0)
+        if (int rc = download(p, p->u0, nullptr, nullptr, snapshots)) return rc;
+    p->stat_launches = 0;
+    const long max_launch = (long)cfg->max_iters + 1;
+    for (long k = 1; k <= max_launch; ++k) {
+        gen_source_kernel<<<grid_for(p->field * B), 256, 0, p->stream>>>(g, c, p->u0, p->u1, p->f, p->y);
+        if (int rc = gen_spectral(p, true, p->y, p->y)) return rc;
+        gen_sweep_kernel<<<dim3(nchunk, B), 256, 0, p->stream>>>(g, c, p->y, p->f, p->u0, p->u1, p->u0, p->u1,
+                                                                 map->kind, gamma, direct, p->gpart, nchunk,
+                                                                 exact_reta ? p->x : nullptr);
+        if (exact_reta) {  // ||G r^m|| (iterate.cpp:131) by a Green application
+            if (int rc = gen_spectral(p, true, p->x, p->x)) return rc;
+            gen_part_kernel<<<dim3(nchunk, B), 256, 0, p->stream>>>(g, c, p->x, p->gpart, nchunk);
+        }
+        gen_finalize_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(c, B, p->gpart, nchunk);
+        CU(cudaGetLastError());
+        p->stat_launches += 8;
+        if (snapshots && k < n_snap)  // u^k in buffer k & 1 for every member still iterating
+            if (int rc = download(p, (k & 1) ? p->u1 : p->u0, nullptr, nullptr, snapshots + 2 * nd * B * k)) return rc;
+        if ((snapshots && n_snap > 0) || k % kGraphSweeps == 0 || k == max_launch) {
+            CU(cudaMemcpyAsync(p->host_active, c.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
             CU(cudaStreamSynchronize(p->stream));
             if (*p->host_active == 0) break;
         }
@@ -1318,6 +1404,21 @@ int cdr_download(bp_problem* p, const double2* src, double* dst, bool host_ptr =
     return BP_OK;
 }
 
+// CC_GREEN column pass of the CDR family: the Neumann tridiagonal x-solve when the handle has its
+// tables (equal to DCT-II -> x scale / lambda -> DCT-III = 2n h^2 scale Tri^-1, the REDFT01
+// REDFT10 pair multiplying by 2n), else the DCT route
+cudaError_t cdr_green(bp_problem* p, const CdrArgs& ac) {
+    if (!p->tri) return launch_cdr(p->log2n, false, CC_GREEN, ac, p->stream);
+    ColArgs c{};
+    c.batch = ac.batch;
+    c.T = reinterpret_cast<double2*>(ac.T);
+    c.status = ac.ctl.status;
+    c.tri = p->tri;
+    const double h = p->grid.lx / p->n;
+    c.tri_scale = 2.0 * p->n * h * h * ac.scale;
+    return launch_tri(p->log2n, CL_CDR, c, p->stream);
+}
+
 // G / L_ref / transforms (transforms.cpp:105-148 with REDFT10 / REDFT01, inverse 1/(4 nx ny))
 //   which 0 G, 2 L_ref, 3 forward transform, 4 inverse transform; out - sub when sub != null
 int cdr_apply(bp_problem* p, int which, const double2* in, double2* out, const double2* sub) {
@@ -1335,7 +1436,7 @@ int cdr_apply(bp_problem* p, int which, const double2* in, double2* out, const d
         case 2:
             CU(launch_cdr(p->log2n, true, RC_FWD, a, p->stream));
             a.scale = inv;
-            CU(launch_cdr(p->log2n, false, which == 0 ? CC_GREEN : CC_LREF, a, p->stream));
+            CU(which == 0 ? cdr_green(p, a) : launch_cdr(p->log2n, false, CC_LREF, a, p->stream));
             a.scale = 1.0;
             CU(launch_cdr(p->log2n, true, RC_INV, a, p->stream));
             return BP_OK;
@@ -1392,7 +1493,7 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
     fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_reta, (size_t)B * p->trace_cap);
     CU(cudaGetLastError());
     CU(launch_cdr(p->log2n, true, RC_B, a, p->stream));
-    CU(launch_cdr(p->log2n, false, CC_GREEN, ac, p->stream));
+    CU(cdr_green(p, ac));
     // norms 2x2, G 3, init_control, 2x fill_nan, RC_B + CC_GREEN
     p->stat_launches = 12;
     p->stat_row_ms = p->stat_col_ms = 0;
@@ -1404,7 +1505,7 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
         CU(launch_cdr(p->log2n, true, RC_A, a, p->stream));
         CU(launch_cdr(p->log2n, true, RC_B, a, p->stream));
         if (ev) CU(cudaEventRecord(ev[1], p->stream));
-        CU(launch_cdr(p->log2n, false, CC_GREEN, ac, p->stream));
+        CU(cdr_green(p, ac));
         if (ev) CU(cudaEventRecord(ev[2], p->stream));
         return BP_OK;
     };
@@ -1506,6 +1607,8 @@ int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* c
         return set_err(BP_EINVAL, "unknown optimal-scalar metric");
     if (p->cdr && (map->kind != BP_MAP_SCALAR || map->gamma_im != 0.0))
         return set_err(BP_ENOTSUP, "CDR family on the GPU: real scalar maps only");
+    if (p->generic && (map->kind == BP_MAP_OPTIMAL_SCALAR || map->kind == BP_MAP_FOURIER_DIAG))
+        return set_err(BP_ENOTSUP, "any-shape grids on the GPU: scalar and pointwise maps");
     if (p->periodic && map->kind == BP_MAP_POINTWISE)
         return set_err(BP_ENOTSUP, "periodic family: the pointwise (i/eta) V map is defined for the "
                                    "Dirichlet family only");
@@ -1570,6 +1673,79 @@ int check_symbol_periodic(const std::vector<double>& xi2, int batch, const doubl
     return BP_OK;
 }
 
+// Any-shape 2-D Dirichlet handle (generic_kernels.cuh): nx, ny >= 1 up to 4095 each, any lx, ly.
+int create_generic(const bp_grid* grid, int32_t batch, const double* k2, const double* k0, const double* eta,
+                   int32_t device, bp_problem** out) {
+    const int nx = grid->nx, ny = grid->ny;
+    if (nx + 1 > 4096 || ny + 1 > 4096)
+        return set_err(BP_ENOTSUP, "GPU any-shape path: nx, ny <= 4095 (power-of-two paths: nx+1 = ny+1 = 2^k <= 4096)");
+    for (int b = 0; b < batch; ++b) {
+        if (!(eta[b] > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
+        if (!std::isfinite(k0[b])) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
+    }
+    const double hx = grid->lx / (nx + 1), hy = grid->ly / (ny + 1);  // grid.hpp:12-24
+    const std::vector<double> ax = gen_lap(nx, hx), ay = gen_lap(ny, hy);
+    if (int rc = check_symbol_generic(ax, ay, batch, k0, eta)) return rc;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return set_err(BP_ECUDA, "no such CUDA device");
+    DeviceGuard guard(device);
+    auto* p = new bp_problem();
+    p->grid = *grid;
+    p->batch = batch;
+    p->device = device;
+    p->dim = 2;
+    p->generic = true;
+    p->gnx = nx;
+    p->gny = ny;
+    p->field = (size_t)nx * ny;
+    p->alloc = p->field * batch;
+    p->dense_pts = p->field;
+    p->inv_h2 = 1.0 / (hx * hx);  // five_point's single h2 = hx^2 (newton_problem.cpp:41)
+    auto fail = [&](int code) {
+        bp_problem_destroy(p);
+        return code;
+    };
+#define CUF(call)                                                                                   \
+    do {                                                                                            \
+        cudaError_t _e = (call);                                                                    \
+        if (_e != cudaSuccess) return fail(set_err(BP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e))); \
+    } while (0)
+    CUF(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    const size_t fb = sizeof(double2) * p->alloc;
+    for (double2** buf : {&p->k2, &p->f, &p->u0, &p->u1, &p->T, &p->x, &p->y, &p->dense}) {
+        CUF(cudaMalloc(buf, fb));
+        CUF(cudaMemsetAsync(*buf, 0, fb, p->stream));
+    }
+    CUF(cudaMalloc(&p->gamma, sizeof(double2) * (size_t)batch));
+    CUF(cudaMalloc(&p->norm_part, sizeof(double) * (size_t)batch * 64));
+    CUF(cudaMalloc(&p->gpart, sizeof(double) * (size_t)batch * 64 * 2));
+    CUF(cudaMalloc(&p->fnorm_l2, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->fnorm_reta, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->ctl_int, sizeof(int) * (5 * (size_t)batch + 1)));
+    CUF(cudaMalloc(&p->counter, sizeof(unsigned) * batch));
+    CUF(cudaMallocHost(&p->host_active, sizeof(int)));
+    CUF(cudaMalloc(&p->dflag, sizeof(int)));
+    CUF(cudaMalloc(&p->k0sq, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->eta, sizeof(double) * batch));
+    CUF(cudaMalloc(&p->gax, sizeof(double) * nx));
+    CUF(cudaMalloc(&p->gay, sizeof(double) * ny));
+    CUF(cudaMemcpyAsync(p->gax, ax.data(), sizeof(double) * nx, cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->gay, ay.data(), sizeof(double) * ny, cudaMemcpyHostToDevice, p->stream));
+    if (int rc = make_gplan(nx + 1, p->gplan_x)) return fail(rc);
+    if (int rc = make_gplan(ny + 1, p->gplan_y)) return fail(rc);
+    std::vector<double> k0sq(batch);
+    for (int b = 0; b < batch; ++b) k0sq[b] = k0[b] * k0[b];
+    CUF(cudaMemcpyAsync(p->k0sq, k0sq.data(), sizeof(double) * batch, cudaMemcpyHostToDevice, p->stream));
+    CUF(cudaMemcpyAsync(p->eta, eta, sizeof(double) * batch, cudaMemcpyHostToDevice, p->stream));
+    if (int rc = upload_k2_checked(p, k2)) return fail(rc);
+    CUF(cudaStreamSynchronize(p->stream));
+    if (int rc = ensure_trace(p, 1000)) return fail(rc);
+#undef CUF
+    *out = p;
+    return BP_OK;
+}
+
 int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, const double* k0,
                 const double* eta, int32_t device, bp_problem** out, bool periodic = false) {
     // Dirichlet: n = nx + 1 cells (interior nx); periodic: n = nx nodes (helmholtz.cpp:11-25)
@@ -1577,6 +1753,9 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     int log2n = 0;
     while ((1 << log2n) < n) ++log2n;
     const int max_log2 = dim == 3 ? kMaxLog2_3d : kMaxLog2;
+    if (!periodic && dim == 2 &&
+        (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > max_log2 || grid->lx != grid->ly))
+        return create_generic(grid, batch, k2, k0, eta, device, out);
     if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > max_log2)
         return set_err(BP_ENOTSUP, periodic ? "GPU periodic path needs square grids with nx = 2^k, 8 <= 2^k <= 4096"
                                    : dim == 3 ? "GPU path needs cubic grids with n+1 = 2^k, 8 <= 2^k <= 512"
@@ -1638,15 +1817,6 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     CUF(cudaMalloc(&p->y, fb));
     for (double2* buf : {p->k2, p->f, p->u0, p->u1, p->T, p->x, p->y})
         CUF(cudaMemsetAsync(buf, 0, fb, p->stream));
-    {
-        // opt-in (BP_TRANSPOSED=1): measured equal to the default column pass on B200 (r01)
-        const char* e = std::getenv("BP_TRANSPOSED");
-        p->transposed = dim == 2 && !periodic && log2n <= 9 && e && std::atoi(e) == 1;
-    }
-    if (p->transposed) {
-        CUF(cudaMalloc(&p->TT, fb));
-        CUF(cudaMemsetAsync(p->TT, 0, fb, p->stream));
-    }
     CUF(cudaMalloc(&p->dense, sizeof(double2) * nd * batch));
     CUF(cudaMalloc(&p->partial, sizeof(double) * (size_t)batch * ((size_t)1 << ((dim - 1) * log2n)) *
                                     kPartStride));
@@ -1750,6 +1920,7 @@ int upload_cdr_medium(bp_problem* p, const double* bx, const double* by, const d
     for (int i = 0; i < 3; ++i)
         CU(cudaMemcpyAsync(dst[i], st[i], bytes, cudaMemcpyDeviceToDevice, p->stream));
     CU(cudaMemcpyAsync(p->sigma0, sigma0, sizeof(double) * p->batch, cudaMemcpyHostToDevice, p->stream));
+    if (int rc = build_tri(p)) return rc;
     CU(cudaStreamSynchronize(p->stream));
     return BP_OK;
 }
@@ -1823,6 +1994,15 @@ int create_cdr_impl(const bp_grid* grid, int32_t batch, const double* bx, const 
     CUF(cudaMemcpyAsync(p->tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->w4, w4.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->lapn, lapn.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
+    {
+        // Green column pass: the Neumann tridiagonal x-solve on real column pairs, n >= 128
+        // (BP_COL_DST=1 keeps the DCT route); tables built by upload_cdr_medium
+        const char* e = std::getenv("BP_COL_DST");
+        if (log2n >= 7 && !(e && e[0] == '1')) {
+            CUF(cudaMalloc(&p->tri, sizeof(double2) * (size_t)batch * (n / 2) * (2 * kTriP + n / kTriP)));
+            CUF(launch_tri(log2n, CL_CDR, ColArgs{}, nullptr, true));
+        }
+    }
     if (int rc = upload_cdr_medium(p, bx, by, sigma, sigma0)) return fail(rc);
     if (int rc = ensure_trace(p, 1000)) return fail(rc);
 #undef CUF
@@ -1994,6 +2174,7 @@ static int slab_create_impl(const bp_grid* grid, int dim, int32_t rank, int32_t 
         CUF(launch_col_pp(log2n, 16, CL_SLAB, C_GREEN, c, nullptr, true));
         CUF(launch_col_pp(log2n, 16, CL_SLAB, C_ONE, c, nullptr, true));
         if (dim == 3) CUF(launch_col_pp(log2n, 16, CL_YBLK, C_ONE, c, nullptr, true));
+        if (log2n >= 6) CUF(launch_tri(log2n, CL_SLAB, c, nullptr, true));
     }
     CUF(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     const size_t fb = sizeof(double2) * p->field, ub = sizeof(double2) * (p->field + 2 * halo);
@@ -2037,6 +2218,16 @@ static int slab_create_impl(const bp_grid* grid, int dim, int32_t rank, int32_t 
     CUF(cudaMemcpyAsync(p->tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->sinp, sinp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->lap, lap.data(), sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
+    {
+        // Green column pass on the rank's column block: tridiagonal x-solve (as create_impl)
+        const char* e = std::getenv("BP_COL_DST");
+        if (log2n >= 6 && !(e && e[0] == '1')) {
+            const size_t lines = (size_t)1 << ((dim - 1) * log2n);
+            CUF(cudaMalloc(&p->tri, sizeof(double2) * lines * (kTriP + n / kTriP)));
+            p->tri_scale = 8.0 * n * h * h * p->green_scale;
+            if (int rc = build_tri(p)) return fail(rc);
+        }
+    }
     std::vector<double2> rows;
     pack_slab_host(k2, n, p->row0, R, rows, dim);
     CUF(cudaMemcpyAsync(p->k2, rows.data(), fb, cudaMemcpyHostToDevice, p->stream));
@@ -2171,7 +2362,11 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
                 c.xchg_log2r = p->slab_log2;
                 for (int r = 0; r < p->slab_nranks; ++r) c.xchg[r] = p->xchg_rows[r];
             }
-            CU(launch_col_pp(p->log2n, 16, CL_SLAB, C_GREEN, c, p->stream));
+            if (p->tri && c.slab_cols % tri_cols_per_cta(p->log2n) == 0) {
+                CU(launch_tri(p->log2n, CL_SLAB, c, p->stream));
+            } else {
+                CU(launch_col_pp(p->log2n, 16, CL_SLAB, C_GREEN, c, p->stream));
+            }
             return BP_OK;
         }
         case BP_SLAB_INV_NORM:  // y <- inverse y-DST of T; sums[1] = local ||y||^2
@@ -2336,12 +2531,14 @@ int bp_problem_destroy(bp_problem* p) {
                     (void*)p->y, (void*)p->dense, (void*)p->partial, (void*)p->gamma, (void*)p->fd, (void*)p->norm_part,
                     (void*)p->fnorm_l2, (void*)p->fnorm_reta, (void*)p->ctl_int, (void*)p->counter,
                     (void*)p->trace_l2, (void*)p->trace_reta, (void*)p->k0sq, (void*)p->eta,
-                    (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2, (void*)p->TT,
+                    (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2,
                     (void*)p->bx, (void*)p->by, (void*)p->sigma, (void*)p->sigma0, (void*)p->lapn,
                     (void*)p->rnorm2, (void*)p->w4, (void*)p->dflag, (void*)p->Tc, (void*)p->slab_sums,
-                    (void*)p->tri})
+                    (void*)p->tri, (void*)p->gax, (void*)p->gay, (void*)p->gpart})
         if (q) cudaFree(q);
     if (p->host_active) cudaFreeHost(p->host_active);
+    free_gplan(p->gplan_x);
+    free_gplan(p->gplan_y);
     if (p->stream && p->own_stream) cudaStreamDestroy(p->stream);
     delete p;
     return BP_OK;
@@ -2372,6 +2569,13 @@ static int pointwise_op(const bp_problem* cp, int op, const double* u, const dou
     if (int rc = upload(p, u, p->x)) return rc;
     if (op == 3)
         if (int rc = upload(p, f, p->f)) return rc;
+    if (p->generic) {
+        gen_pointwise_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(gen_args(p), op, p->x, p->f, p->y);
+        CU(cudaGetLastError());
+        if (int rc = download(p, p->y, nullptr, nullptr, out)) return rc;
+        CU(cudaStreamSynchronize(p->stream));
+        return BP_OK;
+    }
     if (p->periodic && (op == 0 || op == 3)) {
         // pseudospectral A = L_ref - V (helmholtz.cpp:27-32 computes F^-1(|xi|^2 F u) - k2 u;
         // equal to roundoff): y = L_ref x, then y -= V x (and f - y for the residual)
@@ -2415,6 +2619,26 @@ static int spectral_op(const bp_problem* cp, int which, const double* in, const 
         return BP_OK;
     }
     if (int rc = upload(p, in, p->x)) return rc;
+    if (p->generic) {
+        const GenArgs g = gen_args(p);
+        switch (which) {
+            case 0: if (int rc = gen_spectral(p, true, p->x, p->y)) return rc; break;
+            case 1:  // G(V u + f) - u
+                if (int rc = upload(p, f, p->f)) return rc;
+                gen_pointwise_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(g, 4, p->x, p->f, p->y);
+                if (int rc = gen_spectral(p, true, p->y, p->y)) return rc;
+                combine_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(p->y, p->x, nullptr,
+                                                                                   p->field * p->batch);
+                break;
+            case 2: if (int rc = gen_spectral(p, false, p->x, p->y)) return rc; break;
+            case 3: if (int rc = gen_dst2(p, p->x, p->y, 1.0)) return rc; break;
+            default: if (int rc = gen_dst2(p, p->x, p->y, g.gscale)) return rc; break;
+        }
+        CU(cudaGetLastError());
+        if (int rc = download(p, p->y, nullptr, nullptr, out)) return rc;
+        CU(cudaStreamSynchronize(p->stream));
+        return BP_OK;
+    }
     if (p->periodic) {
         if (which == 1)
             if (int rc = upload(p, f, p->f)) return rc;
@@ -2503,8 +2727,9 @@ static int run_impl(const bp_problem* cp, const bp_map* map, const double* f, co
     if (u0)  // periodic: the physical u0 is transformed into U^0 by run_core_periodic
         if (int rc = upload(p, u0, p->periodic ? p->x : p->u0, host_ptr)) return rc;
     ComputeTurn turn(p);
-    const int rc = p->periodic ? run_core_periodic(p, map, cfg, u0 != nullptr, snapshots, n_snap)
-                               : run_core(p, map, cfg, u0 != nullptr, snapshots, n_snap);
+    const int rc = p->periodic  ? run_core_periodic(p, map, cfg, u0 != nullptr, snapshots, n_snap)
+                   : p->generic ? run_core_generic(p, map, cfg, u0 != nullptr, snapshots, n_snap)
+                                : run_core(p, map, cfg, u0 != nullptr, snapshots, n_snap);
     if (rc) return rc;
     turn.release();
     return finish_run(p, cfg, u_out, host_ptr, res_l2, res_reta, info);
@@ -2542,7 +2767,10 @@ int bp_problem_set_medium(bp_problem* p, const double* k2, const double* k0, con
         if (!(eta[b] > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
         if (!std::isfinite(k0[b])) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
     }
-    if (p->periodic) {
+    if (p->generic) {
+        const double hx = p->grid.lx / (p->gnx + 1), hy = p->grid.ly / (p->gny + 1);
+        if (int rc = check_symbol_generic(gen_lap(p->gnx, hx), gen_lap(p->gny, hy), p->batch, k0, eta)) return rc;
+    } else if (p->periodic) {
         if (int rc = check_symbol_periodic(xi2_table(p->n, p->grid.lx), p->batch, k0, eta)) return rc;
     } else if (int rc = check_symbol(p->grid, p->dim, p->batch, k0, eta)) {
         return rc;

@@ -26,13 +26,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-// Opt-in (measured slower, r01: c1 row 463 vs 365 us, c4 +13 %): twiddles and the
-// pre-processing sines read from the device tables (tw, sinp: L1-resident,
-// one load each) instead of being built by in-register complex multiplications: r01 ncu showed
-// FP64 as the binding pipe, and the multiplication chains also serialised each butterfly.
-#ifndef BS_TW_TABLE
-#define BS_TW_TABLE 0
-#endif
+// Twiddles and pre-processing sines are built by in-register complex multiplications from one
+// table load each (device tables for every power measured slower, r01: c1 row 463 vs 365 us,
+// c4 +13 % -- L1 latency on the butterfly critical path).
 
 namespace bs {
 
@@ -426,13 +422,7 @@ struct DstEngine {
                 const int jm = jj % NS;
                 // exp(-2 pi i jm r / (NS R)) = w^r with w = tw[jm N/(NS R)]: one load per butterfly
                 double2 pw[R];
-#if BS_TW_TABLE
-                pw[0] = make_double2(1.0, 0.0);
-#pragma unroll
-                for (int r = 1; r < R; ++r) pw[r] = __ldg(&tw[jm * r * (N / (NS * R))]);
-#else
                 twiddle_powers<R>(__ldg(&tw[jm * (N / (NS * R))]), pw);
-#endif
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     // jj + r STRIDE_IN = t + (T b + r STRIDE_IN), a multiple of T added
@@ -481,12 +471,8 @@ struct DstEngine {
     // 2 sin(pi j/N) for j = t + T m (sinp holds 2 sin(pi j/N), j < N)
     __device__ __forceinline__ static double sin2(const double* __restrict__ sinp, int t, int m, double st,
                                                   double ct) {
-#if BS_TW_TABLE
-        return __ldg(&sinp[t + T * m]);
-#else
         constexpr int STEP = 16 / P;
         return fma(st, kCS16[m * STEP].c, ct * kCS16[m * STEP].s);
-#endif
     }
 
     template <class Pol>
@@ -497,7 +483,7 @@ struct DstEngine {
         double2 v[P];
         // 2 sin(pi t/N), 2 cos(pi t/N): the engine computes 4x the sine sum (the 1/2 factors
         // of pre- and post-processing are folded into the caller's scale, exact powers of 2)
-        const double st = BS_TW_TABLE ? 0.0 : 2.0 * __ldg(&sinp[t]), ct = BS_TW_TABLE ? 0.0 : 2.0 * __ldg(&sinp[t + H]);
+        const double st = 2.0 * __ldg(&sinp[t]), ct = 2.0 * __ldg(&sinp[t + H]);
 #pragma unroll
         for (int m = 0; m < P; ++m) {
             const int j = t + T * m;
@@ -518,7 +504,7 @@ struct DstEngine {
     __device__ __forceinline__ static void run_smem(double2 (&v)[P], double2 (&y)[P], int t, double2* buf,
                                                     const double2* __restrict__ tw,
                                                     const double* __restrict__ sinp, const Pol& pol) {
-        const double st = BS_TW_TABLE ? 0.0 : 2.0 * __ldg(&sinp[t]), ct = BS_TW_TABLE ? 0.0 : 2.0 * __ldg(&sinp[t + H]);
+        const double st = 2.0 * __ldg(&sinp[t]), ct = 2.0 * __ldg(&sinp[t + H]);
         // x_{N-j}, j = t + T m: (T - t) + T (P-1-m) for t > 0; T (P-m) (its own slot P-m)
         // for t = 0 (the split needs T - t < T, so lane 0 takes a direct constant index)
         const int bt = G::pidx(t), tm = (T - t) & (T - 1), btm = G::pidx(tm);
@@ -557,18 +543,12 @@ struct DstEngine {
         constexpr bool KS = K == 8 && H % 64 == 0;
         const int pk = G::pidx(t * K), ph0 = G::pidx(H - t * K), ph1 = G::pidx(H - t * K - K);
         const int pn0 = G::pidx((N - t * K) & (N - 1)), pn1 = G::pidx(N - t * K - K);
-#if !BS_TW_TABLE
         const double2 w0 = __ldg(&tw[t * K]), w1 = __ldg(&tw[1]);
         double2 w = w0;           // exp(-2 pi i k/N), stepped by exp(-2 pi i/N)
-#endif
 #pragma unroll
         for (int i = 0; i < K; ++i) {
             const int k = t * K + i;
-#if BS_TW_TABLE
-            const double2 w = __ldg(&tw[k]);
-#else
             if (i > 0) w = cmul(w, w1);
-#endif
             const double2 a = buf[KS ? pk + i : G::pidx(k)];
             const double2 b = cmul(buf[KS ? pk + i + G::pidx(H) : G::pidx(k + H)], w);
             const double2 Wk = cadd(a, b);

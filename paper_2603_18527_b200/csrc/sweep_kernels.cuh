@@ -40,9 +40,6 @@
 #ifndef BS_ROW_REGS
 #define BS_ROW_REGS 128
 #endif
-// column kernels with warp-private engines (col_group_w) for lines of 32 threads (r01:
-// 277 vs 246 us on c1 -- the engines' own stride patterns conflict where the c-fastest map
-// of col_group does not; kept for experiments, off)
 #ifndef BS_COL_LD256
 #define BS_COL_LD256 1  // 256-bit paired-column loads in the 2-column (n >= 2048) column kernel
 #endif
@@ -51,9 +48,6 @@
 #endif
 #ifndef BS_COL_WIDE
 #define BS_COL_WIDE 1  // warp-contiguous engines + named barriers for 2-column CTAs (n >= 2048)
-#endif
-#ifndef BS_COL_WARP
-#define BS_COL_WARP 0
 #endif
 #ifndef BS_RSM_ALL
 #define BS_RSM_ALL 1
@@ -134,7 +128,6 @@ struct RowArgs {
     double2* out;              // R_INV output (padded)
     const double2* sub;        // R_INV: optional field subtracted from the output
     double2* T;                // intermediate (padded)
-    double2* TT;               // transposed intermediate (TOUT kernels write it, tcol reads it)
     double2* u0;               // iterate ping
     double2* u1;               // iterate pong
     double2* X;                // direction x^m (optimal-scalar / FourierDiag modes)
@@ -178,7 +171,6 @@ struct ColArgs {
     const double* lap;         // (4/h^2) sin^2(j pi / (2n)), j < n
     double scale;              // C_ONE scale / Green normalisation 4/n^2 (/ engine gain)
     const double2* fd;         // C_FD: FourierDiag multiplier, padded n x n (shared by the batch)
-    const double2* TT;         // tcol: transposed input [member][q][i]
     double2* T;
     const double2* tw;
     const double* sinp;
@@ -329,8 +321,6 @@ struct RowGeom {
 // DIM = 2: lines are the rows of each member (x index i, y contiguous), five-point stencil.
 // DIM = 3: lines are the z-lines (x, y) of each member ([x][y][z], z contiguous), seven-point
 //          stencil (the 3-D extension of config c3; no reference counterpart).
-// TOUT: write the forward transform transposed ([member][q][i], a.TT) through a CTA-wide
-// shared-memory tile (128-B segments), for the warp-per-line column pass tcol_kernel.
 // SLAB: the launch covers one rank's x-slab (RowArgs::slab_log2 / row0 / slab_sums); a separate
 // instantiation so the whole-member path keeps its compile-time indexing.
 // One group of EPB lines (the work of one CTA).  `staged`: the group's operands are already
@@ -354,7 +344,7 @@ __device__ __forceinline__ size_t t_index(int sl, size_t mem, int i, int j) {
     }
 }
 
-template <int LOG2N, int MODE, int NW, int PP, int DIM, bool TOUT, bool SLAB>
+template <int LOG2N, int MODE, int NW, int PP, int DIM, bool SLAB>
 __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, const bool staged) {
     using G = Geom<LOG2N, PP>;
     using RG = RowGeom<LOG2N, PP, NW>;
@@ -371,7 +361,6 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     const int t = threadIdx.x % T;
     const int e = threadIdx.x / T;
     const long grow = grp * EPB + e;
-    static_assert(!SLAB || !TOUT, "slabs: row-major handoff only");
     // log2(lines per member or slab): a slab holds 2^slab_log2 rows (2-D) / x-planes (3-D)
     const int lsh = SLAB ? a.slab_log2 + (DIM - 2) * LOG2N : LLINES;
     const int b = (int)(grow >> lsh);
@@ -682,37 +671,22 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         }
 #pragma unroll
         for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y2[l];
-        if constexpr (TOUT) {
-            static_assert(DIM == 2 && T <= 32, "transposed handoff: 2-D lines of <= 512");
-            __syncthreads();
-            // tile (EPB rows x N) -> TT[b][q][i]: lanes = 8 consecutive rows x 4 modes
-            const long g0 = grp * EPB;
-            for (int k = threadIdx.x; k < EPB * N; k += NW * 32) {
-                const int ee = k % EPB, qq = k / EPB;
-                const long g = g0 + ee;
-                const int bb = (int)(g >> LOG2N);
-                if (bb < a.batch)
-                    a.TT[((size_t)bb << (2 * LOG2N)) + (size_t)qq * N + (g & (N - 1))] =
-                        smem[ee * G::PAD_N + G::pidx(qq)];
-            }
-        } else {
-            pol.sync();
+        pol.sync();
 #pragma unroll
-            for (int mm = 0; mm < P; ++mm) {
-                const int j = t + T * mm;
-                if (valid) {
-                    const double2 v = buf[G::at_stride(t, G::pidx(t), mm)];
-                    size_t ix = tix(j);
-                    if constexpr (SLAB) {
-                        if (a.xchg_on) {  // block d -> rank d's receive buffer, at block xchg_rank
-                            const int lb = 2 * sl + (DIM - 2) * LOG2N;  // log2 elements per block
-                            const size_t d = ix >> lb;
-                            a.xchg[d][((size_t)a.xchg_rank << lb) + (ix & ((1ull << lb) - 1))] = v;
-                            continue;
-                        }
+        for (int mm = 0; mm < P; ++mm) {
+            const int j = t + T * mm;
+            if (valid) {
+                const double2 v = buf[G::at_stride(t, G::pidx(t), mm)];
+                size_t ix = tix(j);
+                if constexpr (SLAB) {
+                    if (a.xchg_on) {  // block d -> rank d's receive buffer, at block xchg_rank
+                        const int lb = 2 * sl + (DIM - 2) * LOG2N;  // log2 elements per block
+                        const size_t d = ix >> lb;
+                        a.xchg[d][((size_t)a.xchg_rank << lb) + (ix & ((1ull << lb) - 1))] = v;
+                        continue;
                     }
-                    a.T[ix] = v;
                 }
+                a.T[ix] = v;
             }
         }
     }
@@ -848,91 +822,12 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     }
 }
 
-template <int LOG2N, int MODE, int NW, int PP, int DIM = 2, bool TOUT = false, bool SLAB = false>
+template <int LOG2N, int MODE, int NW, int PP, int DIM = 2, bool SLAB = false>
 __global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? BS_ROW_REGS : 80>::value))
 row_kernel(const RowArgs a) {
     // (a persistent variant looping over groups with next-group L2 prefetch measured 23-48 %
     // slower on c1, r01: the hardware's CTA scheduling is kept)
-    row_group<LOG2N, MODE, NW, PP, DIM, TOUT, SLAB>(a, blockIdx.x, false);
-}
-
-// ------------------------------------------------------------------ transposed column kernel
-// Warp-per-line x-pass over the transposed intermediate written by the TOUT row kernel: line
-// (member b, mode q) = TT[b][q][0..n), forward x-DST, x w_pq (Green 4/(n^2 lambda) or the
-// FourierDiag m_pq), inverse x-DST, written back row-major T[b][i][q] through a CTA tile.
-template <int LOG2N, int MODE, int NW, int PP>
-__global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? 128 : 80>::value))
-tcol_kernel(const ColArgs a) {
-    using G = Geom<LOG2N, PP>;
-    using RG = RowGeom<LOG2N, PP, NW>;
-    using Pol = typename PolicyFor<G::T>::type;
-    using Engine = DstEngine<LOG2N, PP>;
-    constexpr int N = G::N, P = G::P, T = G::T;
-    constexpr int EPB = RG::EPB;
-    static_assert(T <= 32, "transposed column pass: lines of <= 512");
-    extern __shared__ double2 smem[];
-
-    const int t = threadIdx.x % T;
-    const int e = threadIdx.x / T;
-    const long g = (long)blockIdx.x * EPB + e;
-    const int b = (int)(g >> LOG2N);
-    const int q = (int)(g & (N - 1));
-    bool valid = b < a.batch;
-    if (valid && a.status) valid = __ldcg(&a.status[b]) == ST_ACTIVE;
-    if (!__syncthreads_or(valid)) return;
-    double2* buf = smem + e * G::PAD_N;
-    const Pol pol{};
-    const double2 zero = make_double2(0.0, 0.0);
-    const size_t line = ((size_t)(valid ? b : 0) << (2 * LOG2N)) + (size_t)q * N;
-
-    double2 x[P], xm[P], y[P];
-#pragma unroll
-    for (int mm = 0; mm < P; ++mm) {
-        const int j = t + T * mm;
-        x[mm] = valid ? a.TT[line + j] : zero;
-        xm[mm] = (valid && j != 0) ? a.TT[line + (N - j)] : zero;  // mirror: L1 hit
-    }
-    Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
-    {
-        const double k0sq = valid ? a.k0sq[b] : 0.0, eta = valid ? a.eta[b] : 1.0;
-        const double lq = a.lap[q];
-#pragma unroll
-        for (int l = 0; l < P; ++l) {
-            const int p = t * P + l;
-            double2 w;
-            if constexpr (MODE == C_FD) {
-                w = cscale(a.fd[(size_t)p * N + q], a.scale);
-            } else {  // C_GREEN: scale / lambda, lambda = (a_p + a_q) - (k0^2 + i eta)
-                const double lr = (a.lap[p] + lq) - k0sq;
-                const double li = -eta;
-                const double s = a.scale * rcp_green(fma(lr, lr, li * li));
-                w = make_double2(lr * s, -li * s);
-            }
-            y[l] = (p == 0 || q == 0) ? zero : cmul(y[l], w);
-        }
-    }
-    // contiguous -> stride layout for the inverse transform (+ its mirror by shuffles)
-#pragma unroll
-    for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y[l];
-    pol.sync();
-#pragma unroll
-    for (int mm = 0; mm < P; ++mm) x[mm] = buf[G::at_stride(t, G::pidx(t), mm)];
-    pol.sync();
-    pol.mirror(x, xm, t, buf, typename G::Pidx{});
-    Engine::run(x, xm, y, t, buf, a.tw, a.sinp, pol);
-#pragma unroll
-    for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y[l];
-    __syncthreads();
-    // tile (EPB modes x N rows) -> T[b][i][q0 .. q0+EPB)
-    const long g0 = (long)blockIdx.x * EPB;
-    for (int k = threadIdx.x; k < EPB * N; k += NW * 32) {
-        const int ee = k % EPB, ii = k / EPB;
-        const long gg = g0 + ee;
-        const int bb = (int)(gg >> LOG2N);
-        if (bb < a.batch && (!a.status || __ldcg(&a.status[bb]) == ST_ACTIVE))
-            a.T[((size_t)bb << (2 * LOG2N)) + (size_t)ii * N + (gg & (N - 1))] =
-                smem[ee * G::PAD_N + G::pidx(ii)];
-    }
+    row_group<LOG2N, MODE, NW, PP, DIM, SLAB>(a, blockIdx.x, false);
 }
 
 // ------------------------------------------------------------------ column kernel
@@ -949,7 +844,8 @@ struct ColGeom {
 //           CL_SLAB: 2-D x-lines of the n x slab_cols column block a rank holds after the
 //           all-to-all of a slab-decomposed grid (row stride slab_cols, global column col0 + q).
 //           CL_YBLK: 3-D slab y-lines on the dest-blocked layout (t_index<3, true>).
-enum ColLayout { CL_PLANE = 0, CL_X3 = 2, CL_SLAB = 3, CL_YBLK = 4 };
+//           CL_CDR: config c4 real column pairs (the tridiagonal pass only, tri_kernels.cuh).
+enum ColLayout { CL_PLANE = 0, CL_X3 = 2, CL_SLAB = 3, CL_YBLK = 4, CL_CDR = 5 };
 
 #ifndef BS_COL_REVERSE
 #define BS_COL_REVERSE 1
@@ -1025,119 +921,12 @@ __device__ __forceinline__ void finalize_member3(const ColArgs& a, int b) {
     }
 }
 
-// Column group with warp-private engines (lines of T <= 32 threads): the CTA stages its C
-// columns into C shared-memory lines with coalesced row-segment loads, each engine (one warp
-// or warp segment) transforms its own line with warp-level sync and shuffle scans (no CTA
-// barriers, no shared-memory scan inside the transforms), and the CTA stores the lines back
-// with the same row-segment pattern.  Two CTA barriers per group in total.
-template <int LOG2N, int MODE, int C, int PP, int LAYOUT>
-__device__ __forceinline__ void col_group_w(const ColArgs& a, const int bid) {
-    using G = Geom<LOG2N, PP>;
-    using Engine = DstEngine<LOG2N, PP>;
-    constexpr int N = G::N, P = G::P, T = G::T;
-    static_assert(T <= 32, "warp-private column engines");
-    constexpr int THREADS = C * T;
-    extern __shared__ double2 smem[];
-    const int e = threadIdx.x / T, t = threadIdx.x % T;  // engine e = column q0 + e
-    constexpr int GROUPS = N / C;
-    int b, yl = 0, qa0;
-    size_t mem;
-    size_t LS = LAYOUT == CL_X3 ? (size_t)N * N : (size_t)N;
-    if constexpr (LAYOUT == CL_SLAB) {
-        const int groups = a.slab_cols / C;
-        b = bid / groups;
-        qa0 = (bid % groups) * C;
-        LS = (size_t)a.slab_cols;
-        mem = (size_t)b * N * a.slab_cols;
-    } else if constexpr (LAYOUT == CL_X3) {
-        const int grp = bid / GROUPS;
-        b = grp >> LOG2N;
-        yl = grp & (N - 1);
-        if (yl == 0) return;
-        mem = ((size_t)b << (3 * LOG2N)) + (size_t)yl * N;
-        qa0 = (bid % GROUPS) * C;
-    } else {
-        const int plane = bid / GROUPS;
-        b = plane / a.planes_per_member;
-        if (a.planes_per_member > 1 && (plane & (N - 1)) == 0) return;
-        mem = (size_t)plane * N * N;
-        qa0 = (bid % GROUPS) * C;
-    }
-    const int q = (LAYOUT == CL_SLAB ? a.col0 : 0) + qa0 + e;  // global column of this engine
-    if (a.status) {
-        const bool active = __ldcg(&a.status[b]) == ST_ACTIVE;  // read before finalising
-        if constexpr (LAYOUT == CL_PLANE) {
-            if (a.finalize && active && a.planes_per_member == 1 && (bid % GROUPS) == 0 && threadIdx.x < 32)
-                finalize_member(a, b, 1 << a.fin_lsh);
-            if (a.finalize && active && a.planes_per_member > 1) {  // 3-D (see col_group)
-                const int pim = (bid / GROUPS) & (N - 1), g = bid % GROUPS;
-                if (col_reversed<LAYOUT>(a) ? (pim == N - 1 && g == GROUPS - 1) : (pim == 1 && g == 0))
-                    finalize_member3<LOG2N>(a, b);
-            }
-        }
-        if (!active) return;  // uniform per CTA
-    }
-    const double2 zero = make_double2(0.0, 0.0);
-
-    // coalesced staging: consecutive threads = consecutive columns of one row (C*16-B segments);
-    // line stride PAD_N is odd in 16-B units, so the C lines of one row hit distinct banks
-#pragma unroll
-    for (int k0 = 0; k0 < C * N; k0 += THREADS) {
-        const int k = k0 + threadIdx.x, j = k / C, cc = k % C;
-        smem[cc * G::PAD_N + j] = a.T[mem + (size_t)j * LS + qa0 + cc];  // unpadded (run_smem<true>)
-    }
-    __syncthreads();
-    double2* buf = smem + e * G::PAD_N;
-    const WarpSeg<T> pol{};
-    double2 x[P], y[P];
-    Engine::template run_smem<true>(x, y, t, buf, a.tw, a.sinp, pol);
-    if constexpr (MODE == C_ONE) {
-#pragma unroll
-        for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = cscale(y[l], a.scale);
-    } else {
-        const double k0sq = a.k0sq[b], eta = a.eta[b];
-        const double lq = LAYOUT == CL_X3 ? a.lap[yl] + a.lap[q] : a.lap[q];
-#pragma unroll
-        for (int l = 0; l < P; ++l) {
-            const int p = t * P + l;
-            // lambda = (a_p + a_q) - (k0^2 + i eta)   (symbol.cpp:69-80 + shift_symbol :97-100)
-            const double lr = (a.lap[p] + lq) - k0sq;
-            const double li = -eta;
-            double2 w;
-            if constexpr (MODE == C_FD) {
-                const size_t fi = LAYOUT == CL_X3 ? ((size_t)p * N + yl) * N + q : (size_t)p * N + q;
-                w = cscale(a.fd[fi], a.scale);
-            } else if constexpr (MODE == C_GREEN) {
-                const double s = a.scale * rcp_green(fma(lr, lr, li * li));
-                w = make_double2(lr * s, -li * s);  // scale / lambda
-            } else {
-                w = make_double2(lr * a.scale, li * a.scale);  // scale * lambda
-            }
-            buf[G::pidx(p)] = (p == 0 || q == 0) ? zero : cmul(y[l], w);
-        }
-        pol.sync();
-        Engine::run_smem(x, y, t, buf, a.tw, a.sinp, pol);
-#pragma unroll
-        for (int l = 0; l < P; ++l) buf[G::at_block(t, G::pidx(t * P), l)] = y[l];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k0 = 0; k0 < C * N; k0 += THREADS) {
-        const int k = k0 + threadIdx.x, j = k / C, cc = k % C;
-        a.T[mem + (size_t)j * LS + qa0 + cc] = smem[cc * G::PAD_N + G::pidx(j)];
-    }
-}
-
 // One CTA's column group (bid = the CTA index of the column launch).
 template <int LOG2N, int MODE, int C, int PP, int LAYOUT>
 __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
     using G = Geom<LOG2N, PP>;
     using Engine = DstEngine<LOG2N, PP>;
     constexpr int N = G::N, P = G::P, T = G::T;
-    if constexpr (BS_COL_WARP && G::T == 32) {
-        col_group_w<LOG2N, MODE, C, PP, LAYOUT>(a, bid);
-        return;
-    }
     extern __shared__ double2 smem[];
     // WIDE (two 2048/4096-point columns per CTA): warp-contiguous engines synchronised by their
     // own named barriers (the engines no longer wait for each other at every pass), the CTA
@@ -1374,37 +1163,6 @@ col_kernel(const ColArgs a) {
     // wrote (their T still in L2) and ends on the first ones, which the next row pass then
     // reads first, again from L2: each handoff reuses the L2-resident tail of the other pass.
     col_group<LOG2N, MODE, C, PP, LAYOUT>(a, col_reversed<LAYOUT>(a) ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
-}
-
-// ------------------------------------------------------------------ mixed (pipelined) kernel
-// One launch = the fused row pass (R_SWEEP) of one half of the batch AND the column pass
-// (C_GREEN) of the other half, CTAs interleaved 1:1 so every SM co-runs both roles: the row
-// role streams HBM (96 B/pt) while the column role is FP64/issue-bound (32 B/pt), so each
-// fills the other's idle resource.  The halves alternate roles launch by launch (the column
-// half is half a sweep behind); per member the launch sequence is the plain R_SWEEP, C_GREEN
-// alternation, so results are bit-identical to the two-launch sweep.
-template <int LOG2N, int NW, int PP, int C>
-struct MixedGeom {
-    static constexpr int THREADS = NW * 32;
-    static_assert(THREADS == C * Geom<LOG2N, PP>::T, "row and column CTAs of equal size");
-    static constexpr size_t SMEM = RowGeom<LOG2N, PP, NW>::SMEM > ColGeom<LOG2N, PP, C>::SMEM
-                                       ? RowGeom<LOG2N, PP, NW>::SMEM
-                                       : ColGeom<LOG2N, PP, C>::SMEM;
-};
-
-template <int LOG2N, int NW, int PP, int C>
-__global__ void __launch_bounds__(NW * 32, (MinBlocks<NW * 32, PP >= 16 ? 128 : 80>::value))
-mixed_kernel(const RowArgs ra, const ColArgs ca, const int nrow, const int ncol) {
-    const int bid = blockIdx.x;
-    const int m = nrow < ncol ? nrow : ncol;
-    if (bid < 2 * m) {
-        if (bid & 1) col_group<LOG2N, C_GREEN, C, PP, CL_PLANE>(ca, bid >> 1);
-        else row_group<LOG2N, R_SWEEP, NW, PP, 2, false, false>(ra, bid >> 1, false);
-    } else if (nrow > ncol) {
-        row_group<LOG2N, R_SWEEP, NW, PP, 2, false, false>(ra, bid - m, false);
-    } else {
-        col_group<LOG2N, C_GREEN, C, PP, CL_PLANE>(ca, bid - m);
-    }
 }
 
 }  // namespace bs

@@ -35,21 +35,21 @@ inline int row_lines_per_cta(int log2n, int pp) {
     return nw * 32 / t;
 }
 
-template <int L, int MODE, int PP, int DIM, bool TOUT = false, bool SLAB = false>
+template <int L, int MODE, int PP, int DIM, bool SLAB = false>
 cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
     constexpr int NWR = RowWarps<L, PP>::value;
     using RG = RowGeom<L, PP, NWR>;
     // slab launches (2-D, row-major handoff, the modes the slab driver uses) -> SLAB instance
-    constexpr bool SLAB_OK = !TOUT && PP == 16 &&
+    constexpr bool SLAB_OK = PP == 16 &&
                              (MODE == R_FWD || MODE == R_FWD_BORN || MODE == R_INV || MODE == R_SWEEP);
     if constexpr (SLAB_OK && !SLAB) {
         if (a.slab_log2 || prepare) {
-            const cudaError_t e = launch_row_t<L, MODE, PP, DIM, false, true>(a, s, prepare);
+            const cudaError_t e = launch_row_t<L, MODE, PP, DIM, true>(a, s, prepare);
             if (!prepare || e != cudaSuccess) return e;
         }
     }
     if (!SLAB && a.slab_log2 && !prepare) return cudaErrorInvalidValue;
-    auto k = row_kernel<L, MODE, NWR, PP, DIM, TOUT, SLAB>;
+    auto k = row_kernel<L, MODE, NWR, PP, DIM, SLAB>;
     if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
     const long rows = (long)a.batch << (SLAB ? a.slab_log2 + (DIM - 2) * L : (DIM - 1) * L);
     const int grid = (int)((rows + RG::EPB - 1) / RG::EPB);
@@ -103,14 +103,20 @@ cudaError_t launch_col_p(int mode, const ColArgs& a, cudaStream_t s, bool prepar
     }
 }
 
+// columns per CTA of the tridiagonal column pass (host side of TriGeom::C)
+inline int tri_cols_per_cta(int log2n) {
+    const int segs = (1 << log2n) / kTriP;
+    return segs >= TRI_THREADS ? 2 : TRI_THREADS / segs;
+}
+
 // ---- Green column pass as a tridiagonal x-solve (n >= 64): persistent CTAs, one per
 // resident slot (occupancy queried once per instance)
 template <int L, int LAYOUT>
 cudaError_t launch_tri_t(const ColArgs& a, cudaStream_t s, bool prepare) {
     if constexpr (L >= 6) {
         using TG = TriGeom<L>;
-        using TT = TriTile<L>;
-        auto k = tri_kernel<L, LAYOUT>;
+        using TT = TriTile<L, LAYOUT == CL_CDR>;
+        auto k = tri_kernel<L, LAYOUT, LAYOUT == CL_CDR>;
         if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TT::SMEM);
         static int slots = [&] {
             int dev = 0, sms = 0, per = 0;
@@ -119,43 +125,15 @@ cudaError_t launch_tri_t(const ColArgs& a, cudaStream_t s, bool prepare) {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, TG::THREADS, TT::SMEM);
             return sms * (per > 0 ? per : 1);
         }();
-        const long tiles = (long)a.batch * (LAYOUT == CL_X3 ? (1L << L) : 1L) * ((1 << L) / TG::C);
+        const long tiles = LAYOUT == CL_SLAB  ? (long)(a.slab_cols / TG::C)
+                           : LAYOUT == CL_CDR ? (long)a.batch * ((1 << L) / 2 / TG::C)
+                                              : (long)a.batch * (LAYOUT == CL_X3 ? (1L << L) : 1L) * ((1 << L) / TG::C);
+        if (LAYOUT == CL_SLAB && (a.slab_cols % TG::C) != 0) return cudaErrorInvalidValue;
+        if (LAYOUT == CL_CDR && (1 << L) / 2 < TG::C) return cudaErrorInvalidValue;
         const int grid = (int)(tiles < slots ? tiles : slots);
         if (grid == 0) return cudaSuccess;
         k<<<grid, TG::THREADS, TT::SMEM, s>>>(a);
         return cudaGetLastError();
-    }
-    return cudaErrorInvalidValue;
-}
-
-// ---- transposed 2-D handoff (n <= 512): TOUT row kernels + warp-per-line column pass
-template <int L, int MODE, int PP>
-cudaError_t launch_tcol_t(const ColArgs& a, cudaStream_t s, bool prepare) {
-    using RG = RowGeom<L, PP, kRowWarps>;
-    auto k = tcol_kernel<L, MODE, kRowWarps, PP>;
-    if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RG::SMEM);
-    const long lines = (long)a.batch << L;
-    k<<<(int)((lines + RG::EPB - 1) / RG::EPB), kRowWarps * 32, RG::SMEM, s>>>(a);
-    return cudaGetLastError();
-}
-
-template <int L>
-cudaError_t launch_transposed_p(bool row, int mode, const RowArgs& a, const ColArgs& c,
-                                cudaStream_t s, bool prep) {
-    if constexpr (Geom<L, 16>::T <= 32) {
-        if (row) {
-            switch (mode) {
-                case R_FWD_BORN: return launch_row_t<L, R_FWD_BORN, 16, 2, true>(a, s, prep);
-                case R_SWEEP: return launch_row_t<L, R_SWEEP, 16, 2, true>(a, s, prep);
-                case R_OPT_B: return launch_row_t<L, R_OPT_B, 16, 2, true>(a, s, prep);
-                case R_RETA_A: return launch_row_t<L, R_RETA_A, 16, 2, true>(a, s, prep);
-                case R_FD_A: return launch_row_t<L, R_FD_A, 16, 2, true>(a, s, prep);
-                case R_FD_B: return launch_row_t<L, R_FD_B, 16, 2, true>(a, s, prep);
-                default: return cudaErrorInvalidValue;
-            }
-        }
-        if (mode == C_FD) return launch_tcol_t<L, C_FD, 16>(c, s, prep);
-        return launch_tcol_t<L, C_GREEN, 16>(c, s, prep);
     }
     return cudaErrorInvalidValue;
 }
@@ -244,24 +222,6 @@ cudaError_t launch_periodic_p(bool row, int mode, const PerArgs& a, cudaStream_t
     }
 }
 
-// ---- mixed launch: R_SWEEP rows of one half-batch + C_GREEN columns of the other (2-D, P = 16)
-template <int L>
-cudaError_t launch_mixed_t(const RowArgs& ra, const ColArgs& ca, cudaStream_t s, bool prepare) {
-    constexpr int C = ColCols<L>::value;
-    if constexpr (kRowWarps * 32 == C * Geom<L, 16>::T) {
-        using MG = MixedGeom<L, kRowWarps, 16, C>;
-        using RG = RowGeom<L, 16, kRowWarps>;
-        auto k = mixed_kernel<L, kRowWarps, 16, C>;
-        if (prepare) return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG::SMEM);
-        const int nrow = (int)((((long)ra.batch << L) + RG::EPB - 1) / RG::EPB);
-        const int ncol = ca.batch * ((1 << L) / C);
-        if (nrow + ncol == 0) return cudaSuccess;
-        k<<<nrow + ncol, MG::THREADS, MG::SMEM, s>>>(ra, ca, nrow, ncol);
-        return cudaGetLastError();
-    }
-    return cudaErrorInvalidValue;
-}
-
 // 3-D kernels exist for n <= 512 (P = 16)
 constexpr int kMaxLog2_3d = 9;
 
@@ -305,18 +265,13 @@ struct Pp8 {
                                      bool prep) {                                               \
         return launch_periodic_p<L>(row, mode, a, s, prep);                                     \
     }                                                                                           \
-    cudaError_t launch_transposed_L##L(bool row, int mode, const RowArgs& a, const ColArgs& c,  \
-                                       cudaStream_t s, bool prep) {                             \
-        return launch_transposed_p<L>(row, mode, a, c, s, prep);                                \
-    }                                                                                           \
     cudaError_t launch_cdr_L##L(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep) { \
         return launch_cdr_p<L>(row, mode, a, s, prep);                                          \
     }                                                                                           \
-    cudaError_t launch_mixed_L##L(const RowArgs& ra, const ColArgs& ca, cudaStream_t s, bool prep) { \
-        return launch_mixed_t<L>(ra, ca, s, prep);                                              \
-    }                                                                                           \
     cudaError_t launch_tri_L##L(int layout, const ColArgs& a, cudaStream_t s, bool prep) {     \
         if (layout == CL_PLANE) return launch_tri_t<L, CL_PLANE>(a, s, prep);                   \
+        if (layout == CL_SLAB) return launch_tri_t<L, CL_SLAB>(a, s, prep);                     \
+        if (layout == CL_CDR) return launch_tri_t<L, CL_CDR>(a, s, prep);                       \
         if constexpr (L <= kMaxLog2_3d)                                                         \
             if (layout == CL_X3) return launch_tri_t<L, CL_X3>(a, s, prep);                     \
         return cudaErrorInvalidValue;                                                           \
@@ -329,10 +284,7 @@ struct Pp8 {
                                 bool prep);                                                     \
     cudaError_t launch_periodic_L##L(bool row, int mode, const PerArgs& a, cudaStream_t s,      \
                                      bool prep);                                                \
-    cudaError_t launch_transposed_L##L(bool row, int mode, const RowArgs& a, const ColArgs& c,  \
-                                       cudaStream_t s, bool prep);                              \
     cudaError_t launch_cdr_L##L(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep); \
-    cudaError_t launch_mixed_L##L(const RowArgs& ra, const ColArgs& ca, cudaStream_t s, bool prep); \
     cudaError_t launch_tri_L##L(int layout, const ColArgs& a, cudaStream_t s, bool prep);
 
 BS_DECLARE_SIZE(3)

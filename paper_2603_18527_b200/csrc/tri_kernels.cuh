@@ -42,9 +42,6 @@ constexpr int kTriP = 16;  // rows per segment
 #ifndef TRI_REV
 #define TRI_REV 1
 #endif
-#ifndef TRI_PF
-#define TRI_PF 0  // tiles prefetched into L2 ahead of the shared-memory prefetch
-#endif
 
 template <int LOG2N>
 struct TriGeom {
@@ -59,6 +56,8 @@ struct TriGeom {
     // shared-memory row pitches, odd in 16-B units: the CW columns a warp reads at one index
     // land on distinct bank groups (pitch TS = 48 put all 8 on one group: 8-way conflicts)
     static constexpr int TSP = TS + 1;
+    // Neumann (CDR) lines: + p'_15 and the 15 upward pivots of the last segment's system
+    static constexpr int TSN = TS + 16;
     static constexpr int SP = S + 1;
     static constexpr int LPC = S < 32 ? S : 32;          // lanes per column (reduced phase)
     static constexpr int CH = S / LPC;                   // warps per column (reduced phase)
@@ -121,6 +120,45 @@ static __global__ void tri_setup_kernel(const double* __restrict__ lap, const do
     }
 }
 
+// Neumann pivot tables (CL_CDR), one thread per (member, real column q), written into the
+// .x (q even) / .y (q odd) component of the pair's entries.  Layout per pair: [0..14] p_1..p_15,
+// [15] gamma, [16 + s] pr_s (s = 0..S-1, modified first / last diagonals), [16 + S] p'_15,
+// [17 + S + k] q'_{k+1} (k = 0..14).
+static __global__ void tri_setup_neumann_kernel(const double* __restrict__ lapn, const double* __restrict__ sigma0,
+                                                double h2, int batch, int log2n, double2* __restrict__ tab) {
+    const int n = 1 << log2n, S = n / kTriP, TS = 32 + S;
+    const long idx = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    if (idx >= ((long)batch << log2n)) return;
+    const int b = (int)(idx >> log2n), q = (int)(idx & (n - 1));
+    double* t = reinterpret_cast<double*>(tab + ((size_t)b * (n / 2) + q / 2) * TS) + (q & 1);
+    auto at = [&](int k) -> double& { return t[2 * k]; };
+    const double d = 2.0 + h2 * (lapn[q] + sigma0[b]);
+    double p = 1.0 / d, g = p, p14 = 0.0;
+    at(0) = p;
+    for (int k = 1; k < kTriP - 1; ++k) {
+        if (k == kTriP - 2) p14 = p;
+        p = 1.0 / (d - p);
+        g *= p;
+        at(k) = p;
+    }
+    at(15) = g;
+    const double delta = p;
+    double qk = 1.0 / (d - 1.0);
+    at(17 + S) = qk;
+    for (int k = 1; k < kTriP - 1; ++k) {
+        qk = 1.0 / (d - qk);
+        at(17 + S + k) = qk;
+    }
+    const double deltap = qk;
+    at(16 + S) = 1.0 / (d - 1.0 - p14);
+    double pr = 0.0;
+    for (int s = 0; s < S; ++s) {
+        const double D = s == 0 ? d - 1.0 - delta : (s == S - 1 ? d - delta - deltap : d - 2.0 * delta);
+        pr = 1.0 / (D - g * g * pr);
+        at(16 + s) = pr;
+    }
+}
+
 // cp.async (16 B, L2 only) global -> shared
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -133,12 +171,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // element (row r, column c) at e + e / (16 C), e = r C + c -- one pad slot per 16 rows, so the
 // 16-row segments a warp reads (SPW segments x CW columns per load) fall on distinct bank
 // groups for every C.
-template <int LOG2N>
+template <int LOG2N, bool NEU = false>
 struct TriTile {
     using G = TriGeom<LOG2N>;
     static constexpr int TB = G::C * G::N + G::N / kTriP;   // tile buffer (double2)
+    static constexpr int TSX = NEU ? G::TSN : G::TS;        // table entries per line
+    static constexpr int TSXP = TSX + 1;                    // shared pitch (odd)
     static constexpr size_t SMEM =
-        sizeof(double2) * ((size_t)TB + 2 * (size_t)G::C * G::TSP + 3 * (size_t)G::C * G::SP + 2 * (size_t)G::C * G::CH);
+        sizeof(double2) * ((size_t)TB + 2 * (size_t)G::C * TSXP + 3 * (size_t)G::C * G::SP + 2 * (size_t)G::C * G::CH);
     __device__ __forceinline__ static int sidx(int r, int c) {
         const int e = r * G::C + c;
         return e + e / (kTriP * G::C);
@@ -148,20 +188,43 @@ struct TriTile {
 // Line-tile addressing per layout.  CL_PLANE (2-D): tile (b, q0): lines = columns q0..q0+C-1
 // of member b, row stride n, table lines b n + q.  CL_X3 (3-D x-lines): tile (b, y, z0): lines
 // (y, z0..z0+C-1), row (= x) stride n^2, table lines (b n + y) n + z; the padding y-plane is
-// skipped (its lines are the Dirichlet zero).
+// skipped (its lines are the Dirichlet zero).  CL_SLAB (a rank's n x slab_cols column block
+// after the forward all-to-all, batch 1): tile qa0: block columns qa0..qa0+C-1, row stride
+// slab_cols; global lines col0 + qa (2-D) or, with slab3, the (y, z) pairs col0 n + qa (3-D).
+// CL_CDR (config c4, real n x n fields): a line is a pair of adjacent real columns (one 16-B
+// double2 per row, the DCT route's packing), n / 2 pairs per member, row stride n / 2.
 template <int LOG2N, int LAYOUT>
 struct TriLines {
     static constexpr int N = 1 << LOG2N, C = TriGeom<LOG2N>::C, GROUPS = N / C;
     int b, q0, yl;
-    size_t base, tline;
+    size_t base, tline, ls;
     bool skip;
     __device__ __forceinline__ static long count(const ColArgs& a) {
+        if constexpr (LAYOUT == CL_SLAB) return a.slab_cols / C;
+        if constexpr (LAYOUT == CL_CDR) return (long)a.batch * (N / 2 >= C ? N / 2 / C : 1);
         return LAYOUT == CL_X3 ? (long)a.batch * N * GROUPS : (long)a.batch * GROUPS;
     }
-    static constexpr size_t LS = LAYOUT == CL_X3 ? (size_t)N * N : (size_t)N;
-    __device__ __forceinline__ TriLines(long t) {
+    __device__ __forceinline__ TriLines(long t, const ColArgs& a) {
         q0 = (int)(t % GROUPS) * C;
-        if constexpr (LAYOUT == CL_X3) {
+        ls = LAYOUT == CL_X3 ? (size_t)N * N : (size_t)N;
+        if constexpr (LAYOUT == CL_CDR) {
+            constexpr int PG = N / 2 >= C ? N / 2 / C : 1;  // pair groups per member (launch needs n/2 >= C)
+            b = (int)(t / PG);
+            q0 = (int)(t % PG) * C;  // pair index
+            yl = 0;
+            ls = N / 2;
+            base = ((size_t)b << (2 * LOG2N - 1)) + q0;
+            tline = (size_t)b * (N / 2) + q0;
+            skip = false;
+        } else if constexpr (LAYOUT == CL_SLAB) {
+            q0 = (int)t * C;  // block column
+            b = 0;
+            yl = 0;
+            ls = (size_t)a.slab_cols;
+            base = q0;
+            tline = (a.slab3 ? (size_t)a.col0 * N : (size_t)a.col0) + q0;
+            skip = false;
+        } else if constexpr (LAYOUT == CL_X3) {
             const long g = t / GROUPS;  // (b, y)
             b = (int)(g >> LOG2N);
             yl = (int)(g & (N - 1));
@@ -184,15 +247,35 @@ struct TriLines {
 // stores straight from registers.  Load phase mapping: warp w, lane l -> column
 // (w / WPG) CW + l mod CW, segment (w mod WPG) SPW + l / CW.  Reduced phase: thread t ->
 // column t / S, segment t mod S (a column's segments on consecutive lanes).
-template <int LOG2N, int LAYOUT>
+//
+// NEU (config c4, CL_CDR): the real Neumann system of the cell-centred grid, d = 2 + h^2 (a_q +
+// sigma0) with d - 1 in the first and last rows (reflective ghosts; the DCT-II spectrum of
+// symbol.cpp:81-92).  Each line carries two real columns, so every operation is component-wise.
+// X_0 = z_0 is an unknown separator (reduced diagonal d - 1 - delta), and the last segment's
+// interior ends in the modified row (its own last pivot p'_15, upward pivots q'_k, corner
+// delta'; reduced diagonal d - delta - delta').  The reduced pivots of tri_setup_neumann_kernel
+// carry the modified diagonals, so the scans are the Dirichlet ones.
+template <bool NEU>
+__device__ __forceinline__ double2 tmul(double2 a, double2 b) {
+    if constexpr (NEU) return make_double2(a.x * b.x, a.y * b.y);
+    else return cmul(a, b);
+}
+template <bool NEU>
+__device__ __forceinline__ double2 tfma(double2 a, double2 b, double2 c) {
+    if constexpr (NEU) return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
+    else return cfma(a, b, c);
+}
+
+template <int LOG2N, int LAYOUT, bool NEU = false>
 __global__ void __launch_bounds__(TriGeom<LOG2N>::THREADS, TriGeom<LOG2N>::THREADS >= 512 ? 1 : 2)
 tri_kernel(const ColArgs a) {
     using G = TriGeom<LOG2N>;
-    using TT = TriTile<LOG2N>;
+    using TT = TriTile<LOG2N, NEU>;
     using TL = TriLines<LOG2N, LAYOUT>;
-    constexpr int N = G::N, S = G::S, C = G::C, TS = G::TS, TSP = G::TSP, SP = G::SP, LPC = G::LPC,
+    constexpr int N = G::N, S = G::S, C = G::C, TS = TT::TSX, TSP = TT::TSXP, SP = G::SP, LPC = G::LPC,
                   CH = G::CH;
-    static_assert(LAYOUT == CL_PLANE || LAYOUT == CL_X3, "layout");
+    static_assert(LAYOUT == CL_PLANE || LAYOUT == CL_X3 || LAYOUT == CL_SLAB || LAYOUT == CL_CDR, "layout");
+    static_assert(NEU == (LAYOUT == CL_CDR), "Neumann lines are CDR column pairs");
     extern __shared__ double2 sm[];
     double2* tbuf = sm;                    // [TB] tile
     double2* tabs = tbuf + TT::TB;         // [2][C][TSP] pivot tables (double-buffered)
@@ -203,26 +286,19 @@ tri_kernel(const ColArgs a) {
 
     const long ntiles = TL::count(a);
     // reversed order on multi-plane launches: start on the row pass's L2-resident tail
-    const bool rev = TRI_REV && col_reversed<LAYOUT == CL_X3 ? CL_PLANE : LAYOUT>(a);
+    const bool rev = TRI_REV && (LAYOUT == CL_CDR ? a.batch > 1 : col_reversed<LAYOUT == CL_X3 ? CL_PLANE : LAYOUT>(a));
     auto tile_at = [&](long k) { return rev ? ntiles - 1 - k : k; };
     auto issue = [&](long k, int tb) {
-        const TL ln(tile_at(k));
+        const TL ln(tile_at(k), a);
         const double2* src = a.T + ln.base;
 #pragma unroll 4
         for (int e = threadIdx.x; e < C * N; e += G::THREADS)
-            cp_async16(tbuf + e + e / (kTriP * C), src + (size_t)(e / C) * TL::LS + (e % C));
+            cp_async16(tbuf + e + e / (kTriP * C), src + (size_t)(e / C) * ln.ls + (e % C));
         const double2* ts = a.tri + ln.tline * TS;
         double2* td = tabs + tb * C * TSP;
         for (int k2 = threadIdx.x; k2 < C * TS; k2 += G::THREADS) cp_async16(td + (k2 / TS) * TSP + k2 % TS, ts + k2);
     };
 
-    // L2 prefetch of a tile's rows (fire-and-forget: keeps DRAM busy TRI_PF tiles ahead without
-    // holding shared memory or registers)
-    auto prefetch = [&](long k) {
-        const TL ln(tile_at(k));
-        for (int r = threadIdx.x; r < N; r += G::THREADS)
-            prefetch_l2(a.T + ln.base + (size_t)r * TL::LS, C * sizeof(double2));
-    };
 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = (w / G::WPG) * G::CW + lane % G::CW;
@@ -234,12 +310,9 @@ tri_kernel(const ColArgs a) {
     long k = blockIdx.x;
     if (k < ntiles) issue(k, 0);
     cp_async_commit();
-#pragma unroll 1
-    for (int j = 1; j <= TRI_PF; ++j)
-        if (k + j * gridDim.x < ntiles) prefetch(k + j * gridDim.x);
     for (int it = 0; k < ntiles; k += gridDim.x, ++it) {
         // member status: issued before the tile wait so its round trip overlaps it
-        const int stv = a.status ? __ldcg(&a.status[TL(tile_at(k)).b]) : (int)ST_ACTIVE;
+        const int stv = a.status ? __ldcg(&a.status[TL(tile_at(k), a).b]) : (int)ST_ACTIVE;
         cp_async_wait_all();
         __syncthreads();
         double2 v[kTriP];
@@ -248,10 +321,9 @@ tri_kernel(const ColArgs a) {
         __syncthreads();  // tile buffer free: prefetch the next tile under this one's solve
         if (k + gridDim.x < ntiles) issue(k + gridDim.x, (it + 1) & 1);
         cp_async_commit();
-        if (TRI_PF > 0 && k + (TRI_PF + 1) * (long)gridDim.x < ntiles) prefetch(k + (TRI_PF + 1) * (long)gridDim.x);
 
         const long t = tile_at(k);
-        const TL ln(t);
+        const TL ln(t, a);
         if (ln.skip) continue;
         if (a.status) {
             const bool active = stv == ST_ACTIVE;  // read before finalising
@@ -263,17 +335,19 @@ tri_kernel(const ColArgs a) {
 
         // 1. zero-boundary eliminations of the interior, downwards and upwards (shared pivots)
         const double2* pt = tab + c * TSP;
+        // Neumann: the last segment eliminates upwards with its own pivots and ends on p'_15
+        const bool lastseg = NEU && s == S - 1;
+        const double2* pu = lastseg ? pt + 17 + S : pt;
+        const double2 plast = lastseg ? pt[16 + S] : pt[kTriP - 2];
         {
             double2 yd = v[1], yu = v[kTriP - 1];
 #pragma unroll
             for (int j = 1; j < kTriP - 1; ++j) {
-                const double2 p = pt[j - 1];
-                yd = cfma(p, yd, v[1 + j]);
-                yu = cfma(p, yu, v[kTriP - 1 - j]);
+                yd = tfma<NEU>(pt[j - 1], yd, v[1 + j]);
+                yu = tfma<NEU>(NEU ? pu[j - 1] : pt[j - 1], yu, v[kTriP - 1 - j]);
             }
-            const double2 p15 = pt[kTriP - 2];
-            zl[c * SP + s] = cmul(p15, yd);
-            red[c * SP + s] = cfma(p15, yu, v[0]);
+            zl[c * SP + s] = tmul<NEU>(plast, yd);
+            red[c * SP + s] = tfma<NEU>(NEU ? pu[kTriP - 2] : plast, yu, v[0]);
         }
         __syncthreads();
 
@@ -284,15 +358,15 @@ tri_kernel(const ColArgs a) {
             const double2 gam = tr[15];
             const double2 prs = tr[16 + sr];
             const double2 prm = sr > 0 ? tr[16 + sr - 1] : zero;
-            double2 A = cmul(gam, prm);
-            double2 B = sr > 0 ? cadd(red[cr * SP + sr], zl[cr * SP + sr - 1]) : zero;
+            double2 A = tmul<NEU>(gam, prm);
+            double2 B = sr > 0 ? cadd(red[cr * SP + sr], zl[cr * SP + sr - 1]) : (NEU ? red[cr * SP] : zero);
 #pragma unroll
             for (int d = 1; d < LPC; d <<= 1) {
                 const double ax = __shfl_up_sync(0xffffffffu, A.x, d, LPC), ay = __shfl_up_sync(0xffffffffu, A.y, d, LPC);
                 const double bx = __shfl_up_sync(0xffffffffu, B.x, d, LPC), by = __shfl_up_sync(0xffffffffu, B.y, d, LPC);
                 if (ls >= d) {
-                    B = cfma(A, make_double2(bx, by), B);
-                    A = cmul(A, make_double2(ax, ay));
+                    B = tfma<NEU>(A, make_double2(bx, by), B);
+                    A = tmul<NEU>(A, make_double2(ax, ay));
                 }
             }
             double2 y = B;
@@ -303,19 +377,19 @@ tri_kernel(const ColArgs a) {
                 }
                 __syncthreads();
                 double2 yc = zero;  // y at the end of the previous chunk
-                for (int j = 0; j < ch; ++j) yc = cfma(tot[(cr * CH + j) * 2], yc, tot[(cr * CH + j) * 2 + 1]);
-                y = cfma(A, yc, B);
+                for (int j = 0; j < ch; ++j) yc = tfma<NEU>(tot[(cr * CH + j) * 2], yc, tot[(cr * CH + j) * 2 + 1]);
+                y = tfma<NEU>(A, yc, B);
                 __syncthreads();  // tot reused below
             }
-            A = cmul(gam, prs);
-            B = cmul(prs, y);
+            A = tmul<NEU>(gam, prs);
+            B = tmul<NEU>(prs, y);
 #pragma unroll
             for (int d = 1; d < LPC; d <<= 1) {
                 const double ax = __shfl_down_sync(0xffffffffu, A.x, d, LPC), ay = __shfl_down_sync(0xffffffffu, A.y, d, LPC);
                 const double bx = __shfl_down_sync(0xffffffffu, B.x, d, LPC), by = __shfl_down_sync(0xffffffffu, B.y, d, LPC);
                 if (ls + d < LPC) {
-                    B = cfma(A, make_double2(bx, by), B);
-                    A = cmul(A, make_double2(ax, ay));
+                    B = tfma<NEU>(A, make_double2(bx, by), B);
+                    A = tmul<NEU>(A, make_double2(ax, ay));
                 }
             }
             double2 X = B;
@@ -326,8 +400,8 @@ tri_kernel(const ColArgs a) {
                 }
                 __syncthreads();
                 double2 xc = zero;  // X at the start of the next chunk
-                for (int j = CH - 1; j > ch; --j) xc = cfma(tot[(cr * CH + j) * 2], xc, tot[(cr * CH + j) * 2 + 1]);
-                X = cfma(A, xc, B);
+                for (int j = CH - 1; j > ch; --j) xc = tfma<NEU>(tot[(cr * CH + j) * 2], xc, tot[(cr * CH + j) * 2 + 1]);
+                X = tfma<NEU>(A, xc, B);
             }
             xs[cr * SP + sr] = X;
             if (sr == S - 1) xs[cr * SP + S] = zero;
@@ -338,16 +412,31 @@ tri_kernel(const ColArgs a) {
         const double2 xl = xs[c * SP + s], xr = xs[c * SP + s + 1];
         v[1] = cadd(v[1], xl);
 #pragma unroll
-        for (int i = 2; i < kTriP; ++i) v[i] = cfma(pt[i - 2], v[i - 1], v[i]);
-        v[kTriP - 1] = cmul(pt[kTriP - 2], cadd(v[kTriP - 1], xr));
+        for (int i = 2; i < kTriP; ++i) v[i] = tfma<NEU>(pt[i - 2], v[i - 1], v[i]);
+        v[kTriP - 1] = tmul<NEU>(plast, cadd(v[kTriP - 1], xr));  // (Neumann last segment: xr = X_S = 0)
 #pragma unroll
-        for (int i = kTriP - 2; i >= 1; --i) v[i] = cmul(pt[i - 1], cadd(v[i], v[i + 1]));
+        for (int i = kTriP - 2; i >= 1; --i) v[i] = tmul<NEU>(pt[i - 1], cadd(v[i], v[i + 1]));
         v[0] = xl;
-        // Dirichlet zero line (q = 0; 3-D: z = 0): its table is zero, store zeros explicitly
-        const bool zc = ln.q0 + c == 0;
-        double2* col = a.T + ln.base + (size_t)(kTriP * s) * TL::LS + c;
+        // Dirichlet zero line (2-D: q = 0; 3-D: z = 0): its table is zero, store zeros explicitly
+        // (on a slab the zero lines' all-zero tables already give zeros)
+        const bool zc = LAYOUT != CL_SLAB && LAYOUT != CL_CDR && ln.q0 + c == 0;
+        if constexpr (LAYOUT == CL_SLAB) {
+            if (a.xchg_on) {
+                // fused inverse exchange: row j belongs to source rank j >> xchg_log2r; stored into
+                // that rank's t_rows at block xchg_rank (same element map as col_group's st_out)
+                const int rr = a.xchg_log2r;
 #pragma unroll
-        for (int i = 0; i < kTriP; ++i) col[(size_t)i * TL::LS] = zc ? zero : cscale(v[i], sc);
+                for (int i = 0; i < kTriP; ++i) {
+                    const int j = kTriP * s + i;
+                    a.xchg[j >> rr][(((size_t)a.xchg_rank << rr) + (size_t)(j & ((1 << rr) - 1))) * ln.ls + ln.q0 + c] =
+                        cscale(v[i], sc);
+                }
+                continue;
+            }
+        }
+        double2* col = a.T + ln.base + (size_t)(kTriP * s) * ln.ls + c;
+#pragma unroll
+        for (int i = 0; i < kTriP; ++i) col[(size_t)i * ln.ls] = zc ? zero : cscale(v[i], sc);
     }
     cp_async_wait_all();
 }

@@ -72,8 +72,8 @@ class SlabPart:
                                             device, C.byref(h)))
         self._h = h
         # launch on the framework's current stream: the collectives are ordered with the kernels
-        stream = torch.cuda.current_stream(device).cuda_stream
-        _check(self._lib.bp_problem_set_stream(self._h, C.c_void_p(stream)))
+        self.stream = torch.cuda.current_stream(device)
+        _check(self._lib.bp_problem_set_stream(self._h, C.c_void_p(self.stream.cuda_stream)))
         v = N.SlabView()
         _check(self._lib.bp_slab_view(self._h, C.byref(v)))
         self.rows, self.row0, self.n = v.rows, v.row0, v.n
@@ -94,6 +94,11 @@ class SlabPart:
 
     def __del__(self):
         self.close()
+
+    def set_stream(self, stream) -> None:
+        """Launch on `stream` (a torch.cuda.Stream) from now on (graph capture, run_slab)."""
+        self.stream = stream
+        _check(self._lib.bp_problem_set_stream(self._h, C.c_void_p(stream.cuda_stream)))
 
     def _refresh_views(self):
         v = N.SlabView()
@@ -260,11 +265,21 @@ class SlabResult:
     sweeps_launched: int
 
 
+def _graphable(parts) -> bool:
+    return all(isinstance(p, SlabPart) for p in parts)
+
+
 def run_slab(parts, comm, cmap, f, config: IterationConfig | None = None, u0=None,
-             stage_fields: bool = True, fetch: bool = True) -> SlabResult:
+             stage_fields: bool = True, fetch: bool = True, graph: bool = True) -> SlabResult:
     """bp::run (iterate.cpp:88-153) on a slab-decomposed grid; every rank gets the same trace.
     stage_fields=False: f / u0 are already resident from an earlier call (bench: device-resident
-    value); fetch=False: no result download (u and trace are None)."""
+    value); fetch=False: no result download (u and trace are None).
+    graph=True (GPU parts): the sweep loop runs as a CUDA graph of POLL_SWEEPS sweeps -- halo
+    exchange, SWEEP, the entry all-reduce, FINALIZE and the column pass with its two transposes
+    (NCCL collectives and the kernels of the C ABI, captured together on one stream) -- replayed
+    until every member terminated: no per-sweep host issue on the critical path.  A member that
+    terminates inside a replay stops there (its kernels exit on the device status), exactly as
+    the single-device graph path."""
     config = config or IterationConfig()
     cmap = cmap if cmap is not None else ScalarMap(1.0)
 
@@ -297,7 +312,8 @@ def run_slab(parts, comm, cmap, f, config: IterationConfig | None = None, u0=Non
         p.stage(FWD_BORN)
     col_pass()
     launched = 0
-    for k in range(config.max_iters + 1):
+
+    def sweep(k):
         comm.halo(parts, k & 1)
         for p in parts:
             p.stage(SWEEP, cmap=cmap)
@@ -305,10 +321,47 @@ def run_slab(parts, comm, cmap, f, config: IterationConfig | None = None, u0=Non
         for p in parts:
             p.stage(FINALIZE)
         col_pass()
-        launched += 1
-        if (k + 1) % POLL_SWEEPS == 0 or k == config.max_iters:
-            if parts[0].active() == 0:
-                break
+
+    if graph and _graphable(parts):
+        import torch
+        prev = [p.stream for p in parts]
+        # one capture per (parts, comm, map, config): later calls replay it (capture and
+        # instantiation cost milliseconds -- a bench step is ~100 ms)
+        key = (id(comm), type(cmap).__name__, getattr(cmap, "gamma", None), config.format, config.rtol,
+               config.max_iters)
+        cache = parts[0].__dict__.setdefault("_graphs", {})
+        if key not in cache:
+            cap = torch.cuda.Stream(device=parts[0].device)
+            cap.wait_stream(prev[0])
+            for p in parts:
+                p.set_stream(cap)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                for k in range(POLL_SWEEPS):  # buffer parity k & 1 repeats every replay
+                    sweep(k)
+            cache[key] = (g, cap)
+        g, cap = cache[key]
+        cap.wait_stream(prev[0])
+        for p in parts:
+            p.set_stream(cap)
+        try:
+            while launched < config.max_iters + 1:
+                with torch.cuda.stream(cap):
+                    g.replay()
+                launched += POLL_SWEEPS
+                if parts[0].active() == 0:  # synchronises the capture stream
+                    break
+        finally:
+            for p, st in zip(parts, prev):
+                st.wait_stream(cap)
+                p.set_stream(st)
+    else:
+        for k in range(config.max_iters + 1):
+            sweep(k)
+            launched += 1
+            if (k + 1) % POLL_SWEEPS == 0 or k == config.max_iters:
+                if parts[0].active() == 0:
+                    break
     if not fetch:
         return SlabResult(None, None, launched)
     u = np.zeros(parts[0].shape, np.complex128)

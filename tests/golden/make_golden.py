@@ -190,6 +190,53 @@ def dct_golden():
     np.savez_compressed(os.path.join(HERE, "ref_dct.npz"), **out)
 
 
+def generic_golden():
+    """ref_generic.npz -- any-shape Dirichlet grids (rectangular, sides not 2^k - 1, lx != ly):
+    the reference's own operators (oracle/_ref, FFTW-API shim) and bp::run trajectories with the
+    scalar and pointwise maps (NPBS) and the Direct format, for the GPU any-shape path
+    (tests/test_gpu_generic.py).  Media: c = 1 + 0.3 g (g smoothed seeded noise, unit max-abs),
+    k = omega / c, 10 points per wavelength in x, absorption 5 %, k0 = mean k,
+    eta = 1.01 max|k^2 - k0^2|, a Gaussian source at the grid centre."""
+    from scipy.ndimage import gaussian_filter
+    rng = np.random.default_rng(2026)
+    out = {}
+    # a, b, d: hx == hy (ly = lx (ny+1)/(nx+1)): A = five_point - k2 and L_ref - V agree and the
+    # solves converge; c: hx != hy -- five_point takes hx^2 only (kernels.cpp:56-69) while the
+    # symbol uses both spacings, so the reference's own run stagnates; the GPU must too
+    for tag, (nx, ny, lx, ly) in {"a": (16, 12, 1.0, 13 / 17), "b": (13, 21, 1.0, 22 / 14),
+                                  "c": (100, 37, 2.0, 1.0), "d": (96, 127, 1.0, 128 / 97)}.items():
+        hx, hy = lx / (nx + 1), ly / (ny + 1)
+        g = gaussian_filter(rng.standard_normal((nx, ny)), 2.0)
+        g /= np.abs(g).max()
+        kk = 2 * np.pi / (10.0 * hx) / (1.0 + 0.2 * g)
+        k2 = (kk * kk) * (1.0 + 0.05j)
+        k0 = float(kk.mean())
+        eta = float(1.01 * np.abs(k2 - k0 * k0).max())
+        X, Y = np.meshgrid((np.arange(nx) + 1) * hx, (np.arange(ny) + 1) * hy, indexing="ij")
+        f = np.exp(-((X - lx / 2) ** 2 + (Y - ly / 2) ** 2) / (2 * (3 * hx) ** 2)) + 0j
+        x = rng.standard_normal((nx, ny)) + 1j * rng.standard_normal((nx, ny))
+        r = ReferenceProblem(k2, k0, eta, lx, ly)
+        out.update({f"{tag}_shape": np.array([nx, ny]), f"{tag}_l": np.array([lx, ly]), f"{tag}_k2": k2,
+                    f"{tag}_f": f, f"{tag}_k0": k0, f"{tag}_eta": eta, f"{tag}_x": x,
+                    f"{tag}_G": r.apply_G(x), f"{tag}_A": r.apply_A(x), f"{tag}_L": r.apply_Lref(x),
+                    f"{tag}_V": r.apply_V(x), f"{tag}_born": r.born_residual(x, f),
+                    f"{tag}_res": r.residual(x, f),
+                    f"{tag}_fwd": (sf.dstn(x.real, type=1) + 1j * sf.dstn(x.imag, type=1)) * 0.25,
+                    f"{tag}_inv": (sf.dstn(x.real, type=1) + 1j * sf.dstn(x.imag, type=1)) / ((nx + 1) * (ny + 1))})
+        for name, kw in {"pw": dict(map_kind=MAP_POINTWISE), "sc": dict(map_kind=MAP_SCALAR, gamma=1.0),
+                         "dir": dict(map_kind=MAP_POINTWISE, fmt=FMT_DIRECT)}.items():
+            u, l2, rt, info = Reference.run_batch(k2[None], np.array([k0]), np.array([eta]), f[None],
+                                                  rtol=1e-8, max_iters=3000, lx=lx, ly=ly, **kw)
+            it, term = info[0]
+            out[f"{tag}_{name}_u"] = u[0]
+            out[f"{tag}_{name}_l2"] = l2[0, :it + 1]
+            out[f"{tag}_{name}_reta"] = rt[0, :it + 1]
+            out[f"{tag}_{name}_iters"] = it
+            out[f"{tag}_{name}_term"] = term
+            print("generic", tag, name, it, term)
+    np.savez_compressed(os.path.join(HERE, "ref_generic.npz"), **out)
+
+
 def io_golden():
     d = os.path.join(HERE, "ref_io")
     os.makedirs(d, exist_ok=True)
@@ -208,8 +255,8 @@ def io_golden():
 
 if __name__ == "__main__":
     Reference.set_mode("serial")
-    if sys.argv[1:] in (["dct"], ["io"], ["round2"]):
-        {"dct": dct_golden, "io": io_golden, "round2": round2_golden}[sys.argv[1]]()
+    if sys.argv[1:] in (["dct"], ["io"], ["round2"], ["generic"]):
+        {"dct": dct_golden, "io": io_golden, "round2": round2_golden, "generic": generic_golden}[sys.argv[1]]()
         sys.exit(0)
     io_golden()
     dct_golden()
@@ -221,4 +268,5 @@ if __name__ == "__main__":
     run_golden()
     periodic_golden()
     round2_golden()
+    generic_golden()
     print("golden fixtures written to", HERE)

@@ -57,7 +57,10 @@ def test_cdr_operators_match_oracle(gpu, n):
                "G": o.apply_G(ub), "born": o.born_residual(ub, fb), "res": o.residual(ub, fb)}
         for k, e in exp.items():
             assert np.abs(e.imag).max() < 1e-12 * np.abs(e.real).max()
-            assert rel(out[k][b], e.real) < OP_TOL, (k, b)
+            # G: the tridiagonal column pass's forward error scales with the column system's
+            # conditioning (test_gpu_tri.cdr_tol); the DCT route (BP_COL_DST=1) holds OP_TOL
+            tol = max(OP_TOL, 1e-15 * (4.0 * n * n + s0[b]) / s0[b]) if k in ("G", "born") else OP_TOL
+            assert rel(out[k][b], e.real) < tol, (k, b)
 
 
 @pytest.mark.parametrize("n", [16, 64])

@@ -1,0 +1,78 @@
+"""Repeat-run determinism of every kernel family (compute-sanitizer is closed on the GPU pool:
+the runner refuses it).  Shared-memory races, reads of uninitialised shared or global memory
+and barrier mistakes show up as run-to-run differences; every reduction here has a fixed order,
+so three runs of the same solve must agree BIT FOR BIT -- including on the tridiagonal column
+pass's cp.async double buffer, the named-barrier engines and the slab exchanges.  Small grids
+(many CTAs per SM, different co-scheduling each run) and the production sizes' kernels
+(n = 512 / 1024 / 4096 instances) are both exercised."""
+import numpy as np
+import pytest
+
+import paper_2603_18527_b200 as bs
+from paper_2603_18527_b200.slab import LocalComm, SlabPart, run_slab
+
+pytestmark = pytest.mark.gpu
+
+
+def same3(fn):
+    outs = [fn() for _ in range(3)]
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
+
+
+def inst(n, batch=2, dim=2, seed=0):
+    return bs.make_instances(bs.InstanceSpec(n=n, ppw=8.0, contrast=0.5, sigma_cells=2.0, dim=dim,
+                                             seed=seed), 0, batch)
+
+
+@pytest.mark.parametrize("n", [64, 512, 4096])
+@pytest.mark.parametrize("route", ["tri", "dst"])
+def test_dirichlet_deterministic(gpu, monkeypatch, n, route):
+    monkeypatch.setenv("BP_COL_DST", "1" if route == "dst" else "0")
+    k2, f, k0, eta = inst(n, batch=2 if n < 4096 else 1)
+    cfg = bs.IterationConfig(rtol=1e-30, max_iters=12)
+
+    def go():
+        with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+            outs = []
+            for cmap in (bs.PointwiseMap(), bs.OptimalScalarMap("reta")):
+                r = bs.run(p, cmap, f, cfg)
+                outs += [r.u, r.traces[0].res_l2_rel]
+            return outs
+    same3(go)
+
+
+def test_3d_periodic_cdr_deterministic(gpu):
+    k3, f3, k03, eta3 = inst(64, batch=1, dim=3)
+    bx, by, sg, s0, fc = bs.make_cdr_instances(bs.CdrSpec(n=1024), 0, 2)
+    rng = np.random.default_rng(1)
+    k2p = 400.0 * (1.0 + 0.2 * rng.standard_normal((2, 256, 256))) * (1.0 + 0.1j)
+    etap = 1.01 * np.abs(k2p - 400.0).reshape(2, -1).max(axis=1)
+    fp = rng.standard_normal((2, 256, 256)) + 0j
+    cfg = bs.IterationConfig(rtol=1e-30, max_iters=10)
+
+    def go():
+        with bs.HelmholtzDirichlet(k3, k03, eta3, dim=3) as p:
+            a = bs.run(p, bs.PointwiseMap(), f3, cfg).u
+        with bs.CdrNeumann(bx, by, sg, s0) as p:
+            b = bs.run(p, bs.ScalarMap(1.0), fc, cfg).u
+        with bs.HelmholtzPeriodic(k2p, np.full(2, 20.0), etap) as p:
+            c = bs.run(p, bs.OptimalScalarMap("euclidean"), fp, cfg).u
+        return [a, b, c]
+    same3(go)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_slab_deterministic(gpu, fused):
+    k2, f, k0, eta = inst(512, batch=1)
+    cfg = bs.IterationConfig(rtol=1e-30, max_iters=20)
+
+    def go():
+        parts = [SlabPart(k2[0], float(k0[0]), float(eta[0]), r, 4) for r in range(4)]
+        try:
+            return [run_slab(parts, LocalComm(fused=fused), bs.PointwiseMap(), f[0], cfg).u]
+        finally:
+            for p in parts:
+                p.close()
+    same3(go)

@@ -62,7 +62,9 @@ def test_transforms_match_scipy_goldens(gpu):
 
 
 def test_unsupported_shapes_raise(gpu):
-    for shape in [(16, 12), (3, 5), (14, 14), (1022, 1022), (8191, 8191)]:
+    # any 2-D shape up to 4095 per side runs (power-of-two kernels or the any-shape path,
+    # test_gpu_generic.py); longer sides are not implemented
+    for shape in [(4096, 4096), (8191, 8191), (5000, 12)]:
         with pytest.raises(NotImplementedError):
             bs.HelmholtzDirichlet(np.ones(shape, np.complex128), 1.0, 1.0)
 
@@ -414,39 +416,20 @@ def test_config2_grid_first_sweeps(gpu):
     assert_run_parity(res.trace, res.u, ref)
 
 
-def test_transposed_handoff_matches(gpu, monkeypatch):
-    """The opt-in transposed row->column handoff (BP_TRANSPOSED=1) gives the same iterates."""
+def test_column_routes_match(gpu, monkeypatch):
+    """The Green column pass as a tridiagonal x-solve (default) and as the transform pair
+    (BP_COL_DST=1) give the same iterates for every correction map, both against the oracle."""
     k2, f, k0, eta = instance(128, batch=2, ppw=10.0, contrast=0.3, seed=9)
     cfg = bs.IterationConfig(rtol=1e-9, max_iters=400)
-    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
-        base = bs.run(p, bs.PointwiseMap(), f, cfg)
-    monkeypatch.setenv("BP_TRANSPOSED", "1")
-    for cmap in (bs.PointwiseMap(), bs.OptimalScalarMap("euclidean"), _fd_map(128)):
-        with bs.HelmholtzDirichlet(k2, k0, eta) as p:
-            tr = bs.run(p, cmap, f, cfg)
+    for cmap in (bs.PointwiseMap(), bs.OptimalScalarMap("euclidean"), bs.OptimalScalarMap("reta"),
+                 _fd_map(128)):
+        runs = []
+        for route in ("0", "1"):
+            monkeypatch.setenv("BP_COL_DST", route)
+            with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+                runs.append(bs.run(p, cmap, f, cfg))
         ref = _oracle_run(k2[0], f[0], k0[0], eta[0], cmap, 1e-9, 400)
-        assert_run_parity(tr.traces[0], tr.u[0], ref)
-        if isinstance(cmap, bs.PointwiseMap):
-            assert rel(tr.u, base.u) < 1e-13
-
-
-@pytest.mark.parametrize("n", [512, 1024])
-def test_mixed_pipeline_matches(gpu, monkeypatch, n):
-    """The opt-in mixed pipeline (BP_MIXED=1: one launch = rows of one half-batch + columns of
-    the other) gives the same members, traces and termination sweeps; an odd batch
-    makes the halves unequal (1 + 2 members)."""
-    k2, f, k0, eta = instance(n, batch=3, ppw=60.0, contrast=0.1, seed=11)
-    f[2] *= -1e2
-    cfg = bs.IterationConfig(rtol=1e-5, max_iters=300)
-    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
-        base = bs.run(p, bs.PointwiseMap(), f, cfg)
-    monkeypatch.setenv("BP_MIXED", "1")
-    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
-        mixed = bs.run(p, bs.PointwiseMap(), f, cfg)
-    for b in range(3):
-        assert mixed.traces[b].iters == base.traces[b].iters
-        assert mixed.traces[b].terminated == base.traces[b].terminated
-        # same arithmetic; the mixed kernel is a separate compilation (FMA contraction may
-        # differ), so roundoff-level agreement rather than bit identity
-        assert rel(mixed.u[b], base.u[b]) < 1e-12
-        assert np.allclose(mixed.traces[b].res_l2_rel, base.traces[b].res_l2_rel, rtol=1e-10, atol=0)
+        for r in runs:
+            assert_run_parity(r.traces[0], r.u[0], ref)
+        assert runs[0].traces[1].iters == runs[1].traces[1].iters
+        assert rel(runs[0].u, runs[1].u) < FIELD_TOL  # (the random FourierDiag map diverges)

@@ -106,3 +106,61 @@ def test_set_medium_rebuilds_tri_tables(gpu):
     with handle(k2a, k0a, etaa, False) as p, handle(k2b, k0b, etab, False) as q:
         p.set_medium(k2b, k0b, etab)
         assert np.array_equal(p.apply_G(x), q.apply_G(x))
+
+
+def cdr_tol(n, s0):
+    """Operator tolerance of the Neumann elimination: its forward error grows with the
+    conditioning of the q = 0 column system, kappa = (4 n^2 + sigma0) / sigma0 (h^2 units), while
+    the DCT route's orthogonal transforms do not (measured: 2.4e-13 at n = 256, 4.1e-12 at
+    n = 1024 with sigma0 ~ 25).  Iterates stay within the north_star's 1e-10 (test_gpu_cdr full
+    solves); BP_COL_DST=1 selects the DCT route."""
+    kappa = (4.0 * n * n + float(np.min(s0))) / float(np.min(s0))
+    return max(OP_TOL, 1e-15 * kappa)
+
+
+@pytest.mark.parametrize("n", [128, 256, 1024])
+def test_cdr_green_tri_matches_dct_route(gpu, n):
+    """Config c4's Neumann column pass as the real tridiagonal x-solve (modified first and last
+    rows) against the DCT-II / DCT-III route and the oracle (tolerance: cdr_tol)."""
+    bx, by, sigma, s0, f = bs.make_cdr_instances(bs.CdrSpec(n=n, seed=5), 0, 2)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(bx.shape)
+    old = os.environ.get("BP_COL_DST")
+    got = []
+    try:
+        for route in ("1", "0"):
+            os.environ["BP_COL_DST"] = route
+            with bs.CdrNeumann(bx, by, sigma, s0) as p:
+                got.append(p.apply_G(x))
+    finally:
+        if old is None:
+            os.environ.pop("BP_COL_DST", None)
+        else:
+            os.environ["BP_COL_DST"] = old
+    tol = cdr_tol(n, s0)
+    for b in range(2):
+        assert rel(got[1][b], got[0][b]) < tol, (b, rel(got[1][b], got[0][b]), tol)
+    if n <= 256:
+        o = OracleProblem.cdr(bx[0], by[0], sigma[0], float(s0[0]))
+        assert rel(got[1][0], o.apply_G(x[0] + 0j).real) < tol
+
+
+def test_cdr_run_tri_matches_dct_route(gpu):
+    bx, by, sigma, s0, f = bs.make_cdr_instances(bs.CdrSpec(n=256, seed=3), 0, 2)
+    cfg = bs.IterationConfig(rtol=1e-8, max_iters=400)
+    old = os.environ.get("BP_COL_DST")
+    res = []
+    try:
+        for route in ("1", "0"):
+            os.environ["BP_COL_DST"] = route
+            with bs.CdrNeumann(bx, by, sigma, s0) as p:
+                res.append(bs.run(p, bs.ScalarMap(1.0), f, cfg))
+    finally:
+        if old is None:
+            os.environ.pop("BP_COL_DST", None)
+        else:
+            os.environ["BP_COL_DST"] = old
+    for b in range(2):
+        assert res[0].traces[b].iters == res[1].traces[b].iters
+        assert res[0].traces[b].terminated == res[1].traces[b].terminated
+        assert rel(res[1].u[b], res[0].u[b]) < FIELD_TOL
