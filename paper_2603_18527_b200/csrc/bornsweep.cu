@@ -241,6 +241,10 @@ cudaError_t launch_tri(int log2n, int layout, const ColArgs& a, cudaStream_t s, 
     BS_SIZE_CASES(launch_tri_L, layout, a, s, prep)
 }
 
+cudaError_t launch_cluster(int log2n, const ClArgs& a, int batch, cudaStream_t s, bool prep = false) {
+    BS_SIZE_CASES(launch_cluster_L, a, batch, s, prep)
+}
+
 cudaError_t launch_row(int log2n, int dim, int mode, const RowArgs& a, cudaStream_t s) {
     return launch_row_pp(log2n, points_per_thread(log2n), dim, mode, a, s);
 }
@@ -869,6 +873,22 @@ int sweep_once(bp_problem* p, const SweepPlan& plan, const RowArgs& a, const Col
     return BP_OK;
 }
 
+// whole-solve cluster kernel applies: 2-D Dirichlet n = 64 / 128 with the tridiagonal tables,
+// the fused scalar / pointwise sweep, and a device that runs the cluster shape
+bool cluster_enabled(const bp_problem* p, const SweepPlan& plan) {
+    static const bool env_off = [] {
+        const char* e = std::getenv("BP_CLUSTER");
+        return e && e[0] == '0';
+    }();
+    if (env_off || p->dim != 2 || p->periodic || p->cdr || p->generic || p->slab_log2 || !p->tri) return false;
+    if (p->log2n != 6 && p->log2n != 7) return false;
+    if (!(plan.n == 2 && plan.row[0] && (plan.mode[0] == R_SWEEP || plan.mode[0] == R_SWEEP_D))) return false;
+    static int ok[2] = {-1, -1};  // per size: the cluster shape launches on this device
+    int& k = ok[p->log2n - 6];
+    if (k < 0) k = launch_cluster(p->log2n, ClArgs{}, 1, nullptr, true) == cudaSuccess ? 1 : 0;
+    return k == 1;
+}
+
 // The driver: bp::run over the batch.  f_dev/u0_dev padded device fields already staged.
 int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool have_u0,
              double* snapshots, int n_snap) {
@@ -927,6 +947,23 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         c.fin_lsh = (p->dim - 1) * p->log2n;
         c.fin_step = row_lines_per_cta(p->log2n, points_per_thread(p->log2n));
         c.ctl = a.ctl;
+    }
+
+    // n = 64 / 128 grids with the scalar / pointwise sweep: the whole solve as ONE cluster kernel
+    // (cluster_kernels.cuh), the grid resident in the cluster's distributed shared memory
+    // (BP_CLUSTER=0 keeps the two-launch graph loop)
+    if (cluster_enabled(p, plan) && !(snapshots && n_snap > 0) && !p->timing) {
+        ClArgs ca{};
+        ca.row = a;
+        ca.row.defer_final = 0;
+        ca.col = c;
+        const double h = p->grid.lx / p->n;
+        ca.h2 = h * h;
+        ca.direct = cfg->format == BP_FMT_DIRECT;
+        CU(launch_cluster(p->log2n, ca, B, p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+        p->stat_launches = 8 + 2 + 3 + (have_u0 ? 1 : 0) + 1;
+        return BP_OK;
     }
 
     // kernels launched so far in this run: pack f (+ pack u0), 2x norms (2 each), Green

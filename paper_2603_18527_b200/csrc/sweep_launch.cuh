@@ -6,6 +6,7 @@
 #include "periodic_kernels.cuh"
 #include "sweep_kernels.cuh"
 #include "tri_kernels.cuh"
+#include "cluster_kernels.cuh"
 
 namespace bs {
 
@@ -134,6 +135,37 @@ cudaError_t launch_tri_t(const ColArgs& a, cudaStream_t s, bool prepare) {
         if (grid == 0) return cudaSuccess;
         k<<<grid, TG::THREADS, TT::SMEM, s>>>(a);
         return cudaGetLastError();
+    }
+    return cudaErrorInvalidValue;
+}
+
+// ---- whole-solve cluster kernel (n = 64 / 128: the grid in one cluster's shared memory)
+template <int L>
+cudaError_t launch_cluster_t(const ClArgs& a, int batch, cudaStream_t s, bool prepare) {
+    if constexpr (L == 6 || L == 7) {
+        using CG = ClGeom<L>;
+        auto k = cluster_solve_kernel<L>;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(batch * CG::CL));
+        cfg.blockDim = dim3(CG::THREADS);
+        cfg.dynamicSmemBytes = CG::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CG::CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (prepare) {  // attributes + can this device co-schedule the cluster at all
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CG::SMEM);
+            if (e == cudaSuccess && CG::CL > 8)
+                e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            int clusters = 0;
+            if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&clusters, k, &cfg);
+            return e != cudaSuccess ? e : (clusters > 0 ? cudaSuccess : cudaErrorInvalidConfiguration);
+        }
+        return cudaLaunchKernelEx(&cfg, k, a);
     }
     return cudaErrorInvalidValue;
 }
@@ -268,6 +300,9 @@ struct Pp8 {
     cudaError_t launch_cdr_L##L(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep) { \
         return launch_cdr_p<L>(row, mode, a, s, prep);                                          \
     }                                                                                           \
+    cudaError_t launch_cluster_L##L(const ClArgs& a, int batch, cudaStream_t s, bool prep) {   \
+        return launch_cluster_t<L>(a, batch, s, prep);                                          \
+    }                                                                                           \
     cudaError_t launch_tri_L##L(int layout, const ColArgs& a, cudaStream_t s, bool prep) {     \
         if (layout == CL_PLANE) return launch_tri_t<L, CL_PLANE>(a, s, prep);                   \
         if (layout == CL_SLAB) return launch_tri_t<L, CL_SLAB>(a, s, prep);                     \
@@ -285,7 +320,8 @@ struct Pp8 {
     cudaError_t launch_periodic_L##L(bool row, int mode, const PerArgs& a, cudaStream_t s,      \
                                      bool prep);                                                \
     cudaError_t launch_cdr_L##L(bool row, int mode, const CdrArgs& a, cudaStream_t s, bool prep); \
-    cudaError_t launch_tri_L##L(int layout, const ColArgs& a, cudaStream_t s, bool prep);
+    cudaError_t launch_tri_L##L(int layout, const ColArgs& a, cudaStream_t s, bool prep);       \
+    cudaError_t launch_cluster_L##L(const ClArgs& a, int batch, cudaStream_t s, bool prep);
 
 BS_DECLARE_SIZE(3)
 BS_DECLARE_SIZE(4)
