@@ -15,8 +15,11 @@
  *   grid     DirichletInterior, h = lx/(nx+1) (proj/include/bp/grid.hpp:12-24).
  *   DST-I    forward = plain sine sum, inverse carries 4/((nx+1)(ny+1))
  *            (proj/include/bp/transforms.hpp:15-24).
- * Supported on the GPU: square grids with nx+1 = ny+1 = 2^k, 8 <= 2^k <= 4096
- * (other shapes return BP_ENOTSUP; the reference accepts any size through FFTW).
+ * Supported on the GPU (2-D Dirichlet): any nx, ny in [2, 4095] and any lx, ly -- square
+ * grids with nx+1 = ny+1 = 2^k (8 <= 2^k <= 4096) and lx == ly run the fused kernels, every
+ * other shape the any-shape path (radix-2 / Bluestein line transforms; scalar and pointwise
+ * maps); the reference accepts any size through FFTW (proj/src/transforms.cpp:39-65).
+ * 3-D, periodic and CDR handles: power-of-two sides as stated at their constructors.
  *
  * Errors: every function returns a status; nothing throws across the boundary.
  *   BP_EINVAL   <-> std::invalid_argument (e.g. proj/src/problem.cpp:16, iterate.cpp:90-94,
@@ -121,7 +124,8 @@ typedef struct bp_problem bp_problem;
 const char* bp_last_error(void);
 int bp_abi_version(void);
 
-/* Dirichlet five-point Helmholtz batch: A = L_D - k2, L_ref = L_D - (k0^2 + i eta),
+/* Dirichlet five-point Helmholtz batch (grid->bc = BP_BC_DIRICHLET; BP_BC_PERIODIC gives the
+ * reference's periodic pseudospectral HelmholtzProblem, nx = ny = 2^k): A = L_D - k2, L_ref = L_D - (k0^2 + i eta),
  * V = k2 - (k0^2 + i eta)   (HelmholtzProblem ctor, proj/src/helmholtz.cpp:11-25, with the
  * DirichletInterior five-point pattern of proj/src/newton_problem.cpp:17-44).
  * k2: batch*nx*ny complex (sponge damping already folded in, like make_helmholtz);
