@@ -262,8 +262,10 @@ class HelmholtzDirichlet:
 
 class HelmholtzPeriodic(HelmholtzDirichlet):
     """The reference's own family: bp::HelmholtzProblem (helmholtz.cpp:11-53), periodic
-    pseudospectral, A = F^-1(|xi|^2 F u) - k2 u, FFT basis; nx = ny = 2^k nodes, h = lx/nx.
-    On the GPU the iterate is carried in Fourier space (maps: ScalarMap, FourierDiagMap)."""
+    pseudospectral, A = F^-1(|xi|^2 F u) - k2 u, FFT basis, h = lx/nx.  nx = ny = 2^k with
+    lx == ly: fused FFT kernels, iterate carried in Fourier space (maps: ScalarMap,
+    OptimalScalarMap, FourierDiagMap); any other nx x ny <= 4096: the any-shape path
+    (radix-2 / Bluestein DFT lines, ScalarMap)."""
 
     BC = BC_PERIODIC
 

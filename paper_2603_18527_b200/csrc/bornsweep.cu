@@ -370,6 +370,7 @@ struct bp_problem {
     // any-shape 2-D Dirichlet handle (nx, ny not of the form 2^k - 1, or nx != ny): dense nx x ny
     // layout, line transforms by radix-2 / Bluestein (generic_kernels.cuh)
     bool generic = false;
+    bool gper = false;   // any-shape periodic family (DFT lines, |xi|^2 symbol)
     int gnx = 0, gny = 0;
     GLinePlan gplan_x, gplan_y;
     double *gax = nullptr, *gay = nullptr, *gpart = nullptr;
@@ -708,12 +709,15 @@ GenArgs gen_args(const bp_problem* p) {
     g.eta = p->eta;
     g.ax = p->gax;
     g.ay = p->gay;
-    g.gscale = 4.0 / ((double)(p->gnx + 1) * (p->gny + 1));
+    // inverse normalisation: DST-I 4/((nx+1)(ny+1)); DFT 1/(nx ny) (transforms.cpp:96-103)
+    g.gscale = p->gper ? 1.0 / ((double)p->gnx * p->gny) : 4.0 / ((double)(p->gnx + 1) * (p->gny + 1));
     return g;
 }
 
-// DST-I (mode GL_DST) of every y-line (axis 0) or x-line (axis 1) of the dense batch
-int gen_lines(bp_problem* p, int axis, const double2* in, double2* out, double scale) {
+// line transform of every y-line (axis 0) or x-line (axis 1) of the dense batch: DST-I
+// (Dirichlet handles) or the unnormalised forward / backward DFT (periodic handles, inverse)
+int gen_lines(bp_problem* p, int axis, const double2* in, double2* out, double scale, bool inverse = false,
+              const int* status = nullptr) {
     const GLinePlan& pl = axis == 0 ? p->gplan_y : p->gplan_x;
     GLineArgs a{};
     a.in = in;
@@ -738,30 +742,38 @@ int gen_lines(bp_problem* p, int axis, const double2* in, double2* out, double s
     a.filt = pl.filt;
     a.tw = pl.tw;
     a.scale = scale;
+    a.status = status;
     const int smem = (int)(sizeof(double2) * (pl.n + std::max(pl.L, pl.n / 2 + 256)));
     static bool attr = [] {
-        cudaFuncSetAttribute(gline_kernel<GL_DST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        for (auto k : {gline_kernel<GL_DST>, gline_kernel<GL_DFT>, gline_kernel<GL_IDFT>})
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         return true;
     }();
     (void)attr;
-    gline_kernel<GL_DST><<<(unsigned)a.lines, 256, smem, p->stream>>>(a);
+    if (!p->gper) gline_kernel<GL_DST><<<(unsigned)a.lines, 256, smem, p->stream>>>(a);
+    else if (inverse) gline_kernel<GL_IDFT><<<(unsigned)a.lines, 256, smem, p->stream>>>(a);
+    else gline_kernel<GL_DFT><<<(unsigned)a.lines, 256, smem, p->stream>>>(a);
     CU(cudaGetLastError());
     return BP_OK;
 }
 
-// 2-D DST-I (plain sine sums, transforms.hpp:18-20) of a dense batch, x scale
-int gen_dst2(bp_problem* p, const double2* in, double2* out, double scale) {
-    if (int rc = gen_lines(p, 0, in, out, 1.0)) return rc;
-    return gen_lines(p, 1, out, out, scale);
+// 2-D DST-I (plain sine sums, transforms.hpp:18-20) of a dense batch, x scale; periodic handles:
+// the unnormalised 2-D DFT (inverse: backward DFT), x scale
+int gen_dst2(bp_problem* p, const double2* in, double2* out, double scale, bool inverse = false,
+             const int* status = nullptr) {
+    if (int rc = gen_lines(p, 0, in, out, 1.0, inverse, status)) return rc;
+    return gen_lines(p, 1, out, out, scale, inverse, status);
 }
 
 // G (divide) / L_ref (multiply): S^-1 diag(lambda^-+1) S with S^-1 = 4/((nx+1)(ny+1)) S
-int gen_spectral(bp_problem* p, bool divide, const double2* in, double2* out) {
+// (periodic: F^-1 diag(.) F with F^-1 = backward DFT / (nx ny); mode 2 = |xi|^2 only, A's part)
+int gen_spectral(bp_problem* p, bool divide, const double2* in, double2* out, int mode = -1) {
     const GenArgs g = gen_args(p);
     if (int rc = gen_dst2(p, in, p->T, 1.0)) return rc;
-    gen_symbol_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(g, divide ? 1 : 0, g.gscale, p->T);
+    gen_symbol_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(g, mode >= 0 ? mode : (divide ? 1 : 0),
+                                                                             p->gper ? 1.0 : g.gscale, p->T);
     CU(cudaGetLastError());
-    return gen_dst2(p, p->T, out, 1.0);
+    return gen_dst2(p, p->T, out, p->gper ? g.gscale : 1.0, p->gper);
 }
 
 // Problem ctor guard (symbol.cpp:102-111) over the any-shape symbol
@@ -1095,6 +1107,32 @@ int run_core_generic(bp_problem* p, const bp_map* map, const bp_iter_config* cfg
     const double2 gamma = make_double2(map->gamma_re, map->gamma_im);
     const int direct = cfg->format == BP_FMT_DIRECT;
     const size_t nd = p->dense_pts;
+    if (p->gper) {
+        // iterate carried in Fourier space as well (U = DFT(u^m) in x, Q in y): per sweep one
+        // forward transform (of q^m) and one backward (u^{m+1} for the members still active)
+        if (int rc = gen_dst2(p, p->u0, p->x, 1.0)) return rc;
+        if (snapshots && n_snap > 0)
+            if (int rc = download(p, p->u0, nullptr, nullptr, snapshots)) return rc;
+        p->stat_launches = 0;
+        const long max_launch = (long)cfg->max_iters + 1;
+        for (long k = 1; k <= max_launch; ++k) {
+            gen_source_kernel<<<grid_for(p->field * B), 256, 0, p->stream>>>(g, c, p->u0, p->u1, p->f, p->y);
+            if (int rc = gen_dst2(p, p->y, p->y, 1.0)) return rc;
+            gen_psweep_kernel<<<dim3(nchunk, B), 256, 0, p->stream>>>(g, c, p->y, p->x, gamma, direct, p->gpart, nchunk);
+            gen_finalize_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(c, B, p->gpart, nchunk);
+            if (int rc = gen_dst2(p, p->x, (k & 1) ? p->u1 : p->u0, g.gscale, true, c.status)) return rc;
+            CU(cudaGetLastError());
+            p->stat_launches += 8;
+            if (snapshots && k < n_snap)
+                if (int rc = download(p, (k & 1) ? p->u1 : p->u0, nullptr, nullptr, snapshots + 2 * nd * B * k)) return rc;
+            if ((snapshots && n_snap > 0) || k % kGraphSweeps == 0 || k == max_launch) {
+                CU(cudaMemcpyAsync(p->host_active, c.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+                CU(cudaStreamSynchronize(p->stream));
+                if (*p->host_active == 0) break;
+            }
+        }
+        return BP_OK;
+    }
     // hx != hy: five_point (hx^2 only, kernels.cpp:56-69) and the two-spacing symbol differ, the
     // key identity ||G r|| = ||G(V u + f) - u|| no longer holds -- apply G to r explicitly
     const bool exact_reta = std::fabs(p->grid.lx / (p->gnx + 1) - p->grid.ly / (p->gny + 1)) >
@@ -1646,7 +1684,7 @@ int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* c
         return set_err(BP_ENOTSUP, "CDR family on the GPU: real scalar maps only");
     if (p->generic && (map->kind == BP_MAP_OPTIMAL_SCALAR || map->kind == BP_MAP_FOURIER_DIAG))
         return set_err(BP_ENOTSUP, "any-shape grids on the GPU: scalar and pointwise maps");
-    if (p->periodic && map->kind == BP_MAP_POINTWISE)
+    if ((p->periodic || p->gper) && map->kind == BP_MAP_POINTWISE)
         return set_err(BP_ENOTSUP, "periodic family: the pointwise (i/eta) V map is defined for the "
                                    "Dirichlet family only");
     return BP_OK;
@@ -1711,17 +1749,22 @@ int check_symbol_periodic(const std::vector<double>& xi2, int batch, const doubl
 }
 
 // Any-shape 2-D Dirichlet handle (generic_kernels.cuh): nx, ny >= 1 up to 4095 each, any lx, ly.
+// periodic: the reference's own HelmholtzProblem on any nx x ny <= 4096 (DFT lines, |xi|^2 symbol,
+// pseudospectral A; helmholtz.cpp:11-53), scalar maps
 int create_generic(const bp_grid* grid, int32_t batch, const double* k2, const double* k0, const double* eta,
-                   int32_t device, bp_problem** out) {
+                   int32_t device, bp_problem** out, bool periodic = false) {
     const int nx = grid->nx, ny = grid->ny;
-    if (nx + 1 > 4096 || ny + 1 > 4096)
-        return set_err(BP_ENOTSUP, "GPU any-shape path: nx, ny <= 4095 (power-of-two paths: nx+1 = ny+1 = 2^k <= 4096)");
+    if (nx + (periodic ? 0 : 1) > 4096 || ny + (periodic ? 0 : 1) > 4096)
+        return set_err(BP_ENOTSUP, periodic ? "GPU any-shape periodic path: nx, ny <= 4096"
+                                            : "GPU any-shape path: nx, ny <= 4095 (power-of-two paths: nx+1 = ny+1 = 2^k <= 4096)");
     for (int b = 0; b < batch; ++b) {
         if (!(eta[b] > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
         if (!std::isfinite(k0[b])) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
     }
-    const double hx = grid->lx / (nx + 1), hy = grid->ly / (ny + 1);  // grid.hpp:12-24
-    const std::vector<double> ax = gen_lap(nx, hx), ay = gen_lap(ny, hy);
+    // Dirichlet: h = l/(n+1) (grid.hpp:12-24), DST-I factors; periodic: h = l/n, xi^2 (FFT order)
+    const double hx = periodic ? grid->lx / nx : grid->lx / (nx + 1), hy = periodic ? grid->ly / ny : grid->ly / (ny + 1);
+    const std::vector<double> ax = periodic ? xi2_table(nx, grid->lx) : gen_lap(nx, hx);
+    const std::vector<double> ay = periodic ? xi2_table(ny, grid->ly) : gen_lap(ny, hy);
     if (int rc = check_symbol_generic(ax, ay, batch, k0, eta)) return rc;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
@@ -1733,6 +1776,7 @@ int create_generic(const bp_grid* grid, int32_t batch, const double* k2, const d
     p->device = device;
     p->dim = 2;
     p->generic = true;
+    p->gper = periodic;
     p->gnx = nx;
     p->gny = ny;
     p->field = (size_t)nx * ny;
@@ -1769,8 +1813,8 @@ int create_generic(const bp_grid* grid, int32_t batch, const double* k2, const d
     CUF(cudaMalloc(&p->gay, sizeof(double) * ny));
     CUF(cudaMemcpyAsync(p->gax, ax.data(), sizeof(double) * nx, cudaMemcpyHostToDevice, p->stream));
     CUF(cudaMemcpyAsync(p->gay, ay.data(), sizeof(double) * ny, cudaMemcpyHostToDevice, p->stream));
-    if (int rc = make_gplan(nx + 1, p->gplan_x)) return fail(rc);
-    if (int rc = make_gplan(ny + 1, p->gplan_y)) return fail(rc);
+    if (int rc = make_gplan(periodic ? nx : nx + 1, p->gplan_x)) return fail(rc);
+    if (int rc = make_gplan(periodic ? ny : ny + 1, p->gplan_y)) return fail(rc);
     std::vector<double> k0sq(batch);
     for (int b = 0; b < batch; ++b) k0sq[b] = k0[b] * k0[b];
     CUF(cudaMemcpyAsync(p->k0sq, k0sq.data(), sizeof(double) * batch, cudaMemcpyHostToDevice, p->stream));
@@ -1790,9 +1834,9 @@ int create_impl(const bp_grid* grid, int dim, int32_t batch, const double* k2, c
     int log2n = 0;
     while ((1 << log2n) < n) ++log2n;
     const int max_log2 = dim == 3 ? kMaxLog2_3d : kMaxLog2;
-    if (!periodic && dim == 2 &&
+    if (dim == 2 &&
         (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > max_log2 || grid->lx != grid->ly))
-        return create_generic(grid, batch, k2, k0, eta, device, out);
+        return create_generic(grid, batch, k2, k0, eta, device, out, periodic);
     if (grid->nx != grid->ny || (1 << log2n) != n || log2n < kMinLog2 || log2n > max_log2)
         return set_err(BP_ENOTSUP, periodic ? "GPU periodic path needs square grids with nx = 2^k, 8 <= 2^k <= 4096"
                                    : dim == 3 ? "GPU path needs cubic grids with n+1 = 2^k, 8 <= 2^k <= 512"
@@ -2606,6 +2650,17 @@ static int pointwise_op(const bp_problem* cp, int op, const double* u, const dou
     if (int rc = upload(p, u, p->x)) return rc;
     if (op == 3)
         if (int rc = upload(p, f, p->f)) return rc;
+    if (p->gper && (op == 0 || op == 3)) {
+        // pseudospectral A u = F^-1(|xi|^2 F u) - k2 u (helmholtz.cpp:27-32)
+        if (int rc = gen_spectral(p, false, p->x, p->y, 2)) return rc;
+        gen_pointwise_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(gen_args(p), 5, p->x, p->f, p->T);
+        combine_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(p->y, p->T, op == 3 ? p->f : nullptr,
+                                                                           p->field * p->batch);
+        CU(cudaGetLastError());
+        if (int rc = download(p, p->y, nullptr, nullptr, out)) return rc;
+        CU(cudaStreamSynchronize(p->stream));
+        return BP_OK;
+    }
     if (p->generic) {
         gen_pointwise_kernel<<<grid_for(p->field * p->batch), 256, 0, p->stream>>>(gen_args(p), op, p->x, p->f, p->y);
         CU(cudaGetLastError());
@@ -2669,7 +2724,7 @@ static int spectral_op(const bp_problem* cp, int which, const double* in, const 
                 break;
             case 2: if (int rc = gen_spectral(p, false, p->x, p->y)) return rc; break;
             case 3: if (int rc = gen_dst2(p, p->x, p->y, 1.0)) return rc; break;
-            default: if (int rc = gen_dst2(p, p->x, p->y, g.gscale)) return rc; break;
+            default: if (int rc = gen_dst2(p, p->x, p->y, g.gscale, p->gper)) return rc; break;
         }
         CU(cudaGetLastError());
         if (int rc = download(p, p->y, nullptr, nullptr, out)) return rc;
@@ -2804,7 +2859,10 @@ int bp_problem_set_medium(bp_problem* p, const double* k2, const double* k0, con
         if (!(eta[b] > 0.0)) return set_err(BP_EINVAL, "HelmholtzProblem: eta must be > 0");
         if (!std::isfinite(k0[b])) return set_err(BP_EINVAL, "HelmholtzProblem: k0 not finite");
     }
-    if (p->generic) {
+    if (p->gper) {
+        if (int rc = check_symbol_generic(xi2_table(p->gnx, p->grid.lx), xi2_table(p->gny, p->grid.ly), p->batch, k0, eta))
+            return rc;
+    } else if (p->generic) {
         const double hx = p->grid.lx / (p->gnx + 1), hy = p->grid.ly / (p->gny + 1);
         if (int rc = check_symbol_generic(gen_lap(p->gnx, hx), gen_lap(p->gny, hy), p->batch, k0, eta)) return rc;
     } else if (p->periodic) {

@@ -32,6 +32,7 @@ struct GLineArgs {
     const double2* filt;   // [L] FFT_L of the wrapped conj chirp (Bluestein)
     const double2* tw;     // [L / 2] exp(-2 pi i k / L)
     double scale;
+    const int* status;     // nullable: lines of members that are no longer ACTIVE are skipped
 };
 
 // In-place radix-2 DIT FFT (forward, exp(-)) of F[0..L) holding the line in bit-reversed order.
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(256) gline_kernel(const GLineArgs a) {
     extern __shared__ double2 gsm[];
     const long l = blockIdx.x;
     if (l >= a.lines) return;
+    if (a.status && __ldcg(&a.status[l / a.lpm]) != ST_ACTIVE) return;  // uniform per CTA
     const int n = a.n, L = a.L, lg = a.lgL, T = blockDim.x, t = threadIdx.x;
     const bool blue = L != n;
     const long base = (l / a.lpm) * a.mstride + (l % a.lpm) * a.lstride;
@@ -187,7 +189,7 @@ __device__ __forceinline__ double2 gen_stencil(const double2* __restrict__ u, lo
     return s;
 }
 
-// op: 0 A u, 1 V u, 2 V^H u, 3 f - A u, 4 V u + f
+// op: 0 A u, 1 V u, 2 V^H u, 3 f - A u, 4 V u + f, 5 k2 u
 __global__ void gen_pointwise_kernel(GenArgs g, int op, const double2* __restrict__ u,
                                      const double2* __restrict__ f, double2* __restrict__ out) {
     const long per = (long)g.nx * g.ny, total = per * g.batch;
@@ -201,6 +203,7 @@ __global__ void gen_pointwise_kernel(GenArgs g, int op, const double2* __restric
         if (op == 1) o = cmul(uu, V);
         else if (op == 2) o = cmul(cconj(V), uu);
         else if (op == 4) o = cadd(cmul(V, uu), f[idx]);
+        else if (op == 5) o = cmul(kk, uu);
         else {
             o = csub(cscale(gen_stencil(u, idx, i, j, g.nx, g.ny), g.inv_h2), cmul(kk, uu));
             if (op == 3) o = csub(f[idx], o);
@@ -219,7 +222,9 @@ __global__ void gen_symbol_kernel(GenArgs g, int divide, double scale, double2* 
         const int p = (int)(r / g.ny), q = (int)(r % g.ny);
         const double lr = (g.ax[p] + g.ay[q]) - g.k0sq[b], li = -g.eta[b];
         double2 w;
-        if (divide) {
+        if (divide == 2) {
+            w = make_double2((g.ax[p] + g.ay[q]) * scale, 0.0);  // |xi|^2 (periodic A's symbol part)
+        } else if (divide) {
             const double s = scale / fma(lr, lr, li * li);
             w = make_double2(lr * s, -li * s);
         } else {
@@ -313,6 +318,51 @@ __global__ void __launch_bounds__(256) gen_part_kernel(GenArgs g, Control c, con
         __syncthreads();
     }
     if (threadIdx.x == 0) part[((long)b * nchunk + ch) * 2 + 1] = red[0];
+}
+
+// Periodic any-shape sweep in Fourier space (U = DFT(u^m), Q = DFT(V u^m + f)): R = Q/lambda - U
+// is the transform of r_bs and lambda R that of the residual f - A u^m = q - L_ref u^m, so both
+// trace norms follow by Parseval (sum |x|^2 = sum |X|^2 / (nx ny)) without another transform;
+// U^{m+1} = U + gamma R (Direct: + gamma lambda R).  Inactive members are left untouched.
+__global__ void __launch_bounds__(256) gen_psweep_kernel(GenArgs g, Control c, const double2* __restrict__ Q,
+                                                         double2* __restrict__ U, double2 gamma, int direct,
+                                                         double* __restrict__ part, int nchunk) {
+    const int b = blockIdx.y, ch = blockIdx.x;
+    __shared__ double red[2][256];
+    const bool active = __ldcg(&c.status[b]) == ST_ACTIVE;
+    const long per = (long)g.nx * g.ny;
+    const long chunk = (per + nchunk - 1) / nchunk, lo = ch * chunk, hi = min(per, lo + chunk);
+    double s0 = 0.0, s1 = 0.0;
+    if (active) {
+        for (long r = lo + threadIdx.x; r < hi; r += blockDim.x) {
+            const long idx = b * per + r;
+            const int p = (int)(r / g.ny), q = (int)(r % g.ny);
+            const double lr = (g.ax[p] + g.ay[q]) - g.k0sq[b], li = -g.eta[b];
+            const double inv = 1.0 / fma(lr, lr, li * li);
+            const double2 qq = Q[idx], uu = U[idx];
+            const double2 z = make_double2((qq.x * lr + qq.y * li) * inv, (qq.y * lr - qq.x * li) * inv);
+            const double2 R = csub(z, uu);
+            const double2 lR = cmul(make_double2(lr, li), R);
+            s0 += cnorm(lR);
+            s1 += cnorm(R);
+            U[idx] = cadd(uu, cmul(gamma, direct ? lR : R));
+        }
+    }
+    red[0][threadIdx.x] = s0;
+    red[1][threadIdx.x] = s1;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if (threadIdx.x < h) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + h];
+            red[1][threadIdx.x] += red[1][threadIdx.x + h];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double invn = 1.0 / (double)per;
+        part[((long)b * nchunk + ch) * 2] = red[0][0] * invn;
+        part[((long)b * nchunk + ch) * 2 + 1] = red[1][0] * invn;
+    }
 }
 
 // entry m of every active member from the chunk partials (fixed order) + termination test

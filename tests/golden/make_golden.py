@@ -234,6 +234,35 @@ def generic_golden():
             out[f"{tag}_{name}_iters"] = it
             out[f"{tag}_{name}_term"] = term
             print("generic", tag, name, it, term)
+    # the reference's own periodic HelmholtzProblem on any shape (pa: 16 x 12, pb: 24 x 20 with
+    # lx != ly, pc: 100 x 37): operators, transforms and scalar-map runs (NPBS, relaxed, Direct)
+    for tag, (nx, ny, lx, ly) in {"pa": (16, 12, 1.0, 1.0), "pb": (24, 20, 1.0, 0.8),
+                                  "pc": (100, 37, 2.0, 1.0)}.items():
+        g = gaussian_filter(rng.standard_normal((nx, ny)), 2.0, mode="wrap")
+        g /= np.abs(g).max()
+        kk = 2 * np.pi / (12.0 * lx / nx) / (1.0 + 0.2 * g)
+        k2 = (kk * kk) * (1.0 + 0.05j)
+        k0 = float(kk.mean())
+        eta = float(1.01 * np.abs(k2 - k0 * k0).max())
+        X, Y = np.meshgrid(np.arange(nx) * lx / nx, np.arange(ny) * ly / ny, indexing="ij")
+        f = np.exp(-((X - lx / 2) ** 2 + (Y - ly / 2) ** 2) / (2 * (3 * lx / nx) ** 2)) + 0j
+        x = rng.standard_normal((nx, ny)) + 1j * rng.standard_normal((nx, ny))
+        r = ReferenceProblem(k2, k0, eta, lx, ly, periodic=True)
+        out.update({f"{tag}_shape": np.array([nx, ny]), f"{tag}_l": np.array([lx, ly]), f"{tag}_k2": k2,
+                    f"{tag}_f": f, f"{tag}_k0": k0, f"{tag}_eta": eta, f"{tag}_x": x,
+                    f"{tag}_G": r.apply_G(x), f"{tag}_A": r.apply_A(x), f"{tag}_L": r.apply_Lref(x),
+                    f"{tag}_V": r.apply_V(x), f"{tag}_born": r.born_residual(x, f),
+                    f"{tag}_res": r.residual(x, f), f"{tag}_fwd": r.forward_dst(x), f"{tag}_inv": r.inverse_dst(x)})
+        for name, kw in {"sc": dict(map_kind=MAP_SCALAR, gamma=1.0),
+                         "rx": dict(map_kind=MAP_SCALAR, gamma=0.9 + 0.05j),
+                         "dir": dict(map_kind=MAP_SCALAR, gamma=2e-5, fmt=FMT_DIRECT)}.items():
+            rr = r.run(f, rtol=1e-8, max_iters=3000, **kw)
+            out[f"{tag}_{name}_u"] = rr.u
+            out[f"{tag}_{name}_l2"] = rr.res_l2
+            out[f"{tag}_{name}_reta"] = rr.res_reta
+            out[f"{tag}_{name}_iters"] = rr.iters
+            out[f"{tag}_{name}_term"] = rr.terminated
+            print("generic periodic", tag, name, rr.iters, rr.terminated)
     np.savez_compressed(os.path.join(HERE, "ref_generic.npz"), **out)
 
 

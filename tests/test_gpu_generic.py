@@ -109,3 +109,53 @@ def test_any_shape_limits(gpu):
     with bs.HelmholtzDirichlet(np.ones((16, 12), np.complex128), 1.0, 1.0) as p:
         with pytest.raises(NotImplementedError):
             bs.run(p, bs.OptimalScalarMap("euclidean"), np.ones((16, 12), np.complex128))
+
+
+# ------------------------------------------------------------------ periodic family, any shape
+PTAGS = ["pa", "pb", "pc"]
+
+
+def phandle(g, t, batch=1):
+    lx, ly = g[f"{t}_l"]
+    k2 = np.repeat(g[f"{t}_k2"][None], batch, axis=0)
+    return bs.HelmholtzPeriodic(k2, float(g[f"{t}_k0"]), float(g[f"{t}_eta"]), lx=float(lx), ly=float(ly))
+
+
+@pytest.mark.parametrize("t", PTAGS)
+def test_periodic_operators_match_reference(gpu, g, t):
+    x, f = g[f"{t}_x"], g[f"{t}_f"]
+    with phandle(g, t) as p:
+        got = dict(G=p.apply_G(x), A=p.apply_A(x), L=p.apply_Lref(x), V=p.apply_V(x),
+                   born=p.born_residual(x, f), res=p.residual(x, f), fwd=p.forward_transform(x),
+                   inv=p.inverse_transform(x))
+    for k, v in got.items():
+        assert rel(v, g[f"{t}_{k}"]) < OP_TOL, (t, k, rel(v, g[f"{t}_{k}"]))
+
+
+@pytest.mark.parametrize("t", PTAGS)
+@pytest.mark.parametrize("name", ["sc", "rx", "dir"])
+def test_periodic_runs_match_reference(gpu, g, t, name):
+    gamma = {"sc": 1.0, "rx": 0.9 + 0.05j, "dir": 2e-5}[name]
+    cfg = bs.IterationConfig("direct" if name == "dir" else "npbs", 1e-8, 3000)
+    with phandle(g, t, batch=2) as p:
+        r = bs.run(p, bs.ScalarMap(gamma), np.repeat(g[f"{t}_f"][None], 2, axis=0), cfg)
+    it, term = int(g[f"{t}_{name}_iters"]), str(g[f"{t}_{name}_term"])
+    for b in range(2):
+        tr = r.traces[b]
+        assert tr.terminated == term and abs(tr.iters - it) <= 1, (t, name, tr.iters, it, tr.terminated)
+        k = min(tr.iters, it) + 1
+        np.testing.assert_allclose(tr.res_l2_rel[:k], g[f"{t}_{name}_l2"][:k], rtol=1e-8, atol=1e-13)
+        np.testing.assert_allclose(tr.res_reta_rel[:k], g[f"{t}_{name}_reta"][:k], rtol=1e-8, atol=1e-13)
+        if term != "diverged":
+            assert rel(r.u[b], g[f"{t}_{name}_u"]) < FIELD_TOL
+    assert np.array_equal(r.u[0], r.u[1])
+
+
+def test_periodic_fft_round_trip_16x12(gpu):
+    """verify.cpp:90-100 'roundtrip_fft' on the 16 x 12 periodic grid."""
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((16, 12)) + 1j * rng.standard_normal((16, 12))
+    with bs.HelmholtzPeriodic(np.full((16, 12), 4.0 + 0j), 2.0, 1.0) as p:
+        fw = p.forward_transform(x)
+        assert rel(fw, np.fft.fft2(x)) < OP_TOL
+        assert rel(p.inverse_transform(fw), x) < 1e-12
