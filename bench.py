@@ -274,7 +274,8 @@ def load_traffic(config):
     try:
         with open(path) as fh:
             d = json.load(fh)[config]
-        return d["row"]["dram_bytes_per_launch"], f"{os.path.relpath(path, ROOT)} ({d['source']})"
+        t = d["row"]["dram_bytes_per_launch"] + (d["row_b"]["dram_bytes_per_launch"] if "row_b" in d else 0.0)
+        return t, f"{os.path.relpath(path, ROOT)} ({d['source']})"
     except Exception:
         return None, None
 

@@ -205,10 +205,7 @@ struct ColArgs {
 // 1/eta of the pointwise map hoisted out of the row kernel's element loop: measured slower on
 // c1 (r02: 337.5 vs 329.5 us per row launch) -- the hoisted reciprocal stays live through the
 // unrolled loop and pushes the 128-register kernel into spills, which cost more than the
-// per-element divide
-#ifndef BS_INV_ETA_SMEM
-#define BS_INV_ETA_SMEM 0  // 1/eta of the line kept in shared memory, re-read per element
-#endif
+// per-element divide; so did re-reading it from shared memory per element (335.5 vs 331 us)
 #ifndef BS_INV_ETA_HOIST
 #define BS_INV_ETA_HOIST 0
 #endif
@@ -417,11 +414,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     // pointwise map gamma(x) = (i/eta) V(x): one division per line, not one per element (the
     // unrolled element loop otherwise carried an FP64 divide + slow-path call per element)
     [[maybe_unused]] const double inv_eta = BS_INV_ETA_HOIST ? 1.0 / eta : 0.0;
-    // BS_INV_ETA_SMEM: the line's 1/eta in shared memory, read through a volatile pointer at
-    // every use (one broadcast LDS instead of an FP64 divide, and no register held across the
-    // unrolled element loop); published before the element phase by the engine's syncs
-    __shared__ double s_inv_eta[EPB];
-    if (BS_INV_ETA_SMEM && t == 0) s_inv_eta[e] = 1.0 / eta;
+
 
     // Stage the element-wise operands of this row (and the stencil halo rows at the CTA's
     // edges) into L2 while the transform runs: the loads after the engine then hit L2.
@@ -592,9 +585,6 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
                     double2 g = a.gamma;
 #if BS_INV_ETA_HOIST
                     if (a.map_kind == MK_POINTWISE) g = cscale(mul_pi(V), inv_eta);  // (i/eta) V
-#elif BS_INV_ETA_SMEM
-                    if (a.map_kind == MK_POINTWISE)
-                        g = cscale(mul_pi(V), *static_cast<volatile double*>(&s_inv_eta[e]));
 #else
                     if (a.map_kind == MK_POINTWISE) g = cscale(mul_pi(V), 1.0 / eta);
 #endif
