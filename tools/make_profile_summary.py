@@ -83,7 +83,7 @@ with open(os.path.join(out_dir, f"{tag}_ncu_full.md"), "w") as fh:
                  to_bytes(vals["dram__bytes_read.sum"]) + to_bytes(vals["dram__bytes_write.sum"]),
                  "duration": " ".join(vals["gpu__time_duration.sum"])}
         # the sweep's row pass (R_SWEEP, or the c4 RC_A/RC_B pair) and its column pass
-        if re.search(r"row_kernel<\d+, 3,|crow_kernel<\d+, 2,|prow_kernel", name):
+        if re.search(r"\brow_kernel<\d+, 3,|crow_kernel<\d+, 2,|prow_kernel", name):
             summary["row"] = entry
         if re.search(r"crow_kernel<\d+, 3,", name):
             summary["row_b"] = entry
