@@ -398,6 +398,12 @@ struct bp_problem {
     int* dflag = nullptr;        // device flag of nonfinite_kernel
     // graph cache
     cudaGraphExec_t graph = nullptr;
+    // small batches (< kSplitWaves row waves): the batch as two halves, each its own graph on its
+    // own stream, so one half's column pass fills the other half's row-launch tail
+    cudaGraphExec_t graph2 = nullptr;
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t ev_join = nullptr;
+    int graph_split = -1;
     int graph_map_kind = -1;
     int graph_metric = -1;
     int graph_format = -1;
@@ -486,6 +492,52 @@ ColArgs col_args(const bp_problem* p) {
     c.tw = p->tw;
     c.sinp = p->sinp;
     c.status = nullptr;
+    return c;
+}
+
+// Arguments restricted to members [b0, b0 + nb) of the batch (the split-batch graphs): every
+// per-member array is offset, n_active stays shared.
+Control control_range(Control c, const bp_problem* p, int b0) {
+    c.status += b0;
+    c.sweep += b0;
+    c.iters += b0;
+    c.term += b0;
+    c.result_buf += b0;
+    c.counter += b0;
+    c.partial += ((size_t)b0 << (p->log2n * (p->dim - 1))) * kPartStride;
+    c.gamma += b0;
+    c.fnorm_l2 += b0;
+    c.fnorm_reta += b0;
+    c.trace_l2 += (size_t)b0 * c.trace_stride;
+    c.trace_reta += (size_t)b0 * c.trace_stride;
+    return c;
+}
+
+RowArgs row_args_range(const RowArgs& a0, const bp_problem* p, int b0, int nb) {
+    RowArgs a = a0;
+    const size_t fo = (size_t)b0 * p->field;
+    a.batch = nb;
+    a.k0sq += b0;
+    a.eta += b0;
+    a.k2 += fo;
+    a.f += fo;
+    a.T += fo;
+    a.u0 += fo;
+    a.u1 += fo;
+    if (a.X) a.X += fo;
+    a.ctl = control_range(a.ctl, p, b0);
+    return a;
+}
+
+ColArgs col_args_range(const ColArgs& c0, const bp_problem* p, int b0, int nb) {
+    ColArgs c = c0;
+    c.batch = nb;
+    c.k0sq += b0;
+    c.eta += b0;
+    c.T += (size_t)b0 * p->field;
+    if (c.status) c.status += b0;
+    if (c.tri) c.tri += (size_t)b0 * ((size_t)1 << ((p->dim - 1) * p->log2n)) * (kTriP + p->n / kTriP);
+    if (c.finalize) c.ctl = control_range(c.ctl, p, b0);
     return c;
 }
 
@@ -815,6 +867,8 @@ int ensure_trace(bp_problem* p, int max_iters) {
     if (p->graph) {
         cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
+        if (p->graph2) cudaGraphExecDestroy(p->graph2);
+        p->graph2 = nullptr;
     }
     return BP_OK;
 }
@@ -885,13 +939,33 @@ int sweep_once(bp_problem* p, const SweepPlan& plan, const RowArgs& a, const Col
     return BP_OK;
 }
 
+// Split the batch into two concurrently replayed halves when the row launch is only a few
+// waves deep (measured c1 at 8 members: 86 % of the 64-member per-GPU rate, 1.73 waves).  The
+// two-launch scalar / pointwise plan only (its per-half finalisation is self-contained);
+// BP_SPLIT=0 disables.  Returns the first half's size or 0.
+constexpr double kSplitWaves = 8.0;
+int split_batch(const bp_problem* p, const SweepPlan& plan) {
+    const char* env = std::getenv("BP_SPLIT");  // read per run (tests toggle it)
+    const bool env_off = env && env[0] == '0';
+    if (env_off || p->batch < 2 || p->dim != 2 || p->periodic || p->cdr || p->generic || p->slab_log2) return 0;
+    if (!(plan.n == 2 && plan.row[0] && (plan.mode[0] == R_SWEEP || plan.mode[0] == R_SWEEP_D))) return 0;
+    static int sms = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    const double row_ctas = (double)((long)p->batch << p->log2n) / row_lines_per_cta(p->log2n, points_per_thread(p->log2n));
+    const bool force = env && env[0] == '2';  // BP_SPLIT=2: split at any depth (experiments)
+    if (!force && row_ctas / (2.0 * sms) >= kSplitWaves) return 0;
+    return p->batch / 2;
+}
+
 // whole-solve cluster kernel applies: 2-D Dirichlet n = 64 / 128 with the tridiagonal tables,
 // the fused scalar / pointwise sweep, and a device that runs the cluster shape
 bool cluster_enabled(const bp_problem* p, const SweepPlan& plan) {
-    static const bool env_off = [] {
-        const char* e = std::getenv("BP_CLUSTER");
-        return e && e[0] == '0';
-    }();
+    const char* env = std::getenv("BP_CLUSTER");  // read per run (tests toggle it)
+    const bool env_off = env && env[0] == '0';
     if (env_off || p->dim != 2 || p->periodic || p->cdr || p->generic || p->slab_log2 || !p->tri) return false;
     if (p->log2n != 6 && p->log2n != 7) return false;
     if (!(plan.n == 2 && plan.row[0] && (plan.mode[0] == R_SWEEP || plan.mode[0] == R_SWEEP_D))) return false;
@@ -1044,19 +1118,44 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         if (rc) return rc;
     } else {
         // graph of kGraphSweeps sweeps, replayed until every member terminated
-        const bool reuse = p->graph && p->graph_map_kind == map->kind &&
+        const int split = split_batch(p, plan);  // 0 = one graph, else the first half's size
+        const bool reuse = p->graph && p->graph_split == split && p->graph_map_kind == map->kind &&
                            p->graph_metric == map->metric && p->graph_format == cfg->format &&
                            p->graph_gamma.x == map->gamma_re && p->graph_gamma.y == map->gamma_im &&
                            p->graph_max_iters == cfg->max_iters && p->graph_rtol == cfg->rtol;
         if (!reuse) {
             if (p->graph) cudaGraphExecDestroy(p->graph);
             p->graph = nullptr;
+            if (p->graph2) cudaGraphExecDestroy(p->graph2);
+            p->graph2 = nullptr;
             cudaGraph_t g;
-            CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-            for (int s = 0; s < kGraphSweeps; ++s) sweep_once(p, plan, a, c, nullptr);
-            CU(cudaStreamEndCapture(p->stream, &g));
-            CU(cudaGraphInstantiate(&p->graph, g, 0));
-            cudaGraphDestroy(g);
+            if (!split) {
+                CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+                for (int s = 0; s < kGraphSweeps; ++s) sweep_once(p, plan, a, c, nullptr);
+                CU(cudaStreamEndCapture(p->stream, &g));
+                CU(cudaGraphInstantiate(&p->graph, g, 0));
+                cudaGraphDestroy(g);
+            } else {
+                if (!p->stream2) CU(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+                if (!p->ev_join) CU(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+                const int h = split;
+                const RowArgs ah[2] = {row_args_range(a, p, 0, h), row_args_range(a, p, h, B - h)};
+                const ColArgs ch[2] = {col_args_range(c, p, 0, h), col_args_range(c, p, h, B - h)};
+                cudaStream_t keep = p->stream;
+                for (int k = 0; k < 2; ++k) {  // sweep_once launches on p->stream: capture each half
+                    p->stream = k ? p->stream2 : keep;
+                    cudaError_t e = cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal);
+                    for (int sw = 0; e == cudaSuccess && sw < kGraphSweeps; ++sw) sweep_once(p, plan, ah[k], ch[k], nullptr);
+                    if (e == cudaSuccess) e = cudaStreamEndCapture(p->stream, &g);
+                    if (e == cudaSuccess) {
+                        e = cudaGraphInstantiate(k ? &p->graph2 : &p->graph, g, 0);
+                        cudaGraphDestroy(g);
+                    }
+                    p->stream = keep;
+                    CU(e);
+                }
+            }
+            p->graph_split = split;
             p->graph_map_kind = map->kind;
             p->graph_metric = map->metric;
             p->graph_format = cfg->format;
@@ -1065,8 +1164,17 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             p->graph_rtol = cfg->rtol;
         }
         long launched = 0;
+        if (split) {  // the second half's stream starts after everything enqueued so far
+            CU(cudaEventRecord(p->ev_join, p->stream));
+            CU(cudaStreamWaitEvent(p->stream2, p->ev_join, 0));
+        }
         while (launched < max_launch) {
             CU(cudaGraphLaunch(p->graph, p->stream));
+            if (split) {
+                CU(cudaGraphLaunch(p->graph2, p->stream2));
+                CU(cudaEventRecord(p->ev_join, p->stream2));
+                CU(cudaStreamWaitEvent(p->stream, p->ev_join, 0));  // both halves before the poll
+            }
             launched += kGraphSweeps;
             p->stat_launches += (int64_t)kps * kGraphSweeps;
             CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
@@ -1630,6 +1738,8 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
     if (!reuse) {
         if (p->graph) cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
+        if (p->graph2) cudaGraphExecDestroy(p->graph2);
+        p->graph2 = nullptr;
         cudaGraph_t g;
         CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
         for (int s = 0; s < kGraphSweeps; ++s) sweep(nullptr);
@@ -2602,6 +2712,9 @@ int bp_problem_destroy(bp_problem* p) {
     DeviceGuard guard(p->device);
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->graph) cudaGraphExecDestroy(p->graph);
+    if (p->graph2) cudaGraphExecDestroy(p->graph2);
+    if (p->stream2) cudaStreamDestroy(p->stream2);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
     if (p->u_alloc0) p->u0 = p->u_alloc0;
     if (p->u_alloc1) p->u1 = p->u_alloc1;
     if (p->own_T) {  // external exchange buffers (bp_slab_set_exchange) are not ours to free

@@ -76,3 +76,23 @@ def test_slab_deterministic(gpu, fused):
             for p in parts:
                 p.close()
     same3(go)
+
+
+@pytest.mark.parametrize("n,batch", [(256, 2), (512, 3), (512, 8), (1024, 5)])
+def test_split_batch_bit_identical(gpu, monkeypatch, n, batch):
+    """Small batches run as two concurrently replayed half-batch graphs (BP_SPLIT, default on
+    below 8 row waves): members are independent, so every member's u and traces are bit-identical
+    to the single-graph run, terminations included (members converge at different sweeps)."""
+    k2, f, k0, eta = inst(n, batch=batch, seed=batch)
+    f[0] *= 10.0
+    cfg = bs.IterationConfig(rtol=1e-5, max_iters=400)
+    res = []
+    for split in ("0", "1"):
+        monkeypatch.setenv("BP_SPLIT", split)
+        with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+            res.append(bs.run(p, bs.PointwiseMap(), f, cfg))
+    for b in range(batch):
+        assert res[0].traces[b].iters == res[1].traces[b].iters
+        assert res[0].traces[b].terminated == res[1].traces[b].terminated
+        assert np.array_equal(res[0].traces[b].res_l2_rel, res[1].traces[b].res_l2_rel)
+        assert np.array_equal(res[0].u[b], res[1].u[b])
