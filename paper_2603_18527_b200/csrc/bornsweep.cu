@@ -400,9 +400,10 @@ struct bp_problem {
     cudaGraphExec_t graph = nullptr;
     // small batches (< kSplitWaves row waves): the batch as two halves, each its own graph on its
     // own stream, so one half's column pass fills the other half's row-launch tail
-    cudaGraphExec_t graph2 = nullptr;
-    cudaStream_t stream2 = nullptr;
-    cudaEvent_t ev_join = nullptr;
+    static constexpr int kMaxSplit = 4;
+    cudaGraphExec_t graph2[kMaxSplit - 1]{};  // parts 1.. (part 0 is `graph` on `stream`)
+    cudaStream_t stream2[kMaxSplit - 1]{};
+    cudaEvent_t ev_join[kMaxSplit]{};
     int graph_split = -1;
     int graph_map_kind = -1;
     int graph_metric = -1;
@@ -867,8 +868,10 @@ int ensure_trace(bp_problem* p, int max_iters) {
     if (p->graph) {
         cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
-        if (p->graph2) cudaGraphExecDestroy(p->graph2);
-        p->graph2 = nullptr;
+        for (auto& g2 : p->graph2) {
+            if (g2) cudaGraphExecDestroy(g2);
+            g2 = nullptr;
+        }
     }
     return BP_OK;
 }
@@ -944,8 +947,15 @@ int sweep_once(bp_problem* p, const SweepPlan& plan, const RowArgs& a, const Col
 // GPU.  Measured on c1: 8 members 30.0 -> 34.9 Gpts/s (the row launch is 1.73 waves deep), 32
 // members 34.9 -> 35.7, 64 members 34.6 -> 35.1.  The two-launch scalar / pointwise plan only
 // (its per-half finalisation is self-contained); BP_SPLIT=0 disables.  Returns the first half's
-// size or 0.
+// size or 0.  BP_SPLIT=K (3, 4): K parts.
 constexpr double kSplitWaves = 1e30;  // every depth (BP_SPLIT=2 kept as the explicit spelling)
+// parts: 4 for shallow batches (c1 at 8 members: 34.8 -> 36.4 Gpts/s with 4 vs 2 parts), 2 above
+// 16 members (64 members: 35.1 with 2, 35.0 with 3 or 4); BP_SPLIT=K overrides
+int split_parts(int batch) {
+    const char* env = std::getenv("BP_SPLIT");
+    const int k = env ? std::atoi(env) : (batch <= 16 ? 4 : 2);
+    return std::max(2, std::min(k, (int)bp_problem::kMaxSplit));
+}
 int split_batch(const bp_problem* p, const SweepPlan& plan) {
     const char* env = std::getenv("BP_SPLIT");  // read per run (tests toggle it)
     const bool env_off = env && env[0] == '0';
@@ -1120,7 +1130,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         if (rc) return rc;
     } else {
         // graph of kGraphSweeps sweeps, replayed until every member terminated
-        const int split = split_batch(p, plan);  // 0 = one graph, else the first half's size
+        int split = split_batch(p, plan) ? std::min(split_parts(B), B) : 0;  // 0 = one graph, else parts
         const bool reuse = p->graph && p->graph_split == split && p->graph_map_kind == map->kind &&
                            p->graph_metric == map->metric && p->graph_format == cfg->format &&
                            p->graph_gamma.x == map->gamma_re && p->graph_gamma.y == map->gamma_im &&
@@ -1128,8 +1138,10 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         if (!reuse) {
             if (p->graph) cudaGraphExecDestroy(p->graph);
             p->graph = nullptr;
-            if (p->graph2) cudaGraphExecDestroy(p->graph2);
-            p->graph2 = nullptr;
+            for (auto& g2 : p->graph2) {
+                if (g2) cudaGraphExecDestroy(g2);
+                g2 = nullptr;
+            }
             cudaGraph_t g;
             if (!split) {
                 CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
@@ -1138,24 +1150,28 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
                 CU(cudaGraphInstantiate(&p->graph, g, 0));
                 cudaGraphDestroy(g);
             } else {
-                if (!p->stream2) CU(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
-                if (!p->ev_join) CU(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
-                const int h = split;
-                const RowArgs ah[2] = {row_args_range(a, p, 0, h), row_args_range(a, p, h, B - h)};
-                const ColArgs ch[2] = {col_args_range(c, p, 0, h), col_args_range(c, p, h, B - h)};
+                const int K = std::min(split_parts(B), B);
+                for (int k = 0; k < K; ++k) {
+                    if (k && !p->stream2[k - 1]) CU(cudaStreamCreateWithFlags(&p->stream2[k - 1], cudaStreamNonBlocking));
+                    if (!p->ev_join[k]) CU(cudaEventCreateWithFlags(&p->ev_join[k], cudaEventDisableTiming));
+                }
                 cudaStream_t keep = p->stream;
-                for (int k = 0; k < 2; ++k) {  // sweep_once launches on p->stream: capture each half
-                    p->stream = k ? p->stream2 : keep;
+                for (int k = 0; k < K; ++k) {  // sweep_once launches on p->stream: capture each part
+                    const int b0 = (int)((long)B * k / K), b1 = (int)((long)B * (k + 1) / K);
+                    const RowArgs ak = row_args_range(a, p, b0, b1 - b0);
+                    const ColArgs ck = col_args_range(c, p, b0, b1 - b0);
+                    p->stream = k ? p->stream2[k - 1] : keep;
                     cudaError_t e = cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal);
-                    for (int sw = 0; e == cudaSuccess && sw < kGraphSweeps; ++sw) sweep_once(p, plan, ah[k], ch[k], nullptr);
+                    for (int sw = 0; e == cudaSuccess && sw < kGraphSweeps; ++sw) sweep_once(p, plan, ak, ck, nullptr);
                     if (e == cudaSuccess) e = cudaStreamEndCapture(p->stream, &g);
                     if (e == cudaSuccess) {
-                        e = cudaGraphInstantiate(k ? &p->graph2 : &p->graph, g, 0);
+                        e = cudaGraphInstantiate(k ? &p->graph2[k - 1] : &p->graph, g, 0);
                         cudaGraphDestroy(g);
                     }
                     p->stream = keep;
                     CU(e);
                 }
+                split = K;
             }
             p->graph_split = split;
             p->graph_map_kind = map->kind;
@@ -1166,16 +1182,16 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             p->graph_rtol = cfg->rtol;
         }
         long launched = 0;
-        if (split) {  // the second half's stream starts after everything enqueued so far
-            CU(cudaEventRecord(p->ev_join, p->stream));
-            CU(cudaStreamWaitEvent(p->stream2, p->ev_join, 0));
+        if (split) {  // the other parts' streams start after everything enqueued so far
+            CU(cudaEventRecord(p->ev_join[0], p->stream));
+            for (int k = 1; k < split; ++k) CU(cudaStreamWaitEvent(p->stream2[k - 1], p->ev_join[0], 0));
         }
         while (launched < max_launch) {
             CU(cudaGraphLaunch(p->graph, p->stream));
-            if (split) {
-                CU(cudaGraphLaunch(p->graph2, p->stream2));
-                CU(cudaEventRecord(p->ev_join, p->stream2));
-                CU(cudaStreamWaitEvent(p->stream, p->ev_join, 0));  // both halves before the poll
+            for (int k = 1; k < split; ++k) {
+                CU(cudaGraphLaunch(p->graph2[k - 1], p->stream2[k - 1]));
+                CU(cudaEventRecord(p->ev_join[k], p->stream2[k - 1]));
+                CU(cudaStreamWaitEvent(p->stream, p->ev_join[k], 0));  // every part before the poll
             }
             launched += kGraphSweeps;
             p->stat_launches += (int64_t)kps * kGraphSweeps;
@@ -1740,8 +1756,10 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
     if (!reuse) {
         if (p->graph) cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
-        if (p->graph2) cudaGraphExecDestroy(p->graph2);
-        p->graph2 = nullptr;
+        for (auto& g2 : p->graph2) {
+            if (g2) cudaGraphExecDestroy(g2);
+            g2 = nullptr;
+        }
         cudaGraph_t g;
         CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
         for (int s = 0; s < kGraphSweeps; ++s) sweep(nullptr);
@@ -2714,9 +2732,12 @@ int bp_problem_destroy(bp_problem* p) {
     DeviceGuard guard(p->device);
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->graph) cudaGraphExecDestroy(p->graph);
-    if (p->graph2) cudaGraphExecDestroy(p->graph2);
-    if (p->stream2) cudaStreamDestroy(p->stream2);
-    if (p->ev_join) cudaEventDestroy(p->ev_join);
+    for (auto g2 : p->graph2)
+        if (g2) cudaGraphExecDestroy(g2);
+    for (auto s2 : p->stream2)
+        if (s2) cudaStreamDestroy(s2);
+    for (auto ev : p->ev_join)
+        if (ev) cudaEventDestroy(ev);
     if (p->u_alloc0) p->u0 = p->u_alloc0;
     if (p->u_alloc1) p->u1 = p->u_alloc1;
     if (p->own_T) {  // external exchange buffers (bp_slab_set_exchange) are not ours to free
