@@ -1194,7 +1194,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
                 CU(cudaStreamWaitEvent(p->stream, p->ev_join[k], 0));  // every part before the poll
             }
             launched += kGraphSweeps;
-            p->stat_launches += (int64_t)kps * kGraphSweeps;
+            p->stat_launches += (int64_t)kps * kGraphSweeps * std::max(split, 1);  // every part's graph
             CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
                                p->stream));
             CU(cudaStreamSynchronize(p->stream));
@@ -1561,6 +1561,27 @@ CdrArgs cdr_args(const bp_problem* p) {
     return a;
 }
 
+// members [b0, b0 + nb) of a CDR batch (split-batch graphs): per-member arrays offset, the
+// per-pair partials at the crow kernels' own stride (n/2 pairs per member)
+CdrArgs cdr_args_range(const CdrArgs& a0, const bp_problem* p, int b0, int nb) {
+    CdrArgs a = a0;
+    const size_t fo = (size_t)b0 * p->field;
+    a.batch = nb;
+    a.sigma0 += b0;
+    a.bx += fo;
+    a.by += fo;
+    a.sigma += fo;
+    a.f += fo;
+    a.T += fo;
+    a.u0 += fo;
+    a.u1 += fo;
+    a.rnorm2 += b0;
+    Control c = control_range(a.ctl, p, b0);
+    c.partial = a0.ctl.partial + (size_t)b0 * (p->n / 2) * kPartStride;
+    a.ctl = c;
+    return a;
+}
+
 // A u, V u, f - A u, V u + f on real fields (ops 0, 1, 3, 4): the same upwind stencil as the
 // RC_B prologue (cdr_kernels.cuh), elementwise for the operator API
 __global__ void cdr_stencil_kernel(int op, const double* __restrict__ u, const double* __restrict__ f,
@@ -1608,13 +1629,13 @@ int cdr_download(bp_problem* p, const double2* src, double* dst, bool host_ptr =
 // CC_GREEN column pass of the CDR family: the Neumann tridiagonal x-solve when the handle has its
 // tables (equal to DCT-II -> x scale / lambda -> DCT-III = 2n h^2 scale Tri^-1, the REDFT01
 // REDFT10 pair multiplying by 2n), else the DCT route
-cudaError_t cdr_green(bp_problem* p, const CdrArgs& ac) {
+cudaError_t cdr_green(bp_problem* p, const CdrArgs& ac, int b0 = 0) {
     if (!p->tri) return launch_cdr(p->log2n, false, CC_GREEN, ac, p->stream);
     ColArgs c{};
     c.batch = ac.batch;
     c.T = reinterpret_cast<double2*>(ac.T);
     c.status = ac.ctl.status;
-    c.tri = p->tri;
+    c.tri = p->tri + (size_t)b0 * (p->n / 2) * (2 * kTriP + p->n / kTriP);
     const double h = p->grid.lx / p->n;
     c.tri_scale = 2.0 * p->n * h * h * ac.scale;
     return launch_tri(p->log2n, CL_CDR, c, p->stream);
@@ -1751,8 +1772,13 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
         for (auto& e : ev) cudaEventDestroy(e);
         return rc;
     }
-    const bool reuse = p->graph && p->graph_map_kind == map->kind && p->graph_gamma.x == map->gamma_re &&
-                       p->graph_max_iters == cfg->max_iters && p->graph_rtol == cfg->rtol;
+    // split-batch graphs as the Dirichlet path (run_core): parts replayed concurrently on their
+    // own streams (BP_SPLIT=0 disables)
+    const char* senv = std::getenv("BP_SPLIT");
+    const int split = (B >= 2 && !(senv && senv[0] == '0')) ? std::min(split_parts(B), B) : 0;
+    const bool reuse = p->graph && p->graph_split == split && p->graph_map_kind == map->kind &&
+                       p->graph_gamma.x == map->gamma_re && p->graph_max_iters == cfg->max_iters &&
+                       p->graph_rtol == cfg->rtol;
     if (!reuse) {
         if (p->graph) cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
@@ -1761,11 +1787,40 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
             g2 = nullptr;
         }
         cudaGraph_t g;
-        CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-        for (int s = 0; s < kGraphSweeps; ++s) sweep(nullptr);
-        CU(cudaStreamEndCapture(p->stream, &g));
-        CU(cudaGraphInstantiate(&p->graph, g, 0));
-        cudaGraphDestroy(g);
+        if (!split) {
+            CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+            for (int s = 0; s < kGraphSweeps; ++s) sweep(nullptr);
+            CU(cudaStreamEndCapture(p->stream, &g));
+            CU(cudaGraphInstantiate(&p->graph, g, 0));
+            cudaGraphDestroy(g);
+        } else {
+            for (int k = 0; k < split; ++k) {
+                if (k && !p->stream2[k - 1]) CU(cudaStreamCreateWithFlags(&p->stream2[k - 1], cudaStreamNonBlocking));
+                if (!p->ev_join[k]) CU(cudaEventCreateWithFlags(&p->ev_join[k], cudaEventDisableTiming));
+            }
+            cudaStream_t keep = p->stream;
+            for (int k = 0; k < split; ++k) {
+                const int b0 = (int)((long)B * k / split), b1 = (int)((long)B * (k + 1) / split);
+                const CdrArgs ak = cdr_args_range(a, p, b0, b1 - b0);
+                CdrArgs ack = cdr_args_range(ac, p, b0, b1 - b0);
+                p->stream = k ? p->stream2[k - 1] : keep;
+                cudaError_t e = cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal);
+                for (int sw = 0; e == cudaSuccess && sw < kGraphSweeps; ++sw) {
+                    if (e == cudaSuccess) e = launch_cdr(p->log2n, true, RC_A, ak, p->stream);
+                    if (e == cudaSuccess) e = launch_cdr(p->log2n, true, RC_B, ak, p->stream);
+                    if (e == cudaSuccess) e = cdr_green(p, ack, b0);
+                }
+                cudaError_t e2 = cudaStreamEndCapture(p->stream, &g);
+                if (e == cudaSuccess) e = e2;
+                if (e == cudaSuccess) {
+                    e = cudaGraphInstantiate(k ? &p->graph2[k - 1] : &p->graph, g, 0);
+                    cudaGraphDestroy(g);
+                }
+                p->stream = keep;
+                CU(e);
+            }
+        }
+        p->graph_split = split;
         p->graph_map_kind = map->kind;
         p->graph_metric = map->metric;
         p->graph_gamma = make_double2(map->gamma_re, 0.0);
@@ -1773,10 +1828,19 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
         p->graph_rtol = cfg->rtol;
     }
     long launched = 0;
+    if (split) {
+        CU(cudaEventRecord(p->ev_join[0], p->stream));
+        for (int k = 1; k < split; ++k) CU(cudaStreamWaitEvent(p->stream2[k - 1], p->ev_join[0], 0));
+    }
     while (launched < max_launch) {
         CU(cudaGraphLaunch(p->graph, p->stream));
+        for (int k = 1; k < split; ++k) {
+            CU(cudaGraphLaunch(p->graph2[k - 1], p->stream2[k - 1]));
+            CU(cudaEventRecord(p->ev_join[k], p->stream2[k - 1]));
+            CU(cudaStreamWaitEvent(p->stream, p->ev_join[k], 0));
+        }
         launched += kGraphSweeps;
-        p->stat_launches += 3 * kGraphSweeps;
+        p->stat_launches += 3 * kGraphSweeps * std::max(split, 1);
         if (int rc = poll()) return rc;
         if (*p->host_active == 0) break;
     }

@@ -96,3 +96,21 @@ def test_split_batch_bit_identical(gpu, monkeypatch, n, batch):
         assert res[0].traces[b].terminated == res[1].traces[b].terminated
         assert np.array_equal(res[0].traces[b].res_l2_rel, res[1].traces[b].res_l2_rel)
         assert np.array_equal(res[0].u[b], res[1].u[b])
+
+
+@pytest.mark.parametrize("batch", [2, 5])
+def test_cdr_split_batch_bit_identical(gpu, monkeypatch, batch):
+    """The CDR family's split-batch graphs (run_core_cdr): members bit-identical to one graph."""
+    bx, by, sg, s0, f = bs.make_cdr_instances(bs.CdrSpec(n=256, seed=batch), 0, batch)
+    f[0] *= 3.0
+    cfg = bs.IterationConfig(rtol=1e-9, max_iters=200)
+    res = []
+    for split in ("0", "1"):
+        monkeypatch.setenv("BP_SPLIT", split)
+        with bs.CdrNeumann(bx, by, sg, s0) as p:
+            res.append(bs.run(p, bs.ScalarMap(1.0), f, cfg))
+    for b in range(batch):
+        assert res[0].traces[b].iters == res[1].traces[b].iters
+        assert res[0].traces[b].terminated == res[1].traces[b].terminated
+        assert np.array_equal(res[0].traces[b].res_l2_rel, res[1].traces[b].res_l2_rel)
+        assert np.array_equal(res[0].u[b], res[1].u[b])
