@@ -69,8 +69,8 @@ typedef struct {
  * relaxation gamma(x) = (i/eta) V(x) ("scalar/diagonal relaxation").
  * Supported on the GPU (bp_run):
  *   SCALAR          every family and path (CDR: real gamma only)
- *   OPTIMAL_SCALAR  Dirichlet 2-D / 3-D and periodic, both metrics; not on slabs or CDR
- *   FOURIER_DIAG    Dirichlet 2-D / 3-D and periodic; not on slabs or CDR
+ *   OPTIMAL_SCALAR  Dirichlet 2-D / 3-D (single device and slabs) and periodic, both metrics
+ *   FOURIER_DIAG    Dirichlet 2-D / 3-D (single device and slabs) and periodic
  *   POINTWISE       Dirichlet 2-D / 3-D, single device and slabs (a Dirichlet-family map)
  * anything else returns BP_ENOTSUP. */
 enum {
@@ -230,8 +230,17 @@ int bp_pipeline_destroy(bp_pipeline* pl);
  * [nranks][R][R] = n x R column block.  The driver (paper_2603_18527_b200/slab.py) runs, per
  * sweep: halo exchange of u^m's edge rows -> BP_SLAB_SWEEP -> all-reduce sums[0..1] ->
  * BP_SLAB_FINALIZE (the termination test of iterate.cpp:134-150 on identical sums on every
- * rank) -> all-to-all t_rows -> t_cols -> BP_SLAB_COL -> all-to-all back.  Scalar and pointwise
- * maps; bp_run semantics otherwise. */
+ * rank) -> all-to-all t_rows -> t_cols -> BP_SLAB_COL -> all-to-all back (scalar and pointwise
+ * maps).  The other reference maps (correction.cpp:22-76) run the staged sweeps, "colpass" =
+ * all-to-all, BP_SLAB_COL, all-to-all back:
+ *   OptimalScalar, Euclidean:  halo -> OPT_A -> all-reduce sums[0..4] -> FINALIZE(a0 = 1: the
+ *                              entry and gamma = <w, r>/<w, w>) -> OPT_B -> colpass
+ *   OptimalScalar, R_eta:      halo -> RETA_A -> all-reduce sums[0..1] -> FINALIZE -> colpass
+ *                              (G V x) -> RETA_C -> all-reduce sums[0..2] -> GAMMA -> OPT_B -> colpass
+ *   FourierDiag:               halo -> FD_A -> all-reduce sums[0..1] -> FINALIZE -> all-to-all,
+ *                              COL_FD (the rank's block of m, bp_slab_set_multiplier),
+ *                              all-to-all back -> FD_B -> colpass
+ * bp_run semantics otherwise (CBS / NPBS formats). */
 enum {
     BP_SLAB_FWD_F = 0,     /* t_rows <- y-DST of f; sums[0] = local ||f||^2 */
     BP_SLAB_COL = 1,       /* t_cols: x-DST, x Green weights, inverse x-DST (in place) */
@@ -240,14 +249,22 @@ enum {
     BP_SLAB_FWD_BORN = 4,  /* t_rows <- y-DST of V u^0 + f */
     BP_SLAB_SWEEP = 5,     /* fused sweep; sums[0..1] = local entry sums */
     BP_SLAB_FINALIZE = 6,  /* trace entry + termination from the all-reduced sums */
-    BP_SLAB_ZERO_U = 7     /* u^0 <- 0 on the device (a cold start without re-staging f) */
+    BP_SLAB_ZERO_U = 7,    /* u^0 <- 0 on the device (a cold start without re-staging f) */
+    BP_SLAB_OPT_A = 8,     /* entry sums, <w, r>, |w|^2 (w = A x) -> sums[0..4]; keeps x^m */
+    BP_SLAB_OPT_B = 9,     /* u^{m+1} = u^m + gamma x^m; t_rows <- y-DST of V u^{m+1} + f */
+    BP_SLAB_RETA_A = 10,   /* entry sums -> sums[0..1]; keeps x^m; t_rows <- y-DST of V x^m */
+    BP_SLAB_RETA_C = 11,   /* t_rows = G V x^m: w = x - G V x; <w, x>, |w|^2 -> sums[0..2] */
+    BP_SLAB_FD_A = 12,     /* entry sums -> sums[0..1]; t_rows <- y-DST of x^m */
+    BP_SLAB_FD_B = 13,     /* t_rows = du: u^{m+1} = u^m + du; t_rows <- y-DST of V u^{m+1} + f */
+    BP_SLAB_COL_FD = 14,   /* t_cols: x-DST, x m (FourierDiag multiplier block), inverse x-DST */
+    BP_SLAB_GAMMA = 15     /* gamma from the all-reduced sums[0..2] (R_eta metric) */
 };
 typedef struct {
     int32_t rank, nranks, rows, row0, n;
     int64_t block_elems;           /* R*R complex per destination rank */
     void* t_rows;                  /* device [nranks][R][R] complex128 */
     void* t_cols;                  /* device [nranks][R][R] complex128 */
-    void* sums;                    /* device double[4] */
+    void* sums;                    /* device double[8] */
     void* u_first[2];              /* device: first / last owned row of u ping (0) and pong (1) */
     void* u_last[2];
     void* u_halo_lo[2];            /* device: halo rows (row0 - 1, row0 + R) */
@@ -281,6 +298,10 @@ int bp_slab_set_exchange(bp_problem* p, int32_t enable, void* local_t_rows, void
 int bp_slab_view(const bp_problem* p, bp_slab_view_t* v);
 /* f, u0: the FULL dense nx*ny fields (host); u0 may be null */
 int bp_slab_set_fields(bp_problem* p, const double* f, const double* u0);
+/* FourierDiagMap on slabs (correction.cpp:63-68): m is the FULL dense mode-layout multiplier
+ * (nx*ny, or nx^3, complex, host); the rank keeps the block of its own columns, i.e. the
+ * multiplier lives in the distributed mode layout of t_cols. */
+int bp_slab_set_multiplier(bp_problem* p, const double* m);
 int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter_config* cfg,
                   double a0, double a1);
 int bp_slab_active(bp_problem* p, int32_t* n_active);

@@ -709,11 +709,42 @@ void bpo_apply_V(const bpo_problem* p, const double* u_c, double* out_c) {
     for (long i = 0; i < n; ++i) out[i] = u[i] * p->v[i];
 }
 
-/* proj/src/helmholtz.cpp:41-46 */
+/* Transpose of cdr_parts' upwind convection (a real operator: its adjoint is its transpose).
+ * Row k of conv reads u_k and one upwind neighbour per direction; column m therefore collects
+ * its own diagonal entries and the rows of the neighbours whose upwind side is m.  Boundary
+ * rows whose upwind neighbour is the reflective ghost contribute nothing (c - c = 0). */
+static void cdr_conv_transpose(const bpo_problem* p, const bpo_c* y, bpo_c* out) {
+    const int nx = p->nx, ny = p->ny;
+    const double ih = (double)nx / p->lx;
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < ny; ++j) {
+            const long k = (long)i * ny + j;
+            const double vx = p->bx[k], vy = p->by[k];
+            bpo_c t = 0.0;
+            if (vx >= 0.0 && i > 0) t += vx * ih * y[k];
+            if (vx < 0.0 && i < nx - 1) t -= vx * ih * y[k];
+            if (i < nx - 1 && p->bx[k + ny] >= 0.0) t -= p->bx[k + ny] * ih * y[k + ny];
+            if (i > 0 && p->bx[k - ny] < 0.0) t += p->bx[k - ny] * ih * y[k - ny];
+            if (vy >= 0.0 && j > 0) t += vy * ih * y[k];
+            if (vy < 0.0 && j < ny - 1) t -= vy * ih * y[k];
+            if (j < ny - 1 && p->by[k + 1] >= 0.0) t -= p->by[k + 1] * ih * y[k + 1];
+            if (j > 0 && p->by[k - 1] < 0.0) t += p->by[k - 1] * ih * y[k - 1];
+            out[k] = t;
+        }
+}
+
+/* proj/src/helmholtz.cpp:41-46; CDR (c4): V^H = V^T = (sigma0 - sigma) - conv^T, the role of
+ * CdrProblem::apply_V_adjoint (proj/src/cdr.cpp:139-176) for the upwind family */
 void bpo_apply_V_adjoint(const bpo_problem* p, const double* u_c, double* out_c) {
     const bpo_c* u = (const bpo_c*)u_c;
     bpo_c* out = (bpo_c*)out_c;
     const long n = npts(p);
+    if (p->cdr) {
+        cdr_conv_transpose(p, u, out);
+        for (long i = 0; i < n; ++i) out[i] = (p->sigma0 - p->sigma[i]) * u[i] - out[i];
+        return;
+    }
     for (long i = 0; i < n; ++i) out[i] = conj(p->v[i]) * u[i];
 }
 

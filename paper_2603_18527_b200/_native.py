@@ -92,6 +92,7 @@ ABI_FUNCTIONS = {
     "bp_slab_set_exchange": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                        C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "bp_slab_set_fields": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "bp_slab_set_multiplier": (C.c_int, [C.c_void_p, _dp]),
     "bp_slab_stage": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Map), C.POINTER(IterConfig),
                                 C.c_double, C.c_double]),
     "bp_slab_active": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),

@@ -349,6 +349,7 @@ struct bp_problem {
     double2 *u_alloc0 = nullptr, *u_alloc1 = nullptr;  // u with one halo row each side
     double2* Tc = nullptr;                              // column-side block
     double* slab_sums = nullptr;
+    bool slab_fd = false;  // bp_slab_set_multiplier uploaded the rank's FourierDiag block into fd
     bool slab_running = false;
     // fused exchange (bp_slab_set_exchange)
     bool xchg_on = false;
@@ -1582,8 +1583,9 @@ CdrArgs cdr_args_range(const CdrArgs& a0, const bp_problem* p, int b0, int nb) {
     return a;
 }
 
-// A u, V u, f - A u, V u + f on real fields (ops 0, 1, 3, 4): the same upwind stencil as the
-// RC_B prologue (cdr_kernels.cuh), elementwise for the operator API
+// A u, V u, V^T u, f - A u, V u + f on real fields (ops 0 .. 4): the same upwind stencil as the
+// RC_B prologue (cdr_kernels.cuh), elementwise for the operator API; V^T is the role of
+// Problem::apply_V_adjoint (problem.hpp:28) for this real family
 __global__ void cdr_stencil_kernel(int op, const double* __restrict__ u, const double* __restrict__ f,
                                    const double* __restrict__ bx, const double* __restrict__ by,
                                    const double* __restrict__ sigma, const double* __restrict__ sigma0,
@@ -1607,6 +1609,19 @@ __global__ void cdr_stencil_kernel(int op, const double* __restrict__ u, const d
         switch (op) {
             case 0: r = (lap + conv) + sg * c; break;
             case 1: r = (sigma0[b] - sg) * c - conv; break;
+            case 2: {  // V^T u: the transposed upwind stencil (column idx of conv)
+                double t = 0.0;
+                if (vx >= 0.0 && i > 0) t += vx * ih * c;
+                if (vx < 0.0 && i < n - 1) t -= vx * ih * c;
+                if (i < n - 1 && bx[idx + n] >= 0.0) t -= bx[idx + n] * ih * e;
+                if (i > 0 && bx[idx - n] < 0.0) t += bx[idx - n] * ih * w;
+                if (vy >= 0.0 && j > 0) t += vy * ih * c;
+                if (vy < 0.0 && j < n - 1) t -= vy * ih * c;
+                if (j < n - 1 && by[idx + 1] >= 0.0) t -= by[idx + 1] * ih * no;
+                if (j > 0 && by[idx - 1] < 0.0) t += by[idx - 1] * ih * so;
+                r = (sigma0[b] - sg) * c - t;
+                break;
+            }
             case 3: r = f[idx] - ((lap + conv) + sg * c); break;
             default: r = ((sigma0[b] - sg) * c - conv) + f[idx]; break;
         }
@@ -2292,9 +2307,13 @@ int create_cdr_impl(const bp_grid* grid, int32_t batch, const double* bx, const 
 // collectives between them: all-to-all of the blocked row-side T (t_rows) into the column-side
 // block (t_cols) and back, the u halo-row exchange, and the all-reduce of the two trace sums.
 
-__global__ void slab_finalize_kernel(Control c, const double* sums) {
-    if (threadIdx.x == 0 && blockIdx.x == 0 && c.status[0] == ST_ACTIVE)
-        finalize_entry(c, 0, c.sweep[0], sums[0], sums[1]);
+// entry != 0: trace entry m + termination test from sums[0..1]; gamma_off >= 0: the
+// optimal-scalar gamma (correction.cpp:10-18) from sums[gamma_off .. gamma_off + 2]
+__global__ void slab_finalize_kernel(Control c, const double* sums, int entry, int gamma_off) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && c.status[0] == ST_ACTIVE) {
+        if (gamma_off >= 0) finalize_gamma(c, 0, sums[gamma_off], sums[gamma_off + 1], sums[gamma_off + 2]);
+        if (entry) finalize_entry(c, 0, c.sweep[0], sums[0], sums[1]);
+    }
 }
 
 // dense reference rows (nx*ny interior, x slow) -> padded slab rows [row0, row0 + R) (host)
@@ -2448,6 +2467,7 @@ static int slab_create_impl(const bp_grid* grid, int dim, int32_t rank, int32_t 
         ColArgs c{};
         CUF(launch_col_pp(log2n, 16, CL_SLAB, C_GREEN, c, nullptr, true));
         CUF(launch_col_pp(log2n, 16, CL_SLAB, C_ONE, c, nullptr, true));
+        CUF(launch_col_pp(log2n, 16, CL_SLAB, C_FD, c, nullptr, true));
         if (dim == 3) CUF(launch_col_pp(log2n, 16, CL_YBLK, C_ONE, c, nullptr, true));
         if (log2n >= 6) CUF(launch_tri(log2n, CL_SLAB, c, nullptr, true));
     }
@@ -2463,8 +2483,8 @@ static int slab_create_impl(const bp_grid* grid, int dim, int32_t rank, int32_t 
     }
     p->u0 = p->u_alloc0 + halo;
     p->u1 = p->u_alloc1 + halo;
-    CUF(cudaMalloc(&p->slab_sums, sizeof(double) * 4));
-    CUF(cudaMemsetAsync(p->slab_sums, 0, sizeof(double) * 4, p->stream));
+    CUF(cudaMalloc(&p->slab_sums, sizeof(double) * 8));
+    CUF(cudaMemsetAsync(p->slab_sums, 0, sizeof(double) * 8, p->stream));
     CUF(cudaMalloc(&p->partial, sizeof(double) * (size_t)R * (dim == 3 ? n : 1) * kPartStride));
     CUF(cudaMalloc(&p->gamma, sizeof(double2)));
     CUF(cudaMalloc(&p->norm_part, sizeof(double) * 64));
@@ -2606,6 +2626,31 @@ int bp_slab_set_fields(bp_problem* p, const double* f, const double* u0) {
     return BP_OK;
 }
 
+int bp_slab_set_multiplier(bp_problem* p, const double* m) {
+    if (int rc = check_problem(p)) return rc;
+    if (!p->slab_log2 || !m) return set_err(BP_EINVAL, "slab: null multiplier or not a slab problem");
+    DeviceGuard guard(p->device);
+    // the rank's block of m in the t_cols layout: line (row) px = the x mode, column qa = the
+    // rank's y mode (2-D) / (y, z) mode pair (3-D); Dirichlet zero modes stay 0
+    const int n = p->n, nd = n - 1, R = 1 << p->slab_log2, col0 = p->slab_rank * R;
+    const size_t cols = p->dim == 3 ? (size_t)R * n : (size_t)R;
+    std::vector<double2> blk((size_t)n * cols, make_double2(0.0, 0.0));
+    for (int px = 1; px < n; ++px)
+        for (size_t qa = 0; qa < cols; ++qa) {
+            const int yq = col0 + (p->dim == 3 ? (int)(qa >> p->log2n) : (int)qa);
+            const int zq = p->dim == 3 ? (int)(qa & (size_t)(n - 1)) : 1;
+            if (yq == 0 || zq == 0) continue;
+            const size_t di = p->dim == 3 ? ((size_t)(px - 1) * nd + (yq - 1)) * nd + (zq - 1)
+                                          : (size_t)(px - 1) * nd + (yq - 1);
+            blk[(size_t)px * cols + qa] = make_double2(m[2 * di], m[2 * di + 1]);
+        }
+    if (!p->fd) CU(cudaMalloc(&p->fd, sizeof(double2) * blk.size()));
+    CU(cudaMemcpyAsync(p->fd, blk.data(), sizeof(double2) * blk.size(), cudaMemcpyHostToDevice, p->stream));
+    CU(cudaStreamSynchronize(p->stream));  // the staging vector goes out of scope
+    p->slab_fd = true;
+    return BP_OK;
+}
+
 int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter_config* cfg,
                   double a0, double a1) {
     if (int rc = check_problem(p)) return rc;
@@ -2623,8 +2668,11 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
             if (d3)
                 if (int rc = slab_ylines(p, a.ctl, true)) return rc;
             return norms(p, p->f, p->slab_sums, true);
-        case BP_SLAB_COL: {  // column (x-line) pass on the rank's received block
+        case BP_SLAB_COL:
+        case BP_SLAB_COL_FD: {  // column (x-line) pass on the rank's received block
             ColArgs c = col_args(p);
+            if (stage == BP_SLAB_COL_FD && !p->slab_fd)
+                return set_err(BP_EINVAL, "slab FourierDiag: bp_slab_set_multiplier first");
             c.T = p->Tc;
             c.slab_cols = (1 << p->slab_log2) * (d3 ? p->n : 1);  // 3-D: (y, z) pairs
             c.col0 = p->slab_rank * (1 << p->slab_log2);
@@ -2637,7 +2685,10 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
                 c.xchg_log2r = p->slab_log2;
                 for (int r = 0; r < p->slab_nranks; ++r) c.xchg[r] = p->xchg_rows[r];
             }
-            if (p->tri && c.slab_cols % tri_cols_per_cta(p->log2n) == 0) {
+            if (stage == BP_SLAB_COL_FD) {  // x-DST, x m (correction.cpp:63-68), inverse x-DST
+                c.fd = p->fd;
+                CU(launch_col_pp(p->log2n, 16, CL_SLAB, C_FD, c, p->stream));
+            } else if (p->tri && c.slab_cols % tri_cols_per_cta(p->log2n) == 0) {
                 CU(launch_tri(p->log2n, CL_SLAB, c, p->stream));
             } else {
                 CU(launch_col_pp(p->log2n, 16, CL_SLAB, C_GREEN, c, p->stream));
@@ -2656,6 +2707,9 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
             if (!(cfg->rtol > 0.0 && cfg->rtol < 1.0)) return set_err(BP_EINVAL, "run: rtol must lie in (0,1)");
             if (cfg->max_iters < 1) return set_err(BP_EINVAL, "run: max_iters must be >= 1");
             if (!(a0 > 0.0)) return set_err(BP_EINVAL, "run: zero source");
+            if (cfg->format != BP_FMT_NPBS && cfg->format != BP_FMT_CBS)
+                return set_err(cfg->format == BP_FMT_DIRECT ? BP_ENOTSUP : BP_EINVAL,
+                               "slab decomposition: the CBS / NPBS formats");
             if (int rc = ensure_trace(p, cfg->max_iters)) return rc;
             p->slab_max_iters = cfg->max_iters;
             p->slab_rtol = cfg->rtol;
@@ -2678,7 +2732,8 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
             return BP_OK;
         case BP_SLAB_SWEEP:  // fused scalar / pointwise sweep; sums[0..1] = local entry sums
             if (!map || (map->kind != BP_MAP_SCALAR && map->kind != BP_MAP_POINTWISE))
-                return set_err(BP_ENOTSUP, "slab decomposition: scalar and pointwise maps only");
+                return set_err(BP_EINVAL, "BP_SLAB_SWEEP is the scalar / pointwise sweep (the other maps "
+                                          "run BP_SLAB_OPT_* / RETA_* / FD_*)");
             a.map_kind = map->kind;
             a.gamma = make_double2(map->gamma_re, map->gamma_im);
             if (d3)
@@ -2689,10 +2744,35 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
         case BP_SLAB_ZERO_U:
             CU(cudaMemsetAsync(p->u_alloc0, 0, sizeof(double2) * (p->field + 2 * slab_halo(p)), p->stream));
             return BP_OK;
-        case BP_SLAB_FINALIZE:  // sums hold the all-reduced entry sums
-            slab_finalize_kernel<<<1, 32, 0, p->stream>>>(a.ctl, p->slab_sums);
+        case BP_SLAB_FINALIZE:  // sums hold the all-reduced entry sums (a0 = 1: + gamma from sums[2..4])
+            slab_finalize_kernel<<<1, 32, 0, p->stream>>>(a.ctl, p->slab_sums, 1, a0 == 1.0 ? 2 : -1);
             CU(cudaGetLastError());
             return BP_OK;
+        case BP_SLAB_GAMMA:  // sums[0..2] hold the all-reduced <w, x> and |w|^2 (R_eta metric)
+            slab_finalize_kernel<<<1, 32, 0, p->stream>>>(a.ctl, p->slab_sums, 0, 0);
+            CU(cudaGetLastError());
+            return BP_OK;
+        // OptimalScalar / FourierDiag sweeps (plan_for's row stages; the driver puts the
+        // reductions, BP_SLAB_FINALIZE / BP_SLAB_GAMMA and the column passes between them)
+        case BP_SLAB_OPT_A:   // entry sums + <w, r>, |w|^2 -> sums[0..4]; x^m -> X
+        case BP_SLAB_RETA_A:  // entry sums -> sums[0..1]; x^m -> X; t_rows <- y-DST of V x^m
+        case BP_SLAB_RETA_C:  // t_rows = G V x: w = x - G V x; <w, x>, |w|^2 -> sums[0..2]
+        case BP_SLAB_OPT_B:   // u^{m+1} = u^m + gamma x^m; t_rows <- y-DST of V u^{m+1} + f
+        case BP_SLAB_FD_A:    // entry sums -> sums[0..1]; t_rows <- y-DST of x^m
+        case BP_SLAB_FD_B: {  // t_rows = du: u^{m+1} = u^m + du; t_rows <- y-DST of V u^{m+1} + f
+            const int mode = stage == BP_SLAB_OPT_A    ? R_OPT_A
+                             : stage == BP_SLAB_RETA_A ? R_RETA_A
+                             : stage == BP_SLAB_RETA_C ? R_RETA_C
+                             : stage == BP_SLAB_OPT_B  ? R_OPT_B
+                             : stage == BP_SLAB_FD_A   ? R_FD_A
+                                                       : R_FD_B;
+            const bool inv = mode != R_OPT_B, fwd = mode != R_OPT_A && mode != R_RETA_C;
+            if (d3 && inv)
+                if (int rc = slab_ylines(p, a.ctl)) return rc;
+            CU(launch_row(p->log2n, dim, mode, a, p->stream));
+            if (d3 && fwd) return slab_ylines(p, a.ctl, true);
+            return BP_OK;
+        }
     }
     return set_err(BP_EINVAL, "unknown slab stage");
 }
@@ -2838,7 +2918,6 @@ static int pointwise_op(const bp_problem* cp, int op, const double* u, const dou
     auto* p = const_cast<bp_problem*>(cp);
     DeviceGuard guard(p->device);
     if (p->cdr) {
-        if (op == 2) return set_err(BP_ENOTSUP, "CDR family: V is not normal; no adjoint on the GPU");
         if (int rc = cdr_upload(p, u, p->x)) return rc;
         if (op == 3)
             if (int rc = cdr_upload(p, f, p->f)) return rc;

@@ -146,8 +146,9 @@ struct RowArgs {
     // x-slab of a grid distributed over ranks (2-D, batch 1; 0 = whole members): the launch
     // covers 2^slab_log2 rows starting at global row row0; u / k2 / f hold those rows (u with
     // one halo row on each side), T is blocked [dest rank][row][col within the dest's block]
-    // for the all-to-all, and ENTRY modes write their per-slab sums to slab_sums instead of
-    // finalising (the driver all-reduces them and launches finalize_kernel)
+    // for the all-to-all, and the reducing modes write their per-slab sums (RowSpec::NPART of
+    // them: entry sums, then the optimal-scalar numerator / denominator) to slab_sums instead
+    // of finalising (the driver all-reduces them and launches slab_finalize_kernel)
     int slab_log2;
     int row0;
     double* slab_sums;
@@ -772,13 +773,13 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
                         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s[k] += red[k][w];
                     }
                     a.ctl.counter[b] = 0u;
-                    if constexpr (MODE == R_OPT_A) finalize_gamma(a.ctl, b, s[2], s[3], s[4]);
-                    if constexpr (MODE == R_RETA_C) finalize_gamma(a.ctl, b, s[0], s[1], s[2]);
-                    if constexpr (S::ENTRY) {
-                        if constexpr (SLAB) {
-                            a.slab_sums[2 * b] = s[0];
-                            a.slab_sums[2 * b + 1] = s[1];
-                        } else {
+                    if constexpr (SLAB) {  // this rank's sums; finalised after the all-reduce
+#pragma unroll
+                        for (int k = 0; k < S::NPART; ++k) a.slab_sums[k] = s[k];
+                    } else {
+                        if constexpr (MODE == R_OPT_A) finalize_gamma(a.ctl, b, s[2], s[3], s[4]);
+                        if constexpr (MODE == R_RETA_C) finalize_gamma(a.ctl, b, s[0], s[1], s[2]);
+                        if constexpr (S::ENTRY) {
                             // m of this member (thread 0's own line may be a padding line, for
                             // which m was not read); the counter is advanced only here
                             const int mb = __ldcg(&a.ctl.sweep[b]) - (S::POST ? 1 : 0);
@@ -808,15 +809,13 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
             for (int k = 0; k < S::NPART; ++k) s[k] = pol.sum(s[k], t);
             if (t == 0) {
                 a.ctl.counter[b] = 0u;
-                if constexpr (MODE == R_OPT_A) finalize_gamma(a.ctl, b, s[2], s[3], s[4]);
-                if constexpr (MODE == R_RETA_C) finalize_gamma(a.ctl, b, s[0], s[1], s[2]);
-                if constexpr (S::ENTRY) {
-                    if constexpr (SLAB) {  // partial sums of this rank, finalised after the all-reduce
-                        a.slab_sums[2 * b] = s[0];
-                        a.slab_sums[2 * b + 1] = s[1];
-                    } else {
-                        finalize_entry(a.ctl, b, m, s[0], s[1]);
-                    }
+                if constexpr (SLAB) {  // this rank's sums (batch 1), finalised after the all-reduce
+#pragma unroll
+                    for (int k = 0; k < S::NPART; ++k) a.slab_sums[k] = s[k];
+                } else {
+                    if constexpr (MODE == R_OPT_A) finalize_gamma(a.ctl, b, s[2], s[3], s[4]);
+                    if constexpr (MODE == R_RETA_C) finalize_gamma(a.ctl, b, s[0], s[1], s[2]);
+                    if constexpr (S::ENTRY) finalize_entry(a.ctl, b, m, s[0], s[1]);
                 }
             }
         }
@@ -1119,7 +1118,10 @@ __device__ __forceinline__ void col_group(const ColArgs& a, const int bid) {
             double2 w;
             if constexpr (MODE == C_FD) {
                 // FourierDiag m (correction.cpp:63-68), padded mode layout shared by the batch
-                const size_t fi = LAYOUT == CL_X3 ? ((size_t)p * N + yl) * N + q : (size_t)p * N + q;
+                // (CL_SLAB: the rank's own n x slab_cols block of m, in the t_cols layout)
+                const size_t fi = LAYOUT == CL_X3     ? ((size_t)p * N + yl) * N + q
+                                  : LAYOUT == CL_SLAB ? (size_t)p * LS + qa
+                                                      : (size_t)p * N + q;
                 w = cscale(a.fd[fi], a.scale);
             } else if constexpr (MODE == C_GREEN) {
                 const double s = a.scale * rcp_green(fma(lr, lr, li * li));

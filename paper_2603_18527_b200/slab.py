@@ -13,7 +13,11 @@ the y-DSTs (rows: local), the x-DSTs (columns: every rank's rows) and the five-p
     all-to-all        back
 
 which is bp::run (proj/src/iterate.cpp:88-153) with the transposes of the distributed
-transform.  The driver is written against two small interfaces so the same host logic runs
+transform.  That is the scalar / pointwise sweep; OptimalScalarMap (both metrics) and
+FourierDiagMap (correction.cpp:22-76) run the staged sweeps of `_sweep_for`: their extra global
+reductions (<w, r>, <w, w>) are all-reduced with the entry sums, the R_eta metric and FourierDiag
+take a second distributed transform pair per sweep, and the FourierDiag multiplier lives in
+the distributed mode layout (each rank holds the block of its own columns).  The driver is written against two small interfaces so the same host logic runs
 
   * on GPUs: `SlabPart` (the C-ABI slab handle, include/bornsweep.h bp_slab_*) with
     `DistComm` (torch.distributed, NCCL) -- one part per process, or with `LocalComm` -- several
@@ -32,7 +36,8 @@ import numpy as np
 from . import _native as N
 from .api import BC_DIRICHLET, TERMINATION, IterationConfig, IterationTrace, ScalarMap, _check, _ptr
 
-FWD_F, COL, INV_NORM, INIT, FWD_BORN, SWEEP, FINALIZE, ZERO_U = range(8)
+(FWD_F, COL, INV_NORM, INIT, FWD_BORN, SWEEP, FINALIZE, ZERO_U, OPT_A, OPT_B, RETA_A, RETA_C, FD_A, FD_B,
+ COL_FD, GAMMA) = range(16)
 POLL_SWEEPS = 16
 
 
@@ -81,7 +86,7 @@ class SlabPart:
         # per destination: R x R (2-D) / R x R x n (3-D) complex, flattened
         self.t_rows = _dev_tensor(v.t_rows, (nranks, v.block_elems), "<c16", d)
         self.t_cols = _dev_tensor(v.t_cols, (nranks, v.block_elems), "<c16", d)
-        self.sums = _dev_tensor(v.sums, (4,), "<f8", d)
+        self.sums = _dev_tensor(v.sums, (8,), "<f8", d)
         self.u_first = [_dev_tensor(v.u_first[k], (hl,), "<c16", d) for k in range(2)]
         self.u_last = [_dev_tensor(v.u_last[k], (hl,), "<c16", d) for k in range(2)]
         self.u_halo_lo = [_dev_tensor(v.u_halo_lo[k], (hl,), "<c16", d) for k in range(2)]
@@ -123,6 +128,13 @@ class SlabPart:
         f = np.ascontiguousarray(np.asarray(f, np.complex128))
         u0 = None if u0 is None else np.ascontiguousarray(np.asarray(u0, np.complex128))
         _check(self._lib.bp_slab_set_fields(self._h, _ptr(f), _ptr(u0)))
+
+    def set_multiplier(self, m):
+        """FourierDiagMap multiplier (full dense mode layout); the rank keeps its column block."""
+        m = np.ascontiguousarray(np.asarray(m, np.complex128))
+        if m.shape != tuple(self.shape):
+            raise ValueError(f"FourierDiag multiplier shape {m.shape} != grid {tuple(self.shape)}")
+        _check(self._lib.bp_slab_set_multiplier(self._h, _ptr(m)))
 
     def stage(self, code: int, cmap=None, config: IterationConfig | None = None, a0=0.0, a1=0.0):
         mp = cmap._c() if cmap is not None else None
@@ -313,13 +325,46 @@ def run_slab(parts, comm, cmap, f, config: IterationConfig | None = None, u0=Non
     col_pass()
     launched = 0
 
+    def stage_all(code, **kw):
+        for p in parts:
+            p.stage(code, **kw)
+
+    kind = type(cmap).__name__
+    if kind == "FourierDiagMap":
+        for p in parts:
+            p.set_multiplier(cmap.m)
+
     def sweep(k):
+        # the launch sequences of plan_for (csrc/bornsweep.cu) with the collectives between
         comm.halo(parts, k & 1)
-        for p in parts:
-            p.stage(SWEEP, cmap=cmap)
-        comm.allreduce(parts)
-        for p in parts:
-            p.stage(FINALIZE)
+        if kind == "OptimalScalarMap" and cmap.metric == "euclidean":
+            stage_all(OPT_A)            # entry sums + <w, r>, |w|^2 with w = A x (correction.cpp:33-36)
+            comm.allreduce(parts, 5)
+            stage_all(FINALIZE, a0=1.0)  # entry m and gamma = <w, r> / <w, w>
+            stage_all(OPT_B)
+        elif kind == "OptimalScalarMap":
+            if cmap.metric != "reta":
+                raise ValueError(f"unknown optimal-scalar metric {cmap.metric!r}")
+            stage_all(RETA_A)           # entry sums; V x -> forward transform
+            comm.allreduce(parts)
+            stage_all(FINALIZE)
+            col_pass()                  # G V x
+            stage_all(RETA_C)           # w = x - G V x (correction.cpp:38-44): <w, x>, |w|^2
+            comm.allreduce(parts, 3)
+            stage_all(GAMMA)
+            stage_all(OPT_B)
+        elif kind == "FourierDiagMap":
+            stage_all(FD_A)             # entry sums; x -> forward transform
+            comm.allreduce(parts)
+            stage_all(FINALIZE)
+            comm.transpose(parts, True)
+            stage_all(COL_FD)           # x m in mode space (correction.cpp:63-68)
+            comm.transpose(parts, False)
+            stage_all(FD_B)
+        else:
+            stage_all(SWEEP, cmap=cmap)
+            comm.allreduce(parts)
+            stage_all(FINALIZE)
         col_pass()
 
     if graph and _graphable(parts):
@@ -327,8 +372,8 @@ def run_slab(parts, comm, cmap, f, config: IterationConfig | None = None, u0=Non
         prev = [p.stream for p in parts]
         # one capture per (parts, comm, map, config): later calls replay it (capture and
         # instantiation cost milliseconds -- a bench step is ~100 ms)
-        key = (id(comm), type(cmap).__name__, getattr(cmap, "gamma", None), config.format, config.rtol,
-               config.max_iters)
+        key = (id(comm), kind, getattr(cmap, "gamma", None), getattr(cmap, "metric", None), config.format,
+               config.rtol, config.max_iters)
         cache = parts[0].__dict__.setdefault("_graphs", {})
         if key not in cache:
             cap = torch.cuda.Stream(device=parts[0].device)

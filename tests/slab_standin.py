@@ -13,7 +13,8 @@ import scipy.fft as sf
 import torch
 
 from paper_2603_18527_b200.api import TERMINATION, IterationTrace
-from paper_2603_18527_b200.slab import COL, FINALIZE, FWD_BORN, FWD_F, INIT, INV_NORM, SWEEP, ZERO_U
+from paper_2603_18527_b200.slab import (COL, COL_FD, FD_A, FD_B, FINALIZE, FWD_BORN, FWD_F, GAMMA, INIT, INV_NORM,
+                                        OPT_A, OPT_B, RETA_A, RETA_C, SWEEP, ZERO_U)
 
 
 def _sine(a):
@@ -39,7 +40,7 @@ class NumpySlabPart:
         self.lap = 4.0 / self.h ** 2 * np.sin(j * np.pi / (2 * n)) ** 2
         self._T = np.zeros((nranks, R, R), np.complex128)
         self._Tc = np.zeros((nranks, R, R), np.complex128)
-        self._sums = np.zeros(4)
+        self._sums = np.zeros(8)
         self._u = [np.zeros((R + 2, n), np.complex128) for _ in range(2)]
         self.t_rows, self.t_cols = torch.from_numpy(self._T), torch.from_numpy(self._Tc)
         self.sums = torch.from_numpy(self._sums)
@@ -100,9 +101,100 @@ class NumpySlabPart:
             self.iters, self.term, self.result_buf, self.status = m, term, m & 1, 1
         self.sweep = m + 1
 
+    # ---- primitives of the staged OptimalScalar / FourierDiag sweeps (2-D; overridden in 3-D)
+    def _rows_fwd(self, field):
+        self._block(_sine(field))
+
+    def _rows_inv(self):
+        return _sine(self._unblock())
+
+    def _interior(self):
+        return self.valid[:, None] & (np.arange(self.n) != 0)[None, :]
+
+    def _stencil(self, ua):
+        R = self.rows
+        u = ua[1:R + 1]
+        uw = np.zeros_like(u)
+        uw[:, 1:] = u[:, :-1]
+        ue = np.zeros_like(u)
+        ue[:, :-1] = u[:, 1:]
+        return 4.0 * u - ua[0:R] - ua[2:R + 2] - uw - ue
+
+    def _mode_weights(self):
+        """(x mode, local column) mask of the non-zero Dirichlet modes, t_cols layout"""
+        n, R = self.n, self.rows
+        q = self.rank * R + np.arange(R)
+        w = np.ones((n, R))
+        w[0, :] = 0
+        w[:, q == 0] = 0
+        return w
+
+    def set_multiplier(self, m):
+        n, R = self.n, self.rows
+        full = np.zeros((n, n), np.complex128)
+        full[1:, 1:] = np.asarray(m, np.complex128)
+        self.fd = full[:, self.rank * R:(self.rank + 1) * R].copy()
+
+    def _col_fd(self):
+        n, R = self.n, self.rows
+        M = self._Tc.reshape(n, -1)
+        scale = (2.0 / n) ** (3 if M.shape[1] != R else 2)  # forward x inverse sine sums
+        M[...] = _sine_ax(_sine_ax(M, 0) * (self.fd.reshape(n, -1) * scale), 0)
+
+    def _map_stage(self, code):
+        """OPT_A / OPT_B / RETA_A / RETA_C / FD_A / FD_B (csrc/sweep_kernels.cuh RowMode)."""
+        if self.status != 0:
+            return
+        R = self.rows
+        mask = self._interior()
+        if code in (OPT_A, RETA_A, FD_A):  # entry modes: m = sweep
+            ua = self._u[self.sweep & 1]
+            u = ua[1:R + 1]
+            r = self.f - (self._stencil(ua) / self.h ** 2 - self.k2 * u)
+            x = (self._rows_inv() - u) * mask
+            self._sums[0] = np.sum((np.abs(r) ** 2)[mask])
+            self._sums[1] = np.sum((np.abs(x) ** 2)[mask])
+            if code == OPT_A:  # w = A x = r - V x (key identity), gamma = <w, r> / <w, w>
+                w = (r - self.V * x)[mask]
+                num = np.vdot(w, r[mask])
+                self._sums[2:5] = num.real, num.imag, np.sum(np.abs(w) ** 2)
+                self.x = x
+            elif code == RETA_A:
+                self.x = x
+                self._rows_fwd(self.V * x)
+            else:
+                self._rows_fwd(x)
+            return
+        m = self.sweep - 1  # post modes: entry m was recorded
+        if code == RETA_C:
+            w = (self.x - self._rows_inv())[mask]
+            num = np.vdot(w, self.x[mask])
+            self._sums[0:3] = num.real, num.imag, np.sum(np.abs(w) ** 2)
+            return
+        u = self._u[m & 1][1:R + 1]
+        du = self.gamma * self.x if code == OPT_B else self._rows_inv()
+        unew = (u + du) * mask
+        nxt = self._u[(m + 1) & 1][1:R + 1]
+        nxt[self.valid] = unew[self.valid]
+        self._rows_fwd(self.V * nxt + self.f)
+
+    def _gamma(self, off):
+        if self.status != 0:
+            return
+        num = complex(self._sums[off], self._sums[off + 1])
+        den = self._sums[off + 2]
+        self.gamma = num / den if den > 0 and math.isfinite(den) else 0.0
+
     def stage(self, code, cmap=None, config=None, a0=0.0, a1=0.0):
         R, n = self.rows, self.n
-        if code == FWD_F:
+        if code in (OPT_A, OPT_B, RETA_A, RETA_C, FD_A, FD_B):
+            self._map_stage(code)
+        elif code == GAMMA:
+            self._gamma(0)
+        elif code == COL_FD:
+            if self.status == 0:
+                self._col_fd()
+        elif code == FWD_F:
             self._block(_sine(self.f))
             self._sums[0] = np.sum(np.abs(self.f) ** 2)
         elif code == COL:
@@ -157,6 +249,8 @@ class NumpySlabPart:
             self._block(_sine(self.V * nxt + self.f))
         elif code == FINALIZE:
             if self.status == 0:
+                if a0 == 1.0:
+                    self._gamma(2)
                 self._finalize(self._sums[0], self._sums[1])
         elif code == ZERO_U:
             self._u[0][...] = 0
@@ -203,7 +297,7 @@ class NumpySlabPart3(NumpySlabPart):
         self.lap = 4.0 / self.h ** 2 * np.sin(j * np.pi / (2 * n)) ** 2
         self._T = np.zeros((nranks, R * R * n), np.complex128)
         self._Tc = np.zeros((nranks, R * R * n), np.complex128)
-        self._sums = np.zeros(4)
+        self._sums = np.zeros(8)
         self._u = [np.zeros((R + 2, n, n), np.complex128) for _ in range(2)]
         self.t_rows, self.t_cols = torch.from_numpy(self._T), torch.from_numpy(self._Tc)
         self.sums = torch.from_numpy(self._sums)
@@ -241,9 +335,40 @@ class NumpySlabPart3(NumpySlabPart):
         if u0 is not None:
             self._u[0][1:self.rows + 1] = self._pack(np.asarray(u0, np.complex128))
 
+    def _rows_fwd(self, field):
+        self._block(self._yz(field))
+
+    def _rows_inv(self):
+        return self._yz(self._unblock())
+
+    def _interior(self):
+        j = np.arange(self.n) != 0
+        return self.valid[:, None, None] & j[None, :, None] & j[None, None, :]
+
+    def _stencil(self, ua):
+        R = self.rows
+        u = ua[1:R + 1]
+        s = 6.0 * u - ua[0:R] - ua[2:R + 2]
+        for ax in (1, 2):
+            lo, hi = np.zeros_like(u), np.zeros_like(u)
+            a, b = [slice(None)] * 3, [slice(None)] * 3
+            a[ax], b[ax] = slice(1, None), slice(None, -1)
+            lo[tuple(a)] = u[tuple(b)]
+            hi[tuple(b)] = u[tuple(a)]
+            s = s - lo - hi
+        return s
+
+    def set_multiplier(self, m):
+        n, R = self.n, self.rows
+        full = np.zeros((n, n, n), np.complex128)
+        full[1:, 1:, 1:] = np.asarray(m, np.complex128)
+        self.fd = full[:, self.rank * R:(self.rank + 1) * R, :].copy()
+
     def stage(self, code, cmap=None, config=None, a0=0.0, a1=0.0):
         R, n = self.rows, self.n
-        if code == FWD_F:
+        if code in (OPT_A, OPT_B, RETA_A, RETA_C, FD_A, FD_B, GAMMA, COL_FD):
+            NumpySlabPart.stage(self, code, cmap, config, a0, a1)
+        elif code == FWD_F:
             self._block(self._yz(self.f))
             self._sums[0] = np.sum(np.abs(self.f) ** 2)
         elif code == COL:

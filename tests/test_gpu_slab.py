@@ -82,8 +82,88 @@ def test_slab_errors(gpu):
     parts = parts_for(k2, k0, eta, 2)
     with pytest.raises(ValueError, match="zero source"):
         run_slab(parts, LocalComm(), bs.ScalarMap(1.0), np.zeros_like(f))
-    with pytest.raises(NotImplementedError):
-        run_slab(parts, LocalComm(), bs.OptimalScalarMap(), f)
+    with pytest.raises(NotImplementedError):  # IterFormat::Direct: single-device handles only
+        run_slab(parts, LocalComm(), bs.ScalarMap(1.0), f, bs.IterationConfig(format="direct"))
+    with pytest.raises(ValueError):
+        run_slab(parts, LocalComm(), bs.FourierDiagMap(np.ones((3, 3), complex)), f)
+
+
+# ------------------------------------------------- OptimalScalar / FourierDiag maps on slabs
+def fd_multiplier(shape, seed=11):
+    rng = np.random.default_rng(seed)
+    return 0.9 + 0.05 * (rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+
+
+def staged_maps(shape):
+    return [bs.OptimalScalarMap("euclidean"), bs.OptimalScalarMap("reta"), bs.FourierDiagMap(fd_multiplier(shape))]
+
+
+def oracle_map_run(k2, f, k0, eta, cmap, rtol, max_iters):
+    from oracle import MAP_FOURIER_DIAG, MAP_OPTIMAL_SCALAR, METRIC_EUCLIDEAN, METRIC_RETA
+    p = OracleProblem(k2, k0, eta)
+    if isinstance(cmap, bs.FourierDiagMap):
+        return p.run(f, map_kind=MAP_FOURIER_DIAG, m=cmap.m, rtol=rtol, max_iters=max_iters)
+    metric = METRIC_EUCLIDEAN if cmap.metric == "euclidean" else METRIC_RETA
+    return p.run(f, map_kind=MAP_OPTIMAL_SCALAR, metric=metric, rtol=rtol, max_iters=max_iters)
+
+
+MAP_IDS = ["optimal_l2", "optimal_reta", "fourier_diag"]
+
+
+@pytest.mark.parametrize("n,nranks", [(64, 1), (64, 2), (64, 8), (256, 4)])
+@pytest.mark.parametrize("which", [0, 1, 2], ids=MAP_IDS)
+def test_slab_staged_maps_match_oracle(gpu, n, nranks, which):
+    """correction.cpp:22-76 on a slab-decomposed grid: the optimal-scalar reductions are
+    all-reduced with the entry sums, the FourierDiag multiplier is held per column block."""
+    k2, f, k0, eta = instance(n)
+    cmap = staged_maps(k2.shape)[which]
+    cfg = bs.IterationConfig(rtol=1e-7, max_iters=4000)
+    res = run_slab(parts_for(k2, k0, eta, nranks), LocalComm(), cmap, f, cfg)
+    ref = oracle_map_run(k2, f, k0, eta, cmap, 1e-7, 4000)
+    assert res.trace.terminated == ref.terminated
+    assert abs(res.trace.iters - ref.iters) <= 1
+    # a run that stops one sweep apart (the residual crosses rtol within roundoff of the
+    # threshold) differs by that sweep's update, O(rtol); equal counts compare at 1e-10
+    assert rel(res.u, ref.u) < (FIELD_TOL if res.trace.iters == ref.iters else 1e-7)
+    k = min(res.trace.iters, ref.iters) + 1
+    np.testing.assert_allclose(res.trace.res_l2_rel[:k], ref.res_l2[:k], rtol=1e-7, atol=1e-13)
+    np.testing.assert_allclose(res.trace.res_reta_rel[:k], ref.res_reta[:k], rtol=1e-7, atol=1e-13)
+    # the iterate after a fixed number of sweeps, within the north_star's 1e-10
+    m = min(60, ref.iters - 1)
+    cfg_m = bs.IterationConfig(rtol=1e-7, max_iters=m)
+    res_m = run_slab(parts_for(k2, k0, eta, nranks), LocalComm(), cmap, f, cfg_m)
+    ref_m = oracle_map_run(k2, f, k0, eta, cmap, 1e-7, m)
+    assert res_m.trace.iters == ref_m.iters == m
+    assert rel(res_m.u, ref_m.u) < FIELD_TOL
+
+
+@pytest.mark.parametrize("which", [0, 1, 2], ids=MAP_IDS)
+def test_slab_staged_maps_match_single_gpu_path(gpu, which):
+    k2, f, k0, eta = instance(256, seed=7)
+    cmap = staged_maps(k2.shape)[which]
+    cfg = bs.IterationConfig(rtol=1e-6, max_iters=40)
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        one = bs.run(p, cmap, f, cfg)
+    for fused in (False, True):
+        res = run_slab(parts_for(k2, k0, eta, 4), LocalComm(fused=fused), cmap, f, cfg)
+        assert res.trace.iters == one.trace.iters
+        assert rel(res.u, one.u) < 1e-11
+        np.testing.assert_allclose(res.trace.res_l2_rel, one.trace.res_l2_rel, rtol=1e-10)
+
+
+@pytest.mark.parametrize("n,nranks", [(32, 2), (64, 4)])
+@pytest.mark.parametrize("which", [0, 1, 2], ids=MAP_IDS)
+def test_slab3d_staged_maps_match_oracle(gpu, n, nranks, which):
+    k2, f, k0, eta = inst3(n, seed=n + nranks)
+    cmap = staged_maps(k2.shape)[which]
+    cfg = bs.IterationConfig(rtol=1e-7, max_iters=2000)
+    res = run_slab([SlabPart(k2, k0, eta, r, nranks) for r in range(nranks)], LocalComm(), cmap, f, cfg)
+    ref = oracle_map_run(k2, f, k0, eta, cmap, 1e-7, 2000)
+    assert res.trace.terminated == ref.terminated
+    assert abs(res.trace.iters - ref.iters) <= 1
+    assert rel(res.u, ref.u) < FIELD_TOL
+    k = min(res.trace.iters, ref.iters) + 1
+    np.testing.assert_allclose(res.trace.res_l2_rel[:k], ref.res_l2[:k], rtol=1e-8, atol=1e-13)
 
 
 # ---------------------------------------------------------------------------- 3-D slabs (c3)

@@ -73,6 +73,29 @@ def test_oracle_cdr_splitting_identities():
     assert np.abs(p.apply_A(one) - sigma).max() < 1e-10
 
 
+@pytest.mark.parametrize("seed", [3, 8])
+def test_oracle_cdr_adjoint_identity(seed):
+    """<V u, y> = <u, V^H y> (the reference's verify-suite adjoint check, verify.cpp:196-210, on
+    the upwind family: V is real, so V^H is the transposed stencil), and A^H = L_ref^H - V^H
+    against a dense assembly of A on a small grid."""
+    bx, by, sigma, s0, f = _cdr_problem(16, seed)
+    p = OracleProblem.cdr(bx, by, sigma, s0)
+    rng = np.random.default_rng(seed)
+    u = rng.standard_normal(bx.shape) + 1j * rng.standard_normal(bx.shape)
+    y = rng.standard_normal(bx.shape) + 1j * rng.standard_normal(bx.shape)
+    lhs = np.vdot(y, p.apply_V(u))
+    rhs = np.vdot(p.apply_V_adjoint(y), u)
+    assert abs(lhs - rhs) < 1e-12 * abs(lhs)
+    # dense V (column by column) and its transpose
+    n = bx.size
+    V = np.empty((n, n))
+    for k in range(n):
+        e = np.zeros(n, complex)
+        e[k] = 1.0
+        V[:, k] = p.apply_V(e.reshape(bx.shape)).real.ravel()
+    assert rel(p.apply_V_adjoint(y).ravel(), V.T @ y.ravel()) < 1e-13
+
+
 def test_oracle_cdr_upwind_direction():
     """A linear ramp u = x: the upwind x-difference is exact (h) inside, the reflective ghost
     zeroes the difference at the boundary cell it looks through."""

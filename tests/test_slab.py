@@ -50,6 +50,56 @@ def test_local_slab_driver_matches_oracle(nranks, cmap):
     np.testing.assert_allclose(res.trace.res_reta_rel[:k], ref.res_reta[:k], rtol=1e-9, atol=1e-13)
 
 
+def fd_multiplier(shape, seed=11):
+    """a non-trivial FourierDiag multiplier close enough to 1 that the iteration still converges"""
+    rng = np.random.default_rng(seed)
+    return 0.9 + 0.05 * (rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+
+
+def oracle_map_run(k2, f, k0, eta, cmap, rtol, max_iters):
+    from oracle import MAP_FOURIER_DIAG, MAP_OPTIMAL_SCALAR, METRIC_EUCLIDEAN, METRIC_RETA
+    p = OracleProblem(k2, k0, eta)
+    if isinstance(cmap, bs.FourierDiagMap):
+        return p.run(f, map_kind=MAP_FOURIER_DIAG, m=cmap.m, rtol=rtol, max_iters=max_iters)
+    metric = METRIC_EUCLIDEAN if cmap.metric == "euclidean" else METRIC_RETA
+    return p.run(f, map_kind=MAP_OPTIMAL_SCALAR, metric=metric, rtol=rtol, max_iters=max_iters)
+
+
+def staged_maps(shape):
+    return [bs.OptimalScalarMap("euclidean"), bs.OptimalScalarMap("reta"), bs.FourierDiagMap(fd_multiplier(shape))]
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4])
+@pytest.mark.parametrize("which", [0, 1, 2], ids=["optimal_l2", "optimal_reta", "fourier_diag"])
+def test_local_slab_driver_staged_maps_match_oracle(nranks, which):
+    """OptimalScalarMap (both metrics) and FourierDiagMap (correction.cpp:22-76) on slabs: the
+    extra global reductions and the distributed-layout multiplier."""
+    k2, f, k0, eta = instance(32)
+    cmap = staged_maps(k2.shape)[which]
+    cfg = bs.IterationConfig(rtol=1e-8, max_iters=3000)
+    parts = [NumpySlabPart(k2, k0, eta, r, nranks) for r in range(nranks)]
+    res = run_slab(parts, LocalComm(), cmap, f, cfg)
+    ref = oracle_map_run(k2, f, k0, eta, cmap, 1e-8, 3000)
+    assert res.trace.terminated == ref.terminated == "converged"
+    assert abs(res.trace.iters - ref.iters) <= 1
+    assert rel(res.u, ref.u) < FIELD_TOL
+    k = min(res.trace.iters, ref.iters) + 1
+    np.testing.assert_allclose(res.trace.res_l2_rel[:k], ref.res_l2[:k], rtol=1e-8, atol=1e-13)
+    np.testing.assert_allclose(res.trace.res_reta_rel[:k], ref.res_reta[:k], rtol=1e-8, atol=1e-13)
+
+
+@pytest.mark.parametrize("which", [0, 1, 2], ids=["optimal_l2", "optimal_reta", "fourier_diag"])
+def test_local_slab3d_driver_staged_maps_match_oracle(which):
+    k2, f, k0, eta = instance3(16)
+    cmap = staged_maps(k2.shape)[which]
+    parts = [NumpySlabPart3(k2, k0, eta, r, 2) for r in range(2)]
+    res = run_slab(parts, LocalComm(), cmap, f, bs.IterationConfig(rtol=1e-8, max_iters=3000))
+    ref = oracle_map_run(k2, f, k0, eta, cmap, 1e-8, 3000)
+    assert res.trace.terminated == ref.terminated == "converged"
+    assert abs(res.trace.iters - ref.iters) <= 1
+    assert rel(res.u, ref.u) < FIELD_TOL
+
+
 def test_local_slab_driver_warm_start_and_max_iters():
     k2, f, k0, eta = instance(32, seed=5)
     u0 = 1e-3 * (np.random.default_rng(2).standard_normal(k2.shape) + 0j)
@@ -94,7 +144,7 @@ def test_local_slab3d_driver_matches_oracle(nranks):
     assert rel(res.u, ref.u) < FIELD_TOL
 
 
-def _worker(rank, world, port, q, dim=2):
+def _worker(rank, world, port, q, dim=2, which=-1):
     import torch.distributed as dist
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     from slab_standin import NumpySlabPart, NumpySlabPart3
@@ -104,20 +154,22 @@ def _worker(rank, world, port, q, dim=2):
     try:
         k2, f, k0, eta = instance3(16) if dim == 3 else instance(32)
         part = Part(k2, k0, eta, rank, world)
-        res = run_slab([part], DistComm(), bs.PointwiseMap(), f, bs.IterationConfig(rtol=1e-8, max_iters=3000))
+        cmap = bs.PointwiseMap() if which < 0 else staged_maps(k2.shape)[which]
+        res = run_slab([part], DistComm(), cmap, f, bs.IterationConfig(rtol=1e-8, max_iters=3000))
         q.put((rank, part.row0, part.rows, res.u, res.trace.iters, res.trace.terminated,
                res.trace.res_l2_rel, res.sweeps_launched))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("dim", [2, 3])
-def test_two_rank_gloo_slab_matches_oracle(dim):
+@pytest.mark.parametrize("dim,which", [(2, -1), (3, -1), (2, 0), (2, 1), (2, 2)],
+                         ids=["2d", "3d", "2d_optimal_l2", "2d_optimal_reta", "2d_fourier_diag"])
+def test_two_rank_gloo_slab_matches_oracle(dim, which):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, dim)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, dim, which)) for r in range(2)]
     for p in procs:
         p.start()
     results = sorted([q.get(timeout=300) for _ in procs], key=lambda r: r[0])
@@ -125,7 +177,10 @@ def test_two_rank_gloo_slab_matches_oracle(dim):
         p.join(timeout=60)
         assert p.exitcode == 0
     k2, f, k0, eta = instance3(16) if dim == 3 else instance(32)
-    ref = oracle_run(k2, f, k0, eta, bs.PointwiseMap(), 1e-8, 3000)
+    if which < 0:
+        ref = oracle_run(k2, f, k0, eta, bs.PointwiseMap(), 1e-8, 3000)
+    else:
+        ref = oracle_map_run(k2, f, k0, eta, staged_maps(k2.shape)[which], 1e-8, 3000)
     u = np.zeros_like(ref.u)
     for rank, row0, rows, ur, iters, term, l2, launched in results:
         lo, hi = max(row0 - 1, 0), min(row0 + rows - 1, k2.shape[0])
