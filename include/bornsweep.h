@@ -69,9 +69,10 @@ typedef struct {
  * relaxation gamma(x) = (i/eta) V(x) ("scalar/diagonal relaxation").
  * Supported on the GPU (bp_run):
  *   SCALAR          every family and path (CDR: real gamma only)
- *   OPTIMAL_SCALAR  Dirichlet 2-D / 3-D (single device and slabs) and periodic, both metrics
- *   FOURIER_DIAG    Dirichlet 2-D / 3-D (single device and slabs) and periodic
- *   POINTWISE       Dirichlet 2-D / 3-D, single device and slabs (a Dirichlet-family map)
+ *   OPTIMAL_SCALAR  Dirichlet 2-D (any shape) / 3-D, single device and slabs, and periodic (any
+ *                   shape), both metrics, every format
+ *   FOURIER_DIAG    Dirichlet 2-D (any shape) / 3-D, single device and slabs, and periodic (any shape)
+ *   POINTWISE       Dirichlet 2-D (any shape) / 3-D, single device and slabs (a Dirichlet-family map)
  * anything else returns BP_ENOTSUP. */
 enum {
     BP_MAP_SCALAR = 0,         /* ScalarMap{gamma}                                      */

@@ -375,6 +375,7 @@ struct bp_problem {
     int gnx = 0, gny = 0;
     GLinePlan gplan_x, gplan_y;
     double *gax = nullptr, *gay = nullptr, *gpart = nullptr;
+    double2 *gm0 = nullptr, *gm1 = nullptr, *gm2 = nullptr;  // any-shape staged maps: u^m, direction, w
     cudaStream_t stream = nullptr;
     // device constants
     double2* k2 = nullptr;
@@ -1292,6 +1293,116 @@ int run_core_generic(bp_problem* p, const bp_map* map, const bp_iter_config* cfg
     return BP_OK;
 }
 
+// A u on an any-shape handle (dense batch): five-point stencil (Dirichlet, kernels.cpp:56-69) or
+// the pseudospectral F^-1(|xi|^2 F u) - k2 u (periodic, helmholtz.cpp:27-32); f != null: f - A u.
+// tmp: scratch field (periodic only).  gen_spectral uses p->T.
+int gen_apply_A(bp_problem* p, const double2* u, const double2* f, double2* out, double2* tmp) {
+    const GenArgs g = gen_args(p);
+    const size_t total = p->field * p->batch;
+    if (p->gper) {
+        if (int rc = gen_spectral(p, false, u, out, 2)) return rc;
+        gen_pointwise_kernel<<<grid_for(total), 256, 0, p->stream>>>(g, 5, u, nullptr, tmp);
+        combine_kernel<<<grid_for(total), 256, 0, p->stream>>>(out, tmp, f, total);
+    } else {
+        gen_pointwise_kernel<<<grid_for(total), 256, 0, p->stream>>>(g, f ? 3 : 0, u, f, out);
+    }
+    CU(cudaGetLastError());
+    return BP_OK;
+}
+
+// bp::run with OptimalScalarMap (both metrics) or FourierDiagMap on an any-shape handle
+// (Dirichlet or periodic): the reference's loop (iterate.cpp:105-150, correction.cpp:22-76)
+// operator by operator in physical space -- r = f - A u, G r for the R_eta trace, the direction
+// (r, G r, or the Born residual G(V u + f) - u), the map, the update -- with the reductions and
+// the termination test on the device.  Generic, not fused: the any-shape path serves shapes the
+// fused kernels do not take (run_sweep at an arbitrary n, bench.cpp:140-151).
+int run_core_generic_maps(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool have_u0,
+                          double* snapshots, int n_snap) {
+    const int B = p->batch;
+    const GenArgs g = gen_args(p);
+    const size_t total = p->field * B, fb = sizeof(double2) * total;
+    Control c = make_control(p);
+    c.max_iters = cfg->max_iters;
+    c.rtol = cfg->rtol;
+    if (!p->gm0) {
+        CU(cudaMalloc(&p->gm0, fb));
+        CU(cudaMalloc(&p->gm1, fb));
+        CU(cudaMalloc(&p->gm2, fb));
+    }
+    if (map->kind == BP_MAP_FOURIER_DIAG) {
+        if (!p->fd) CU(cudaMalloc(&p->fd, sizeof(double2) * p->field));
+        CU(cudaMemcpyAsync(p->fd, map->m, sizeof(double2) * p->field, cudaMemcpyHostToDevice, p->stream));
+    }
+    if (int rc = norms(p, p->f, p->fnorm_l2)) return rc;
+    if (int rc = gen_spectral(p, true, p->f, p->y)) return rc;
+    if (int rc = norms(p, p->y, p->fnorm_reta)) return rc;
+    std::vector<double> fn(B);
+    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    for (int b = 0; b < B; ++b)
+        if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
+    if (!have_u0) CU(cudaMemsetAsync(p->u0, 0, fb, p->stream));
+    CU(cudaMemsetAsync(p->u1, 0, fb, p->stream));
+    init_control_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(c, B);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_l2, (size_t)B * p->trace_cap);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_reta, (size_t)B * p->trace_cap);
+    CU(cudaGetLastError());
+    const int nchunk = 64;
+    const size_t nd = p->dense_pts;
+    double2 *U = p->gm0, *R = p->x, *GR = p->y, *X = p->gm1, *W = p->gm2, *tmp = p->dense;
+    if (snapshots && n_snap > 0)
+        if (int rc = download(p, p->u0, nullptr, nullptr, snapshots)) return rc;
+    p->stat_launches = 0;
+    const long max_launch = (long)cfg->max_iters + 1;
+    for (long k = 1; k <= max_launch; ++k) {
+        // entry m = k - 1: r^m = f - A u^m, G r^m (iterate.cpp:108-110, 128-132)
+        gen_gather_kernel<<<grid_for(total), 256, 0, p->stream>>>(g, c, p->u0, p->u1, U);
+        if (int rc = gen_apply_A(p, U, p->f, R, tmp)) return rc;
+        if (int rc = gen_spectral(p, true, R, GR)) return rc;
+        // direction (iterate.cpp:118-123), before the entry advances the sweep counter
+        const double2* D = R;
+        if (cfg->format == BP_FMT_CBS) {
+            D = GR;
+        } else if (cfg->format == BP_FMT_NPBS) {  // born_residual (problem.cpp:41-49)
+            gen_pointwise_kernel<<<grid_for(total), 256, 0, p->stream>>>(g, 4, U, p->f, X);
+            if (int rc = gen_spectral(p, true, X, X)) return rc;
+            gen_sub_kernel<<<grid_for(total), 256, 0, p->stream>>>(X, X, U, (long)total);
+            D = X;
+        }
+        gen_norms_kernel<<<dim3(nchunk, B), 256, 0, p->stream>>>(g, c, R, GR, p->gpart, nchunk);
+        gen_finalize_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(c, B, p->gpart, nchunk);
+        // apply_correction (correction.cpp:22-76) for the members still active
+        if (map->kind == BP_MAP_OPTIMAL_SCALAR) {
+            if (map->metric == BP_METRIC_RETA) {  // w = x - G V x, gamma = <w, x> / <w, w>
+                gen_pointwise_kernel<<<grid_for(total), 256, 0, p->stream>>>(g, 1, D, nullptr, W);
+                if (int rc = gen_spectral(p, true, W, W)) return rc;
+                gen_sub_kernel<<<grid_for(total), 256, 0, p->stream>>>(W, D, W, (long)total);
+                gen_dot_kernel<<<dim3(nchunk, B), 256, 0, p->stream>>>(g, c, W, D, p->gpart, nchunk);
+            } else {  // w = A x, gamma = <w, r> / <w, w>
+                if (int rc = gen_apply_A(p, D, nullptr, W, tmp)) return rc;
+                gen_dot_kernel<<<dim3(nchunk, B), 256, 0, p->stream>>>(g, c, W, R, p->gpart, nchunk);
+            }
+            gen_gamma_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(c, B, p->gpart, nchunk);
+            gen_update_kernel<<<grid_for(total), 256, 0, p->stream>>>(g, c, p->u0, p->u1, D, 1);
+        } else {  // FourierDiag: du = T^-1(m T x) (correction.cpp:63-68)
+            if (int rc = gen_dst2(p, D, W, 1.0)) return rc;
+            gen_modemul_kernel<<<grid_for(total), 256, 0, p->stream>>>(g, W, p->fd);
+            if (int rc = gen_dst2(p, W, W, g.gscale, p->gper)) return rc;
+            gen_update_kernel<<<grid_for(total), 256, 0, p->stream>>>(g, c, p->u0, p->u1, W, 0);
+        }
+        CU(cudaGetLastError());
+        p->stat_launches += 16;
+        if (snapshots && k < n_snap)  // u^k in buffer k & 1 for every member still iterating
+            if (int rc = download(p, (k & 1) ? p->u1 : p->u0, nullptr, nullptr, snapshots + 2 * nd * B * k)) return rc;
+        if ((snapshots && n_snap > 0) || k % kGraphSweeps == 0 || k == max_launch) {
+            CU(cudaMemcpyAsync(p->host_active, c.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            if (*p->host_active == 0) break;
+        }
+    }
+    return BP_OK;
+}
+
 int finish_run_periodic(bp_problem* p, double* u_out, bool host_ptr);
 int finish_run_cdr(bp_problem* p, double* u_out, bool host_ptr);
 int finish_run_traces(bp_problem* p, const bp_iter_config* cfg, double* res_l2, double* res_reta,
@@ -1891,8 +2002,6 @@ int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* c
         return set_err(BP_EINVAL, "unknown optimal-scalar metric");
     if (p->cdr && (map->kind != BP_MAP_SCALAR || map->gamma_im != 0.0))
         return set_err(BP_ENOTSUP, "CDR family on the GPU: real scalar maps only");
-    if (p->generic && (map->kind == BP_MAP_OPTIMAL_SCALAR || map->kind == BP_MAP_FOURIER_DIAG))
-        return set_err(BP_ENOTSUP, "any-shape grids on the GPU: scalar and pointwise maps");
     if ((p->periodic || p->gper) && map->kind == BP_MAP_POINTWISE)
         return set_err(BP_ENOTSUP, "periodic family: the pointwise (i/eta) V map is defined for the "
                                    "Dirichlet family only");
@@ -2009,7 +2118,7 @@ int create_generic(const bp_grid* grid, int32_t batch, const double* k2, const d
     }
     CUF(cudaMalloc(&p->gamma, sizeof(double2) * (size_t)batch));
     CUF(cudaMalloc(&p->norm_part, sizeof(double) * (size_t)batch * 64));
-    CUF(cudaMalloc(&p->gpart, sizeof(double) * (size_t)batch * 64 * 2));
+    CUF(cudaMalloc(&p->gpart, sizeof(double) * (size_t)batch * 64 * 4));
     CUF(cudaMalloc(&p->fnorm_l2, sizeof(double) * batch));
     CUF(cudaMalloc(&p->fnorm_reta, sizeof(double) * batch));
     CUF(cudaMalloc(&p->ctl_int, sizeof(int) * (5 * (size_t)batch + 1)));
@@ -2895,7 +3004,8 @@ int bp_problem_destroy(bp_problem* p) {
                     (void*)p->tw, (void*)p->sinp, (void*)p->lap, (void*)p->xi2,
                     (void*)p->bx, (void*)p->by, (void*)p->sigma, (void*)p->sigma0, (void*)p->lapn,
                     (void*)p->rnorm2, (void*)p->w4, (void*)p->dflag, (void*)p->Tc, (void*)p->slab_sums,
-                    (void*)p->tri, (void*)p->gax, (void*)p->gay, (void*)p->gpart})
+                    (void*)p->tri, (void*)p->gax, (void*)p->gay, (void*)p->gpart, (void*)p->gm0, (void*)p->gm1,
+                    (void*)p->gm2})
         if (q) cudaFree(q);
     if (p->host_active) cudaFreeHost(p->host_active);
     free_gplan(p->gplan_x);
@@ -3099,7 +3209,10 @@ static int run_impl(const bp_problem* cp, const bp_map* map, const double* f, co
         if (int rc = upload(p, u0, p->periodic ? p->x : p->u0, host_ptr)) return rc;
     ComputeTurn turn(p);
     const int rc = p->periodic  ? run_core_periodic(p, map, cfg, u0 != nullptr, snapshots, n_snap)
-                   : p->generic ? run_core_generic(p, map, cfg, u0 != nullptr, snapshots, n_snap)
+                   : p->generic
+                       ? ((map->kind == BP_MAP_OPTIMAL_SCALAR || map->kind == BP_MAP_FOURIER_DIAG)
+                              ? run_core_generic_maps(p, map, cfg, u0 != nullptr, snapshots, n_snap)
+                              : run_core_generic(p, map, cfg, u0 != nullptr, snapshots, n_snap))
                                 : run_core(p, map, cfg, u0 != nullptr, snapshots, n_snap);
     if (rc) return rc;
     turn.release();

@@ -377,6 +377,113 @@ __global__ void gen_finalize_kernel(Control c, int batch, const double* __restri
     finalize_entry(c, b, c.sweep[b], s0, s1);
 }
 
+// ---- OptimalScalar / FourierDiag maps on any-shape handles (staged sweep, run_core_generic_maps)
+// per-chunk partials of sum conj(a) b (re, im) and sum |a|^2 over the ACTIVE members
+__global__ void __launch_bounds__(256) gen_dot_kernel(GenArgs g, Control c, const double2* __restrict__ a,
+                                                      const double2* __restrict__ bb, double* __restrict__ part,
+                                                      int nchunk) {
+    const int b = blockIdx.y, ch = blockIdx.x;
+    __shared__ double red[3][256];
+    const long per = (long)g.nx * g.ny;
+    const long chunk = (per + nchunk - 1) / nchunk, lo = ch * chunk, hi = min(per, lo + chunk);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (__ldcg(&c.status[b]) == ST_ACTIVE)
+        for (long r = lo + threadIdx.x; r < hi; r += blockDim.x) {
+            const double2 w = a[b * per + r], x = bb[b * per + r];
+            s0 += w.x * x.x + w.y * x.y;
+            s1 += w.x * x.y - w.y * x.x;
+            s2 += cnorm(w);
+        }
+    red[0][threadIdx.x] = s0;
+    red[1][threadIdx.x] = s1;
+    red[2][threadIdx.x] = s2;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if (threadIdx.x < h)
+            for (int k = 0; k < 3; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x < 3) part[((long)b * nchunk + ch) * 4 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// gamma_b = <w, r> / <w, w> (correction.cpp:10-18) from the chunk partials, fixed order
+__global__ void gen_gamma_kernel(Control c, int batch, const double* __restrict__ part, int nchunk) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch || c.status[b] != ST_ACTIVE) return;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < nchunk; ++k) {
+        s0 += part[((long)b * nchunk + k) * 4];
+        s1 += part[((long)b * nchunk + k) * 4 + 1];
+        s2 += part[((long)b * nchunk + k) * 4 + 2];
+    }
+    finalize_gamma(c, b, s0, s1, s2);
+}
+
+// per-chunk |a|^2 -> part[..][0], |b|^2 -> part[..][1] of the ACTIVE members (the trace entry)
+__global__ void __launch_bounds__(256) gen_norms_kernel(GenArgs g, Control c, const double2* __restrict__ a,
+                                                        const double2* __restrict__ bb, double* __restrict__ part,
+                                                        int nchunk) {
+    const int b = blockIdx.y, ch = blockIdx.x;
+    __shared__ double red[2][256];
+    const long per = (long)g.nx * g.ny;
+    const long chunk = (per + nchunk - 1) / nchunk, lo = ch * chunk, hi = min(per, lo + chunk);
+    double s0 = 0.0, s1 = 0.0;
+    if (__ldcg(&c.status[b]) == ST_ACTIVE)
+        for (long r = lo + threadIdx.x; r < hi; r += blockDim.x) {
+            s0 += cnorm(a[b * per + r]);
+            s1 += cnorm(bb[b * per + r]);
+        }
+    red[0][threadIdx.x] = s0;
+    red[1][threadIdx.x] = s1;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if (threadIdx.x < h) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + h];
+            red[1][threadIdx.x] += red[1][threadIdx.x + h];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < 2) part[((long)b * nchunk + ch) * 2 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// u^{m+1} = u^m + gamma_b x (use_gamma) or u^m + x, for the members still ACTIVE after entry m
+// was recorded (m = sweep - 1); u^m in buffer m & 1, u^{m+1} into the other one
+__global__ void gen_update_kernel(GenArgs g, Control c, double2* __restrict__ u0, double2* __restrict__ u1,
+                                  const double2* __restrict__ x, int use_gamma) {
+    const long per = (long)g.nx * g.ny, total = per * g.batch;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+        const int b = (int)(idx / per);
+        if (__ldcg(&c.status[b]) != ST_ACTIVE) continue;
+        const int m = __ldcg(&c.sweep[b]) - 1;
+        const double2* u = (m & 1) ? u1 : u0;
+        double2* un = (m & 1) ? u0 : u1;
+        const double2 d = use_gamma ? cmul(c.gamma[b], x[idx]) : x[idx];
+        un[idx] = cadd(u[idx], d);
+    }
+}
+
+// u^m of every member (buffer sweep & 1) gathered into one dense array (operator inputs)
+__global__ void gen_gather_kernel(GenArgs g, Control c, const double2* __restrict__ u0,
+                                  const double2* __restrict__ u1, double2* __restrict__ out) {
+    const long per = (long)g.nx * g.ny, total = per * g.batch;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+        const int b = (int)(idx / per);
+        out[idx] = ((__ldcg(&c.sweep[b]) & 1) ? u1 : u0)[idx];
+    }
+}
+
+// x <- x * m (FourierDiag multiplier, one nx x ny mode array shared by the batch), or a - b
+__global__ void gen_modemul_kernel(GenArgs g, double2* __restrict__ x, const double2* __restrict__ m) {
+    const long per = (long)g.nx * g.ny, total = per * g.batch;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x)
+        x[idx] = cmul(x[idx], m[idx % per]);
+}
+__global__ void gen_sub_kernel(double2* __restrict__ out, const double2* __restrict__ a,
+                               const double2* __restrict__ b, long total) {
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x)
+        out[idx] = csub(a[idx], b[idx]);
+}
+
 // dense result copy: member b from buffer p1 when select[b] (its result_buf) else p0
 __global__ void gen_select_kernel(const double2* __restrict__ p0, const double2* __restrict__ p1,
                                   const int* __restrict__ select, double2* __restrict__ out, long per, int batch) {

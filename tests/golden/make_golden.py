@@ -26,8 +26,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-from oracle import (FMT_DIRECT, MAP_OPTIMAL_SCALAR, MAP_POINTWISE, MAP_SCALAR, Reference,  # noqa: E402
-                    ReferenceProblem)
+from oracle import (FMT_CBS, FMT_DIRECT, MAP_FOURIER_DIAG, MAP_OPTIMAL_SCALAR, MAP_POINTWISE,  # noqa: E402
+                    MAP_SCALAR, Reference, ReferenceProblem)
 import paper_2603_18527_b200 as bs  # noqa: E402
 
 
@@ -266,6 +266,42 @@ def generic_golden():
     np.savez_compressed(os.path.join(HERE, "ref_generic.npz"), **out)
 
 
+def generic_maps_golden():
+    """ref_generic_maps.npz -- OptimalScalarMap (both metrics, NPBS and Direct) and FourierDiagMap
+    runs of the reference's own bp::run / apply_correction (oracle/_ref; iterate.cpp:88-153,
+    correction.cpp:22-76) on the any-shape grids of ref_generic.npz (Dirichlet a-d, periodic
+    pa-pc): the iterate and traces after 30 sweeps (per-iterate parity; the optimal-scalar
+    trajectory amplifies roundoff over long runs) and the full solve's count / termination / u."""
+    g = np.load(os.path.join(HERE, "ref_generic.npz"))
+    rng = np.random.default_rng(4242)
+    out = {}
+    for tag in ["a", "b", "c", "d", "pa", "pb", "pc"]:
+        per = tag.startswith("p")
+        k2, f = g[f"{tag}_k2"], g[f"{tag}_f"]
+        lx, ly = (float(v) for v in g[f"{tag}_l"])
+        r = ReferenceProblem(k2, float(g[f"{tag}_k0"]), float(g[f"{tag}_eta"]), lx, ly, periodic=per)
+        m = 0.9 + 0.05 * (rng.standard_normal(k2.shape) + 1j * rng.standard_normal(k2.shape))
+        out[f"{tag}_m"] = m
+        runs = {"opt": dict(map_kind=MAP_OPTIMAL_SCALAR, metric=0),
+                "reta": dict(map_kind=MAP_OPTIMAL_SCALAR, metric=1),
+                "optcbs": dict(map_kind=MAP_OPTIMAL_SCALAR, metric=0, fmt=FMT_CBS),
+                "optdir": dict(map_kind=MAP_OPTIMAL_SCALAR, metric=0, fmt=FMT_DIRECT),
+                "fd": dict(map_kind=MAP_FOURIER_DIAG, m=m)}
+        for name, kw in runs.items():
+            r30 = r.run(f, rtol=1e-12, max_iters=30, **kw)
+            full = r.run(f, rtol=1e-8, max_iters=3000, **kw)
+            out[f"{tag}_{name}_u30"] = r30.u
+            out[f"{tag}_{name}_l2_30"] = r30.res_l2
+            out[f"{tag}_{name}_reta_30"] = r30.res_reta
+            out[f"{tag}_{name}_iters30"] = r30.iters
+            out[f"{tag}_{name}_u"] = full.u
+            out[f"{tag}_{name}_iters"] = full.iters
+            out[f"{tag}_{name}_term"] = full.terminated
+            out[f"{tag}_{name}_l2_last"] = full.res_l2[-1]
+            print("generic maps", tag, name, r30.iters, full.iters, full.terminated)
+    np.savez_compressed(os.path.join(HERE, "ref_generic_maps.npz"), **out)
+
+
 def io_golden():
     d = os.path.join(HERE, "ref_io")
     os.makedirs(d, exist_ok=True)
@@ -284,8 +320,9 @@ def io_golden():
 
 if __name__ == "__main__":
     Reference.set_mode("serial")
-    if sys.argv[1:] in (["dct"], ["io"], ["round2"], ["generic"]):
-        {"dct": dct_golden, "io": io_golden, "round2": round2_golden, "generic": generic_golden}[sys.argv[1]]()
+    if sys.argv[1:] in (["dct"], ["io"], ["round2"], ["generic"], ["generic_maps"]):
+        {"dct": dct_golden, "io": io_golden, "round2": round2_golden, "generic": generic_golden,
+         "generic_maps": generic_maps_golden}[sys.argv[1]]()
         sys.exit(0)
     io_golden()
     dct_golden()
@@ -298,4 +335,5 @@ if __name__ == "__main__":
     periodic_golden()
     round2_golden()
     generic_golden()
+    generic_maps_golden()
     print("golden fixtures written to", HERE)
