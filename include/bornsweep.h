@@ -70,7 +70,7 @@ typedef struct {
  * Supported on the GPU (bp_run):
  *   SCALAR          every family and path (CDR: real gamma only)
  *   OPTIMAL_SCALAR  Dirichlet 2-D (any shape) / 3-D, single device and slabs, and periodic (any
- *                   shape), both metrics, every format
+ *                   shape), both metrics, every format; CDR (CBS / NPBS)
  *   FOURIER_DIAG    Dirichlet 2-D (any shape) / 3-D, single device and slabs, and periodic (any shape)
  *   POINTWISE       Dirichlet 2-D (any shape) / 3-D, single device and slabs (a Dirichlet-family map)
  * anything else returns BP_ENOTSUP. */
@@ -143,7 +143,9 @@ int bp_problem_create3d(const bp_grid3* grid, int32_t batch, const double* k2, c
  * nx = ny = 2^k, 8 <= 2^k <= 4096.  A = -Lap_N + b . grad_upwind + sigma (reflective ghosts),
  * L_ref = -Lap_N + sigma0, V = L_ref - A.  bx, by, sigma: batch*nx*ny REAL; sigma0: batch.
  * Every field argument of the entry points below is REAL (nx*ny doubles per member) on a CDR
- * handle; maps: real BP_MAP_SCALAR only; bp_apply_V_adjoint -> BP_ENOTSUP. */
+ * handle; maps: real BP_MAP_SCALAR (the fused sweep) and BP_MAP_OPTIMAL_SCALAR (both metrics,
+ * CBS / NPBS; a staged sweep); a complex gamma or a mode-space multiplier would leave the real
+ * field layout (BP_ENOTSUP).  bp_apply_V_adjoint applies V^T (the transposed upwind stencil). */
 int bp_problem_create_cdr(const bp_grid* grid, int32_t batch, const double* bx, const double* by,
                           const double* sigma, const double* sigma0, int32_t device,
                           bp_problem** out);

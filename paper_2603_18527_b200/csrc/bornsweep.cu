@@ -1814,6 +1814,84 @@ int cdr_stencil(bp_problem* p, int op, const double2* u, const double2* f, doubl
     return BP_OK;
 }
 
+// bp::run with OptimalScalarMap (both metrics, correction.cpp:22-48) on the CDR family: the
+// reference's loop operator by operator on the real fields (as run_core_generic_maps; the real
+// arrays are read as pairs, whose complex inner product's real part is the real one), gamma real.
+int run_core_cdr_maps(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool have_u0,
+                      double* snapshots, int n_snap) {
+    const int B = p->batch;
+    const size_t total = p->field * B / 2, rb = sizeof(double) * p->field * B;  // double2 pairs
+    if (!p->gamma) CU(cudaMalloc(&p->gamma, sizeof(double2) * (size_t)B));
+    Control c = make_control(p);
+    c.max_iters = cfg->max_iters;
+    c.rtol = cfg->rtol;
+    GenArgs g{};
+    g.batch = B;
+    g.nx = p->n;
+    g.ny = p->n / 2;
+    if (!p->gm1) {
+        CU(cudaMalloc(&p->gm1, rb));
+        CU(cudaMalloc(&p->gm2, rb));
+    }
+    if (!p->gpart) CU(cudaMalloc(&p->gpart, sizeof(double) * (size_t)B * 64 * 4));
+    if (int rc = norms(p, p->f, p->fnorm_l2)) return rc;
+    if (int rc = cdr_apply(p, 0, p->f, p->y, nullptr)) return rc;
+    if (int rc = norms(p, p->y, p->fnorm_reta)) return rc;
+    std::vector<double> fn(B);
+    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    for (int b = 0; b < B; ++b)
+        if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
+    if (!have_u0) CU(cudaMemsetAsync(p->u0, 0, sizeof(double2) * p->alloc, p->stream));
+    CU(cudaMemsetAsync(p->u1, 0, sizeof(double2) * p->alloc, p->stream));
+    init_control_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(c, B);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_l2, (size_t)B * p->trace_cap);
+    fill_nan_kernel<<<grid_for((size_t)B * p->trace_cap), 256, 0, p->stream>>>(p->trace_reta, (size_t)B * p->trace_cap);
+    CU(cudaGetLastError());
+    const int nchunk = 64;
+    const size_t nd = p->field;
+    double2 *R = p->x, *GR = p->y, *X = p->gm1, *W = p->gm2;
+    if (snapshots && n_snap > 0)
+        if (int rc = cdr_download(p, p->u0, snapshots)) return rc;
+    p->stat_launches = 0;
+    const long max_launch = (long)cfg->max_iters + 1;
+    for (long k = 1; k <= max_launch; ++k) {
+        // every member still active is at sweep m = k - 1: u^m in buffer m & 1
+        const double2* U = ((k - 1) & 1) ? p->u1 : p->u0;
+        if (int rc = cdr_stencil(p, 3, U, p->f, R)) return rc;       // r = f - A u
+        if (int rc = cdr_apply(p, 0, R, GR, nullptr)) return rc;      // G r (R_eta trace)
+        const double2* D = GR;                                        // CBS
+        if (cfg->format == BP_FMT_NPBS) {                             // G(V u + f) - u
+            if (int rc = cdr_stencil(p, 4, U, p->f, X)) return rc;
+            if (int rc = cdr_apply(p, 0, X, X, U)) return rc;
+            D = X;
+        }
+        gen_norms_kernel<<<dim3(nchunk, B), 256, 0, p->stream>>>(g, c, R, GR, p->gpart, nchunk);
+        gen_finalize_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(c, B, p->gpart, nchunk);
+        if (map->metric == BP_METRIC_RETA) {  // w = x - G V x, gamma = <w, x> / <w, w>
+            if (int rc = cdr_stencil(p, 1, D, nullptr, W)) return rc;
+            if (int rc = cdr_apply(p, 0, W, W, nullptr)) return rc;
+            gen_sub_kernel<<<grid_for(total), 256, 0, p->stream>>>(W, D, W, (long)total);
+            gen_dot_kernel<<<dim3(nchunk, B), 256, 0, p->stream>>>(g, c, W, D, p->gpart, nchunk);
+        } else {  // w = A x, gamma = <w, r> / <w, w>
+            if (int rc = cdr_stencil(p, 0, D, nullptr, W)) return rc;
+            gen_dot_kernel<<<dim3(nchunk, B), 256, 0, p->stream>>>(g, c, W, R, p->gpart, nchunk);
+        }
+        gen_gamma_kernel<<<(B + 127) / 128, 128, 0, p->stream>>>(c, B, p->gpart, nchunk, 1);
+        gen_update_kernel<<<grid_for(total), 256, 0, p->stream>>>(g, c, p->u0, p->u1, D, 1);
+        CU(cudaGetLastError());
+        p->stat_launches += 16;
+        if (snapshots && k < n_snap)
+            if (int rc = cdr_download(p, (k & 1) ? p->u1 : p->u0, snapshots + nd * B * k)) return rc;
+        if ((snapshots && n_snap > 0) || k % kGraphSweeps == 0 || k == max_launch) {
+            CU(cudaMemcpyAsync(p->host_active, c.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            if (*p->host_active == 0) break;
+        }
+    }
+    return BP_OK;
+}
+
 // bp::run for the CDR family: sweep m = RC_A (entry m, u^{m+1}), RC_B (r^{m+1}, q^{m+1}, rows),
 // CC_GREEN (columns); the first RC_B + CC_GREEN pair stages q^0.
 int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool have_u0,
@@ -2000,8 +2078,8 @@ int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* c
     if (map->kind == BP_MAP_OPTIMAL_SCALAR && map->metric != BP_METRIC_EUCLIDEAN &&
         map->metric != BP_METRIC_RETA)
         return set_err(BP_EINVAL, "unknown optimal-scalar metric");
-    if (p->cdr && (map->kind != BP_MAP_SCALAR || map->gamma_im != 0.0))
-        return set_err(BP_ENOTSUP, "CDR family on the GPU: real scalar maps only");
+    if (p->cdr && !((map->kind == BP_MAP_SCALAR && map->gamma_im == 0.0) || map->kind == BP_MAP_OPTIMAL_SCALAR))
+        return set_err(BP_ENOTSUP, "CDR family on the GPU (real fields): real scalar and optimal-scalar maps");
     if ((p->periodic || p->gper) && map->kind == BP_MAP_POINTWISE)
         return set_err(BP_ENOTSUP, "periodic family: the pointwise (i/eta) V map is defined for the "
                                    "Dirichlet family only");
@@ -3200,7 +3278,10 @@ static int run_impl(const bp_problem* cp, const bp_map* map, const double* f, co
         if (u0)
             if (int rc = cdr_upload(p, u0, p->u0, host_ptr)) return rc;
         ComputeTurn turn(p);
-        if (int rc = run_core_cdr(p, map, cfg, u0 != nullptr, snapshots, n_snap)) return rc;
+        if (int rc = map->kind == BP_MAP_OPTIMAL_SCALAR
+                         ? run_core_cdr_maps(p, map, cfg, u0 != nullptr, snapshots, n_snap)
+                         : run_core_cdr(p, map, cfg, u0 != nullptr, snapshots, n_snap))
+            return rc;
         turn.release();
         return finish_run(p, cfg, u_out, host_ptr, res_l2, res_reta, info);
     }

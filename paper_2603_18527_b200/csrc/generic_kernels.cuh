@@ -407,7 +407,9 @@ __global__ void __launch_bounds__(256) gen_dot_kernel(GenArgs g, Control c, cons
 }
 
 // gamma_b = <w, r> / <w, w> (correction.cpp:10-18) from the chunk partials, fixed order
-__global__ void gen_gamma_kernel(Control c, int batch, const double* __restrict__ part, int nchunk) {
+// (real_only: real fields read as pairs -- the CDR family -- have a real inner product, s0)
+__global__ void gen_gamma_kernel(Control c, int batch, const double* __restrict__ part, int nchunk,
+                                 int real_only = 0) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= batch || c.status[b] != ST_ACTIVE) return;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -416,7 +418,7 @@ __global__ void gen_gamma_kernel(Control c, int batch, const double* __restrict_
         s1 += part[((long)b * nchunk + k) * 4 + 1];
         s2 += part[((long)b * nchunk + k) * 4 + 2];
     }
-    finalize_gamma(c, b, s0, s1, s2);
+    finalize_gamma(c, b, s0, real_only ? 0.0 : s1, s2);
 }
 
 // per-chunk |a|^2 -> part[..][0], |b|^2 -> part[..][1] of the ACTIVE members (the trace entry)

@@ -83,6 +83,33 @@ def test_cdr_run_per_iterate_matches_oracle(gpu, n):
         assert abs(t.fnorm_reta - ro.fnorm_reta) < 1e-12 * ro.fnorm_reta
 
 
+@pytest.mark.parametrize("metric", ["euclidean", "reta"])
+@pytest.mark.parametrize("fmt", ["npbs", "cbs"])
+def test_cdr_optimal_scalar_matches_oracle(gpu, metric, fmt):
+    """OptimalScalarMap (correction.cpp:22-48) on the CDR family: per-iterate parity over the
+    first sweeps, then the full solve's count and field."""
+    from oracle import FMT_CBS, FMT_NPBS, MAP_OPTIMAL_SCALAR
+    n, n_snap = 64, 20
+    bx, by, sigma, s0, f = media(n, 2, seed=6)
+    cmap = bs.OptimalScalarMap(metric)
+    with bs.CdrNeumann(bx, by, sigma, s0) as p:
+        r = bs.run(p, cmap, f, bs.IterationConfig(fmt, 1e-8, 500), n_snap=n_snap)
+    for b in range(2):
+        ro = oracle(bx[b], by[b], sigma[b], s0[b]).run(
+            f[b] + 0j, map_kind=MAP_OPTIMAL_SCALAR, metric=0 if metric == "euclidean" else 1,
+            fmt=FMT_CBS if fmt == "cbs" else FMT_NPBS, rtol=1e-8, max_iters=500, n_snap=n_snap)
+        t = r.traces[b]
+        assert t.terminated == ro.terminated == "converged"
+        assert abs(t.iters - ro.iters) <= 1
+        k = min(t.iters, ro.iters, n_snap - 1) + 1
+        np.testing.assert_allclose(t.res_l2_rel[:k], ro.res_l2[:k], rtol=1e-8, atol=1e-14)
+        np.testing.assert_allclose(t.res_reta_rel[:k], ro.res_reta[:k], rtol=1e-8, atol=1e-14)
+        for m in range(1, k):
+            assert np.abs(ro.snapshots[m].imag).max() < 1e-12 * np.abs(ro.snapshots[m].real).max()
+            assert rel(r.snapshots[m, b], ro.snapshots[m].real) < FIELD_TOL, m
+        assert rel(r.u[b], ro.u.real) < (FIELD_TOL if t.iters == ro.iters else 1e-7)
+
+
 def test_cdr_relaxed_gamma_and_u0(gpu):
     n = 32
     bx, by, sigma, s0, f = media(n, 2, seed=8)
@@ -134,8 +161,8 @@ def test_cdr_errors(gpu):
         bs.CdrNeumann(z, z, z, 0.0)
     with bs.CdrNeumann(z, z, z + 1.0, 1.0) as p:
         f = np.ones((1, 32, 32))
-        with pytest.raises(NotImplementedError):
-            bs.run(p, bs.OptimalScalarMap(), f)
+        with pytest.raises(NotImplementedError):  # real fields: no complex relaxation, no mode-space map
+            bs.run(p, bs.FourierDiagMap(np.ones((32, 32), complex)), f)
         with pytest.raises(NotImplementedError):
             bs.run(p, bs.ScalarMap(1.0 + 0.5j), f)
         with pytest.raises(ValueError):
