@@ -6,6 +6,7 @@
 #include "periodic_kernels.cuh"
 #include "sweep_kernels.cuh"
 #include "tri_kernels.cuh"
+#include "tri_wide_kernels.cuh"
 #include "cluster_kernels.cuh"
 
 namespace bs {
@@ -109,10 +110,55 @@ inline int tri_cols_per_cta(int log2n) {
     return segs >= TRI_THREADS ? 2 : TRI_THREADS / segs;
 }
 
+// ---- long lines (n >= 2048), 2-D whole members: wide tiles over 4-CTA clusters
+// (tri_wide_kernels.cuh); BP_TRI_WIDE=0 keeps the two-column tiles.  Returns
+// cudaErrorNotSupported when the wide kernel does not apply (caller falls back).
+template <int L>
+cudaError_t launch_tri_wide_t(const ColArgs& a, cudaStream_t s, bool prepare) {
+    if constexpr (L >= 11 && (1 << L) / BS_TRIW_CLW / kTriP >= 32) {
+        using TW = TriWide<L>;
+        auto k = tri_wide_kernel<L>;
+        cudaLaunchConfig_t cfg{};
+        cfg.blockDim = dim3(TW::THREADS);
+        cfg.gridDim = dim3(TW::CLW);
+        cfg.dynamicSmemBytes = TW::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = TW::CLW;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        static int clusters = [&] {  // co-resident clusters on this device (0: not launchable)
+            int n = 0;
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TW::SMEM) != cudaSuccess ||
+                cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                n = 0;
+            }
+            return n;
+        }();
+        const char* env = std::getenv("BP_TRI_WIDE");  // read per launch (tests toggle it)
+        if (clusters <= 0 || (env && env[0] == '0')) return cudaErrorNotSupported;
+        if (prepare) return cudaSuccess;
+        const long tiles = (long)a.batch * ((1 << L) / TW::WC);
+        const long ncl = tiles < clusters ? tiles : clusters;
+        if (ncl == 0) return cudaSuccess;
+        cfg.gridDim = dim3((unsigned)(ncl * TW::CLW));
+        return cudaLaunchKernelEx(&cfg, k, a);
+    }
+    return cudaErrorNotSupported;
+}
+
 // ---- Green column pass as a tridiagonal x-solve (n >= 64): persistent CTAs, one per
 // resident slot (occupancy queried once per instance)
 template <int L, int LAYOUT>
 cudaError_t launch_tri_t(const ColArgs& a, cudaStream_t s, bool prepare) {
+    if constexpr (L >= 11 && LAYOUT == CL_PLANE) {
+        const cudaError_t e = launch_tri_wide_t<L>(a, s, prepare);
+        if (e != cudaErrorNotSupported && !prepare) return e;
+    }
     if constexpr (L >= 6) {
         using TG = TriGeom<L>;
         using TT = TriTile<L, LAYOUT == CL_CDR>;

@@ -97,6 +97,26 @@ def test_run_tri_iterates_match_transform_route(gpu):
         assert rel(st[m][0], ref.snapshots[m]) < FIELD_TOL, m
 
 
+@pytest.mark.parametrize("n,batch", [(2048, 2), (4096, 1)])
+def test_wide_cluster_pass_bit_identical(gpu, monkeypatch, n, batch):
+    """The wide-tile cluster kernel (tri_wide_kernels.cuh, n >= 2048: 8-column tiles over 4-CTA
+    clusters, chunk maps exchanged through DSMEM) performs tri_kernel's arithmetic in the same
+    order: G and a short run are bit-identical with it on (default) and off (BP_TRI_WIDE=0)."""
+    k2, f, k0, eta = bs.make_instances(bs.InstanceSpec(n=n, ppw=6.0, contrast=0.5, seed=4), 0, batch)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(k2.shape) + 1j * rng.standard_normal(k2.shape)
+    cfg = bs.IterationConfig(rtol=1e-30, max_iters=5)
+    out = {}
+    for wide in ("1", "0"):
+        monkeypatch.setenv("BP_TRI_WIDE", wide)
+        with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+            out[wide] = (p.apply_G(x), bs.run(p, bs.PointwiseMap(), f, cfg))
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1].u, out["0"][1].u)
+    for a, b in zip(out["1"][1].traces, out["0"][1].traces):
+        assert np.array_equal(a.res_l2_rel, b.res_l2_rel) and np.array_equal(a.res_reta_rel, b.res_reta_rel)
+
+
 def test_set_medium_rebuilds_tri_tables(gpu):
     n = 128
     k2a, _, k0a, etaa = bs.make_instances(bs.InstanceSpec(n=n, ppw=8.0, contrast=0.5, seed=1), 0, 2)
