@@ -396,7 +396,8 @@ struct bp_problem {
     unsigned* counter = nullptr;
     double *trace_l2 = nullptr, *trace_reta = nullptr;
     int trace_cap = 0;
-    int* host_active = nullptr;  // pinned
+    int* host_active = nullptr;  // pinned (written by the device: publish_int)
+    double* host_fn = nullptr;   // pinned [batch]: ||f|| for the zero-source check
     int* dflag = nullptr;        // device flag of nonfinite_kernel
     // graph cache
     cudaGraphExec_t graph = nullptr;
@@ -551,12 +552,39 @@ int check_problem(const bp_problem* p) {
 
 int upload(bp_problem* p, const double* host, double2* dst, bool host_ptr = true);
 
+// Small device -> host reads on the run's critical path (the poll of n_active after every graph
+// replay, ||f|| for the zero-source check) go through zero-copy stores into pinned host memory
+// instead of cudaMemcpyAsync: a 4-byte D2H copy queues on the copy engine BEHIND another handle's
+// result download (bs.Pipeline: the previous job's 267 MB of u on c1), which stalled the start of
+// every compute turn by that copy's ~4.6 ms (r02h: e2e 32.5 -> see DESIGN 5).
+__global__ void publish_int_kernel(const int* __restrict__ src, volatile int* dst) {
+    *dst = *src;
+    __threadfence_system();
+}
+__global__ void publish_doubles_kernel(const double* __restrict__ src, volatile double* dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    __threadfence_system();
+}
+cudaError_t publish_int(bp_problem* p, const int* dev) {
+    publish_int_kernel<<<1, 1, 0, p->stream>>>(dev, p->host_active);
+    return cudaGetLastError();
+}
+// ||f|| per member -> host (synchronises the stream)
+int read_fnorm(bp_problem* p, std::vector<double>& fn) {
+    if (!p->host_fn) CU(cudaMallocHost(&p->host_fn, sizeof(double) * p->batch));
+    publish_doubles_kernel<<<1, 128, 0, p->stream>>>(p->fnorm_l2, p->host_fn, p->batch);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(p->stream));
+    for (int b = 0; b < p->batch; ++b) fn[b] = p->host_fn[b];
+    return BP_OK;
+}
+
 // true when the n doubles at dev (device memory) are all finite; synchronises the stream
 int all_finite(bp_problem* p, const double* dev, size_t n, bool* ok) {
     CU(cudaMemsetAsync(p->dflag, 0, sizeof(int), p->stream));
     nonfinite_kernel<<<grid_for(n), 256, 0, p->stream>>>(dev, n, p->dflag);
     CU(cudaGetLastError());
-    CU(cudaMemcpyAsync(p->host_active, p->dflag, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    CU(publish_int(p, p->dflag));
     CU(cudaStreamSynchronize(p->stream));
     *ok = *p->host_active == 0;
     return BP_OK;
@@ -1019,8 +1047,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
     rc = norms(p, p->y, p->fnorm_reta);
     if (rc) return rc;
     std::vector<double> fn(B);
-    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
+    if (int rc = read_fnorm(p, fn)) return rc;
     for (int b = 0; b < B; ++b)
         if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
 
@@ -1095,8 +1122,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
                               snapshots + 2 * nd * B * k);
                 if (rc) return rc;
             }
-            CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
-                               p->stream));
+            CU(publish_int(p, a.ctl.n_active));
             CU(cudaStreamSynchronize(p->stream));
             if (*p->host_active == 0) break;
         }
@@ -1115,8 +1141,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             if (rc) break;
             launched += kGraphSweeps;
             p->stat_launches += (int64_t)kps * kGraphSweeps;
-            CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
-                               p->stream));
+            CU(publish_int(p, a.ctl.n_active));
             CU(cudaStreamSynchronize(p->stream));
             for (int s = 0; s < kGraphSweeps; ++s) {
                 for (int k = 0; k < plan.n; ++k) {
@@ -1197,8 +1222,7 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             }
             launched += kGraphSweeps;
             p->stat_launches += (int64_t)kps * kGraphSweeps * std::max(split, 1);  // every part's graph
-            CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
-                               p->stream));
+            CU(publish_int(p, a.ctl.n_active));
             CU(cudaStreamSynchronize(p->stream));
             if (*p->host_active == 0) break;
         }
@@ -1221,8 +1245,7 @@ int run_core_generic(bp_problem* p, const bp_map* map, const bp_iter_config* cfg
     if (int rc = gen_spectral(p, true, p->f, p->y)) return rc;
     if (int rc = norms(p, p->y, p->fnorm_reta)) return rc;
     std::vector<double> fn(B);
-    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
+    if (int rc = read_fnorm(p, fn)) return rc;
     for (int b = 0; b < B; ++b)
         if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
     if (!have_u0) CU(cudaMemsetAsync(p->u0, 0, sizeof(double2) * p->alloc, p->stream));
@@ -1254,7 +1277,7 @@ int run_core_generic(bp_problem* p, const bp_map* map, const bp_iter_config* cfg
             if (snapshots && k < n_snap)
                 if (int rc = download(p, (k & 1) ? p->u1 : p->u0, nullptr, nullptr, snapshots + 2 * nd * B * k)) return rc;
             if ((snapshots && n_snap > 0) || k % kGraphSweeps == 0 || k == max_launch) {
-                CU(cudaMemcpyAsync(p->host_active, c.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+                CU(publish_int(p, c.n_active));
                 CU(cudaStreamSynchronize(p->stream));
                 if (*p->host_active == 0) break;
             }
@@ -1285,7 +1308,7 @@ int run_core_generic(bp_problem* p, const bp_map* map, const bp_iter_config* cfg
         if (snapshots && k < n_snap)  // u^k in buffer k & 1 for every member still iterating
             if (int rc = download(p, (k & 1) ? p->u1 : p->u0, nullptr, nullptr, snapshots + 2 * nd * B * k)) return rc;
         if ((snapshots && n_snap > 0) || k % kGraphSweeps == 0 || k == max_launch) {
-            CU(cudaMemcpyAsync(p->host_active, c.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+            CU(publish_int(p, c.n_active));
             CU(cudaStreamSynchronize(p->stream));
             if (*p->host_active == 0) break;
         }
@@ -1337,8 +1360,7 @@ int run_core_generic_maps(bp_problem* p, const bp_map* map, const bp_iter_config
     if (int rc = gen_spectral(p, true, p->f, p->y)) return rc;
     if (int rc = norms(p, p->y, p->fnorm_reta)) return rc;
     std::vector<double> fn(B);
-    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
+    if (int rc = read_fnorm(p, fn)) return rc;
     for (int b = 0; b < B; ++b)
         if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
     if (!have_u0) CU(cudaMemsetAsync(p->u0, 0, fb, p->stream));
@@ -1395,7 +1417,7 @@ int run_core_generic_maps(bp_problem* p, const bp_map* map, const bp_iter_config
         if (snapshots && k < n_snap)  // u^k in buffer k & 1 for every member still iterating
             if (int rc = download(p, (k & 1) ? p->u1 : p->u0, nullptr, nullptr, snapshots + 2 * nd * B * k)) return rc;
         if ((snapshots && n_snap > 0) || k % kGraphSweeps == 0 || k == max_launch) {
-            CU(cudaMemcpyAsync(p->host_active, c.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+            CU(publish_int(p, c.n_active));
             CU(cudaStreamSynchronize(p->stream));
             if (*p->host_active == 0) break;
         }
@@ -1545,8 +1567,7 @@ int run_core_periodic(bp_problem* p, const bp_map* map, const bp_iter_config* cf
     if (int rc = periodic_apply(p, 0, p->f, p->y, nullptr)) return rc;
     if (int rc = norms(p, p->y, p->fnorm_reta)) return rc;
     std::vector<double> fn(B);
-    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
+    if (int rc = read_fnorm(p, fn)) return rc;
     for (int b = 0; b < B; ++b)
         if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
     // U^0 = F u0 (u0 staged in p->x by the caller) or 0
@@ -1601,8 +1622,7 @@ int run_core_periodic(bp_problem* p, const bp_map* map, const bp_iter_config* cf
                 if (int rc = periodic_apply(p, 4, (k & 1) ? p->u1 : p->u0, p->y, nullptr)) return rc;
                 if (int rc = download(p, p->y, nullptr, nullptr, snapshots + 2 * nd * B * k)) return rc;
             }
-            CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
-                               p->stream));
+            CU(publish_int(p, a.ctl.n_active));
             CU(cudaStreamSynchronize(p->stream));
             if (*p->host_active == 0) break;
         }
@@ -1620,8 +1640,7 @@ int run_core_periodic(bp_problem* p, const bp_map* map, const bp_iter_config* cf
         if (rc) break;
         launched += kGraphSweeps;
         p->stat_launches += per_sweep * kGraphSweeps;
-        CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost,
-                           p->stream));
+        CU(publish_int(p, a.ctl.n_active));
         CU(cudaStreamSynchronize(p->stream));
         if (p->timing) {
             for (int s = 0; s < kGraphSweeps; ++s) {
@@ -1838,8 +1857,7 @@ int run_core_cdr_maps(bp_problem* p, const bp_map* map, const bp_iter_config* cf
     if (int rc = cdr_apply(p, 0, p->f, p->y, nullptr)) return rc;
     if (int rc = norms(p, p->y, p->fnorm_reta)) return rc;
     std::vector<double> fn(B);
-    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
+    if (int rc = read_fnorm(p, fn)) return rc;
     for (int b = 0; b < B; ++b)
         if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
     if (!have_u0) CU(cudaMemsetAsync(p->u0, 0, sizeof(double2) * p->alloc, p->stream));
@@ -1884,7 +1902,7 @@ int run_core_cdr_maps(bp_problem* p, const bp_map* map, const bp_iter_config* cf
         if (snapshots && k < n_snap)
             if (int rc = cdr_download(p, (k & 1) ? p->u1 : p->u0, snapshots + nd * B * k)) return rc;
         if ((snapshots && n_snap > 0) || k % kGraphSweeps == 0 || k == max_launch) {
-            CU(cudaMemcpyAsync(p->host_active, c.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+            CU(publish_int(p, c.n_active));
             CU(cudaStreamSynchronize(p->stream));
             if (*p->host_active == 0) break;
         }
@@ -1908,8 +1926,7 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
     if (int rc = cdr_apply(p, 0, p->f, p->y, nullptr)) return rc;
     if (int rc = norms(p, p->y, p->fnorm_reta)) return rc;
     std::vector<double> fn(B);
-    CU(cudaMemcpyAsync(fn.data(), p->fnorm_l2, sizeof(double) * B, cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
+    if (int rc = read_fnorm(p, fn)) return rc;
     for (int b = 0; b < B; ++b)
         if (!(fn[b] > 0.0)) return set_err(BP_EINVAL, "run: zero source");
     if (!have_u0) CU(cudaMemsetAsync(p->u0, 0, sizeof(double2) * p->alloc, p->stream));
@@ -1936,7 +1953,7 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
         return BP_OK;
     };
     auto poll = [&]() -> int {
-        CU(cudaMemcpyAsync(p->host_active, a.ctl.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+        CU(publish_int(p, a.ctl.n_active));
         CU(cudaStreamSynchronize(p->stream));
         return BP_OK;
     };
@@ -2969,7 +2986,7 @@ int bp_slab_active(bp_problem* p, int32_t* n_active) {
     if (!n_active) return set_err(BP_EINVAL, "null output");
     DeviceGuard guard(p->device);
     Control c = make_control(p);
-    CU(cudaMemcpyAsync(p->host_active, c.n_active, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    CU(publish_int(p, c.n_active));
     CU(cudaStreamSynchronize(p->stream));
     *n_active = *p->host_active;
     return BP_OK;
@@ -3086,6 +3103,7 @@ int bp_problem_destroy(bp_problem* p) {
                     (void*)p->gm2})
         if (q) cudaFree(q);
     if (p->host_active) cudaFreeHost(p->host_active);
+    if (p->host_fn) cudaFreeHost(p->host_fn);
     free_gplan(p->gplan_x);
     free_gplan(p->gplan_y);
     if (p->stream && p->own_stream) cudaStreamDestroy(p->stream);
