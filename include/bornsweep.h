@@ -90,8 +90,8 @@ typedef struct {
 } bp_map;
 
 /* bp::IterFormat / IterationConfig (proj/include/bp/iterate.hpp:12-18).  DIRECT (direction
- * = r, iterate.cpp:118-123) runs on the single-device Helmholtz families (Dirichlet, periodic);
- * slabs and CDR take CBS / NPBS only (BP_ENOTSUP). */
+ * = r, iterate.cpp:118-123) runs on the Helmholtz families (Dirichlet incl. slabs, periodic);
+ * CDR takes CBS / NPBS only (BP_ENOTSUP). */
 enum { BP_FMT_DIRECT = 0, BP_FMT_CBS = 1, BP_FMT_NPBS = 2 };
 typedef struct {
     int32_t format;   /* default BP_FMT_NPBS */
@@ -243,7 +243,11 @@ int bp_pipeline_destroy(bp_pipeline* pl);
  *   FourierDiag:               halo -> FD_A -> all-reduce sums[0..1] -> FINALIZE -> all-to-all,
  *                              COL_FD (the rank's block of m, bp_slab_set_multiplier),
  *                              all-to-all back -> FD_B -> colpass
- * bp_run semantics otherwise (CBS / NPBS formats). */
+ * IterFormat::Direct (cfg->format at BP_SLAB_INIT): the same sequences with the direction r^m;
+ * OptimalScalar-Euclidean + Direct needs w = A r = L_ref r - V r:
+ *   halo -> FD_A(a0 = 1: keeps r) -> all-reduce sums[0..1] -> FINALIZE -> all-to-all, COL_LREF,
+ *   all-to-all back -> RETA_C(a0 = 1) -> all-reduce sums[0..2] -> GAMMA -> OPT_B -> colpass
+ * bp_run semantics otherwise. */
 enum {
     BP_SLAB_FWD_F = 0,     /* t_rows <- y-DST of f; sums[0] = local ||f||^2 */
     BP_SLAB_COL = 1,       /* t_cols: x-DST, x Green weights, inverse x-DST (in place) */
@@ -260,7 +264,8 @@ enum {
     BP_SLAB_FD_A = 12,     /* entry sums -> sums[0..1]; t_rows <- y-DST of x^m */
     BP_SLAB_FD_B = 13,     /* t_rows = du: u^{m+1} = u^m + du; t_rows <- y-DST of V u^{m+1} + f */
     BP_SLAB_COL_FD = 14,   /* t_cols: x-DST, x m (FourierDiag multiplier block), inverse x-DST */
-    BP_SLAB_GAMMA = 15     /* gamma from the all-reduced sums[0..2] (R_eta metric) */
+    BP_SLAB_GAMMA = 15,    /* gamma from the all-reduced sums[0..2] (R_eta metric) */
+    BP_SLAB_COL_LREF = 16  /* t_cols: x-DST, x lambda, inverse x-DST (L_ref of the direction) */
 };
 typedef struct {
     int32_t rank, nranks, rows, row0, n;

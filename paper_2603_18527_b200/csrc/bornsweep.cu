@@ -350,6 +350,7 @@ struct bp_problem {
     double2* Tc = nullptr;                              // column-side block
     double* slab_sums = nullptr;
     bool slab_fd = false;  // bp_slab_set_multiplier uploaded the rank's FourierDiag block into fd
+    bool slab_direct = false;  // IterFormat::Direct for the slab run in progress (BP_SLAB_INIT)
     bool slab_running = false;
     // fused exchange (bp_slab_set_exchange)
     bool xchg_on = false;
@@ -2085,9 +2086,9 @@ int validate_run(const bp_problem* p, const bp_map* map, const bp_iter_config* c
     if (cfg->max_iters < 1) return set_err(BP_EINVAL, "run: max_iters must be >= 1");
     if (cfg->format != BP_FMT_NPBS && cfg->format != BP_FMT_CBS && cfg->format != BP_FMT_DIRECT)
         return set_err(BP_EINVAL, "run: unknown iteration format");
-    if (cfg->format == BP_FMT_DIRECT && (p->cdr || p->slab_log2 || p->slab_nranks > 1))
+    if (cfg->format == BP_FMT_DIRECT && p->cdr)
         return set_err(BP_ENOTSUP, "run: the Direct format is implemented for the Helmholtz families "
-                                   "(Dirichlet, periodic) on one device");
+                                   "(Dirichlet, periodic)");
     if (map->kind < BP_MAP_SCALAR || map->kind > BP_MAP_POINTWISE)
         return set_err(BP_EINVAL, "unknown correction map");
     if (map->kind == BP_MAP_FOURIER_DIAG && !map->m)
@@ -2592,6 +2593,7 @@ RowArgs slab_row_args(const bp_problem* p) {
     a.slab_log2 = p->slab_log2;
     a.row0 = p->row0;
     a.slab_sums = p->slab_sums;
+    a.direct = p->slab_direct ? 1 : 0;
     if (p->xchg_on && p->dim == 2) {  // 2-D: the row kernel's forward stores are the exchange
         a.xchg_on = 1;
         a.xchg_rank = p->slab_rank;
@@ -2672,6 +2674,7 @@ static int slab_create_impl(const bp_grid* grid, int dim, int32_t rank, int32_t 
         CUF(launch_col_pp(log2n, 16, CL_SLAB, C_GREEN, c, nullptr, true));
         CUF(launch_col_pp(log2n, 16, CL_SLAB, C_ONE, c, nullptr, true));
         CUF(launch_col_pp(log2n, 16, CL_SLAB, C_FD, c, nullptr, true));
+        CUF(launch_col_pp(log2n, 16, CL_SLAB, C_LREF, c, nullptr, true));
         if (dim == 3) CUF(launch_col_pp(log2n, 16, CL_YBLK, C_ONE, c, nullptr, true));
         if (log2n >= 6) CUF(launch_tri(log2n, CL_SLAB, c, nullptr, true));
     }
@@ -2873,6 +2876,7 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
                 if (int rc = slab_ylines(p, a.ctl, true)) return rc;
             return norms(p, p->f, p->slab_sums, true);
         case BP_SLAB_COL:
+        case BP_SLAB_COL_LREF:
         case BP_SLAB_COL_FD: {  // column (x-line) pass on the rank's received block
             ColArgs c = col_args(p);
             if (stage == BP_SLAB_COL_FD && !p->slab_fd)
@@ -2892,6 +2896,8 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
             if (stage == BP_SLAB_COL_FD) {  // x-DST, x m (correction.cpp:63-68), inverse x-DST
                 c.fd = p->fd;
                 CU(launch_col_pp(p->log2n, 16, CL_SLAB, C_FD, c, p->stream));
+            } else if (stage == BP_SLAB_COL_LREF) {  // x lambda: L_ref of the direction (Direct + Euclidean)
+                CU(launch_col_pp(p->log2n, 16, CL_SLAB, C_LREF, c, p->stream));
             } else if (p->tri && c.slab_cols % tri_cols_per_cta(p->log2n) == 0) {
                 CU(launch_tri(p->log2n, CL_SLAB, c, p->stream));
             } else {
@@ -2911,10 +2917,10 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
             if (!(cfg->rtol > 0.0 && cfg->rtol < 1.0)) return set_err(BP_EINVAL, "run: rtol must lie in (0,1)");
             if (cfg->max_iters < 1) return set_err(BP_EINVAL, "run: max_iters must be >= 1");
             if (!(a0 > 0.0)) return set_err(BP_EINVAL, "run: zero source");
-            if (cfg->format != BP_FMT_NPBS && cfg->format != BP_FMT_CBS)
-                return set_err(cfg->format == BP_FMT_DIRECT ? BP_ENOTSUP : BP_EINVAL,
-                               "slab decomposition: the CBS / NPBS formats");
+            if (cfg->format != BP_FMT_NPBS && cfg->format != BP_FMT_CBS && cfg->format != BP_FMT_DIRECT)
+                return set_err(BP_EINVAL, "run: unknown iteration format");
             if (int rc = ensure_trace(p, cfg->max_iters)) return rc;
+            p->slab_direct = cfg->format == BP_FMT_DIRECT;
             p->slab_max_iters = cfg->max_iters;
             p->slab_rtol = cfg->rtol;
             a = slab_row_args(p);
@@ -2942,7 +2948,7 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
             a.gamma = make_double2(map->gamma_re, map->gamma_im);
             if (d3)
                 if (int rc = slab_ylines(p, a.ctl)) return rc;
-            CU(launch_row(p->log2n, dim, R_SWEEP, a, p->stream));
+            CU(launch_row(p->log2n, dim, p->slab_direct ? R_SWEEP_D : R_SWEEP, a, p->stream));
             if (d3) return slab_ylines(p, a.ctl, true);
             return BP_OK;
         case BP_SLAB_ZERO_U:
@@ -2970,6 +2976,9 @@ int bp_slab_stage(bp_problem* p, int32_t stage, const bp_map* map, const bp_iter
                              : stage == BP_SLAB_OPT_B  ? R_OPT_B
                              : stage == BP_SLAB_FD_A   ? R_FD_A
                                                        : R_FD_B;
+            // Direct + Euclidean optimal scalar (a0 = 1 on FD_A / RETA_C): w = A r = L_ref r - V r, the
+            // direction kept by FD_A and L_ref r arriving through BP_SLAB_COL_LREF (plan_for)
+            a.lw = a0 == 1.0 && (mode == R_FD_A || mode == R_RETA_C);
             const bool inv = mode != R_OPT_B, fwd = mode != R_OPT_A && mode != R_RETA_C;
             if (d3 && inv)
                 if (int rc = slab_ylines(p, a.ctl)) return rc;

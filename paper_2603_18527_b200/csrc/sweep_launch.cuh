@@ -42,7 +42,7 @@ cudaError_t launch_row_t(const RowArgs& a, cudaStream_t s, bool prepare) {
     constexpr int NWR = RowWarps<L, PP>::value;
     using RG = RowGeom<L, PP, NWR>;
     // slab launches (2-D, row-major handoff, the modes the slab driver uses) -> SLAB instance
-    constexpr bool SLAB_OK = PP == 16 && MODE != R_SWEEP_D;
+    constexpr bool SLAB_OK = PP == 16;
     if constexpr (SLAB_OK && !SLAB) {
         if (a.slab_log2 || prepare) {
             const cudaError_t e = launch_row_t<L, MODE, PP, DIM, true>(a, s, prepare);
@@ -329,6 +329,7 @@ struct Pp8 {
             if (mode == C_ONE) return launch_col_t<L, C_ONE, 16, CL_SLAB>(a, s, prep);          \
             if (mode == C_GREEN) return launch_col_t<L, C_GREEN, 16, CL_SLAB>(a, s, prep);      \
             if (mode == C_FD) return launch_col_t<L, C_FD, 16, CL_SLAB>(a, s, prep);            \
+            if (mode == C_LREF) return launch_col_t<L, C_LREF, 16, CL_SLAB>(a, s, prep);        \
             return cudaErrorInvalidValue;                                                       \
         }                                                                                       \
         if (layout == CL_YBLK) {                                                                \

@@ -37,7 +37,7 @@ from . import _native as N
 from .api import BC_DIRICHLET, TERMINATION, IterationConfig, IterationTrace, ScalarMap, _check, _ptr
 
 (FWD_F, COL, INV_NORM, INIT, FWD_BORN, SWEEP, FINALIZE, ZERO_U, OPT_A, OPT_B, RETA_A, RETA_C, FD_A, FD_B,
- COL_FD, GAMMA) = range(16)
+ COL_FD, GAMMA, COL_LREF) = range(17)
 POLL_SWEEPS = 16
 
 
@@ -337,7 +337,18 @@ def run_slab(parts, comm, cmap, f, config: IterationConfig | None = None, u0=Non
     def sweep(k):
         # the launch sequences of plan_for (csrc/bornsweep.cu) with the collectives between
         comm.halo(parts, k & 1)
-        if kind == "OptimalScalarMap" and cmap.metric == "euclidean":
+        if kind == "OptimalScalarMap" and cmap.metric == "euclidean" and config.format == "direct":
+            stage_all(FD_A, a0=1.0)     # entry sums; keeps the direction r; r -> forward transform
+            comm.allreduce(parts)
+            stage_all(FINALIZE)
+            comm.transpose(parts, True)
+            stage_all(COL_LREF)         # L_ref r
+            comm.transpose(parts, False)
+            stage_all(RETA_C, a0=1.0)   # w = A r = L_ref r - V r: <w, r>, |w|^2
+            comm.allreduce(parts, 3)
+            stage_all(GAMMA)
+            stage_all(OPT_B)
+        elif kind == "OptimalScalarMap" and cmap.metric == "euclidean":
             stage_all(OPT_A)            # entry sums + <w, r>, |w|^2 with w = A x (correction.cpp:33-36)
             comm.allreduce(parts, 5)
             stage_all(FINALIZE, a0=1.0)  # entry m and gamma = <w, r> / <w, w>

@@ -13,8 +13,8 @@ import scipy.fft as sf
 import torch
 
 from paper_2603_18527_b200.api import TERMINATION, IterationTrace
-from paper_2603_18527_b200.slab import (COL, COL_FD, FD_A, FD_B, FINALIZE, FWD_BORN, FWD_F, GAMMA, INIT, INV_NORM,
-                                        OPT_A, OPT_B, RETA_A, RETA_C, SWEEP, ZERO_U)
+from paper_2603_18527_b200.slab import (COL, COL_FD, COL_LREF, FD_A, FD_B, FINALIZE, FWD_BORN, FWD_F, GAMMA, INIT,
+                                        INV_NORM, OPT_A, OPT_B, RETA_A, RETA_C, SWEEP, ZERO_U)
 
 
 def _sine(a):
@@ -141,7 +141,34 @@ class NumpySlabPart:
         scale = (2.0 / n) ** (3 if M.shape[1] != R else 2)  # forward x inverse sine sums
         M[...] = _sine_ax(_sine_ax(M, 0) * (self.fd.reshape(n, -1) * scale), 0)
 
-    def _map_stage(self, code):
+    def _col_lref(self):
+        """x-DST, x lambda x (2/n)^dim, inverse x-DST on the received block (L_ref of the direction)"""
+        n, R = self.n, self.rows
+        M = self._Tc.reshape(n, -1)
+        q = self.rank * R + np.arange(R)
+        if M.shape[1] == R:
+            lam = self.lap[:, None] + self.lap[q][None, :] - (self.k0sq + 1j * self.eta)
+            scale = (2.0 / n) ** 2
+        else:
+            lam = (self.lap[:, None, None] + self.lap[q][None, :, None] + self.lap[None, None, :]
+                   - (self.k0sq + 1j * self.eta)).reshape(n, -1)
+            scale = (2.0 / n) ** 3
+        M[...] = _sine_ax(_sine_ax(M, 0) * (lam * scale * self._mode_weights_flat()), 0)
+
+    def _mode_weights_flat(self):
+        n, R = self.n, self.rows
+        q = self.rank * R + np.arange(R)
+        if self._Tc.size == n * R:
+            w = np.ones((n, R))
+            w[0, :] = 0
+            w[:, q == 0] = 0
+            return w
+        w = np.ones((n, R, n))
+        w[0], w[:, :, 0] = 0, 0
+        w[:, q == 0, :] = 0
+        return w.reshape(n, -1)
+
+    def _map_stage(self, code, lw=False):
         """OPT_A / OPT_B / RETA_A / RETA_C / FD_A / FD_B (csrc/sweep_kernels.cuh RowMode)."""
         if self.status != 0:
             return
@@ -150,24 +177,28 @@ class NumpySlabPart:
         if code in (OPT_A, RETA_A, FD_A):  # entry modes: m = sweep
             ua = self._u[self.sweep & 1]
             u = ua[1:R + 1]
-            r = self.f - (self._stencil(ua) / self.h ** 2 - self.k2 * u)
+            r = (self.f - (self._stencil(ua) / self.h ** 2 - self.k2 * u)) * mask
             x = (self._rows_inv() - u) * mask
             self._sums[0] = np.sum((np.abs(r) ** 2)[mask])
             self._sums[1] = np.sum((np.abs(x) ** 2)[mask])
+            d = r if self.direct else x  # the direction (iterate.cpp:118-123)
             if code == OPT_A:  # w = A x = r - V x (key identity), gamma = <w, r> / <w, w>
                 w = (r - self.V * x)[mask]
                 num = np.vdot(w, r[mask])
                 self._sums[2:5] = num.real, num.imag, np.sum(np.abs(w) ** 2)
                 self.x = x
             elif code == RETA_A:
-                self.x = x
-                self._rows_fwd(self.V * x)
+                self.x = d
+                self._rows_fwd(self.V * d)
             else:
-                self._rows_fwd(x)
+                if lw:
+                    self.x = d
+                self._rows_fwd(d)
             return
         m = self.sweep - 1  # post modes: entry m was recorded
         if code == RETA_C:
-            w = (self.x - self._rows_inv())[mask]
+            # R_eta metric: w = x - G V x; Direct + Euclidean (lw): w = L_ref x - V x = A x
+            w = ((self._rows_inv() - self.V * self.x) if lw else (self.x - self._rows_inv()))[mask]
             num = np.vdot(w, self.x[mask])
             self._sums[0:3] = num.real, num.imag, np.sum(np.abs(w) ** 2)
             return
@@ -188,7 +219,10 @@ class NumpySlabPart:
     def stage(self, code, cmap=None, config=None, a0=0.0, a1=0.0):
         R, n = self.rows, self.n
         if code in (OPT_A, OPT_B, RETA_A, RETA_C, FD_A, FD_B):
-            self._map_stage(code)
+            self._map_stage(code, lw=a0 == 1.0)
+        elif code == COL_LREF:
+            if self.status == 0:
+                self._col_lref()
         elif code == GAMMA:
             self._gamma(0)
         elif code == COL_FD:
@@ -216,6 +250,7 @@ class NumpySlabPart:
                 raise ValueError("run: zero source")
             self.fn, self.gn = a0, a1
             self.rtol, self.max_iters = config.rtol, config.max_iters
+            self.direct = config.format == "direct"
             self.l2 = np.full(config.max_iters + 1, np.nan)
             self.rt = np.full(config.max_iters + 1, np.nan)
             self.status, self.sweep = 0, 0
@@ -242,7 +277,7 @@ class NumpySlabPart:
             self._sums[0] = np.sum((np.abs(r) ** 2)[mask])
             self._sums[1] = np.sum((np.abs(x) ** 2)[mask])
             g = 1j / self.eta * self.V if cmap.__class__.__name__ == "PointwiseMap" else complex(cmap.gamma)
-            unew = u + g * x
+            unew = u + g * (r if self.direct else x)
             unew[:, 0] = 0
             nxt = self._u[(m + 1) & 1][1:R + 1]
             nxt[self.valid] = unew[self.valid]
@@ -366,7 +401,7 @@ class NumpySlabPart3(NumpySlabPart):
 
     def stage(self, code, cmap=None, config=None, a0=0.0, a1=0.0):
         R, n = self.rows, self.n
-        if code in (OPT_A, OPT_B, RETA_A, RETA_C, FD_A, FD_B, GAMMA, COL_FD):
+        if code in (OPT_A, OPT_B, RETA_A, RETA_C, FD_A, FD_B, GAMMA, COL_FD, COL_LREF):
             NumpySlabPart.stage(self, code, cmap, config, a0, a1)
         elif code == FWD_F:
             self._block(self._yz(self.f))
@@ -416,7 +451,7 @@ class NumpySlabPart3(NumpySlabPart):
             self._sums[0] = np.sum((np.abs(r) ** 2)[mask])
             self._sums[1] = np.sum((np.abs(x) ** 2)[mask])
             g = 1j / self.eta * self.V if cmap.__class__.__name__ == "PointwiseMap" else complex(cmap.gamma)
-            unew = u + g * x
+            unew = u + g * (r if self.direct else x)
             unew[:, 0, :], unew[:, :, 0] = 0, 0
             nxt = self._u[(m + 1) & 1][1:R + 1]
             nxt[self.valid] = unew[self.valid]

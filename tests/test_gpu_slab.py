@@ -82,8 +82,6 @@ def test_slab_errors(gpu):
     parts = parts_for(k2, k0, eta, 2)
     with pytest.raises(ValueError, match="zero source"):
         run_slab(parts, LocalComm(), bs.ScalarMap(1.0), np.zeros_like(f))
-    with pytest.raises(NotImplementedError):  # IterFormat::Direct: single-device handles only
-        run_slab(parts, LocalComm(), bs.ScalarMap(1.0), f, bs.IterationConfig(format="direct"))
     with pytest.raises(ValueError):
         run_slab(parts, LocalComm(), bs.FourierDiagMap(np.ones((3, 3), complex)), f)
 
@@ -222,3 +220,42 @@ def test_fused_exchange_matches_collectives(gpu, dim, n, nranks):
     assert fused.trace.iters == base.trace.iters
     assert np.array_equal(fused.u, base.u)
     assert np.array_equal(fused.trace.res_l2_rel, base.trace.res_l2_rel)
+
+
+@pytest.mark.parametrize("name", ["scalar", "pointwise", "optimal_l2", "optimal_reta", "fourier_diag"])
+@pytest.mark.parametrize("dim,n,nranks", [(2, 64, 2), (2, 256, 4), (3, 32, 2)])
+def test_slab_direct_format(gpu, name, dim, n, nranks):
+    """IterFormat::Direct (iterate.cpp:118-123) on slabs with every map against the single-GPU
+    path (same kernels modulo the reductions' order) and, for the 2-D cases, the oracle."""
+    from oracle import FMT_DIRECT, MAP_FOURIER_DIAG, MAP_OPTIMAL_SCALAR, METRIC_EUCLIDEAN, METRIC_RETA
+    k2, f, k0, eta = inst3(n, seed=9) if dim == 3 else instance(n, seed=9)
+    h2 = (1.0 / n) ** 2
+    m = 0.1 * h2 * fd_multiplier(k2.shape)
+    cmap, kw = {
+        "scalar": (bs.ScalarMap(0.1 * h2), dict(map_kind=MAP_SCALAR, gamma=0.1 * h2)),
+        "pointwise": (bs.PointwiseMap(), dict(map_kind=MAP_POINTWISE)),
+        "optimal_l2": (bs.OptimalScalarMap("euclidean"), dict(map_kind=MAP_OPTIMAL_SCALAR, metric=METRIC_EUCLIDEAN)),
+        "optimal_reta": (bs.OptimalScalarMap("reta"), dict(map_kind=MAP_OPTIMAL_SCALAR, metric=METRIC_RETA)),
+        "fourier_diag": (bs.FourierDiagMap(m), dict(map_kind=MAP_FOURIER_DIAG, m=m)),
+    }[name]
+    cfg = bs.IterationConfig("direct", 1e-8, 20)
+    for fused in (False, True):
+        res = run_slab([SlabPart(k2, k0, eta, r, nranks) for r in range(nranks)], LocalComm(fused=fused), cmap, f, cfg)
+        with bs.HelmholtzDirichlet(k2[None], np.array([k0]), np.array([eta]), dim=dim) as p:
+            one = bs.run(p, cmap, f[None], cfg)
+        # (Richardson on A with the pointwise or the R_eta-optimal step diverges within a few
+        # sweeps -- on every path alike: same count, same termination)
+        assert res.trace.iters == one.trace.iters
+        assert res.trace.terminated == one.trace.terminated
+        # optimal-scalar trajectories amplify the reductions' roundoff (see the staged-map test)
+        tol = 1e-9 if name.startswith("optimal") else 1e-11
+        if res.trace.terminated != "diverged":
+            assert rel(res.u, one.u[0]) < tol
+        np.testing.assert_allclose(res.trace.res_l2_rel, one.trace.res_l2_rel, rtol=100 * tol)
+        np.testing.assert_allclose(res.trace.res_reta_rel, one.trace.res_reta_rel, rtol=100 * tol)
+    if dim == 2:
+        ref = OracleProblem(k2, k0, eta).run(f, fmt=FMT_DIRECT, rtol=1e-8, max_iters=20, **kw)
+        assert res.trace.iters == ref.iters and res.trace.terminated == ref.terminated
+        if ref.terminated != "diverged":
+            assert rel(res.u, ref.u) < FIELD_TOL
+        np.testing.assert_allclose(res.trace.res_l2_rel, ref.res_l2, rtol=1e-8, atol=1e-13)

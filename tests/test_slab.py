@@ -100,6 +100,31 @@ def test_local_slab3d_driver_staged_maps_match_oracle(which):
     assert rel(res.u, ref.u) < FIELD_TOL
 
 
+@pytest.mark.parametrize("name", ["scalar", "pointwise", "optimal_l2", "optimal_reta", "fourier_diag"])
+def test_local_slab_driver_direct_format_matches_oracle(name):
+    """IterFormat::Direct (direction = r, iterate.cpp:118-123) on slabs with every map; the
+    Euclidean optimal scalar then needs w = A r through a distributed L_ref application."""
+    from oracle import (FMT_DIRECT, MAP_FOURIER_DIAG, MAP_OPTIMAL_SCALAR, METRIC_EUCLIDEAN, METRIC_RETA)
+    k2, f, k0, eta = instance(32)
+    h2 = (1.0 / 32) ** 2
+    m = 0.1 * h2 * fd_multiplier(k2.shape)  # Richardson on A needs a step of the order of h^2
+    cmap, kw = {
+        "scalar": (bs.ScalarMap(0.1 * h2), dict(map_kind=MAP_SCALAR, gamma=0.1 * h2)),
+        "pointwise": (bs.PointwiseMap(), dict(map_kind=MAP_POINTWISE)),
+        "optimal_l2": (bs.OptimalScalarMap("euclidean"), dict(map_kind=MAP_OPTIMAL_SCALAR, metric=METRIC_EUCLIDEAN)),
+        "optimal_reta": (bs.OptimalScalarMap("reta"), dict(map_kind=MAP_OPTIMAL_SCALAR, metric=METRIC_RETA)),
+        "fourier_diag": (bs.FourierDiagMap(m), dict(map_kind=MAP_FOURIER_DIAG, m=m)),
+    }[name]
+    cfg = bs.IterationConfig("direct", 1e-8, 25)
+    parts = [NumpySlabPart(k2, k0, eta, r, 2) for r in range(2)]
+    res = run_slab(parts, LocalComm(), cmap, f, cfg)
+    ref = OracleProblem(k2, k0, eta).run(f, fmt=FMT_DIRECT, rtol=1e-8, max_iters=25, **kw)
+    assert res.trace.terminated == ref.terminated and res.trace.iters == ref.iters
+    assert rel(res.u, ref.u) < FIELD_TOL
+    np.testing.assert_allclose(res.trace.res_l2_rel, ref.res_l2, rtol=1e-8, atol=1e-13)
+    np.testing.assert_allclose(res.trace.res_reta_rel, ref.res_reta, rtol=1e-8, atol=1e-13)
+
+
 def test_local_slab_driver_warm_start_and_max_iters():
     k2, f, k0, eta = instance(32, seed=5)
     u0 = 1e-3 * (np.random.default_rng(2).standard_normal(k2.shape) + 0j)
