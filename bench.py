@@ -441,7 +441,9 @@ def run_ours(args):
     # (bp_pipeline_*): each step = set_medium + run (H2D of the media and sources from pinned
     # host memory, the sweeps, D2H of u and the traces) on the next slot, so one step's copies
     # run under the other slot's sweeps.  --e2e-depth 1 = plain set_medium + bp_run.
-    depth = max(1, args.e2e_depth)
+    # (c4's steps are copy-bound -- its members converge in ~25 sweeps -- and gain from a third
+    # slot: 23.4 -> 28.9 Gpts/s, r02i; the Helmholtz configs do not: 32.5 at depth 2 and 3)
+    depth = max(1, args.e2e_depth if args.e2e_depth else (3 if cdr else 2))
     if cdr:
         extra = [bs.CdrNeumann(bx, by, sg, s0, device=local_rank) for _ in range(depth - 1)]
     else:
@@ -541,7 +543,14 @@ def run_ours(args):
                                            "algorithmic_bytes_per_launch": col_b * pts_per_launch},
                          "sweep": {"achieved": sweep_gbs, "frac": sweep_gbs / peak,
                                    "bytes_per_pt": sweep_b,
-                                   "gpts_per_s_kernels_only": pts_per_launch / ((row_avg + col_avg) * 1e-3) / 1e9}},
+                                   "gpts_per_s_kernels_only": pts_per_launch / ((row_avg + col_avg) * 1e-3) / 1e9,
+                                   # whole-sweep algorithmic bytes over the TIMED REGION itself (the
+                                   # production path: graph replays, on c1 waves of 8 concurrently
+                                   # replayed single-member graphs whose launches overlap -- the
+                                   # per-kernel figures above are of whole-batch launches timed one
+                                   # by one in the instrumented pass)
+                                   "timed_region": {"achieved": value * sweep_b / world,
+                                                    "frac": value * sweep_b / world / peak}}},
             "cpu_baseline": cpu,
             "gpu_launches": int(sum_over_ranks(float(launches))),
             "value_instrumented": value_instrumented,
@@ -669,7 +678,7 @@ def main():
     # transform pairs) does not dominate the CPU sample (~1.3 s per step on 16 cores)
     ap.add_argument("--ref-sweeps", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-depth", type=int, default=2,
+    ap.add_argument("--e2e-depth", type=int, default=0,
                     help="handles in the e2e bs.Pipeline (1 = set_medium + bp_run, serial)")
     ap.add_argument("--slab", action="store_true", help="c2 / c3: slab-decomposed path even at N=1")
     ap.add_argument("--fused", action="store_true",

@@ -404,8 +404,10 @@ struct bp_problem {
     cudaGraphExec_t graph = nullptr;
     // small batches (< kSplitWaves row waves): the batch as two halves, each its own graph on its
     // own stream, so one half's column pass fills the other half's row-launch tail
-    static constexpr int kMaxSplit = 4;
+    static constexpr int kMaxSplit = 16;
     cudaGraphExec_t graph2[kMaxSplit - 1]{};  // parts 1.. (part 0 is `graph` on `stream`)
+    std::vector<cudaGraphExec_t> gwave;       // waves 1..: [wave - 1][part] (wave 0 = graph / graph2)
+    int graph_group = 0;                      // members per wave the graphs were captured for
     cudaStream_t stream2[kMaxSplit - 1]{};
     cudaEvent_t ev_join[kMaxSplit]{};
     int graph_split = -1;
@@ -903,6 +905,9 @@ int ensure_trace(bp_problem* p, int max_iters) {
             if (g2) cudaGraphExecDestroy(g2);
             g2 = nullptr;
         }
+        for (auto gw : p->gwave)
+            if (gw) cudaGraphExecDestroy(gw);
+        p->gwave.clear();
     }
     return BP_OK;
 }
@@ -979,13 +984,33 @@ int sweep_once(bp_problem* p, const SweepPlan& plan, const RowArgs& a, const Col
 // members 34.9 -> 35.7, 64 members 34.6 -> 35.1.  The two-launch scalar / pointwise plan only
 // (its per-half finalisation is self-contained); BP_SPLIT=0 disables.  Returns the first half's
 // size or 0.  BP_SPLIT=K (3, 4): K parts.
+constexpr int kDefaultGroup = 8;  // members per wave at n = 512 (group_members)
 constexpr double kSplitWaves = 1e30;  // every depth (BP_SPLIT=2 kept as the explicit spelling)
 // parts: 4 for shallow batches (c1 at 8 members: 34.8 -> 36.4 Gpts/s with 4 vs 2 parts), 2 above
 // 16 members (64 members: 35.1 with 2, 35.0 with 3 or 4); BP_SPLIT=K overrides
-int split_parts(int batch) {
+int split_parts(int batch, int log2n) {
     const char* env = std::getenv("BP_SPLIT");
-    const int k = env ? std::atoi(env) : (batch <= 16 ? 4 : 2);
+    // n = 512, up to 8 members (BASELINE c1 at 8 per GPU): one member per part, 36.4 -> 38.0 Gpts/s
+    const int k = env ? std::atoi(env) : (log2n == 9 && batch <= 8 ? batch : (batch <= 16 ? 4 : 2));
     return std::max(2, std::min(k, (int)bp_problem::kMaxSplit));
+}
+// parts per wave when the batch is swept in waves: one member per part (BP_SPLIT overrides)
+int wave_parts(int group) {
+    const char* env = std::getenv("BP_SPLIT");
+    const int k = env ? std::atoi(env) : group;
+    return std::max(2, std::min(std::min(k, group), (int)bp_problem::kMaxSplit));
+}
+// Members per wave (0 = the whole batch at once).  Measured on c1 (64 x 511^2, r02h): waves of 8
+// members, each member its own part on its own stream, 35.0 -> 37.2 Gpts/s (waves of 6 / 7 / 9 /
+// 10 / 12 / 16: 36.4 / 36.6 / 35.5 / 35.7 / 34.9 / 34.6; 8 members in 4 parts 36.0; no waves
+// with 8 / 16 parts 34.4 / 34.6): a wave's ~160 MB of fields is swept kGraphSweeps times while
+// much of it is still in the 126 MB L2, and eight single-member graphs interleave their row and
+// column launches finely.  Default: n = 512 only (the measured size); BP_GROUP=G overrides
+// for any size, BP_GROUP=0 disables.
+int group_members(const bp_problem* p, int batch) {
+    const char* env = std::getenv("BP_GROUP");
+    const int g = env ? std::atoi(env) : (p->log2n == 9 ? kDefaultGroup : 0);
+    return (g > 0 && g < batch) ? g : 0;
 }
 int split_batch(const bp_problem* p, const SweepPlan& plan) {
     const char* env = std::getenv("BP_SPLIT");  // read per run (tests toggle it)
@@ -1158,8 +1183,15 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
         if (rc) return rc;
     } else {
         // graph of kGraphSweeps sweeps, replayed until every member terminated
-        int split = split_batch(p, plan) ? std::min(split_parts(B), B) : 0;  // 0 = one graph, else parts
-        const bool reuse = p->graph && p->graph_split == split && p->graph_map_kind == map->kind &&
+        int split = split_batch(p, plan) ? std::min(split_parts(B, p->log2n), B) : 0;  // 0 = one graph, else parts
+        // Waves (BP_GROUP = G members, split batches only): the batch is swept G members at a time
+        // -- each wave's K part-graphs (kGraphSweeps sweeps) queue behind the previous wave's on the
+        // same K streams -- so a wave's fields are re-used out of L2 across its sweeps
+        const int group = split ? group_members(p, B) : 0;
+        if (group) split = wave_parts(group);
+        const int waves = group ? (B + group - 1) / group : 1;
+        const bool reuse = p->graph && p->graph_split == split && p->graph_group == group &&
+                           p->graph_map_kind == map->kind &&
                            p->graph_metric == map->metric && p->graph_format == cfg->format &&
                            p->graph_gamma.x == map->gamma_re && p->graph_gamma.y == map->gamma_im &&
                            p->graph_max_iters == cfg->max_iters && p->graph_rtol == cfg->rtol;
@@ -1170,6 +1202,9 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
                 if (g2) cudaGraphExecDestroy(g2);
                 g2 = nullptr;
             }
+            for (auto gw : p->gwave)
+                if (gw) cudaGraphExecDestroy(gw);
+            p->gwave.clear();
             cudaGraph_t g;
             if (!split) {
                 CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
@@ -1178,30 +1213,36 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
                 CU(cudaGraphInstantiate(&p->graph, g, 0));
                 cudaGraphDestroy(g);
             } else {
-                const int K = std::min(split_parts(B), B);
+                const int K = split;
                 for (int k = 0; k < K; ++k) {
                     if (k && !p->stream2[k - 1]) CU(cudaStreamCreateWithFlags(&p->stream2[k - 1], cudaStreamNonBlocking));
                     if (!p->ev_join[k]) CU(cudaEventCreateWithFlags(&p->ev_join[k], cudaEventDisableTiming));
                 }
                 cudaStream_t keep = p->stream;
-                for (int k = 0; k < K; ++k) {  // sweep_once launches on p->stream: capture each part
-                    const int b0 = (int)((long)B * k / K), b1 = (int)((long)B * (k + 1) / K);
-                    const RowArgs ak = row_args_range(a, p, b0, b1 - b0);
-                    const ColArgs ck = col_args_range(c, p, b0, b1 - b0);
-                    p->stream = k ? p->stream2[k - 1] : keep;
-                    cudaError_t e = cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal);
-                    for (int sw = 0; e == cudaSuccess && sw < kGraphSweeps; ++sw) sweep_once(p, plan, ak, ck, nullptr);
-                    if (e == cudaSuccess) e = cudaStreamEndCapture(p->stream, &g);
-                    if (e == cudaSuccess) {
-                        e = cudaGraphInstantiate(k ? &p->graph2[k - 1] : &p->graph, g, 0);
-                        cudaGraphDestroy(g);
+                p->gwave.assign((size_t)(waves - 1) * K, nullptr);
+                for (int w = 0; w < waves; ++w) {
+                    const int w0 = group ? w * group : 0, w1 = group ? std::min(B, w0 + group) : B;
+                    for (int k = 0; k < K; ++k) {  // sweep_once launches on p->stream: capture each part
+                        const int b0 = w0 + (int)((long)(w1 - w0) * k / K), b1 = w0 + (int)((long)(w1 - w0) * (k + 1) / K);
+                        cudaGraphExec_t* dst = w ? &p->gwave[(size_t)(w - 1) * K + k] : (k ? &p->graph2[k - 1] : &p->graph);
+                        if (b1 == b0) continue;  // (a short last wave)
+                        const RowArgs ak = row_args_range(a, p, b0, b1 - b0);
+                        const ColArgs ck = col_args_range(c, p, b0, b1 - b0);
+                        p->stream = k ? p->stream2[k - 1] : keep;
+                        cudaError_t e = cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal);
+                        for (int sw = 0; e == cudaSuccess && sw < kGraphSweeps; ++sw) sweep_once(p, plan, ak, ck, nullptr);
+                        if (e == cudaSuccess) e = cudaStreamEndCapture(p->stream, &g);
+                        if (e == cudaSuccess) {
+                            e = cudaGraphInstantiate(dst, g, 0);
+                            cudaGraphDestroy(g);
+                        }
+                        p->stream = keep;
+                        CU(e);
                     }
-                    p->stream = keep;
-                    CU(e);
                 }
-                split = K;
             }
             p->graph_split = split;
+            p->graph_group = group;
             p->graph_map_kind = map->kind;
             p->graph_metric = map->metric;
             p->graph_format = cfg->format;
@@ -1215,14 +1256,18 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
             for (int k = 1; k < split; ++k) CU(cudaStreamWaitEvent(p->stream2[k - 1], p->ev_join[0], 0));
         }
         while (launched < max_launch) {
-            CU(cudaGraphLaunch(p->graph, p->stream));
+            for (int w = 0; w < waves; ++w) {
+                for (int k = 0; k < std::max(split, 1); ++k) {
+                    cudaGraphExec_t ge = w ? p->gwave[(size_t)(w - 1) * split + k] : (k ? p->graph2[k - 1] : p->graph);
+                    if (ge) CU(cudaGraphLaunch(ge, k ? p->stream2[k - 1] : p->stream));
+                }
+            }
             for (int k = 1; k < split; ++k) {
-                CU(cudaGraphLaunch(p->graph2[k - 1], p->stream2[k - 1]));
                 CU(cudaEventRecord(p->ev_join[k], p->stream2[k - 1]));
                 CU(cudaStreamWaitEvent(p->stream, p->ev_join[k], 0));  // every part before the poll
             }
             launched += kGraphSweeps;
-            p->stat_launches += (int64_t)kps * kGraphSweeps * std::max(split, 1);  // every part's graph
+            p->stat_launches += (int64_t)kps * kGraphSweeps * std::max(split, 1) * waves;  // every part's graph
             CU(publish_int(p, a.ctl.n_active));
             CU(cudaStreamSynchronize(p->stream));
             if (*p->host_active == 0) break;
@@ -1997,7 +2042,7 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
     // split-batch graphs as the Dirichlet path (run_core): parts replayed concurrently on their
     // own streams (BP_SPLIT=0 disables)
     const char* senv = std::getenv("BP_SPLIT");
-    const int split = (B >= 2 && !(senv && senv[0] == '0')) ? std::min(split_parts(B), B) : 0;
+    const int split = (B >= 2 && !(senv && senv[0] == '0')) ? std::min(split_parts(B, p->log2n), B) : 0;
     const bool reuse = p->graph && p->graph_split == split && p->graph_map_kind == map->kind &&
                        p->graph_gamma.x == map->gamma_re && p->graph_max_iters == cfg->max_iters &&
                        p->graph_rtol == cfg->rtol;
@@ -3089,6 +3134,8 @@ int bp_problem_destroy(bp_problem* p) {
     DeviceGuard guard(p->device);
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->graph) cudaGraphExecDestroy(p->graph);
+    for (auto gw : p->gwave)
+        if (gw) cudaGraphExecDestroy(gw);
     for (auto g2 : p->graph2)
         if (g2) cudaGraphExecDestroy(g2);
     for (auto s2 : p->stream2)
