@@ -37,7 +37,10 @@ int set_err(int code, const std::string& msg) {
             return set_err(BP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
     } while (0)
 
-constexpr int kGraphSweeps = 16;
+#ifndef BS_GRAPH_SWEEPS
+#define BS_GRAPH_SWEEPS 16
+#endif
+constexpr int kGraphSweeps = BS_GRAPH_SWEEPS;
 constexpr double kPi = 3.14159265358979323846;
 // sinp table: sin(pi j/n)
 constexpr double kSinScale = 1.0;
