@@ -232,6 +232,58 @@ __device__ __forceinline__ double rcp_green(double x) {
 #endif
 }
 
+// L2 eviction-priority hints (experiment knob BS_L2_HINTS): with the batch swept in waves of 8
+// members (bornsweep.cu group_members) a wave's fields are re-read every sweep, but its 160 MB do
+// not fit the L2.  Bit 1: the medium k2 and the source f (read once per sweep, never written) are
+// loaded evict_first -- measured on c1: 37.4 -> 38.6 Gpts/s (38.1 -> 39.2 on a less power-capped
+// board); bit 4: the intermediate T (written by one launch, read by the next) loaded and stored
+// evict_last, row kernel and tridiagonal pass -- 39.17 -> 39.53; bit 2: the iterate likewise --
+// all three together measured lower (38.3 vs 38.6).  Default 5 = bits 1 + 4.
+#ifndef BS_L2_HINTS
+#define BS_L2_HINTS 5
+#endif
+#define BS_L2_STREAM (BS_L2_HINTS & 1)  // k2, f loads evict_first
+#define BS_L2_KEEP_U (BS_L2_HINTS & 2)  // iterate loads / stores evict_last
+#define BS_L2_KEEP_T (BS_L2_HINTS & 4)  // intermediate T loads / stores evict_last
+// (sm_100a: the plain .L2::evict_* qualifiers need 256-bit accesses; 128-bit ones take a policy)
+__device__ __forceinline__ unsigned long long l2_policy_first() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ unsigned long long l2_policy_last() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p, [[maybe_unused]] unsigned long long pol) {
+#if BS_L2_STREAM
+    double2 v;
+    asm("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+#else
+    return *p;
+#endif
+}
+template <bool ON>
+__device__ __forceinline__ double2 ld_keep(const double2* p, [[maybe_unused]] unsigned long long pol) {
+    if constexpr (ON) {
+        double2 v;
+        asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol) : "memory");
+        return v;
+    } else {
+        return *p;
+    }
+}
+template <bool ON>
+__device__ __forceinline__ void st_keep(double2* p, double2 v, [[maybe_unused]] unsigned long long pol) {
+    if constexpr (ON) {
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+    } else {
+        *p = v;
+    }
+}
+
 // TMA bulk prefetch of a contiguous range into L2 (sm_90+: cp.async.bulk.prefetch.L2).
 // bytes: multiple of 16, address 16-B aligned.  Fire-and-forget, no registers held.
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
@@ -359,6 +411,8 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     constexpr unsigned VALID_LINES = DIM == 3 ? (unsigned)((N - 1) * (N - 1)) : (unsigned)(N - 1);
     extern __shared__ double2 smem[];
 
+    [[maybe_unused]] const unsigned long long pol_s = BS_L2_STREAM ? l2_policy_first() : 0ull;
+    [[maybe_unused]] const unsigned long long pol_k = (BS_L2_KEEP_U || BS_L2_KEEP_T) ? l2_policy_last() : 0ull;
     const int t = threadIdx.x % T;
     const int e = threadIdx.x / T;
     const long grow = grp * EPB + e;
@@ -383,7 +437,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         const int i0 = valid ? i : 0;
 #pragma unroll
         for (int mm = 0; mm < P; ++mm)  // in bounds for every thread (member / line clamped)
-            xT[mm] = a.T[t_index<LOG2N, DIM, SLAB>(sl0, mem0, i0, t + T * mm)];
+            xT[mm] = ld_keep<(BS_L2_KEEP_T != 0)>(&a.T[t_index<LOG2N, DIM, SLAB>(sl0, mem0, i0, t + T * mm)], pol_k);
     }
     int m = 0;  // trace entry this launch belongs to
     if (S::ITER && valid) {
@@ -498,14 +552,14 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
         Opnd o;
         o.un = o.us = o.uw = o.ue = o.ua = o.ub = o.x = zero;
         const int j = t + T * mm;
-        o.u = ucur[row + j];
-        o.k2 = a.k2[row + j];
-        o.f = a.f[row + j];
+        o.u = ld_keep<(BS_L2_KEEP_U != 0)>(&ucur[row + j], pol_k);
+        o.k2 = ld_stream(&a.k2[row + j], pol_s);
+        o.f = ld_stream(&a.f[row + j], pol_s);
         if constexpr (S::ENTRY) {
-            o.un = ucur[row - N + j];
-            o.us = ucur[row + N + j];
-            o.uw = ucur[row + j - 1];
-            o.ue = ucur[row + j + 1];
+            o.un = ld_keep<(BS_L2_KEEP_U != 0)>(&ucur[row - N + j], pol_k);
+            o.us = ld_keep<(BS_L2_KEEP_U != 0)>(&ucur[row + N + j], pol_k);
+            o.uw = ld_keep<(BS_L2_KEEP_U != 0)>(&ucur[row + j - 1], pol_k);
+            o.ue = ld_keep<(BS_L2_KEEP_U != 0)>(&ucur[row + j + 1], pol_k);
             if constexpr (DIM == 3) {
                 o.ua = ucur[row - PLANE + j];
                 o.ub = ucur[row + PLANE + j];
@@ -591,7 +645,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
 #endif
                     double2 unew = cadd(u, cmul(g, d));
                     if (j == 0) unew = zero;
-                    if (valid) unext[row + j] = unew;
+                    if (valid) st_keep<(BS_L2_KEEP_U != 0)>(&unext[row + j], unew, pol_k);
                     qv = cadd(cmul(V, unew), f);
                 } else if constexpr (MODE == R_OPT_A) {
                     // w = A x = (L_ref - V) G r = r - V x (key identity; the reference applies
@@ -623,7 +677,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
                 }
                 double2 unew = cadd(u, du);
                 if (j == 0) unew = zero;
-                if (valid) unext[row + j] = unew;
+                if (valid) st_keep<(BS_L2_KEEP_U != 0)>(&unext[row + j], unew, pol_k);
                 qv = cadd(cmul(V, unew), f);
             }
         }
@@ -688,7 +742,7 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
                         continue;
                     }
                 }
-                a.T[ix] = v;
+                st_keep<(BS_L2_KEEP_T != 0)>(&a.T[ix], v, pol_k);
             }
         }
     }

@@ -164,6 +164,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+// same with an L2 eviction-priority policy (sweep_kernels.cuh l2_policy_*); bit 4 of BS_L2_HINTS
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, unsigned long long pol) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -284,6 +289,7 @@ tri_kernel(const ColArgs a) {
     double2* xs = zl + C * SP;             // [C][SP] separators (X_S = 0 at [S])
     double2* tot = xs + C * SP;            // [C][CH] chunk maps (A, B)
 
+    [[maybe_unused]] const unsigned long long keep_pol = BS_L2_KEEP_T ? l2_policy_last() : 0ull;
     const long ntiles = TL::count(a);
     // reversed order on multi-plane launches: start on the row pass's L2-resident tail
     const bool rev = TRI_REV && (LAYOUT == CL_CDR ? a.batch > 1 : col_reversed<LAYOUT == CL_X3 ? CL_PLANE : LAYOUT>(a));
@@ -292,8 +298,14 @@ tri_kernel(const ColArgs a) {
         const TL ln(tile_at(k), a);
         const double2* src = a.T + ln.base;
 #pragma unroll 4
-        for (int e = threadIdx.x; e < C * N; e += G::THREADS)
+        for (int e = threadIdx.x; e < C * N; e += G::THREADS) {
+#if BS_L2_KEEP_T
+            if (LAYOUT == CL_PLANE)
+                cp_async16_hint(tbuf + e + e / (kTriP * C), src + (size_t)(e / C) * ln.ls + (e % C), keep_pol);
+            else
+#endif
             cp_async16(tbuf + e + e / (kTriP * C), src + (size_t)(e / C) * ln.ls + (e % C));
+        }
         const double2* ts = a.tri + ln.tline * TS;
         double2* td = tabs + tb * C * TSP;
         for (int k2 = threadIdx.x; k2 < C * TS; k2 += G::THREADS) cp_async16(td + (k2 / TS) * TSP + k2 % TS, ts + k2);
@@ -436,7 +448,10 @@ tri_kernel(const ColArgs a) {
         }
         double2* col = a.T + ln.base + (size_t)(kTriP * s) * ln.ls + c;
 #pragma unroll
-        for (int i = 0; i < kTriP; ++i) col[(size_t)i * ln.ls] = zc ? zero : cscale(v[i], sc);
+        for (int i = 0; i < kTriP; ++i) {
+            if (LAYOUT == CL_PLANE) st_keep<(BS_L2_KEEP_T != 0)>(&col[(size_t)i * ln.ls], zc ? zero : cscale(v[i], sc), keep_pol);
+            else col[(size_t)i * ln.ls] = zc ? zero : cscale(v[i], sc);
+        }
     }
     cp_async_wait_all();
 }
