@@ -98,6 +98,33 @@ def test_split_batch_bit_identical(gpu, monkeypatch, n, batch):
         assert np.array_equal(res[0].u[b], res[1].u[b])
 
 
+def test_waves_bit_identical(gpu, monkeypatch):
+    """n = 512 batches are swept in waves of 8 members, each member its own concurrently replayed
+    graph (BP_GROUP / BP_SPLIT; here 19 members: waves of 8, 8 and 3): every member's u and
+    traces are bit-identical to the single-graph run and to the member solved alone."""
+    batch = 19
+    k2, f, k0, eta = inst(512, batch=batch, seed=7)
+    f[3] *= 10.0
+    cfg = bs.IterationConfig(rtol=0.5, max_iters=200)  # members stop at different sweeps
+    monkeypatch.delenv("BP_GROUP", raising=False)
+    monkeypatch.delenv("BP_SPLIT", raising=False)
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        waves = bs.run(p, bs.PointwiseMap(), f, cfg)
+    monkeypatch.setenv("BP_SPLIT", "0")
+    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+        one = bs.run(p, bs.PointwiseMap(), f, cfg)
+    with bs.HelmholtzDirichlet(k2[11:12], k0[11:12], eta[11:12]) as p:
+        alone = bs.run(p, bs.PointwiseMap(), f[11:12], cfg)
+    assert len({t.iters for t in waves.traces}) > 1
+    for b in range(batch):
+        assert waves.traces[b].iters == one.traces[b].iters
+        assert waves.traces[b].terminated == one.traces[b].terminated
+        assert np.array_equal(waves.traces[b].res_l2_rel, one.traces[b].res_l2_rel)
+        assert np.array_equal(waves.u[b], one.u[b])
+    assert np.array_equal(waves.u[11], alone.u[0])
+    assert np.array_equal(waves.traces[11].res_reta_rel, alone.traces[0].res_reta_rel)
+
+
 @pytest.mark.parametrize("batch", [2, 5])
 def test_cdr_split_batch_bit_identical(gpu, monkeypatch, batch):
     """The CDR family's split-batch graphs (run_core_cdr): members bit-identical to one graph."""
