@@ -1012,7 +1012,7 @@ int wave_parts(int group) {
 // for any size, BP_GROUP=0 disables.
 int group_members(const bp_problem* p, int batch) {
     const char* env = std::getenv("BP_GROUP");
-    const int g = env ? std::atoi(env) : (p->log2n == 9 ? kDefaultGroup : 0);
+    const int g = env ? std::atoi(env) : (p->log2n == 9 && !p->cdr ? kDefaultGroup : 0);
     return (g > 0 && g < batch) ? g : 0;
 }
 int split_batch(const bp_problem* p, const SweepPlan& plan) {
@@ -2045,8 +2045,13 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
     // split-batch graphs as the Dirichlet path (run_core): parts replayed concurrently on their
     // own streams (BP_SPLIT=0 disables)
     const char* senv = std::getenv("BP_SPLIT");
-    const int split = (B >= 2 && !(senv && senv[0] == '0')) ? std::min(split_parts(B, p->log2n), B) : 0;
-    const bool reuse = p->graph && p->graph_split == split && p->graph_map_kind == map->kind &&
+    int split = (B >= 2 && !(senv && senv[0] == '0')) ? std::min(split_parts(B, p->log2n), B) : 0;
+    // waves as run_core (BP_GROUP = members per wave; off by default for this family)
+    const int group = split ? group_members(p, B) : 0;
+    if (group) split = wave_parts(group);
+    const int waves = group ? (B + group - 1) / group : 1;
+    const bool reuse = p->graph && p->graph_split == split && p->graph_group == group &&
+                       p->graph_map_kind == map->kind &&
                        p->graph_gamma.x == map->gamma_re && p->graph_max_iters == cfg->max_iters &&
                        p->graph_rtol == cfg->rtol;
     if (!reuse) {
@@ -2056,6 +2061,9 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
             if (g2) cudaGraphExecDestroy(g2);
             g2 = nullptr;
         }
+        for (auto gw : p->gwave)
+            if (gw) cudaGraphExecDestroy(gw);
+        p->gwave.clear();
         cudaGraph_t g;
         if (!split) {
             CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
@@ -2069,28 +2077,35 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
                 if (!p->ev_join[k]) CU(cudaEventCreateWithFlags(&p->ev_join[k], cudaEventDisableTiming));
             }
             cudaStream_t keep = p->stream;
-            for (int k = 0; k < split; ++k) {
-                const int b0 = (int)((long)B * k / split), b1 = (int)((long)B * (k + 1) / split);
-                const CdrArgs ak = cdr_args_range(a, p, b0, b1 - b0);
-                CdrArgs ack = cdr_args_range(ac, p, b0, b1 - b0);
-                p->stream = k ? p->stream2[k - 1] : keep;
-                cudaError_t e = cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal);
-                for (int sw = 0; e == cudaSuccess && sw < kGraphSweeps; ++sw) {
-                    if (e == cudaSuccess) e = launch_cdr(p->log2n, true, RC_A, ak, p->stream);
-                    if (e == cudaSuccess) e = launch_cdr(p->log2n, true, RC_B, ak, p->stream);
-                    if (e == cudaSuccess) e = cdr_green(p, ack, b0);
+            p->gwave.assign((size_t)(waves - 1) * split, nullptr);
+            for (int w = 0; w < waves; ++w) {
+                const int w0 = group ? w * group : 0, w1 = group ? std::min(B, w0 + group) : B;
+                for (int k = 0; k < split; ++k) {
+                    const int b0 = w0 + (int)((long)(w1 - w0) * k / split), b1 = w0 + (int)((long)(w1 - w0) * (k + 1) / split);
+                    cudaGraphExec_t* dst = w ? &p->gwave[(size_t)(w - 1) * split + k] : (k ? &p->graph2[k - 1] : &p->graph);
+                    if (b1 == b0) continue;
+                    const CdrArgs ak = cdr_args_range(a, p, b0, b1 - b0);
+                    CdrArgs ack = cdr_args_range(ac, p, b0, b1 - b0);
+                    p->stream = k ? p->stream2[k - 1] : keep;
+                    cudaError_t e = cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal);
+                    for (int sw = 0; e == cudaSuccess && sw < kGraphSweeps; ++sw) {
+                        if (e == cudaSuccess) e = launch_cdr(p->log2n, true, RC_A, ak, p->stream);
+                        if (e == cudaSuccess) e = launch_cdr(p->log2n, true, RC_B, ak, p->stream);
+                        if (e == cudaSuccess) e = cdr_green(p, ack, b0);
+                    }
+                    cudaError_t e2 = cudaStreamEndCapture(p->stream, &g);
+                    if (e == cudaSuccess) e = e2;
+                    if (e == cudaSuccess) {
+                        e = cudaGraphInstantiate(dst, g, 0);
+                        cudaGraphDestroy(g);
+                    }
+                    p->stream = keep;
+                    CU(e);
                 }
-                cudaError_t e2 = cudaStreamEndCapture(p->stream, &g);
-                if (e == cudaSuccess) e = e2;
-                if (e == cudaSuccess) {
-                    e = cudaGraphInstantiate(k ? &p->graph2[k - 1] : &p->graph, g, 0);
-                    cudaGraphDestroy(g);
-                }
-                p->stream = keep;
-                CU(e);
             }
         }
         p->graph_split = split;
+        p->graph_group = group;
         p->graph_map_kind = map->kind;
         p->graph_metric = map->metric;
         p->graph_gamma = make_double2(map->gamma_re, 0.0);
@@ -2103,14 +2118,18 @@ int run_core_cdr(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bo
         for (int k = 1; k < split; ++k) CU(cudaStreamWaitEvent(p->stream2[k - 1], p->ev_join[0], 0));
     }
     while (launched < max_launch) {
-        CU(cudaGraphLaunch(p->graph, p->stream));
+        for (int w = 0; w < waves; ++w) {
+            for (int k = 0; k < std::max(split, 1); ++k) {
+                cudaGraphExec_t ge = w ? p->gwave[(size_t)(w - 1) * split + k] : (k ? p->graph2[k - 1] : p->graph);
+                if (ge) CU(cudaGraphLaunch(ge, k ? p->stream2[k - 1] : p->stream));
+            }
+        }
         for (int k = 1; k < split; ++k) {
-            CU(cudaGraphLaunch(p->graph2[k - 1], p->stream2[k - 1]));
             CU(cudaEventRecord(p->ev_join[k], p->stream2[k - 1]));
             CU(cudaStreamWaitEvent(p->stream, p->ev_join[k], 0));
         }
         launched += kGraphSweeps;
-        p->stat_launches += 3 * kGraphSweeps * std::max(split, 1);
+        p->stat_launches += 3 * kGraphSweeps * std::max(split, 1) * waves;
         if (int rc = poll()) return rc;
         if (*p->host_active == 0) break;
     }
