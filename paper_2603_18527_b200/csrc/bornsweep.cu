@@ -47,10 +47,23 @@ constexpr double kSinScale = 1.0;
 constexpr double kSymbolDivGuard = 1e-14;  // proj/include/bp/symbol.hpp:24
 
 // ------------------------------------------------------------------ small kernels
+// The staging kernels of the host path (pack / unpack / finite check) stream hundreds of MB per
+// step through the L2 while ANOTHER handle's sweeps (bs.Pipeline) live off their L2-resident
+// waves: their global accesses carry evict_first so they do not displace that data.
+__device__ __forceinline__ double2 ld_once(const double2* p, unsigned long long pol) {
+    double2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_once(double2* p, double2 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+
 // dense (reference layout, (n-1)^dim per member) -> padded (n^dim per member, zero node at 0)
 __global__ void pack_kernel(const double2* __restrict__ dense, double2* __restrict__ padded,
                             int batch, int log2n, int dim) {
     const int n = 1 << log2n, nd = n - 1;
+    const unsigned long long pol = l2_policy_first();
     const size_t total = (size_t)batch << (dim * log2n);
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
          idx += (size_t)gridDim.x * blockDim.x) {
@@ -61,9 +74,9 @@ __global__ void pack_kernel(const double2* __restrict__ dense, double2* __restri
         if (dense && i > 0 && j > 0 && x > 0) {
             const size_t plane = dim == 3 ? (size_t)(x - 1) * nd : 0;
             const size_t per = dim == 3 ? (size_t)nd * nd * nd : (size_t)nd * nd;
-            v = dense[b * per + ((plane + (i - 1)) * nd + (j - 1))];
+            v = ld_once(&dense[b * per + ((plane + (i - 1)) * nd + (j - 1))], pol);
         }
-        padded[idx] = v;
+        padded[idx] = v;  // (the field the sweeps read next: default priority)
     }
 }
 
@@ -74,6 +87,7 @@ __global__ void unpack_kernel(const double2* __restrict__ p0, const double2* __r
     const int n = 1 << log2n, nd = n - 1;
     const size_t per = dim == 3 ? (size_t)nd * nd * nd : (size_t)nd * nd;
     const size_t total = (size_t)batch * per;
+    const unsigned long long pol = l2_policy_first();
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
          idx += (size_t)gridDim.x * blockDim.x) {
         const size_t b = idx / per;
@@ -84,7 +98,7 @@ __global__ void unpack_kernel(const double2* __restrict__ p0, const double2* __r
         const int x = (int)(r / nd) + 1;  // 3-D only
         const double2* src = (select && select[b]) ? p1 : p0;
         const size_t line = dim == 3 ? ((size_t)x << log2n) + i : (size_t)i;
-        dense[idx] = src[(b << (dim * log2n)) + (line << log2n) + j];
+        st_once(&dense[idx], ld_once(&src[(b << (dim * log2n)) + (line << log2n) + j], pol), pol);
     }
 }
 

@@ -326,7 +326,13 @@ tri_kernel(const ColArgs a) {
         // member status: issued before the tile wait so its round trip overlaps it
         const int stv = a.status ? __ldcg(&a.status[TL(tile_at(k), a).b]) : (int)ST_ACTIVE;
         cp_async_wait_all();
-        __syncthreads();
+        // ONE decision per CTA: another CTA may finalise this member's entry (status -> DONE)
+        // while this CTA's warps read the status, and warps that disagreed took different paths
+        // around the barriers below -- in a persistent CTA that corrupted the tiles it solved
+        // next, i.e. other members (found by the waves determinism stress, r02j: members next to
+        // an early-terminating one converged sweeps late or never).  A member seen DONE by any
+        // thread is done: skipping its tile is always safe.
+        const bool tile_active = __syncthreads_and(stv == (int)ST_ACTIVE) != 0;
         double2 v[kTriP];
 #pragma unroll
         for (int i = 0; i < kTriP; ++i) v[i] = tbuf[TT::sidx(kTriP * s + i, c)];
@@ -338,7 +344,7 @@ tri_kernel(const ColArgs a) {
         const TL ln(t, a);
         if (ln.skip) continue;
         if (a.status) {
-            const bool active = stv == ST_ACTIVE;  // read before finalising
+            const bool active = tile_active;  // read before finalising, uniform over the CTA
             if constexpr (LAYOUT == CL_PLANE)
                 if (a.finalize && active && ln.q0 == 0 && threadIdx.x < 32) finalize_member(a, ln.b, 1 << a.fin_lsh);
             if (!active) continue;  // uniform per CTA

@@ -110,17 +110,24 @@ def test_waves_bit_identical(gpu, monkeypatch):
     monkeypatch.delenv("BP_SPLIT", raising=False)
     with bs.HelmholtzDirichlet(k2, k0, eta) as p:
         waves = bs.run(p, bs.PointwiseMap(), f, cfg)
-    monkeypatch.setenv("BP_SPLIT", "0")
-    with bs.HelmholtzDirichlet(k2, k0, eta) as p:
-        one = bs.run(p, bs.PointwiseMap(), f, cfg)
+    assert len({t.iters for t in waves.traces}) > 1
+    # Multi-member launches, several times each: members that terminate flip their status while
+    # the persistent column CTAs of the same launch read it (the race fixed in tri_kernel, r02j:
+    # before, neighbours of an early-terminating member converged sweeps late in ~half the runs)
+    for env in ({"BP_SPLIT": "0"}, {"BP_GROUP": "0", "BP_SPLIT": "2"}) * 3:
+        for k in ("BP_GROUP", "BP_SPLIT"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with bs.HelmholtzDirichlet(k2, k0, eta) as p:
+            one = bs.run(p, bs.PointwiseMap(), f, cfg)
+        for b in range(batch):
+            assert waves.traces[b].iters == one.traces[b].iters, (env, b)
+            assert waves.traces[b].terminated == one.traces[b].terminated
+            assert np.array_equal(waves.traces[b].res_l2_rel, one.traces[b].res_l2_rel)
+            assert np.array_equal(waves.u[b], one.u[b])
     with bs.HelmholtzDirichlet(k2[11:12], k0[11:12], eta[11:12]) as p:
         alone = bs.run(p, bs.PointwiseMap(), f[11:12], cfg)
-    assert len({t.iters for t in waves.traces}) > 1
-    for b in range(batch):
-        assert waves.traces[b].iters == one.traces[b].iters
-        assert waves.traces[b].terminated == one.traces[b].terminated
-        assert np.array_equal(waves.traces[b].res_l2_rel, one.traces[b].res_l2_rel)
-        assert np.array_equal(waves.u[b], one.u[b])
     assert np.array_equal(waves.u[11], alone.u[0])
     assert np.array_equal(waves.traces[11].res_reta_rel, alone.traces[0].res_reta_rel)
 

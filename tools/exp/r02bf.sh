@@ -1,0 +1,8 @@
+#!/bin/bash
+O=gpurun_out/r02bf; mkdir -p $O
+for i in 1 2 3; do
+  timeout 300 python bench.py --no-cpu --steps 15 > $O/bench_$i.json 2>> $O/bench.err
+  python -c "import json;d=json.load(open('$O/bench_$i.json'));print('value',round(d['value'],3),'e2e',round(d['e2e']['value'],3),d['clocks']['sm_mhz'])"
+done
+timeout 1800 python -m pytest tests -m gpu -q > $O/gpu_tests.log 2>&1; echo "rc=$?" >> $O/gpu_tests.log
+tail -n 3 $O/gpu_tests.log
