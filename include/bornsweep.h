@@ -17,8 +17,8 @@
  *            (proj/include/bp/transforms.hpp:15-24).
  * Supported on the GPU (2-D Dirichlet): any nx, ny in [2, 4095] and any lx, ly -- square
  * grids with nx+1 = ny+1 = 2^k (8 <= 2^k <= 4096) and lx == ly run the fused kernels, every
- * other shape the any-shape path (radix-2 / Bluestein line transforms; scalar and pointwise
- * maps); the reference accepts any size through FFTW (proj/src/transforms.cpp:39-65).
+ * other shape the any-shape path (radix-2 / Bluestein line transforms; every map and format);
+ * the reference accepts any size through FFTW (proj/src/transforms.cpp:39-65).
  * 3-D, periodic and CDR handles: power-of-two sides as stated at their constructors.
  *
  * Errors: every function returns a status; nothing throws across the boundary.
