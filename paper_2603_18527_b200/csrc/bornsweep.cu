@@ -483,6 +483,9 @@ Control make_control(const bp_problem* p) {
 
 RowArgs row_args(const bp_problem* p) {
     RowArgs a{};
+    // L2 hints: single-member handles and 3-D always; multi-member 2-D batches only in the waves'
+    // single-member launches (run_core sets them there)
+    a.l2_hints = (p->batch == 1 || p->dim == 3) ? BS_L2_HINTS : 0;
     a.batch = p->batch;
     a.inv_h2 = p->inv_h2;
     a.k0sq = p->k0sq;
@@ -503,6 +506,7 @@ RowArgs row_args(const bp_problem* p) {
 
 ColArgs col_args(const bp_problem* p) {
     ColArgs c{};
+    c.l2_hints = (p->batch == 1 || p->dim == 3) ? BS_L2_HINTS : 0;
     c.batch = p->batch;
     c.k0sq = p->k0sq;
     c.eta = p->eta;
@@ -1243,8 +1247,10 @@ int run_core(bp_problem* p, const bp_map* map, const bp_iter_config* cfg, bool h
                         const int b0 = w0 + (int)((long)(w1 - w0) * k / K), b1 = w0 + (int)((long)(w1 - w0) * (k + 1) / K);
                         cudaGraphExec_t* dst = w ? &p->gwave[(size_t)(w - 1) * K + k] : (k ? &p->graph2[k - 1] : &p->graph);
                         if (b1 == b0) continue;  // (a short last wave)
-                        const RowArgs ak = row_args_range(a, p, b0, b1 - b0);
-                        const ColArgs ck = col_args_range(c, p, b0, b1 - b0);
+                        RowArgs ak = row_args_range(a, p, b0, b1 - b0);
+                        ColArgs ck = col_args_range(c, p, b0, b1 - b0);
+                        // a wave's fields (or a small batch's single-member parts) live in L2
+                        if (group || b1 - b0 == 1) ak.l2_hints = ck.l2_hints = BS_L2_HINTS;
                         p->stream = k ? p->stream2[k - 1] : keep;
                         cudaError_t e = cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal);
                         for (int sw = 0; e == cudaSuccess && sw < kGraphSweeps; ++sw) sweep_once(p, plan, ak, ck, nullptr);

@@ -163,6 +163,8 @@ struct RowArgs {
     int xchg_on;
     int xchg_rank;
     double2* xchg[kMaxXchg];
+    // L2 eviction-priority hints of this launch (BS_L2_HINTS bits; 0 = normal priority)
+    int l2_hints;
 };
 
 struct ColArgs {
@@ -201,6 +203,7 @@ struct ColArgs {
     // the scale that makes it equal the transform route (8 n h^2 x scale)
     const double2* tri;
     double tri_scale;
+    int l2_hints;  // as RowArgs::l2_hints (the tridiagonal pass keeps T: bit 4)
 };
 
 // 1/eta of the pointwise map hoisted out of the row kernel's element loop: measured slower on
@@ -249,6 +252,11 @@ __device__ __forceinline__ double rcp_green(double x) {
 __device__ __forceinline__ unsigned long long l2_policy_first() {
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ unsigned long long l2_policy_normal() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 __device__ __forceinline__ unsigned long long l2_policy_last() {
@@ -411,8 +419,14 @@ __device__ __forceinline__ void row_group(const RowArgs& a, const long grp, cons
     constexpr unsigned VALID_LINES = DIM == 3 ? (unsigned)((N - 1) * (N - 1)) : (unsigned)(N - 1);
     extern __shared__ double2 smem[];
 
-    [[maybe_unused]] const unsigned long long pol_s = BS_L2_STREAM ? l2_policy_first() : 0ull;
-    [[maybe_unused]] const unsigned long long pol_k = (BS_L2_KEEP_U || BS_L2_KEEP_T) ? l2_policy_last() : 0ull;
+    // the launch decides (RowArgs::l2_hints): the priorities pay off where a launch's fields are
+    // re-read out of L2 by the next launches (the waves' single-member launches, single-member
+    // handles); a launch over a whole multi-member batch measured slower with them (row kernel
+    // 0.351 -> 0.360 ms on c1) and keeps the normal priority
+    [[maybe_unused]] const unsigned long long pol_s =
+        BS_L2_STREAM ? ((a.l2_hints & 1) ? l2_policy_first() : l2_policy_normal()) : 0ull;
+    [[maybe_unused]] const unsigned long long pol_k =
+        (BS_L2_KEEP_U || BS_L2_KEEP_T) ? ((a.l2_hints & 4) ? l2_policy_last() : l2_policy_normal()) : 0ull;
     const int t = threadIdx.x % T;
     const int e = threadIdx.x / T;
     const long grow = grp * EPB + e;

@@ -289,7 +289,8 @@ tri_kernel(const ColArgs a) {
     double2* xs = zl + C * SP;             // [C][SP] separators (X_S = 0 at [S])
     double2* tot = xs + C * SP;            // [C][CH] chunk maps (A, B)
 
-    [[maybe_unused]] const unsigned long long keep_pol = BS_L2_KEEP_T ? l2_policy_last() : 0ull;
+    [[maybe_unused]] const unsigned long long keep_pol =
+        BS_L2_KEEP_T ? ((a.l2_hints & 4) ? l2_policy_last() : l2_policy_normal()) : 0ull;
     const long ntiles = TL::count(a);
     // reversed order on multi-plane launches: start on the row pass's L2-resident tail
     const bool rev = TRI_REV && (LAYOUT == CL_CDR ? a.batch > 1 : col_reversed<LAYOUT == CL_X3 ? CL_PLANE : LAYOUT>(a));
